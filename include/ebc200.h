@@ -1,0 +1,125 @@
+/*
+ * ebc200.h -- C-ABI of the B200 (sm_100a) Exemplar-based Clustering hot path.
+ *
+ * Drop-in boundary for the reference package ebcsum 0.1.0 (arXiv 2105.12026).
+ * The reference is pure Python, so "the FFI it would bind" is a ctypes binding
+ * from its optimizer/objective layer; INTEGRATION.md shows that stub.  Every
+ * entry point below names the reference function it replaces.
+ *
+ * Conventions
+ *   - Plain pointers and sizes, no torch types.  The caller owns all host
+ *     buffers; the library copies what it keeps.
+ *   - Every call returns an ebc_status; on failure ebc_last_error(ctx) holds a
+ *     message.  EBC_EINDEX carries the reference's exact IndexError text
+ *     ("set {j}: index {i} out of range for ground size {n}", core.py:140-143).
+ *   - A context is single-caller (not re-entrant); calls are synchronous.
+ *   - There is no CPU fallback: without a usable CUDA device ebc_create fails
+ *     with EBC_ECUDA.
+ */
+#ifndef EBC200_H
+#define EBC200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ebc_ctx ebc_ctx;
+
+typedef enum {
+  EBC_OK = 0,
+  EBC_EINVAL = 1, /* -> ValueError   (optimize.py:33-40,71-72; batched.py:190-191) */
+  EBC_EINDEX = 2, /* -> IndexError   (core.py:136-143; ebc.py:119-120)             */
+  EBC_ECUDA = 3,  /* -> RuntimeError (device / driver failure)                      */
+  EBC_ECOMM = 4   /* -> RuntimeError (sharded exchange failure)                     */
+} ebc_status;
+
+/* Storage precision of the ground matrix (core.py:13-55 Precision). */
+typedef enum {
+  EBC_F32 = 0, /* Precision.FP32                                              */
+  EBC_F16 = 1, /* Precision.FP16_STORAGE: IEEE half storage, fp32 arithmetic  */
+  EBC_F64 = 2  /* Precision.FP64                                              */
+} ebc_dtype;
+
+/* Library version string, e.g. "ebc200 0.1.0 sm_100a". */
+const char* ebc_version(void);
+
+/* Number of CUDA devices visible to the library (0 when none). */
+int ebc_device_count(void);
+
+/* Upload the N x d row-major ground matrix V (element type `dtype`, already in
+ * storage precision) and the fp64 auxiliary vector e0 (d entries; NULL = the
+ * zero vector), pad V to 16-byte rows on `device`, and compute the baseline
+ * loss L({e0}) once.
+ * Replaces: GroundMatrix.__init__ (core.py:107-124) + EbcFunction.__init__
+ *           (ebc.py:55-72, baseline at :72). */
+int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double* e0,
+               int32_t device, ebc_ctx** out);
+
+/* L({e0}) -- EbcFunction.baseline_loss (ebc.py:72). */
+int ebc_baseline(const ebc_ctx* ctx, double* out);
+
+/* f(S_j) for l sets given in CSR form (offsets has l+1 entries, idx holds the
+ * members), fp64, in set order; empty sets give exactly 0.0.  On an index
+ * outside [0, n) returns EBC_EINDEX and reports the first offending set/index
+ * in set order.
+ * Replaces: evaluate_with_backend (optimize.py:43-57) ->
+ *           evaluate_multiset_batched (batched.py:180-240) / the naive oracle
+ *           evaluate_multiset_naive (ebc.py:109-121). */
+int ebc_eval_multiset(ebc_ctx* ctx, const int64_t* offsets, const int64_t* idx, int64_t l,
+                      double* out_f, int64_t* out_bad_set, int64_t* out_bad_index);
+
+/* Full Greedy(k) on this device: k steps of screen -> certified fp64 refine ->
+ * argmax with the reference tie window -> cached-min update, no host sync
+ * between steps.  out_sel/out_val/out_gain receive k entries (out_val[s] is
+ * f after s+1 selections); *out_evals = sum over steps of the frontier size.
+ * Replaces: greedy_maximize (optimize.py:60-91). */
+int ebc_greedy(ebc_ctx* ctx, int32_t k, int64_t* out_sel, double* out_val, double* out_gain,
+               int64_t* out_evals);
+
+/* ---- candidate-sharded Greedy (one process per GPU) ----
+ * V is replicated; this context screens only candidates [c0, c1).  A step is
+ *   ebc_shard_step   -> local certified list (index, exact fp64 gain)
+ *   (host exchange across ranks; global pick, see paper_2105_12026_b200/sharded.py)
+ *   ebc_shard_commit -> fold the globally chosen index into the cached minima.
+ */
+int ebc_shard_set_range(ebc_ctx* ctx, int64_t c0, int64_t c1);
+
+/* Screen + refine the local candidates for the current step.  Writes up to
+ * `cap` (index, gain64) pairs; *out_count is the full list length (may exceed
+ * cap: call again with a larger buffer, results are cached until commit).
+ * *out_current = f(S) of the current selection. */
+int ebc_shard_step(ebc_ctx* ctx, int64_t* out_idx, double* out_gain, int64_t cap,
+                   int64_t* out_count, double* out_current);
+
+/* Select ground index `s` (any rank's candidate): cm <- min(cm, d(., s)),
+ * returns the new f(S) in *out_value. */
+int ebc_shard_commit(ebc_ctx* ctx, int64_t s, double* out_value);
+
+/* Reset the selection state to S = {} (cached minima back to d(., e0)). */
+int ebc_reset(ebc_ctx* ctx);
+
+/* Enable per-step CUDA-event timing of the kernel families (off by default). */
+int ebc_set_timing(ebc_ctx* ctx, int on);
+
+/* Device-time of the last ebc_greedy / ebc_eval_multiset call split by kernel
+ * family, in milliseconds (CUDA events on the library stream): [0] screen,
+ * [1] refine+pick, [2] cached-min update, [3] whole call.  For bench.py. */
+int ebc_last_timings(const ebc_ctx* ctx, double* out_ms4);
+
+/* Kernel launches issued by the last call (bench.py's gpu_launches). */
+int64_t ebc_last_launches(const ebc_ctx* ctx);
+
+/* Free all device state. */
+void ebc_destroy(ebc_ctx* ctx);
+
+/* Message for the last failing call on ctx (or a global message when ctx is
+ * NULL, e.g. after a failed ebc_create). */
+const char* ebc_last_error(const ebc_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* EBC200_H */

@@ -1,0 +1,626 @@
+// ebc200.cu -- host runtime + C-ABI (include/ebc200.h) of the B200 EBC hot path.
+//
+// One context per EbcFunction (ebc.py:46-106): the ground matrix lives on the
+// device for the context's life in the padded row-major layout of DESIGN.md §3,
+// next to the fp64 e0-distances, the fp64/fp32 cached minima and the scratch of
+// the Greedy step.  All work runs on one stream; a Greedy run never synchronises
+// with the host between steps.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/ebc200.h"
+#include "kernels.cuh"
+
+using namespace ebc;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+}  // namespace
+
+struct ebc_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  int64_t n = 0;
+  int d = 0;
+  int dtype = EBC_F32;
+  int pitch = 0;      // elements per device row
+  int64_t n_pad = 0;  // rows allocated (zero padded)
+  int d4 = 0;
+  int nchunks = 0;    // ceil(n / RCH)
+  float kappa2 = 0.f;  // tau = kappa2 * cm32
+  double baseline = 0.0;
+  int64_t c0 = 0, c1 = 0;  // screened candidate range
+  int64_t steps_done = 0;   // selections since the last reset
+
+  // device state
+  float* V32 = nullptr;   // fp32 / widened fp16 grounds
+  double* V64 = nullptr;  // fp64 grounds
+  double* e0d = nullptr;
+  double* cm64 = nullptr;
+  float2* pt = nullptr;
+  unsigned char* selected = nullptr;
+  double* chunkpart = nullptr;  // nchunks
+  unsigned int* counter = nullptr;
+  double* cur = nullptr;
+  int64_t* best = nullptr;
+  long long* maxlb = nullptr;
+  int* wcount = nullptr;
+  int64_t* wlist = nullptr;  // n
+  double* wgain = nullptr;   // n
+  double* ub = nullptr;      // n
+  DevBuf part_g, part_e, part_r, sel_out, val_out, gain_out, ms_part, ms_off, ms_idx, ms_out;
+
+  // timing / accounting
+  bool timing = false;
+  std::vector<cudaEvent_t> ev;
+  double last_ms[4] = {0, 0, 0, 0};
+  int64_t launches = 0;
+  std::string err;
+};
+
+namespace {
+
+int fail(ebc_ctx* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  g_err = msg;
+  return code;
+}
+
+#define CU(call)                                                                                   \
+  do {                                                                                             \
+    cudaError_t e_ = (call);                                                                       \
+    if (e_ != cudaSuccess)                                                                         \
+      return fail(ctx, EBC_ECUDA, std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " + \
+                                      __FILE__ + ":" + std::to_string(__LINE__) + " (" #call ")"); \
+  } while (0)
+
+#define KCHECK()                                                                                   \
+  do {                                                                                             \
+    ++ctx->launches;                                                                               \
+    cudaError_t e_ = cudaGetLastError();                                                           \
+    if (e_ != cudaSuccess)                                                                         \
+      return fail(ctx, EBC_ECUDA, std::string("kernel launch failed: ") + cudaGetErrorString(e_) + \
+                                      " at " + __FILE__ + ":" + std::to_string(__LINE__));         \
+  } while (0)
+
+int ensure(ebc_ctx* ctx, DevBuf& b, size_t bytes) {
+  if (b.bytes >= bytes) return EBC_OK;
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.bytes = 0;
+  CU(cudaMalloc(&b.p, bytes));
+  b.bytes = bytes;
+  return EBC_OK;
+}
+
+// Row pitch (elements) of the device copy: 16-byte rows; for fp32 the pitch in
+// float4 units is odd so that 4 or 8 consecutive rows read by one LDS.128 hit
+// disjoint bank groups.
+int pitch_for(int d, int dtype) {
+  if (dtype == EBC_F64) return (d + 1) / 2 * 2;
+  int p = (d + 3) / 4 * 4;
+  if ((p / 4) % 2 == 0) p += 4;
+  return p;
+}
+
+struct ScreenPlan {
+  int stages;
+  size_t smem;
+  int ncb;
+  int ntiles;
+  int tps;
+  int nsplit;
+};
+
+ScreenPlan plan_screen(const ebc_ctx* ctx) {
+  ScreenPlan p;
+  p.stages = 4;
+  while (p.stages > 2 && screen_smem_bytes(ctx->pitch, p.stages) > 110 * 1024) p.stages /= 2;
+  p.smem = screen_smem_bytes(ctx->pitch, p.stages);
+  const int64_t ncand = ctx->c1 - ctx->c0;
+  p.ncb = (int)((ncand + screen::CT_ - 1) / screen::CT_);
+  p.ntiles = (int)((ctx->n + screen::PT_ - 1) / screen::PT_);
+  const int64_t target = 8LL * ctx->num_sms;  // >= 4 waves at 2 CTAs/SM
+  int want = (int)std::min<int64_t>(p.ntiles, std::max<int64_t>(1, (target + p.ncb - 1) / std::max(1, p.ncb)));
+  p.tps = (p.ntiles + want - 1) / want;
+  p.nsplit = (p.ntiles + p.tps - 1) / p.tps;
+  return p;
+}
+
+template <int ST>
+int launch_screen_t(ebc_ctx* ctx, const ScreenPlan& p) {
+  auto kern = k_screen<ST>;
+  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
+  dim3 grid(p.ncb, p.nsplit);
+  kern<<<grid, screen::THREADS, p.smem, ctx->stream>>>(
+      ctx->V32, ctx->pt, ctx->pitch, ctx->d4, ctx->c0, p.ntiles, p.tps, (double*)ctx->part_g.p,
+      (float*)ctx->part_e.p, ctx->n_pad);
+  KCHECK();
+  return EBC_OK;
+}
+
+// One step's candidate screen + certified window + exact refine + pick.
+// commit: single-device mode (mark the winner, record it as step `step`).
+int run_step_select(ebc_ctx* ctx, int step, int commit, int64_t* sel_dev) {
+  const int64_t ncand = ctx->c1 - ctx->c0;
+  CU(cudaMemsetAsync(ctx->wcount, 0, sizeof(int), ctx->stream));
+  const int fin_blocks = (int)((ncand + 255) / 256);
+  if (ctx->dtype != EBC_F64) {
+    ScreenPlan p = plan_screen(ctx);
+    int rc = ensure(ctx, ctx->part_g, (size_t)p.nsplit * ctx->n_pad * sizeof(double));
+    if (rc) return rc;
+    rc = ensure(ctx, ctx->part_e, (size_t)p.nsplit * ctx->n_pad * sizeof(float));
+    if (rc) return rc;
+    if (ctx->timing) CU(cudaEventRecord(ctx->ev[0], ctx->stream));
+    if (p.stages == 4)
+      rc = launch_screen_t<4>(ctx, p);
+    else
+      rc = launch_screen_t<2>(ctx, p);
+    if (rc) return rc;
+    if (ctx->timing) CU(cudaEventRecord(ctx->ev[1], ctx->stream));
+    // lower bounds are clamped at 0 (every gain is a sum of max(0, .) terms), so
+    // key 0 (= +0.0) is a valid neutral element for the max
+    CU(cudaMemsetAsync(ctx->maxlb, 0, sizeof(long long), ctx->stream));
+    // per-thread fp32 error accumulators see at most tps*TP terms: inflate
+    const double nterms = (double)p.tps * screen::TP * 8 * 2 + 64.0;
+    const double einfl = 1.0 + 2.0 * nterms * 5.960464477539063e-08 + 1.0 / 64.0;
+    k_finalize<<<fin_blocks, 256, 0, ctx->stream>>>(ctx->c0, ctx->c1, p.nsplit, (double*)ctx->part_g.p,
+                                                   (float*)ctx->part_e.p, ctx->n_pad, einfl, ctx->selected,
+                                                   ctx->ub, ctx->maxlb);
+    KCHECK();
+    const double margin = (double)ctx->n * 1e-12 * std::max(1.0, std::fabs(ctx->baseline)) * 1.01;
+    k_window<<<fin_blocks, 256, 0, ctx->stream>>>(ctx->c0, ctx->c1, ctx->ub, ctx->maxlb, margin, ctx->wcount,
+                                                 ctx->wlist);
+    KCHECK();
+  } else {
+    if (ctx->timing) {
+      CU(cudaEventRecord(ctx->ev[0], ctx->stream));
+      CU(cudaEventRecord(ctx->ev[1], ctx->stream));
+    }
+    k_window_all<<<fin_blocks, 256, 0, ctx->stream>>>(ctx->c0, ctx->c1, ctx->selected, ctx->wcount, ctx->wlist);
+    KCHECK();
+  }
+  // exact fp64 gains of the window
+  int rc = ensure(ctx, ctx->part_r, (size_t)ctx->n * ctx->nchunks * sizeof(double));
+  if (rc) return rc;
+  const int rgrid = 4 * ctx->num_sms;
+  const size_t rsmem = (size_t)ctx->d * sizeof(double);
+  if (ctx->dtype == EBC_F64) {
+    CU(cudaFuncSetAttribute(k_refine<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem + 1024));
+    k_refine<double><<<rgrid, RED_THREADS, rsmem, ctx->stream>>>(ctx->V64, ctx->pitch, ctx->n, ctx->d, ctx->cm64,
+                                                               ctx->wcount, ctx->wlist, ctx->nchunks,
+                                                               (double*)ctx->part_r.p);
+  } else {
+    CU(cudaFuncSetAttribute(k_refine<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem + 1024));
+    k_refine<float><<<rgrid, RED_THREADS, rsmem, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->n, ctx->d, ctx->cm64,
+                                                              ctx->wcount, ctx->wlist, ctx->nchunks,
+                                                              (double*)ctx->part_r.p);
+  }
+  KCHECK();
+  k_pick<<<1, 1024, 0, ctx->stream>>>(ctx->wcount, ctx->wlist, ctx->nchunks, (double*)ctx->part_r.p,
+                                      1.0 / (double)ctx->n, ctx->cur, ctx->wgain, ctx->best, commit, step,
+                                      ctx->selected, sel_dev);
+  KCHECK();
+  if (ctx->timing) CU(cudaEventRecord(ctx->ev[2], ctx->stream));
+  return EBC_OK;
+}
+
+int run_update(ebc_ctx* ctx, int step, double* val_dev, double* gain_dev) {
+  const size_t smem = (size_t)ctx->d * sizeof(double);
+  if (ctx->dtype == EBC_F64) {
+    CU(cudaFuncSetAttribute(k_update<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024));
+    k_update<double><<<ctx->nchunks, RED_THREADS, smem, ctx->stream>>>(
+        ctx->V64, ctx->pitch, ctx->n, ctx->d, ctx->best, ctx->kappa2, ctx->e0d, ctx->cm64, ctx->pt, ctx->chunkpart,
+        ctx->counter, 1.0 / (double)ctx->n, ctx->cur, val_dev, gain_dev, step);
+  } else {
+    CU(cudaFuncSetAttribute(k_update<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024));
+    k_update<float><<<ctx->nchunks, RED_THREADS, smem, ctx->stream>>>(
+        ctx->V32, ctx->pitch, ctx->n, ctx->d, ctx->best, ctx->kappa2, ctx->e0d, ctx->cm64, ctx->pt, ctx->chunkpart,
+        ctx->counter, 1.0 / (double)ctx->n, ctx->cur, val_dev, gain_dev, step);
+  }
+  KCHECK();
+  if (ctx->timing) CU(cudaEventRecord(ctx->ev[3], ctx->stream));
+  return EBC_OK;
+}
+
+int do_reset(ebc_ctx* ctx) {
+  const int blocks = (int)((ctx->n + 255) / 256);
+  k_reset<<<blocks, 256, 0, ctx->stream>>>(ctx->n, ctx->e0d, ctx->kappa2, ctx->cm64, ctx->pt, ctx->selected);
+  KCHECK();
+  CU(cudaMemsetAsync(ctx->cur, 0, sizeof(double), ctx->stream));
+  ctx->steps_done = 0;
+  return EBC_OK;
+}
+
+void free_ctx(ebc_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  void* ptrs[] = {c->V32, c->V64, c->e0d, c->cm64, c->pt, c->selected, c->chunkpart, c->counter, c->cur, c->best,
+                  c->maxlb, c->wcount, c->wlist, c->wgain, c->ub};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  DevBuf* bufs[] = {&c->part_g, &c->part_e, &c->part_r, &c->sel_out, &c->val_out,
+                    &c->gain_out, &c->ms_part, &c->ms_off, &c->ms_idx, &c->ms_out};
+  for (DevBuf* b : bufs)
+    if (b->p) cudaFree(b->p);
+  for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+}  // namespace
+
+// ============================================================================ C-ABI
+
+extern "C" {
+
+const char* ebc_version(void) { return "ebc200 0.1.0 sm_100a"; }
+
+int ebc_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+const char* ebc_last_error(const ebc_ctx* ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
+
+int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double* e0, int32_t device,
+               ebc_ctx** out) {
+  ebc_ctx* ctx = nullptr;
+  if (!out) return fail(nullptr, EBC_EINVAL, "ebc_create: out is NULL");
+  *out = nullptr;
+  if (!V || n < 1 || d < 1) return fail(nullptr, EBC_EINVAL, "ground data must be at least 1x1");
+  if (dtype != EBC_F32 && dtype != EBC_F16 && dtype != EBC_F64)
+    return fail(nullptr, EBC_EINVAL, "unknown dtype " + std::to_string(dtype));
+  int ndev = 0;
+  cudaError_t ce = cudaGetDeviceCount(&ndev);
+  if (ce != cudaSuccess || ndev < 1)
+    return fail(nullptr, EBC_ECUDA,
+                std::string("no CUDA device available for the b200 backend: ") + cudaGetErrorString(ce));
+  if (device < 0 || device >= ndev)
+    return fail(nullptr, EBC_EINVAL, "device " + std::to_string(device) + " out of range");
+
+  ctx = new ebc_ctx();
+  ctx->device = device;
+  ctx->n = n;
+  ctx->d = d;
+  ctx->dtype = dtype;
+  ctx->pitch = pitch_for(d, dtype);
+  ctx->d4 = (d + 3) / 4;
+  ctx->nchunks = (int)((n + RCH - 1) / RCH);
+  ctx->n_pad = ((n + 127) / 128) * 128 + 256;
+  ctx->c0 = 0;
+  ctx->c1 = n;
+  // tau = 2(d+8)u * cm32, slightly inflated
+  ctx->kappa2 = (float)(2.0 * (d + 8) * 5.960464477539063e-08 * (1.0 + 1.0 / 512));
+  int rc = EBC_OK;
+#define CUC(call)                                                                                   \
+  do {                                                                                              \
+    cudaError_t e_ = (call);                                                                        \
+    if (e_ != cudaSuccess) {                                                                        \
+      rc = fail(nullptr, EBC_ECUDA, std::string("CUDA error: ") + cudaGetErrorString(e_) + " (" #call ")"); \
+      free_ctx(ctx);                                                                                \
+      return rc;                                                                                    \
+    }                                                                                               \
+  } while (0)
+  CUC(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CUC(cudaGetDeviceProperties(&prop, device));
+  if (prop.major < 10)
+    rc = fail(nullptr, EBC_ECUDA,
+              std::string("b200 backend needs an sm_100 device, found ") + prop.name + " sm_" +
+                  std::to_string(prop.major * 10 + prop.minor));
+  if (rc) {
+    free_ctx(ctx);
+    return rc;
+  }
+  ctx->num_sms = prop.multiProcessorCount;
+  CUC(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+  const size_t esz = dtype == EBC_F64 ? sizeof(double) : sizeof(float);
+  const size_t src_esz = dtype == EBC_F64 ? 8 : (dtype == EBC_F16 ? 2 : 4);
+  void* Vdev = nullptr;
+  CUC(cudaMalloc(&Vdev, (size_t)ctx->n_pad * ctx->pitch * esz));
+  CUC(cudaMemsetAsync(Vdev, 0, (size_t)ctx->n_pad * ctx->pitch * esz, ctx->stream));
+  if (dtype == EBC_F64)
+    ctx->V64 = (double*)Vdev;
+  else
+    ctx->V32 = (float*)Vdev;
+  void* raw = nullptr;
+  CUC(cudaMalloc(&raw, (size_t)n * d * src_esz));
+  CUC(cudaMemcpyAsync(raw, V, (size_t)n * d * src_esz, cudaMemcpyHostToDevice, ctx->stream));
+  {
+    const int blocks = 8 * ctx->num_sms;
+    if (dtype == EBC_F32)
+      k_pad<float, float><<<blocks, 256, 0, ctx->stream>>>((const float*)raw, n, d, ctx->V32, ctx->pitch);
+    else if (dtype == EBC_F16)
+      k_pad<__half, float><<<blocks, 256, 0, ctx->stream>>>((const __half*)raw, n, d, ctx->V32, ctx->pitch);
+    else
+      k_pad<double, double><<<blocks, 256, 0, ctx->stream>>>((const double*)raw, n, d, ctx->V64, ctx->pitch);
+    CUC(cudaGetLastError());
+  }
+  CUC(cudaMalloc(&ctx->e0d, (size_t)n * sizeof(double)));
+  CUC(cudaMalloc(&ctx->cm64, (size_t)ctx->n_pad * sizeof(double)));
+  CUC(cudaMalloc(&ctx->pt, (size_t)ctx->n_pad * sizeof(float2)));
+  CUC(cudaMemsetAsync(ctx->pt, 0, (size_t)ctx->n_pad * sizeof(float2), ctx->stream));
+  CUC(cudaMalloc(&ctx->selected, (size_t)ctx->n_pad));
+  CUC(cudaMemsetAsync(ctx->selected, 0, (size_t)ctx->n_pad, ctx->stream));
+  CUC(cudaMalloc(&ctx->chunkpart, (size_t)ctx->nchunks * sizeof(double)));
+  CUC(cudaMalloc(&ctx->counter, sizeof(unsigned int)));
+  CUC(cudaMemsetAsync(ctx->counter, 0, sizeof(unsigned int), ctx->stream));
+  CUC(cudaMalloc(&ctx->cur, sizeof(double)));
+  CUC(cudaMemsetAsync(ctx->cur, 0, sizeof(double), ctx->stream));
+  CUC(cudaMalloc(&ctx->best, sizeof(int64_t)));
+  CUC(cudaMalloc(&ctx->maxlb, sizeof(long long)));
+  CUC(cudaMalloc(&ctx->wcount, sizeof(int)));
+  CUC(cudaMalloc(&ctx->wlist, (size_t)n * sizeof(int64_t)));
+  CUC(cudaMalloc(&ctx->wgain, (size_t)n * sizeof(double)));
+  CUC(cudaMalloc(&ctx->ub, (size_t)n * sizeof(double)));
+  double* e0dev = nullptr;
+  CUC(cudaMalloc(&e0dev, (size_t)d * sizeof(double)));
+  {
+    std::vector<double> z;
+    const double* src = e0;
+    if (!src) {
+      z.assign(d, 0.0);
+      src = z.data();
+    }
+    CUC(cudaMemcpyAsync(e0dev, src, (size_t)d * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    CUC(cudaStreamSynchronize(ctx->stream));  // z / caller buffers may go away
+  }
+  if (dtype == EBC_F64)
+    k_init<double><<<ctx->nchunks, RED_THREADS, 0, ctx->stream>>>(ctx->V64, ctx->pitch, n, d, e0dev, ctx->kappa2,
+                                                                 ctx->e0d, ctx->cm64, ctx->pt, ctx->chunkpart);
+  else
+    k_init<float><<<ctx->nchunks, RED_THREADS, 0, ctx->stream>>>(ctx->V32, ctx->pitch, n, d, e0dev, ctx->kappa2,
+                                                                ctx->e0d, ctx->cm64, ctx->pt, ctx->chunkpart);
+  CUC(cudaGetLastError());
+  double* bl = nullptr;
+  CUC(cudaMalloc(&bl, sizeof(double)));
+  k_total<<<1, 32, 0, ctx->stream>>>(ctx->chunkpart, ctx->nchunks, 1.0 / (double)n, bl);
+  CUC(cudaGetLastError());
+  CUC(cudaMemcpyAsync(&ctx->baseline, bl, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CUC(cudaStreamSynchronize(ctx->stream));
+  cudaFree(bl);
+  cudaFree(e0dev);
+  cudaFree(raw);
+  ctx->ev.resize(4);
+  for (auto& e : ctx->ev) CUC(cudaEventCreate(&e));
+#undef CUC
+  *out = ctx;
+  return EBC_OK;
+}
+
+int ebc_baseline(const ebc_ctx* ctx, double* out) {
+  if (!ctx || !out) return fail(nullptr, EBC_EINVAL, "ebc_baseline: NULL argument");
+  *out = ctx->baseline;
+  return EBC_OK;
+}
+
+int ebc_reset(ebc_ctx* ctx) {
+  if (!ctx) return fail(nullptr, EBC_EINVAL, "ebc_reset: NULL context");
+  CU(cudaSetDevice(ctx->device));
+  int rc = do_reset(ctx);
+  if (rc) return rc;
+  CU(cudaStreamSynchronize(ctx->stream));
+  return EBC_OK;
+}
+
+int ebc_set_timing(ebc_ctx* ctx, int on) {
+  if (!ctx) return fail(nullptr, EBC_EINVAL, "ebc_set_timing: NULL context");
+  ctx->timing = on != 0;
+  return EBC_OK;
+}
+
+int ebc_last_timings(const ebc_ctx* ctx, double* out_ms4) {
+  if (!ctx || !out_ms4) return fail(nullptr, EBC_EINVAL, "ebc_last_timings: NULL argument");
+  for (int i = 0; i < 4; ++i) out_ms4[i] = ctx->last_ms[i];
+  return EBC_OK;
+}
+
+int64_t ebc_last_launches(const ebc_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+int ebc_greedy(ebc_ctx* ctx, int32_t k, int64_t* out_sel, double* out_val, double* out_gain, int64_t* out_evals) {
+  if (!ctx) return fail(nullptr, EBC_EINVAL, "ebc_greedy: NULL context");
+  if (k < 1) return fail(ctx, EBC_EINVAL, "k must be >= 1");
+  if (k > ctx->n)
+    return fail(ctx, EBC_EINVAL, "k=" + std::to_string(k) + " exceeds ground size " + std::to_string(ctx->n));
+  if (!out_sel || !out_val || !out_gain) return fail(ctx, EBC_EINVAL, "ebc_greedy: NULL output buffer");
+  CU(cudaSetDevice(ctx->device));
+  ctx->launches = 0;
+  ctx->c0 = 0;
+  ctx->c1 = ctx->n;
+  int rc = ensure(ctx, ctx->sel_out, (size_t)k * sizeof(int64_t));
+  if (!rc) rc = ensure(ctx, ctx->val_out, (size_t)k * sizeof(double));
+  if (!rc) rc = ensure(ctx, ctx->gain_out, (size_t)k * sizeof(double));
+  if (rc) return rc;
+  rc = do_reset(ctx);
+  if (rc) return rc;
+  double acc_ms[4] = {0, 0, 0, 0};
+  cudaEvent_t tstart = nullptr, tend = nullptr;
+  CU(cudaEventCreate(&tstart));
+  CU(cudaEventCreate(&tend));
+  CU(cudaEventRecord(tstart, ctx->stream));
+  for (int s = 0; s < k; ++s) {
+    rc = run_step_select(ctx, s, 1, (int64_t*)ctx->sel_out.p);
+    if (rc) return rc;
+    rc = run_update(ctx, s, (double*)ctx->val_out.p, (double*)ctx->gain_out.p);
+    if (rc) return rc;
+    if (ctx->timing) {
+      CU(cudaEventSynchronize(ctx->ev[3]));
+      float a = 0, b = 0, c = 0;
+      CU(cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]));
+      CU(cudaEventElapsedTime(&b, ctx->ev[1], ctx->ev[2]));
+      CU(cudaEventElapsedTime(&c, ctx->ev[2], ctx->ev[3]));
+      acc_ms[0] += a;
+      acc_ms[1] += b;
+      acc_ms[2] += c;
+    }
+  }
+  CU(cudaEventRecord(tend, ctx->stream));
+  CU(cudaMemcpyAsync(out_sel, ctx->sel_out.p, (size_t)k * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaMemcpyAsync(out_val, ctx->val_out.p, (size_t)k * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaMemcpyAsync(out_gain, ctx->gain_out.p, (size_t)k * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  float tot = 0;
+  CU(cudaEventElapsedTime(&tot, tstart, tend));
+  cudaEventDestroy(tstart);
+  cudaEventDestroy(tend);
+  acc_ms[3] = tot;
+  for (int i = 0; i < 4; ++i) ctx->last_ms[i] = acc_ms[i];
+  ctx->steps_done = k;
+  if (out_evals) {
+    int64_t ev = 0;
+    for (int s = 0; s < k; ++s) ev += ctx->n - s;
+    *out_evals = ev;
+  }
+  for (int s = 0; s < k; ++s)
+    if (out_sel[s] < 0) return fail(ctx, EBC_ECUDA, "greedy step " + std::to_string(s) + " found no candidate");
+  return EBC_OK;
+}
+
+int ebc_shard_set_range(ebc_ctx* ctx, int64_t c0, int64_t c1) {
+  if (!ctx) return fail(nullptr, EBC_EINVAL, "ebc_shard_set_range: NULL context");
+  if (c0 < 0 || c1 < c0 || c1 > ctx->n)
+    return fail(ctx, EBC_EINVAL,
+                "candidate range [" + std::to_string(c0) + ", " + std::to_string(c1) + ") outside [0, n)");
+  ctx->c0 = c0;
+  ctx->c1 = c1;
+  return EBC_OK;
+}
+
+int ebc_shard_step(ebc_ctx* ctx, int64_t* out_idx, double* out_gain, int64_t cap, int64_t* out_count,
+                   double* out_current) {
+  if (!ctx || !out_count) return fail(ctx, EBC_EINVAL, "ebc_shard_step: NULL argument");
+  CU(cudaSetDevice(ctx->device));
+  int count = 0;
+  if (ctx->c1 > ctx->c0) {
+    ctx->launches = 0;
+    int rc = run_step_select(ctx, 0, 0, nullptr);
+    if (rc) return rc;
+    CU(cudaMemcpyAsync(&count, ctx->wcount, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+  }
+  *out_count = count;
+  const int64_t m = std::min<int64_t>(cap, count);
+  if (m > 0) {
+    if (!out_idx || !out_gain) return fail(ctx, EBC_EINVAL, "ebc_shard_step: NULL output buffer");
+    CU(cudaMemcpyAsync(out_idx, ctx->wlist, (size_t)m * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(out_gain, ctx->wgain, (size_t)m * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  if (out_current) CU(cudaMemcpyAsync(out_current, ctx->cur, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return EBC_OK;
+}
+
+int ebc_shard_commit(ebc_ctx* ctx, int64_t s, double* out_value) {
+  if (!ctx) return fail(nullptr, EBC_EINVAL, "ebc_shard_commit: NULL context");
+  if (s < 0 || s >= ctx->n)
+    return fail(ctx, EBC_EINDEX, "index " + std::to_string(s) + " out of range for ground size " +
+                                     std::to_string(ctx->n));
+  CU(cudaSetDevice(ctx->device));
+  CU(cudaMemcpyAsync(ctx->best, &s, sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
+  const unsigned char one = 1;
+  CU(cudaMemcpyAsync(ctx->selected + s, &one, 1, cudaMemcpyHostToDevice, ctx->stream));
+  int rc = run_update(ctx, 0, nullptr, nullptr);
+  if (rc) return rc;
+  double v = 0;
+  CU(cudaMemcpyAsync(&v, ctx->cur, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  ctx->steps_done += 1;
+  if (out_value) *out_value = v;
+  return EBC_OK;
+}
+
+int ebc_eval_multiset(ebc_ctx* ctx, const int64_t* offsets, const int64_t* idx, int64_t l, double* out_f,
+                      int64_t* out_bad_set, int64_t* out_bad_index) {
+  if (!ctx) return fail(nullptr, EBC_EINVAL, "ebc_eval_multiset: NULL context");
+  if (l < 1) return fail(ctx, EBC_EINVAL, "a multiset must contain at least one set");
+  if (!offsets || !out_f) return fail(ctx, EBC_EINVAL, "ebc_eval_multiset: NULL argument");
+  if (offsets[0] != 0) return fail(ctx, EBC_EINVAL, "offsets[0] must be 0");
+  for (int64_t j = 0; j < l; ++j)
+    if (offsets[j + 1] < offsets[j]) return fail(ctx, EBC_EINVAL, "offsets must be non-decreasing");
+  const int64_t nnz = offsets[l];
+  if (nnz > 0 && !idx) return fail(ctx, EBC_EINVAL, "ebc_eval_multiset: NULL idx");
+  // validate in set order (core.py:136-143): negative indices first, as EvalMultiset does
+  for (int64_t j = 0; j < l; ++j)
+    for (int64_t p = offsets[j]; p < offsets[j + 1]; ++p)
+      if (idx[p] < 0) {
+        if (out_bad_set) *out_bad_set = j;
+        if (out_bad_index) *out_bad_index = idx[p];
+        return fail(ctx, EBC_EINDEX, "set " + std::to_string(j) + " contains a negative index");
+      }
+  for (int64_t j = 0; j < l; ++j)
+    for (int64_t p = offsets[j]; p < offsets[j + 1]; ++p)
+      if (idx[p] >= ctx->n) {
+        if (out_bad_set) *out_bad_set = j;
+        if (out_bad_index) *out_bad_index = idx[p];
+        return fail(ctx, EBC_EINDEX, "set " + std::to_string(j) + ": index " + std::to_string(idx[p]) +
+                                         " out of range for ground size " + std::to_string(ctx->n));
+      }
+  CU(cudaSetDevice(ctx->device));
+  ctx->launches = 0;
+  int rc = ensure(ctx, ctx->ms_off, (size_t)(l + 1) * sizeof(int64_t));
+  if (!rc) rc = ensure(ctx, ctx->ms_idx, (size_t)std::max<int64_t>(nnz, 1) * sizeof(int64_t));
+  if (!rc) rc = ensure(ctx, ctx->ms_out, (size_t)l * sizeof(double));
+  if (rc) return rc;
+  const int64_t batch = std::min<int64_t>(l, 65535);
+  rc = ensure(ctx, ctx->ms_part, (size_t)l * ctx->nchunks * sizeof(double));
+  if (rc) return rc;
+  cudaEvent_t a, b;
+  CU(cudaEventCreate(&a));
+  CU(cudaEventCreate(&b));
+  CU(cudaMemcpyAsync(ctx->ms_off.p, offsets, (size_t)(l + 1) * sizeof(int64_t), cudaMemcpyHostToDevice,
+                     ctx->stream));
+  if (nnz > 0)
+    CU(cudaMemcpyAsync(ctx->ms_idx.p, idx, (size_t)nnz * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
+  CU(cudaEventRecord(a, ctx->stream));
+  for (int64_t s0 = 0; s0 < l; s0 += batch) {
+    const int64_t nb = std::min<int64_t>(batch, l - s0);
+    dim3 grid(ctx->nchunks, (unsigned)nb);
+    double* part = (double*)ctx->ms_part.p + s0 * ctx->nchunks;
+    if (ctx->dtype == EBC_F64)
+      k_multiset<double><<<grid, RED_THREADS, 0, ctx->stream>>>(ctx->V64, ctx->pitch, ctx->n, ctx->d, ctx->e0d,
+                                                               (const int64_t*)ctx->ms_off.p,
+                                                               (const int64_t*)ctx->ms_idx.p, s0, ctx->nchunks, part);
+    else
+      k_multiset<float><<<grid, RED_THREADS, 0, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->n, ctx->d, ctx->e0d,
+                                                              (const int64_t*)ctx->ms_off.p,
+                                                              (const int64_t*)ctx->ms_idx.p, s0, ctx->nchunks, part);
+    KCHECK();
+  }
+  k_multiset_final<<<(unsigned)((l + 255) / 256), 256, 0, ctx->stream>>>(
+      (const double*)ctx->ms_part.p, l, ctx->nchunks, 1.0 / (double)ctx->n, (double*)ctx->ms_out.p);
+  KCHECK();
+  CU(cudaEventRecord(b, ctx->stream));
+  CU(cudaMemcpyAsync(out_f, ctx->ms_out.p, (size_t)l * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  float ms = 0;
+  CU(cudaEventElapsedTime(&ms, a, b));
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  ctx->last_ms[0] = ms;
+  ctx->last_ms[1] = 0;
+  ctx->last_ms[2] = 0;
+  ctx->last_ms[3] = ms;
+  return EBC_OK;
+}
+
+void ebc_destroy(ebc_ctx* ctx) { free_ctx(ctx); }
+
+}  // extern "C"

@@ -1,0 +1,605 @@
+// kernels.cuh -- sm_100a kernels for the EBC Greedy / multiset hot path.
+//
+//   K0 k_init           d(v,e0) in fp64, cached minima, baseline partials      (ebc.py:72)
+//   K1 k_screen         fused distance -> min(cm, .) -> sum over V, fp32 FFMA,  (batched.py:202-226
+//                       with a per-candidate certified error bound               at the Greedy call site)
+//   K3 k_finalize/k_window/k_refine/k_pick
+//                       certified near-tie window, exact fp64 gains, argmax with (optimize.py:83-88)
+//                       the reference tie window and lowest-index rule
+//   K4 k_update         fold the chosen exemplar into cm64/cm32, f(S) in fp64    (new: cached-min)
+//   K2 k_multiset       arbitrary CSR sets, fp64, work-matrix row sums           (batched.py:180-240,
+//                                                                                 Alg. 2 batched.py:272-374)
+//
+// Determinism: no floating-point atomics.  Every sum over points uses the same
+// fixed structure -- chunks of RCH points, a fixed 256-thread tree inside each
+// chunk, then a left-to-right pass over chunks -- so a candidate's value never
+// depends on its slot, on the launch shape or on how candidates are sharded
+// across GPUs, and the empty set evaluates to exactly 0.0.
+#pragma once
+#include <cfloat>
+#include <cstdint>
+
+#include "ptx.cuh"
+
+namespace ebc {
+
+constexpr int RCH = 1024;         // points per reduction chunk
+constexpr int RED_THREADS = 256;  // threads of every chunk-reduction block
+
+// ---------------------------------------------------------------- reductions
+
+// Fixed-tree sum over the 256 threads of a block; result valid in thread 0.
+__device__ __forceinline__ double block_sum_256(double v, double* sbuf) {
+  const int t = threadIdx.x;
+  sbuf[t] = v;
+  __syncthreads();
+#pragma unroll
+  for (int s = 128; s > 0; s >>= 1) {
+    if (t < s) sbuf[t] += sbuf[t + s];
+    __syncthreads();
+  }
+  double r = sbuf[0];
+  __syncthreads();
+  return r;
+}
+
+// Sequential left-to-right sum of chunk partials (one thread).
+__device__ __forceinline__ double chunk_total(const double* part, int nchunks) {
+  double s = 0.0;
+  for (int c = 0; c < nchunks; ++c) s += part[c];
+  return s;
+}
+
+// Order-preserving map of a double onto a signed 64-bit key (for atomicMax).
+__device__ __forceinline__ long long dkey(double x) {
+  long long b = __double_as_longlong(x);
+  return b >= 0 ? b : (b ^ 0x7fffffffffffffffLL);
+}
+__device__ __forceinline__ double dkey_inv(long long k) {
+  return __longlong_as_double(k >= 0 ? k : (k ^ 0x7fffffffffffffffLL));
+}
+
+// fp64 squared distance of stored row `row` (type T, `pitch` elements) to a
+// candidate held in shared memory as fp64 -- sequential over dims.
+template <typename T>
+__device__ __forceinline__ double dist64_row(const T* __restrict__ row, const double* cd, int d) {
+  double s = 0.0;
+  for (int k = 0; k < d; ++k) {
+    double t = (double)row[k] - cd[k];
+    s = fma(t, t, s);
+  }
+  return s;
+}
+
+// ---------------------------------------------------------------- K0: init
+
+// Widen/pad the uploaded rows into the device layout (n_pad x pitch, zero pad).
+template <typename S, typename D>
+__global__ void k_pad(const S* __restrict__ src, int64_t n, int d, D* __restrict__ dst, int pitch) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t total = n * (int64_t)pitch;
+  for (; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t v = i / pitch;
+    int k = (int)(i - v * pitch);
+    dst[i] = k < d ? (D)(float)src[v * d + k] : (D)0;
+  }
+}
+template <>
+__global__ void k_pad<double, double>(const double* __restrict__ src, int64_t n, int d,
+                                      double* __restrict__ dst, int pitch) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t total = n * (int64_t)pitch;
+  for (; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t v = i / pitch;
+    int k = (int)(i - v * pitch);
+    dst[i] = k < d ? src[v * d + k] : 0.0;
+  }
+}
+
+// e0d[v] = d(v, e0) (fp64); cm64 = e0d; pt = {-cm32, tau}; chunk partials of e0d.
+template <typename T>
+__global__ void __launch_bounds__(RED_THREADS) k_init(const T* __restrict__ V, int pitch, int64_t n, int d,
+                                                      const double* __restrict__ e0, float kappa2,
+                                                      double* __restrict__ e0d, double* __restrict__ cm64,
+                                                      float2* __restrict__ pt, double* __restrict__ part) {
+  __shared__ double sbuf[RED_THREADS];
+  __shared__ double se0[1024];
+  for (int k = threadIdx.x; k < d && k < 1024; k += blockDim.x) se0[k] = e0[k];
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * RCH;
+  double acc = 0.0;
+  for (int i = 0; i < RCH / RED_THREADS; ++i) {
+    int64_t v = base + threadIdx.x + (int64_t)i * RED_THREADS;
+    if (v < n) {
+      double t = d <= 1024 ? dist64_row(V + v * pitch, se0, d) : dist64_row(V + v * pitch, e0, d);
+      e0d[v] = t;
+      cm64[v] = t;
+      float c32 = (float)t;
+      pt[v] = make_float2(-c32, kappa2 * c32);
+      acc += t;
+    }
+  }
+  double s = block_sum_256(acc, sbuf);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+// Reset the cached minima to d(., e0) (ebc_reset / start of a Greedy run).
+__global__ void k_reset(int64_t n, const double* __restrict__ e0d, float kappa2, double* __restrict__ cm64,
+                        float2* __restrict__ pt, unsigned char* __restrict__ selected) {
+  int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v < n) {
+    double t = e0d[v];
+    cm64[v] = t;
+    float c32 = (float)t;
+    pt[v] = make_float2(-c32, kappa2 * c32);
+    selected[v] = 0;
+  }
+}
+
+__global__ void k_total(const double* __restrict__ part, int nchunks, double scale, double* __restrict__ out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) *out = chunk_total(part, nchunks) * scale;
+}
+
+// ---------------------------------------------------------------- K1: screen
+//
+// gain32[c] = sum_v max(0, cm32[v] - d32(v, c)) for a tile of candidates, with
+// a certified bound e[c] such that |gain32 - gain_exact| <= e*infl + 8u*gain32.
+//
+// Layout: 256 threads = 8 warps as WP x WC = 2 x 4; inside a warp 8 lane-rows
+// (points) x 4 lane-cols (candidates); each thread owns TP=4 points x TC=8
+// candidates -> CTA tile = 64 points x 128 candidates.  The candidate tile is
+// loaded once by the bulk-copy engine and stays in shared memory; V tiles
+// (64 rows + their {-cm32, tau} pairs) stream through an mbarrier ring.
+//
+// Per pair the accumulator starts at -cm32[v], so after the d-dim FADD/FFMA
+// chain it holds s = d32 - cm32 directly:  gain += max(-s, 0),
+// err += (s < tau[v]) ? tau[v] : 0  with tau = 2(d+8)u*cm32.
+namespace screen {
+constexpr int TP = 4, TC = 8, LR = 8, LC = 4, WP = 2, WC = 4;
+constexpr int THREADS = 32 * WP * WC;
+constexpr int PT_ = WP * LR * TP;  // 64 points per V tile
+constexpr int CT_ = WC * LC * TC;  // 128 candidates per CTA
+}  // namespace screen
+
+template <int STAGES>
+__global__ void __launch_bounds__(screen::THREADS, 2)
+    k_screen(const float* __restrict__ V, const float2* __restrict__ pt, int pitch, int d4, int64_t cand0,
+             int ntiles, int tiles_per_split, double* __restrict__ part_g, float* __restrict__ part_e,
+             int64_t part_stride) {
+  using namespace screen;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int wp = warp % WP, wc = warp / WP;
+  const int r = lane & 7, q = lane >> 3;
+
+  const size_t cand_bytes = (size_t)CT_ * pitch * sizeof(float);
+  const size_t vt_bytes = (size_t)PT_ * pitch * sizeof(float);
+  const size_t pt_bytes = (size_t)PT_ * sizeof(float2);
+  float* cs = reinterpret_cast<float*>(smem);
+  unsigned char* stage_base = smem + cand_bytes;
+  const size_t stage_bytes = vt_bytes + pt_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stage_base + STAGES * stage_bytes);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + STAGES;
+  uint64_t* cbar = bars + 2 * STAGES;
+
+  const int t0 = blockIdx.y * tiles_per_split;
+  const int t1 = min(ntiles, t0 + tiles_per_split);
+  const int nt = t1 - t0;
+  const int64_t crow = cand0 + (int64_t)blockIdx.x * CT_;
+
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], WP * WC);
+    }
+    mbar_init(cbar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    mbar_arrive_expect_tx(cbar, (uint32_t)cand_bytes);
+    bulk_g2s(cs, V + crow * pitch, (uint32_t)cand_bytes, cbar);
+    for (int s = 0; s < STAGES && s < nt; ++s) {
+      unsigned char* st = stage_base + s * stage_bytes;
+      const int64_t prow = (int64_t)(t0 + s) * PT_;
+      mbar_arrive_expect_tx(&full[s], (uint32_t)stage_bytes);
+      bulk_g2s(st, V + prow * pitch, (uint32_t)vt_bytes, &full[s]);
+      bulk_g2s(st + vt_bytes, pt + prow, (uint32_t)pt_bytes, &full[s]);
+    }
+  }
+
+  float g[TC], e[TC];
+#pragma unroll
+  for (int j = 0; j < TC; ++j) { g[j] = 0.f; e[j] = 0.f; }
+  double g64 = 0.0;  // this lane's fp64 total for candidate j == r (after transposed reduce)
+
+  const float* crow_s[TC];
+#pragma unroll
+  for (int j = 0; j < TC; ++j) crow_s[j] = cs + (wc * (LC * TC) + q + LC * j) * pitch;
+
+  mbar_wait(cbar, 0);
+
+  for (int it = 0; it < nt; ++it) {
+    const int s = it % STAGES;
+    const uint32_t ph = (it / STAGES) & 1;
+    mbar_wait(&full[s], ph);
+    const float* vs = reinterpret_cast<const float*>(stage_base + s * stage_bytes);
+    const float2* ps = reinterpret_cast<const float2*>(stage_base + s * stage_bytes + vt_bytes);
+
+    float acc[TP][TC];
+    float tau[TP];
+    const float* vrow[TP];
+#pragma unroll
+    for (int i = 0; i < TP; ++i) {
+      const int p = wp * (LR * TP) + r + LR * i;
+      const float2 pp = ps[p];
+      tau[i] = pp.y;
+      vrow[i] = vs + p * pitch;
+#pragma unroll
+      for (int j = 0; j < TC; ++j) acc[i][j] = pp.x;
+    }
+    for (int k4 = 0; k4 < d4; ++k4) {
+      float4 a[TP], b[TC];
+#pragma unroll
+      for (int i = 0; i < TP; ++i) a[i] = *reinterpret_cast<const float4*>(vrow[i] + 4 * k4);
+#pragma unroll
+      for (int j = 0; j < TC; ++j) b[j] = *reinterpret_cast<const float4*>(crow_s[j] + 4 * k4);
+#pragma unroll
+      for (int i = 0; i < TP; ++i) {
+#pragma unroll
+        for (int j = 0; j < TC; ++j) {
+          float t;
+          t = a[i].x - b[j].x; acc[i][j] = fmaf(t, t, acc[i][j]);
+          t = a[i].y - b[j].y; acc[i][j] = fmaf(t, t, acc[i][j]);
+          t = a[i].z - b[j].z; acc[i][j] = fmaf(t, t, acc[i][j]);
+          t = a[i].w - b[j].w; acc[i][j] = fmaf(t, t, acc[i][j]);
+        }
+      }
+    }
+    // stage consumed: release it to the producer
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+
+    // epilogue: s = d32 - cm32
+#pragma unroll
+    for (int i = 0; i < TP; ++i) {
+#pragma unroll
+      for (int j = 0; j < TC; ++j) {
+        const float sv = acc[i][j];
+        g[j] += fmaxf(-sv, 0.f);
+        e[j] += sv < tau[i] ? tau[i] : 0.f;
+      }
+    }
+    // fold this tile's fp32 gains into fp64: transposed butterfly over the 8
+    // lane-rows leaves lane r holding the warp's tile sum of candidate j = r.
+    {
+      float h[4];
+      const bool up4 = (r & 4) != 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float send = up4 ? g[j] : g[j + 4];
+        float keep = up4 ? g[j + 4] : g[j];
+        h[j] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+      }
+      float h2[2];
+      const bool up2 = (r & 2) != 0;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        float send = up2 ? h[j] : h[j + 2];
+        float keep = up2 ? h[j + 2] : h[j];
+        h2[j] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+      }
+      const bool up1 = (r & 1) != 0;
+      float send = up1 ? h2[0] : h2[1];
+      float keep = up1 ? h2[1] : h2[0];
+      float tot = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+      g64 += (double)tot;
+#pragma unroll
+      for (int j = 0; j < TC; ++j) g[j] = 0.f;
+    }
+
+    // producer: refill this stage with tile it + STAGES once every warp released it
+    if (tid == 0 && it + STAGES < nt) {
+      mbar_wait(&empty[s], ph);
+      unsigned char* st = stage_base + s * stage_bytes;
+      const int64_t prow = (int64_t)(t0 + it + STAGES) * PT_;
+      mbar_arrive_expect_tx(&full[s], (uint32_t)stage_bytes);
+      bulk_g2s(st, V + prow * pitch, (uint32_t)vt_bytes, &full[s]);
+      bulk_g2s(st + vt_bytes, pt + prow, (uint32_t)pt_bytes, &full[s]);
+    }
+  }
+
+  // error bound: same transposed reduce in fp32 (covered by the inflation factor)
+  float etot;
+  {
+    float h[4];
+    const bool up4 = (r & 4) != 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float send = up4 ? e[j] : e[j + 4];
+      float keep = up4 ? e[j + 4] : e[j];
+      h[j] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+    float h2[2];
+    const bool up2 = (r & 2) != 0;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      float send = up2 ? h[j] : h[j + 2];
+      float keep = up2 ? h[j + 2] : h[j];
+      h2[j] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+    }
+    const bool up1 = (r & 1) != 0;
+    float send = up1 ? h2[0] : h2[1];
+    float keep = up1 ? h2[1] : h2[0];
+    etot = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+  }
+  // lane (r, q) of warp (wp, wc) now holds candidate  wc*32 + q + 4*r
+  __syncthreads();  // all stages idle: reuse the ring for the cross-warp combine
+  double* rg = reinterpret_cast<double*>(stage_base);
+  float* re = reinterpret_cast<float*>(stage_base + WP * CT_ * sizeof(double));
+  const int cl = wc * (LC * TC) + q + LC * r;
+  rg[wp * CT_ + cl] = g64;
+  re[wp * CT_ + cl] = etot;
+  __syncthreads();
+  if (tid < CT_) {
+    double gs = 0.0;
+    float es = 0.f;
+#pragma unroll
+    for (int w = 0; w < WP; ++w) {
+      gs += rg[w * CT_ + tid];
+      es += re[w * CT_ + tid];
+    }
+    const int64_t c = crow + tid;
+    part_g[blockIdx.y * part_stride + c] = gs;
+    part_e[blockIdx.y * part_stride + c] = es;
+  }
+}
+
+inline size_t screen_smem_bytes(int pitch, int stages) {
+  using namespace screen;
+  size_t cand = (size_t)CT_ * pitch * sizeof(float);
+  size_t stage = (size_t)PT_ * pitch * sizeof(float) + (size_t)PT_ * sizeof(float2);
+  size_t ring = stages * stage;
+  size_t red = (size_t)WP * CT_ * (sizeof(double) + sizeof(float));
+  if (ring < red) ring = red;
+  return cand + ring + (2 * stages + 1) * sizeof(uint64_t);
+}
+
+// ---------------------------------------------------------------- K3: window + refine + pick
+
+// Combine the split partials, form the certified interval [lb, ub] and fold the
+// block's largest lower bound into *maxlb (order-independent atomicMax).
+__global__ void k_finalize(int64_t c0, int64_t c1, int nsplit, const double* __restrict__ part_g,
+                           const float* __restrict__ part_e, int64_t part_stride, double einfl,
+                           const unsigned char* __restrict__ selected, double* __restrict__ ub,
+                           long long* __restrict__ maxlb) {
+  __shared__ long long smax[256];
+  const int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  long long key = dkey(-INFINITY);
+  if (c < c1) {
+    double g = 0.0, e = 0.0;
+    for (int s = 0; s < nsplit; ++s) {
+      g += part_g[s * part_stride + c];
+      e += (double)part_e[s * part_stride + c];
+    }
+    const double eps = e * einfl + 4.8e-7 * g + 1e-300;  // 8u * g
+    if (selected[c]) {
+      ub[c - c0] = -INFINITY;
+    } else {
+      ub[c - c0] = g + eps;
+      key = dkey(fmax(g - eps, 0.0));
+    }
+  }
+  smax[threadIdx.x] = key;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) smax[threadIdx.x] = max(smax[threadIdx.x], smax[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) atomicMax(maxlb, smax[0]);
+}
+
+// W = {c : ub_c >= max lb - margin}  (append order is irrelevant: the pick is by
+// exact value and lowest index).
+__global__ void k_window(int64_t c0, int64_t c1, const double* __restrict__ ub, const long long* __restrict__ maxlb,
+                         double margin, int* __restrict__ wcount, int64_t* __restrict__ wlist) {
+  const int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < c1) {
+    const double thr = dkey_inv(*maxlb) - margin;
+    const double u = ub[c - c0];
+    if (u >= thr && u > -INFINITY) {
+      int slot = atomicAdd(wcount, 1);
+      wlist[slot] = c;
+    }
+  }
+}
+
+// Every candidate of the screen range is in W (FP64 storage: no fp32 screen).
+__global__ void k_window_all(int64_t c0, int64_t c1, const unsigned char* __restrict__ selected,
+                             int* __restrict__ wcount, int64_t* __restrict__ wlist) {
+  const int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < c1 && !selected[c]) {
+    int slot = atomicAdd(wcount, 1);
+    wlist[slot] = c;
+  }
+}
+
+// Exact fp64 gain partials: part_r[w*nchunks + ch] = sum over chunk ch of
+// max(0, cm64[v] - d64(v, c_w)).  Persistent grid over (w, chunk) units.
+template <typename T>
+__global__ void __launch_bounds__(RED_THREADS) k_refine(const T* __restrict__ V, int pitch, int64_t n, int d,
+                                                        const double* __restrict__ cm64,
+                                                        const int* __restrict__ wcount,
+                                                        const int64_t* __restrict__ wlist, int nchunks,
+                                                        double* __restrict__ part_r) {
+  extern __shared__ double cd[];  // d doubles
+  __shared__ double sbuf[RED_THREADS];
+  const int64_t units = (int64_t)(*wcount) * nchunks;
+  for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+    const int64_t w = u / nchunks;
+    const int ch = (int)(u - w * nchunks);
+    const int64_t c = wlist[w];
+    __syncthreads();
+    for (int k = threadIdx.x; k < d; k += blockDim.x) cd[k] = (double)V[c * pitch + k];
+    __syncthreads();
+    double acc = 0.0;
+    for (int i = 0; i < RCH / RED_THREADS; ++i) {
+      const int64_t v = (int64_t)ch * RCH + threadIdx.x + (int64_t)i * RED_THREADS;
+      if (v < n) {
+        const double t = cm64[v] - dist64_row(V + v * pitch, cd, d);
+        acc += t > 0.0 ? t : 0.0;
+      }
+    }
+    const double s = block_sum_256(acc, sbuf);
+    if (threadIdx.x == 0) part_r[u] = s;
+  }
+}
+
+// Exact gains of W, the reference argmax rule (optimize.py:83-85):
+//   top = max value; window = 1e-12*max(1,|top|); best = lowest index with
+//   value >= top - window; value = f(S) + gain/N.
+// commit != 0: mark the winner selected and record it as step `step`.
+__global__ void __launch_bounds__(1024) k_pick(const int* __restrict__ wcount, const int64_t* __restrict__ wlist,
+                                               int nchunks, const double* __restrict__ part_r, double inv_n,
+                                               const double* __restrict__ cur, double* __restrict__ wgain,
+                                               int64_t* __restrict__ best, int commit, int step,
+                                               unsigned char* __restrict__ selected, int64_t* __restrict__ sel_out) {
+  __shared__ double smax[1024];
+  __shared__ long long smin[1024];
+  const int wc = *wcount;
+  const double f = *cur;
+  double top = -INFINITY;
+  for (int w = threadIdx.x; w < wc; w += blockDim.x) {
+    const double gsum = chunk_total(part_r + (int64_t)w * nchunks, nchunks);
+    wgain[w] = gsum;
+    const double val = __dadd_rn(f, __dmul_rn(gsum, inv_n));  // no FMA contraction: host pick() matches
+    top = fmax(top, val);
+  }
+  smax[threadIdx.x] = top;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) smax[threadIdx.x] = fmax(smax[threadIdx.x], smax[threadIdx.x + s]);
+    __syncthreads();
+  }
+  top = smax[0];
+  const double window = 1e-12 * fmax(1.0, fabs(top));
+  long long bi = LLONG_MAX;
+  for (int w = threadIdx.x; w < wc; w += blockDim.x) {
+    const double val = __dadd_rn(f, __dmul_rn(wgain[w], inv_n));
+    if (val >= top - window) bi = min(bi, (long long)wlist[w]);
+  }
+  smin[threadIdx.x] = bi;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) smin[threadIdx.x] = min(smin[threadIdx.x], smin[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const long long b = smin[0] == LLONG_MAX ? -1 : smin[0];
+    *best = b;
+    if (commit && b >= 0) {
+      selected[b] = 1;
+      sel_out[step] = b;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- K4: cached-min update
+
+// cm64 = min(cm64, d64(., s)); pt = {-cm32, tau}; chunk partials of (e0d - cm64).
+// The last block to finish turns the partials into f(S) and the step record.
+template <typename T>
+__global__ void __launch_bounds__(RED_THREADS) k_update(const T* __restrict__ V, int pitch, int64_t n, int d,
+                                                        const int64_t* __restrict__ best, float kappa2,
+                                                        const double* __restrict__ e0d, double* __restrict__ cm64,
+                                                        float2* __restrict__ pt, double* __restrict__ fpart,
+                                                        unsigned int* __restrict__ counter, double inv_n,
+                                                        double* __restrict__ cur, double* __restrict__ val_out,
+                                                        double* __restrict__ gain_out, int step) {
+  extern __shared__ double cd[];
+  __shared__ double sbuf[RED_THREADS];
+  __shared__ bool last;
+  const int64_t s = *best;
+  if (s < 0) return;
+  for (int k = threadIdx.x; k < d; k += blockDim.x) cd[k] = (double)V[s * pitch + k];
+  __syncthreads();
+  double acc = 0.0;
+  for (int i = 0; i < RCH / RED_THREADS; ++i) {
+    const int64_t v = (int64_t)blockIdx.x * RCH + threadIdx.x + (int64_t)i * RED_THREADS;
+    if (v < n) {
+      const double t = dist64_row(V + v * pitch, cd, d);
+      double m = cm64[v];
+      if (t < m) {
+        m = t;
+        cm64[v] = m;
+        const float c32 = (float)m;
+        pt[v] = make_float2(-c32, kappa2 * c32);
+      }
+      acc += e0d[v] - m;
+    }
+  }
+  const double bs = block_sum_256(acc, sbuf);
+  if (threadIdx.x == 0) {
+    fpart[blockIdx.x] = bs;
+    __threadfence();
+    const unsigned int ticket = atomicAdd(counter, 1u);
+    last = (ticket == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    const double fnew = chunk_total(fpart, gridDim.x) * inv_n;
+    const double fold = *cur;
+    if (val_out) val_out[step] = fnew;
+    if (gain_out) gain_out[step] = fnew - fold;
+    *cur = fnew;
+    *counter = 0u;
+  }
+}
+
+// ---------------------------------------------------------------- K2: multiset (work matrix)
+
+// part[j*nchunks + ch] = sum over chunk ch of (e0d[v] - min(e0d[v], min_{s in S_j} d64(v, s))).
+// One block per (chunk, set); members are read through L1 (broadcast across the block).
+template <typename T>
+__global__ void __launch_bounds__(RED_THREADS) k_multiset(const T* __restrict__ V, int pitch, int64_t n, int d,
+                                                          const double* __restrict__ e0d,
+                                                          const int64_t* __restrict__ offsets,
+                                                          const int64_t* __restrict__ idx, int64_t set0,
+                                                          int nchunks, double* __restrict__ part) {
+  __shared__ double sbuf[RED_THREADS];
+  const int ch = blockIdx.x;
+  const int64_t j = set0 + blockIdx.y;
+  const int64_t m0 = offsets[j], m1 = offsets[j + 1];
+  double acc = 0.0;
+  for (int i = 0; i < RCH / RED_THREADS; ++i) {
+    const int64_t v = (int64_t)ch * RCH + threadIdx.x + (int64_t)i * RED_THREADS;
+    if (v < n) {
+      const double base = e0d[v];
+      double m = base;
+      const T* row = V + v * pitch;
+      for (int64_t p = m0; p < m1; ++p) {
+        const T* mem = V + idx[p] * pitch;
+        double s = 0.0;
+        for (int k = 0; k < d; ++k) {
+          const double t = (double)row[k] - (double)__ldg(mem + k);
+          s = fma(t, t, s);
+        }
+        m = fmin(m, s);
+      }
+      acc += base - m;
+    }
+  }
+  const double bs = block_sum_256(acc, sbuf);
+  if (threadIdx.x == 0) part[blockIdx.y * (int64_t)nchunks + ch] = bs;
+}
+
+__global__ void k_multiset_final(const double* __restrict__ part, int64_t l, int nchunks, double inv_n,
+                                 double* __restrict__ out) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < l) out[j] = chunk_total(part + j * nchunks, nchunks) * inv_n;
+}
+
+}  // namespace ebc

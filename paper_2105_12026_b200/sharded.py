@@ -1,0 +1,168 @@
+"""Candidate-sharded Greedy across GPUs, one process per GPU.
+
+V and the cached minima are replicated on every rank; rank r screens only the
+candidates [c0, c1) of a contiguous partition of the ground indices.  Per
+Greedy step:
+
+  1. ``engine.local_step()`` -- on the device: fp32 screen of the local
+     candidates, certified window, exact fp64 gains of the window.  Returns the
+     local list (index, gain64) and f(S).
+  2. ``allgather_candidates`` -- NCCL (or gloo) all-gather of those (index,
+     gain) pairs; a handful of 16-byte records per rank.
+  3. ``pick`` -- every rank applies the reference argmax rule (optimize.py:83-85)
+     to the union; all ranks hold bit-identical inputs, so they agree.
+  4. ``engine.commit(best)`` -- every rank folds the winner into its cached
+     minima and recomputes f(S) with the fixed-order fp64 reduction.
+
+Why the union of local windows gives the single-GPU answer: a local window
+W_r = {c in shard r : ub_c >= max_{c' in shard r} lb_c' - margin} contains
+every candidate of shard r whose exact value is within the reference tie
+window of the global top, and each candidate's exact gain is
+computed with the same point chunking on every rank.  So selections are
+identical for any number of ranks.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _native
+from .core import Summary
+from .optimize import OptimizerBudget
+
+
+def shard_range(n: int, rank: int, world: int) -> Tuple[int, int]:
+    """Contiguous candidate range of `rank`: ceil(n / world) indices per rank."""
+    per = (n + world - 1) // world
+    c0 = min(n, rank * per)
+    return c0, min(n, c0 + per)
+
+
+def pick(idx: np.ndarray, gain: np.ndarray, current: float, n: int) -> Tuple[int, float]:
+    """Reference argmax rule over exact gains (optimize.py:83-85).
+
+    value_c = f(S) + gain_c / n, computed with separately rounded fp64 ops
+    exactly as the device pick kernel does; top = max value; window =
+    1e-12 * max(1, |top|); the winner is the lowest index with value >= top - window.
+    """
+    if idx.size == 0:
+        raise RuntimeError("no remaining candidate on any rank")
+    inv_n = 1.0 / float(n)
+    values = np.float64(current) + np.asarray(gain, dtype=np.float64) * np.float64(inv_n)
+    top = float(values.max())
+    window = 1e-12 * max(1.0, abs(top))
+    ok = values >= top - window
+    best = int(np.asarray(idx)[ok].min())
+    return best, top
+
+
+def allgather_candidates(idx: np.ndarray, gain: np.ndarray, group=None, device=None):
+    """All-gather variable-length (index, gain) lists: one all_gather of the
+    counts, one of the padded records.  `device` is where the collective's
+    tensors live (a CUDA device for NCCL, CPU for gloo)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    dev = torch.device("cpu") if device is None else torch.device(device)
+    cnt = torch.tensor([idx.size], dtype=torch.int64, device=dev)
+    counts = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
+    dist.all_gather(counts, cnt, group=group)
+    counts = [int(c.item()) for c in counts]
+    m = max(1, max(counts))
+    rec = torch.full((m, 2), float("nan"), dtype=torch.float64, device=dev)
+    if idx.size:
+        # indices < 2^53 are exact in fp64
+        rec[: idx.size, 0] = torch.from_numpy(np.asarray(idx, dtype=np.float64)).to(dev)
+        rec[: idx.size, 1] = torch.from_numpy(np.asarray(gain, dtype=np.float64)).to(dev)
+    recs = [torch.empty_like(rec) for _ in range(world)]
+    dist.all_gather(recs, rec, group=group)
+    out_i: List[np.ndarray] = []
+    out_g: List[np.ndarray] = []
+    for c, r in zip(counts, recs):
+        r = r[:c].cpu().numpy()
+        out_i.append(r[:, 0].astype(np.int64))
+        out_g.append(r[:, 1])
+    return np.concatenate(out_i), np.concatenate(out_g)
+
+
+class NativeShardEngine:
+    """Device side of one rank (wraps ebc_shard_* of include/ebc200.h)."""
+
+    def __init__(self, f, c0: int, c1: int):
+        self.f = f
+        self.lib = f._lib
+        self.ctx = f.native_context
+        _native.check(self.lib.ebc_shard_set_range(self.ctx, c0, c1), self.ctx)
+        _native.check(self.lib.ebc_reset(self.ctx), self.ctx)
+        self.cap = 64
+        self._idx = np.empty(self.cap, dtype=np.int64)
+        self._gain = np.empty(self.cap, dtype=np.float64)
+
+    def local_step(self):
+        count = ctypes.c_int64()
+        cur = ctypes.c_double()
+        while True:
+            rc = self.lib.ebc_shard_step(self.ctx, self._idx.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                         self._gain.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), self.cap,
+                                         ctypes.byref(count), ctypes.byref(cur))
+            _native.check(rc, self.ctx)
+            if count.value <= self.cap:
+                break
+            self.cap = int(count.value)
+            self._idx = np.empty(self.cap, dtype=np.int64)
+            self._gain = np.empty(self.cap, dtype=np.float64)
+        m = int(count.value)
+        return self._idx[:m].copy(), self._gain[:m].copy(), float(cur.value)
+
+    def commit(self, s: int) -> float:
+        out = ctypes.c_double()
+        _native.check(self.lib.ebc_shard_commit(self.ctx, int(s), ctypes.byref(out)), self.ctx)
+        return float(out.value)
+
+    def close(self):
+        # restore the full candidate range for later single-device calls
+        self.lib.ebc_shard_set_range(self.ctx, 0, self.f.ground.n)
+
+
+def greedy_sharded_loop(engine, n: int, k: int, group=None, device=None) -> Summary:
+    """Drive k sharded Greedy steps with any engine exposing local_step/commit."""
+    t0 = time.perf_counter()
+    selected: List[int] = []
+    gains: List[float] = []
+    current = 0.0
+    evaluations = 0
+    for step in range(k):
+        idx, gain, cur = engine.local_step()
+        all_idx, all_gain = allgather_candidates(idx, gain, group=group, device=device)
+        best, _top = pick(all_idx, all_gain, cur, n)
+        newval = engine.commit(best)
+        evaluations += n - step
+        gains.append(newval - current)
+        current = newval
+        selected.append(best)
+    return Summary(selected=selected, value=current, gains=gains, evaluations=evaluations,
+                   runtime_seconds=time.perf_counter() - t0)
+
+
+def greedy_maximize_sharded(f, budget: OptimizerBudget, group=None) -> Summary:
+    """Greedy over all ranks of `group` (torch.distributed must be initialised;
+    each rank passes its own EbcFunction built on its own GPU from the same data)."""
+    import torch
+    import torch.distributed as dist
+
+    n = f.ground.n
+    if budget.k > n:
+        raise ValueError(f"k={budget.k} exceeds ground size {n}")
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    c0, c1 = shard_range(n, rank, world)
+    engine = NativeShardEngine(f, c0, c1)
+    device = f"cuda:{torch.cuda.current_device()}" if dist.get_backend(group) == "nccl" else None
+    try:
+        return greedy_sharded_loop(engine, n, int(budget.k), group=group, device=device)
+    finally:
+        engine.close()

@@ -1,0 +1,234 @@
+"""Parity of the CUDA path (through the C-ABI) with the reference and the oracle.
+
+Bars (BASELINE.json north_star): Greedy-selected indices bit-exact; f values
+within 1e-5 relative for fp32 (we assert far tighter: every reported value is
+an fp64 fixed-order reduction); fp16 storage judged against the fp16-stored
+oracle with the same bars.
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2105_12026_b200 as eb
+from conftest import GOLDEN_DIR, case_sets, load_golden, max_scaled_diff, stored
+from paper_2105_12026_b200.sharded import NativeShardEngine, pick, shard_range
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = load_golden()
+GREEDY = [c for c in GOLDEN["cases"] if c["kind"] == "greedy"]
+MULTI = [c for c in GOLDEN["cases"] if c["kind"] == "multiset"]
+PREC = {"fp64": eb.Precision.FP64, "fp32": eb.Precision.FP32, "fp16-storage": eb.Precision.FP16_STORAGE}
+
+
+def fn(data, precision=eb.Precision.FP64, e0=None):
+    return eb.EbcFunction(eb.GroundMatrix(data, precision), e0=e0)
+
+
+# ------------------------------------------------------------ known answers (reference tests)
+
+def test_two_point_hand_values():
+    f = fn([[1.0, 0.0], [0.0, 1.0]])
+    assert f.baseline_loss == 1.0
+    assert f.value([]) == 0.0
+    assert f.value([0]) == 0.5 and f.value([0, 1]) == 1.0
+    assert f.marginal_gain([], 0) == 0.5 and f.marginal_gain([0], 1) == 0.5
+    assert f.marginal_gain([0], 0) == 0.0
+    ms = eb.EvalMultiset([[0], [1], [0, 1]])
+    assert eb.evaluate_with_backend(f, ms).tolist() == [0.5, 0.5, 1.0]
+    assert eb.evaluate_with_backend(f, eb.EvalMultiset([[]])).tolist() == [0.0]
+
+
+def test_index_errors_name_the_set():
+    f = fn([[1.0, 0.0], [0.0, 1.0]])
+    with pytest.raises(IndexError, match="set 1: index 9 out of range for ground size 2"):
+        eb.evaluate_with_backend(f, eb.EvalMultiset([[0], [9]]))
+    with pytest.raises(IndexError, match="out of range"):
+        f.value([2])
+
+
+def test_three_point_greedy_and_ties():
+    f = fn([[1.0, 0.0], [0.0, 1.0], [5.0, 5.0]])
+    s = eb.greedy_maximize(f, eb.OptimizerBudget(k=1))
+    assert s.selected == [2] and s.value == pytest.approx(50.0 / 3.0, rel=1e-12)
+    assert eb.greedy_maximize(f, eb.OptimizerBudget(k=2)).evaluations == 3 + 2
+    with pytest.raises(ValueError, match="exceeds"):
+        eb.greedy_maximize(f, eb.OptimizerBudget(k=4))
+    g = fn([[3.0, 3.0], [1.0, 1.0], [3.0, 3.0]])
+    assert eb.greedy_maximize(g, eb.OptimizerBudget(k=1)).selected == [0]
+
+
+def test_full_budget_recovers_baseline_and_full_set():
+    rng = np.random.default_rng(1)
+    f = fn(rng.random((12, 3)))
+    s = eb.greedy_maximize(f, eb.OptimizerBudget(k=12))
+    assert s.value == pytest.approx(f.baseline_loss, rel=1e-12)
+    assert sorted(s.selected) == list(range(12))
+    g = fn(rng.random((20, 4)))
+    assert g.value(list(range(20))) == g.baseline_loss
+
+
+def test_non_euclidean_distance_rejected():
+    class Manhattan(eb.Dissimilarity):
+        pass
+    with pytest.raises(ValueError, match="squared Euclidean"):
+        eb.EbcFunction(eb.GroundMatrix([[1.0]]), distance=Manhattan())
+
+
+# ------------------------------------------------------------ reference golden vectors
+
+@pytest.mark.parametrize("case", GREEDY, ids=[c["name"] for c in GREEDY])
+def test_greedy_matches_reference(case):
+    from conftest import case_data
+    f = fn(case_data(case), PREC[case["precision"]], e0=case.get("e0"))
+    assert f.baseline_loss == pytest.approx(case["baseline"], rel=1e-13)
+    s = eb.greedy_maximize(f, eb.OptimizerBudget(k=case["k"]))
+    assert s.selected == case["selected"]
+    assert s.evaluations == case["evaluations"]
+    np.testing.assert_allclose(np.cumsum(s.gains), case["values"], rtol=1e-10, atol=1e-12)
+    assert s.value == pytest.approx(case["value"], rel=1e-10)
+
+
+@pytest.mark.parametrize("case", MULTI, ids=[c["name"] for c in MULTI])
+def test_multiset_matches_reference(case):
+    from conftest import case_data
+    f = fn(case_data(case), PREC[case["precision"]], e0=case.get("e0"))
+    got = eb.evaluate_with_backend(f, eb.EvalMultiset(case_sets(case)))
+    assert max_scaled_diff(got, case["values"]) <= 1e-12
+
+
+# ------------------------------------------------------------ oracle, random instances
+
+@pytest.mark.parametrize("prec", ["fp32", "fp16-storage", "fp64"])
+def test_greedy_random_instances_vs_oracle(prec):
+    rng = np.random.default_rng({"fp32": 11, "fp16-storage": 12, "fp64": 13}[prec])
+    for _ in range(12):
+        n = int(rng.integers(2, 700))
+        d = int(rng.integers(1, 40))
+        k = int(rng.integers(1, min(12, n) + 1))
+        X = rng.standard_normal((n, d)) * rng.choice([0.1, 1.0, 30.0])
+        g = eb.GroundMatrix(X, PREC[prec])
+        f = eb.EbcFunction(g)
+        s = eb.greedy_maximize(f, eb.OptimizerBudget(k=k))
+        sel, vals, gains, evals = oracle.greedy(g.as_float64(), k)
+        assert s.selected == sel, (n, d, k)
+        assert s.evaluations == evals
+        np.testing.assert_allclose(np.cumsum(s.gains), vals, rtol=1e-10, atol=1e-12)
+
+
+def test_multiset_random_instances_vs_oracle():
+    rng = np.random.default_rng(21)
+    for prec in ("fp32", "fp16-storage", "fp64"):
+        for _ in range(6):
+            n = int(rng.integers(2, 3000))
+            d = int(rng.integers(1, 70))
+            l = int(rng.integers(1, 60))
+            X = rng.random((n, d))
+            sets = [rng.choice(n, size=int(rng.integers(0, min(12, n) + 1)), replace=False).tolist()
+                    for _ in range(l)]
+            g = eb.GroundMatrix(X, PREC[prec])
+            f = eb.EbcFunction(g)
+            got = eb.evaluate_with_backend(f, eb.EvalMultiset(sets))
+            want = oracle.eval_multiset(g.as_float64(), sets)
+            assert max_scaled_diff(got, want) <= 1e-12
+
+
+def test_duplicates_and_constant_data():
+    # exact duplicate rows -> exact ties -> lowest index; constant data -> all ties
+    rng = np.random.default_rng(5)
+    X = rng.standard_normal((500, 8)).astype(np.float32)
+    X[300] = X[17]
+    X[450] = X[17] * 3
+    X[451] = X[450]
+    f = fn(X, eb.Precision.FP32)
+    s = eb.greedy_maximize(f, eb.OptimizerBudget(k=8))
+    assert s.selected == oracle.greedy(X.astype(np.float64), 8)[0]
+    z = fn(np.zeros((60, 1)))
+    assert eb.greedy_maximize(z, eb.OptimizerBudget(k=3)).selected == [0, 1, 2]
+
+
+# ------------------------------------------------------------ determinism and sharding
+
+def test_repeatable_and_reset():
+    X = np.random.default_rng(8).standard_normal((3000, 24)).astype(np.float32)
+    f = fn(X, eb.Precision.FP32)
+    a = eb.greedy_maximize(f, eb.OptimizerBudget(k=10))
+    b = eb.greedy_maximize(f, eb.OptimizerBudget(k=10))
+    assert a.selected == b.selected and a.gains == b.gains
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_emulated_sharding_bit_identical(world):
+    """G candidate shards (one context each, all on this GPU) + the host pick
+    rule must give the single-device selection and values bit for bit."""
+    X = np.random.default_rng(9).standard_normal((2500, 20)).astype(np.float32)
+    X[2000] = X[3]
+    k = 8
+    single = eb.greedy_maximize(fn(X, eb.Precision.FP32), eb.OptimizerBudget(k=k))
+    fs = [fn(X, eb.Precision.FP32) for _ in range(world)]
+    engines = [NativeShardEngine(f, *shard_range(X.shape[0], r, world)) for r, f in enumerate(fs)]
+    sel, vals = [], []
+    for _ in range(k):
+        parts = [e.local_step() for e in engines]
+        cur = parts[0][2]
+        assert all(p[2] == cur for p in parts)
+        best, _ = pick(np.concatenate([p[0] for p in parts]), np.concatenate([p[1] for p in parts]), cur,
+                       X.shape[0])
+        newvals = [e.commit(best) for e in engines]
+        assert len(set(newvals)) == 1
+        sel.append(best)
+        vals.append(newvals[0])
+    assert sel == single.selected
+    assert vals[-1] == single.value
+    assert [b - a for a, b in zip([0.0] + vals[:-1], vals)] == single.gains
+
+
+# ------------------------------------------------------------ full BASELINE configs
+
+def _oracle_golden(name):
+    p = os.path.join(GOLDEN_DIR, f"oracle_{name}.json")
+    if not os.path.exists(p):
+        pytest.skip(f"{p} not generated yet")
+    with open(p) as fh:
+        return json.load(fh)
+
+
+@pytest.mark.parametrize("name", ["C2", "C3", "C4"])
+def test_full_config_greedy_vs_oracle(name):
+    import datasets
+    gold = _oracle_golden(name)
+    X = datasets.config_data(name)
+    prec = eb.Precision.FP16_STORAGE if X.dtype == np.float16 else eb.Precision.FP32
+    f = fn(X, prec)
+    assert f.baseline_loss == pytest.approx(gold["baseline"], rel=1e-12)
+    s = eb.greedy_maximize(f, eb.OptimizerBudget(k=gold["k"]))
+    assert s.selected == gold["selected"]
+    np.testing.assert_allclose(np.cumsum(s.gains), gold["values"], rtol=1e-10)
+    # size-independent properties: diminishing gains, gains sum to value, re-evaluation
+    assert all(s.gains[i] >= s.gains[i + 1] - 1e-9 for i in range(len(s.gains) - 1))
+    assert float(np.sum(s.gains)) == pytest.approx(s.value, rel=1e-12)
+    assert f.value(s.selected) == pytest.approx(s.value, rel=1e-12)
+
+
+def test_full_config_c5_multiset_vs_oracle():
+    import datasets
+    gold = _oracle_golden("C5")
+    X, sets = datasets.c5_problem()
+    f = fn(X, eb.Precision.FP32)
+    got = eb.evaluate_with_backend(f, eb.EvalMultiset(sets))
+    assert max_scaled_diff(got, gold["values"]) <= 1e-12
+    np.testing.assert_allclose(got, gold["values"], rtol=1e-9, atol=1e-15)
+
+
+def test_c1_config():
+    import datasets
+    X = datasets.config_data("C1")
+    f = fn(X, eb.Precision.FP32)
+    s = eb.greedy_maximize(f, eb.OptimizerBudget(k=10))
+    assert s.selected == [1507, 551, 871, 19, 1337, 1962, 229, 1110, 669, 1480]
+    assert s.value == pytest.approx(2.332765782, rel=1e-9)
+    assert s.evaluations == 19955
