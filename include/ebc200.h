@@ -100,6 +100,10 @@ int ebc_shard_commit(ebc_ctx* ctx, int64_t s, double* out_value);
 /* Reset the selection state to S = {} (cached minima back to d(., e0)). */
 int ebc_reset(ebc_ctx* ctx);
 
+/* The cudaStream_t all work of this context is issued on (for callers that
+ * record their own CUDA events around library calls). */
+void* ebc_stream(const ebc_ctx* ctx);
+
 /* Enable per-step CUDA-event timing of the kernel families (off by default). */
 int ebc_set_timing(ebc_ctx* ctx, int on);
 

@@ -38,6 +38,7 @@ SIGNATURES = {
     "ebc_shard_step": (ctypes.c_int, [_vp, _i64p, _f64p, _i64, _i64p, _f64p]),
     "ebc_shard_commit": (ctypes.c_int, [_vp, _i64, _f64p]),
     "ebc_reset": (ctypes.c_int, [_vp]),
+    "ebc_stream": (_vp, [_vp]),
     "ebc_set_timing": (ctypes.c_int, [_vp, ctypes.c_int]),
     "ebc_last_timings": (ctypes.c_int, [_vp, _f64p]),
     "ebc_last_launches": (_i64, [_vp]),

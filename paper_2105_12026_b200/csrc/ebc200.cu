@@ -120,37 +120,87 @@ int pitch_for(int d, int dtype) {
 }
 
 struct ScreenPlan {
-  int stages;
+  int shape;  // 0 = ScreenA (2-stage), 1 = ScreenA4 (4-stage), 2 = ScreenB
   size_t smem;
   int ncb;
   int ntiles;
   int tps;
   int nsplit;
+  int tp;
 };
 
-ScreenPlan plan_screen(const ebc_ctx* ctx) {
-  ScreenPlan p;
-  p.stages = 4;
-  while (p.stages > 2 && screen_smem_bytes(ctx->pitch, p.stages) > 110 * 1024) p.stages /= 2;
-  p.smem = screen_smem_bytes(ctx->pitch, p.stages);
+template <class Cfg>
+int plan_shape(const ebc_ctx* ctx, ScreenPlan& p) {
+  p.smem = Cfg::smem_bytes(ctx->pitch);
+  p.tp = Cfg::TP;
   const int64_t ncand = ctx->c1 - ctx->c0;
-  p.ncb = (int)((ncand + screen::CT_ - 1) / screen::CT_);
-  p.ntiles = (int)((ctx->n + screen::PT_ - 1) / screen::PT_);
-  const int64_t target = 8LL * ctx->num_sms;  // >= 4 waves at 2 CTAs/SM
-  int want = (int)std::min<int64_t>(p.ntiles, std::max<int64_t>(1, (target + p.ncb - 1) / std::max(1, p.ncb)));
-  p.tps = (p.ntiles + want - 1) / want;
+  p.ncb = (int)((ncand + Cfg::CT - 1) / Cfg::CT);
+  p.ntiles = (int)((ctx->n + Cfg::PT - 1) / Cfg::PT);
+  // choose the V split that minimises (waves x tiles per CTA), with one tile
+  // of fixed cost per CTA (candidate-tile load, epilogue): wave quantisation
+  // otherwise costs up to ~1/waves of the step
+  int per_sm = (int)std::min<size_t>(Cfg::MINB, (227 * 1024) / (p.smem + 1024));
+  if (per_sm < 1) per_sm = 1;
+  const int64_t slots = (int64_t)per_sm * ctx->num_sms;
+  double best_cost = 1e300;
+  p.tps = p.ntiles;
+  for (int s = 1; s <= 64 && s <= p.ntiles; ++s) {
+    const int tps = (p.ntiles + s - 1) / s;
+    const int ns = (p.ntiles + tps - 1) / tps;
+    const int64_t ctas = (int64_t)p.ncb * ns;
+    const double waves = (double)((ctas + slots - 1) / slots);
+    const double cost = waves * (tps + 1.0);
+    if (cost < best_cost * 0.999) {
+      best_cost = cost;
+      p.tps = tps;
+    }
+  }
   p.nsplit = (p.ntiles + p.tps - 1) / p.tps;
-  return p;
+  return p.smem <= 227 * 1024 ? EBC_OK : EBC_EINVAL;
 }
 
-template <int ST>
+int screen_shape_choice(const ebc_ctx* ctx) {
+  const char* env = getenv("EBC200_SCREEN");
+  if (env && env[0]) return atoi(env);
+  (void)ctx;
+  return 2;
+}
+
+int plan_screen(const ebc_ctx* ctx, ScreenPlan& p) {
+  p.shape = screen_shape_choice(ctx);
+  int rc;
+  if (p.shape == 2) {
+    rc = plan_shape<ScreenB>(ctx, p);
+    if (rc == EBC_OK) return rc;
+    p.shape = 0;
+  }
+  if (p.shape == 1) {
+    rc = plan_shape<ScreenA4>(ctx, p);
+    if (rc == EBC_OK && p.smem <= 110 * 1024) return rc;
+    p.shape = 0;
+  }
+  return plan_shape<ScreenA>(ctx, p);
+}
+
+template <class Cfg>
 int launch_screen_t(ebc_ctx* ctx, const ScreenPlan& p) {
-  auto kern = k_screen<ST>;
+  auto kern = k_screen<Cfg>;
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
   dim3 grid(p.ncb, p.nsplit);
-  kern<<<grid, screen::THREADS, p.smem, ctx->stream>>>(
-      ctx->V32, ctx->pt, ctx->pitch, ctx->d4, ctx->c0, p.ntiles, p.tps, (double*)ctx->part_g.p,
-      (float*)ctx->part_e.p, ctx->n_pad);
+  kern<<<grid, Cfg::THREADS, p.smem, ctx->stream>>>(ctx->V32, ctx->pt, ctx->pitch, ctx->d4, ctx->c0, p.ntiles, p.tps,
+                                                    (double*)ctx->part_g.p, (float*)ctx->part_e.p, ctx->n_pad);
+  KCHECK();
+  return EBC_OK;
+}
+
+// FP64 grounds, or a d too large for any screen tile: every unselected
+// candidate goes straight to the exact fp64 refine.
+int run_window_all(ebc_ctx* ctx, int eb, int fin_blocks) {
+  if (ctx->timing) {
+    CU(cudaEventRecord(ctx->ev[eb + 0], ctx->stream));
+    CU(cudaEventRecord(ctx->ev[eb + 1], ctx->stream));
+  }
+  k_window_all<<<fin_blocks, 256, 0, ctx->stream>>>(ctx->c0, ctx->c1, ctx->selected, ctx->wcount, ctx->wlist);
   KCHECK();
   return EBC_OK;
 }
@@ -158,30 +208,38 @@ int launch_screen_t(ebc_ctx* ctx, const ScreenPlan& p) {
 // One step's candidate screen + certified window + exact refine + pick.
 // commit: single-device mode (mark the winner, record it as step `step`).
 int run_step_select(ebc_ctx* ctx, int step, int commit, int64_t* sel_dev) {
+  const int eb = 4 * step;  // event slot of this step
   const int64_t ncand = ctx->c1 - ctx->c0;
   CU(cudaMemsetAsync(ctx->wcount, 0, sizeof(int), ctx->stream));
   const int fin_blocks = (int)((ncand + 255) / 256);
   if (ctx->dtype != EBC_F64) {
-    ScreenPlan p = plan_screen(ctx);
-    int rc = ensure(ctx, ctx->part_g, (size_t)p.nsplit * ctx->n_pad * sizeof(double));
+    ScreenPlan p;
+    int rc = plan_screen(ctx, p);
+    if (rc) return run_window_all(ctx, eb, fin_blocks);
+    rc = ensure(ctx, ctx->part_g, (size_t)p.nsplit * ctx->n_pad * sizeof(double));
     if (rc) return rc;
     rc = ensure(ctx, ctx->part_e, (size_t)p.nsplit * ctx->n_pad * sizeof(float));
     if (rc) return rc;
-    if (ctx->timing) CU(cudaEventRecord(ctx->ev[0], ctx->stream));
-    if (p.stages == 4)
-      rc = launch_screen_t<4>(ctx, p);
+    if (ctx->timing) CU(cudaEventRecord(ctx->ev[eb + 0], ctx->stream));
+    if (p.shape == 2)
+      rc = launch_screen_t<ScreenB>(ctx, p);
+    else if (p.shape == 1)
+      rc = launch_screen_t<ScreenA4>(ctx, p);
     else
-      rc = launch_screen_t<2>(ctx, p);
+      rc = launch_screen_t<ScreenA>(ctx, p);
     if (rc) return rc;
-    if (ctx->timing) CU(cudaEventRecord(ctx->ev[1], ctx->stream));
+    if (ctx->timing) CU(cudaEventRecord(ctx->ev[eb + 1], ctx->stream));
     // lower bounds are clamped at 0 (every gain is a sum of max(0, .) terms), so
     // key 0 (= +0.0) is a valid neutral element for the max
     CU(cudaMemsetAsync(ctx->maxlb, 0, sizeof(long long), ctx->stream));
     // per-thread fp32 error accumulators see at most tps*TP terms: inflate
-    const double nterms = (double)p.tps * screen::TP * 8 * 2 + 64.0;
-    const double einfl = 1.0 + 2.0 * nterms * 5.960464477539063e-08 + 1.0 / 64.0;
+    const double u = 5.960464477539063e-08;
+    const double nterms = (double)p.tps * p.tp * 8 * 2 + 64.0;
+    const double einfl = 1.0 + 2.0 * nterms * u + 1.0 / 64.0;
+    // fp32 tile sums: TP sequential adds + 3 butterfly levels, then fp64
+    const double gcoef = (p.tp + 8) * u;
     k_finalize<<<fin_blocks, 256, 0, ctx->stream>>>(ctx->c0, ctx->c1, p.nsplit, (double*)ctx->part_g.p,
-                                                   (float*)ctx->part_e.p, ctx->n_pad, einfl, ctx->selected,
+                                                   (float*)ctx->part_e.p, ctx->n_pad, einfl, gcoef, ctx->selected,
                                                    ctx->ub, ctx->maxlb);
     KCHECK();
     const double margin = (double)ctx->n * 1e-12 * std::max(1.0, std::fabs(ctx->baseline)) * 1.01;
@@ -189,39 +247,37 @@ int run_step_select(ebc_ctx* ctx, int step, int commit, int64_t* sel_dev) {
                                                  ctx->wlist);
     KCHECK();
   } else {
-    if (ctx->timing) {
-      CU(cudaEventRecord(ctx->ev[0], ctx->stream));
-      CU(cudaEventRecord(ctx->ev[1], ctx->stream));
-    }
-    k_window_all<<<fin_blocks, 256, 0, ctx->stream>>>(ctx->c0, ctx->c1, ctx->selected, ctx->wcount, ctx->wlist);
-    KCHECK();
+    int rc = run_window_all(ctx, eb, fin_blocks);
+    if (rc) return rc;
   }
   // exact fp64 gains of the window
-  int rc = ensure(ctx, ctx->part_r, (size_t)ctx->n * ctx->nchunks * sizeof(double));
+  const int ng = std::min(ctx->nchunks, 32);
+  int rc = ensure(ctx, ctx->part_r, (size_t)ctx->n * ng * sizeof(double));
   if (rc) return rc;
   const int rgrid = 4 * ctx->num_sms;
   const size_t rsmem = (size_t)ctx->d * sizeof(double);
   if (ctx->dtype == EBC_F64) {
     CU(cudaFuncSetAttribute(k_refine<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem + 1024));
     k_refine<double><<<rgrid, RED_THREADS, rsmem, ctx->stream>>>(ctx->V64, ctx->pitch, ctx->n, ctx->d, ctx->cm64,
-                                                               ctx->wcount, ctx->wlist, ctx->nchunks,
+                                                               ctx->wcount, ctx->wlist, ctx->nchunks, ng,
                                                                (double*)ctx->part_r.p);
   } else {
     CU(cudaFuncSetAttribute(k_refine<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem + 1024));
     k_refine<float><<<rgrid, RED_THREADS, rsmem, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->n, ctx->d, ctx->cm64,
-                                                              ctx->wcount, ctx->wlist, ctx->nchunks,
+                                                              ctx->wcount, ctx->wlist, ctx->nchunks, ng,
                                                               (double*)ctx->part_r.p);
   }
   KCHECK();
-  k_pick<<<1, 1024, 0, ctx->stream>>>(ctx->wcount, ctx->wlist, ctx->nchunks, (double*)ctx->part_r.p,
+  k_pick<<<1, 1024, 0, ctx->stream>>>(ctx->wcount, ctx->wlist, ng, (double*)ctx->part_r.p,
                                       1.0 / (double)ctx->n, ctx->cur, ctx->wgain, ctx->best, commit, step,
                                       ctx->selected, sel_dev);
   KCHECK();
-  if (ctx->timing) CU(cudaEventRecord(ctx->ev[2], ctx->stream));
+  if (ctx->timing) CU(cudaEventRecord(ctx->ev[eb + 2], ctx->stream));
   return EBC_OK;
 }
 
 int run_update(ebc_ctx* ctx, int step, double* val_dev, double* gain_dev) {
+  const int eb = 4 * step;
   const size_t smem = (size_t)ctx->d * sizeof(double);
   if (ctx->dtype == EBC_F64) {
     CU(cudaFuncSetAttribute(k_update<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024));
@@ -235,7 +291,16 @@ int run_update(ebc_ctx* ctx, int step, double* val_dev, double* gain_dev) {
         ctx->counter, 1.0 / (double)ctx->n, ctx->cur, val_dev, gain_dev, step);
   }
   KCHECK();
-  if (ctx->timing) CU(cudaEventRecord(ctx->ev[3], ctx->stream));
+  if (ctx->timing) CU(cudaEventRecord(ctx->ev[eb + 3], ctx->stream));
+  return EBC_OK;
+}
+
+int ensure_events(ebc_ctx* ctx, size_t count) {
+  while (ctx->ev.size() < count) {
+    cudaEvent_t e;
+    CU(cudaEventCreate(&e));
+    ctx->ev.push_back(e);
+  }
   return EBC_OK;
 }
 
@@ -421,6 +486,8 @@ int ebc_reset(ebc_ctx* ctx) {
   return EBC_OK;
 }
 
+void* ebc_stream(const ebc_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
 int ebc_set_timing(ebc_ctx* ctx, int on) {
   if (!ctx) return fail(nullptr, EBC_EINVAL, "ebc_set_timing: NULL context");
   ctx->timing = on != 0;
@@ -451,6 +518,10 @@ int ebc_greedy(ebc_ctx* ctx, int32_t k, int64_t* out_sel, double* out_val, doubl
   if (rc) return rc;
   rc = do_reset(ctx);
   if (rc) return rc;
+  if (ctx->timing) {
+    rc = ensure_events(ctx, 4 * k);
+    if (rc) return rc;
+  }
   double acc_ms[4] = {0, 0, 0, 0};
   cudaEvent_t tstart = nullptr, tend = nullptr;
   CU(cudaEventCreate(&tstart));
@@ -461,22 +532,23 @@ int ebc_greedy(ebc_ctx* ctx, int32_t k, int64_t* out_sel, double* out_val, doubl
     if (rc) return rc;
     rc = run_update(ctx, s, (double*)ctx->val_out.p, (double*)ctx->gain_out.p);
     if (rc) return rc;
-    if (ctx->timing) {
-      CU(cudaEventSynchronize(ctx->ev[3]));
-      float a = 0, b = 0, c = 0;
-      CU(cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]));
-      CU(cudaEventElapsedTime(&b, ctx->ev[1], ctx->ev[2]));
-      CU(cudaEventElapsedTime(&c, ctx->ev[2], ctx->ev[3]));
-      acc_ms[0] += a;
-      acc_ms[1] += b;
-      acc_ms[2] += c;
-    }
   }
   CU(cudaEventRecord(tend, ctx->stream));
   CU(cudaMemcpyAsync(out_sel, ctx->sel_out.p, (size_t)k * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaMemcpyAsync(out_val, ctx->val_out.p, (size_t)k * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaMemcpyAsync(out_gain, ctx->gain_out.p, (size_t)k * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
+  if (ctx->timing) {
+    for (int st = 0; st < k; ++st) {
+      float a = 0, b = 0, c = 0;
+      CU(cudaEventElapsedTime(&a, ctx->ev[4 * st + 0], ctx->ev[4 * st + 1]));
+      CU(cudaEventElapsedTime(&b, ctx->ev[4 * st + 1], ctx->ev[4 * st + 2]));
+      CU(cudaEventElapsedTime(&c, ctx->ev[4 * st + 2], ctx->ev[4 * st + 3]));
+      acc_ms[0] += a;
+      acc_ms[1] += b;
+      acc_ms[2] += c;
+    }
+  }
   float tot = 0;
   CU(cudaEventElapsedTime(&tot, tstart, tend));
   cudaEventDestroy(tstart);

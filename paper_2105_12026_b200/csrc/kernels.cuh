@@ -154,19 +154,60 @@ __global__ void k_total(const double* __restrict__ part, int nchunks, double sca
 // Per pair the accumulator starts at -cm32[v], so after the d-dim FADD/FFMA
 // chain it holds s = d32 - cm32 directly:  gain += max(-s, 0),
 // err += (s < tau[v]) ? tau[v] : 0  with tau = 2(d+8)u*cm32.
-namespace screen {
-constexpr int TP = 4, TC = 8, LR = 8, LC = 4, WP = 2, WC = 4;
-constexpr int THREADS = 32 * WP * WC;
-constexpr int PT_ = WP * LR * TP;  // 64 points per V tile
-constexpr int CT_ = WC * LC * TC;  // 128 candidates per CTA
-}  // namespace screen
+// Tile geometry.  TC is fixed at 8 (the transposed butterfly below hands lane
+// r the tile sum of candidate r); TP (points per thread), the warp grid and the
+// ring depth are template parameters so several shapes can be instantiated.
+template <int TP_, int WP_, int WC_, int STAGES_, int MINB_>
+struct ScreenCfg {
+  static constexpr int TP = TP_, TC = 8, LR = 8, LC = 4, WP = WP_, WC = WC_;
+  static constexpr int STAGES = STAGES_, MINB = MINB_;
+  static constexpr int NWARPS = WP * WC;
+  static constexpr int THREADS = 32 * NWARPS;
+  static constexpr int PT = WP * LR * TP;  // points per V tile
+  static constexpr int CT = WC * LC * TC;  // candidates per CTA
+  static size_t smem_bytes(int pitch) {
+    size_t cand = (size_t)CT * pitch * sizeof(float);
+    size_t stage = (size_t)PT * pitch * sizeof(float) + (size_t)PT * sizeof(float2);
+    size_t ring = STAGES * stage;
+    size_t red = (size_t)WP * CT * (sizeof(double) + sizeof(float));
+    if (ring < red) ring = red;
+    return cand + ring + (STAGES + 1) * sizeof(uint64_t) + STAGES * sizeof(int) + 16;
+  }
+};
 
-template <int STAGES>
-__global__ void __launch_bounds__(screen::THREADS, 2)
+// Transposed butterfly over the 8 lane-rows (lane bits 0..2): on return lane r
+// holds sum over the 8 rows of x[r].  Fixed order -> deterministic.
+__device__ __forceinline__ float rowsum8_transposed(const float (&x)[8], int r) {
+  float h[4];
+  const bool up4 = (r & 4) != 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    float send = up4 ? x[j] : x[j + 4];
+    float keep = up4 ? x[j + 4] : x[j];
+    h[j] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  float h2[2];
+  const bool up2 = (r & 2) != 0;
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    float send = up2 ? h[j] : h[j + 2];
+    float keep = up2 ? h[j + 2] : h[j];
+    h2[j] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+  }
+  const bool up1 = (r & 1) != 0;
+  float send = up1 ? h2[0] : h2[1];
+  float keep = up1 ? h2[1] : h2[0];
+  return keep + __shfl_xor_sync(0xffffffffu, send, 1);
+}
+
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
     k_screen(const float* __restrict__ V, const float2* __restrict__ pt, int pitch, int d4, int64_t cand0,
              int ntiles, int tiles_per_split, double* __restrict__ part_g, float* __restrict__ part_e,
              int64_t part_stride) {
-  using namespace screen;
+  constexpr int TP = Cfg::TP, TC = Cfg::TC, LR = Cfg::LR, LC = Cfg::LC, WP = Cfg::WP;
+  constexpr int STAGES = Cfg::STAGES, NWARPS = Cfg::NWARPS, THREADS = Cfg::THREADS;
+  constexpr int PT_ = Cfg::PT, CT_ = Cfg::CT;
   extern __shared__ __align__(128) unsigned char smem[];
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -179,10 +220,12 @@ __global__ void __launch_bounds__(screen::THREADS, 2)
   float* cs = reinterpret_cast<float*>(smem);
   unsigned char* stage_base = smem + cand_bytes;
   const size_t stage_bytes = vt_bytes + pt_bytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(stage_base + STAGES * stage_bytes);
-  uint64_t* full = bars;
-  uint64_t* empty = bars + STAGES;
-  uint64_t* cbar = bars + 2 * STAGES;
+  size_t ring_bytes = STAGES * stage_bytes;
+  const size_t red_bytes = (size_t)WP * CT_ * (sizeof(double) + sizeof(float));
+  if (ring_bytes < red_bytes) ring_bytes = red_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage_base + ring_bytes);
+  uint64_t* cbar = full + STAGES;
+  int* relcnt = reinterpret_cast<int*>(cbar + 1);
 
   const int t0 = blockIdx.y * tiles_per_split;
   const int t1 = min(ntiles, t0 + tiles_per_split);
@@ -192,7 +235,7 @@ __global__ void __launch_bounds__(screen::THREADS, 2)
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], WP * WC);
+      relcnt[s] = 0;
     }
     mbar_init(cbar, 1);
     fence_mbar_init();
@@ -220,6 +263,19 @@ __global__ void __launch_bounds__(screen::THREADS, 2)
   for (int j = 0; j < TC; ++j) crow_s[j] = cs + (wc * (LC * TC) + q + LC * j) * pitch;
 
   mbar_wait(cbar, 0);
+  // Swap adjacent dims of the resident candidate tile: an LDS.128 lands vector
+  // component j in a register of parity j%2, so pairing v_k (even register)
+  // with c_k now stored in the odd slot makes every FADD read one even and one
+  // odd register -- no register-bank conflict (ncu: dispatch stalls).
+  {
+    float2* c2 = reinterpret_cast<float2*>(cs);
+    const int total2 = CT_ * pitch / 2;
+    for (int i = tid; i < total2; i += THREADS) {
+      const float2 x = c2[i];
+      c2[i] = make_float2(x.y, x.x);
+    }
+  }
+  __syncthreads();
 
   for (int it = 0; it < nt; ++it) {
     const int s = it % STAGES;
@@ -240,6 +296,7 @@ __global__ void __launch_bounds__(screen::THREADS, 2)
 #pragma unroll
       for (int j = 0; j < TC; ++j) acc[i][j] = pp.x;
     }
+#pragma unroll(TP >= 8 ? 1 : 2)
     for (int k4 = 0; k4 < d4; ++k4) {
       float4 a[TP], b[TC];
 #pragma unroll
@@ -251,90 +308,53 @@ __global__ void __launch_bounds__(screen::THREADS, 2)
 #pragma unroll
         for (int j = 0; j < TC; ++j) {
           float t;
-          t = a[i].x - b[j].x; acc[i][j] = fmaf(t, t, acc[i][j]);
-          t = a[i].y - b[j].y; acc[i][j] = fmaf(t, t, acc[i][j]);
-          t = a[i].z - b[j].z; acc[i][j] = fmaf(t, t, acc[i][j]);
-          t = a[i].w - b[j].w; acc[i][j] = fmaf(t, t, acc[i][j]);
+          // b holds (c_{k+1}, c_k, c_{k+3}, c_{k+2}) -- see the swap above
+          t = a[i].x - b[j].y; acc[i][j] = fmaf(t, t, acc[i][j]);
+          t = a[i].y - b[j].x; acc[i][j] = fmaf(t, t, acc[i][j]);
+          t = a[i].z - b[j].w; acc[i][j] = fmaf(t, t, acc[i][j]);
+          t = a[i].w - b[j].z; acc[i][j] = fmaf(t, t, acc[i][j]);
         }
       }
     }
-    // stage consumed: release it to the producer
+    // Stage consumed (every LDS result has been used).  The last warp to
+    // release it refills it with tile it + STAGES: no warp ever waits for
+    // another warp's progress (ncu: long-scoreboard stalls on the ring).
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
+    if (lane == 0) {
+      __threadfence_block();
+      const int old = atomicAdd(&relcnt[s], 1);
+      if (old == NWARPS - 1) {
+        relcnt[s] = 0;
+        if (it + STAGES < nt) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          unsigned char* st = stage_base + s * stage_bytes;
+          const int64_t prow = (int64_t)(t0 + it + STAGES) * PT_;
+          mbar_arrive_expect_tx(&full[s], (uint32_t)stage_bytes);
+          bulk_g2s(st, V + prow * pitch, (uint32_t)vt_bytes, &full[s]);
+          bulk_g2s(st + vt_bytes, pt + prow, (uint32_t)pt_bytes, &full[s]);
+        }
+      }
+    }
+    __syncwarp();
 
-    // epilogue: s = d32 - cm32
+    // epilogue: sv = d32 - cm32
 #pragma unroll
     for (int i = 0; i < TP; ++i) {
 #pragma unroll
       for (int j = 0; j < TC; ++j) {
         const float sv = acc[i][j];
         g[j] += fmaxf(-sv, 0.f);
-        e[j] += sv < tau[i] ? tau[i] : 0.f;
+        e[j] = fmaf(sv < tau[i] ? 1.f : 0.f, tau[i], e[j]);
       }
     }
-    // fold this tile's fp32 gains into fp64: transposed butterfly over the 8
-    // lane-rows leaves lane r holding the warp's tile sum of candidate j = r.
-    {
-      float h[4];
-      const bool up4 = (r & 4) != 0;
+    // fold this tile's fp32 gains into fp64 (lane r: candidate j = r)
+    g64 += (double)rowsum8_transposed(g, r);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        float send = up4 ? g[j] : g[j + 4];
-        float keep = up4 ? g[j + 4] : g[j];
-        h[j] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-      }
-      float h2[2];
-      const bool up2 = (r & 2) != 0;
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        float send = up2 ? h[j] : h[j + 2];
-        float keep = up2 ? h[j + 2] : h[j];
-        h2[j] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
-      }
-      const bool up1 = (r & 1) != 0;
-      float send = up1 ? h2[0] : h2[1];
-      float keep = up1 ? h2[1] : h2[0];
-      float tot = keep + __shfl_xor_sync(0xffffffffu, send, 1);
-      g64 += (double)tot;
-#pragma unroll
-      for (int j = 0; j < TC; ++j) g[j] = 0.f;
-    }
-
-    // producer: refill this stage with tile it + STAGES once every warp released it
-    if (tid == 0 && it + STAGES < nt) {
-      mbar_wait(&empty[s], ph);
-      unsigned char* st = stage_base + s * stage_bytes;
-      const int64_t prow = (int64_t)(t0 + it + STAGES) * PT_;
-      mbar_arrive_expect_tx(&full[s], (uint32_t)stage_bytes);
-      bulk_g2s(st, V + prow * pitch, (uint32_t)vt_bytes, &full[s]);
-      bulk_g2s(st + vt_bytes, pt + prow, (uint32_t)pt_bytes, &full[s]);
-    }
+    for (int j = 0; j < TC; ++j) g[j] = 0.f;
   }
 
   // error bound: same transposed reduce in fp32 (covered by the inflation factor)
-  float etot;
-  {
-    float h[4];
-    const bool up4 = (r & 4) != 0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      float send = up4 ? e[j] : e[j + 4];
-      float keep = up4 ? e[j + 4] : e[j];
-      h[j] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-    }
-    float h2[2];
-    const bool up2 = (r & 2) != 0;
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      float send = up2 ? h[j] : h[j + 2];
-      float keep = up2 ? h[j + 2] : h[j];
-      h2[j] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
-    }
-    const bool up1 = (r & 1) != 0;
-    float send = up1 ? h2[0] : h2[1];
-    float keep = up1 ? h2[1] : h2[0];
-    etot = keep + __shfl_xor_sync(0xffffffffu, send, 1);
-  }
+  const float etot = rowsum8_transposed(e, r);
   // lane (r, q) of warp (wp, wc) now holds candidate  wc*32 + q + 4*r
   __syncthreads();  // all stages idle: reuse the ring for the cross-warp combine
   double* rg = reinterpret_cast<double*>(stage_base);
@@ -357,22 +377,19 @@ __global__ void __launch_bounds__(screen::THREADS, 2)
   }
 }
 
-inline size_t screen_smem_bytes(int pitch, int stages) {
-  using namespace screen;
-  size_t cand = (size_t)CT_ * pitch * sizeof(float);
-  size_t stage = (size_t)PT_ * pitch * sizeof(float) + (size_t)PT_ * sizeof(float2);
-  size_t ring = stages * stage;
-  size_t red = (size_t)WP * CT_ * (sizeof(double) + sizeof(float));
-  if (ring < red) ring = red;
-  return cand + ring + (2 * stages + 1) * sizeof(uint64_t);
-}
+// Instantiated shapes (selected at run time, EBC200_SCREEN overrides):
+//   A: 4x8 per thread, 2 CTAs/SM, 64 pts x 128 cands, 2-stage ring
+//   B: 8x8 per thread, 1 CTA/SM, 128 pts x 128 cands, 3-stage ring
+using ScreenA = ScreenCfg<4, 2, 4, 2, 2>;
+using ScreenA4 = ScreenCfg<4, 2, 4, 4, 2>;
+using ScreenB = ScreenCfg<8, 2, 4, 3, 1>;
 
 // ---------------------------------------------------------------- K3: window + refine + pick
 
 // Combine the split partials, form the certified interval [lb, ub] and fold the
 // block's largest lower bound into *maxlb (order-independent atomicMax).
 __global__ void k_finalize(int64_t c0, int64_t c1, int nsplit, const double* __restrict__ part_g,
-                           const float* __restrict__ part_e, int64_t part_stride, double einfl,
+                           const float* __restrict__ part_e, int64_t part_stride, double einfl, double gcoef,
                            const unsigned char* __restrict__ selected, double* __restrict__ ub,
                            long long* __restrict__ maxlb) {
   __shared__ long long smax[256];
@@ -384,7 +401,7 @@ __global__ void k_finalize(int64_t c0, int64_t c1, int nsplit, const double* __r
       g += part_g[s * part_stride + c];
       e += (double)part_e[s * part_stride + c];
     }
-    const double eps = e * einfl + 4.8e-7 * g + 1e-300;  // 8u * g
+    const double eps = e * einfl + gcoef * g + 1e-300;
     if (selected[c]) {
       ub[c - c0] = -INFINITY;
     } else {
@@ -426,34 +443,40 @@ __global__ void k_window_all(int64_t c0, int64_t c1, const unsigned char* __rest
   }
 }
 
-// Exact fp64 gain partials: part_r[w*nchunks + ch] = sum over chunk ch of
-// max(0, cm64[v] - d64(v, c_w)).  Persistent grid over (w, chunk) units.
+// Exact fp64 gain partials.  The nchunks point chunks are cut into ng fixed
+// groups (ng depends only on n); unit (w, grp) sums its chunks' fixed-tree
+// partials left to right into part_r[w*ng + grp].  Persistent grid over units.
 template <typename T>
 __global__ void __launch_bounds__(RED_THREADS) k_refine(const T* __restrict__ V, int pitch, int64_t n, int d,
                                                         const double* __restrict__ cm64,
                                                         const int* __restrict__ wcount,
-                                                        const int64_t* __restrict__ wlist, int nchunks,
+                                                        const int64_t* __restrict__ wlist, int nchunks, int ng,
                                                         double* __restrict__ part_r) {
   extern __shared__ double cd[];  // d doubles
   __shared__ double sbuf[RED_THREADS];
-  const int64_t units = (int64_t)(*wcount) * nchunks;
+  const int cpg = (nchunks + ng - 1) / ng;
+  const int64_t units = (int64_t)(*wcount) * ng;
   for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
-    const int64_t w = u / nchunks;
-    const int ch = (int)(u - w * nchunks);
+    const int64_t w = u / ng;
+    const int grp = (int)(u - w * ng);
     const int64_t c = wlist[w];
     __syncthreads();
     for (int k = threadIdx.x; k < d; k += blockDim.x) cd[k] = (double)V[c * pitch + k];
     __syncthreads();
-    double acc = 0.0;
-    for (int i = 0; i < RCH / RED_THREADS; ++i) {
-      const int64_t v = (int64_t)ch * RCH + threadIdx.x + (int64_t)i * RED_THREADS;
-      if (v < n) {
-        const double t = cm64[v] - dist64_row(V + v * pitch, cd, d);
-        acc += t > 0.0 ? t : 0.0;
+    double total = 0.0;
+    const int ch1 = min(nchunks, (grp + 1) * cpg);
+    for (int ch = grp * cpg; ch < ch1; ++ch) {
+      double acc = 0.0;
+      for (int i = 0; i < RCH / RED_THREADS; ++i) {
+        const int64_t v = (int64_t)ch * RCH + threadIdx.x + (int64_t)i * RED_THREADS;
+        if (v < n) {
+          const double t = cm64[v] - dist64_row(V + v * pitch, cd, d);
+          acc += t > 0.0 ? t : 0.0;
+        }
       }
+      total += block_sum_256(acc, sbuf);  // identical in every thread
     }
-    const double s = block_sum_256(acc, sbuf);
-    if (threadIdx.x == 0) part_r[u] = s;
+    if (threadIdx.x == 0) part_r[u] = total;
   }
 }
 
@@ -462,7 +485,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_refine(const T* __restrict__ V,
 //   value >= top - window; value = f(S) + gain/N.
 // commit != 0: mark the winner selected and record it as step `step`.
 __global__ void __launch_bounds__(1024) k_pick(const int* __restrict__ wcount, const int64_t* __restrict__ wlist,
-                                               int nchunks, const double* __restrict__ part_r, double inv_n,
+                                               int ng, const double* __restrict__ part_r, double inv_n,
                                                const double* __restrict__ cur, double* __restrict__ wgain,
                                                int64_t* __restrict__ best, int commit, int step,
                                                unsigned char* __restrict__ selected, int64_t* __restrict__ sel_out) {
@@ -472,7 +495,7 @@ __global__ void __launch_bounds__(1024) k_pick(const int* __restrict__ wcount, c
   const double f = *cur;
   double top = -INFINITY;
   for (int w = threadIdx.x; w < wc; w += blockDim.x) {
-    const double gsum = chunk_total(part_r + (int64_t)w * nchunks, nchunks);
+    const double gsum = chunk_total(part_r + (int64_t)w * ng, ng);
     wgain[w] = gsum;
     const double val = __dadd_rn(f, __dmul_rn(gsum, inv_n));  // no FMA contraction: host pick() matches
     top = fmax(top, val);

@@ -232,3 +232,17 @@ def test_c1_config():
     assert s.selected == [1507, 551, 871, 19, 1337, 1962, 229, 1110, 669, 1480]
     assert s.value == pytest.approx(2.332765782, rel=1e-9)
     assert s.evaluations == 19955
+
+
+@pytest.mark.parametrize("d", [3, 97, 150, 200, 700, 3524])
+def test_wide_and_odd_dims_vs_oracle(d):
+    """Every screen tile shape and the refine-all fallback (d too wide for any
+    shared-memory tile, e.g. the paper's case study d=3524)."""
+    rng = np.random.default_rng(d)
+    n = 1000 if d > 1000 else 1500
+    X = rng.standard_normal((n, d)).astype(np.float32)
+    f = fn(X, eb.Precision.FP32)
+    s = eb.greedy_maximize(f, eb.OptimizerBudget(k=5))
+    sel, vals, _, _ = oracle.greedy(X.astype(np.float64), 5)
+    assert s.selected == sel
+    np.testing.assert_allclose(np.cumsum(s.gains), vals, rtol=1e-10)
