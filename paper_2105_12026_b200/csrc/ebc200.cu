@@ -205,6 +205,45 @@ int run_window_all(ebc_ctx* ctx, int eb, int fin_blocks) {
   return EBC_OK;
 }
 
+// fp32 screen of the candidate range + certified window.
+// Returns EBC_EINVAL (nothing launched) when no screen tile fits this d.
+int run_screen_window(ebc_ctx* ctx, int eb, int fin_blocks) {
+  ScreenPlan p;
+  int rc = plan_screen(ctx, p);
+  if (rc) return rc;
+  rc = ensure(ctx, ctx->part_g, (size_t)p.nsplit * ctx->n_pad * sizeof(double));
+  if (rc) return rc;
+  rc = ensure(ctx, ctx->part_e, (size_t)p.nsplit * ctx->n_pad * sizeof(float));
+  if (rc) return rc;
+  if (ctx->timing) CU(cudaEventRecord(ctx->ev[eb + 0], ctx->stream));
+  if (p.shape == 2)
+    rc = launch_screen_t<ScreenB>(ctx, p);
+  else if (p.shape == 1)
+    rc = launch_screen_t<ScreenA4>(ctx, p);
+  else
+    rc = launch_screen_t<ScreenA>(ctx, p);
+  if (rc) return rc;
+  if (ctx->timing) CU(cudaEventRecord(ctx->ev[eb + 1], ctx->stream));
+  // lower bounds are clamped at 0 (every gain is a sum of max(0, .) terms), so
+  // key 0 (= +0.0) is a valid neutral element for the max
+  CU(cudaMemsetAsync(ctx->maxlb, 0, sizeof(long long), ctx->stream));
+  // per-thread fp32 error accumulators see at most tps*TP terms: inflate
+  const double u = 5.960464477539063e-08;
+  const double nterms = (double)p.tps * p.tp * 8 * 2 + 64.0;
+  const double einfl = 1.0 + 2.0 * nterms * u + 1.0 / 64.0;
+  // fp32 tile sums: TP sequential adds + 3 butterfly levels, then fp64
+  const double gcoef = (p.tp + 8) * u;
+  k_finalize<<<fin_blocks, 256, 0, ctx->stream>>>(ctx->c0, ctx->c1, p.nsplit, (double*)ctx->part_g.p,
+                                                 (float*)ctx->part_e.p, ctx->n_pad, einfl, gcoef, ctx->selected,
+                                                 ctx->ub, ctx->maxlb);
+  KCHECK();
+  const double margin = (double)ctx->n * 1e-12 * std::max(1.0, std::fabs(ctx->baseline)) * 1.01;
+  k_window<<<fin_blocks, 256, 0, ctx->stream>>>(ctx->c0, ctx->c1, ctx->ub, ctx->maxlb, margin, ctx->wcount,
+                                               ctx->wlist);
+  KCHECK();
+  return EBC_OK;
+}
+
 // One step's candidate screen + certified window + exact refine + pick.
 // commit: single-device mode (mark the winner, record it as step `step`).
 int run_step_select(ebc_ctx* ctx, int step, int commit, int64_t* sel_dev) {
@@ -212,47 +251,12 @@ int run_step_select(ebc_ctx* ctx, int step, int commit, int64_t* sel_dev) {
   const int64_t ncand = ctx->c1 - ctx->c0;
   CU(cudaMemsetAsync(ctx->wcount, 0, sizeof(int), ctx->stream));
   const int fin_blocks = (int)((ncand + 255) / 256);
-  if (ctx->dtype != EBC_F64) {
-    ScreenPlan p;
-    int rc = plan_screen(ctx, p);
-    if (rc) return run_window_all(ctx, eb, fin_blocks);
-    rc = ensure(ctx, ctx->part_g, (size_t)p.nsplit * ctx->n_pad * sizeof(double));
-    if (rc) return rc;
-    rc = ensure(ctx, ctx->part_e, (size_t)p.nsplit * ctx->n_pad * sizeof(float));
-    if (rc) return rc;
-    if (ctx->timing) CU(cudaEventRecord(ctx->ev[eb + 0], ctx->stream));
-    if (p.shape == 2)
-      rc = launch_screen_t<ScreenB>(ctx, p);
-    else if (p.shape == 1)
-      rc = launch_screen_t<ScreenA4>(ctx, p);
-    else
-      rc = launch_screen_t<ScreenA>(ctx, p);
-    if (rc) return rc;
-    if (ctx->timing) CU(cudaEventRecord(ctx->ev[eb + 1], ctx->stream));
-    // lower bounds are clamped at 0 (every gain is a sum of max(0, .) terms), so
-    // key 0 (= +0.0) is a valid neutral element for the max
-    CU(cudaMemsetAsync(ctx->maxlb, 0, sizeof(long long), ctx->stream));
-    // per-thread fp32 error accumulators see at most tps*TP terms: inflate
-    const double u = 5.960464477539063e-08;
-    const double nterms = (double)p.tps * p.tp * 8 * 2 + 64.0;
-    const double einfl = 1.0 + 2.0 * nterms * u + 1.0 / 64.0;
-    // fp32 tile sums: TP sequential adds + 3 butterfly levels, then fp64
-    const double gcoef = (p.tp + 8) * u;
-    k_finalize<<<fin_blocks, 256, 0, ctx->stream>>>(ctx->c0, ctx->c1, p.nsplit, (double*)ctx->part_g.p,
-                                                   (float*)ctx->part_e.p, ctx->n_pad, einfl, gcoef, ctx->selected,
-                                                   ctx->ub, ctx->maxlb);
-    KCHECK();
-    const double margin = (double)ctx->n * 1e-12 * std::max(1.0, std::fabs(ctx->baseline)) * 1.01;
-    k_window<<<fin_blocks, 256, 0, ctx->stream>>>(ctx->c0, ctx->c1, ctx->ub, ctx->maxlb, margin, ctx->wcount,
-                                                 ctx->wlist);
-    KCHECK();
-  } else {
-    int rc = run_window_all(ctx, eb, fin_blocks);
-    if (rc) return rc;
-  }
+  int rc = ctx->dtype == EBC_F64 ? EBC_EINVAL : run_screen_window(ctx, eb, fin_blocks);
+  if (rc == EBC_EINVAL) rc = run_window_all(ctx, eb, fin_blocks);
+  if (rc) return rc;
   // exact fp64 gains of the window
   const int ng = std::min(ctx->nchunks, 32);
-  int rc = ensure(ctx, ctx->part_r, (size_t)ctx->n * ng * sizeof(double));
+  rc = ensure(ctx, ctx->part_r, (size_t)ctx->n * ng * sizeof(double));
   if (rc) return rc;
   const int rgrid = 4 * ctx->num_sms;
   const size_t rsmem = (size_t)ctx->d * sizeof(double);

@@ -171,7 +171,7 @@ struct ScreenCfg {
     size_t ring = STAGES * stage;
     size_t red = (size_t)WP * CT * (sizeof(double) + sizeof(float));
     if (ring < red) ring = red;
-    return cand + ring + (STAGES + 1) * sizeof(uint64_t) + STAGES * sizeof(int) + 16;
+    return cand + ring + (2 * STAGES + 1) * sizeof(uint64_t) + STAGES * sizeof(int) + 16;
   }
 };
 
@@ -224,7 +224,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
   const size_t red_bytes = (size_t)WP * CT_ * (sizeof(double) + sizeof(float));
   if (ring_bytes < red_bytes) ring_bytes = red_bytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(stage_base + ring_bytes);
-  uint64_t* cbar = full + STAGES;
+  uint64_t* empty = full + STAGES;
+  uint64_t* cbar = empty + STAGES;
   int* relcnt = reinterpret_cast<int*>(cbar + 1);
 
   const int t0 = blockIdx.y * tiles_per_split;
@@ -235,6 +236,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NWARPS);
       relcnt[s] = 0;
     }
     mbar_init(cbar, 1);
@@ -316,15 +318,18 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
         }
       }
     }
-    // Stage consumed (every LDS result has been used).  The last warp to
-    // release it refills it with tile it + STAGES: no warp ever waits for
-    // another warp's progress (ncu: long-scoreboard stalls on the ring).
+    // Stage consumed (every LDS result has been used).  Each warp arrives on
+    // the stage's `empty` mbarrier; the last warp to release it (smem counter)
+    // waits on that barrier -- already complete, so no stall -- and refills the
+    // stage with tile it + STAGES.  No warp ever waits for another warp's
+    // progress, and the mbarrier gives the WAR ordering against the bulk copy.
     __syncwarp();
     if (lane == 0) {
-      __threadfence_block();
+      mbar_arrive(&empty[s]);
       const int old = atomicAdd(&relcnt[s], 1);
       if (old == NWARPS - 1) {
         relcnt[s] = 0;
+        mbar_wait(&empty[s], ph);
         if (it + STAGES < nt) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           unsigned char* st = stage_base + s * stage_bytes;
