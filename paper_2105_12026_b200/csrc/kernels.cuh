@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], NWARPS);
+      mbar_init(&empty[s], THREADS);
       relcnt[s] = 0;
     }
     mbar_init(cbar, 1);
@@ -323,9 +323,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
     // waits on that barrier -- already complete, so no stall -- and refills the
     // stage with tile it + STAGES.  No warp ever waits for another warp's
     // progress, and the mbarrier gives the WAR ordering against the bulk copy.
+    mbar_arrive(&empty[s]);  // every reading thread arrives (count = THREADS)
     __syncwarp();
     if (lane == 0) {
-      mbar_arrive(&empty[s]);
       const int old = atomicAdd(&relcnt[s], 1);
       if (old == NWARPS - 1) {
         relcnt[s] = 0;
