@@ -43,7 +43,7 @@ struct ebc_ctx {
   int64_t n_pad = 0;  // rows allocated (zero padded)
   int d4 = 0;
   int nchunks = 0;    // ceil(n / RCH)
-  float kappa2 = 0.f;  // tau = kappa2 * cm32
+  float gram_kc = 0.f;  // kc = gram_kc * |c|^2
   double baseline = 0.0;
   int64_t c0 = 0, c1 = 0;  // screened candidate range
   int64_t steps_done = 0;   // selections since the last reset
@@ -53,7 +53,13 @@ struct ebc_ctx {
   double* V64 = nullptr;  // fp64 grounds
   double* e0d = nullptr;
   double* cm64 = nullptr;
-  float2* pt = nullptr;
+  float4* pt = nullptr;
+  float* nv32 = nullptr;
+  int* sticky = nullptr;  // adaptive screen: direct form for the rest of the run
+  int* gate = nullptr;    // adaptive screen: run the direct pass this step
+  PtCoef pk{};
+  int screen_mode = 2;    // 0 direct, 1 Gram, 2 adaptive (Gram, direct when the window is wide)
+  int wcap = 256;
   unsigned char* selected = nullptr;
   double* chunkpart = nullptr;  // nchunks
   unsigned int* counter = nullptr;
@@ -182,15 +188,23 @@ int plan_screen(const ebc_ctx* ctx, ScreenPlan& p) {
   return plan_shape<ScreenA>(ctx, p);
 }
 
-template <class Cfg>
-int launch_screen_t(ebc_ctx* ctx, const ScreenPlan& p) {
-  auto kern = k_screen<Cfg>;
+template <class Cfg, bool GRAM>
+int launch_screen_t(ebc_ctx* ctx, const ScreenPlan& p, const int* skip_if_set, const int* run_if_set) {
+  auto kern = k_screen<Cfg, GRAM>;
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
   dim3 grid(p.ncb, p.nsplit);
   kern<<<grid, Cfg::THREADS, p.smem, ctx->stream>>>(ctx->V32, ctx->pt, ctx->pitch, ctx->d4, ctx->c0, p.ntiles, p.tps,
-                                                    (double*)ctx->part_g.p, (float*)ctx->part_e.p, ctx->n_pad);
+                                                    (double*)ctx->part_g.p, (float*)ctx->part_e.p, ctx->n_pad,
+                                                    ctx->gram_kc, skip_if_set, run_if_set);
   KCHECK();
   return EBC_OK;
+}
+
+template <bool GRAM>
+int launch_screen(ebc_ctx* ctx, const ScreenPlan& p, const int* skip_if_set, const int* run_if_set) {
+  if (p.shape == 2) return launch_screen_t<ScreenB, GRAM>(ctx, p, skip_if_set, run_if_set);
+  if (p.shape == 1) return launch_screen_t<ScreenA4, GRAM>(ctx, p, skip_if_set, run_if_set);
+  return launch_screen_t<ScreenA, GRAM>(ctx, p, skip_if_set, run_if_set);
 }
 
 // FP64 grounds, or a d too large for any screen tile: every unselected
@@ -205,7 +219,32 @@ int run_window_all(ebc_ctx* ctx, int eb, int fin_blocks) {
   return EBC_OK;
 }
 
+// finalize + window of one screen pass (gscale 2 for the Gram form, whose
+// accumulators hold t/2).
+int run_finalize_window(ebc_ctx* ctx, const ScreenPlan& p, int fin_blocks, double gscale, const int* skip_if_set,
+                        const int* run_if_set) {
+  // per-thread fp32 error accumulators see at most tps*TP terms: inflate
+  const double u = 5.960464477539063e-08;
+  const double nterms = (double)p.tps * p.tp * 8 * 2 + 64.0;
+  const double einfl = 1.0 + 2.0 * nterms * u + 1.0 / 64.0;
+  // fp32 tile sums: TP sequential adds + 3 butterfly levels, then fp64
+  const double gcoef = (p.tp + 8) * u;
+  k_finalize<<<fin_blocks, 256, 0, ctx->stream>>>(ctx->c0, ctx->c1, p.nsplit, (double*)ctx->part_g.p,
+                                                 (float*)ctx->part_e.p, ctx->n_pad, einfl, gcoef, gscale,
+                                                 ctx->selected, ctx->ub, ctx->maxlb, skip_if_set, run_if_set);
+  KCHECK();
+  const double margin = (double)ctx->n * 1e-12 * std::max(1.0, std::fabs(ctx->baseline)) * 1.01;
+  k_window<<<fin_blocks, 256, 0, ctx->stream>>>(ctx->c0, ctx->c1, ctx->ub, ctx->maxlb, margin, ctx->wcount,
+                                               ctx->wlist, skip_if_set, run_if_set);
+  KCHECK();
+  return EBC_OK;
+}
+
 // fp32 screen of the candidate range + certified window.
+// Modes: direct form; Gram form (v.c on the FMA pipe, 2x fewer instructions);
+// adaptive = Gram, then the direct pass only if the Gram window came out wider
+// than ctx->wcap (clustered data: the Gram bound scales with |v|^2 + |c|^2, the
+// direct one with cm), sticky for the rest of the run.
 // Returns EBC_EINVAL (nothing launched) when no screen tile fits this d.
 int run_screen_window(ebc_ctx* ctx, int eb, int fin_blocks) {
   ScreenPlan p;
@@ -216,31 +255,27 @@ int run_screen_window(ebc_ctx* ctx, int eb, int fin_blocks) {
   rc = ensure(ctx, ctx->part_e, (size_t)p.nsplit * ctx->n_pad * sizeof(float));
   if (rc) return rc;
   if (ctx->timing) CU(cudaEventRecord(ctx->ev[eb + 0], ctx->stream));
-  if (p.shape == 2)
-    rc = launch_screen_t<ScreenB>(ctx, p);
-  else if (p.shape == 1)
-    rc = launch_screen_t<ScreenA4>(ctx, p);
-  else
-    rc = launch_screen_t<ScreenA>(ctx, p);
-  if (rc) return rc;
-  if (ctx->timing) CU(cudaEventRecord(ctx->ev[eb + 1], ctx->stream));
   // lower bounds are clamped at 0 (every gain is a sum of max(0, .) terms), so
   // key 0 (= +0.0) is a valid neutral element for the max
   CU(cudaMemsetAsync(ctx->maxlb, 0, sizeof(long long), ctx->stream));
-  // per-thread fp32 error accumulators see at most tps*TP terms: inflate
-  const double u = 5.960464477539063e-08;
-  const double nterms = (double)p.tps * p.tp * 8 * 2 + 64.0;
-  const double einfl = 1.0 + 2.0 * nterms * u + 1.0 / 64.0;
-  // fp32 tile sums: TP sequential adds + 3 butterfly levels, then fp64
-  const double gcoef = (p.tp + 8) * u;
-  k_finalize<<<fin_blocks, 256, 0, ctx->stream>>>(ctx->c0, ctx->c1, p.nsplit, (double*)ctx->part_g.p,
-                                                 (float*)ctx->part_e.p, ctx->n_pad, einfl, gcoef, ctx->selected,
-                                                 ctx->ub, ctx->maxlb);
-  KCHECK();
-  const double margin = (double)ctx->n * 1e-12 * std::max(1.0, std::fabs(ctx->baseline)) * 1.01;
-  k_window<<<fin_blocks, 256, 0, ctx->stream>>>(ctx->c0, ctx->c1, ctx->ub, ctx->maxlb, margin, ctx->wcount,
-                                               ctx->wlist);
-  KCHECK();
+  if (ctx->screen_mode == 0) {
+    rc = launch_screen<false>(ctx, p, nullptr, nullptr);
+    if (!rc) rc = run_finalize_window(ctx, p, fin_blocks, 1.0, nullptr, nullptr);
+  } else if (ctx->screen_mode == 1) {
+    rc = launch_screen<true>(ctx, p, nullptr, nullptr);
+    if (!rc) rc = run_finalize_window(ctx, p, fin_blocks, 2.0, nullptr, nullptr);
+  } else {
+    rc = launch_screen<true>(ctx, p, ctx->sticky, nullptr);
+    if (!rc) rc = run_finalize_window(ctx, p, fin_blocks, 2.0, ctx->sticky, nullptr);
+    if (!rc) {
+      k_adapt<<<1, 32, 0, ctx->stream>>>(ctx->wcount, ctx->maxlb, ctx->wcap, ctx->sticky, ctx->gate);
+      KCHECK();
+      rc = launch_screen<false>(ctx, p, nullptr, ctx->gate);
+    }
+    if (!rc) rc = run_finalize_window(ctx, p, fin_blocks, 1.0, nullptr, ctx->gate);
+  }
+  if (rc) return rc;
+  if (ctx->timing) CU(cudaEventRecord(ctx->ev[eb + 1], ctx->stream));
   return EBC_OK;
 }
 
@@ -286,12 +321,12 @@ int run_update(ebc_ctx* ctx, int step, double* val_dev, double* gain_dev) {
   if (ctx->dtype == EBC_F64) {
     CU(cudaFuncSetAttribute(k_update<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024));
     k_update<double><<<ctx->nchunks, RED_THREADS, smem, ctx->stream>>>(
-        ctx->V64, ctx->pitch, ctx->n, ctx->d, ctx->best, ctx->kappa2, ctx->e0d, ctx->cm64, ctx->pt, ctx->chunkpart,
+        ctx->V64, ctx->pitch, ctx->n, ctx->d, ctx->best, ctx->pk, ctx->e0d, ctx->nv32, ctx->cm64, ctx->pt, ctx->chunkpart,
         ctx->counter, 1.0 / (double)ctx->n, ctx->cur, val_dev, gain_dev, step);
   } else {
     CU(cudaFuncSetAttribute(k_update<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024));
     k_update<float><<<ctx->nchunks, RED_THREADS, smem, ctx->stream>>>(
-        ctx->V32, ctx->pitch, ctx->n, ctx->d, ctx->best, ctx->kappa2, ctx->e0d, ctx->cm64, ctx->pt, ctx->chunkpart,
+        ctx->V32, ctx->pitch, ctx->n, ctx->d, ctx->best, ctx->pk, ctx->e0d, ctx->nv32, ctx->cm64, ctx->pt, ctx->chunkpart,
         ctx->counter, 1.0 / (double)ctx->n, ctx->cur, val_dev, gain_dev, step);
   }
   KCHECK();
@@ -310,7 +345,8 @@ int ensure_events(ebc_ctx* ctx, size_t count) {
 
 int do_reset(ebc_ctx* ctx) {
   const int blocks = (int)((ctx->n + 255) / 256);
-  k_reset<<<blocks, 256, 0, ctx->stream>>>(ctx->n, ctx->e0d, ctx->kappa2, ctx->cm64, ctx->pt, ctx->selected);
+  k_reset<<<blocks, 256, 0, ctx->stream>>>(ctx->n, ctx->e0d, ctx->nv32, ctx->pk, ctx->cm64, ctx->pt, ctx->selected,
+                                           ctx->sticky);
   KCHECK();
   CU(cudaMemsetAsync(ctx->cur, 0, sizeof(double), ctx->stream));
   ctx->steps_done = 0;
@@ -320,7 +356,7 @@ int do_reset(ebc_ctx* ctx) {
 void free_ctx(ebc_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
-  void* ptrs[] = {c->V32, c->V64, c->e0d, c->cm64, c->pt, c->selected, c->chunkpart, c->counter, c->cur, c->best,
+  void* ptrs[] = {c->V32, c->V64, c->e0d, c->cm64, c->pt, c->nv32, c->sticky, c->gate, c->selected, c->chunkpart, c->counter, c->cur, c->best,
                   c->maxlb, c->wcount, c->wlist, c->wgain, c->ub};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -376,8 +412,18 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
   ctx->n_pad = ((n + 127) / 128) * 128 + 256;
   ctx->c0 = 0;
   ctx->c1 = n;
-  // tau = 2(d+8)u * cm32, slightly inflated
-  ctx->kappa2 = (float)(2.0 * (d + 8) * 5.960464477539063e-08 * (1.0 + 1.0 / 512));
+  // error quanta: direct tau = 2(d+8)u cm32; Gram
+  // kp = (d+4)u/2 (cm32 + 2|v|^2), kc = 1.5 (d+4)u |c|^2 -- all slightly inflated
+  {
+    const double u = 5.960464477539063e-08;
+    ctx->pk.tau_k = (float)(2.0 * (d + 8) * u * (1.0 + 1.0 / 512));
+    ctx->pk.gram_k = (float)(0.5 * (d + 4) * u * (1.0 + 1.0 / 512));
+    ctx->gram_kc = (float)(1.5 * (d + 4) * u * (1.0 + 1.0 / 512));
+    ctx->wcap = (int)std::max<int64_t>(256, n / 64);
+    ctx->screen_mode = d >= 24 ? 2 : 0;
+    const char* m = getenv("EBC200_SCREEN_MODE");
+    if (m && m[0]) ctx->screen_mode = atoi(m);
+  }
   int rc = EBC_OK;
 #define CUC(call)                                                                                   \
   do {                                                                                              \
@@ -425,8 +471,14 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
   }
   CUC(cudaMalloc(&ctx->e0d, (size_t)n * sizeof(double)));
   CUC(cudaMalloc(&ctx->cm64, (size_t)ctx->n_pad * sizeof(double)));
-  CUC(cudaMalloc(&ctx->pt, (size_t)ctx->n_pad * sizeof(float2)));
-  CUC(cudaMemsetAsync(ctx->pt, 0, (size_t)ctx->n_pad * sizeof(float2), ctx->stream));
+  CUC(cudaMalloc(&ctx->pt, (size_t)ctx->n_pad * sizeof(float4)));
+  CUC(cudaMemsetAsync(ctx->pt, 0, (size_t)ctx->n_pad * sizeof(float4), ctx->stream));
+  CUC(cudaMalloc(&ctx->nv32, (size_t)ctx->n_pad * sizeof(float)));
+  CUC(cudaMemsetAsync(ctx->nv32, 0, (size_t)ctx->n_pad * sizeof(float), ctx->stream));
+  CUC(cudaMalloc(&ctx->sticky, sizeof(int)));
+  CUC(cudaMemsetAsync(ctx->sticky, 0, sizeof(int), ctx->stream));
+  CUC(cudaMalloc(&ctx->gate, sizeof(int)));
+  CUC(cudaMemsetAsync(ctx->gate, 0, sizeof(int), ctx->stream));
   CUC(cudaMalloc(&ctx->selected, (size_t)ctx->n_pad));
   CUC(cudaMemsetAsync(ctx->selected, 0, (size_t)ctx->n_pad, ctx->stream));
   CUC(cudaMalloc(&ctx->chunkpart, (size_t)ctx->nchunks * sizeof(double)));
@@ -453,11 +505,11 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
     CUC(cudaStreamSynchronize(ctx->stream));  // z / caller buffers may go away
   }
   if (dtype == EBC_F64)
-    k_init<double><<<ctx->nchunks, RED_THREADS, 0, ctx->stream>>>(ctx->V64, ctx->pitch, n, d, e0dev, ctx->kappa2,
-                                                                 ctx->e0d, ctx->cm64, ctx->pt, ctx->chunkpart);
+    k_init<double><<<ctx->nchunks, RED_THREADS, 0, ctx->stream>>>(ctx->V64, ctx->pitch, n, d, e0dev, ctx->pk,
+                                                                 ctx->e0d, ctx->cm64, ctx->nv32, ctx->pt, ctx->chunkpart);
   else
-    k_init<float><<<ctx->nchunks, RED_THREADS, 0, ctx->stream>>>(ctx->V32, ctx->pitch, n, d, e0dev, ctx->kappa2,
-                                                                ctx->e0d, ctx->cm64, ctx->pt, ctx->chunkpart);
+    k_init<float><<<ctx->nchunks, RED_THREADS, 0, ctx->stream>>>(ctx->V32, ctx->pitch, n, d, e0dev, ctx->pk,
+                                                                ctx->e0d, ctx->cm64, ctx->nv32, ctx->pt, ctx->chunkpart);
   CUC(cudaGetLastError());
   double* bl = nullptr;
   CUC(cudaMalloc(&bl, sizeof(double)));

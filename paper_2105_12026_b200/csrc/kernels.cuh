@@ -71,6 +71,20 @@ __device__ __forceinline__ double dist64_row(const T* __restrict__ row, const do
   return s;
 }
 
+// ---------------------------------------------------------------- per-point screen data
+
+// pt[v] = {-cm32, tau, ip, kp}: the direct screen seeds its accumulator with
+// -cm32 and uses tau = 2(d+8)u*cm32 as error quantum; the Gram screen seeds
+// with ip = (cm32 - nv32)/2 and uses kp.
+struct PtCoef {
+  float tau_k;   // 2(d+8)u (1 + 2^-9)
+  float gram_k;  // (d+4)u/2 (1 + 2^-10)
+};
+
+__device__ __forceinline__ float4 make_pt(float c32, float nv, PtCoef k) {
+  return make_float4(-c32, k.tau_k * c32, (c32 - nv) * 0.5f, k.gram_k * (c32 + 2.f * nv));
+}
+
 // ---------------------------------------------------------------- K0: init
 
 // Widen/pad the uploaded rows into the device layout (n_pad x pitch, zero pad).
@@ -96,12 +110,13 @@ __global__ void k_pad<double, double>(const double* __restrict__ src, int64_t n,
   }
 }
 
-// e0d[v] = d(v, e0) (fp64); cm64 = e0d; pt = {-cm32, tau}; chunk partials of e0d.
+// e0d[v] = d(v, e0) (fp64); nv32 = |v|^2; cm64 = e0d; pt; chunk partials of e0d.
 template <typename T>
 __global__ void __launch_bounds__(RED_THREADS) k_init(const T* __restrict__ V, int pitch, int64_t n, int d,
-                                                      const double* __restrict__ e0, float kappa2,
+                                                      const double* __restrict__ e0, PtCoef pk,
                                                       double* __restrict__ e0d, double* __restrict__ cm64,
-                                                      float2* __restrict__ pt, double* __restrict__ part) {
+                                                      float* __restrict__ nv32, float4* __restrict__ pt,
+                                                      double* __restrict__ part) {
   __shared__ double sbuf[RED_THREADS];
   __shared__ double se0[1024];
   for (int k = threadIdx.x; k < d && k < 1024; k += blockDim.x) se0[k] = e0[k];
@@ -114,8 +129,14 @@ __global__ void __launch_bounds__(RED_THREADS) k_init(const T* __restrict__ V, i
       double t = d <= 1024 ? dist64_row(V + v * pitch, se0, d) : dist64_row(V + v * pitch, e0, d);
       e0d[v] = t;
       cm64[v] = t;
-      float c32 = (float)t;
-      pt[v] = make_float2(-c32, kappa2 * c32);
+      double nv = 0.0;
+      for (int k = 0; k < d; ++k) {
+        const double x = (double)V[v * pitch + k];
+        nv = fma(x, x, nv);
+      }
+      const float n32 = (float)nv;
+      nv32[v] = n32;
+      pt[v] = make_pt((float)t, n32, pk);
       acc += t;
     }
   }
@@ -124,14 +145,15 @@ __global__ void __launch_bounds__(RED_THREADS) k_init(const T* __restrict__ V, i
 }
 
 // Reset the cached minima to d(., e0) (ebc_reset / start of a Greedy run).
-__global__ void k_reset(int64_t n, const double* __restrict__ e0d, float kappa2, double* __restrict__ cm64,
-                        float2* __restrict__ pt, unsigned char* __restrict__ selected) {
+__global__ void k_reset(int64_t n, const double* __restrict__ e0d, const float* __restrict__ nv32, PtCoef pk,
+                        double* __restrict__ cm64, float4* __restrict__ pt, unsigned char* __restrict__ selected,
+                        int* __restrict__ sticky) {
   int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v == 0 && sticky) *sticky = 0;
   if (v < n) {
     double t = e0d[v];
     cm64[v] = t;
-    float c32 = (float)t;
-    pt[v] = make_float2(-c32, kappa2 * c32);
+    pt[v] = make_pt((float)t, nv32[v], pk);
     selected[v] = 0;
   }
 }
@@ -167,7 +189,7 @@ struct ScreenCfg {
   static constexpr int CT = WC * LC * TC;  // candidates per CTA
   static size_t smem_bytes(int pitch) {
     size_t cand = (size_t)CT * pitch * sizeof(float);
-    size_t stage = (size_t)PT * pitch * sizeof(float) + (size_t)PT * sizeof(float2);
+    size_t stage = (size_t)PT * pitch * sizeof(float) + (size_t)PT * sizeof(float4);
     size_t ring = STAGES * stage;
     size_t red = (size_t)WP * CT * (sizeof(double) + sizeof(float));
     if (ring < red) ring = red;
@@ -200,11 +222,14 @@ __device__ __forceinline__ float rowsum8_transposed(const float (&x)[8], int r) 
   return keep + __shfl_xor_sync(0xffffffffu, send, 1);
 }
 
-template <class Cfg>
+template <class Cfg, bool GRAM>
 __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
-    k_screen(const float* __restrict__ V, const float2* __restrict__ pt, int pitch, int d4, int64_t cand0,
+    k_screen(const float* __restrict__ V, const float4* __restrict__ pt, int pitch, int d4, int64_t cand0,
              int ntiles, int tiles_per_split, double* __restrict__ part_g, float* __restrict__ part_e,
-             int64_t part_stride) {
+             int64_t part_stride, float gram_kc, const int* __restrict__ skip_if_set,
+             const int* __restrict__ run_if_set) {
+  if (skip_if_set && *skip_if_set) return;  // adaptive mode: Gram pass skipped (sticky direct)
+  if (run_if_set && !*run_if_set) return;   // adaptive mode: direct pass not needed
   constexpr int TP = Cfg::TP, TC = Cfg::TC, LR = Cfg::LR, LC = Cfg::LC, WP = Cfg::WP;
   constexpr int STAGES = Cfg::STAGES, NWARPS = Cfg::NWARPS, THREADS = Cfg::THREADS;
   constexpr int PT_ = Cfg::PT, CT_ = Cfg::CT;
@@ -216,7 +241,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
 
   const size_t cand_bytes = (size_t)CT_ * pitch * sizeof(float);
   const size_t vt_bytes = (size_t)PT_ * pitch * sizeof(float);
-  const size_t pt_bytes = (size_t)PT_ * sizeof(float2);
+  const size_t pt_bytes = (size_t)PT_ * sizeof(float4);
   float* cs = reinterpret_cast<float*>(smem);
   unsigned char* stage_base = smem + cand_bytes;
   const size_t stage_bytes = vt_bytes + pt_bytes;
@@ -265,6 +290,31 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
   for (int j = 0; j < TC; ++j) crow_s[j] = cs + (wc * (LC * TC) + q + LC * j) * pitch;
 
   mbar_wait(cbar, 0);
+  // Gram form: per-candidate |c|^2 (fp32, sequential -- covered by kc), the
+  // accumulator seed half -|c|^2/2 and the error quantum kc.
+  float ic[TC], kc[TC], cnt[TC];
+#pragma unroll
+  for (int j = 0; j < TC; ++j) {
+    ic[j] = 0.f;
+    kc[j] = 0.f;
+    cnt[j] = 0.f;
+  }
+  if (GRAM) {
+#pragma unroll
+    for (int j = 0; j < TC; ++j) {
+      float nc = 0.f;
+      for (int k4 = 0; k4 < d4; ++k4) {
+        const float4 b = *reinterpret_cast<const float4*>(crow_s[j] + 4 * k4);
+        nc = fmaf(b.x, b.x, nc);
+        nc = fmaf(b.y, b.y, nc);
+        nc = fmaf(b.z, b.z, nc);
+        nc = fmaf(b.w, b.w, nc);
+      }
+      ic[j] = -0.5f * nc;
+      kc[j] = gram_kc * nc;
+    }
+  }
+  __syncthreads();
   // Swap adjacent dims of the resident candidate tile: an LDS.128 lands vector
   // component j in a register of parity j%2, so pairing v_k (even register)
   // with c_k now stored in the odd slot makes every FADD read one even and one
@@ -284,7 +334,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
     const uint32_t ph = (it / STAGES) & 1;
     mbar_wait(&full[s], ph);
     const float* vs = reinterpret_cast<const float*>(stage_base + s * stage_bytes);
-    const float2* ps = reinterpret_cast<const float2*>(stage_base + s * stage_bytes + vt_bytes);
+    const float4* ps = reinterpret_cast<const float4*>(stage_base + s * stage_bytes + vt_bytes);
 
     float acc[TP][TC];
     float tau[TP];
@@ -292,11 +342,11 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
 #pragma unroll
     for (int i = 0; i < TP; ++i) {
       const int p = wp * (LR * TP) + r + LR * i;
-      const float2 pp = ps[p];
-      tau[i] = pp.y;
+      const float4 pp = ps[p];
+      tau[i] = GRAM ? pp.w : pp.y;
       vrow[i] = vs + p * pitch;
 #pragma unroll
-      for (int j = 0; j < TC; ++j) acc[i][j] = pp.x;
+      for (int j = 0; j < TC; ++j) acc[i][j] = GRAM ? pp.z + ic[j] : pp.x;
     }
 #pragma unroll(TP >= 8 ? 1 : 2)
     for (int k4 = 0; k4 < d4; ++k4) {
@@ -309,12 +359,19 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
       for (int i = 0; i < TP; ++i) {
 #pragma unroll
         for (int j = 0; j < TC; ++j) {
-          float t;
           // b holds (c_{k+1}, c_k, c_{k+3}, c_{k+2}) -- see the swap above
-          t = a[i].x - b[j].y; acc[i][j] = fmaf(t, t, acc[i][j]);
-          t = a[i].y - b[j].x; acc[i][j] = fmaf(t, t, acc[i][j]);
-          t = a[i].z - b[j].w; acc[i][j] = fmaf(t, t, acc[i][j]);
-          t = a[i].w - b[j].z; acc[i][j] = fmaf(t, t, acc[i][j]);
+          if (GRAM) {
+            acc[i][j] = fmaf(a[i].x, b[j].y, acc[i][j]);
+            acc[i][j] = fmaf(a[i].y, b[j].x, acc[i][j]);
+            acc[i][j] = fmaf(a[i].z, b[j].w, acc[i][j]);
+            acc[i][j] = fmaf(a[i].w, b[j].z, acc[i][j]);
+          } else {
+            float t;
+            t = a[i].x - b[j].y; acc[i][j] = fmaf(t, t, acc[i][j]);
+            t = a[i].y - b[j].x; acc[i][j] = fmaf(t, t, acc[i][j]);
+            t = a[i].z - b[j].w; acc[i][j] = fmaf(t, t, acc[i][j]);
+            t = a[i].w - b[j].z; acc[i][j] = fmaf(t, t, acc[i][j]);
+          }
         }
       }
     }
@@ -342,14 +399,21 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
     }
     __syncwarp();
 
-    // epilogue: sv = d32 - cm32
+    // epilogue.  direct: acc = d32 - cm32;  Gram: acc = (cm - |v|^2 - |c|^2)/2 + v.c = t/2
 #pragma unroll
     for (int i = 0; i < TP; ++i) {
 #pragma unroll
       for (int j = 0; j < TC; ++j) {
         const float sv = acc[i][j];
-        g[j] += fmaxf(-sv, 0.f);
-        e[j] = fmaf(sv < tau[i] ? 1.f : 0.f, tau[i], e[j]);
+        if (GRAM) {
+          g[j] += fmaxf(sv, 0.f);
+          const float f = (sv + tau[i] > -kc[j]) ? 1.f : 0.f;
+          e[j] = fmaf(f, tau[i], e[j]);
+          cnt[j] += f;
+        } else {
+          g[j] += fmaxf(-sv, 0.f);
+          e[j] = fmaf(sv < tau[i] ? 1.f : 0.f, tau[i], e[j]);
+        }
       }
     }
     // fold this tile's fp32 gains into fp64 (lane r: candidate j = r)
@@ -359,6 +423,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
   }
 
   // error bound: same transposed reduce in fp32 (covered by the inflation factor)
+  if (GRAM) {
+#pragma unroll
+    for (int j = 0; j < TC; ++j) e[j] = fmaf(kc[j], cnt[j], e[j]);
+  }
   const float etot = rowsum8_transposed(e, r);
   // lane (r, q) of warp (wp, wc) now holds candidate  wc*32 + q + 4*r
   __syncthreads();  // all stages idle: reuse the ring for the cross-warp combine
@@ -395,8 +463,11 @@ using ScreenB = ScreenCfg<8, 2, 4, 3, 1>;
 // block's largest lower bound into *maxlb (order-independent atomicMax).
 __global__ void k_finalize(int64_t c0, int64_t c1, int nsplit, const double* __restrict__ part_g,
                            const float* __restrict__ part_e, int64_t part_stride, double einfl, double gcoef,
-                           const unsigned char* __restrict__ selected, double* __restrict__ ub,
-                           long long* __restrict__ maxlb) {
+                           double gscale, const unsigned char* __restrict__ selected, double* __restrict__ ub,
+                           long long* __restrict__ maxlb, const int* __restrict__ skip_if_set,
+                           const int* __restrict__ run_if_set) {
+  if (skip_if_set && *skip_if_set) return;
+  if (run_if_set && !*run_if_set) return;
   __shared__ long long smax[256];
   const int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   long long key = dkey(-INFINITY);
@@ -406,6 +477,8 @@ __global__ void k_finalize(int64_t c0, int64_t c1, int nsplit, const double* __r
       g += part_g[s * part_stride + c];
       e += (double)part_e[s * part_stride + c];
     }
+    g *= gscale;
+    e *= gscale;
     const double eps = e * einfl + gcoef * g + 1e-300;
     if (selected[c]) {
       ub[c - c0] = -INFINITY;
@@ -426,7 +499,10 @@ __global__ void k_finalize(int64_t c0, int64_t c1, int nsplit, const double* __r
 // W = {c : ub_c >= max lb - margin}  (append order is irrelevant: the pick is by
 // exact value and lowest index).
 __global__ void k_window(int64_t c0, int64_t c1, const double* __restrict__ ub, const long long* __restrict__ maxlb,
-                         double margin, int* __restrict__ wcount, int64_t* __restrict__ wlist) {
+                         double margin, int* __restrict__ wcount, int64_t* __restrict__ wlist,
+                         const int* __restrict__ skip_if_set, const int* __restrict__ run_if_set) {
+  if (skip_if_set && *skip_if_set) return;
+  if (run_if_set && !*run_if_set) return;
   const int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c < c1) {
     const double thr = dkey_inv(*maxlb) - margin;
@@ -434,6 +510,22 @@ __global__ void k_window(int64_t c0, int64_t c1, const double* __restrict__ ub, 
     if (u >= thr && u > -INFINITY) {
       int slot = atomicAdd(wcount, 1);
       wlist[slot] = c;
+    }
+  }
+}
+
+// Adaptive screen: after the Gram pass, decide whether the direct pass must
+// run (window larger than `cap`, or direct already sticky for this run).
+__global__ void k_adapt(int* __restrict__ wcount, long long* __restrict__ maxlb, int cap, int* __restrict__ sticky,
+                        int* __restrict__ gate) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    if (*sticky || *wcount > cap) {
+      *sticky = 1;
+      *gate = 1;
+      *wcount = 0;
+      *maxlb = 0;
+    } else {
+      *gate = 0;
     }
   }
 }
@@ -540,9 +632,10 @@ __global__ void __launch_bounds__(1024) k_pick(const int* __restrict__ wcount, c
 // The last block to finish turns the partials into f(S) and the step record.
 template <typename T>
 __global__ void __launch_bounds__(RED_THREADS) k_update(const T* __restrict__ V, int pitch, int64_t n, int d,
-                                                        const int64_t* __restrict__ best, float kappa2,
-                                                        const double* __restrict__ e0d, double* __restrict__ cm64,
-                                                        float2* __restrict__ pt, double* __restrict__ fpart,
+                                                        const int64_t* __restrict__ best, PtCoef pk,
+                                                        const double* __restrict__ e0d, const float* __restrict__ nv32,
+                                                        double* __restrict__ cm64, float4* __restrict__ pt,
+                                                        double* __restrict__ fpart,
                                                         unsigned int* __restrict__ counter, double inv_n,
                                                         double* __restrict__ cur, double* __restrict__ val_out,
                                                         double* __restrict__ gain_out, int step) {
@@ -562,8 +655,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_update(const T* __restrict__ V,
       if (t < m) {
         m = t;
         cm64[v] = m;
-        const float c32 = (float)m;
-        pt[v] = make_float2(-c32, kappa2 * c32);
+        pt[v] = make_pt((float)m, nv32[v], pk);
       }
       acc += e0d[v] - m;
     }
