@@ -333,6 +333,10 @@ def run_ours(args):
             "traffic": traffic,
             "work": "2d FP32 FMA-pipe ops per point-candidate pair (SURVEY.md §8(d)); k_screen launches of one run "
                     "summed; peak = 148 SM x 128 lanes x 1.965 GHz (nominal; MEASURED_PEAKS has no FP32 figure)",
+            "flag": ("frac > 1.0: the adaptive screen runs the Gram form (d FFMA per pair, v.c on the FMA pipe) "
+                     "against the direct-form W = 2d; W is not redefined (SURVEY.md §8(d))")
+                    if achieved > PEAK_FP32_OPS else None,
+            "screen_mode": os.environ.get("EBC200_SCREEN_MODE", "auto (Gram, direct fallback)" if d >= 24 else "direct"),
             "screen_ms_per_step": scr, "screen_share_of_step": scr / step_ms,
         }
         line["gpu_launches"] = int(launches)

@@ -188,9 +188,9 @@ int plan_screen(const ebc_ctx* ctx, ScreenPlan& p) {
   return plan_shape<ScreenA>(ctx, p);
 }
 
-template <class Cfg, bool GRAM>
+template <class Cfg, bool GRAM, int PITCH = 0>
 int launch_screen_t(ebc_ctx* ctx, const ScreenPlan& p, const int* skip_if_set, const int* run_if_set) {
-  auto kern = k_screen<Cfg, GRAM>;
+  auto kern = k_screen<Cfg, GRAM, PITCH>;
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
   dim3 grid(p.ncb, p.nsplit);
   kern<<<grid, Cfg::THREADS, p.smem, ctx->stream>>>(ctx->V32, ctx->pt, ctx->pitch, ctx->d4, ctx->c0, p.ntiles, p.tps,
@@ -202,9 +202,27 @@ int launch_screen_t(ebc_ctx* ctx, const ScreenPlan& p, const int* skip_if_set, c
 
 template <bool GRAM>
 int launch_screen(ebc_ctx* ctx, const ScreenPlan& p, const int* skip_if_set, const int* run_if_set) {
-  if (p.shape == 2) return launch_screen_t<ScreenB, GRAM>(ctx, p, skip_if_set, run_if_set);
+  if (p.shape == 2) {
+    // compile-time pitches for the BASELINE dims (16, 32, 64, 100)
+    switch (ctx->pitch) {
+      case 20: return launch_screen_t<ScreenB, GRAM, 20>(ctx, p, skip_if_set, run_if_set);
+      case 36: return launch_screen_t<ScreenB, GRAM, 36>(ctx, p, skip_if_set, run_if_set);
+      case 68: return launch_screen_t<ScreenB, GRAM, 68>(ctx, p, skip_if_set, run_if_set);
+      case 100: return launch_screen_t<ScreenB, GRAM, 100>(ctx, p, skip_if_set, run_if_set);
+      default: return launch_screen_t<ScreenB, GRAM>(ctx, p, skip_if_set, run_if_set);
+    }
+  }
   if (p.shape == 1) return launch_screen_t<ScreenA4, GRAM>(ctx, p, skip_if_set, run_if_set);
   return launch_screen_t<ScreenA, GRAM>(ctx, p, skip_if_set, run_if_set);
+}
+
+template <typename T, bool BIGD>
+int launch_refine(ebc_ctx* ctx, const T* V, int grid, size_t smem, int ng) {
+  CU(cudaFuncSetAttribute(k_refine<T, BIGD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024));
+  k_refine<T, BIGD><<<grid, RED_THREADS, smem, ctx->stream>>>(V, ctx->pitch, ctx->n, ctx->d, ctx->cm64, ctx->wcount,
+                                                             ctx->wlist, ctx->nchunks, ng, (double*)ctx->part_r.p);
+  KCHECK();
+  return EBC_OK;
 }
 
 // FP64 grounds, or a d too large for any screen tile: every unselected
@@ -291,22 +309,18 @@ int run_step_select(ebc_ctx* ctx, int step, int commit, int64_t* sel_dev) {
   if (rc) return rc;
   // exact fp64 gains of the window
   const int ng = std::min(ctx->nchunks, 32);
-  rc = ensure(ctx, ctx->part_r, (size_t)ctx->n * ng * sizeof(double));
+  rc = ensure(ctx, ctx->part_r, (size_t)(ctx->n + RW) * ng * sizeof(double));
   if (rc) return rc;
   const int rgrid = 4 * ctx->num_sms;
-  const size_t rsmem = (size_t)ctx->d * sizeof(double);
-  if (ctx->dtype == EBC_F64) {
-    CU(cudaFuncSetAttribute(k_refine<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem + 1024));
-    k_refine<double><<<rgrid, RED_THREADS, rsmem, ctx->stream>>>(ctx->V64, ctx->pitch, ctx->n, ctx->d, ctx->cm64,
-                                                               ctx->wcount, ctx->wlist, ctx->nchunks, ng,
-                                                               (double*)ctx->part_r.p);
-  } else {
-    CU(cudaFuncSetAttribute(k_refine<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem + 1024));
-    k_refine<float><<<rgrid, RED_THREADS, rsmem, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->n, ctx->d, ctx->cm64,
-                                                              ctx->wcount, ctx->wlist, ctx->nchunks, ng,
-                                                              (double*)ctx->part_r.p);
-  }
-  KCHECK();
+  const bool bigd = (size_t)RW * ctx->d * sizeof(double) > 160 * 1024;
+  const size_t rsmem = bigd ? 0 : (size_t)RW * ctx->d * sizeof(double);
+  if (ctx->dtype == EBC_F64)
+    rc = bigd ? launch_refine<double, true>(ctx, ctx->V64, rgrid, rsmem, ng)
+              : launch_refine<double, false>(ctx, ctx->V64, rgrid, rsmem, ng);
+  else
+    rc = bigd ? launch_refine<float, true>(ctx, ctx->V32, rgrid, rsmem, ng)
+              : launch_refine<float, false>(ctx, ctx->V32, rgrid, rsmem, ng);
+  if (rc) return rc;
   k_pick<<<1, 1024, 0, ctx->stream>>>(ctx->wcount, ctx->wlist, ng, (double*)ctx->part_r.p,
                                       1.0 / (double)ctx->n, ctx->cur, ctx->wgain, ctx->best, commit, step,
                                       ctx->selected, sel_dev);

@@ -222,14 +222,16 @@ __device__ __forceinline__ float rowsum8_transposed(const float (&x)[8], int r) 
   return keep + __shfl_xor_sync(0xffffffffu, send, 1);
 }
 
-template <class Cfg, bool GRAM>
+template <class Cfg, bool GRAM, int PITCH>
 __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
-    k_screen(const float* __restrict__ V, const float4* __restrict__ pt, int pitch, int d4, int64_t cand0,
+    k_screen(const float* __restrict__ V, const float4* __restrict__ pt, int pitch_rt, int d4, int64_t cand0,
              int ntiles, int tiles_per_split, double* __restrict__ part_g, float* __restrict__ part_e,
              int64_t part_stride, float gram_kc, const int* __restrict__ skip_if_set,
              const int* __restrict__ run_if_set) {
   if (skip_if_set && *skip_if_set) return;  // adaptive mode: Gram pass skipped (sticky direct)
   if (run_if_set && !*run_if_set) return;   // adaptive mode: direct pass not needed
+  // PITCH != 0: compile-time row pitch -> every LDS address is base + immediate
+  const int pitch = PITCH ? PITCH : pitch_rt;
   constexpr int TP = Cfg::TP, TC = Cfg::TC, LR = Cfg::LR, LC = Cfg::LC, WP = Cfg::WP;
   constexpr int STAGES = Cfg::STAGES, NWARPS = Cfg::NWARPS, THREADS = Cfg::THREADS;
   constexpr int PT_ = Cfg::PT, CT_ = Cfg::CT;
@@ -355,17 +357,37 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
       for (int i = 0; i < TP; ++i) a[i] = *reinterpret_cast<const float4*>(vrow[i] + 4 * k4);
 #pragma unroll
       for (int j = 0; j < TC; ++j) b[j] = *reinterpret_cast<const float4*>(crow_s[j] + 4 * k4);
+      // b holds (c_{k+1}, c_k, c_{k+3}, c_{k+2}) -- see the swap above
+      if (GRAM) {
+        // component-outer order: each a[i].comp feeds 8 consecutive FFMAs in
+        // the same operand slot (operand-reuse cache), so only b and acc are
+        // read from the register banks
+#pragma unroll
+        for (int i = 0; i < TP; ++i) {
+#pragma unroll
+          for (int j = 0; j < TC; ++j) acc[i][j] = fmaf(a[i].x, b[j].y, acc[i][j]);
+        }
+#pragma unroll
+        for (int i = 0; i < TP; ++i) {
+#pragma unroll
+          for (int j = 0; j < TC; ++j) acc[i][j] = fmaf(a[i].y, b[j].x, acc[i][j]);
+        }
+#pragma unroll
+        for (int i = 0; i < TP; ++i) {
+#pragma unroll
+          for (int j = 0; j < TC; ++j) acc[i][j] = fmaf(a[i].z, b[j].w, acc[i][j]);
+        }
+#pragma unroll
+        for (int i = 0; i < TP; ++i) {
+#pragma unroll
+          for (int j = 0; j < TC; ++j) acc[i][j] = fmaf(a[i].w, b[j].z, acc[i][j]);
+        }
+      }
 #pragma unroll
       for (int i = 0; i < TP; ++i) {
 #pragma unroll
         for (int j = 0; j < TC; ++j) {
-          // b holds (c_{k+1}, c_k, c_{k+3}, c_{k+2}) -- see the swap above
-          if (GRAM) {
-            acc[i][j] = fmaf(a[i].x, b[j].y, acc[i][j]);
-            acc[i][j] = fmaf(a[i].y, b[j].x, acc[i][j]);
-            acc[i][j] = fmaf(a[i].z, b[j].w, acc[i][j]);
-            acc[i][j] = fmaf(a[i].w, b[j].z, acc[i][j]);
-          } else {
+          if (!GRAM) {
             float t;
             t = a[i].x - b[j].y; acc[i][j] = fmaf(t, t, acc[i][j]);
             t = a[i].y - b[j].x; acc[i][j] = fmaf(t, t, acc[i][j]);
@@ -541,41 +563,94 @@ __global__ void k_window_all(int64_t c0, int64_t c1, const unsigned char* __rest
 }
 
 // Exact fp64 gain partials.  The nchunks point chunks are cut into ng fixed
-// groups (ng depends only on n); unit (w, grp) sums its chunks' fixed-tree
-// partials left to right into part_r[w*ng + grp].  Persistent grid over units.
-template <typename T>
+// groups (ng depends only on n).  A unit is (window group of RW candidates,
+// chunk group): every V row it reads is used for RW candidates (L2 traffic /RW).
+// Per candidate and chunk, each thread sums its 4 points in order, then the
+// 256 per-thread partials are reduced by one warp in a fixed order (8
+// sequential per lane, then a butterfly); chunks are added left to right into
+// part_r[w*ng + grp].  A candidate's value never depends on its RW neighbours,
+// its slot in the window, or the number of ranks.
+constexpr int RW = 8;
+template <typename T, bool BIGD>
 __global__ void __launch_bounds__(RED_THREADS) k_refine(const T* __restrict__ V, int pitch, int64_t n, int d,
                                                         const double* __restrict__ cm64,
                                                         const int* __restrict__ wcount,
                                                         const int64_t* __restrict__ wlist, int nchunks, int ng,
                                                         double* __restrict__ part_r) {
-  extern __shared__ double cd[];  // d doubles
-  __shared__ double sbuf[RED_THREADS];
+  extern __shared__ double cd[];  // RW * d doubles (BIGD: candidates read through L1 instead)
+  __shared__ double red[RW][RED_THREADS];
+  __shared__ int64_t cidx[RW];
+  __shared__ double tot[RW];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int cpg = (nchunks + ng - 1) / ng;
-  const int64_t units = (int64_t)(*wcount) * ng;
+  const int wc = *wcount;
+  const int ngroups = (wc + RW - 1) / RW;
+  const int64_t units = (int64_t)ngroups * ng;
   for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
-    const int64_t w = u / ng;
-    const int grp = (int)(u - w * ng);
-    const int64_t c = wlist[w];
+    const int wg = (int)(u / ng);
+    const int grp = (int)(u - (int64_t)wg * ng);
+    const int nw = min(RW, wc - wg * RW);
     __syncthreads();
-    for (int k = threadIdx.x; k < d; k += blockDim.x) cd[k] = (double)V[c * pitch + k];
+    if (!BIGD) {
+      for (int i = tid; i < RW * d; i += blockDim.x) {
+        const int j = i / d, k = i - j * d;
+        cd[i] = j < nw ? (double)V[wlist[wg * RW + j] * pitch + k] : 0.0;
+      }
+    }
+    if (tid < RW) {
+      tot[tid] = 0.0;
+      cidx[tid] = tid < nw ? wlist[wg * RW + tid] : wlist[wg * RW];
+    }
     __syncthreads();
-    double total = 0.0;
     const int ch1 = min(nchunks, (grp + 1) * cpg);
     for (int ch = grp * cpg; ch < ch1; ++ch) {
-      double acc = 0.0;
+      double acc[RW];
+#pragma unroll
+      for (int j = 0; j < RW; ++j) acc[j] = 0.0;
       for (int i = 0; i < RCH / RED_THREADS; ++i) {
-        const int64_t v = (int64_t)ch * RCH + threadIdx.x + (int64_t)i * RED_THREADS;
+        const int64_t v = (int64_t)ch * RCH + tid + (int64_t)i * RED_THREADS;
         if (v < n) {
-          const double t = cm64[v] - dist64_row(V + v * pitch, cd, d);
-          acc += t > 0.0 ? t : 0.0;
+          double s[RW];
+#pragma unroll
+          for (int j = 0; j < RW; ++j) s[j] = 0.0;
+          const T* row = V + v * pitch;
+          for (int k = 0; k < d; ++k) {
+            const double x = (double)row[k];
+#pragma unroll
+            for (int j = 0; j < RW; ++j) {
+              if (j < nw) {  // block-uniform: a short window does not pay for RW
+                const double cv = BIGD ? (double)__ldg(V + cidx[j] * pitch + k) : cd[j * d + k];
+                const double t = x - cv;
+                s[j] = fma(t, t, s[j]);
+              }
+            }
+          }
+          const double c = cm64[v];
+#pragma unroll
+          for (int j = 0; j < RW; ++j) {
+            const double t = c - s[j];
+            acc[j] += t > 0.0 ? t : 0.0;
+          }
         }
       }
-      total += block_sum_256(acc, sbuf);  // identical in every thread
+#pragma unroll
+      for (int j = 0; j < RW; ++j) red[j][tid] = acc[j];
+      __syncthreads();
+      {
+        // warp `warp` reduces candidate j = warp (RW == 8 warps)
+        double x = 0.0;
+#pragma unroll
+        for (int q = 0; q < RED_THREADS / 32; ++q) x += red[warp][lane * (RED_THREADS / 32) + q];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        if (lane == 0) tot[warp] += x;
+      }
+      __syncthreads();
     }
-    if (threadIdx.x == 0) part_r[u] = total;
+    if (tid < nw) part_r[(int64_t)(wg * RW + tid) * ng + grp] = tot[tid];
   }
 }
+static_assert(RW == RED_THREADS / 32, "one reducing warp per window candidate");
 
 // Exact gains of W, the reference argmax rule (optimize.py:83-85):
 //   top = max value; window = 1e-12*max(1,|top|); best = lowest index with
