@@ -112,6 +112,11 @@ int ebc_set_timing(ebc_ctx* ctx, int on);
  * [1] refine+pick, [2] cached-min update, [3] whole call.  For bench.py. */
 int ebc_last_timings(const ebc_ctx* ctx, double* out_ms4);
 
+/* Screen statistics since the last reset / Greedy run: [0] sum of certified
+ * window sizes, [1] largest window, [2] screen rung in use at the end (0 tensor
+ * Gram, 1 FFMA Gram, 2 direct, -1 n/a), [3] steps. */
+int ebc_last_stats(const ebc_ctx* ctx, int64_t* out4);
+
 /* Kernel launches issued by the last call (bench.py's gpu_launches). */
 int64_t ebc_last_launches(const ebc_ctx* ctx);
 

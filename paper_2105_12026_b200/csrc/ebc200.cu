@@ -18,6 +18,7 @@
 
 #include "../../include/ebc200.h"
 #include "kernels.cuh"
+#include "screen_tc.cuh"
 
 using namespace ebc;
 
@@ -55,11 +56,19 @@ struct ebc_ctx {
   double* cm64 = nullptr;
   float4* pt = nullptr;
   float* nv32 = nullptr;
-  int* sticky = nullptr;  // adaptive screen: direct form for the rest of the run
-  int* gate = nullptr;    // adaptive screen: run the direct pass this step
+  long long* stats = nullptr;  // k_pick: window-size statistics of the last run
+  int* level = nullptr;  // adaptive screen: current rung of the ladder (0 tensor, 1 FFMA Gram, 2 direct)
   PtCoef pk{};
-  int screen_mode = 2;    // 0 direct, 1 Gram, 2 adaptive (Gram, direct when the window is wide)
+  // screen mode: 0 direct, 1 FFMA Gram, 2 adaptive from FFMA Gram, 3 adaptive from the tensor screen
+  int screen_mode = 2;
   int wcap = 256;
+  // tensor-core Gram screen (tcgen05, kind::tf32, 3xTF32)
+  float* Vhi = nullptr;
+  float* Vlo = nullptr;
+  float2* pttc = nullptr;
+  int kpad = 0;
+  int tc_np = 0;  // points per tensor tile (0: tensor screen unavailable)
+  float tc_ka = 0.f, tc_kb = 0.f, tc_kc = 0.f;
   unsigned char* selected = nullptr;
   double* chunkpart = nullptr;  // nchunks
   unsigned int* counter = nullptr;
@@ -189,31 +198,31 @@ int plan_screen(const ebc_ctx* ctx, ScreenPlan& p) {
 }
 
 template <class Cfg, bool GRAM, int PITCH = 0>
-int launch_screen_t(ebc_ctx* ctx, const ScreenPlan& p, const int* skip_if_set, const int* run_if_set) {
+int launch_screen_t(ebc_ctx* ctx, const ScreenPlan& p, const int* level_now, int level) {
   auto kern = k_screen<Cfg, GRAM, PITCH>;
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
   dim3 grid(p.ncb, p.nsplit);
   kern<<<grid, Cfg::THREADS, p.smem, ctx->stream>>>(ctx->V32, ctx->pt, ctx->pitch, ctx->d4, ctx->c0, p.ntiles, p.tps,
                                                     (double*)ctx->part_g.p, (float*)ctx->part_e.p, ctx->n_pad,
-                                                    ctx->gram_kc, skip_if_set, run_if_set);
+                                                    ctx->gram_kc, level_now, level);
   KCHECK();
   return EBC_OK;
 }
 
 template <bool GRAM>
-int launch_screen(ebc_ctx* ctx, const ScreenPlan& p, const int* skip_if_set, const int* run_if_set) {
+int launch_screen(ebc_ctx* ctx, const ScreenPlan& p, const int* level_now, int level) {
   if (p.shape == 2) {
     // compile-time pitches for the BASELINE dims (16, 32, 64, 100)
     switch (ctx->pitch) {
-      case 20: return launch_screen_t<ScreenB, GRAM, 20>(ctx, p, skip_if_set, run_if_set);
-      case 36: return launch_screen_t<ScreenB, GRAM, 36>(ctx, p, skip_if_set, run_if_set);
-      case 68: return launch_screen_t<ScreenB, GRAM, 68>(ctx, p, skip_if_set, run_if_set);
-      case 100: return launch_screen_t<ScreenB, GRAM, 100>(ctx, p, skip_if_set, run_if_set);
-      default: return launch_screen_t<ScreenB, GRAM>(ctx, p, skip_if_set, run_if_set);
+      case 20: return launch_screen_t<ScreenB, GRAM, 20>(ctx, p, level_now, level);
+      case 36: return launch_screen_t<ScreenB, GRAM, 36>(ctx, p, level_now, level);
+      case 68: return launch_screen_t<ScreenB, GRAM, 68>(ctx, p, level_now, level);
+      case 100: return launch_screen_t<ScreenB, GRAM, 100>(ctx, p, level_now, level);
+      default: return launch_screen_t<ScreenB, GRAM>(ctx, p, level_now, level);
     }
   }
-  if (p.shape == 1) return launch_screen_t<ScreenA4, GRAM>(ctx, p, skip_if_set, run_if_set);
-  return launch_screen_t<ScreenA, GRAM>(ctx, p, skip_if_set, run_if_set);
+  if (p.shape == 1) return launch_screen_t<ScreenA4, GRAM>(ctx, p, level_now, level);
+  return launch_screen_t<ScreenA, GRAM>(ctx, p, level_now, level);
 }
 
 template <typename T, bool BIGD>
@@ -237,60 +246,118 @@ int run_window_all(ebc_ctx* ctx, int eb, int fin_blocks) {
   return EBC_OK;
 }
 
-// finalize + window of one screen pass (gscale 2 for the Gram form, whose
-// accumulators hold t/2).
-int run_finalize_window(ebc_ctx* ctx, const ScreenPlan& p, int fin_blocks, double gscale, const int* skip_if_set,
-                        const int* run_if_set) {
-  // per-thread fp32 error accumulators see at most tps*TP terms: inflate
+// finalize + window of one screen pass (gscale 2 for the Gram forms, whose
+// accumulators hold t/2).  nterms bounds the terms of one fp32 error
+// accumulator; gterms the fp32 terms summed before each fp64 fold.
+int run_finalize_window(ebc_ctx* ctx, int nsplit, double nterms, int gterms, int fin_blocks, double gscale,
+                        const int* level_now, int level) {
   const double u = 5.960464477539063e-08;
-  const double nterms = (double)p.tps * p.tp * 8 * 2 + 64.0;
-  const double einfl = 1.0 + 2.0 * nterms * u + 1.0 / 64.0;
-  // fp32 tile sums: TP sequential adds + 3 butterfly levels, then fp64
-  const double gcoef = (p.tp + 8) * u;
-  k_finalize<<<fin_blocks, 256, 0, ctx->stream>>>(ctx->c0, ctx->c1, p.nsplit, (double*)ctx->part_g.p,
+  const double einfl = 1.0 + 2.0 * (nterms + 64.0) * u + 1.0 / 64.0;
+  const double gcoef = (gterms + 8) * u;
+  k_finalize<<<fin_blocks, 256, 0, ctx->stream>>>(ctx->c0, ctx->c1, nsplit, (double*)ctx->part_g.p,
                                                  (float*)ctx->part_e.p, ctx->n_pad, einfl, gcoef, gscale,
-                                                 ctx->selected, ctx->ub, ctx->maxlb, skip_if_set, run_if_set);
+                                                 ctx->selected, ctx->ub, ctx->maxlb, level_now, level);
   KCHECK();
   const double margin = (double)ctx->n * 1e-12 * std::max(1.0, std::fabs(ctx->baseline)) * 1.01;
   k_window<<<fin_blocks, 256, 0, ctx->stream>>>(ctx->c0, ctx->c1, ctx->ub, ctx->maxlb, margin, ctx->wcount,
-                                               ctx->wlist, skip_if_set, run_if_set);
+                                               ctx->wlist, level_now, level);
   KCHECK();
   return EBC_OK;
 }
 
+struct TcPlan {
+  int ncb, ntiles, tps, nsplit;
+  size_t smem;
+};
+
+bool plan_tc(const ebc_ctx* ctx, TcPlan& p) {
+  if (!ctx->tc_np || (ctx->c0 % 8) != 0) return false;
+  const int64_t ncand = ctx->c1 - ctx->c0;
+  p.ncb = (int)((ncand + tc::M - 1) / tc::M);
+  p.ntiles = (int)((ctx->n + ctx->tc_np - 1) / ctx->tc_np);
+  p.smem = tc::smem_bytes(ctx->kpad, ctx->tc_np);
+  const int64_t slots = ctx->num_sms;  // one CTA per SM
+  double best_cost = 1e300;
+  p.tps = p.ntiles;
+  for (int s = 1; s <= 64 && s <= p.ntiles; ++s) {
+    const int tps = (p.ntiles + s - 1) / s;
+    const int ns = (p.ntiles + tps - 1) / tps;
+    const double waves = (double)(((int64_t)p.ncb * ns + slots - 1) / slots);
+    const double cost = waves * (tps + 2.0);
+    if (cost < best_cost * 0.999) {
+      best_cost = cost;
+      p.tps = tps;
+    }
+  }
+  p.nsplit = (p.ntiles + p.tps - 1) / p.tps;
+  return true;
+}
+
+template <int NP>
+int launch_tc_t(ebc_ctx* ctx, const TcPlan& p, const int* level_now, int level) {
+  auto kern = k_screen_tc<NP>;
+  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
+  dim3 grid(p.ncb, p.nsplit);
+  kern<<<grid, tc::THREADS, p.smem, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->d, ctx->Vhi, ctx->Vlo, ctx->pttc,
+                                                   ctx->nv32, ctx->kpad, tc::stages_for(ctx->kpad, ctx->tc_np), ctx->c0,
+                                                   p.ntiles, p.tps, (double*)ctx->part_g.p, (float*)ctx->part_e.p,
+                                                   ctx->n_pad, ctx->tc_kc, level_now, level);
+  KCHECK();
+  return EBC_OK;
+}
+
+int launch_tc(ebc_ctx* ctx, const TcPlan& p, const int* level_now, int level) {
+  if (ctx->tc_np == 64) return launch_tc_t<64>(ctx, p, level_now, level);
+  return launch_tc_t<32>(ctx, p, level_now, level);
+}
+
 // fp32 screen of the candidate range + certified window.
-// Modes: direct form; Gram form (v.c on the FMA pipe, 2x fewer instructions);
-// adaptive = Gram, then the direct pass only if the Gram window came out wider
-// than ctx->wcap (clustered data: the Gram bound scales with |v|^2 + |c|^2, the
-// direct one with cm), sticky for the rest of the run.
+// Modes: 0 direct form; 1 FFMA Gram form (v.c on the FMA pipe); 2 adaptive
+// ladder FFMA Gram -> direct; 3 adaptive ladder tensor-core Gram -> FFMA Gram
+// -> direct.  A rung whose window comes out wider than ctx->wcap hands the step
+// (and the rest of the run) to the next rung: the Gram bounds scale with
+// |v|^2 + |c|^2, the direct one with cm, so clustered data walks down the ladder.
 // Returns EBC_EINVAL (nothing launched) when no screen tile fits this d.
 int run_screen_window(ebc_ctx* ctx, int eb, int fin_blocks) {
   ScreenPlan p;
   int rc = plan_screen(ctx, p);
   if (rc) return rc;
-  rc = ensure(ctx, ctx->part_g, (size_t)p.nsplit * ctx->n_pad * sizeof(double));
+  TcPlan tp{};
+  const bool use_tc = ctx->screen_mode == 3 && plan_tc(ctx, tp);
+  const int nsplit_max = std::max(p.nsplit, use_tc ? tp.nsplit : 0);
+  rc = ensure(ctx, ctx->part_g, (size_t)nsplit_max * ctx->n_pad * sizeof(double));
   if (rc) return rc;
-  rc = ensure(ctx, ctx->part_e, (size_t)p.nsplit * ctx->n_pad * sizeof(float));
+  rc = ensure(ctx, ctx->part_e, (size_t)nsplit_max * ctx->n_pad * sizeof(float));
   if (rc) return rc;
   if (ctx->timing) CU(cudaEventRecord(ctx->ev[eb + 0], ctx->stream));
   // lower bounds are clamped at 0 (every gain is a sum of max(0, .) terms), so
   // key 0 (= +0.0) is a valid neutral element for the max
   CU(cudaMemsetAsync(ctx->maxlb, 0, sizeof(long long), ctx->stream));
+  const double nterms_ffma = (double)p.tps * p.tp * 8 * 2;
   if (ctx->screen_mode == 0) {
-    rc = launch_screen<false>(ctx, p, nullptr, nullptr);
-    if (!rc) rc = run_finalize_window(ctx, p, fin_blocks, 1.0, nullptr, nullptr);
+    rc = launch_screen<false>(ctx, p, nullptr, 0);
+    if (!rc) rc = run_finalize_window(ctx, p.nsplit, nterms_ffma, p.tp, fin_blocks, 1.0, nullptr, 0);
   } else if (ctx->screen_mode == 1) {
-    rc = launch_screen<true>(ctx, p, nullptr, nullptr);
-    if (!rc) rc = run_finalize_window(ctx, p, fin_blocks, 2.0, nullptr, nullptr);
+    rc = launch_screen<true>(ctx, p, nullptr, 0);
+    if (!rc) rc = run_finalize_window(ctx, p.nsplit, nterms_ffma, p.tp, fin_blocks, 2.0, nullptr, 0);
   } else {
-    rc = launch_screen<true>(ctx, p, ctx->sticky, nullptr);
-    if (!rc) rc = run_finalize_window(ctx, p, fin_blocks, 2.0, ctx->sticky, nullptr);
-    if (!rc) {
-      k_adapt<<<1, 32, 0, ctx->stream>>>(ctx->wcount, ctx->maxlb, ctx->wcap, ctx->sticky, ctx->gate);
-      KCHECK();
-      rc = launch_screen<false>(ctx, p, nullptr, ctx->gate);
+    if (use_tc) {
+      rc = launch_tc(ctx, tp, ctx->level, 0);
+      if (!rc) rc = run_finalize_window(ctx, tp.nsplit, (double)tp.tps * ctx->tc_np, 32, fin_blocks, 2.0,
+                                        ctx->level, 0);
+      if (!rc) {
+        k_adapt<<<1, 32, 0, ctx->stream>>>(ctx->wcount, ctx->maxlb, ctx->wcap, ctx->level, 0);
+        KCHECK();
+      }
     }
-    if (!rc) rc = run_finalize_window(ctx, p, fin_blocks, 1.0, nullptr, ctx->gate);
+    if (!rc) rc = launch_screen<true>(ctx, p, ctx->level, 1);
+    if (!rc) rc = run_finalize_window(ctx, p.nsplit, nterms_ffma, p.tp, fin_blocks, 2.0, ctx->level, 1);
+    if (!rc) {
+      k_adapt<<<1, 32, 0, ctx->stream>>>(ctx->wcount, ctx->maxlb, ctx->wcap, ctx->level, 1);
+      KCHECK();
+      rc = launch_screen<false>(ctx, p, ctx->level, 2);
+    }
+    if (!rc) rc = run_finalize_window(ctx, p.nsplit, nterms_ffma, p.tp, fin_blocks, 1.0, ctx->level, 2);
   }
   if (rc) return rc;
   if (ctx->timing) CU(cudaEventRecord(ctx->ev[eb + 1], ctx->stream));
@@ -323,7 +390,7 @@ int run_step_select(ebc_ctx* ctx, int step, int commit, int64_t* sel_dev) {
   if (rc) return rc;
   k_pick<<<1, 1024, 0, ctx->stream>>>(ctx->wcount, ctx->wlist, ng, (double*)ctx->part_r.p,
                                       1.0 / (double)ctx->n, ctx->cur, ctx->wgain, ctx->best, commit, step,
-                                      ctx->selected, sel_dev);
+                                      ctx->selected, sel_dev, ctx->stats, ctx->level);
   KCHECK();
   if (ctx->timing) CU(cudaEventRecord(ctx->ev[eb + 2], ctx->stream));
   return EBC_OK;
@@ -335,12 +402,12 @@ int run_update(ebc_ctx* ctx, int step, double* val_dev, double* gain_dev) {
   if (ctx->dtype == EBC_F64) {
     CU(cudaFuncSetAttribute(k_update<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024));
     k_update<double><<<ctx->nchunks, RED_THREADS, smem, ctx->stream>>>(
-        ctx->V64, ctx->pitch, ctx->n, ctx->d, ctx->best, ctx->pk, ctx->e0d, ctx->nv32, ctx->cm64, ctx->pt, ctx->chunkpart,
+        ctx->V64, ctx->pitch, ctx->n, ctx->d, ctx->best, ctx->pk, ctx->e0d, ctx->nv32, ctx->cm64, ctx->pt, ctx->pttc, ctx->tc_ka, ctx->tc_kb, ctx->chunkpart,
         ctx->counter, 1.0 / (double)ctx->n, ctx->cur, val_dev, gain_dev, step);
   } else {
     CU(cudaFuncSetAttribute(k_update<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024));
     k_update<float><<<ctx->nchunks, RED_THREADS, smem, ctx->stream>>>(
-        ctx->V32, ctx->pitch, ctx->n, ctx->d, ctx->best, ctx->pk, ctx->e0d, ctx->nv32, ctx->cm64, ctx->pt, ctx->chunkpart,
+        ctx->V32, ctx->pitch, ctx->n, ctx->d, ctx->best, ctx->pk, ctx->e0d, ctx->nv32, ctx->cm64, ctx->pt, ctx->pttc, ctx->tc_ka, ctx->tc_kb, ctx->chunkpart,
         ctx->counter, 1.0 / (double)ctx->n, ctx->cur, val_dev, gain_dev, step);
   }
   KCHECK();
@@ -359,8 +426,15 @@ int ensure_events(ebc_ctx* ctx, size_t count) {
 
 int do_reset(ebc_ctx* ctx) {
   const int blocks = (int)((ctx->n + 255) / 256);
+  CU(cudaMemsetAsync(ctx->stats, 0, 4 * sizeof(long long), ctx->stream));
   k_reset<<<blocks, 256, 0, ctx->stream>>>(ctx->n, ctx->e0d, ctx->nv32, ctx->pk, ctx->cm64, ctx->pt, ctx->selected,
-                                           ctx->sticky);
+                                           nullptr, ctx->pttc, ctx->tc_ka, ctx->tc_kb);
+  KCHECK();
+  {
+    // first rung of the adaptive ladder for this run
+    const int start = (ctx->screen_mode == 3 && ctx->tc_np) ? 0 : 1;
+    k_set_int<<<1, 1, 0, ctx->stream>>>(ctx->level, start);
+  }
   KCHECK();
   CU(cudaMemsetAsync(ctx->cur, 0, sizeof(double), ctx->stream));
   ctx->steps_done = 0;
@@ -370,7 +444,7 @@ int do_reset(ebc_ctx* ctx) {
 void free_ctx(ebc_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
-  void* ptrs[] = {c->V32, c->V64, c->e0d, c->cm64, c->pt, c->nv32, c->sticky, c->gate, c->selected, c->chunkpart, c->counter, c->cur, c->best,
+  void* ptrs[] = {c->V32, c->V64, c->e0d, c->cm64, c->pt, c->nv32, c->level, c->stats, c->Vhi, c->Vlo, c->pttc, c->selected, c->chunkpart, c->counter, c->cur, c->best,
                   c->maxlb, c->wcount, c->wlist, c->wgain, c->ub};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -434,7 +508,7 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
     ctx->pk.gram_k = (float)(0.5 * (d + 4) * u * (1.0 + 1.0 / 512));
     ctx->gram_kc = (float)(1.5 * (d + 4) * u * (1.0 + 1.0 / 512));
     ctx->wcap = (int)std::max<int64_t>(256, n / 64);
-    ctx->screen_mode = d >= 24 ? 2 : 0;
+    ctx->screen_mode = d >= 24 ? 3 : 0;
     const char* m = getenv("EBC200_SCREEN_MODE");
     if (m && m[0]) ctx->screen_mode = atoi(m);
   }
@@ -489,10 +563,33 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
   CUC(cudaMemsetAsync(ctx->pt, 0, (size_t)ctx->n_pad * sizeof(float4), ctx->stream));
   CUC(cudaMalloc(&ctx->nv32, (size_t)ctx->n_pad * sizeof(float)));
   CUC(cudaMemsetAsync(ctx->nv32, 0, (size_t)ctx->n_pad * sizeof(float), ctx->stream));
-  CUC(cudaMalloc(&ctx->sticky, sizeof(int)));
-  CUC(cudaMemsetAsync(ctx->sticky, 0, sizeof(int), ctx->stream));
-  CUC(cudaMalloc(&ctx->gate, sizeof(int)));
-  CUC(cudaMemsetAsync(ctx->gate, 0, sizeof(int), ctx->stream));
+  CUC(cudaMalloc(&ctx->stats, 4 * sizeof(long long)));
+  CUC(cudaMemsetAsync(ctx->stats, 0, 4 * sizeof(long long), ctx->stream));
+  CUC(cudaMalloc(&ctx->level, sizeof(int)));
+  CUC(cudaMemsetAsync(ctx->level, 0, sizeof(int), ctx->stream));
+  // tensor-core screen: fp32-path grounds whose 128-candidate tile of hi+lo
+  // operands plus a 2-stage ring of NP-point tiles fits shared memory
+  if (dtype != EBC_F64 && ctx->screen_mode == 3) {
+    ctx->kpad = (d + 7) / 8 * 8;
+    for (int np : {64, 32}) {
+      if (ctx->kpad <= 128 && tc::stages_for(ctx->kpad, np) >= 2) {
+        ctx->tc_np = np;
+        break;
+      }
+    }
+    if (ctx->tc_np) {
+      const double u = 5.960464477539063e-08;
+      const double ktc = 3.0 * std::ldexp(1.0, -20) + (3.0 * ctx->kpad + 16.0) * std::ldexp(1.0, -23);
+      ctx->tc_ka = (float)(4.0 * u * 1.01);
+      ctx->tc_kb = (float)((4.0 * u + 0.5 * ktc) * 1.01);
+      ctx->tc_kc = (float)((4.0 * u + 0.5 * ktc) * 1.01);
+      const size_t ve = (size_t)ctx->n_pad * ctx->kpad;
+      CUC(cudaMalloc(&ctx->Vhi, ve * sizeof(float)));
+      CUC(cudaMalloc(&ctx->Vlo, ve * sizeof(float)));
+      CUC(cudaMalloc(&ctx->pttc, (size_t)ctx->n_pad * sizeof(float2)));
+      CUC(cudaMemsetAsync(ctx->pttc, 0, (size_t)ctx->n_pad * sizeof(float2), ctx->stream));
+    }
+  }
   CUC(cudaMalloc(&ctx->selected, (size_t)ctx->n_pad));
   CUC(cudaMemsetAsync(ctx->selected, 0, (size_t)ctx->n_pad, ctx->stream));
   CUC(cudaMalloc(&ctx->chunkpart, (size_t)ctx->nchunks * sizeof(double)));
@@ -520,11 +617,18 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
   }
   if (dtype == EBC_F64)
     k_init<double><<<ctx->nchunks, RED_THREADS, 0, ctx->stream>>>(ctx->V64, ctx->pitch, n, d, e0dev, ctx->pk,
-                                                                 ctx->e0d, ctx->cm64, ctx->nv32, ctx->pt, ctx->chunkpart);
+                                                                 ctx->e0d, ctx->cm64, ctx->nv32, ctx->pt, ctx->chunkpart,
+                                                                 nullptr, 0.f, 0.f);
   else
     k_init<float><<<ctx->nchunks, RED_THREADS, 0, ctx->stream>>>(ctx->V32, ctx->pitch, n, d, e0dev, ctx->pk,
-                                                                ctx->e0d, ctx->cm64, ctx->nv32, ctx->pt, ctx->chunkpart);
+                                                                ctx->e0d, ctx->cm64, ctx->nv32, ctx->pt, ctx->chunkpart,
+                                                                ctx->pttc, ctx->tc_ka, ctx->tc_kb);
   CUC(cudaGetLastError());
+  if (ctx->tc_np) {
+    k_split_tf32<<<8 * ctx->num_sms, 256, 0, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->n_pad, d, ctx->kpad,
+                                                           ctx->Vhi, ctx->Vlo);
+    CUC(cudaGetLastError());
+  }
   double* bl = nullptr;
   CUC(cudaMalloc(&bl, sizeof(double)));
   k_total<<<1, 32, 0, ctx->stream>>>(ctx->chunkpart, ctx->nchunks, 1.0 / (double)n, bl);
@@ -571,6 +675,15 @@ int ebc_last_timings(const ebc_ctx* ctx, double* out_ms4) {
 }
 
 int64_t ebc_last_launches(const ebc_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+int ebc_last_stats(const ebc_ctx* ctx, int64_t* out4) {
+  if (!ctx || !out4) return fail(nullptr, EBC_EINVAL, "ebc_last_stats: NULL argument");
+  long long v[4];
+  if (cudaMemcpy(v, ctx->stats, sizeof(v), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return fail(const_cast<ebc_ctx*>(ctx), EBC_ECUDA, "ebc_last_stats: copy failed");
+  for (int i = 0; i < 4; ++i) out4[i] = v[i];
+  return EBC_OK;
+}
 
 int ebc_greedy(ebc_ctx* ctx, int32_t k, int64_t* out_sel, double* out_val, double* out_gain, int64_t* out_evals) {
   if (!ctx) return fail(nullptr, EBC_EINVAL, "ebc_greedy: NULL context");

@@ -116,7 +116,8 @@ __global__ void __launch_bounds__(RED_THREADS) k_init(const T* __restrict__ V, i
                                                       const double* __restrict__ e0, PtCoef pk,
                                                       double* __restrict__ e0d, double* __restrict__ cm64,
                                                       float* __restrict__ nv32, float4* __restrict__ pt,
-                                                      double* __restrict__ part) {
+                                                      double* __restrict__ part, float2* __restrict__ pttc,
+                                                      float tc_ka, float tc_kb) {
   __shared__ double sbuf[RED_THREADS];
   __shared__ double se0[1024];
   for (int k = threadIdx.x; k < d && k < 1024; k += blockDim.x) se0[k] = e0[k];
@@ -137,6 +138,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_init(const T* __restrict__ V, i
       const float n32 = (float)nv;
       nv32[v] = n32;
       pt[v] = make_pt((float)t, n32, pk);
+      if (pttc) pttc[v] = make_float2(((float)t - n32) * 0.5f, tc_ka * (float)t + tc_kb * n32);
       acc += t;
     }
   }
@@ -147,15 +149,20 @@ __global__ void __launch_bounds__(RED_THREADS) k_init(const T* __restrict__ V, i
 // Reset the cached minima to d(., e0) (ebc_reset / start of a Greedy run).
 __global__ void k_reset(int64_t n, const double* __restrict__ e0d, const float* __restrict__ nv32, PtCoef pk,
                         double* __restrict__ cm64, float4* __restrict__ pt, unsigned char* __restrict__ selected,
-                        int* __restrict__ sticky) {
+                        int* __restrict__ sticky, float2* __restrict__ pttc, float tc_ka, float tc_kb) {
   int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (v == 0 && sticky) *sticky = 0;
   if (v < n) {
     double t = e0d[v];
     cm64[v] = t;
     pt[v] = make_pt((float)t, nv32[v], pk);
+    if (pttc) pttc[v] = make_float2(((float)t - nv32[v]) * 0.5f, tc_ka * (float)t + tc_kb * nv32[v]);
     selected[v] = 0;
   }
+}
+
+__global__ void k_set_int(int* __restrict__ p, int v) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) *p = v;
 }
 
 __global__ void k_total(const double* __restrict__ part, int nchunks, double scale, double* __restrict__ out) {
@@ -226,10 +233,8 @@ template <class Cfg, bool GRAM, int PITCH>
 __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
     k_screen(const float* __restrict__ V, const float4* __restrict__ pt, int pitch_rt, int d4, int64_t cand0,
              int ntiles, int tiles_per_split, double* __restrict__ part_g, float* __restrict__ part_e,
-             int64_t part_stride, float gram_kc, const int* __restrict__ skip_if_set,
-             const int* __restrict__ run_if_set) {
-  if (skip_if_set && *skip_if_set) return;  // adaptive mode: Gram pass skipped (sticky direct)
-  if (run_if_set && !*run_if_set) return;   // adaptive mode: direct pass not needed
+             int64_t part_stride, float gram_kc, const int* __restrict__ level_now, int level) {
+  if (level_now && *level_now != level) return;  // adaptive screen: not this level's turn
   // PITCH != 0: compile-time row pitch -> every LDS address is base + immediate
   const int pitch = PITCH ? PITCH : pitch_rt;
   constexpr int TP = Cfg::TP, TC = Cfg::TC, LR = Cfg::LR, LC = Cfg::LC, WP = Cfg::WP;
@@ -486,10 +491,8 @@ using ScreenB = ScreenCfg<8, 2, 4, 3, 1>;
 __global__ void k_finalize(int64_t c0, int64_t c1, int nsplit, const double* __restrict__ part_g,
                            const float* __restrict__ part_e, int64_t part_stride, double einfl, double gcoef,
                            double gscale, const unsigned char* __restrict__ selected, double* __restrict__ ub,
-                           long long* __restrict__ maxlb, const int* __restrict__ skip_if_set,
-                           const int* __restrict__ run_if_set) {
-  if (skip_if_set && *skip_if_set) return;
-  if (run_if_set && !*run_if_set) return;
+                           long long* __restrict__ maxlb, const int* __restrict__ level_now, int level) {
+  if (level_now && *level_now != level) return;
   __shared__ long long smax[256];
   const int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   long long key = dkey(-INFINITY);
@@ -522,9 +525,8 @@ __global__ void k_finalize(int64_t c0, int64_t c1, int nsplit, const double* __r
 // exact value and lowest index).
 __global__ void k_window(int64_t c0, int64_t c1, const double* __restrict__ ub, const long long* __restrict__ maxlb,
                          double margin, int* __restrict__ wcount, int64_t* __restrict__ wlist,
-                         const int* __restrict__ skip_if_set, const int* __restrict__ run_if_set) {
-  if (skip_if_set && *skip_if_set) return;
-  if (run_if_set && !*run_if_set) return;
+                         const int* __restrict__ level_now, int level) {
+  if (level_now && *level_now != level) return;
   const int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c < c1) {
     const double thr = dkey_inv(*maxlb) - margin;
@@ -536,18 +538,17 @@ __global__ void k_window(int64_t c0, int64_t c1, const double* __restrict__ ub, 
   }
 }
 
-// Adaptive screen: after the Gram pass, decide whether the direct pass must
-// run (window larger than `cap`, or direct already sticky for this run).
-__global__ void k_adapt(int* __restrict__ wcount, long long* __restrict__ maxlb, int cap, int* __restrict__ sticky,
-                        int* __restrict__ gate) {
+// Adaptive screen: the screens form a ladder of decreasing speed and
+// increasing precision (0 tensor-core Gram, 1 FFMA Gram, 2 direct).  After the
+// pass of `level`, a window wider than `cap` moves the run to level + 1 for the
+// rest of the run and clears the window state for the next pass.
+__global__ void k_adapt(int* __restrict__ wcount, long long* __restrict__ maxlb, int cap, int* __restrict__ level_now,
+                        int level) {
   if (threadIdx.x == 0 && blockIdx.x == 0) {
-    if (*sticky || *wcount > cap) {
-      *sticky = 1;
-      *gate = 1;
+    if (*level_now == level && *wcount > cap) {
+      *level_now = level + 1;
       *wcount = 0;
       *maxlb = 0;
-    } else {
-      *gate = 0;
     }
   }
 }
@@ -660,7 +661,8 @@ __global__ void __launch_bounds__(1024) k_pick(const int* __restrict__ wcount, c
                                                int ng, const double* __restrict__ part_r, double inv_n,
                                                const double* __restrict__ cur, double* __restrict__ wgain,
                                                int64_t* __restrict__ best, int commit, int step,
-                                               unsigned char* __restrict__ selected, int64_t* __restrict__ sel_out) {
+                                               unsigned char* __restrict__ selected, int64_t* __restrict__ sel_out,
+                                               long long* __restrict__ stats, const int* __restrict__ level_now) {
   __shared__ double smax[1024];
   __shared__ long long smin[1024];
   const int wc = *wcount;
@@ -694,6 +696,12 @@ __global__ void __launch_bounds__(1024) k_pick(const int* __restrict__ wcount, c
   if (threadIdx.x == 0) {
     const long long b = smin[0] == LLONG_MAX ? -1 : smin[0];
     *best = b;
+    if (stats) {  // [0] sum of window sizes, [1] max window, [2] screen rung, [3] steps
+      stats[0] += wc;
+      stats[1] = max(stats[1], (long long)wc);
+      stats[2] = level_now ? *level_now : -1;
+      stats[3] += 1;
+    }
     if (commit && b >= 0) {
       selected[b] = 1;
       sel_out[step] = b;
@@ -710,6 +718,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_update(const T* __restrict__ V,
                                                         const int64_t* __restrict__ best, PtCoef pk,
                                                         const double* __restrict__ e0d, const float* __restrict__ nv32,
                                                         double* __restrict__ cm64, float4* __restrict__ pt,
+                                                        float2* __restrict__ pttc, float tc_ka, float tc_kb,
                                                         double* __restrict__ fpart,
                                                         unsigned int* __restrict__ counter, double inv_n,
                                                         double* __restrict__ cur, double* __restrict__ val_out,
@@ -731,6 +740,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_update(const T* __restrict__ V,
         m = t;
         cm64[v] = m;
         pt[v] = make_pt((float)m, nv32[v], pk);
+        if (pttc) pttc[v] = make_float2(((float)m - nv32[v]) * 0.5f, tc_ka * (float)m + tc_kb * nv32[v]);
       }
       acc += e0d[v] - m;
     }

@@ -1,0 +1,329 @@
+// screen_tc.cuh -- tcgen05 (5th-gen tensor core) Gram-form candidate screen.
+//
+// Same contract as k_screen<Cfg, GRAM=true> (kernels.cuh): for a tile of 128
+// candidates, accumulate over all points gain/2 = sum_v max(0, t/2) with
+// t/2 = (cm - |v|^2 - |c|^2)/2 + v.c, plus a certified error bound -- but the
+// dot products v.c come from tcgen05.mma (kind::tf32) instead of FFMA:
+//
+//   v.c ~= hi(v).hi(c) + hi(v).lo(c) + lo(v).hi(c)      ("3xTF32")
+//
+// with hi = x truncated to TF32 and lo = x - hi, so every product carries
+// ~2^-20 relative error and the fp32 accumulation in TMEM adds at most
+// (3 Kpad + 16) 2^-23 relative to sum |v_k c_k| (DESIGN.md §4 "tensor screen").
+//
+// CTA = 6 warps:  warp 0 = bulk-copy producer + TMEM allocator,
+//                 warp 1 = MMA issuer (one elected lane),
+//                 warps 2..5 = epilogue, one candidate per thread (= TMEM lane).
+// Operands are staged by the bulk-copy engine straight from pre-split,
+// UMMA-canonical copies of V (K-major, no swizzle: 8-row x 16-byte core
+// matrices, LBO = 128 B between K chunks, SBO = Kpad*32 B between row groups),
+// so no thread touches operand data.  Accumulators: 2 TMEM buffers of NP
+// columns (M = 128 lanes = candidates, N = NP points), double-buffered against
+// the epilogue; V tiles: 2-stage smem ring.
+#pragma once
+#include <cstdint>
+
+#include "ptx.cuh"
+
+namespace ebc {
+namespace tc {
+
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// smem matrix descriptor: K-major, SWIZZLE_NONE, version 1 (sm_100)
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // version
+  return d;                // base_offset 0, lbo_mode 0, layout SWIZZLE_NONE (0)
+}
+
+// instruction descriptor: kind::tf32, D fp32, A/B tf32, both K-major
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, {%5, %6, %7, %8}, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc), "r"(0), "r"(0), "r"(0), "r"(0)
+      : "memory");
+}
+
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "elect.sync _|P1, 0xffffffff;\n\t"
+      "selp.b32 %0, 1, 0, P1;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
+__device__ __forceinline__ void commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr)
+      : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+constexpr int M = 128;        // candidates per CTA (UMMA M)
+constexpr int THREADS = 192;  // 6 warps
+constexpr int MAX_STAGES = 4;
+// TMEM columns: A_hi [0,128), A_lo [128,256), accumulators [256 + b*NP, ...)
+constexpr uint32_t COL_AHI = 0, COL_ALO = 128, COL_ACC = 256, TMEM_COLS = 512;
+
+__device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc,
+                                            uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, {%5, %6, %7, %8}, p;\n\t}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc), "r"(0), "r"(0), "r"(0), "r"(0)
+      : "memory");
+}
+
+// The three 3xTF32 products of one K step in a single asm block: hi.hi (sets
+// or accumulates), hi.lo, lo.hi.  One statement = one issue sequence.
+__device__ __forceinline__ void mma3_tf32_ts(uint32_t tmem_d, uint32_t a_hi, uint32_t a_lo, uint64_t b_hi,
+                                             uint64_t b_lo, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "setp.eq.b32 q, %6, %6;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %3, %5, {%7, %7, %7, %7}, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %4, %5, {%7, %7, %7, %7}, q;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2], %3, %5, {%7, %7, %7, %7}, q;\n\t}\n" ::"r"(tmem_d),
+      "r"(a_hi), "r"(a_lo), "l"(b_hi), "l"(b_lo), "r"(idesc), "r"(acc), "r"(0)
+      : "memory");
+}
+
+__device__ __forceinline__ void st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+      "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]),
+      "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]),
+      "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+
+inline int stages_for(int kpad, int np) {
+  const size_t stage = 2 * (size_t)np * kpad * 4;
+  const size_t budget = 220 * 1024;
+  int st = (int)(budget / stage);
+  return st > MAX_STAGES ? MAX_STAGES : st;
+}
+
+inline size_t smem_bytes(int kpad, int np) {
+  const size_t stage = 2 * (size_t)np * kpad * 4;  // B_hi, B_lo
+  return stages_for(kpad, np) * stage + 4 * MAX_STAGES * sizeof(uint64_t) + 64;
+}
+
+}  // namespace tc
+
+// Split V into TF32 hi/lo parts in the UMMA canonical K-major blocked layout:
+// element (v, k) at ((v/8 * KC + k/4) * 8 + v%8) * 4 + k%4, KC = kpad/4.
+__global__ void k_split_tf32(const float* __restrict__ V32, int pitch, int64_t nrows, int d, int kpad,
+                             float* __restrict__ hi, float* __restrict__ lo) {
+  const int KC = kpad / 4;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t total = nrows * kpad;
+  for (; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = i / kpad;
+    const int k = (int)(i - v * kpad);
+    const float x = k < d ? V32[v * pitch + k] : 0.f;
+    const float h = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+    const float l = x - h;  // exact
+    const int64_t off = (((v >> 3) * KC + (k >> 2)) * 8 + (v & 7)) * 4 + (k & 3);
+    hi[off] = h;
+    lo[off] = l;
+  }
+}
+
+// One CTA: candidates [cand0 + 128*bx, +128) x V tiles [t0, t1) of NP points.
+// A (candidates, hi and lo) lives in TMEM for the CTA's life (MMA "TS" form:
+// the tensor core reads only the B tiles from shared memory); B tiles stream
+// through a STAGES-deep bulk-copy ring released by the MMA commit alone; the
+// per-point seed/quantum {ip, kp} is read by the epilogue through L1.
+template <int NP>
+__global__ void __launch_bounds__(tc::THREADS, 1)
+    k_screen_tc(const float* __restrict__ V32, int pitch, int d, const float* __restrict__ Vhi,
+                const float* __restrict__ Vlo, const float2* __restrict__ pttc, const float* __restrict__ nv32,
+                int kpad, int stages, int64_t cand0, int ntiles, int tiles_per_split, double* __restrict__ part_g,
+                float* __restrict__ part_e, int64_t part_stride, float kc_coef, const int* __restrict__ level_now,
+                int level) {
+  using namespace tc;
+  if (level_now && *level_now != level) return;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t b_bytes = (uint32_t)NP * kpad * 4;
+  const uint32_t stage_bytes = 2 * b_bytes;
+  unsigned char* stage0 = smem;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)stages * stage_bytes);
+  uint64_t* full = bars;                   // [stages] operands landed
+  uint64_t* sempty = bars + MAX_STAGES;    // [stages] operands consumed (MMA commit)
+  uint64_t* tfull = bars + 2 * MAX_STAGES;       // [2] accumulator ready
+  uint64_t* tempty = bars + 2 * MAX_STAGES + 2;  // [2] accumulator drained (128 epilogue threads)
+  uint64_t* aready = bars + 2 * MAX_STAGES + 4;  // A written to TMEM (128 epilogue threads)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * MAX_STAGES + 5);
+
+  const int t0 = blockIdx.y * tiles_per_split;
+  const int t1 = min(ntiles, t0 + tiles_per_split);
+  const int nt = t1 - t0;
+  const int64_t crow = cand0 + (int64_t)blockIdx.x * M;
+
+  if (tid == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&sempty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 128);
+    }
+    mbar_init(aready, 128);
+    fence_mbar_init();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- producer
+    if (lane == 0) {
+      for (int it = 0; it < nt; ++it) {
+        const int s = it % stages;
+        if (it >= stages) mbar_wait(&sempty[s], ((it / stages) - 1) & 1);
+        unsigned char* st = stage0 + s * stage_bytes;
+        const int64_t prow = (int64_t)(t0 + it) * NP;
+        mbar_arrive_expect_tx(&full[s], stage_bytes);
+        bulk_g2s(st, Vhi + prow * kpad, b_bytes, &full[s]);
+        bulk_g2s(st + b_bytes, Vlo + prow * kpad, b_bytes, &full[s]);
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer: the whole warp walks the loop (warp-uniform
+    // operands stay in uniform registers), one elected lane issues
+    constexpr uint32_t idesc = idesc_tf32(M, NP);
+    const uint32_t sbo = (uint32_t)kpad * 32;  // 8 rows x kpad floats
+    const int ksteps = kpad / 8;
+    mbar_wait(aready, 0);
+    fence_after();
+    for (int it = 0; it < nt; ++it) {
+      const int s = it % stages, b = it & 1;
+      mbar_wait(&full[s], (it / stages) & 1);
+      if (it >= 2) mbar_wait(&tempty[b], ((it >> 1) - 1) & 1);
+      fence_after();
+      const uint32_t bhi = smem_u32(stage0 + s * stage_bytes);
+      const uint32_t dt = tmem + COL_ACC + (uint32_t)(b * NP);
+      // descriptors built once per tile; K step j advances the start-address
+      // field by 256 B (= 16 in 16-byte units) and A by 8 TMEM columns
+      const uint64_t dhi = sdesc(bhi, 128, sbo);
+      const uint64_t dlo = sdesc(bhi + b_bytes, 128, sbo);
+      const uint32_t ahi = tmem + COL_AHI, alo = tmem + COL_ALO;
+      if (elect_one()) {
+#pragma unroll 4
+        for (int j = 0; j < ksteps; ++j) {
+          mma3_tf32_ts(dt, ahi + 8 * j, alo + 8 * j, dhi + 16 * j, dlo + 16 * j, idesc, j > 0);
+        }
+        commit(&sempty[s]);  // operands consumed -> producer may refill
+        commit(&tfull[b]);   // accumulator ready for the epilogue
+      }
+      __syncwarp();
+    }
+  } else {
+    // ---------------- epilogue: thread = candidate = TMEM lane
+    const int q = warp & 3;  // TMEM lane quadrant of this warp
+    const int cl = q * 32 + lane;
+    const int64_t c = crow + cl;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    {
+      // A_hi / A_lo of this candidate into TMEM columns [0,128) / [128,256)
+      const float* row = V32 + c * pitch;
+#pragma unroll 1
+      for (int blk = 0; blk < 4; ++blk) {
+        uint32_t rh[32], rl[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int k = blk * 32 + i;
+          const float x = k < d ? row[k] : 0.f;
+          const uint32_t h = __float_as_uint(x) & 0xFFFFE000u;
+          rh[i] = h;
+          rl[i] = __float_as_uint(x - __uint_as_float(h));
+        }
+        st32(tmem + lane_off + COL_AHI + blk * 32, rh);
+        st32(tmem + lane_off + COL_ALO + blk * 32, rl);
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      fence_before();
+      mbar_arrive(aready);
+    }
+    const float nc = nv32[c];
+    const float ic = -0.5f * nc;
+    const float kc = kc_coef * nc;
+    double g64 = 0.0;
+    float e = 0.f, cnt = 0.f;
+    for (int it = 0; it < nt; ++it) {
+      const int b = it & 1;
+      const float2* pp = pttc + (int64_t)(t0 + it) * NP;
+      mbar_wait(&tfull[b], (it >> 1) & 1);
+      fence_after();
+#pragma unroll
+      for (int h = 0; h < NP / 32; ++h) {
+        float S[32];
+        ld32(tmem + lane_off + COL_ACC + (uint32_t)(b * NP + h * 32), S);
+        if (h == NP / 32 - 1) {
+          fence_before();
+          mbar_arrive(&tempty[b]);  // all columns of this buffer are in registers
+        }
+        float g = 0.f;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const float2 p = __ldg(pp + h * 32 + i);  // broadcast through L1
+          const float acc = (p.x + ic) + S[i];
+          g += fmaxf(acc, 0.f);
+          const float f = (acc + p.y > -kc) ? 1.f : 0.f;
+          e = fmaf(f, p.y, e);
+          cnt += f;
+        }
+        g64 += (double)g;
+      }
+    }
+    e = fmaf(kc, cnt, e);
+    part_g[blockIdx.y * part_stride + c] = g64;
+    part_e[blockIdx.y * part_stride + c] = e;
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+}
+
+}  // namespace ebc

@@ -101,6 +101,14 @@ def last_timings(f: EbcFunction):
     return tuple(float(x) for x in out)
 
 
+def last_stats(f: EbcFunction):
+    """(sum of window sizes, max window, screen rung at the end, steps) of the last run."""
+    out = np.zeros(4, dtype=np.int64)
+    _native.check(f._lib.ebc_last_stats(f.native_context, out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))),
+                  f.native_context)
+    return tuple(int(x) for x in out)
+
+
 def last_launches(f: EbcFunction) -> int:
     return int(f._lib.ebc_last_launches(f.native_context))
 

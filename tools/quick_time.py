@@ -21,7 +21,7 @@ def run(name, n, d, k, prec=eb.Precision.FP32, gen="gaussian"):
     peak = 148 * 128 * 1.965e9
     print(f"{name}: n={n} d={d} k={k} total {t[3]:.2f} ms screen {t[0]:.2f} refine {t[1]:.2f} update {t[2]:.2f}"
           f" | screen {ops / (t[0] * 1e-3) / peak:.3f} of FMA peak, whole {ops / (t[3] * 1e-3) / peak:.3f}"
-          f" evals/s {pairs / (t[3] * 1e-3):.3e} launches {optimize.last_launches(f)} sel {s.selected[:5]}")
+          f" evals/s {pairs / (t[3] * 1e-3):.3e} launches {optimize.last_launches(f)} stats {optimize.last_stats(f)} sel {s.selected[:3]}")
     optimize.set_timing(f, False)
     t0 = time.perf_counter(); s2 = eb.greedy_maximize(f, eb.OptimizerBudget(k=k)); t1 = time.perf_counter()
     print(f"   untimed run wall {1e3 * (t1 - t0):.2f} ms, same selection {s2.selected == s.selected}")
