@@ -307,6 +307,7 @@ int launch_tc_t(ebc_ctx* ctx, const TcPlan& p, const int* level_now, int level) 
 }
 
 int launch_tc(ebc_ctx* ctx, const TcPlan& p, const int* level_now, int level) {
+  if (ctx->tc_np == 128) return launch_tc_t<128>(ctx, p, level_now, level);
   if (ctx->tc_np == 64) return launch_tc_t<64>(ctx, p, level_now, level);
   return launch_tc_t<32>(ctx, p, level_now, level);
 }
@@ -571,7 +572,10 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
   // operands plus a 2-stage ring of NP-point tiles fits shared memory
   if (dtype != EBC_F64 && ctx->screen_mode == 3) {
     ctx->kpad = (d + 7) / 8 * 8;
-    for (int np : {64, 32}) {
+    int nps[3] = {128, 64, 32};
+    const char* npenv = getenv("EBC200_TC_NP");
+    if (npenv && npenv[0]) nps[0] = atoi(npenv);
+    for (int np : nps) {
       if (ctx->kpad <= 128 && tc::stages_for(ctx->kpad, np) >= 2) {
         ctx->tc_np = np;
         break;
