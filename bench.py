@@ -127,6 +127,15 @@ def flush_l2(torch, dev):
     buf.fill_(1.0)
 
 
+def load_measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh)
+    except (OSError, ValueError):
+        return None
+
+
 def load_profile_traffic(config: str):
     """dram bytes per launch of k_screen from the committed ncu --set full summary."""
     path = os.path.join(ROOT, "profiles", "screen_ncu_summary.json")
@@ -254,6 +263,7 @@ def run_ours(args):
     clocks = ClockSampler(dev_index)
     clocks.start()
     times_ms, screen_ms, launches = [], [], 0
+    stats = None
     for _ in range(args.steps):
         flush_l2(torch, dev)
         torch.cuda.synchronize(dev)
@@ -270,6 +280,7 @@ def run_ours(args):
             t = optimize.last_timings(f)
             screen_ms.append(t[0])
             launches += optimize.last_launches(f)
+            stats = optimize.last_stats(f)
         if ref_sel is not None and s.selected != ref_sel:
             raise RuntimeError("selection changed between runs")
     clk = clocks.stop()
@@ -326,19 +337,38 @@ def run_ours(args):
         ops = 2.0 * d * E
         achieved = ops / (scr * 1e-3)
         traffic, prof = load_profile_traffic(args.config)
-        line["roofline"] = {
-            "bound": "fma", "kernel": "k_screen (fused distance->min->sum, fp32 FFMA)",
-            "achieved": achieved / 1e12, "peak": PEAK_FP32_OPS / 1e12, "unit": "TFLOP/s",
-            "frac": achieved / PEAK_FP32_OPS,
-            "traffic": traffic,
-            "work": "2d FP32 FMA-pipe ops per point-candidate pair (SURVEY.md §8(d)); k_screen launches of one run "
-                    "summed; peak = 148 SM x 128 lanes x 1.965 GHz (nominal; MEASURED_PEAKS has no FP32 figure)",
-            "flag": ("frac > 1.0: the adaptive screen runs the Gram form (d FFMA per pair, v.c on the FMA pipe) "
-                     "against the direct-form W = 2d; W is not redefined (SURVEY.md §8(d))")
-                    if achieved > PEAK_FP32_OPS else None,
-            "screen_mode": os.environ.get("EBC200_SCREEN_MODE", "auto (Gram, direct fallback)" if d >= 24 else "direct"),
-            "screen_ms_per_step": scr, "screen_share_of_step": scr / step_ms,
-        }
+        rung = stats[2] if stats else -1
+        fma_equiv = {"achieved": achieved / 1e12, "peak": PEAK_FP32_OPS / 1e12, "unit": "TFLOP/s",
+                     "frac": achieved / PEAK_FP32_OPS,
+                     "work": "W = 2d FP32 FMA-pipe ops per point-candidate pair (SURVEY.md §8(d)), not redefined; "
+                             "peak = 148 SM x 128 lanes x 1.965 GHz (nominal)"}
+        if rung == 0:
+            # tensor rung: 3xTF32 products = 3 x 2d flops per pair on tcgen05 kind::tf32; TF32 runs at half
+            # the BF16 rate on sm_100, so the peak is the driver-measured dense BF16 figure / 2
+            peaks = load_measured_peaks()
+            bf16 = peaks.get("bf16_tflops") if peaks else None
+            tpeak = (bf16 / 2.0) if bf16 else 1590.0 / 2.0
+            tach = 6.0 * d * E / (scr * 1e-3) / 1e12
+            line["roofline"] = {
+                "bound": "tensor", "kernel": "k_screen_tc (tcgen05 3xTF32 Gram screen, TMEM epilogue)",
+                "achieved": tach, "peak": tpeak, "unit": "TFLOP/s", "frac": tach / tpeak,
+                "peak_source": ("MEASURED_PEAKS.json bf16_tflops / 2" if bf16 else "fallback 1.59 PF bf16 / 2")
+                               + "; nominal dense TF32 = 1125 TFLOP/s",
+                "traffic": traffic,
+                "work": "6d TF32 flops per point-candidate pair (3 products hi.hi + hi.lo + lo.hi, d not padded)",
+                "fma_equiv": dict(fma_equiv, flag="frac > 1.0 expected: tensor cores vs the FP32 FMA roofline"),
+                "screen_ms_per_step": scr, "screen_share_of_step": scr / step_ms, "screen_rung": rung,
+            }
+        else:
+            line["roofline"] = {
+                "bound": "fma", "kernel": "k_screen (fused distance->min->sum on the FP32 FMA pipe)",
+                "achieved": fma_equiv["achieved"], "peak": fma_equiv["peak"], "unit": "TFLOP/s",
+                "frac": fma_equiv["frac"], "traffic": traffic, "work": fma_equiv["work"],
+                "flag": ("frac > 1.0: the Gram rung issues d FFMA per pair against the direct-form W = 2d"
+                         if achieved > PEAK_FP32_OPS else None),
+                "screen_ms_per_step": scr, "screen_share_of_step": scr / step_ms, "screen_rung": rung,
+            }
+        line["window"] = {"sum": stats[0], "max": stats[1], "steps": stats[3]} if stats else None
         line["gpu_launches"] = int(launches)
         if rank == 0 and not args.no_cpu_baseline:
             threads = len(os.sched_getaffinity(0))
