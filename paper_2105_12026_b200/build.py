@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libebc200.so")
 SOURCES = ["ebc200.cu"]
-HEADERS = ["kernels.cuh", "ptx.cuh", "screen_tc.cuh"]
+HEADERS = ["kernels.cuh", "ptx.cuh", "screen_tc.cuh", "multiset.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

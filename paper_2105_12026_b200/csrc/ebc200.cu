@@ -19,6 +19,10 @@
 #include "../../include/ebc200.h"
 #include "kernels.cuh"
 #include "screen_tc.cuh"
+#include "multiset.cuh"
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_reduce.cuh>
 
 using namespace ebc;
 
@@ -80,6 +84,12 @@ struct ebc_ctx {
   double* wgain = nullptr;   // n
   double* ub = nullptr;      // n
   DevBuf part_g, part_e, part_r, sel_out, val_out, gain_out, ms_part, ms_off, ms_idx, ms_out;
+  // sparse work-matrix path
+  DevBuf ms_mbuf, ms_setof, ms_pairs, ms_keys, ms_vals, ms_keys2, ms_vals2, ms_ukeys, ms_uvals, ms_cub;
+  float4* pt0 = nullptr;  // per-point screen data seeded with d(., e0)
+  int* ms_count = nullptr;
+  int* ms_nruns = nullptr;
+  int ms_mode = 1;        // 1: sparse (flagged) path when possible, 0: dense only
 
   // timing / accounting
   bool timing = false;
@@ -197,32 +207,35 @@ int plan_screen(const ebc_ctx* ctx, ScreenPlan& p) {
   return plan_shape<ScreenA>(ctx, p);
 }
 
-template <class Cfg, bool GRAM, int PITCH = 0>
-int launch_screen_t(ebc_ctx* ctx, const ScreenPlan& p, const int* level_now, int level) {
-  auto kern = k_screen<Cfg, GRAM, PITCH>;
+template <class Cfg, int MODE, int PITCH = 0>
+int launch_screen_t(ebc_ctx* ctx, const ScreenPlan& p, const int* level_now, int level, const float* Vc = nullptr,
+                    FlagOut fo = FlagOut{}, const float4* ptv = nullptr) {
+  auto kern = k_screen<Cfg, MODE, PITCH>;
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
   dim3 grid(p.ncb, p.nsplit);
-  kern<<<grid, Cfg::THREADS, p.smem, ctx->stream>>>(ctx->V32, ctx->pt, ctx->pitch, ctx->d4, ctx->c0, p.ntiles, p.tps,
+  kern<<<grid, Cfg::THREADS, p.smem, ctx->stream>>>(ctx->V32, ptv ? ptv : ctx->pt, ctx->pitch, ctx->d4, ctx->c0,
+                                                    p.ntiles, p.tps,
                                                     (double*)ctx->part_g.p, (float*)ctx->part_e.p, ctx->n_pad,
-                                                    ctx->gram_kc, level_now, level);
+                                                    ctx->gram_kc, level_now, level, Vc, fo);
   KCHECK();
   return EBC_OK;
 }
 
-template <bool GRAM>
-int launch_screen(ebc_ctx* ctx, const ScreenPlan& p, const int* level_now, int level) {
+template <int MODE>
+int launch_screen(ebc_ctx* ctx, const ScreenPlan& p, const int* level_now, int level, const float* Vc = nullptr,
+                  FlagOut fo = FlagOut{}, const float4* ptv = nullptr) {
   if (p.shape == 2) {
     // compile-time pitches for the BASELINE dims (16, 32, 64, 100)
     switch (ctx->pitch) {
-      case 20: return launch_screen_t<ScreenB, GRAM, 20>(ctx, p, level_now, level);
-      case 36: return launch_screen_t<ScreenB, GRAM, 36>(ctx, p, level_now, level);
-      case 68: return launch_screen_t<ScreenB, GRAM, 68>(ctx, p, level_now, level);
-      case 100: return launch_screen_t<ScreenB, GRAM, 100>(ctx, p, level_now, level);
-      default: return launch_screen_t<ScreenB, GRAM>(ctx, p, level_now, level);
+      case 20: return launch_screen_t<ScreenB, MODE, 20>(ctx, p, level_now, level, Vc, fo, ptv);
+      case 36: return launch_screen_t<ScreenB, MODE, 36>(ctx, p, level_now, level, Vc, fo, ptv);
+      case 68: return launch_screen_t<ScreenB, MODE, 68>(ctx, p, level_now, level, Vc, fo, ptv);
+      case 100: return launch_screen_t<ScreenB, MODE, 100>(ctx, p, level_now, level, Vc, fo, ptv);
+      default: return launch_screen_t<ScreenB, MODE>(ctx, p, level_now, level, Vc, fo, ptv);
     }
   }
-  if (p.shape == 1) return launch_screen_t<ScreenA4, GRAM>(ctx, p, level_now, level);
-  return launch_screen_t<ScreenA, GRAM>(ctx, p, level_now, level);
+  if (p.shape == 1) return launch_screen_t<ScreenA4, MODE>(ctx, p, level_now, level, Vc, fo, ptv);
+  return launch_screen_t<ScreenA, MODE>(ctx, p, level_now, level, Vc, fo, ptv);
 }
 
 template <typename T, bool BIGD>
@@ -336,10 +349,10 @@ int run_screen_window(ebc_ctx* ctx, int eb, int fin_blocks) {
   CU(cudaMemsetAsync(ctx->maxlb, 0, sizeof(long long), ctx->stream));
   const double nterms_ffma = (double)p.tps * p.tp * 8 * 2;
   if (ctx->screen_mode == 0) {
-    rc = launch_screen<false>(ctx, p, nullptr, 0);
+    rc = launch_screen<0>(ctx, p, nullptr, 0);
     if (!rc) rc = run_finalize_window(ctx, p.nsplit, nterms_ffma, p.tp, fin_blocks, 1.0, nullptr, 0);
   } else if (ctx->screen_mode == 1) {
-    rc = launch_screen<true>(ctx, p, nullptr, 0);
+    rc = launch_screen<1>(ctx, p, nullptr, 0);
     if (!rc) rc = run_finalize_window(ctx, p.nsplit, nterms_ffma, p.tp, fin_blocks, 2.0, nullptr, 0);
   } else {
     if (use_tc) {
@@ -351,12 +364,12 @@ int run_screen_window(ebc_ctx* ctx, int eb, int fin_blocks) {
         KCHECK();
       }
     }
-    if (!rc) rc = launch_screen<true>(ctx, p, ctx->level, 1);
+    if (!rc) rc = launch_screen<1>(ctx, p, ctx->level, 1);
     if (!rc) rc = run_finalize_window(ctx, p.nsplit, nterms_ffma, p.tp, fin_blocks, 2.0, ctx->level, 1);
     if (!rc) {
       k_adapt<<<1, 32, 0, ctx->stream>>>(ctx->wcount, ctx->maxlb, ctx->wcap, ctx->level, 1);
       KCHECK();
-      rc = launch_screen<false>(ctx, p, ctx->level, 2);
+      rc = launch_screen<0>(ctx, p, ctx->level, 2);
     }
     if (!rc) rc = run_finalize_window(ctx, p.nsplit, nterms_ffma, p.tp, fin_blocks, 1.0, ctx->level, 2);
   }
@@ -449,13 +462,104 @@ void free_ctx(ebc_ctx* c) {
                   c->maxlb, c->wcount, c->wlist, c->wgain, c->ub};
   for (void* p : ptrs)
     if (p) cudaFree(p);
-  DevBuf* bufs[] = {&c->part_g, &c->part_e, &c->part_r, &c->sel_out, &c->val_out,
-                    &c->gain_out, &c->ms_part, &c->ms_off, &c->ms_idx, &c->ms_out};
+  DevBuf* bufs[] = {&c->part_g, &c->part_e, &c->part_r, &c->sel_out, &c->val_out, &c->gain_out, &c->ms_part,
+                    &c->ms_off, &c->ms_idx, &c->ms_out, &c->ms_mbuf, &c->ms_setof, &c->ms_pairs, &c->ms_keys,
+                    &c->ms_vals, &c->ms_keys2, &c->ms_vals2, &c->ms_ukeys, &c->ms_uvals, &c->ms_cub};
+  void* more[] = {c->pt0, c->ms_count, c->ms_nruns};
+  for (void* p : more)
+    if (p) cudaFree(p);
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
+}
+
+// Sparse work-matrix path (multiset.cuh).  Offsets/idx are already on the
+// device (ms_off / ms_idx).  Returns EBC_EINVAL (results not written) when the
+// flagged-pair buffer overflows -- the caller then runs the dense kernel.
+int multiset_sparse(ebc_ctx* ctx, int64_t l, int64_t nnz) {
+  const int64_t mrows = ((nnz + 127) / 128) * 128 + 128;
+  int rc = ensure(ctx, ctx->ms_mbuf, (size_t)mrows * ctx->pitch * sizeof(float));
+  if (!rc) rc = ensure(ctx, ctx->ms_setof, (size_t)mrows * sizeof(int));
+  if (rc) return rc;
+  if (!ctx->pt0) {
+    CU(cudaMalloc(&ctx->pt0, (size_t)ctx->n_pad * sizeof(float4)));
+    CU(cudaMemsetAsync(ctx->pt0, 0, (size_t)ctx->n_pad * sizeof(float4), ctx->stream));
+    CU(cudaMalloc(&ctx->ms_count, sizeof(int)));
+    CU(cudaMalloc(&ctx->ms_nruns, sizeof(int)));
+    k_make_pt0<<<(unsigned)((ctx->n + 255) / 256), 256, 0, ctx->stream>>>(ctx->n, ctx->e0d, ctx->nv32, ctx->pk,
+                                                                          ctx->pt0);
+    KCHECK();
+  }
+  CU(cudaMemsetAsync(ctx->ms_mbuf.p, 0, (size_t)mrows * ctx->pitch * sizeof(float), ctx->stream));
+  k_gather_members<<<8 * ctx->num_sms, 256, 0, ctx->stream>>>(ctx->V32, ctx->pitch, (const int64_t*)ctx->ms_idx.p,
+                                                              (const int64_t*)ctx->ms_off.p, l, nnz,
+                                                              (float*)ctx->ms_mbuf.p, (int*)ctx->ms_setof.p);
+  KCHECK();
+  // flag screen: candidates = member rows, seed = d(., e0)
+  const int cap = 16 << 20;
+  rc = ensure(ctx, ctx->ms_pairs, (size_t)cap * sizeof(uint2));
+  if (rc) return rc;
+  CU(cudaMemsetAsync(ctx->ms_count, 0, sizeof(int), ctx->stream));
+  const int64_t sc0 = ctx->c0, sc1 = ctx->c1;
+  ctx->c0 = 0;
+  ctx->c1 = nnz;
+  ScreenPlan p;
+  rc = plan_screen(ctx, p);
+  FlagOut fo{(uint2*)ctx->ms_pairs.p, ctx->ms_count, cap, ctx->n, nnz};
+  if (!rc) rc = launch_screen<2>(ctx, p, nullptr, 0, (const float*)ctx->ms_mbuf.p, fo, ctx->pt0);
+  ctx->c0 = sc0;
+  ctx->c1 = sc1;
+  if (rc) return rc;
+  int cnt = 0;
+  CU(cudaMemcpyAsync(&cnt, ctx->ms_count, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  if (cnt > cap) return EBC_EINVAL;  // dense fallback
+  const int64_t items = std::max(cnt, 1);
+  rc = ensure(ctx, ctx->ms_keys, (size_t)items * 8);
+  if (!rc) rc = ensure(ctx, ctx->ms_vals, (size_t)items * 8);
+  if (!rc) rc = ensure(ctx, ctx->ms_keys2, (size_t)items * 8);
+  if (!rc) rc = ensure(ctx, ctx->ms_vals2, (size_t)items * 8);
+  if (!rc) rc = ensure(ctx, ctx->ms_ukeys, (size_t)items * 8);
+  if (!rc) rc = ensure(ctx, ctx->ms_uvals, (size_t)items * 8);
+  if (rc) return rc;
+  unsigned long long* keys = (unsigned long long*)ctx->ms_keys.p;
+  double* vals = (double*)ctx->ms_vals.p;
+  if (cnt > 0) {
+    k_flag_exact<float><<<4 * ctx->num_sms, 256, 0, ctx->stream>>>(
+        (const uint2*)ctx->ms_pairs.p, ctx->ms_count, cap, ctx->V32, ctx->pitch, ctx->d,
+        (const int64_t*)ctx->ms_idx.p, (const int*)ctx->ms_setof.p, ctx->e0d, ctx->n, keys, vals);
+    KCHECK();
+  }
+  // sort by (set, point) and take the max term per key
+  const int end_bit = 64;  // key = set * n + point; ~0 marks a non-contributing pair
+  size_t tb1 = 0, tb2 = 0;
+  CU(cub::DeviceRadixSort::SortPairs(nullptr, tb1, keys, (unsigned long long*)ctx->ms_keys2.p, vals,
+                                     (double*)ctx->ms_vals2.p, (int)items, 0, end_bit, ctx->stream));
+  CU(cub::DeviceReduce::ReduceByKey(nullptr, tb2, (unsigned long long*)ctx->ms_keys2.p,
+                                    (unsigned long long*)ctx->ms_ukeys.p, (double*)ctx->ms_vals2.p,
+                                    (double*)ctx->ms_uvals.p, ctx->ms_nruns, DMax(), (int)items, ctx->stream));
+  rc = ensure(ctx, ctx->ms_cub, std::max(tb1, tb2) + 256);
+  if (rc) return rc;
+  size_t tb = ctx->ms_cub.bytes;
+  if (cnt > 0) {
+    CU(cub::DeviceRadixSort::SortPairs(ctx->ms_cub.p, tb, keys, (unsigned long long*)ctx->ms_keys2.p, vals,
+                                       (double*)ctx->ms_vals2.p, cnt, 0, end_bit, ctx->stream));
+    ++ctx->launches;
+    tb = ctx->ms_cub.bytes;
+    CU(cub::DeviceReduce::ReduceByKey(ctx->ms_cub.p, tb, (unsigned long long*)ctx->ms_keys2.p,
+                                      (unsigned long long*)ctx->ms_ukeys.p, (double*)ctx->ms_vals2.p,
+                                      (double*)ctx->ms_uvals.p, ctx->ms_nruns, DMax(), cnt, ctx->stream));
+    ++ctx->launches;
+  } else {
+    CU(cudaMemsetAsync(ctx->ms_nruns, 0, sizeof(int), ctx->stream));
+  }
+  k_sparse_set_sum<<<(unsigned)l, RED_THREADS, 0, ctx->stream>>>(
+      (const unsigned long long*)ctx->ms_ukeys.p, (const double*)ctx->ms_uvals.p, ctx->ms_nruns, ctx->n, l,
+      1.0 / (double)ctx->n, (double*)ctx->ms_out.p);
+  KCHECK();
+  return EBC_OK;
 }
 
 }  // namespace
@@ -510,6 +614,8 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
     ctx->gram_kc = (float)(1.5 * (d + 4) * u * (1.0 + 1.0 / 512));
     ctx->wcap = (int)std::max<int64_t>(256, n / 64);
     ctx->screen_mode = d >= 24 ? 3 : 0;
+    const char* mm = getenv("EBC200_MULTISET_MODE");
+    if (mm && mm[0]) ctx->ms_mode = atoi(mm);
     const char* m = getenv("EBC200_SCREEN_MODE");
     if (m && m[0]) ctx->screen_mode = atoi(m);
   }
@@ -849,7 +955,22 @@ int ebc_eval_multiset(ebc_ctx* ctx, const int64_t* offsets, const int64_t* idx, 
   if (nnz > 0)
     CU(cudaMemcpyAsync(ctx->ms_idx.p, idx, (size_t)nnz * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
   CU(cudaEventRecord(a, ctx->stream));
-  for (int64_t s0 = 0; s0 < l; s0 += batch) {
+  bool done = false;
+  if (ctx->dtype != EBC_F64 && ctx->ms_mode == 1) {
+    ScreenPlan probe;
+    const int64_t sc0 = ctx->c0, sc1 = ctx->c1;
+    ctx->c0 = 0;
+    ctx->c1 = std::max<int64_t>(nnz, 1);
+    const bool fits = plan_screen(ctx, probe) == EBC_OK;
+    ctx->c0 = sc0;
+    ctx->c1 = sc1;
+    if (fits && nnz > 0) {
+      rc = multiset_sparse(ctx, l, nnz);
+      if (rc == EBC_OK) done = true;
+      else if (rc != EBC_EINVAL) return rc;
+    }
+  }
+  for (int64_t s0 = 0; !done && s0 < l; s0 += batch) {
     const int64_t nb = std::min<int64_t>(batch, l - s0);
     dim3 grid(ctx->nchunks, (unsigned)nb);
     double* part = (double*)ctx->ms_part.p + s0 * ctx->nchunks;
@@ -863,9 +984,11 @@ int ebc_eval_multiset(ebc_ctx* ctx, const int64_t* offsets, const int64_t* idx, 
                                                               (const int64_t*)ctx->ms_idx.p, s0, ctx->nchunks, part);
     KCHECK();
   }
-  k_multiset_final<<<(unsigned)((l + 255) / 256), 256, 0, ctx->stream>>>(
-      (const double*)ctx->ms_part.p, l, ctx->nchunks, 1.0 / (double)ctx->n, (double*)ctx->ms_out.p);
-  KCHECK();
+  if (!done) {
+    k_multiset_final<<<(unsigned)((l + 255) / 256), 256, 0, ctx->stream>>>(
+        (const double*)ctx->ms_part.p, l, ctx->nchunks, 1.0 / (double)ctx->n, (double*)ctx->ms_out.p);
+    KCHECK();
+  }
   CU(cudaEventRecord(b, ctx->stream));
   CU(cudaMemcpyAsync(out_f, ctx->ms_out.p, (size_t)l * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));

@@ -161,6 +161,13 @@ __global__ void k_reset(int64_t n, const double* __restrict__ e0d, const float* 
   }
 }
 
+// pt0[v] = screen data seeded with d(v, e0) (work-matrix flag screen).
+__global__ void k_make_pt0(int64_t n, const double* __restrict__ e0d, const float* __restrict__ nv32, PtCoef pk,
+                           float4* __restrict__ pt0) {
+  const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v < n) pt0[v] = make_pt((float)e0d[v], nv32[v], pk);
+}
+
 __global__ void k_set_int(int* __restrict__ p, int v) {
   if (threadIdx.x == 0 && blockIdx.x == 0) *p = v;
 }
@@ -229,11 +236,25 @@ __device__ __forceinline__ float rowsum8_transposed(const float (&x)[8], int r) 
   return keep + __shfl_xor_sync(0xffffffffu, send, 1);
 }
 
-template <class Cfg, bool GRAM, int PITCH>
+// MODE 0: direct-form gains; 1: Gram-form gains; 2: direct-form *flags* -- append
+// every (point, candidate) pair that is possibly closer than the seed distance
+// (K2 work-matrix path: candidates are set members, seed = d(v, e0)).
+struct FlagOut {
+  uint2* pairs;      // (point, candidate row) of possibly-contributing pairs
+  int* count;        // appended pairs (may exceed cap: overflow -> caller falls back)
+  int cap;
+  int64_t npoints;   // valid point rows
+  int64_t ncands;    // valid candidate rows
+};
+
+template <class Cfg, int MODE, int PITCH>
 __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
     k_screen(const float* __restrict__ V, const float4* __restrict__ pt, int pitch_rt, int d4, int64_t cand0,
              int ntiles, int tiles_per_split, double* __restrict__ part_g, float* __restrict__ part_e,
-             int64_t part_stride, float gram_kc, const int* __restrict__ level_now, int level) {
+             int64_t part_stride, float gram_kc, const int* __restrict__ level_now, int level,
+             const float* __restrict__ Vc, FlagOut fo) {
+  constexpr bool GRAM = MODE == 1;
+  constexpr bool FLAG = MODE == 2;
   if (level_now && *level_now != level) return;  // adaptive screen: not this level's turn
   // PITCH != 0: compile-time row pitch -> every LDS address is base + immediate
   const int pitch = PITCH ? PITCH : pitch_rt;
@@ -277,7 +298,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
   __syncthreads();
   if (tid == 0) {
     mbar_arrive_expect_tx(cbar, (uint32_t)cand_bytes);
-    bulk_g2s(cs, V + crow * pitch, (uint32_t)cand_bytes, cbar);
+    bulk_g2s(cs, (Vc ? Vc : V) + crow * pitch, (uint32_t)cand_bytes, cbar);
     for (int s = 0; s < STAGES && s < nt; ++s) {
       unsigned char* st = stage_base + s * stage_bytes;
       const int64_t prow = (int64_t)(t0 + s) * PT_;
@@ -427,6 +448,23 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
     __syncwarp();
 
     // epilogue.  direct: acc = d32 - cm32;  Gram: acc = (cm - |v|^2 - |c|^2)/2 + v.c = t/2
+    if (FLAG) {
+#pragma unroll
+      for (int i = 0; i < TP; ++i) {
+#pragma unroll
+        for (int j = 0; j < TC; ++j) {
+          if (acc[i][j] < tau[i]) {  // rare: possibly closer than e0
+            const int64_t v = (int64_t)(t0 + it) * PT_ + wp * (LR * TP) + r + LR * i;
+            const int64_t m = crow + wc * (LC * TC) + q + LC * j;
+            if (v < fo.npoints && m < fo.ncands) {
+              const int slot = atomicAdd(fo.count, 1);
+              if (slot < fo.cap) fo.pairs[slot] = make_uint2((unsigned)v, (unsigned)m);
+            }
+          }
+        }
+      }
+      continue;
+    }
 #pragma unroll
     for (int i = 0; i < TP; ++i) {
 #pragma unroll
@@ -449,6 +487,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
     for (int j = 0; j < TC; ++j) g[j] = 0.f;
   }
 
+  if (FLAG) return;
   // error bound: same transposed reduce in fp32 (covered by the inflation factor)
   if (GRAM) {
 #pragma unroll

@@ -246,3 +246,25 @@ def test_wide_and_odd_dims_vs_oracle(d):
     sel, vals, _, _ = oracle.greedy(X.astype(np.float64), 5)
     assert s.selected == sel
     np.testing.assert_allclose(np.cumsum(s.gains), vals, rtol=1e-10)
+
+
+def test_sparse_work_matrix_bit_identical_to_dense(monkeypatch):
+    """The flagged (sparse) work-matrix path must reproduce the dense kernel bit
+    for bit: same fp64 terms, same chunk/tree/left-to-right reduction."""
+    rng = np.random.default_rng(31)
+    cases = []
+    for n, d, l, size in [(5000, 64, 64, 10), (3000, 16, 40, 3), (2000, 100, 20, 50), (1500, 7, 30, 0)]:
+        X = rng.standard_normal((n, d)).astype(np.float32)
+        sets = [rng.choice(n, size=size, replace=False).tolist() for _ in range(l)]
+        sets.append(list(range(n)))  # the full set: exactly the baseline
+        sets.append([])              # the empty set: exactly 0
+        cases.append((X, sets))
+    for X, sets in cases:
+        out = {}
+        for mode in ("0", "1"):
+            monkeypatch.setenv("EBC200_MULTISET_MODE", mode)
+            f = fn(X, eb.Precision.FP32)
+            out[mode] = eb.evaluate_with_backend(f, eb.EvalMultiset(sets))
+            assert out[mode][-1] == 0.0
+            assert out[mode][-2] == f.baseline_loss
+        assert out["0"].tolist() == out["1"].tolist()
