@@ -13,7 +13,7 @@ from .core import (Dissimilarity, EvalMultiset, GroundMatrix, Precision, Squared
                    make_auxiliary_vector, squared_euclidean)
 from .ebc import EbcFunction
 from .optimize import (BACKENDS, OptimizerBudget, evaluate_multiset_batched, evaluate_with_backend,
-                       greedy_maximize, parse_backend_spec)
+                       greedy_maximize, parse_backend_spec, sieve_stream_maximize)
 from .sharded import greedy_maximize_sharded
 
 __version__ = "0.1.0"
@@ -22,5 +22,5 @@ __all__ = [
     "Dissimilarity", "EvalMultiset", "GroundMatrix", "Precision", "SquaredEuclidean", "Summary",
     "make_auxiliary_vector", "squared_euclidean", "EbcFunction", "BACKENDS", "OptimizerBudget",
     "evaluate_multiset_batched", "evaluate_with_backend", "greedy_maximize", "parse_backend_spec",
-    "greedy_maximize_sharded",
+    "greedy_maximize_sharded", "sieve_stream_maximize",
 ]

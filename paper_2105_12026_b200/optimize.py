@@ -10,6 +10,7 @@ multiset S_multi = {S u {c}} on the host each step.
 from __future__ import annotations
 
 import ctypes
+import math
 import time
 from dataclasses import dataclass
 from typing import Tuple
@@ -115,3 +116,64 @@ def last_launches(f: EbcFunction) -> int:
 
 def set_timing(f: EbcFunction, on: bool) -> None:
     _native.check(f._lib.ebc_set_timing(f.native_context, 1 if on else 0), f.native_context)
+
+
+def sieve_stream_maximize(stream, f: EbcFunction, k: int, epsilon: float = 0.1) -> Summary:
+    """Single-pass threshold-sieve maximization (optimize.py:140-197 contract).
+
+    Thresholds live on the geometric grid (1+epsilon)^i covering [m, 2km],
+    m = best singleton value seen so far; a sieve with threshold tau admits the
+    streamed element e while it holds fewer than k elements and
+    f(S+e) - f(S) >= (tau/2 - f(S)) / (k - |S|).  The best sieve is returned;
+    an empty stream gives an empty summary of value 0.
+
+    Device work per element: one evaluation of {e} and one batched work-matrix
+    evaluation of {S_r u {e}} over every live sieve r that can still admit e
+    (sieve decisions for one element are independent, so they batch).
+    """
+    if k < 1:
+        raise ValueError("k must be >= 1")
+    if not 0.0 < epsilon < 1.0:
+        raise ValueError("epsilon must lie in (0, 1)")
+    t0 = time.perf_counter()
+    log_base = math.log1p(epsilon)
+    sieves: dict = {}      # exponent -> [threshold, selected, value, gains]
+    best_single = 0.0
+    evaluations = 0
+    n = f.ground.n
+    for raw in stream:
+        e = int(raw)
+        if not 0 <= e < n:
+            raise IndexError(f"index {e} out of range for ground size {n}")
+        single = f.value([e])
+        evaluations += 1
+        if single > best_single:
+            best_single = single
+            lo = math.ceil(math.log(best_single) / log_base - 1e-12)
+            hi = math.floor(math.log(2.0 * k * best_single) / log_base + 1e-12)
+            for ex in [x for x in sieves if x < lo or x > hi]:
+                del sieves[ex]
+            for ex in range(lo, hi + 1):
+                sieves.setdefault(ex, [(1.0 + epsilon) ** ex, [], 0.0, []])
+        live = [ex for ex in sorted(sieves) if len(sieves[ex][1]) < k and e not in sieves[ex][1]]
+        if not live:
+            continue
+        values = f.evaluate_multiset(EvalMultiset([sieves[ex][1] + [e] for ex in live]))
+        evaluations += len(live)
+        for ex, val in zip(live, values):
+            sv = sieves[ex]
+            gain = float(val) - sv[2]
+            need = (sv[0] / 2.0 - sv[2]) / (k - len(sv[1]))
+            if gain >= need:
+                sv[1].append(e)
+                sv[2] += gain
+                sv[3].append(gain)
+    runtime = time.perf_counter() - t0
+    if not sieves:
+        return Summary(selected=[], value=0.0, gains=[], evaluations=evaluations, runtime_seconds=runtime)
+    best = None
+    for ex in sorted(sieves):
+        if best is None or sieves[ex][2] > best[2]:
+            best = sieves[ex]
+    return Summary(selected=list(best[1]), value=best[2], gains=list(best[3]), evaluations=evaluations,
+                   runtime_seconds=runtime)

@@ -268,3 +268,28 @@ def test_sparse_work_matrix_bit_identical_to_dense(monkeypatch):
             assert out[mode][-1] == 0.0
             assert out[mode][-2] == f.baseline_loss
         assert out["0"].tolist() == out["1"].tolist()
+
+
+SIEVE = load_golden("reference_sieve.json")["cases"]
+
+
+@pytest.mark.parametrize("case", SIEVE, ids=[c["name"] for c in SIEVE])
+def test_sieve_streaming_matches_reference(case):
+    from conftest import case_data
+    X = case_data(case)
+    f = fn(X, PREC[case["precision"]])
+    stream = range(X.shape[0]) if case["stream"] == "range" else case["stream"]
+    s = eb.sieve_stream_maximize(stream, f, case["k"], case["epsilon"])
+    assert s.selected == case["selected"]
+    assert s.evaluations == case["evaluations"]
+    assert s.value == pytest.approx(case["value"], rel=1e-9, abs=1e-12)
+    np.testing.assert_allclose(s.gains, case["gains"], rtol=1e-8, atol=1e-12)
+
+
+def test_sieve_validation_and_empty_stream():
+    f = fn([[1.0, 0.0], [0.0, 1.0], [5.0, 5.0]])
+    assert eb.sieve_stream_maximize([], f, 2).value == 0.0
+    with pytest.raises(ValueError, match="epsilon"):
+        eb.sieve_stream_maximize([0], f, 1, epsilon=1.5)
+    s = eb.sieve_stream_maximize([1], f, 1)
+    assert s.selected == [1] and s.value == pytest.approx(f.value([1]), rel=1e-12)
