@@ -91,6 +91,16 @@ struct ebc_ctx {
   int* ms_nruns = nullptr;
   int ms_mode = 1;        // 1: sparse (flagged) path when possible, 0: dense only
 
+  // CUDA graphs of whole Greedy runs, keyed by k (rebuilt when buffers move)
+  struct Graph {
+    int k;
+    int64_t epoch;
+    int64_t launches;
+    cudaGraphExec_t exec;
+  };
+  std::vector<Graph> graphs;
+  int64_t alloc_epoch = 0;
+  bool use_graphs = true;
   // timing / accounting
   bool timing = false;
   std::vector<cudaEvent_t> ev;
@@ -131,6 +141,7 @@ int ensure(ebc_ctx* ctx, DevBuf& b, size_t bytes) {
   b.bytes = 0;
   CU(cudaMalloc(&b.p, bytes));
   b.bytes = bytes;
+  ++ctx->alloc_epoch;  // cached graphs hold the old pointers
   return EBC_OK;
 }
 
@@ -438,6 +449,23 @@ int ensure_events(ebc_ctx* ctx, size_t count) {
   return EBC_OK;
 }
 
+int do_reset(ebc_ctx* ctx);
+int run_step_select(ebc_ctx* ctx, int step, int commit, int64_t* sel_dev);
+int run_update(ebc_ctx* ctx, int step, double* val_dev, double* gain_dev);
+
+// Reset + the k steps of a Greedy run, all on ctx->stream (no host sync).
+int enqueue_greedy(ebc_ctx* ctx, int k) {
+  int rc = do_reset(ctx);
+  if (rc) return rc;
+  for (int s = 0; s < k; ++s) {
+    rc = run_step_select(ctx, s, 1, (int64_t*)ctx->sel_out.p);
+    if (rc) return rc;
+    rc = run_update(ctx, s, (double*)ctx->val_out.p, (double*)ctx->gain_out.p);
+    if (rc) return rc;
+  }
+  return EBC_OK;
+}
+
 int do_reset(ebc_ctx* ctx) {
   const int blocks = (int)((ctx->n + 255) / 256);
   CU(cudaMemsetAsync(ctx->stats, 0, 4 * sizeof(long long), ctx->stream));
@@ -471,6 +499,7 @@ void free_ctx(ebc_ctx* c) {
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
+  for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -614,6 +643,8 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
     ctx->gram_kc = (float)(1.5 * (d + 4) * u * (1.0 + 1.0 / 512));
     ctx->wcap = (int)std::max<int64_t>(256, n / 64);
     ctx->screen_mode = d >= 24 ? 3 : 0;
+    const char* gg = getenv("EBC200_GRAPHS");
+    if (gg && gg[0] == '0') ctx->use_graphs = false;
     const char* mm = getenv("EBC200_MULTISET_MODE");
     if (mm && mm[0]) ctx->ms_mode = atoi(mm);
     const char* m = getenv("EBC200_SCREEN_MODE");
@@ -809,8 +840,6 @@ int ebc_greedy(ebc_ctx* ctx, int32_t k, int64_t* out_sel, double* out_val, doubl
   if (!rc) rc = ensure(ctx, ctx->val_out, (size_t)k * sizeof(double));
   if (!rc) rc = ensure(ctx, ctx->gain_out, (size_t)k * sizeof(double));
   if (rc) return rc;
-  rc = do_reset(ctx);
-  if (rc) return rc;
   if (ctx->timing) {
     rc = ensure_events(ctx, 4 * k);
     if (rc) return rc;
@@ -820,11 +849,47 @@ int ebc_greedy(ebc_ctx* ctx, int32_t k, int64_t* out_sel, double* out_val, doubl
   CU(cudaEventCreate(&tstart));
   CU(cudaEventCreate(&tend));
   CU(cudaEventRecord(tstart, ctx->stream));
-  for (int s = 0; s < k; ++s) {
-    rc = run_step_select(ctx, s, 1, (int64_t*)ctx->sel_out.p);
+  // The k-step loop has no host decision in it, so after one eager run it is
+  // captured as a CUDA graph and later runs with the same k replay it (one
+  // launch instead of ~10 per step: matters for small N, e.g. C1).
+  const bool graph_ok = ctx->use_graphs && !ctx->timing;
+  ebc_ctx::Graph* cached = nullptr;
+  for (auto& g : ctx->graphs)
+    if (g.k == k && g.epoch == ctx->alloc_epoch) cached = &g;
+  if (graph_ok && cached) {
+    CU(cudaGraphLaunch(cached->exec, ctx->stream));
+    ctx->launches = cached->launches;
+  } else {
+    rc = enqueue_greedy(ctx, k);
     if (rc) return rc;
-    rc = run_update(ctx, s, (double*)ctx->val_out.p, (double*)ctx->gain_out.p);
-    if (rc) return rc;
+    if (graph_ok) {
+      const int64_t before = ctx->launches;
+      cudaGraph_t graph = nullptr;
+      cudaGraphExec_t exec = nullptr;
+      bool ok = cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+      const int64_t epoch = ctx->alloc_epoch;
+      if (ok) {
+        const int crc = enqueue_greedy(ctx, k);
+        ok = cudaStreamEndCapture(ctx->stream, &graph) == cudaSuccess && crc == EBC_OK &&
+             epoch == ctx->alloc_epoch;
+      }
+      if (ok) ok = cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess;
+      if (graph) cudaGraphDestroy(graph);
+      cudaGetLastError();  // a failed capture only disables graphs
+      if (ok) {
+        for (auto it = ctx->graphs.begin(); it != ctx->graphs.end();)
+          if (it->k == k) {
+            cudaGraphExecDestroy(it->exec);
+            it = ctx->graphs.erase(it);
+          } else {
+            ++it;
+          }
+        ctx->graphs.push_back({k, epoch, ctx->launches - before, exec});
+      } else {
+        ctx->use_graphs = false;
+      }
+      ctx->launches = before;
+    }
   }
   CU(cudaEventRecord(tend, ctx->stream));
   CU(cudaMemcpyAsync(out_sel, ctx->sel_out.p, (size_t)k * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
