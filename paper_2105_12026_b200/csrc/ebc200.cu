@@ -67,8 +67,9 @@ struct ebc_ctx {
   int screen_mode = 2;
   int wcap = 256;
   // tensor-core Gram screen (tcgen05, kind::tf32, 3xTF32)
-  float* Vhi = nullptr;
-  float* Vlo = nullptr;
+  void* Vhi = nullptr;
+  void* Vlo = nullptr;
+  int tc_bf16 = 0;  // 1: BF16 split (kind::f16), 0: TF32 split (kind::tf32)
   float2* pttc = nullptr;
   int kpad = 0;
   int tc_np = 0;  // points per tensor tile (0: tensor screen unavailable)
@@ -299,7 +300,7 @@ bool plan_tc(const ebc_ctx* ctx, TcPlan& p) {
   const int64_t ncand = ctx->c1 - ctx->c0;
   p.ncb = (int)((ncand + tc::M - 1) / tc::M);
   p.ntiles = (int)((ctx->n + ctx->tc_np - 1) / ctx->tc_np);
-  p.smem = tc::smem_bytes(ctx->kpad, ctx->tc_np);
+  p.smem = tc::smem_bytes(ctx->kpad, ctx->tc_np, ctx->tc_bf16 ? 2 : 4);
   const int64_t slots = ctx->num_sms;  // one CTA per SM
   double best_cost = 1e300;
   p.tps = p.ntiles;
@@ -317,13 +318,14 @@ bool plan_tc(const ebc_ctx* ctx, TcPlan& p) {
   return true;
 }
 
-template <int NP>
+template <int NP, bool BF>
 int launch_tc_t(ebc_ctx* ctx, const TcPlan& p, const int* level_now, int level) {
-  auto kern = k_screen_tc<NP>;
+  auto kern = k_screen_tc<NP, BF>;
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
   dim3 grid(p.ncb, p.nsplit);
-  kern<<<grid, tc::THREADS, p.smem, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->d, ctx->Vhi, ctx->Vlo, ctx->pttc,
-                                                   ctx->nv32, ctx->kpad, tc::stages_for(ctx->kpad, ctx->tc_np), ctx->c0,
+  kern<<<grid, tc::THREADS, p.smem, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->d, (const unsigned char*)ctx->Vhi,
+                                                   (const unsigned char*)ctx->Vlo, ctx->pttc, ctx->nv32, ctx->kpad,
+                                                   tc::stages_for(ctx->kpad, ctx->tc_np, BF ? 2 : 4), ctx->c0,
                                                    p.ntiles, p.tps, (double*)ctx->part_g.p, (float*)ctx->part_e.p,
                                                    ctx->n_pad, ctx->tc_kc, level_now, level);
   KCHECK();
@@ -331,9 +333,14 @@ int launch_tc_t(ebc_ctx* ctx, const TcPlan& p, const int* level_now, int level) 
 }
 
 int launch_tc(ebc_ctx* ctx, const TcPlan& p, const int* level_now, int level) {
-  if (ctx->tc_np == 128) return launch_tc_t<128>(ctx, p, level_now, level);
-  if (ctx->tc_np == 64) return launch_tc_t<64>(ctx, p, level_now, level);
-  return launch_tc_t<32>(ctx, p, level_now, level);
+  if (ctx->tc_bf16) {
+    if (ctx->tc_np == 128) return launch_tc_t<128, true>(ctx, p, level_now, level);
+    if (ctx->tc_np == 64) return launch_tc_t<64, true>(ctx, p, level_now, level);
+    return launch_tc_t<32, true>(ctx, p, level_now, level);
+  }
+  if (ctx->tc_np == 128) return launch_tc_t<128, false>(ctx, p, level_now, level);
+  if (ctx->tc_np == 64) return launch_tc_t<64, false>(ctx, p, level_now, level);
+  return launch_tc_t<32, false>(ctx, p, level_now, level);
 }
 
 // fp32 screen of the candidate range + certified window.
@@ -708,25 +715,30 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
   // tensor-core screen: fp32-path grounds whose 128-candidate tile of hi+lo
   // operands plus a 2-stage ring of NP-point tiles fits shared memory
   if (dtype != EBC_F64 && ctx->screen_mode == 3) {
-    ctx->kpad = (d + 7) / 8 * 8;
+    const char* kind = getenv("EBC200_TC_KIND");
+    ctx->tc_bf16 = (kind && kind[0]) ? atoi(kind) : 1;
+    const int es = ctx->tc_bf16 ? 2 : 4;
+    ctx->kpad = ctx->tc_bf16 ? (d + 15) / 16 * 16 : (d + 7) / 8 * 8;
     int nps[3] = {128, 64, 32};
     const char* npenv = getenv("EBC200_TC_NP");
     if (npenv && npenv[0]) nps[0] = atoi(npenv);
     for (int np : nps) {
-      if (ctx->kpad <= 128 && tc::stages_for(ctx->kpad, np) >= 2) {
+      if (ctx->kpad <= 128 && tc::stages_for(ctx->kpad, np, es) >= 2) {
         ctx->tc_np = np;
         break;
       }
     }
     if (ctx->tc_np) {
       const double u = 5.960464477539063e-08;
-      const double ktc = 3.0 * std::ldexp(1.0, -20) + (3.0 * ctx->kpad + 16.0) * std::ldexp(1.0, -23);
+      // split error (dropped low-order products) + fp32 accumulation of 3*kpad products
+      const double split = ctx->tc_bf16 ? 3.1 * std::ldexp(1.0, -18) : 3.0 * std::ldexp(1.0, -20);
+      const double ktc = split + (3.0 * ctx->kpad + 16.0) * std::ldexp(1.0, -23);
       ctx->tc_ka = (float)(4.0 * u * 1.01);
       ctx->tc_kb = (float)((4.0 * u + 0.5 * ktc) * 1.01);
       ctx->tc_kc = (float)((4.0 * u + 0.5 * ktc) * 1.01);
       const size_t ve = (size_t)ctx->n_pad * ctx->kpad;
-      CUC(cudaMalloc(&ctx->Vhi, ve * sizeof(float)));
-      CUC(cudaMalloc(&ctx->Vlo, ve * sizeof(float)));
+      CUC(cudaMalloc(&ctx->Vhi, ve * es));
+      CUC(cudaMalloc(&ctx->Vlo, ve * es));
       CUC(cudaMalloc(&ctx->pttc, (size_t)ctx->n_pad * sizeof(float2)));
       CUC(cudaMemsetAsync(ctx->pttc, 0, (size_t)ctx->n_pad * sizeof(float2), ctx->stream));
     }
@@ -766,8 +778,12 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
                                                                 ctx->pttc, ctx->tc_ka, ctx->tc_kb);
   CUC(cudaGetLastError());
   if (ctx->tc_np) {
-    k_split_tf32<<<8 * ctx->num_sms, 256, 0, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->n_pad, d, ctx->kpad,
-                                                           ctx->Vhi, ctx->Vlo);
+    if (ctx->tc_bf16)
+      k_split_bf16<<<8 * ctx->num_sms, 256, 0, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->n_pad, d, ctx->kpad,
+                                                             (__nv_bfloat16*)ctx->Vhi, (__nv_bfloat16*)ctx->Vlo);
+    else
+      k_split_tf32<<<8 * ctx->num_sms, 256, 0, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->n_pad, d, ctx->kpad,
+                                                             (float*)ctx->Vhi, (float*)ctx->Vlo);
     CUC(cudaGetLastError());
   }
   double* bl = nullptr;

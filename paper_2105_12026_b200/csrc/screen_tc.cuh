@@ -23,6 +23,8 @@
 #pragma once
 #include <cstdint>
 
+#include <cuda_bf16.h>
+
 #include "ptx.cuh"
 
 namespace ebc {
@@ -44,6 +46,10 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
 // instruction descriptor: kind::tf32, D fp32, A/B tf32, both K-major
 __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+// kind::f16 with BF16 A/B, fp32 D, both K-major
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
@@ -117,6 +123,20 @@ __device__ __forceinline__ void mma3_tf32_ts(uint32_t tmem_d, uint32_t a_hi, uin
       : "memory");
 }
 
+// Same for the BF16 split (kind::f16, K = 16 per instruction).
+__device__ __forceinline__ void mma3_bf16_ts(uint32_t tmem_d, uint32_t a_hi, uint32_t a_lo, uint64_t b_hi,
+                                             uint64_t b_lo, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "setp.eq.b32 q, %6, %6;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %3, %5, {%7, %7, %7, %7}, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %4, %5, {%7, %7, %7, %7}, q;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %3, %5, {%7, %7, %7, %7}, q;\n\t}\n" ::"r"(tmem_d),
+      "r"(a_hi), "r"(a_lo), "l"(b_hi), "l"(b_lo), "r"(idesc), "r"(acc), "r"(0)
+      : "memory");
+}
+
 __device__ __forceinline__ void st32(uint32_t taddr, const uint32_t (&r)[32]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
@@ -128,16 +148,16 @@ __device__ __forceinline__ void st32(uint32_t taddr, const uint32_t (&r)[32]) {
       : "memory");
 }
 
-inline int stages_for(int kpad, int np) {
-  const size_t stage = 2 * (size_t)np * kpad * 4;
+inline int stages_for(int kpad, int np, int es = 4) {
+  const size_t stage = 2 * (size_t)np * kpad * es;
   const size_t budget = 220 * 1024;
   int st = (int)(budget / stage);
   return st > MAX_STAGES ? MAX_STAGES : st;
 }
 
-inline size_t smem_bytes(int kpad, int np) {
-  const size_t stage = 2 * (size_t)np * kpad * 4;  // B_hi, B_lo
-  return stages_for(kpad, np) * stage + 4 * MAX_STAGES * sizeof(uint64_t) + 64;
+inline size_t smem_bytes(int kpad, int np, int es = 4) {
+  const size_t stage = 2 * (size_t)np * kpad * es;  // B_hi, B_lo
+  return stages_for(kpad, np, es) * stage + 4 * MAX_STAGES * sizeof(uint64_t) + 64;
 }
 
 }  // namespace tc
@@ -161,15 +181,35 @@ __global__ void k_split_tf32(const float* __restrict__ V32, int pitch, int64_t n
   }
 }
 
+// BF16 split: x = h + m + l, h = bf16(x), m = bf16(x - h); the screen uses h, m.
+// Layout as above with 8-element (16-byte) chunks: element (v, k) at
+// ((v/8 * KC + k/8) * 8 + v%8) * 8 + k%8, KC = kpad/8.
+__global__ void k_split_bf16(const float* __restrict__ V32, int pitch, int64_t nrows, int d, int kpad,
+                             __nv_bfloat16* __restrict__ hi, __nv_bfloat16* __restrict__ lo) {
+  const int KC = kpad / 8;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t total = nrows * kpad;
+  for (; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = i / kpad;
+    const int k = (int)(i - v * kpad);
+    const float x = k < d ? V32[v * pitch + k] : 0.f;
+    const __nv_bfloat16 h = __float2bfloat16_rn(x);
+    const __nv_bfloat16 m = __float2bfloat16_rn(x - __bfloat162float(h));
+    const int64_t off = (((v >> 3) * KC + (k >> 3)) * 8 + (v & 7)) * 8 + (k & 7);
+    hi[off] = h;
+    lo[off] = m;
+  }
+}
+
 // One CTA: candidates [cand0 + 128*bx, +128) x V tiles [t0, t1) of NP points.
 // A (candidates, hi and lo) lives in TMEM for the CTA's life (MMA "TS" form:
 // the tensor core reads only the B tiles from shared memory); B tiles stream
 // through a STAGES-deep bulk-copy ring released by the MMA commit alone; the
 // per-point seed/quantum {ip, kp} is read by the epilogue through L1.
-template <int NP>
+template <int NP, bool BF>
 __global__ void __launch_bounds__(tc::THREADS, 1)
-    k_screen_tc(const float* __restrict__ V32, int pitch, int d, const float* __restrict__ Vhi,
-                const float* __restrict__ Vlo, const float2* __restrict__ pttc, const float* __restrict__ nv32,
+    k_screen_tc(const float* __restrict__ V32, int pitch, int d, const unsigned char* __restrict__ Vhi,
+                const unsigned char* __restrict__ Vlo, const float2* __restrict__ pttc, const float* __restrict__ nv32,
                 int kpad, int stages, int64_t cand0, int ntiles, int tiles_per_split, double* __restrict__ part_g,
                 float* __restrict__ part_e, int64_t part_stride, float kc_coef, const int* __restrict__ level_now,
                 int level) {
@@ -177,7 +217,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   if (level_now && *level_now != level) return;
   extern __shared__ __align__(128) unsigned char smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint32_t b_bytes = (uint32_t)NP * kpad * 4;
+  constexpr int ES = BF ? 2 : 4;  // operand element bytes
+  const uint32_t b_bytes = (uint32_t)NP * kpad * ES;
   const uint32_t stage_bytes = 2 * b_bytes;
   unsigned char* stage0 = smem;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)stages * stage_bytes);
@@ -224,16 +265,16 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         unsigned char* st = stage0 + s * stage_bytes;
         const int64_t prow = (int64_t)(t0 + it) * NP;
         mbar_arrive_expect_tx(&full[s], stage_bytes);
-        bulk_g2s(st, Vhi + prow * kpad, b_bytes, &full[s]);
-        bulk_g2s(st + b_bytes, Vlo + prow * kpad, b_bytes, &full[s]);
+        bulk_g2s(st, Vhi + prow * kpad * ES, b_bytes, &full[s]);
+        bulk_g2s(st + b_bytes, Vlo + prow * kpad * ES, b_bytes, &full[s]);
       }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer: the whole warp walks the loop (warp-uniform
     // operands stay in uniform registers), one elected lane issues
-    constexpr uint32_t idesc = idesc_tf32(M, NP);
-    const uint32_t sbo = (uint32_t)kpad * 32;  // 8 rows x kpad floats
-    const int ksteps = kpad / 8;
+    constexpr uint32_t idesc = BF ? idesc_bf16(M, NP) : idesc_tf32(M, NP);
+    const uint32_t sbo = (uint32_t)kpad * 8 * ES;  // 8 rows x kpad elements
+    const int ksteps = kpad / (BF ? 16 : 8);       // 32 bytes of K per instruction
     mbar_wait(aready, 0);
     fence_after();
     for (int it = 0; it < nt; ++it) {
@@ -251,7 +292,10 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       if (elect_one()) {
 #pragma unroll 4
         for (int j = 0; j < ksteps; ++j) {
-          mma3_tf32_ts(dt, ahi + 8 * j, alo + 8 * j, dhi + 16 * j, dlo + 16 * j, idesc, j > 0);
+          if (BF)
+            mma3_bf16_ts(dt, ahi + 8 * j, alo + 8 * j, dhi + 16 * j, dlo + 16 * j, idesc, j > 0);
+          else
+            mma3_tf32_ts(dt, ahi + 8 * j, alo + 8 * j, dhi + 16 * j, dlo + 16 * j, idesc, j > 0);
         }
         commit(&sempty[s]);  // operands consumed -> producer may refill
         commit(&tfull[b]);   // accumulator ready for the epilogue
@@ -268,15 +312,26 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       // A_hi / A_lo of this candidate into TMEM columns [0,128) / [128,256)
       const float* row = V32 + c * pitch;
 #pragma unroll 1
-      for (int blk = 0; blk < 4; ++blk) {
+      for (int blk = 0; blk < (BF ? 2 : 4); ++blk) {
         uint32_t rh[32], rl[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
-          const int k = blk * 32 + i;
-          const float x = k < d ? row[k] : 0.f;
-          const uint32_t h = __float_as_uint(x) & 0xFFFFE000u;
-          rh[i] = h;
-          rl[i] = __float_as_uint(x - __uint_as_float(h));
+          if (BF) {
+            // column = packed pair (k = 2i, 2i+1), low half = even k
+            const int k = blk * 64 + 2 * i;
+            const float x0 = k < d ? row[k] : 0.f, x1 = k + 1 < d ? row[k + 1] : 0.f;
+            const __nv_bfloat16 h0 = __float2bfloat16_rn(x0), h1 = __float2bfloat16_rn(x1);
+            const __nv_bfloat16 m0 = __float2bfloat16_rn(x0 - __bfloat162float(h0));
+            const __nv_bfloat16 m1 = __float2bfloat16_rn(x1 - __bfloat162float(h1));
+            rh[i] = (uint32_t)__bfloat16_as_ushort(h0) | ((uint32_t)__bfloat16_as_ushort(h1) << 16);
+            rl[i] = (uint32_t)__bfloat16_as_ushort(m0) | ((uint32_t)__bfloat16_as_ushort(m1) << 16);
+          } else {
+            const int k = blk * 32 + i;
+            const float x = k < d ? row[k] : 0.f;
+            const uint32_t h = __float_as_uint(x) & 0xFFFFE000u;
+            rh[i] = h;
+            rl[i] = __float_as_uint(x - __uint_as_float(h));
+          }
         }
         st32(tmem + lane_off + COL_AHI + blk * 32, rh);
         st32(tmem + lane_off + COL_ALO + blk * 32, rl);
