@@ -93,7 +93,8 @@ __device__ __forceinline__ void ld32(uint32_t taddr, float (&v)[32]) {
 }
 
 constexpr int M = 128;        // candidates per CTA (UMMA M)
-constexpr int THREADS = 192;  // 6 warps
+constexpr int EPI_WARPGROUPS = 2;                     // epilogue warpgroups (slices of the point columns)
+constexpr int THREADS = 64 + 128 * EPI_WARPGROUPS;   // producer + MMA warp + epilogue
 constexpr int MAX_STAGES = 4;
 // TMEM columns: A_hi [0,128), A_lo [128,256), accumulators [256 + b*NP, ...)
 constexpr uint32_t COL_AHI = 0, COL_ALO = 128, COL_ACC = 256, TMEM_COLS = 512;
@@ -241,9 +242,9 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 128);
+      mbar_init(&tempty[b], 128 * EPI_WARPGROUPS);
     }
-    mbar_init(aready, 128);
+    mbar_init(aready, 128 * EPI_WARPGROUPS);
     fence_mbar_init();
   }
   if (warp == 0) {
@@ -303,14 +304,18 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       __syncwarp();
     }
   } else {
-    // ---------------- epilogue: thread = candidate = TMEM lane
-    const int q = warp & 3;  // TMEM lane quadrant of this warp
+    // ---------------- epilogue: EPI_WARPGROUPS x 4 warps; thread = candidate
+    // (TMEM lane) x one slice of the tile's point columns
+    const int q = warp & 3;                    // TMEM lane quadrant of this warp
+    const int half = (warp - 2) >> 2;          // which slice of the NP columns
+    constexpr int SLICE = NP / EPI_WARPGROUPS;
     const int cl = q * 32 + lane;
     const int64_t c = crow + cl;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     {
-      // A_hi / A_lo of this candidate into TMEM columns [0,128) / [128,256)
+      // A of this candidate into TMEM: slice 0 writes hi [0,128), the last slice lo [128,256)
       const float* row = V32 + c * pitch;
+      const bool do_hi = half == 0, do_lo = half == EPI_WARPGROUPS - 1;
 #pragma unroll 1
       for (int blk = 0; blk < (BF ? 2 : 4); ++blk) {
         uint32_t rh[32], rl[32];
@@ -333,8 +338,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
             rl[i] = __float_as_uint(x - __uint_as_float(h));
           }
         }
-        st32(tmem + lane_off + COL_AHI + blk * 32, rh);
-        st32(tmem + lane_off + COL_ALO + blk * 32, rl);
+        if (do_hi) st32(tmem + lane_off + COL_AHI + blk * 32, rh);
+        if (do_lo) st32(tmem + lane_off + COL_ALO + blk * 32, rl);
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       fence_before();
@@ -347,16 +352,16 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     float e = 0.f, cnt = 0.f;
     for (int it = 0; it < nt; ++it) {
       const int b = it & 1;
-      const float2* pp = pttc + (int64_t)(t0 + it) * NP;
+      const float2* pp = pttc + (int64_t)(t0 + it) * NP + half * SLICE;
       mbar_wait(&tfull[b], (it >> 1) & 1);
       fence_after();
 #pragma unroll
-      for (int h = 0; h < NP / 32; ++h) {
+      for (int h = 0; h < SLICE / 32; ++h) {
         float S[32];
-        ld32(tmem + lane_off + COL_ACC + (uint32_t)(b * NP + h * 32), S);
-        if (h == NP / 32 - 1) {
+        ld32(tmem + lane_off + COL_ACC + (uint32_t)(b * NP + half * SLICE + h * 32), S);
+        if (h == SLICE / 32 - 1) {
           fence_before();
-          mbar_arrive(&tempty[b]);  // all columns of this buffer are in registers
+          mbar_arrive(&tempty[b]);  // this thread's columns of the buffer are in registers
         }
         float g = 0.f;
 #pragma unroll
@@ -372,8 +377,25 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       }
     }
     e = fmaf(kc, cnt, e);
-    part_g[blockIdx.y * part_stride + c] = g64;
-    part_e[blockIdx.y * part_stride + c] = e;
+    // combine the slices of each candidate in slice order (named barrier over
+    // the epilogue warps only)
+    double* xg = reinterpret_cast<double*>(stage0);  // the ring is idle once every tile is consumed
+    float* xe = reinterpret_cast<float*>(stage0 + (size_t)EPI_WARPGROUPS * M * sizeof(double));
+    asm volatile("bar.sync 1, %0;" ::"n"(EPI_WARPGROUPS * 128));
+    xg[half * M + cl] = g64;
+    xe[half * M + cl] = e;
+    asm volatile("bar.sync 1, %0;" ::"n"(EPI_WARPGROUPS * 128));
+    if (half == 0) {
+      double gs = 0.0;
+      float es = 0.f;
+#pragma unroll
+      for (int w = 0; w < EPI_WARPGROUPS; ++w) {
+        gs += xg[w * M + cl];
+        es += xe[w * M + cl];
+      }
+      part_g[blockIdx.y * part_stride + c] = gs;
+      part_e[blockIdx.y * part_stride + c] = es;
+    }
   }
   fence_before();
   __syncthreads();
