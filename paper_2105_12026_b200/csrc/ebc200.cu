@@ -71,6 +71,7 @@ struct ebc_ctx {
   void* Vlo = nullptr;
   int tc_bf16 = 0;  // 1: BF16 split (kind::f16), 0: TF32 split (kind::tf32)
   float2* pttc = nullptr;
+  float* kpmax = nullptr;  // per tensor tile: max error quantum kp (reset state)
   int kpad = 0;
   int tc_np = 0;  // points per tensor tile (0: tensor screen unavailable)
   float tc_ka = 0.f, tc_kb = 0.f, tc_kc = 0.f;
@@ -324,7 +325,7 @@ int launch_tc_t(ebc_ctx* ctx, const TcPlan& p, const int* level_now, int level) 
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
   dim3 grid(p.ncb, p.nsplit);
   kern<<<grid, tc::THREADS, p.smem, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->d, (const unsigned char*)ctx->Vhi,
-                                                   (const unsigned char*)ctx->Vlo, ctx->pttc, ctx->nv32, ctx->kpad,
+                                                   (const unsigned char*)ctx->Vlo, ctx->pttc, ctx->kpmax, ctx->nv32, ctx->kpad,
                                                    tc::stages_for(ctx->kpad, ctx->tc_np, BF ? 2 : 4), ctx->c0,
                                                    p.ntiles, p.tps, (double*)ctx->part_g.p, (float*)ctx->part_e.p,
                                                    ctx->n_pad, ctx->tc_kc, level_now, level);
@@ -493,7 +494,7 @@ int do_reset(ebc_ctx* ctx) {
 void free_ctx(ebc_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
-  void* ptrs[] = {c->V32, c->V64, c->e0d, c->cm64, c->pt, c->nv32, c->level, c->stats, c->Vhi, c->Vlo, c->pttc, c->selected, c->chunkpart, c->counter, c->cur, c->best,
+  void* ptrs[] = {c->V32, c->V64, c->e0d, c->cm64, c->pt, c->nv32, c->level, c->stats, c->Vhi, c->Vlo, c->pttc, c->kpmax, c->selected, c->chunkpart, c->counter, c->cur, c->best,
                   c->maxlb, c->wcount, c->wlist, c->wgain, c->ub};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -740,6 +741,7 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
       CUC(cudaMalloc(&ctx->Vhi, ve * es));
       CUC(cudaMalloc(&ctx->Vlo, ve * es));
       CUC(cudaMalloc(&ctx->pttc, (size_t)ctx->n_pad * sizeof(float2)));
+      CUC(cudaMalloc(&ctx->kpmax, (size_t)(ctx->n_pad / ctx->tc_np + 1) * sizeof(float)));
       CUC(cudaMemsetAsync(ctx->pttc, 0, (size_t)ctx->n_pad * sizeof(float2), ctx->stream));
     }
   }
@@ -778,6 +780,11 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
                                                                 ctx->pttc, ctx->tc_ka, ctx->tc_kb);
   CUC(cudaGetLastError());
   if (ctx->tc_np) {
+    {
+      const int64_t ntl = ctx->n_pad / ctx->tc_np;
+      k_tile_kpmax<<<(unsigned)((ntl + 255) / 256), 256, 0, ctx->stream>>>(ctx->pttc, ntl, ctx->tc_np, ctx->kpmax);
+      CUC(cudaGetLastError());
+    }
     if (ctx->tc_bf16)
       k_split_bf16<<<8 * ctx->num_sms, 256, 0, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->n_pad, d, ctx->kpad,
                                                              (__nv_bfloat16*)ctx->Vhi, (__nv_bfloat16*)ctx->Vlo);

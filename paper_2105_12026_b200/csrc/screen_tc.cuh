@@ -93,8 +93,10 @@ __device__ __forceinline__ void ld32(uint32_t taddr, float (&v)[32]) {
 }
 
 constexpr int M = 128;        // candidates per CTA (UMMA M)
-constexpr int EPI_WARPGROUPS = 2;                     // epilogue warpgroups (slices of the point columns)
-constexpr int THREADS = 64 + 128 * EPI_WARPGROUPS;   // producer + MMA warp + epilogue
+constexpr int EPI_WARPGROUPS = 2;  // epilogue warpgroups (slices of the point columns)
+constexpr int MMA_WARPS = 2;       // tiles alternate between issuing warps (one per accumulator buffer)
+constexpr int EPI_WARP0 = 1 + MMA_WARPS;
+constexpr int THREADS = 32 * EPI_WARP0 + 128 * EPI_WARPGROUPS;  // producer + MMA warps + epilogue
 constexpr int MAX_STAGES = 4;
 // TMEM columns: A_hi [0,128), A_lo [128,256), accumulators [256 + b*NP, ...)
 constexpr uint32_t COL_AHI = 0, COL_ALO = 128, COL_ACC = 256, TMEM_COLS = 512;
@@ -202,6 +204,16 @@ __global__ void k_split_bf16(const float* __restrict__ V32, int pitch, int64_t n
   }
 }
 
+// kpmax[t] = max over the NP points of tile t of kp (pttc[v].y).
+__global__ void k_tile_kpmax(const float2* __restrict__ pttc, int64_t ntiles, int np, float* __restrict__ kpmax) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < ntiles) {
+    float m = 0.f;
+    for (int i = 0; i < np; ++i) m = fmaxf(m, pttc[t * np + i].y);
+    kpmax[t] = m;
+  }
+}
+
 // One CTA: candidates [cand0 + 128*bx, +128) x V tiles [t0, t1) of NP points.
 // A (candidates, hi and lo) lives in TMEM for the CTA's life (MMA "TS" form:
 // the tensor core reads only the B tiles from shared memory); B tiles stream
@@ -210,7 +222,8 @@ __global__ void k_split_bf16(const float* __restrict__ V32, int pitch, int64_t n
 template <int NP, bool BF>
 __global__ void __launch_bounds__(tc::THREADS, 1)
     k_screen_tc(const float* __restrict__ V32, int pitch, int d, const unsigned char* __restrict__ Vhi,
-                const unsigned char* __restrict__ Vlo, const float2* __restrict__ pttc, const float* __restrict__ nv32,
+                const unsigned char* __restrict__ Vlo, const float2* __restrict__ pttc,
+                const float* __restrict__ kpmax, const float* __restrict__ nv32,
                 int kpad, int stages, int64_t cand0, int ntiles, int tiles_per_split, double* __restrict__ part_g,
                 float* __restrict__ part_e, int64_t part_stride, float kc_coef, const int* __restrict__ level_now,
                 int level) {
@@ -270,26 +283,29 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         bulk_g2s(st + b_bytes, Vlo + prow * kpad * ES, b_bytes, &full[s]);
       }
     }
-  } else if (warp == 1) {
-    // ---------------- MMA issuer: the whole warp walks the loop (warp-uniform
-    // operands stay in uniform registers), one elected lane issues
+  } else if (warp < EPI_WARP0) {
+    // ---------------- MMA issuers: warp 1 + b issues the tiles that use
+    // accumulator buffer b, so one warp's barrier waits and register set-up
+    // overlap the other's queued MMAs.  The whole warp walks the loop
+    // (warp-uniform operands stay in uniform registers), one elected lane issues.
     constexpr uint32_t idesc = BF ? idesc_bf16(M, NP) : idesc_tf32(M, NP);
     const uint32_t sbo = (uint32_t)kpad * 8 * ES;  // 8 rows x kpad elements
     const int ksteps = kpad / (BF ? 16 : 8);       // 32 bytes of K per instruction
+    const int b = warp - 1;
+    const uint32_t dt = tmem + COL_ACC + (uint32_t)(b * NP);
+    const uint32_t ahi = tmem + COL_AHI, alo = tmem + COL_ALO;
     mbar_wait(aready, 0);
     fence_after();
-    for (int it = 0; it < nt; ++it) {
-      const int s = it % stages, b = it & 1;
+    for (int it = b; it < nt; it += 2) {
+      const int s = it % stages;
       mbar_wait(&full[s], (it / stages) & 1);
       if (it >= 2) mbar_wait(&tempty[b], ((it >> 1) - 1) & 1);
       fence_after();
       const uint32_t bhi = smem_u32(stage0 + s * stage_bytes);
-      const uint32_t dt = tmem + COL_ACC + (uint32_t)(b * NP);
       // descriptors built once per tile; K step j advances the start-address
       // field by 256 B (= 16 in 16-byte units) and A by 8 TMEM columns
       const uint64_t dhi = sdesc(bhi, 128, sbo);
       const uint64_t dlo = sdesc(bhi + b_bytes, 128, sbo);
-      const uint32_t ahi = tmem + COL_AHI, alo = tmem + COL_ALO;
       if (elect_one()) {
 #pragma unroll 4
         for (int j = 0; j < ksteps; ++j) {
@@ -307,7 +323,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     // ---------------- epilogue: EPI_WARPGROUPS x 4 warps; thread = candidate
     // (TMEM lane) x one slice of the tile's point columns
     const int q = warp & 3;                    // TMEM lane quadrant of this warp
-    const int half = (warp - 2) >> 2;          // which slice of the NP columns
+    const int half = (warp - EPI_WARP0) >> 2;  // which slice of the NP columns
     constexpr int SLICE = NP / EPI_WARPGROUPS;
     const int cl = q * 32 + lane;
     const int64_t c = crow + cl;
@@ -349,10 +365,15 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     const float ic = -0.5f * nc;
     const float kc = kc_coef * nc;
     double g64 = 0.0;
-    float e = 0.f, cnt = 0.f;
+    float e = 0.f;
     for (int it = 0; it < nt; ++it) {
       const int b = it & 1;
       const float2* pp = pttc + (int64_t)(t0 + it) * NP + half * SLICE;
+      // one error quantum per tile: kpmax = max_v kp over the tile (bounds every
+      // pair's kp_v; computed at reset, cm only decreases within a run)
+      const float kq = kpmax[t0 + it] + kc;
+      const float thr = -kq;
+      float cnt = 0.f;
       mbar_wait(&tfull[b], (it >> 1) & 1);
       fence_after();
 #pragma unroll
@@ -363,20 +384,22 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
           fence_before();
           mbar_arrive(&tempty[b]);  // this thread's columns of the buffer are in registers
         }
+        const float4* pp4 = reinterpret_cast<const float4*>(pp + h * 32);
         float g = 0.f;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float2 p = __ldg(pp + h * 32 + i);  // broadcast through L1
-          const float acc = (p.x + ic) + S[i];
-          g += fmaxf(acc, 0.f);
-          const float f = (acc + p.y > -kc) ? 1.f : 0.f;
-          e = fmaf(f, p.y, e);
-          cnt += f;
+        for (int i = 0; i < 16; ++i) {
+          const float4 p = __ldg(pp4 + i);  // {ip, kp} of two points, broadcast through L1
+          const float a0 = (p.x + ic) + S[2 * i];
+          const float a1 = (p.z + ic) + S[2 * i + 1];
+          g += fmaxf(a0, 0.f);
+          g += fmaxf(a1, 0.f);
+          cnt += (a0 > thr) ? 1.f : 0.f;
+          cnt += (a1 > thr) ? 1.f : 0.f;
         }
         g64 += (double)g;
       }
+      e = fmaf(cnt, kq, e);
     }
-    e = fmaf(kc, cnt, e);
     // combine the slices of each candidate in slice order (named barrier over
     // the epilogue warps only)
     double* xg = reinterpret_cast<double*>(stage0);  // the ring is idle once every tile is consumed
