@@ -94,9 +94,17 @@ __device__ __forceinline__ void ld32(uint32_t taddr, float (&v)[32]) {
 
 constexpr int M = 128;        // candidates per CTA (UMMA M)
 constexpr int EPI_WARPGROUPS = 2;  // epilogue warpgroups (slices of the point columns)
-constexpr int MMA_WARPS = 2;       // tiles alternate between issuing warps (one per accumulator buffer)
+constexpr int MMA_WARPS = 3;       // one issuing warp per accumulator buffer (tiles round-robin)
 constexpr int EPI_WARP0 = 1 + MMA_WARPS;
 constexpr int THREADS = 32 * EPI_WARP0 + 128 * EPI_WARPGROUPS;  // producer + MMA warps + epilogue
+// accumulator buffers: BF16 operands (A = 2 x 56 columns) leave room for 3 x 128
+// fp32 accumulators in the 512 TMEM columns, TF32 (A = 2 x 128) for 2
+template <bool BF>
+struct TmemMap {
+  static constexpr int NB = BF ? 3 : 2;
+  static constexpr uint32_t ALO = BF ? 64 : 128;
+  static constexpr uint32_t ACC = BF ? 128 : 256;
+};
 constexpr int MAX_STAGES = 4;
 // TMEM columns: A_hi [0,128), A_lo [128,256), accumulators [256 + b*NP, ...)
 constexpr uint32_t COL_AHI = 0, COL_ALO = 128, COL_ACC = 256, TMEM_COLS = 512;
@@ -160,7 +168,7 @@ inline int stages_for(int kpad, int np, int es = 4) {
 
 inline size_t smem_bytes(int kpad, int np, int es = 4) {
   const size_t stage = 2 * (size_t)np * kpad * es;  // B_hi, B_lo
-  return stages_for(kpad, np, es) * stage + 4 * MAX_STAGES * sizeof(uint64_t) + 64;
+  return stages_for(kpad, np, es) * stage + (2 * MAX_STAGES + 8) * sizeof(uint64_t) + 64;
 }
 
 }  // namespace tc
@@ -238,10 +246,10 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)stages * stage_bytes);
   uint64_t* full = bars;                   // [stages] operands landed
   uint64_t* sempty = bars + MAX_STAGES;    // [stages] operands consumed (MMA commit)
-  uint64_t* tfull = bars + 2 * MAX_STAGES;       // [2] accumulator ready
-  uint64_t* tempty = bars + 2 * MAX_STAGES + 2;  // [2] accumulator drained (128 epilogue threads)
-  uint64_t* aready = bars + 2 * MAX_STAGES + 4;  // A written to TMEM (128 epilogue threads)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * MAX_STAGES + 5);
+  uint64_t* tfull = bars + 2 * MAX_STAGES;       // [3] accumulator ready
+  uint64_t* tempty = bars + 2 * MAX_STAGES + 3;  // [3] accumulator drained (all epilogue threads)
+  uint64_t* aready = bars + 2 * MAX_STAGES + 6;  // A written to TMEM (all epilogue threads)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * MAX_STAGES + 7);
 
   const int t0 = blockIdx.y * tiles_per_split;
   const int t1 = min(ntiles, t0 + tiles_per_split);
@@ -253,7 +261,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       mbar_init(&full[s], 1);
       mbar_init(&sempty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < 3; ++b) {
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], 128 * EPI_WARPGROUPS);
     }
@@ -291,15 +299,16 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     constexpr uint32_t idesc = BF ? idesc_bf16(M, NP) : idesc_tf32(M, NP);
     const uint32_t sbo = (uint32_t)kpad * 8 * ES;  // 8 rows x kpad elements
     const int ksteps = kpad / (BF ? 16 : 8);       // 32 bytes of K per instruction
+    constexpr int NB = TmemMap<BF>::NB;
     const int b = warp - 1;
-    const uint32_t dt = tmem + COL_ACC + (uint32_t)(b * NP);
-    const uint32_t ahi = tmem + COL_AHI, alo = tmem + COL_ALO;
+    const uint32_t dt = tmem + TmemMap<BF>::ACC + (uint32_t)(b * NP);
+    const uint32_t ahi = tmem + COL_AHI, alo = tmem + TmemMap<BF>::ALO;
     mbar_wait(aready, 0);
     fence_after();
-    for (int it = b; it < nt; it += 2) {
+    for (int it = b; it < nt && b < NB; it += NB) {
       const int s = it % stages;
       mbar_wait(&full[s], (it / stages) & 1);
-      if (it >= 2) mbar_wait(&tempty[b], ((it >> 1) - 1) & 1);
+      if (it >= NB) mbar_wait(&tempty[b], ((it / NB) - 1) & 1);
       fence_after();
       const uint32_t bhi = smem_u32(stage0 + s * stage_bytes);
       // descriptors built once per tile; K step j advances the start-address
@@ -355,7 +364,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
           }
         }
         if (do_hi) st32(tmem + lane_off + COL_AHI + blk * 32, rh);
-        if (do_lo) st32(tmem + lane_off + COL_ALO + blk * 32, rl);
+        if (do_lo) st32(tmem + lane_off + TmemMap<BF>::ALO + blk * 32, rl);
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       fence_before();
@@ -366,20 +375,21 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     const float kc = kc_coef * nc;
     double g64 = 0.0;
     float e = 0.f;
+    constexpr int NB = TmemMap<BF>::NB;
     for (int it = 0; it < nt; ++it) {
-      const int b = it & 1;
+      const int b = it % NB;
       const float2* pp = pttc + (int64_t)(t0 + it) * NP + half * SLICE;
       // one error quantum per tile: kpmax = max_v kp over the tile (bounds every
       // pair's kp_v; computed at reset, cm only decreases within a run)
       const float kq = kpmax[t0 + it] + kc;
       const float thr = -kq;
       float cnt = 0.f;
-      mbar_wait(&tfull[b], (it >> 1) & 1);
+      mbar_wait(&tfull[b], (it / NB) & 1);
       fence_after();
 #pragma unroll
       for (int h = 0; h < SLICE / 32; ++h) {
         float S[32];
-        ld32(tmem + lane_off + COL_ACC + (uint32_t)(b * NP + half * SLICE + h * 32), S);
+        ld32(tmem + lane_off + TmemMap<BF>::ACC + (uint32_t)(b * NP + half * SLICE + h * 32), S);
         if (h == SLICE / 32 - 1) {
           fence_before();
           mbar_arrive(&tempty[b]);  // this thread's columns of the buffer are in registers

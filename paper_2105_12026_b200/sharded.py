@@ -35,9 +35,15 @@ from .core import Summary
 from .optimize import OptimizerBudget
 
 
+SHARD_ALIGN = 128  # candidate tile of the screens: shard starts stay tile aligned
+
+
 def shard_range(n: int, rank: int, world: int) -> Tuple[int, int]:
-    """Contiguous candidate range of `rank`: ceil(n / world) indices per rank."""
+    """Contiguous candidate range of `rank`: ceil(n / world) indices per rank,
+    rounded up to a multiple of the 128-candidate screen tile (so every rank
+    can use the tensor-core screen, whose tiles need 8-aligned starts)."""
     per = (n + world - 1) // world
+    per = (per + SHARD_ALIGN - 1) // SHARD_ALIGN * SHARD_ALIGN
     c0 = min(n, rank * per)
     return c0, min(n, c0 + per)
 
