@@ -97,6 +97,18 @@ int ebc_shard_step(ebc_ctx* ctx, int64_t* out_idx, double* out_gain, int64_t cap
  * returns the new f(S) in *out_value. */
 int ebc_shard_commit(ebc_ctx* ctx, int64_t s, double* out_value);
 
+/* One host round trip per sharded Greedy step: commit `commit_idx` (if >= 0),
+ * then (if run_step) screen + refine the local candidates; the first `cap`
+ * window entries (index, gain64), the full window size and f(S) after the
+ * commit come back with a single stream synchronisation.  If *out_count > cap,
+ * fetch all of it with ebc_shard_fetch (the window stays on the device until
+ * the next advance). */
+int ebc_shard_advance(ebc_ctx* ctx, int64_t commit_idx, int32_t run_step, int64_t* out_idx,
+                      double* out_gain, int64_t cap, int64_t* out_count, double* out_current);
+
+/* Copy the first `count` entries of the current local window to the host. */
+int ebc_shard_fetch(const ebc_ctx* ctx, int64_t* out_idx, double* out_gain, int64_t count);
+
 /* Reset the selection state to S = {} (cached minima back to d(., e0)). */
 int ebc_reset(ebc_ctx* ctx);
 

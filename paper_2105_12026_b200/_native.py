@@ -37,6 +37,8 @@ SIGNATURES = {
     "ebc_shard_set_range": (ctypes.c_int, [_vp, _i64, _i64]),
     "ebc_shard_step": (ctypes.c_int, [_vp, _i64p, _f64p, _i64, _i64p, _f64p]),
     "ebc_shard_commit": (ctypes.c_int, [_vp, _i64, _f64p]),
+    "ebc_shard_advance": (ctypes.c_int, [_vp, _i64, _i32, _i64p, _f64p, _i64, _i64p, _f64p]),
+    "ebc_shard_fetch": (ctypes.c_int, [_vp, _i64p, _f64p, _i64]),
     "ebc_reset": (ctypes.c_int, [_vp]),
     "ebc_stream": (_vp, [_vp]),
     "ebc_set_timing": (ctypes.c_int, [_vp, ctypes.c_int]),

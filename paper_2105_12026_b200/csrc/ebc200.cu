@@ -981,6 +981,51 @@ int ebc_shard_step(ebc_ctx* ctx, int64_t* out_idx, double* out_gain, int64_t cap
   return EBC_OK;
 }
 
+int ebc_shard_advance(ebc_ctx* ctx, int64_t commit_idx, int32_t run_step, int64_t* out_idx, double* out_gain,
+                      int64_t cap, int64_t* out_count, double* out_current) {
+  if (!ctx || !out_count || !out_current) return fail(ctx, EBC_EINVAL, "ebc_shard_advance: NULL argument");
+  if (commit_idx >= ctx->n)
+    return fail(ctx, EBC_EINDEX, "index " + std::to_string(commit_idx) + " out of range for ground size " +
+                                     std::to_string(ctx->n));
+  CU(cudaSetDevice(ctx->device));
+  ctx->launches = 0;
+  if (commit_idx >= 0) {
+    CU(cudaMemcpyAsync(ctx->best, &commit_idx, sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
+    const unsigned char one = 1;
+    CU(cudaMemcpyAsync(ctx->selected + commit_idx, &one, 1, cudaMemcpyHostToDevice, ctx->stream));
+    int rc = run_update(ctx, 0, nullptr, nullptr);
+    if (rc) return rc;
+    ctx->steps_done += 1;
+  }
+  int count = 0;
+  const bool step = run_step && ctx->c1 > ctx->c0;
+  if (step) {
+    int rc = run_step_select(ctx, 0, 0, nullptr);
+    if (rc) return rc;
+    CU(cudaMemcpyAsync(&count, ctx->wcount, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    const int64_t m = std::min<int64_t>(cap, ctx->n);
+    if (m > 0 && out_idx && out_gain) {
+      // optimistic: the first `cap` entries travel with the same sync
+      CU(cudaMemcpyAsync(out_idx, ctx->wlist, (size_t)m * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+      CU(cudaMemcpyAsync(out_gain, ctx->wgain, (size_t)m * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    }
+  }
+  CU(cudaMemcpyAsync(out_current, ctx->cur, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  *out_count = count;
+  return EBC_OK;
+}
+
+int ebc_shard_fetch(const ebc_ctx* ctx, int64_t* out_idx, double* out_gain, int64_t count) {
+  if (!ctx || (count > 0 && (!out_idx || !out_gain))) return fail(nullptr, EBC_EINVAL, "ebc_shard_fetch: NULL argument");
+  if (count > ctx->n) return fail(const_cast<ebc_ctx*>(ctx), EBC_EINVAL, "ebc_shard_fetch: count exceeds n");
+  if (count <= 0) return EBC_OK;
+  if (cudaMemcpy(out_idx, ctx->wlist, (size_t)count * sizeof(int64_t), cudaMemcpyDeviceToHost) != cudaSuccess ||
+      cudaMemcpy(out_gain, ctx->wgain, (size_t)count * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return fail(const_cast<ebc_ctx*>(ctx), EBC_ECUDA, "ebc_shard_fetch: copy failed");
+  return EBC_OK;
+}
+
 int ebc_shard_commit(ebc_ctx* ctx, int64_t s, double* out_value) {
   if (!ctx) return fail(nullptr, EBC_EINVAL, "ebc_shard_commit: NULL context");
   if (s < 0 || s >= ctx->n)

@@ -125,6 +125,25 @@ class NativeShardEngine:
         m = int(count.value)
         return self._idx[:m].copy(), self._gain[:m].copy(), float(cur.value)
 
+    def advance(self, commit_idx: int, run_step: bool):
+        """Commit `commit_idx` (-1: none) and screen the next step, one host sync."""
+        count = ctypes.c_int64()
+        cur = ctypes.c_double()
+        rc = self.lib.ebc_shard_advance(self.ctx, int(commit_idx), 1 if run_step else 0,
+                                        self._idx.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                        self._gain.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), self.cap,
+                                        ctypes.byref(count), ctypes.byref(cur))
+        _native.check(rc, self.ctx)
+        m = int(count.value)
+        if m > self.cap:
+            self.cap = m
+            self._idx = np.empty(m, dtype=np.int64)
+            self._gain = np.empty(m, dtype=np.float64)
+            _native.check(self.lib.ebc_shard_fetch(self.ctx, self._idx.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                                   self._gain.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), m),
+                          self.ctx)
+        return self._idx[:m].copy(), self._gain[:m].copy(), float(cur.value)
+
     def commit(self, s: int) -> float:
         out = ctypes.c_double()
         _native.check(self.lib.ebc_shard_commit(self.ctx, int(s), ctypes.byref(out)), self.ctx)
@@ -136,17 +155,20 @@ class NativeShardEngine:
 
 
 def greedy_sharded_loop(engine, n: int, k: int, group=None, device=None) -> Summary:
-    """Drive k sharded Greedy steps with any engine exposing local_step/commit."""
+    """Drive k sharded Greedy steps with any engine exposing
+    advance(commit_idx, run_step) -> (idx, gain, f(S)): one device round trip
+    and one all-gather per step."""
     t0 = time.perf_counter()
     selected: List[int] = []
     gains: List[float] = []
     current = 0.0
     evaluations = 0
+    idx, gain, cur = engine.advance(-1, True)
     for step in range(k):
-        idx, gain, cur = engine.local_step()
         all_idx, all_gain = allgather_candidates(idx, gain, group=group, device=device)
         best, _top = pick(all_idx, all_gain, cur, n)
-        newval = engine.commit(best)
+        idx, gain, newval = engine.advance(best, step + 1 < k)
+        cur = newval
         evaluations += n - step
         gains.append(newval - current)
         current = newval

@@ -172,13 +172,14 @@ def test_emulated_sharding_bit_identical(world):
     fs = [fn(X, eb.Precision.FP32) for _ in range(world)]
     engines = [NativeShardEngine(f, *shard_range(X.shape[0], r, world)) for r, f in enumerate(fs)]
     sel, vals = [], []
-    for _ in range(k):
-        parts = [e.local_step() for e in engines]
+    parts = [e.advance(-1, True) for e in engines]
+    for step in range(k):
         cur = parts[0][2]
         assert all(p[2] == cur for p in parts)
         best, _ = pick(np.concatenate([p[0] for p in parts]), np.concatenate([p[1] for p in parts]), cur,
                        X.shape[0])
-        newvals = [e.commit(best) for e in engines]
+        parts = [e.advance(best, step + 1 < k) for e in engines]
+        newvals = [p[2] for p in parts]
         assert len(set(newvals)) == 1
         sel.append(best)
         vals.append(newvals[0])

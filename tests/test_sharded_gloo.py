@@ -40,6 +40,12 @@ class ExactShardEngine:
             gains[a] = np.maximum(self.cm - d, 0.0).sum()
         return idx, gains, self.cur
 
+    def advance(self, commit_idx, run_step):
+        cur = self.commit(commit_idx) if commit_idx >= 0 else self.cur
+        if not run_step:
+            return np.zeros(0, dtype=np.int64), np.zeros(0), cur
+        return self.local_step()
+
     def commit(self, s):
         d = ((self.V - self.V[s]) ** 2).sum(axis=1)
         self.cm = np.minimum(self.cm, d)
@@ -69,8 +75,8 @@ def _worker(rank, world, port, V, k, q):
 @pytest.mark.parametrize("world", [2, 3])
 def test_sharded_greedy_matches_single_process(world):
     rng = np.random.default_rng(17)
-    V = rng.standard_normal((61, 4))
-    V[40] = V[7]  # exact duplicate across shards: the lowest index must win
+    V = rng.standard_normal((300, 4))
+    V[200] = V[7]  # exact duplicate across shards: the lowest index must win
     k = 6
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
