@@ -343,21 +343,29 @@ def run_ours(args):
                      "work": "W = 2d FP32 FMA-pipe ops per point-candidate pair (SURVEY.md §8(d)), not redefined; "
                              "peak = 148 SM x 128 lanes x 1.965 GHz (nominal)"}
         if rung == 0:
-            # tensor rung: 3xTF32 products = 3 x 2d flops per pair on tcgen05 kind::tf32; TF32 runs at half
-            # the BF16 rate on sm_100, so the peak is the driver-measured dense BF16 figure / 2
+            # tensor rung: 3 split products = 3 x 2d flops per pair (d, not the padded K).
+            # BF16 split (kind::f16): peak = driver-measured dense BF16; TF32 split
+            # (kind::tf32, half the BF16 rate on sm_100): peak = measured BF16 / 2
+            info = optimize.screen_info(f)
+            bf = info[2] == 1
             peaks = load_measured_peaks()
             bf16 = peaks.get("bf16_tflops") if peaks else None
-            tpeak = (bf16 / 2.0) if bf16 else 1590.0 / 2.0
+            base = bf16 if bf16 else 1590.0
+            tpeak = base if bf else base / 2.0
             tach = 6.0 * d * E / (scr * 1e-3) / 1e12
             line["roofline"] = {
-                "bound": "tensor", "kernel": "k_screen_tc (tcgen05 3xTF32 Gram screen, TMEM epilogue)",
+                "bound": "tensor",
+                "kernel": "k_screen_tc (tcgen05 %s Gram screen, TMEM operands and accumulators)"
+                          % ("BF16x3 kind::f16" if bf else "3xTF32 kind::tf32"),
                 "achieved": tach, "peak": tpeak, "unit": "TFLOP/s", "frac": tach / tpeak,
-                "peak_source": ("MEASURED_PEAKS.json bf16_tflops / 2" if bf16 else "fallback 1.59 PF bf16 / 2")
-                               + "; nominal dense TF32 = 1125 TFLOP/s",
+                "peak_source": ("MEASURED_PEAKS.json bf16_tflops" if bf16 else "fallback 1.59 PF bf16")
+                               + ("" if bf else " / 2 (TF32)") + "; nominal dense BF16 = 2250 TFLOP/s",
                 "traffic": traffic,
-                "work": "6d TF32 flops per point-candidate pair (3 products hi.hi + hi.lo + lo.hi, d not padded)",
+                "work": "6d tensor flops per point-candidate pair (3 split products, d not padded)",
                 "fma_equiv": dict(fma_equiv, flag="frac > 1.0 expected: tensor cores vs the FP32 FMA roofline"),
                 "screen_ms_per_step": scr, "screen_share_of_step": scr / step_ms, "screen_rung": rung,
+                "screen_info": {"mode": info[0], "tile_points": info[1], "split": "bf16" if bf else "tf32",
+                                "kpad": info[3]},
             }
         else:
             line["roofline"] = {

@@ -129,6 +129,12 @@ int ebc_last_timings(const ebc_ctx* ctx, double* out_ms4);
  * Gram, 1 FFMA Gram, 2 direct, -1 n/a), [3] steps. */
 int ebc_last_stats(const ebc_ctx* ctx, int64_t* out4);
 
+/* Screen configuration: [0] mode (0 direct, 1 FFMA Gram, 2 ladder from FFMA
+ * Gram, 3 ladder from the tensor screen), [1] points per tensor tile (0: no
+ * tensor screen), [2] tensor operand split (1 BF16 h+m, 0 TF32 hi+lo, -1 n/a),
+ * [3] padded K of the tensor operands. */
+int ebc_screen_info(const ebc_ctx* ctx, int64_t* out4);
+
 /* Kernel launches issued by the last call (bench.py's gpu_launches). */
 int64_t ebc_last_launches(const ebc_ctx* ctx);
 

@@ -45,6 +45,7 @@ SIGNATURES = {
     "ebc_last_timings": (ctypes.c_int, [_vp, _f64p]),
     "ebc_last_launches": (_i64, [_vp]),
     "ebc_last_stats": (ctypes.c_int, [_vp, _i64p]),
+    "ebc_screen_info": (ctypes.c_int, [_vp, _i64p]),
     "ebc_destroy": (None, [_vp]),
     "ebc_last_error": (ctypes.c_char_p, [_vp]),
 }

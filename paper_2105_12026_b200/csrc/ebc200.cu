@@ -840,6 +840,15 @@ int ebc_last_timings(const ebc_ctx* ctx, double* out_ms4) {
 
 int64_t ebc_last_launches(const ebc_ctx* ctx) { return ctx ? ctx->launches : -1; }
 
+int ebc_screen_info(const ebc_ctx* ctx, int64_t* out4) {
+  if (!ctx || !out4) return fail(nullptr, EBC_EINVAL, "ebc_screen_info: NULL argument");
+  out4[0] = ctx->screen_mode;
+  out4[1] = ctx->tc_np;
+  out4[2] = ctx->tc_np ? ctx->tc_bf16 : -1;
+  out4[3] = ctx->kpad;
+  return EBC_OK;
+}
+
 int ebc_last_stats(const ebc_ctx* ctx, int64_t* out4) {
   if (!ctx || !out4) return fail(nullptr, EBC_EINVAL, "ebc_last_stats: NULL argument");
   long long v[4];

@@ -110,6 +110,14 @@ def last_stats(f: EbcFunction):
     return tuple(int(x) for x in out)
 
 
+def screen_info(f: EbcFunction):
+    """(mode, tensor tile points, tensor split 1=BF16/0=TF32/-1, padded K)."""
+    out = np.zeros(4, dtype=np.int64)
+    _native.check(f._lib.ebc_screen_info(f.native_context, out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))),
+                  f.native_context)
+    return tuple(int(x) for x in out)
+
+
 def last_launches(f: EbcFunction) -> int:
     return int(f._lib.ebc_last_launches(f.native_context))
 
