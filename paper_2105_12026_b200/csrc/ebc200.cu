@@ -408,7 +408,10 @@ int run_step_select(ebc_ctx* ctx, int step, int commit, int64_t* sel_dev) {
   if (rc == EBC_EINVAL) rc = run_window_all(ctx, eb, fin_blocks);
   if (rc) return rc;
   // exact fp64 gains of the window
-  const int ng = std::min(ctx->nchunks, 32);
+  // point-chunk groups per window candidate: as many as 256 MB of partials allow
+  // (a short window is latency-bound: more groups = more blocks in flight)
+  const int64_t ng_mem = (int64_t)(256ull << 20) / (8 * (ctx->n + RW));
+  const int ng = (int)std::max<int64_t>(1, std::min<int64_t>(ctx->nchunks, std::max<int64_t>(32, ng_mem)));
   rc = ensure(ctx, ctx->part_r, (size_t)(ctx->n + RW) * ng * sizeof(double));
   if (rc) return rc;
   const int rgrid = 4 * ctx->num_sms;
