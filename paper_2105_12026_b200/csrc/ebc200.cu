@@ -101,6 +101,7 @@ struct ebc_ctx {
     cudaGraphExec_t exec;
   };
   std::vector<Graph> graphs;
+  std::vector<int> eager_ks;  // k values run eagerly once (captured on the next run)
   int64_t alloc_epoch = 0;
   bool use_graphs = true;
   // timing / accounting
@@ -884,47 +885,51 @@ int ebc_greedy(ebc_ctx* ctx, int32_t k, int64_t* out_sel, double* out_val, doubl
   CU(cudaEventCreate(&tstart));
   CU(cudaEventCreate(&tend));
   CU(cudaEventRecord(tstart, ctx->stream));
-  // The k-step loop has no host decision in it, so after one eager run it is
-  // captured as a CUDA graph and later runs with the same k replay it (one
-  // launch instead of ~10 per step: matters for small N, e.g. C1).
+  // The k-step loop has no host decision in it, so the second run with the
+  // same k is captured as a CUDA graph and launched; later runs replay it (one
+  // launch instead of ~10 per step: matters for small N, e.g. C1).  The first
+  // run stays eager, so a context used once (the e2e path) never pays for
+  // capture + instantiation.
   const bool graph_ok = ctx->use_graphs && !ctx->timing;
   ebc_ctx::Graph* cached = nullptr;
   for (auto& g : ctx->graphs)
     if (g.k == k && g.epoch == ctx->alloc_epoch) cached = &g;
+  const bool seen = std::find(ctx->eager_ks.begin(), ctx->eager_ks.end(), k) != ctx->eager_ks.end();
+  if (graph_ok && !cached && seen) {
+    const int64_t before = ctx->launches;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    bool ok = cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+    const int64_t epoch = ctx->alloc_epoch;
+    if (ok) {
+      const int crc = enqueue_greedy(ctx, k);
+      ok = cudaStreamEndCapture(ctx->stream, &graph) == cudaSuccess && crc == EBC_OK && epoch == ctx->alloc_epoch;
+    }
+    if (ok) ok = cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess;
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();  // a failed capture only disables graphs
+    if (ok) {
+      for (auto it = ctx->graphs.begin(); it != ctx->graphs.end();)
+        if (it->k == k) {
+          cudaGraphExecDestroy(it->exec);
+          it = ctx->graphs.erase(it);
+        } else {
+          ++it;
+        }
+      ctx->graphs.push_back({k, epoch, ctx->launches - before, exec});
+      cached = &ctx->graphs.back();
+    } else {
+      ctx->use_graphs = false;
+    }
+    ctx->launches = before;
+  }
   if (graph_ok && cached) {
     CU(cudaGraphLaunch(cached->exec, ctx->stream));
     ctx->launches = cached->launches;
   } else {
     rc = enqueue_greedy(ctx, k);
     if (rc) return rc;
-    if (graph_ok) {
-      const int64_t before = ctx->launches;
-      cudaGraph_t graph = nullptr;
-      cudaGraphExec_t exec = nullptr;
-      bool ok = cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
-      const int64_t epoch = ctx->alloc_epoch;
-      if (ok) {
-        const int crc = enqueue_greedy(ctx, k);
-        ok = cudaStreamEndCapture(ctx->stream, &graph) == cudaSuccess && crc == EBC_OK &&
-             epoch == ctx->alloc_epoch;
-      }
-      if (ok) ok = cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess;
-      if (graph) cudaGraphDestroy(graph);
-      cudaGetLastError();  // a failed capture only disables graphs
-      if (ok) {
-        for (auto it = ctx->graphs.begin(); it != ctx->graphs.end();)
-          if (it->k == k) {
-            cudaGraphExecDestroy(it->exec);
-            it = ctx->graphs.erase(it);
-          } else {
-            ++it;
-          }
-        ctx->graphs.push_back({k, epoch, ctx->launches - before, exec});
-      } else {
-        ctx->use_graphs = false;
-      }
-      ctx->launches = before;
-    }
+    if (!seen) ctx->eager_ks.push_back(k);
   }
   CU(cudaEventRecord(tend, ctx->stream));
   CU(cudaMemcpyAsync(out_sel, ctx->sel_out.p, (size_t)k * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));

@@ -395,18 +395,29 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
           mbar_arrive(&tempty[b]);  // this thread's columns of the buffer are in registers
         }
         const float4* pp4 = reinterpret_cast<const float4*>(pp + h * 32);
-        float g = 0.f;
+        // b = S + ip per pair, a = b + ic.  fl(b + ic) is monotone in b, so
+        // max_i a_i = fl(max_i b_i + ic): when that is <= thr (< 0) every pair
+        // of the chunk adds exactly 0 to the gain and to the count, and the
+        // chunk is skipped -- the common case (few points are closer to a
+        // candidate than to the current summary).
+        float mb = -INFINITY;
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const float4 p = __ldg(pp4 + i);  // {ip, kp} of two points, broadcast through L1
-          const float a0 = (p.x + ic) + S[2 * i];
-          const float a1 = (p.z + ic) + S[2 * i + 1];
-          g += fmaxf(a0, 0.f);
-          g += fmaxf(a1, 0.f);
-          cnt += (a0 > thr) ? 1.f : 0.f;
-          cnt += (a1 > thr) ? 1.f : 0.f;
+          S[2 * i] += p.x;
+          S[2 * i + 1] += p.z;
+          mb = fmaxf(mb, fmaxf(S[2 * i], S[2 * i + 1]));
         }
-        g64 += (double)g;
+        if (mb + ic > thr) {
+          float g = 0.f;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float a = S[i] + ic;
+            g += fmaxf(a, 0.f);
+            cnt += (a > thr) ? 1.f : 0.f;
+          }
+          g64 += (double)g;
+        }
       }
       e = fmaf(cnt, kq, e);
     }
