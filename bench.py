@@ -343,29 +343,32 @@ def run_ours(args):
                      "work": "W = 2d FP32 FMA-pipe ops per point-candidate pair (SURVEY.md §8(d)), not redefined; "
                              "peak = 148 SM x 128 lanes x 1.965 GHz (nominal)"}
         if rung == 0:
-            # tensor rung: 3 split products = 3 x 2d flops per pair (d, not the padded K).
-            # BF16 split (kind::f16): peak = driver-measured dense BF16; TF32 split
-            # (kind::tf32, half the BF16 rate on sm_100): peak = measured BF16 / 2
+            # tensor rung.  BF16 split (kind::f16): 3 products = 6d flops per pair
+            # against the driver-measured dense BF16 peak; FP16 grounds (kind::f16,
+            # one exact product) 2d flops per pair, same peak; TF32 split
+            # (kind::tf32, half the BF16 rate on sm_100): 6d against measured BF16 / 2
             info = optimize.screen_info(f)
-            bf = info[2] == 1
+            kind = int(info[2])
+            kname = {0: "3xTF32 kind::tf32", 1: "BF16x3 kind::f16", 2: "FP16x1 kind::f16"}[kind]
+            nprod = 1 if kind == 2 else 3
             peaks = load_measured_peaks()
             bf16 = peaks.get("bf16_tflops") if peaks else None
             base = bf16 if bf16 else 1590.0
-            tpeak = base if bf else base / 2.0
-            tach = 6.0 * d * E / (scr * 1e-3) / 1e12
+            tpeak = base / 2.0 if kind == 0 else base
+            tach = 2.0 * nprod * d * E / (scr * 1e-3) / 1e12
             line["roofline"] = {
                 "bound": "tensor",
-                "kernel": "k_screen_tc (tcgen05 %s Gram screen, TMEM operands and accumulators)"
-                          % ("BF16x3 kind::f16" if bf else "3xTF32 kind::tf32"),
+                "kernel": "k_screen_tc (tcgen05 %s Gram screen, TMEM operands and accumulators)" % kname,
                 "achieved": tach, "peak": tpeak, "unit": "TFLOP/s", "frac": tach / tpeak,
                 "peak_source": ("MEASURED_PEAKS.json bf16_tflops" if bf16 else "fallback 1.59 PF bf16")
-                               + ("" if bf else " / 2 (TF32)") + "; nominal dense BF16 = 2250 TFLOP/s",
+                               + (" / 2 (TF32)" if kind == 0 else "") + "; nominal dense BF16 = 2250 TFLOP/s",
                 "traffic": traffic,
-                "work": "6d tensor flops per point-candidate pair (3 split products, d not padded)",
+                "work": "%dd tensor flops per point-candidate pair (%d product%s, d not padded)"
+                        % (2 * nprod, nprod, "s of the split" if nprod > 1 else " of the fp16 values"),
                 "fma_equiv": dict(fma_equiv, flag="frac > 1.0 expected: tensor cores vs the FP32 FMA roofline"),
                 "screen_ms_per_step": scr, "screen_share_of_step": scr / step_ms, "screen_rung": rung,
-                "screen_info": {"mode": info[0], "tile_points": info[1], "split": "bf16" if bf else "tf32",
-                                "kpad": info[3]},
+                "screen_info": {"mode": info[0], "tile_points": info[1],
+                                "operands": {0: "tf32 split", 1: "bf16 split", 2: "fp16"}[kind], "kpad": info[3]},
             }
         else:
             line["roofline"] = {

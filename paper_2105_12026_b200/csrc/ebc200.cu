@@ -69,8 +69,8 @@ struct ebc_ctx {
   // tensor-core Gram screen (tcgen05, kind::tf32, 3xTF32)
   void* Vhi = nullptr;
   void* Vlo = nullptr;
-  int tc_bf16 = 0;  // 1: BF16 split (kind::f16), 0: TF32 split (kind::tf32)
-  float2* pttc = nullptr;
+  int tc_kind = 1;  // tc::KIND_TF32 / KIND_BF16 (fp32 grounds) / KIND_F16 (fp16 grounds)
+  float* pttc = nullptr;  // per point ip = (cm32 - |v|^2)/2, the tensor screen seed
   float* kpmax = nullptr;  // per tensor tile: max error quantum kp (reset state)
   int kpad = 0;
   int tc_np = 0;  // points per tensor tile (0: tensor screen unavailable)
@@ -297,12 +297,15 @@ struct TcPlan {
   size_t smem;
 };
 
+int tc_es(int kind) { return kind == tc::KIND_TF32 ? 4 : 2; }
+int tc_parts(int kind) { return kind == tc::KIND_F16 ? 1 : 2; }
+
 bool plan_tc(const ebc_ctx* ctx, TcPlan& p) {
   if (!ctx->tc_np || (ctx->c0 % 8) != 0) return false;
   const int64_t ncand = ctx->c1 - ctx->c0;
   p.ncb = (int)((ncand + tc::M - 1) / tc::M);
   p.ntiles = (int)((ctx->n + ctx->tc_np - 1) / ctx->tc_np);
-  p.smem = tc::smem_bytes(ctx->kpad, ctx->tc_np, ctx->tc_bf16 ? 2 : 4);
+  p.smem = tc::smem_bytes(ctx->kpad, ctx->tc_np, tc_es(ctx->tc_kind), tc_parts(ctx->tc_kind));
   const int64_t slots = ctx->num_sms;  // one CTA per SM
   double best_cost = 1e300;
   p.tps = p.ntiles;
@@ -320,14 +323,14 @@ bool plan_tc(const ebc_ctx* ctx, TcPlan& p) {
   return true;
 }
 
-template <int NP, bool BF>
+template <int NP, int KIND>
 int launch_tc_t(ebc_ctx* ctx, const TcPlan& p, const int* level_now, int level) {
-  auto kern = k_screen_tc<NP, BF>;
+  auto kern = k_screen_tc<NP, KIND>;
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
   dim3 grid(p.ncb, p.nsplit);
   kern<<<grid, tc::THREADS, p.smem, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->d, (const unsigned char*)ctx->Vhi,
                                                    (const unsigned char*)ctx->Vlo, ctx->pttc, ctx->kpmax, ctx->nv32, ctx->kpad,
-                                                   tc::stages_for(ctx->kpad, ctx->tc_np, BF ? 2 : 4), ctx->c0,
+                                                   tc::stages_for(ctx->kpad, ctx->tc_np, tc_es(KIND), tc_parts(KIND)), ctx->c0,
                                                    p.ntiles, p.tps, (double*)ctx->part_g.p, (float*)ctx->part_e.p,
                                                    ctx->n_pad, ctx->tc_kc, level_now, level);
   KCHECK();
@@ -335,14 +338,17 @@ int launch_tc_t(ebc_ctx* ctx, const TcPlan& p, const int* level_now, int level) 
 }
 
 int launch_tc(ebc_ctx* ctx, const TcPlan& p, const int* level_now, int level) {
-  if (ctx->tc_bf16) {
-    if (ctx->tc_np == 128) return launch_tc_t<128, true>(ctx, p, level_now, level);
-    if (ctx->tc_np == 64) return launch_tc_t<64, true>(ctx, p, level_now, level);
-    return launch_tc_t<32, true>(ctx, p, level_now, level);
+  switch (ctx->tc_kind) {
+    case tc::KIND_F16:
+      if (ctx->tc_np == 128) return launch_tc_t<128, tc::KIND_F16>(ctx, p, level_now, level);
+      return launch_tc_t<64, tc::KIND_F16>(ctx, p, level_now, level);
+    case tc::KIND_BF16:
+      if (ctx->tc_np == 128) return launch_tc_t<128, tc::KIND_BF16>(ctx, p, level_now, level);
+      return launch_tc_t<64, tc::KIND_BF16>(ctx, p, level_now, level);
+    default:
+      if (ctx->tc_np == 128) return launch_tc_t<128, tc::KIND_TF32>(ctx, p, level_now, level);
+      return launch_tc_t<64, tc::KIND_TF32>(ctx, p, level_now, level);
   }
-  if (ctx->tc_np == 128) return launch_tc_t<128, false>(ctx, p, level_now, level);
-  if (ctx->tc_np == 64) return launch_tc_t<64, false>(ctx, p, level_now, level);
-  return launch_tc_t<32, false>(ctx, p, level_now, level);
 }
 
 // fp32 screen of the candidate range + certified window.
@@ -720,33 +726,40 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
   // tensor-core screen: fp32-path grounds whose 128-candidate tile of hi+lo
   // operands plus a 2-stage ring of NP-point tiles fits shared memory
   if (dtype != EBC_F64 && ctx->screen_mode == 3) {
+    // FP16 grounds: one exact FP16 product; fp32 grounds: the BF16 split
     const char* kind = getenv("EBC200_TC_KIND");
-    ctx->tc_bf16 = (kind && kind[0]) ? atoi(kind) : 1;
-    const int es = ctx->tc_bf16 ? 2 : 4;
-    ctx->kpad = ctx->tc_bf16 ? (d + 15) / 16 * 16 : (d + 7) / 8 * 8;
-    int nps[3] = {128, 64, 32};
+    ctx->tc_kind = (kind && kind[0]) ? atoi(kind) : (dtype == EBC_F16 ? tc::KIND_F16 : tc::KIND_BF16);
+    if (ctx->tc_kind == tc::KIND_F16 && dtype != EBC_F16) ctx->tc_kind = tc::KIND_BF16;  // fp32 values are not fp16
+    if (ctx->tc_kind < 0 || ctx->tc_kind > 2) ctx->tc_kind = tc::KIND_BF16;
+    const int es = tc_es(ctx->tc_kind), parts = tc_parts(ctx->tc_kind);
+    ctx->kpad = es == 2 ? (d + 15) / 16 * 16 : (d + 7) / 8 * 8;
+    int nps[2] = {128, 64};  // points per tile (64 only for wide TF32 operands)
     const char* npenv = getenv("EBC200_TC_NP");
-    if (npenv && npenv[0]) nps[0] = atoi(npenv);
+    if (npenv && atoi(npenv) == 64) nps[0] = 64;
     for (int np : nps) {
-      if (ctx->kpad <= 128 && tc::stages_for(ctx->kpad, np, es) >= 2) {
+      if (ctx->kpad <= 128 && tc::stages_for(ctx->kpad, np, es, parts) >= 2) {
         ctx->tc_np = np;
         break;
       }
     }
     if (ctx->tc_np) {
       const double u = 5.960464477539063e-08;
-      // split error (dropped low-order products) + fp32 accumulation of 3*kpad products
-      const double split = ctx->tc_bf16 ? 3.1 * std::ldexp(1.0, -18) : 3.0 * std::ldexp(1.0, -20);
-      const double ktc = split + (3.0 * ctx->kpad + 16.0) * std::ldexp(1.0, -23);
+      // split error (dropped low-order products) + fp32 accumulation of parts*kpad
+      // products (FP16: no split error, fp16 x fp16 products are exact)
+      const double split = ctx->tc_kind == tc::KIND_F16    ? 0.0
+                           : ctx->tc_kind == tc::KIND_BF16 ? 3.1 * std::ldexp(1.0, -18)
+                                                           : 3.0 * std::ldexp(1.0, -20);
+      const double nprod = ctx->tc_kind == tc::KIND_F16 ? 1.0 : 3.0;
+      const double ktc = split + (nprod * ctx->kpad + 16.0) * std::ldexp(1.0, -23);
       ctx->tc_ka = (float)(4.0 * u * 1.01);
       ctx->tc_kb = (float)((4.0 * u + 0.5 * ktc) * 1.01);
       ctx->tc_kc = (float)((4.0 * u + 0.5 * ktc) * 1.01);
       const size_t ve = (size_t)ctx->n_pad * ctx->kpad;
       CUC(cudaMalloc(&ctx->Vhi, ve * es));
-      CUC(cudaMalloc(&ctx->Vlo, ve * es));
-      CUC(cudaMalloc(&ctx->pttc, (size_t)ctx->n_pad * sizeof(float2)));
+      if (parts == 2) CUC(cudaMalloc(&ctx->Vlo, ve * es));
+      CUC(cudaMalloc(&ctx->pttc, (size_t)ctx->n_pad * sizeof(float)));
       CUC(cudaMalloc(&ctx->kpmax, (size_t)(ctx->n_pad / ctx->tc_np + 1) * sizeof(float)));
-      CUC(cudaMemsetAsync(ctx->pttc, 0, (size_t)ctx->n_pad * sizeof(float2), ctx->stream));
+      CUC(cudaMemsetAsync(ctx->pttc, 0, (size_t)ctx->n_pad * sizeof(float), ctx->stream));
     }
   }
   CUC(cudaMalloc(&ctx->selected, (size_t)ctx->n_pad));
@@ -786,10 +799,14 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
   if (ctx->tc_np) {
     {
       const int64_t ntl = ctx->n_pad / ctx->tc_np;
-      k_tile_kpmax<<<(unsigned)((ntl + 255) / 256), 256, 0, ctx->stream>>>(ctx->pttc, ntl, ctx->tc_np, ctx->kpmax);
+      k_tile_kpmax<<<(unsigned)((ntl + 255) / 256), 256, 0, ctx->stream>>>(ctx->e0d, ctx->nv32, n, ntl, ctx->tc_np,
+                                                                            ctx->tc_ka, ctx->tc_kb, ctx->kpmax);
       CUC(cudaGetLastError());
     }
-    if (ctx->tc_bf16)
+    if (ctx->tc_kind == tc::KIND_F16)
+      k_split_f16<<<8 * ctx->num_sms, 256, 0, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->n_pad, d, ctx->kpad,
+                                                            (__half*)ctx->Vhi);
+    else if (ctx->tc_kind == tc::KIND_BF16)
       k_split_bf16<<<8 * ctx->num_sms, 256, 0, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->n_pad, d, ctx->kpad,
                                                              (__nv_bfloat16*)ctx->Vhi, (__nv_bfloat16*)ctx->Vlo);
     else
@@ -848,7 +865,7 @@ int ebc_screen_info(const ebc_ctx* ctx, int64_t* out4) {
   if (!ctx || !out4) return fail(nullptr, EBC_EINVAL, "ebc_screen_info: NULL argument");
   out4[0] = ctx->screen_mode;
   out4[1] = ctx->tc_np;
-  out4[2] = ctx->tc_np ? ctx->tc_bf16 : -1;
+  out4[2] = ctx->tc_np ? ctx->tc_kind : -1;
   out4[3] = ctx->kpad;
   return EBC_OK;
 }

@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_init(const T* __restrict__ V, i
                                                       const double* __restrict__ e0, PtCoef pk,
                                                       double* __restrict__ e0d, double* __restrict__ cm64,
                                                       float* __restrict__ nv32, float4* __restrict__ pt,
-                                                      double* __restrict__ part, float2* __restrict__ pttc,
+                                                      double* __restrict__ part, float* __restrict__ pttc,
                                                       float tc_ka, float tc_kb) {
   __shared__ double sbuf[RED_THREADS];
   __shared__ double se0[1024];
@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_init(const T* __restrict__ V, i
       const float n32 = (float)nv;
       nv32[v] = n32;
       pt[v] = make_pt((float)t, n32, pk);
-      if (pttc) pttc[v] = make_float2(((float)t - n32) * 0.5f, tc_ka * (float)t + tc_kb * n32);
+      if (pttc) pttc[v] = ((float)t - n32) * 0.5f;
       acc += t;
     }
   }
@@ -149,14 +149,14 @@ __global__ void __launch_bounds__(RED_THREADS) k_init(const T* __restrict__ V, i
 // Reset the cached minima to d(., e0) (ebc_reset / start of a Greedy run).
 __global__ void k_reset(int64_t n, const double* __restrict__ e0d, const float* __restrict__ nv32, PtCoef pk,
                         double* __restrict__ cm64, float4* __restrict__ pt, unsigned char* __restrict__ selected,
-                        int* __restrict__ sticky, float2* __restrict__ pttc, float tc_ka, float tc_kb) {
+                        int* __restrict__ sticky, float* __restrict__ pttc, float tc_ka, float tc_kb) {
   int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (v == 0 && sticky) *sticky = 0;
   if (v < n) {
     double t = e0d[v];
     cm64[v] = t;
     pt[v] = make_pt((float)t, nv32[v], pk);
-    if (pttc) pttc[v] = make_float2(((float)t - nv32[v]) * 0.5f, tc_ka * (float)t + tc_kb * nv32[v]);
+    if (pttc) pttc[v] = ((float)t - nv32[v]) * 0.5f;
     selected[v] = 0;
   }
 }
@@ -757,7 +757,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_update(const T* __restrict__ V,
                                                         const int64_t* __restrict__ best, PtCoef pk,
                                                         const double* __restrict__ e0d, const float* __restrict__ nv32,
                                                         double* __restrict__ cm64, float4* __restrict__ pt,
-                                                        float2* __restrict__ pttc, float tc_ka, float tc_kb,
+                                                        float* __restrict__ pttc, float tc_ka, float tc_kb,
                                                         double* __restrict__ fpart,
                                                         unsigned int* __restrict__ counter, double inv_n,
                                                         double* __restrict__ cur, double* __restrict__ val_out,
@@ -779,7 +779,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_update(const T* __restrict__ V,
         m = t;
         cm64[v] = m;
         pt[v] = make_pt((float)m, nv32[v], pk);
-        if (pttc) pttc[v] = make_float2(((float)m - nv32[v]) * 0.5f, tc_ka * (float)m + tc_kb * nv32[v]);
+        if (pttc) pttc[v] = ((float)m - nv32[v]) * 0.5f;
       }
       acc += e0d[v] - m;
     }

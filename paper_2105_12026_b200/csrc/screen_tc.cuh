@@ -24,6 +24,7 @@
 #include <cstdint>
 
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include "ptx.cuh"
 
@@ -51,6 +52,16 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
+// kind::f16 with FP16 A/B (format 0), fp32 D, both K-major
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
+  return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// Operand kinds of the tensor screen.
+//   KIND_TF32: 3xTF32 split (kind::tf32), KIND_BF16: 3-product BF16 split
+//   (kind::f16), KIND_F16: FP16-stored grounds, one exact FP16 product per
+//   element (fp16 x fp16 has 22 significant bits: exact in the fp32 accumulator).
+enum { KIND_TF32 = 0, KIND_BF16 = 1, KIND_F16 = 2 };
 
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
   asm volatile(
@@ -92,6 +103,45 @@ __device__ __forceinline__ void ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 64 consecutive accumulator columns of this warp's lanes, one wait.
+__device__ __forceinline__ void ld64(uint32_t taddr, float (&v)[64]) {
+  uint32_t r[64];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32, %33, %34, %35, "
+      "%36, %37, %38, %39, %40, %41, %42, %43, %44, %45, %46, %47, %48, %49, %50, %51, %52, %53, %54, %55, %56, "
+      "%57, %58, %59, %60, %61, %62, %63}, [%64];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]),
+        "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]),
+        "=r"(r[40]), "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]),
+        "=r"(r[48]), "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]),
+        "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
+      : "r"(taddr)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 64; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+template <int W>
+__device__ __forceinline__ void ldcols(uint32_t taddr, float (&v)[W]) {
+  if constexpr (W == 64) {
+    ld64(taddr, v);
+  } else {
+    static_assert(W % 32 == 0, "columns per thread: multiple of 32");
+#pragma unroll
+    for (int h = 0; h < W / 32; ++h) {
+      float t[32];
+      ld32(taddr + 32 * h, t);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[32 * h + i] = t[i];
+    }
+  }
+}
+
 constexpr int M = 128;        // candidates per CTA (UMMA M)
 constexpr int EPI_WARPGROUPS = 2;  // epilogue warpgroups (slices of the point columns)
 constexpr int MMA_WARPS = 3;       // one issuing warp per accumulator buffer (tiles round-robin)
@@ -99,11 +149,14 @@ constexpr int EPI_WARP0 = 1 + MMA_WARPS;
 constexpr int THREADS = 32 * EPI_WARP0 + 128 * EPI_WARPGROUPS;  // producer + MMA warps + epilogue
 // accumulator buffers: BF16 operands (A = 2 x 56 columns) leave room for 3 x 128
 // fp32 accumulators in the 512 TMEM columns, TF32 (A = 2 x 128) for 2
-template <bool BF>
+template <int KIND>
 struct TmemMap {
-  static constexpr int NB = BF ? 3 : 2;
-  static constexpr uint32_t ALO = BF ? 64 : 128;
-  static constexpr uint32_t ACC = BF ? 128 : 256;
+  static constexpr bool W16 = KIND != KIND_TF32;  // 16-bit operands: 2 elements per TMEM column
+  static constexpr int NB = W16 ? 3 : 2;
+  static constexpr uint32_t ALO = W16 ? 64 : 128;
+  static constexpr uint32_t ACC = W16 ? 128 : 256;
+  static constexpr int PARTS = KIND == KIND_F16 ? 1 : 2;  // operand parts per point tile
+  static constexpr int ES = W16 ? 2 : 4;                  // operand element bytes
 };
 constexpr int MAX_STAGES = 4;
 // TMEM columns: A_hi [0,128), A_lo [128,256), accumulators [256 + b*NP, ...)
@@ -134,6 +187,16 @@ __device__ __forceinline__ void mma3_tf32_ts(uint32_t tmem_d, uint32_t a_hi, uin
       : "memory");
 }
 
+// One FP16 product per K step (KIND_F16).
+__device__ __forceinline__ void mma1_f16_ts(uint32_t tmem_d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, {%5, %5, %5, %5}, p;\n\t}\n" ::"r"(tmem_d),
+      "r"(a), "l"(b), "r"(idesc), "r"(acc), "r"(0)
+      : "memory");
+}
+
 // Same for the BF16 split (kind::f16, K = 16 per instruction).
 __device__ __forceinline__ void mma3_bf16_ts(uint32_t tmem_d, uint32_t a_hi, uint32_t a_lo, uint64_t b_hi,
                                              uint64_t b_lo, uint32_t idesc, uint32_t acc) {
@@ -159,16 +222,19 @@ __device__ __forceinline__ void st32(uint32_t taddr, const uint32_t (&r)[32]) {
       : "memory");
 }
 
-inline int stages_for(int kpad, int np, int es = 4) {
-  const size_t stage = 2 * (size_t)np * kpad * es;
+inline int stages_for(int kpad, int np, int es = 4, int parts = 2) {
+  const size_t stage = (size_t)parts * np * kpad * es;
   const size_t budget = 220 * 1024;
   int st = (int)(budget / stage);
   return st > MAX_STAGES ? MAX_STAGES : st;
 }
 
-inline size_t smem_bytes(int kpad, int np, int es = 4) {
-  const size_t stage = 2 * (size_t)np * kpad * es;  // B_hi, B_lo
-  return stages_for(kpad, np, es) * stage + (2 * MAX_STAGES + 8) * sizeof(uint64_t) + 64;
+inline size_t smem_bytes(int kpad, int np, int es = 4, int parts = 2) {
+  const size_t stage = (size_t)parts * np * kpad * es;  // B_hi (, B_lo)
+  size_t ring = stages_for(kpad, np, es, parts) * stage;
+  const size_t xchg = EPI_WARPGROUPS * 128 * (sizeof(double) + sizeof(float));  // slice exchange reuses the ring
+  if (ring < xchg) ring = xchg;
+  return ring + (2 * MAX_STAGES + 8) * sizeof(uint64_t) + 64;
 }
 
 }  // namespace tc
@@ -212,12 +278,32 @@ __global__ void k_split_bf16(const float* __restrict__ V32, int pitch, int64_t n
   }
 }
 
-// kpmax[t] = max over the NP points of tile t of kp (pttc[v].y).
-__global__ void k_tile_kpmax(const float2* __restrict__ pttc, int64_t ntiles, int np, float* __restrict__ kpmax) {
+// FP16 grounds: V (exactly widened to fp32) back to fp16, same blocked layout.
+__global__ void k_split_f16(const float* __restrict__ V32, int pitch, int64_t nrows, int d, int kpad,
+                            __half* __restrict__ hi) {
+  const int KC = kpad / 8;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t total = nrows * kpad;
+  for (; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = i / kpad;
+    const int k = (int)(i - v * kpad);
+    const float x = k < d ? V32[v * pitch + k] : 0.f;
+    const int64_t off = (((v >> 3) * KC + (k >> 3)) * 8 + (v & 7)) * 8 + (k & 7);
+    hi[off] = __float2half_rn(x);
+  }
+}
+
+// kpmax[t] = max over the NP points of tile t of kp = ka*cm32 + kb*|v|^2 at
+// reset (cm = d(., e0)); cm only decreases within a run, so it bounds every step.
+__global__ void k_tile_kpmax(const double* __restrict__ e0d, const float* __restrict__ nv32, int64_t n,
+                             int64_t ntiles, int np, float ka, float kb, float* __restrict__ kpmax) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t < ntiles) {
     float m = 0.f;
-    for (int i = 0; i < np; ++i) m = fmaxf(m, pttc[t * np + i].y);
+    for (int i = 0; i < np; ++i) {
+      const int64_t v = t * np + i;
+      if (v < n) m = fmaxf(m, ka * (float)e0d[v] + kb * nv32[v]);
+    }
     kpmax[t] = m;
   }
 }
@@ -227,10 +313,10 @@ __global__ void k_tile_kpmax(const float2* __restrict__ pttc, int64_t ntiles, in
 // the tensor core reads only the B tiles from shared memory); B tiles stream
 // through a STAGES-deep bulk-copy ring released by the MMA commit alone; the
 // per-point seed/quantum {ip, kp} is read by the epilogue through L1.
-template <int NP, bool BF>
+template <int NP, int KIND>
 __global__ void __launch_bounds__(tc::THREADS, 1)
     k_screen_tc(const float* __restrict__ V32, int pitch, int d, const unsigned char* __restrict__ Vhi,
-                const unsigned char* __restrict__ Vlo, const float2* __restrict__ pttc,
+                const unsigned char* __restrict__ Vlo, const float* __restrict__ pttc,
                 const float* __restrict__ kpmax, const float* __restrict__ nv32,
                 int kpad, int stages, int64_t cand0, int ntiles, int tiles_per_split, double* __restrict__ part_g,
                 float* __restrict__ part_e, int64_t part_stride, float kc_coef, const int* __restrict__ level_now,
@@ -239,9 +325,11 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   if (level_now && *level_now != level) return;
   extern __shared__ __align__(128) unsigned char smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  constexpr int ES = BF ? 2 : 4;  // operand element bytes
+  using TM = TmemMap<KIND>;
+  constexpr bool BF = TM::W16;  // 16-bit operands (BF16 split or FP16)
+  constexpr int ES = TM::ES;    // operand element bytes
   const uint32_t b_bytes = (uint32_t)NP * kpad * ES;
-  const uint32_t stage_bytes = 2 * b_bytes;
+  const uint32_t stage_bytes = TM::PARTS * b_bytes;
   unsigned char* stage0 = smem;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)stages * stage_bytes);
   uint64_t* full = bars;                   // [stages] operands landed
@@ -288,7 +376,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         const int64_t prow = (int64_t)(t0 + it) * NP;
         mbar_arrive_expect_tx(&full[s], stage_bytes);
         bulk_g2s(st, Vhi + prow * kpad * ES, b_bytes, &full[s]);
-        bulk_g2s(st + b_bytes, Vlo + prow * kpad * ES, b_bytes, &full[s]);
+        if (TM::PARTS == 2) bulk_g2s(st + b_bytes, Vlo + prow * kpad * ES, b_bytes, &full[s]);
       }
     }
   } else if (warp < EPI_WARP0) {
@@ -296,13 +384,14 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     // accumulator buffer b, so one warp's barrier waits and register set-up
     // overlap the other's queued MMAs.  The whole warp walks the loop
     // (warp-uniform operands stay in uniform registers), one elected lane issues.
-    constexpr uint32_t idesc = BF ? idesc_bf16(M, NP) : idesc_tf32(M, NP);
+    constexpr uint32_t idesc =
+        KIND == KIND_F16 ? idesc_f16(M, NP) : (KIND == KIND_BF16 ? idesc_bf16(M, NP) : idesc_tf32(M, NP));
     const uint32_t sbo = (uint32_t)kpad * 8 * ES;  // 8 rows x kpad elements
     const int ksteps = kpad / (BF ? 16 : 8);       // 32 bytes of K per instruction
-    constexpr int NB = TmemMap<BF>::NB;
+    constexpr int NB = TM::NB;
     const int b = warp - 1;
-    const uint32_t dt = tmem + TmemMap<BF>::ACC + (uint32_t)(b * NP);
-    const uint32_t ahi = tmem + COL_AHI, alo = tmem + TmemMap<BF>::ALO;
+    const uint32_t dt = tmem + TM::ACC + (uint32_t)(b * NP);
+    const uint32_t ahi = tmem + COL_AHI, alo = tmem + TM::ALO;
     mbar_wait(aready, 0);
     fence_after();
     for (int it = b; it < nt && b < NB; it += NB) {
@@ -318,7 +407,9 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       if (elect_one()) {
 #pragma unroll 4
         for (int j = 0; j < ksteps; ++j) {
-          if (BF)
+          if (KIND == KIND_F16)
+            mma1_f16_ts(dt, ahi + 8 * j, dhi + 16 * j, idesc, j > 0);
+          else if (KIND == KIND_BF16)
             mma3_bf16_ts(dt, ahi + 8 * j, alo + 8 * j, dhi + 16 * j, dlo + 16 * j, idesc, j > 0);
           else
             mma3_tf32_ts(dt, ahi + 8 * j, alo + 8 * j, dhi + 16 * j, dlo + 16 * j, idesc, j > 0);
@@ -340,13 +431,19 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     {
       // A of this candidate into TMEM: slice 0 writes hi [0,128), the last slice lo [128,256)
       const float* row = V32 + c * pitch;
-      const bool do_hi = half == 0, do_lo = half == EPI_WARPGROUPS - 1;
+      const bool do_hi = half == 0, do_lo = TM::PARTS == 2 && half == EPI_WARPGROUPS - 1;
 #pragma unroll 1
       for (int blk = 0; blk < (BF ? 2 : 4); ++blk) {
         uint32_t rh[32], rl[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
-          if (BF) {
+          if (KIND == KIND_F16) {
+            const int k = blk * 64 + 2 * i;
+            const float x0 = k < d ? row[k] : 0.f, x1 = k + 1 < d ? row[k + 1] : 0.f;
+            rh[i] = (uint32_t)__half_as_ushort(__float2half_rn(x0)) |
+                    ((uint32_t)__half_as_ushort(__float2half_rn(x1)) << 16);
+            rl[i] = 0u;
+          } else if (BF) {
             // column = packed pair (k = 2i, 2i+1), low half = even k
             const int k = blk * 64 + 2 * i;
             const float x0 = k < d ? row[k] : 0.f, x1 = k + 1 < d ? row[k + 1] : 0.f;
@@ -364,7 +461,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
           }
         }
         if (do_hi) st32(tmem + lane_off + COL_AHI + blk * 32, rh);
-        if (do_lo) st32(tmem + lane_off + TmemMap<BF>::ALO + blk * 32, rl);
+        if (do_lo) st32(tmem + lane_off + TM::ALO + blk * 32, rl);
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       fence_before();
@@ -375,51 +472,63 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     const float kc = kc_coef * nc;
     double g64 = 0.0;
     float e = 0.f;
-    constexpr int NB = TmemMap<BF>::NB;
+    constexpr int NB = TM::NB;
+    constexpr int SW = SLICE;  // accumulator columns per thread and tile
     for (int it = 0; it < nt; ++it) {
       const int b = it % NB;
-      const float2* pp = pttc + (int64_t)(t0 + it) * NP + half * SLICE;
+      // this slice's point seeds ip: issued before the accumulator wait so the
+      // (L1-broadcast) loads overlap the MMA
+      float ipv[SW];
+      {
+        const float4* pp4 = reinterpret_cast<const float4*>(pttc + (int64_t)(t0 + it) * NP + half * SLICE);
+#pragma unroll
+        for (int i = 0; i < SW / 4; ++i) {
+          const float4 p = __ldg(pp4 + i);
+          ipv[4 * i] = p.x;
+          ipv[4 * i + 1] = p.y;
+          ipv[4 * i + 2] = p.z;
+          ipv[4 * i + 3] = p.w;
+        }
+      }
       // one error quantum per tile: kpmax = max_v kp over the tile (bounds every
       // pair's kp_v; computed at reset, cm only decreases within a run)
       const float kq = kpmax[t0 + it] + kc;
       const float thr = -kq;
-      float cnt = 0.f;
       mbar_wait(&tfull[b], (it / NB) & 1);
       fence_after();
+      float S[SW];
+      ldcols<SW>(tmem + lane_off + TM::ACC + (uint32_t)(b * NP + half * SLICE), S);
+      fence_before();
+      mbar_arrive(&tempty[b]);  // this thread's columns of the buffer are in registers
+      // b = S + ip per pair, a = b + ic.  fl(b + ic) is monotone in b, so
+      // max_i a_i = fl(max_i b_i + ic): when that is <= thr (< 0) every pair
+      // adds exactly 0 to the gain and to the count, and the tile is skipped --
+      // the common case (few points are closer to a candidate than to the summary).
+      float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-      for (int h = 0; h < SLICE / 32; ++h) {
-        float S[32];
-        ld32(tmem + lane_off + TmemMap<BF>::ACC + (uint32_t)(b * NP + half * SLICE + h * 32), S);
-        if (h == SLICE / 32 - 1) {
-          fence_before();
-          mbar_arrive(&tempty[b]);  // this thread's columns of the buffer are in registers
-        }
-        const float4* pp4 = reinterpret_cast<const float4*>(pp + h * 32);
-        // b = S + ip per pair, a = b + ic.  fl(b + ic) is monotone in b, so
-        // max_i a_i = fl(max_i b_i + ic): when that is <= thr (< 0) every pair
-        // of the chunk adds exactly 0 to the gain and to the count, and the
-        // chunk is skipped -- the common case (few points are closer to a
-        // candidate than to the current summary).
-        float mb = -INFINITY;
+      for (int i = 0; i < SW; ++i) S[i] += ipv[i];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const float4 p = __ldg(pp4 + i);  // {ip, kp} of two points, broadcast through L1
-          S[2 * i] += p.x;
-          S[2 * i + 1] += p.z;
-          mb = fmaxf(mb, fmaxf(S[2 * i], S[2 * i + 1]));
-        }
-        if (mb + ic > thr) {
+      for (int i = 0; i < SW; i += 8) {
+        m4[(i / 8) & 3] = fmaxf(m4[(i / 8) & 3], fmaxf(fmaxf(S[i], S[i + 1]), S[i + 2]));
+        m4[(i / 8) & 3] = fmaxf(m4[(i / 8) & 3], fmaxf(fmaxf(S[i + 3], S[i + 4]), S[i + 5]));
+        m4[(i / 8) & 3] = fmaxf(m4[(i / 8) & 3], fmaxf(S[i + 6], S[i + 7]));
+      }
+      const float mb = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+      if (mb + ic > thr) {
+        float cnt = 0.f;
+#pragma unroll
+        for (int h = 0; h < SW; h += 32) {
           float g = 0.f;
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
+          for (int i = h; i < h + 32; ++i) {
             const float a = S[i] + ic;
             g += fmaxf(a, 0.f);
             cnt += (a > thr) ? 1.f : 0.f;
           }
           g64 += (double)g;
         }
+        e = fmaf(cnt, kq, e);
       }
-      e = fmaf(cnt, kq, e);
     }
     // combine the slices of each candidate in slice order (named barrier over
     // the epilogue warps only)

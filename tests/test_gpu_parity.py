@@ -294,3 +294,33 @@ def test_sieve_validation_and_empty_stream():
         eb.sieve_stream_maximize([0], f, 1, epsilon=1.5)
     s = eb.sieve_stream_maximize([1], f, 1)
     assert s.selected == [1] and s.value == pytest.approx(f.value([1]), rel=1e-12)
+
+
+# ------------------------------------------------------------ every screen implementation
+
+@pytest.mark.parametrize("d", [32, 100])
+@pytest.mark.parametrize("variant", ["tc-tf32", "tc-bf16", "tc-f16", "ffma-gram", "direct"])
+@pytest.mark.parametrize("prec", ["fp32", "fp16-storage"])
+def test_every_screen_variant_vs_oracle(monkeypatch, variant, prec, d):
+    """Each rung of the adaptive ladder and each tensor operand kind, forced by
+    the development switches, selects exactly what the fp64 oracle selects; the
+    ladder stays on the forced rung for Gaussian data."""
+    from paper_2105_12026_b200 import optimize
+    if variant == "tc-f16" and prec != "fp16-storage":
+        pytest.skip("FP16 operands only for fp16-stored grounds")
+    mode, kind, rung = {"tc-tf32": ("3", "0", 0), "tc-bf16": ("3", "1", 0), "tc-f16": ("3", "2", 0),
+                        "ffma-gram": ("1", "", 1), "direct": ("0", "", 2)}[variant]
+    monkeypatch.setenv("EBC200_SCREEN_MODE", mode)
+    monkeypatch.setenv("EBC200_TC_KIND", kind)
+    rng = np.random.default_rng(100 + d)
+    X = rng.standard_normal((4000, d)).astype(np.float32)
+    g = eb.GroundMatrix(X, PREC[prec])
+    f = eb.EbcFunction(g)
+    if mode == "3":
+        assert optimize.screen_info(f)[2] == int(kind)
+    s = eb.greedy_maximize(f, eb.OptimizerBudget(k=6))
+    sel, vals, _, _ = oracle.greedy(g.as_float64(), 6)
+    assert s.selected == sel
+    np.testing.assert_allclose(np.cumsum(s.gains), vals, rtol=1e-10)
+    if mode == "3":
+        assert optimize.last_stats(f)[2] == rung
