@@ -70,11 +70,18 @@ struct ebc_ctx {
   void* Vhi = nullptr;
   void* Vlo = nullptr;
   int tc_kind = 1;  // tc::KIND_TF32 / KIND_BF16 (fp32 grounds) / KIND_F16 (fp16 grounds)
-  float* pttc = nullptr;  // per point ip = (cm32 - |v|^2)/2, the tensor screen seed
-  float* kpmax = nullptr;  // per tensor tile: max error quantum kp (reset state)
+  float* pttc = nullptr;   // na x n_pad seeds ip_a(v) = (cm32 - |v - mu_a|^2)/2
+  float* kpmax = nullptr;  // na x tc_ntl: per (anchor, point tile) max error quantum kp (reset state)
+  int tc_na = 1;           // anchors (0 = the origin)
+  int64_t tc_ntl = 0;      // point tiles of the tensor screen
+  float* anchors = nullptr;         // na x pitch
+  float* nva = nullptr;             // na x n_pad: |v - mu_a|^2
+  int* tile_anchor = nullptr;       // per 128-row candidate block
+  float* tc_vmax = nullptr;         // per point tile: max |v|
+  unsigned long long* fps_keys = nullptr;
   int kpad = 0;
   int tc_np = 0;  // points per tensor tile (0: tensor screen unavailable)
-  float tc_ka = 0.f, tc_kb = 0.f, tc_kc = 0.f;
+  float tc_kp = 0.f, tc_kc = 0.f, tc_kx = 0.f;  // anchored bound coefficients
   unsigned char* selected = nullptr;
   double* chunkpart = nullptr;  // nchunks
   unsigned int* counter = nullptr;
@@ -328,11 +335,13 @@ int launch_tc_t(ebc_ctx* ctx, const TcPlan& p, const int* level_now, int level) 
   auto kern = k_screen_tc<NP, KIND>;
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
   dim3 grid(p.ncb, p.nsplit);
+  TcAnchors an{ctx->anchors, ctx->pitch, ctx->tile_anchor, ctx->pttc, ctx->n_pad, ctx->kpmax, ctx->tc_ntl,
+               ctx->tc_vmax, ctx->tc_kc, ctx->tc_kx};
   kern<<<grid, tc::THREADS, p.smem, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->d, (const unsigned char*)ctx->Vhi,
-                                                   (const unsigned char*)ctx->Vlo, ctx->pttc, ctx->kpmax, ctx->nv32, ctx->kpad,
+                                                   (const unsigned char*)ctx->Vlo, an, ctx->kpad,
                                                    tc::stages_for(ctx->kpad, ctx->tc_np, tc_es(KIND), tc_parts(KIND)), ctx->c0,
                                                    p.ntiles, p.tps, (double*)ctx->part_g.p, (float*)ctx->part_e.p,
-                                                   ctx->n_pad, ctx->tc_kc, level_now, level);
+                                                   ctx->n_pad, level_now, level);
   KCHECK();
   return EBC_OK;
 }
@@ -439,18 +448,29 @@ int run_step_select(ebc_ctx* ctx, int step, int commit, int64_t* sel_dev) {
   return EBC_OK;
 }
 
+TcSeeds tc_seeds(const ebc_ctx* ctx) {
+  TcSeeds s;
+  if (ctx->pttc) {
+    s.ipa = ctx->pttc;
+    s.nva = ctx->nva;
+    s.na = ctx->tc_na;
+    s.stride = ctx->n_pad;
+  }
+  return s;
+}
+
 int run_update(ebc_ctx* ctx, int step, double* val_dev, double* gain_dev) {
   const int eb = 4 * step;
   const size_t smem = (size_t)ctx->d * sizeof(double);
   if (ctx->dtype == EBC_F64) {
     CU(cudaFuncSetAttribute(k_update<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024));
     k_update<double><<<ctx->nchunks, RED_THREADS, smem, ctx->stream>>>(
-        ctx->V64, ctx->pitch, ctx->n, ctx->d, ctx->best, ctx->pk, ctx->e0d, ctx->nv32, ctx->cm64, ctx->pt, ctx->pttc, ctx->tc_ka, ctx->tc_kb, ctx->chunkpart,
+        ctx->V64, ctx->pitch, ctx->n, ctx->d, ctx->best, ctx->pk, ctx->e0d, ctx->nv32, ctx->cm64, ctx->pt, tc_seeds(ctx), ctx->chunkpart,
         ctx->counter, 1.0 / (double)ctx->n, ctx->cur, val_dev, gain_dev, step);
   } else {
     CU(cudaFuncSetAttribute(k_update<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024));
     k_update<float><<<ctx->nchunks, RED_THREADS, smem, ctx->stream>>>(
-        ctx->V32, ctx->pitch, ctx->n, ctx->d, ctx->best, ctx->pk, ctx->e0d, ctx->nv32, ctx->cm64, ctx->pt, ctx->pttc, ctx->tc_ka, ctx->tc_kb, ctx->chunkpart,
+        ctx->V32, ctx->pitch, ctx->n, ctx->d, ctx->best, ctx->pk, ctx->e0d, ctx->nv32, ctx->cm64, ctx->pt, tc_seeds(ctx), ctx->chunkpart,
         ctx->counter, 1.0 / (double)ctx->n, ctx->cur, val_dev, gain_dev, step);
   }
   KCHECK();
@@ -488,7 +508,7 @@ int do_reset(ebc_ctx* ctx) {
   const int blocks = (int)((ctx->n + 255) / 256);
   CU(cudaMemsetAsync(ctx->stats, 0, 4 * sizeof(long long), ctx->stream));
   k_reset<<<blocks, 256, 0, ctx->stream>>>(ctx->n, ctx->e0d, ctx->nv32, ctx->pk, ctx->cm64, ctx->pt, ctx->selected,
-                                           nullptr, ctx->pttc, ctx->tc_ka, ctx->tc_kb);
+                                           nullptr, tc_seeds(ctx));
   KCHECK();
   {
     // first rung of the adaptive ladder for this run
@@ -504,7 +524,7 @@ int do_reset(ebc_ctx* ctx) {
 void free_ctx(ebc_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
-  void* ptrs[] = {c->V32, c->V64, c->e0d, c->cm64, c->pt, c->nv32, c->level, c->stats, c->Vhi, c->Vlo, c->pttc, c->kpmax, c->selected, c->chunkpart, c->counter, c->cur, c->best,
+  void* ptrs[] = {c->V32, c->V64, c->e0d, c->cm64, c->pt, c->nv32, c->level, c->stats, c->Vhi, c->Vlo, c->pttc, c->kpmax, c->anchors, c->nva, c->tile_anchor, c->tc_vmax, c->fps_keys, c->selected, c->chunkpart, c->counter, c->cur, c->best,
                   c->maxlb, c->wcount, c->wlist, c->wgain, c->ub};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -751,15 +771,31 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
                                                            : 3.0 * std::ldexp(1.0, -20);
       const double nprod = ctx->tc_kind == tc::KIND_F16 ? 1.0 : 3.0;
       const double ktc = split + (nprod * ctx->kpad + 16.0) * std::ldexp(1.0, -23);
-      ctx->tc_ka = (float)(4.0 * u * 1.01);
-      ctx->tc_kb = (float)((4.0 * u + 0.5 * ktc) * 1.01);
-      ctx->tc_kc = (float)((4.0 * u + 0.5 * ktc) * 1.01);
+      // anchored bound: kp = (d+8)u (cm + |v - mu|^2),
+      // kc = (d+8)u (|mu| |c'| + |c'|^2), kx = ktc + 4u per |v| |c'|
+      ctx->tc_kp = (float)((d + 8) * u * 1.01);
+      ctx->tc_kc = (float)((d + 8) * u * 1.01);
+      ctx->tc_kx = (float)((ktc + 4.0 * u) * 1.01);
+      // anchors: the origin plus farthest points (FP16 operands need c' = c exactly: origin only)
+      const char* na_env = getenv("EBC200_TC_ANCHORS");
+      ctx->tc_na = (na_env && na_env[0]) ? std::max(1, atoi(na_env)) : 32;
+      if (ctx->tc_kind == tc::KIND_F16) ctx->tc_na = 1;
+      ctx->tc_na = (int)std::min<int64_t>(ctx->tc_na, n);
+      ctx->tc_ntl = ctx->n_pad / ctx->tc_np;
       const size_t ve = (size_t)ctx->n_pad * ctx->kpad;
+      const size_t nas = (size_t)ctx->tc_na * ctx->n_pad;
       CUC(cudaMalloc(&ctx->Vhi, ve * es));
       if (parts == 2) CUC(cudaMalloc(&ctx->Vlo, ve * es));
-      CUC(cudaMalloc(&ctx->pttc, (size_t)ctx->n_pad * sizeof(float)));
-      CUC(cudaMalloc(&ctx->kpmax, (size_t)(ctx->n_pad / ctx->tc_np + 1) * sizeof(float)));
-      CUC(cudaMemsetAsync(ctx->pttc, 0, (size_t)ctx->n_pad * sizeof(float), ctx->stream));
+      CUC(cudaMalloc(&ctx->pttc, nas * sizeof(float)));
+      CUC(cudaMalloc(&ctx->nva, nas * sizeof(float)));
+      CUC(cudaMemsetAsync(ctx->nva, 0, nas * sizeof(float), ctx->stream));
+      CUC(cudaMalloc(&ctx->kpmax, (size_t)ctx->tc_na * ctx->tc_ntl * sizeof(float)));
+      CUC(cudaMalloc(&ctx->tc_vmax, (size_t)ctx->tc_ntl * sizeof(float)));
+      CUC(cudaMalloc(&ctx->anchors, (size_t)ctx->tc_na * ctx->pitch * sizeof(float)));
+      CUC(cudaMalloc(&ctx->tile_anchor, (size_t)(ctx->n_pad / 128 + 1) * sizeof(int)));
+      CUC(cudaMemsetAsync(ctx->tile_anchor, 0, (size_t)(ctx->n_pad / 128 + 1) * sizeof(int), ctx->stream));
+      CUC(cudaMalloc(&ctx->fps_keys, (size_t)(ctx->tc_na + 1) * sizeof(unsigned long long)));
+      CUC(cudaMemsetAsync(ctx->fps_keys, 0, (size_t)(ctx->tc_na + 1) * sizeof(unsigned long long), ctx->stream));
     }
   }
   CUC(cudaMalloc(&ctx->selected, (size_t)ctx->n_pad));
@@ -789,19 +825,38 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
   }
   if (dtype == EBC_F64)
     k_init<double><<<ctx->nchunks, RED_THREADS, 0, ctx->stream>>>(ctx->V64, ctx->pitch, n, d, e0dev, ctx->pk,
-                                                                 ctx->e0d, ctx->cm64, ctx->nv32, ctx->pt, ctx->chunkpart,
-                                                                 nullptr, 0.f, 0.f);
+                                                                 ctx->e0d, ctx->cm64, ctx->nv32, ctx->pt, ctx->chunkpart);
   else
     k_init<float><<<ctx->nchunks, RED_THREADS, 0, ctx->stream>>>(ctx->V32, ctx->pitch, n, d, e0dev, ctx->pk,
-                                                                ctx->e0d, ctx->cm64, ctx->nv32, ctx->pt, ctx->chunkpart,
-                                                                ctx->pttc, ctx->tc_ka, ctx->tc_kb);
+                                                                ctx->e0d, ctx->cm64, ctx->nv32, ctx->pt, ctx->chunkpart);
   CUC(cudaGetLastError());
   if (ctx->tc_np) {
     {
-      const int64_t ntl = ctx->n_pad / ctx->tc_np;
-      k_tile_kpmax<<<(unsigned)((ntl + 255) / 256), 256, 0, ctx->stream>>>(ctx->e0d, ctx->nv32, n, ntl, ctx->tc_np,
-                                                                            ctx->tc_ka, ctx->tc_kb, ctx->kpmax);
+      // anchors (farthest-point sampling from the origin), |v - mu_a|^2, the
+      // anchor of each candidate block, seeds and per-tile error quanta
+      float* mind = nullptr;
+      CUC(cudaMalloc(&mind, (size_t)n * sizeof(float)));
+      for (int a = 0; a < ctx->tc_na; ++a) {
+        k_fps_step<<<2 * ctx->num_sms, 256, 0, ctx->stream>>>(ctx->V32, ctx->pitch, n, d, a, ctx->tc_na, mind,
+                                                              ctx->fps_keys, ctx->anchors, ctx->pitch);
+        CUC(cudaGetLastError());
+      }
+      k_nva<<<8 * ctx->num_sms, 256, 0, ctx->stream>>>(ctx->V32, ctx->pitch, n, d, ctx->anchors, ctx->pitch,
+                                                       ctx->tc_na, ctx->nva, ctx->n_pad);
       CUC(cudaGetLastError());
+      k_tile_anchor<<<(unsigned)((n + 127) / 128), 128, 0, ctx->stream>>>(ctx->V32, ctx->pitch, n, d, ctx->anchors,
+                                                                          ctx->pitch, ctx->tc_na, ctx->tile_anchor);
+      CUC(cudaGetLastError());
+      k_seed_ipa<<<(unsigned)((ctx->n_pad + 255) / 256), 256, 0, ctx->stream>>>(ctx->cm64, n, ctx->n_pad,
+                                                                                 tc_seeds(ctx));
+      CUC(cudaGetLastError());
+      const int64_t cells = (int64_t)ctx->tc_na * ctx->tc_ntl;
+      k_tile_kpmax<<<(unsigned)((cells + 255) / 256), 256, 0, ctx->stream>>>(
+          ctx->e0d, ctx->nv32, ctx->nva, ctx->n_pad, ctx->tc_na, n, ctx->tc_ntl, ctx->tc_np, ctx->tc_kp, ctx->kpmax,
+          ctx->tc_vmax);
+      CUC(cudaGetLastError());
+      CUC(cudaStreamSynchronize(ctx->stream));
+      cudaFree(mind);
     }
     if (ctx->tc_kind == tc::KIND_F16)
       k_split_f16<<<8 * ctx->num_sms, 256, 0, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->n_pad, d, ctx->kpad,

@@ -85,6 +85,19 @@ __device__ __forceinline__ float4 make_pt(float c32, float nv, PtCoef k) {
   return make_float4(-c32, k.tau_k * c32, (c32 - nv) * 0.5f, k.gram_k * (c32 + 2.f * nv));
 }
 
+// Tensor-screen seeds (screen_tc.cuh): per anchor a and point v,
+// ip_a[v] = (cm32 - nva_a[v]) / 2 with nva_a[v] = |v - mu_a|^2 (fp64, rounded).
+struct TcSeeds {
+  float* ipa = nullptr;        // na x stride
+  const float* nva = nullptr;  // na x stride
+  int na = 0;
+  int64_t stride = 0;
+};
+
+__device__ __forceinline__ void write_seeds(const TcSeeds& s, int64_t v, float cm32) {
+  for (int a = 0; a < s.na; ++a) s.ipa[a * s.stride + v] = (cm32 - s.nva[a * s.stride + v]) * 0.5f;
+}
+
 // ---------------------------------------------------------------- K0: init
 
 // Widen/pad the uploaded rows into the device layout (n_pad x pitch, zero pad).
@@ -116,8 +129,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_init(const T* __restrict__ V, i
                                                       const double* __restrict__ e0, PtCoef pk,
                                                       double* __restrict__ e0d, double* __restrict__ cm64,
                                                       float* __restrict__ nv32, float4* __restrict__ pt,
-                                                      double* __restrict__ part, float* __restrict__ pttc,
-                                                      float tc_ka, float tc_kb) {
+                                                      double* __restrict__ part) {
   __shared__ double sbuf[RED_THREADS];
   __shared__ double se0[1024];
   for (int k = threadIdx.x; k < d && k < 1024; k += blockDim.x) se0[k] = e0[k];
@@ -138,7 +150,6 @@ __global__ void __launch_bounds__(RED_THREADS) k_init(const T* __restrict__ V, i
       const float n32 = (float)nv;
       nv32[v] = n32;
       pt[v] = make_pt((float)t, n32, pk);
-      if (pttc) pttc[v] = ((float)t - n32) * 0.5f;
       acc += t;
     }
   }
@@ -149,14 +160,14 @@ __global__ void __launch_bounds__(RED_THREADS) k_init(const T* __restrict__ V, i
 // Reset the cached minima to d(., e0) (ebc_reset / start of a Greedy run).
 __global__ void k_reset(int64_t n, const double* __restrict__ e0d, const float* __restrict__ nv32, PtCoef pk,
                         double* __restrict__ cm64, float4* __restrict__ pt, unsigned char* __restrict__ selected,
-                        int* __restrict__ sticky, float* __restrict__ pttc, float tc_ka, float tc_kb) {
+                        int* __restrict__ sticky, TcSeeds seeds) {
   int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (v == 0 && sticky) *sticky = 0;
   if (v < n) {
     double t = e0d[v];
     cm64[v] = t;
     pt[v] = make_pt((float)t, nv32[v], pk);
-    if (pttc) pttc[v] = ((float)t - nv32[v]) * 0.5f;
+    if (seeds.ipa) write_seeds(seeds, v, (float)t);
     selected[v] = 0;
   }
 }
@@ -757,7 +768,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_update(const T* __restrict__ V,
                                                         const int64_t* __restrict__ best, PtCoef pk,
                                                         const double* __restrict__ e0d, const float* __restrict__ nv32,
                                                         double* __restrict__ cm64, float4* __restrict__ pt,
-                                                        float* __restrict__ pttc, float tc_ka, float tc_kb,
+                                                        TcSeeds seeds,
                                                         double* __restrict__ fpart,
                                                         unsigned int* __restrict__ counter, double inv_n,
                                                         double* __restrict__ cur, double* __restrict__ val_out,
@@ -779,7 +790,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_update(const T* __restrict__ V,
         m = t;
         cm64[v] = m;
         pt[v] = make_pt((float)m, nv32[v], pk);
-        if (pttc) pttc[v] = ((float)m - nv32[v]) * 0.5f;
+        if (seeds.ipa) write_seeds(seeds, v, (float)m);
       }
       acc += e0d[v] - m;
     }

@@ -293,20 +293,153 @@ __global__ void k_split_f16(const float* __restrict__ V32, int pitch, int64_t nr
   }
 }
 
-// kpmax[t] = max over the NP points of tile t of kp = ka*cm32 + kb*|v|^2 at
-// reset (cm = d(., e0)); cm only decreases within a run, so it bounds every step.
-__global__ void k_tile_kpmax(const double* __restrict__ e0d, const float* __restrict__ nv32, int64_t n,
-                             int64_t ntiles, int np, float ka, float kb, float* __restrict__ kpmax) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t < ntiles) {
-    float m = 0.f;
-    for (int i = 0; i < np; ++i) {
-      const int64_t v = t * np + i;
-      if (v < n) m = fmaxf(m, ka * (float)e0d[v] + kb * nv32[v]);
+// ---------------------------------------------------------------- anchors
+// The tensor screen computes v.c' with c' = c - mu_a, mu_a the anchor of the
+// candidate tile (anchor 0 = the origin, the plain Gram form).  Its error scales
+// with |v| |c'| instead of |v|^2 + |c|^2, so clustered data (C4) keeps narrow
+// windows.  Anchors: farthest-point sampling from the origin; each 128-candidate
+// block takes the anchor that minimises max |c - mu_a|.  Every choice is valid --
+// the bounds use each candidate's own |c'| -- the choice only sets their width.
+
+__device__ __forceinline__ unsigned long long fps_key(float dist, int64_t v) {
+  return ((unsigned long long)__float_as_uint(fmaxf(dist, 0.f)) << 32) | (0xFFFFFFFFull - (unsigned long long)v);
+}
+
+// Step a of farthest-point sampling: anchor a is the origin (a = 0) or the
+// point keyed in keys[a]; fold it into mind and key the next farthest point.
+__global__ void k_fps_step(const float* __restrict__ V32, int pitch, int64_t n, int d, int a, int na,
+                           float* __restrict__ mind, unsigned long long* __restrict__ keys,
+                           float* __restrict__ anchors, int apitch) {
+  __shared__ unsigned long long sk[32];
+  int64_t src = -1;
+  if (a > 0) src = (int64_t)(0xFFFFFFFFull - (keys[a] & 0xFFFFFFFFull));
+  if (blockIdx.x == 0)
+    for (int k = threadIdx.x; k < apitch; k += blockDim.x)
+      anchors[(int64_t)a * apitch + k] = (src >= 0 && k < d) ? V32[src * pitch + k] : 0.f;
+  unsigned long long best = 0;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+    float t = 0.f;
+    const float* row = V32 + v * pitch;
+    if (src >= 0) {
+      const float* mu = V32 + src * pitch;
+      for (int k = 0; k < d; ++k) {
+        const float x = row[k] - mu[k];
+        t = fmaf(x, x, t);
+      }
+    } else {
+      for (int k = 0; k < d; ++k) t = fmaf(row[k], row[k], t);
     }
-    kpmax[t] = m;
+    const float m = a == 0 ? t : fminf(mind[v], t);
+    mind[v] = m;
+    const unsigned long long key = fps_key(m, v);
+    best = key > best ? key : best;
+  }
+  if (a + 1 >= na) return;
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long other = __shfl_xor_sync(0xffffffff, best, o);
+    best = other > best ? other : best;
+  }
+  if ((threadIdx.x & 31) == 0) sk[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) best = sk[w] > best ? sk[w] : best;
+    atomicMax(&keys[a + 1], best);
   }
 }
+
+// nva[a][v] = |v - mu_a|^2 (fp64 sum, rounded to fp32) for every anchor.
+__global__ void k_nva(const float* __restrict__ V32, int pitch, int64_t n, int d, const float* __restrict__ anchors,
+                      int apitch, int na, float* __restrict__ nva, int64_t stride) {
+  const int64_t total = (int64_t)na * n;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int a = (int)(i / n);
+    const int64_t v = i - (int64_t)a * n;
+    const float* row = V32 + v * pitch;
+    const float* mu = anchors + (int64_t)a * apitch;
+    double t = 0.0;
+    for (int k = 0; k < d; ++k) {
+      const double x = (double)row[k] - (double)mu[k];
+      t = fma(x, x, t);
+    }
+    nva[a * stride + v] = (float)t;
+  }
+}
+
+// Per 128-candidate block: the anchor minimising max_c |c - mu_a|^2 (ties: lower a).
+__global__ void k_tile_anchor(const float* __restrict__ V32, int pitch, int64_t n, int d,
+                              const float* __restrict__ anchors, int apitch, int na, int* __restrict__ tile_anchor) {
+  __shared__ float wmax[4];
+  const int64_t c = (int64_t)blockIdx.x * 128 + threadIdx.x;
+  float best = INFINITY;
+  int besta = 0;
+  for (int a = 0; a < na; ++a) {
+    float t = 0.f;
+    if (c < n) {
+      const float* row = V32 + c * pitch;
+      const float* mu = anchors + (int64_t)a * apitch;
+      for (int k = 0; k < d; ++k) {
+        const float x = row[k] - mu[k];
+        t = fmaf(x, x, t);
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) t = fmaxf(t, __shfl_xor_sync(0xffffffff, t, o));
+    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = t;
+    __syncthreads();
+    const float m = fmaxf(fmaxf(wmax[0], wmax[1]), fmaxf(wmax[2], wmax[3]));
+    if (m < best) {
+      best = m;
+      besta = a;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) tile_anchor[blockIdx.x] = besta;
+}
+
+// Seeds from the cached minima for every anchor; padded points get -1e30 so
+// they can never contribute (a = S + ip + ic stays hugely negative).
+__global__ void k_seed_ipa(const double* __restrict__ cm64, int64_t n, int64_t n_pad, TcSeeds seeds) {
+  const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v < n)
+    write_seeds(seeds, v, (float)cm64[v]);
+  else if (v < n_pad)
+    for (int a = 0; a < seeds.na; ++a) seeds.ipa[a * seeds.stride + v] = -1e30f;
+}
+
+// kpmax[a][t] = max over the NP points of tile t of kp = KP (cm32 + nva_a) at
+// reset (cm = d(., e0)); cm only decreases within a run, so it bounds every step.
+// vmax[t] = max |v| over the tile (rounded up).
+__global__ void k_tile_kpmax(const double* __restrict__ e0d, const float* __restrict__ nv32,
+                             const float* __restrict__ nva, int64_t stride, int na, int64_t n, int64_t ntiles,
+                             int np, float kp_coef, float* __restrict__ kpmax, float* __restrict__ vmax) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)na * ntiles) return;
+  const int a = (int)(i / ntiles);
+  const int64_t t = i - (int64_t)a * ntiles;
+  float m = 0.f, vm = 0.f;
+  for (int j = 0; j < np; ++j) {
+    const int64_t v = t * np + j;
+    if (v < n) {
+      m = fmaxf(m, kp_coef * ((float)e0d[v] + nva[a * stride + v]));
+      vm = fmaxf(vm, nv32[v]);
+    }
+  }
+  kpmax[a * ntiles + t] = m * (1.f + 1e-6f);
+  if (a == 0) vmax[t] = sqrtf(vm) * (1.f + 1e-5f);
+}
+
+// Anchor data of the tensor screen (kernel argument).
+struct TcAnchors {
+  const float* mu;          // na x apitch
+  int apitch;
+  const int* tile_anchor;   // per 128-row block of candidates
+  const float* ipa;         // na x ipstride seeds
+  int64_t ipstride;
+  const float* kpmax;       // na x kpstride
+  int64_t kpstride;
+  const float* vmax;        // per point tile
+  float kc;                 // kc = kc_coef (|mu| |c'| + |c'|^2)
+  float kx;                 // per pair MMA term kx |v|max |c'|
+};
 
 // One CTA: candidates [cand0 + 128*bx, +128) x V tiles [t0, t1) of NP points.
 // A (candidates, hi and lo) lives in TMEM for the CTA's life (MMA "TS" form:
@@ -316,10 +449,9 @@ __global__ void k_tile_kpmax(const double* __restrict__ e0d, const float* __rest
 template <int NP, int KIND>
 __global__ void __launch_bounds__(tc::THREADS, 1)
     k_screen_tc(const float* __restrict__ V32, int pitch, int d, const unsigned char* __restrict__ Vhi,
-                const unsigned char* __restrict__ Vlo, const float* __restrict__ pttc,
-                const float* __restrict__ kpmax, const float* __restrict__ nv32,
+                const unsigned char* __restrict__ Vlo, TcAnchors an,
                 int kpad, int stages, int64_t cand0, int ntiles, int tiles_per_split, double* __restrict__ part_g,
-                float* __restrict__ part_e, int64_t part_stride, float kc_coef, const int* __restrict__ level_now,
+                float* __restrict__ part_e, int64_t part_stride, const int* __restrict__ level_now,
                 int level) {
   using namespace tc;
   if (level_now && *level_now != level) return;
@@ -428,25 +560,38 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     const int cl = q * 32 + lane;
     const int64_t c = crow + cl;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    const int anc = an.tile_anchor[crow >> 7];  // anchor of this candidate block
+    const float* mu = an.mu + (int64_t)anc * an.apitch;
+    float cn2 = 0.f, mc = 0.f, mn2 = 0.f;
     {
       // A of this candidate into TMEM: slice 0 writes hi [0,128), the last slice lo [128,256)
       const float* row = V32 + c * pitch;
       const bool do_hi = half == 0, do_lo = TM::PARTS == 2 && half == EPI_WARPGROUPS - 1;
+      auto cprime = [&](int k) -> float {  // c' = fl(c - mu), accumulating |c'|^2, mu.c', |mu|^2
+        if (k >= d) return 0.f;
+        const float m = mu[k];
+        const float x = row[k] - m;
+        cn2 = fmaf(x, x, cn2);
+        mc = fmaf(m, x, mc);
+        mn2 = fmaf(m, m, mn2);
+        return x;
+      };
 #pragma unroll 1
       for (int blk = 0; blk < (BF ? 2 : 4); ++blk) {
         uint32_t rh[32], rl[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
           if (KIND == KIND_F16) {
+            // FP16 operands only with the origin anchor (c' = c, exactly fp16)
             const int k = blk * 64 + 2 * i;
-            const float x0 = k < d ? row[k] : 0.f, x1 = k + 1 < d ? row[k + 1] : 0.f;
+            const float x0 = cprime(k), x1 = cprime(k + 1);
             rh[i] = (uint32_t)__half_as_ushort(__float2half_rn(x0)) |
                     ((uint32_t)__half_as_ushort(__float2half_rn(x1)) << 16);
             rl[i] = 0u;
           } else if (BF) {
             // column = packed pair (k = 2i, 2i+1), low half = even k
             const int k = blk * 64 + 2 * i;
-            const float x0 = k < d ? row[k] : 0.f, x1 = k + 1 < d ? row[k + 1] : 0.f;
+            const float x0 = cprime(k), x1 = cprime(k + 1);
             const __nv_bfloat16 h0 = __float2bfloat16_rn(x0), h1 = __float2bfloat16_rn(x1);
             const __nv_bfloat16 m0 = __float2bfloat16_rn(x0 - __bfloat162float(h0));
             const __nv_bfloat16 m1 = __float2bfloat16_rn(x1 - __bfloat162float(h1));
@@ -454,7 +599,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
             rl[i] = (uint32_t)__bfloat16_as_ushort(m0) | ((uint32_t)__bfloat16_as_ushort(m1) << 16);
           } else {
             const int k = blk * 32 + i;
-            const float x = k < d ? row[k] : 0.f;
+            const float x = cprime(k);
             const uint32_t h = __float_as_uint(x) & 0xFFFFE000u;
             rh[i] = h;
             rl[i] = __float_as_uint(x - __uint_as_float(h));
@@ -467,9 +612,14 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       fence_before();
       mbar_arrive(aready);
     }
-    const float nc = nv32[c];
-    const float ic = -0.5f * nc;
-    const float kc = kc_coef * nc;
+    // t/2 = ip_a(v) + v.c' + ic, ic = -(mu.c' + |c'|^2/2); per-pair error bound
+    // kpmax[a][tile] + kc + kx |v|max(tile) |c'|  (DESIGN.md §4 "anchored tensor screen")
+    const float cn = sqrtf(cn2) * (1.f + 1e-5f);
+    const float ic = -(mc + 0.5f * cn2);
+    const float kc = an.kc * (sqrtf(mn2) * (1.f + 1e-5f) * cn + cn2);
+    const float kxc = an.kx * cn;
+    const float* ipa = an.ipa + (int64_t)anc * an.ipstride;
+    const float* kpa = an.kpmax + (int64_t)anc * an.kpstride;
     double g64 = 0.0;
     float e = 0.f;
     constexpr int NB = TM::NB;
@@ -480,7 +630,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       // (L1-broadcast) loads overlap the MMA
       float ipv[SW];
       {
-        const float4* pp4 = reinterpret_cast<const float4*>(pttc + (int64_t)(t0 + it) * NP + half * SLICE);
+        const float4* pp4 = reinterpret_cast<const float4*>(ipa + (int64_t)(t0 + it) * NP + half * SLICE);
 #pragma unroll
         for (int i = 0; i < SW / 4; ++i) {
           const float4 p = __ldg(pp4 + i);
@@ -492,7 +642,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       }
       // one error quantum per tile: kpmax = max_v kp over the tile (bounds every
       // pair's kp_v; computed at reset, cm only decreases within a run)
-      const float kq = kpmax[t0 + it] + kc;
+      const float kq = kpa[t0 + it] + fmaf(kxc, __ldg(an.vmax + t0 + it), kc);
       const float thr = -kq;
       mbar_wait(&tfull[b], (it / NB) & 1);
       fence_after();
