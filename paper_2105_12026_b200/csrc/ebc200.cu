@@ -79,6 +79,7 @@ struct ebc_ctx {
   int* tile_anchor = nullptr;       // per 128-row candidate block
   float* tc_vmax = nullptr;         // per point tile: max |v|
   unsigned long long* fps_keys = nullptr;
+  float* ipa0 = nullptr;            // na x n_pad seeds at the reset state (work-matrix flag screen)
   int kpad = 0;
   int tc_np = 0;  // points per tensor tile (0: tensor screen unavailable)
   float tc_kp = 0.f, tc_kc = 0.f, tc_kx = 0.f;  // anchored bound coefficients
@@ -94,11 +95,12 @@ struct ebc_ctx {
   double* ub = nullptr;      // n
   DevBuf part_g, part_e, part_r, sel_out, val_out, gain_out, ms_part, ms_off, ms_idx, ms_out;
   // sparse work-matrix path
+  DevBuf ms_tanchor;
   DevBuf ms_mbuf, ms_setof, ms_pairs, ms_keys, ms_vals, ms_keys2, ms_vals2, ms_ukeys, ms_uvals, ms_cub;
   float4* pt0 = nullptr;  // per-point screen data seeded with d(., e0)
   int* ms_count = nullptr;
   int* ms_nruns = nullptr;
-  int ms_mode = 1;        // 1: sparse (flagged) path when possible, 0: dense only
+  int ms_mode = 1;        // 1: sparse path, tensor flag screen when available; 2: sparse, FFMA flag screen; 0: dense only
 
   // CUDA graphs of whole Greedy runs, keyed by k (rebuilt when buffers move)
   struct Graph {
@@ -341,9 +343,39 @@ int launch_tc_t(ebc_ctx* ctx, const TcPlan& p, const int* level_now, int level) 
                                                    (const unsigned char*)ctx->Vlo, an, ctx->kpad,
                                                    tc::stages_for(ctx->kpad, ctx->tc_np, tc_es(KIND), tc_parts(KIND)), ctx->c0,
                                                    p.ntiles, p.tps, (double*)ctx->part_g.p, (float*)ctx->part_e.p,
-                                                   ctx->n_pad, level_now, level);
+                                                   ctx->n_pad, level_now, level, nullptr, FlagOut{});
   KCHECK();
   return EBC_OK;
+}
+
+// Work-matrix flag screen on the tensor cores: candidates = gathered member rows.
+template <int NP, int KIND>
+int launch_tc_flag_t(ebc_ctx* ctx, const TcPlan& p, const float* Vc, const int* tanchor, FlagOut fo) {
+  auto kern = k_screen_tc<NP, KIND, true>;
+  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
+  dim3 grid(p.ncb, p.nsplit);
+  TcAnchors an{ctx->anchors, ctx->pitch, tanchor, ctx->ipa0, ctx->n_pad, ctx->kpmax, ctx->tc_ntl,
+               ctx->tc_vmax, ctx->tc_kc, ctx->tc_kx};
+  kern<<<grid, tc::THREADS, p.smem, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->d, (const unsigned char*)ctx->Vhi,
+                                                   (const unsigned char*)ctx->Vlo, an, ctx->kpad,
+                                                   tc::stages_for(ctx->kpad, ctx->tc_np, tc_es(KIND), tc_parts(KIND)), 0,
+                                                   p.ntiles, p.tps, nullptr, nullptr, 0, nullptr, 0, Vc, fo);
+  KCHECK();
+  return EBC_OK;
+}
+
+int launch_tc_flag(ebc_ctx* ctx, const TcPlan& p, const float* Vc, const int* tanchor, FlagOut fo) {
+  switch (ctx->tc_kind) {
+    case tc::KIND_F16:
+      if (ctx->tc_np == 128) return launch_tc_flag_t<128, tc::KIND_F16>(ctx, p, Vc, tanchor, fo);
+      return launch_tc_flag_t<64, tc::KIND_F16>(ctx, p, Vc, tanchor, fo);
+    case tc::KIND_BF16:
+      if (ctx->tc_np == 128) return launch_tc_flag_t<128, tc::KIND_BF16>(ctx, p, Vc, tanchor, fo);
+      return launch_tc_flag_t<64, tc::KIND_BF16>(ctx, p, Vc, tanchor, fo);
+    default:
+      if (ctx->tc_np == 128) return launch_tc_flag_t<128, tc::KIND_TF32>(ctx, p, Vc, tanchor, fo);
+      return launch_tc_flag_t<64, tc::KIND_TF32>(ctx, p, Vc, tanchor, fo);
+  }
 }
 
 int launch_tc(ebc_ctx* ctx, const TcPlan& p, const int* level_now, int level) {
@@ -524,11 +556,11 @@ int do_reset(ebc_ctx* ctx) {
 void free_ctx(ebc_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
-  void* ptrs[] = {c->V32, c->V64, c->e0d, c->cm64, c->pt, c->nv32, c->level, c->stats, c->Vhi, c->Vlo, c->pttc, c->kpmax, c->anchors, c->nva, c->tile_anchor, c->tc_vmax, c->fps_keys, c->selected, c->chunkpart, c->counter, c->cur, c->best,
+  void* ptrs[] = {c->V32, c->V64, c->e0d, c->cm64, c->pt, c->nv32, c->level, c->stats, c->Vhi, c->Vlo, c->pttc, c->kpmax, c->anchors, c->nva, c->tile_anchor, c->tc_vmax, c->fps_keys, c->ipa0, c->selected, c->chunkpart, c->counter, c->cur, c->best,
                   c->maxlb, c->wcount, c->wlist, c->wgain, c->ub};
   for (void* p : ptrs)
     if (p) cudaFree(p);
-  DevBuf* bufs[] = {&c->part_g, &c->part_e, &c->part_r, &c->sel_out, &c->val_out, &c->gain_out, &c->ms_part,
+  DevBuf* bufs[] = {&c->ms_tanchor, &c->part_g, &c->part_e, &c->part_r, &c->sel_out, &c->val_out, &c->gain_out, &c->ms_part,
                     &c->ms_off, &c->ms_idx, &c->ms_out, &c->ms_mbuf, &c->ms_setof, &c->ms_pairs, &c->ms_keys,
                     &c->ms_vals, &c->ms_keys2, &c->ms_vals2, &c->ms_ukeys, &c->ms_uvals, &c->ms_cub};
   void* more[] = {c->pt0, c->ms_count, c->ms_nruns};
@@ -572,10 +604,30 @@ int multiset_sparse(ebc_ctx* ctx, int64_t l, int64_t nnz) {
   const int64_t sc0 = ctx->c0, sc1 = ctx->c1;
   ctx->c0 = 0;
   ctx->c1 = nnz;
-  ScreenPlan p;
-  rc = plan_screen(ctx, p);
   FlagOut fo{(uint2*)ctx->ms_pairs.p, ctx->ms_count, cap, ctx->n, nnz};
-  if (!rc) rc = launch_screen<2>(ctx, p, nullptr, 0, (const float*)ctx->ms_mbuf.p, fo, ctx->pt0);
+  TcPlan tp{};
+  if (ctx->ms_mode == 1 && ctx->screen_mode == 3 && plan_tc(ctx, tp)) {
+    // tensor-core flag screen: anchors of the member blocks, reset-state seeds
+    rc = ensure(ctx, ctx->ms_tanchor, (size_t)(mrows / 128 + 1) * sizeof(int));
+    if (!rc && !ctx->ipa0) {
+      CU(cudaMalloc(&ctx->ipa0, (size_t)ctx->tc_na * ctx->n_pad * sizeof(float)));
+      TcSeeds s0 = tc_seeds(ctx);
+      s0.ipa = ctx->ipa0;
+      k_seed_ipa<<<(unsigned)((ctx->n_pad + 255) / 256), 256, 0, ctx->stream>>>(ctx->e0d, ctx->n, ctx->n_pad, s0);
+      KCHECK();
+    }
+    if (!rc) {
+      k_tile_anchor<<<(unsigned)((nnz + 127) / 128), 128, 0, ctx->stream>>>(
+          (const float*)ctx->ms_mbuf.p, ctx->pitch, nnz, ctx->d, ctx->anchors, ctx->pitch, ctx->tc_na,
+          (int*)ctx->ms_tanchor.p);
+      KCHECK();
+      rc = launch_tc_flag(ctx, tp, (const float*)ctx->ms_mbuf.p, (const int*)ctx->ms_tanchor.p, fo);
+    }
+  } else {
+    ScreenPlan p;
+    rc = plan_screen(ctx, p);
+    if (!rc) rc = launch_screen<2>(ctx, p, nullptr, 0, (const float*)ctx->ms_mbuf.p, fo, ctx->pt0);
+  }
   ctx->c0 = sc0;
   ctx->c1 = sc1;
   if (rc) return rc;
@@ -1178,7 +1230,7 @@ int ebc_eval_multiset(ebc_ctx* ctx, const int64_t* offsets, const int64_t* idx, 
     CU(cudaMemcpyAsync(ctx->ms_idx.p, idx, (size_t)nnz * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
   CU(cudaEventRecord(a, ctx->stream));
   bool done = false;
-  if (ctx->dtype != EBC_F64 && ctx->ms_mode == 1) {
+  if (ctx->dtype != EBC_F64 && ctx->ms_mode >= 1) {
     ScreenPlan probe;
     const int64_t sc0 = ctx->c0, sc1 = ctx->c1;
     ctx->c0 = 0;

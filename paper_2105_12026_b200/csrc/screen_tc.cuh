@@ -446,13 +446,16 @@ struct TcAnchors {
 // the tensor core reads only the B tiles from shared memory); B tiles stream
 // through a STAGES-deep bulk-copy ring released by the MMA commit alone; the
 // per-point seed/quantum {ip, kp} is read by the epilogue through L1.
-template <int NP, int KIND>
+// FLAG: work-matrix flag screen (multiset.cuh) -- candidates are the gathered
+// member rows Vc, seeds are the reset state (cm = d(., e0)), and every pair that
+// is possibly closer than e0 (a > -kq) is appended to fo instead of summed.
+template <int NP, int KIND, bool FLAG = false>
 __global__ void __launch_bounds__(tc::THREADS, 1)
     k_screen_tc(const float* __restrict__ V32, int pitch, int d, const unsigned char* __restrict__ Vhi,
                 const unsigned char* __restrict__ Vlo, TcAnchors an,
                 int kpad, int stages, int64_t cand0, int ntiles, int tiles_per_split, double* __restrict__ part_g,
                 float* __restrict__ part_e, int64_t part_stride, const int* __restrict__ level_now,
-                int level) {
+                int level, const float* __restrict__ Vc = nullptr, FlagOut fo = FlagOut{}) {
   using namespace tc;
   if (level_now && *level_now != level) return;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -565,7 +568,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     float cn2 = 0.f, mc = 0.f, mn2 = 0.f;
     {
       // A of this candidate into TMEM: slice 0 writes hi [0,128), the last slice lo [128,256)
-      const float* row = V32 + c * pitch;
+      const float* row = (FLAG ? Vc : V32) + c * pitch;
       const bool do_hi = half == 0, do_lo = TM::PARTS == 2 && half == EPI_WARPGROUPS - 1;
       auto cprime = [&](int k) -> float {  // c' = fl(c - mu), accumulating |c'|^2, mu.c', |mu|^2
         if (k >= d) return 0.f;
@@ -664,7 +667,20 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         m4[(i / 8) & 3] = fmaxf(m4[(i / 8) & 3], fmaxf(S[i + 6], S[i + 7]));
       }
       const float mb = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
-      if (mb + ic > thr) {
+      if (FLAG) {
+        if (mb + ic > thr) {
+#pragma unroll
+          for (int i = 0; i < SW; ++i) {
+            if (S[i] + ic > thr) {  // rare: possibly closer than e0
+              const int64_t v = (int64_t)(t0 + it) * NP + half * SLICE + i;
+              if (v < fo.npoints && c < fo.ncands) {
+                const int slot = atomicAdd(fo.count, 1);
+                if (slot < fo.cap) fo.pairs[slot] = make_uint2((unsigned)v, (unsigned)c);
+              }
+            }
+          }
+        }
+      } else if (mb + ic > thr) {
         float cnt = 0.f;
 #pragma unroll
         for (int h = 0; h < SW; h += 32) {
@@ -680,6 +696,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         e = fmaf(cnt, kq, e);
       }
     }
+    if (!FLAG) {
     // combine the slices of each candidate in slice order (named barrier over
     // the epilogue warps only)
     double* xg = reinterpret_cast<double*>(stage0);  // the ring is idle once every tile is consumed
@@ -698,6 +715,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       }
       part_g[blockIdx.y * part_stride + c] = gs;
       part_e[blockIdx.y * part_stride + c] = es;
+    }
     }
   }
   fence_before();

@@ -262,13 +262,13 @@ def test_sparse_work_matrix_bit_identical_to_dense(monkeypatch):
         cases.append((X, sets))
     for X, sets in cases:
         out = {}
-        for mode in ("0", "1"):
+        for mode in ("0", "1", "2"):
             monkeypatch.setenv("EBC200_MULTISET_MODE", mode)
             f = fn(X, eb.Precision.FP32)
             out[mode] = eb.evaluate_with_backend(f, eb.EvalMultiset(sets))
             assert out[mode][-1] == 0.0
             assert out[mode][-2] == f.baseline_loss
-        assert out["0"].tolist() == out["1"].tolist()
+        assert out["0"].tolist() == out["1"].tolist() == out["2"].tolist()
 
 
 SIEVE = load_golden("reference_sieve.json")["cases"]
