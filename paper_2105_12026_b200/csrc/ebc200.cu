@@ -80,6 +80,12 @@ struct ebc_ctx {
   float* tc_vmax = nullptr;         // per point tile: max |v|
   unsigned long long* fps_keys = nullptr;
   float* ipa0 = nullptr;            // na x n_pad seeds at the reset state (work-matrix flag screen)
+  // certified tile-pair pruning of the tensor screen
+  bool tc_prune = true;
+  float* tile_rad = nullptr;        // per 128-row candidate block: max |c - mu_anchor|
+  float* rho = nullptr;             // na x tc_ntl: min |v - mu_a| over the point tile
+  float* cmx = nullptr;             // tc_ntl: max cm over the point tile (refreshed every screen)
+  float* cmx0 = nullptr;            // tc_ntl: the same at the reset state (cm = d(., e0))
   int kpad = 0;
   int tc_np = 0;  // points per tensor tile (0: tensor screen unavailable)
   float tc_kp = 0.f, tc_kc = 0.f, tc_kx = 0.f;  // anchored bound coefficients
@@ -95,7 +101,7 @@ struct ebc_ctx {
   double* ub = nullptr;      // n
   DevBuf part_g, part_e, part_r, sel_out, val_out, gain_out, ms_part, ms_off, ms_idx, ms_out;
   // sparse work-matrix path
-  DevBuf ms_tanchor;
+  DevBuf ms_tanchor, ms_trad;
   DevBuf ms_mbuf, ms_setof, ms_pairs, ms_keys, ms_vals, ms_keys2, ms_vals2, ms_ukeys, ms_uvals, ms_cub;
   float4* pt0 = nullptr;  // per-point screen data seeded with d(., e0)
   int* ms_count = nullptr;
@@ -304,6 +310,8 @@ int run_finalize_window(ebc_ctx* ctx, int nsplit, double nterms, int gterms, int
 struct TcPlan {
   int ncb, ntiles, tps, nsplit;
   size_t smem;
+  int stages;
+  int list_cap;  // kept-tile list entries (0: pruning off)
 };
 
 int tc_es(int kind) { return kind == tc::KIND_TF32 ? 4 : 2; }
@@ -314,7 +322,6 @@ bool plan_tc(const ebc_ctx* ctx, TcPlan& p) {
   const int64_t ncand = ctx->c1 - ctx->c0;
   p.ncb = (int)((ncand + tc::M - 1) / tc::M);
   p.ntiles = (int)((ctx->n + ctx->tc_np - 1) / ctx->tc_np);
-  p.smem = tc::smem_bytes(ctx->kpad, ctx->tc_np, tc_es(ctx->tc_kind), tc_parts(ctx->tc_kind));
   const int64_t slots = ctx->num_sms;  // one CTA per SM
   double best_cost = 1e300;
   p.tps = p.ntiles;
@@ -329,6 +336,18 @@ bool plan_tc(const ebc_ctx* ctx, TcPlan& p) {
     }
   }
   p.nsplit = (p.ntiles + p.tps - 1) / p.tps;
+  const int es = tc_es(ctx->tc_kind), parts = tc_parts(ctx->tc_kind);
+  p.list_cap = 0;
+  p.stages = tc::stages_for(ctx->kpad, ctx->tc_np, es, parts);
+  if (ctx->tc_prune && p.tps <= 65535) {
+    const size_t lb = tc::list_bytes_for(p.tps);
+    const int st = tc::stages_for(ctx->kpad, ctx->tc_np, es, parts, lb);
+    if (st >= 2 && st >= p.stages - 1) {  // keep the ring at least as deep, minus one stage at most
+      p.list_cap = p.tps;
+      p.stages = st;
+    }
+  }
+  p.smem = tc::smem_bytes(ctx->kpad, ctx->tc_np, es, parts, p.list_cap ? tc::list_bytes_for(p.tps) : 0);
   return true;
 }
 
@@ -338,10 +357,10 @@ int launch_tc_t(ebc_ctx* ctx, const TcPlan& p, const int* level_now, int level) 
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
   dim3 grid(p.ncb, p.nsplit);
   TcAnchors an{ctx->anchors, ctx->pitch, ctx->tile_anchor, ctx->pttc, ctx->n_pad, ctx->kpmax, ctx->tc_ntl,
-               ctx->tc_vmax, ctx->tc_kc, ctx->tc_kx};
+               ctx->tc_vmax, ctx->tc_kc, ctx->tc_kx, p.list_cap ? ctx->rho : nullptr, ctx->tile_rad, ctx->cmx,
+               p.list_cap};
   kern<<<grid, tc::THREADS, p.smem, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->d, (const unsigned char*)ctx->Vhi,
-                                                   (const unsigned char*)ctx->Vlo, an, ctx->kpad,
-                                                   tc::stages_for(ctx->kpad, ctx->tc_np, tc_es(KIND), tc_parts(KIND)), ctx->c0,
+                                                   (const unsigned char*)ctx->Vlo, an, ctx->kpad, p.stages, ctx->c0,
                                                    p.ntiles, p.tps, (double*)ctx->part_g.p, (float*)ctx->part_e.p,
                                                    ctx->n_pad, level_now, level, nullptr, FlagOut{});
   KCHECK();
@@ -350,31 +369,33 @@ int launch_tc_t(ebc_ctx* ctx, const TcPlan& p, const int* level_now, int level) 
 
 // Work-matrix flag screen on the tensor cores: candidates = gathered member rows.
 template <int NP, int KIND>
-int launch_tc_flag_t(ebc_ctx* ctx, const TcPlan& p, const float* Vc, const int* tanchor, FlagOut fo) {
+int launch_tc_flag_t(ebc_ctx* ctx, const TcPlan& p, const float* Vc, const int* tanchor, const float* trad,
+                     FlagOut fo) {
   auto kern = k_screen_tc<NP, KIND, true>;
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
   dim3 grid(p.ncb, p.nsplit);
   TcAnchors an{ctx->anchors, ctx->pitch, tanchor, ctx->ipa0, ctx->n_pad, ctx->kpmax, ctx->tc_ntl,
-               ctx->tc_vmax, ctx->tc_kc, ctx->tc_kx};
+               ctx->tc_vmax, ctx->tc_kc, ctx->tc_kx, p.list_cap ? ctx->rho : nullptr, trad, ctx->cmx0,
+               p.list_cap};
   kern<<<grid, tc::THREADS, p.smem, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->d, (const unsigned char*)ctx->Vhi,
-                                                   (const unsigned char*)ctx->Vlo, an, ctx->kpad,
-                                                   tc::stages_for(ctx->kpad, ctx->tc_np, tc_es(KIND), tc_parts(KIND)), 0,
+                                                   (const unsigned char*)ctx->Vlo, an, ctx->kpad, p.stages, 0,
                                                    p.ntiles, p.tps, nullptr, nullptr, 0, nullptr, 0, Vc, fo);
   KCHECK();
   return EBC_OK;
 }
 
-int launch_tc_flag(ebc_ctx* ctx, const TcPlan& p, const float* Vc, const int* tanchor, FlagOut fo) {
+int launch_tc_flag(ebc_ctx* ctx, const TcPlan& p, const float* Vc, const int* tanchor, const float* trad,
+                   FlagOut fo) {
   switch (ctx->tc_kind) {
     case tc::KIND_F16:
-      if (ctx->tc_np == 128) return launch_tc_flag_t<128, tc::KIND_F16>(ctx, p, Vc, tanchor, fo);
-      return launch_tc_flag_t<64, tc::KIND_F16>(ctx, p, Vc, tanchor, fo);
+      if (ctx->tc_np == 128) return launch_tc_flag_t<128, tc::KIND_F16>(ctx, p, Vc, tanchor, trad, fo);
+      return launch_tc_flag_t<64, tc::KIND_F16>(ctx, p, Vc, tanchor, trad, fo);
     case tc::KIND_BF16:
-      if (ctx->tc_np == 128) return launch_tc_flag_t<128, tc::KIND_BF16>(ctx, p, Vc, tanchor, fo);
-      return launch_tc_flag_t<64, tc::KIND_BF16>(ctx, p, Vc, tanchor, fo);
+      if (ctx->tc_np == 128) return launch_tc_flag_t<128, tc::KIND_BF16>(ctx, p, Vc, tanchor, trad, fo);
+      return launch_tc_flag_t<64, tc::KIND_BF16>(ctx, p, Vc, tanchor, trad, fo);
     default:
-      if (ctx->tc_np == 128) return launch_tc_flag_t<128, tc::KIND_TF32>(ctx, p, Vc, tanchor, fo);
-      return launch_tc_flag_t<64, tc::KIND_TF32>(ctx, p, Vc, tanchor, fo);
+      if (ctx->tc_np == 128) return launch_tc_flag_t<128, tc::KIND_TF32>(ctx, p, Vc, tanchor, trad, fo);
+      return launch_tc_flag_t<64, tc::KIND_TF32>(ctx, p, Vc, tanchor, trad, fo);
   }
 }
 
@@ -423,6 +444,12 @@ int run_screen_window(ebc_ctx* ctx, int eb, int fin_blocks) {
     if (!rc) rc = run_finalize_window(ctx, p.nsplit, nterms_ffma, p.tp, fin_blocks, 2.0, nullptr, 0);
   } else {
     if (use_tc) {
+      if (tp.list_cap) {
+        k_tile_cmmax<<<(unsigned)((ctx->tc_ntl * 32 + 255) / 256), 256, 0, ctx->stream>>>(ctx->cm64, ctx->n,
+                                                                                          ctx->tc_ntl, ctx->tc_np,
+                                                                                          ctx->cmx);
+        KCHECK();
+      }
       rc = launch_tc(ctx, tp, ctx->level, 0);
       if (!rc) rc = run_finalize_window(ctx, tp.nsplit, (double)tp.tps * ctx->tc_np, 32, fin_blocks, 2.0,
                                         ctx->level, 0);
@@ -556,11 +583,11 @@ int do_reset(ebc_ctx* ctx) {
 void free_ctx(ebc_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
-  void* ptrs[] = {c->V32, c->V64, c->e0d, c->cm64, c->pt, c->nv32, c->level, c->stats, c->Vhi, c->Vlo, c->pttc, c->kpmax, c->anchors, c->nva, c->tile_anchor, c->tc_vmax, c->fps_keys, c->ipa0, c->selected, c->chunkpart, c->counter, c->cur, c->best,
+  void* ptrs[] = {c->V32, c->V64, c->e0d, c->cm64, c->pt, c->nv32, c->level, c->stats, c->Vhi, c->Vlo, c->pttc, c->kpmax, c->anchors, c->nva, c->tile_anchor, c->tc_vmax, c->fps_keys, c->ipa0, c->tile_rad, c->rho, c->cmx, c->cmx0, c->selected, c->chunkpart, c->counter, c->cur, c->best,
                   c->maxlb, c->wcount, c->wlist, c->wgain, c->ub};
   for (void* p : ptrs)
     if (p) cudaFree(p);
-  DevBuf* bufs[] = {&c->ms_tanchor, &c->part_g, &c->part_e, &c->part_r, &c->sel_out, &c->val_out, &c->gain_out, &c->ms_part,
+  DevBuf* bufs[] = {&c->ms_tanchor, &c->ms_trad, &c->part_g, &c->part_e, &c->part_r, &c->sel_out, &c->val_out, &c->gain_out, &c->ms_part,
                     &c->ms_off, &c->ms_idx, &c->ms_out, &c->ms_mbuf, &c->ms_setof, &c->ms_pairs, &c->ms_keys,
                     &c->ms_vals, &c->ms_keys2, &c->ms_vals2, &c->ms_ukeys, &c->ms_uvals, &c->ms_cub};
   void* more[] = {c->pt0, c->ms_count, c->ms_nruns};
@@ -609,6 +636,7 @@ int multiset_sparse(ebc_ctx* ctx, int64_t l, int64_t nnz) {
   if (ctx->ms_mode == 1 && ctx->screen_mode == 3 && plan_tc(ctx, tp)) {
     // tensor-core flag screen: anchors of the member blocks, reset-state seeds
     rc = ensure(ctx, ctx->ms_tanchor, (size_t)(mrows / 128 + 1) * sizeof(int));
+    if (!rc) rc = ensure(ctx, ctx->ms_trad, (size_t)(mrows / 128 + 1) * sizeof(float));
     if (!rc && !ctx->ipa0) {
       CU(cudaMalloc(&ctx->ipa0, (size_t)ctx->tc_na * ctx->n_pad * sizeof(float)));
       TcSeeds s0 = tc_seeds(ctx);
@@ -619,9 +647,10 @@ int multiset_sparse(ebc_ctx* ctx, int64_t l, int64_t nnz) {
     if (!rc) {
       k_tile_anchor<<<(unsigned)((nnz + 127) / 128), 128, 0, ctx->stream>>>(
           (const float*)ctx->ms_mbuf.p, ctx->pitch, nnz, ctx->d, ctx->anchors, ctx->pitch, ctx->tc_na,
-          (int*)ctx->ms_tanchor.p);
+          (int*)ctx->ms_tanchor.p, (float*)ctx->ms_trad.p);
       KCHECK();
-      rc = launch_tc_flag(ctx, tp, (const float*)ctx->ms_mbuf.p, (const int*)ctx->ms_tanchor.p, fo);
+      rc = launch_tc_flag(ctx, tp, (const float*)ctx->ms_mbuf.p, (const int*)ctx->ms_tanchor.p,
+                          (const float*)ctx->ms_trad.p, fo);
     }
   } else {
     ScreenPlan p;
@@ -847,6 +876,13 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
       CUC(cudaMalloc(&ctx->tile_anchor, (size_t)(ctx->n_pad / 128 + 1) * sizeof(int)));
       CUC(cudaMemsetAsync(ctx->tile_anchor, 0, (size_t)(ctx->n_pad / 128 + 1) * sizeof(int), ctx->stream));
       CUC(cudaMalloc(&ctx->fps_keys, (size_t)(ctx->tc_na + 1) * sizeof(unsigned long long)));
+      const char* pr_env = getenv("EBC200_TC_PRUNE");
+      ctx->tc_prune = !(pr_env && pr_env[0] == '0');
+      CUC(cudaMalloc(&ctx->tile_rad, (size_t)(ctx->n_pad / 128 + 1) * sizeof(float)));
+      CUC(cudaMemsetAsync(ctx->tile_rad, 0, (size_t)(ctx->n_pad / 128 + 1) * sizeof(float), ctx->stream));
+      CUC(cudaMalloc(&ctx->rho, (size_t)ctx->tc_na * ctx->tc_ntl * sizeof(float)));
+      CUC(cudaMalloc(&ctx->cmx, (size_t)ctx->tc_ntl * sizeof(float)));
+      CUC(cudaMalloc(&ctx->cmx0, (size_t)ctx->tc_ntl * sizeof(float)));
       CUC(cudaMemsetAsync(ctx->fps_keys, 0, (size_t)(ctx->tc_na + 1) * sizeof(unsigned long long), ctx->stream));
     }
   }
@@ -897,7 +933,8 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
                                                        ctx->tc_na, ctx->nva, ctx->n_pad);
       CUC(cudaGetLastError());
       k_tile_anchor<<<(unsigned)((n + 127) / 128), 128, 0, ctx->stream>>>(ctx->V32, ctx->pitch, n, d, ctx->anchors,
-                                                                          ctx->pitch, ctx->tc_na, ctx->tile_anchor);
+                                                                          ctx->pitch, ctx->tc_na, ctx->tile_anchor,
+                                                                          ctx->tile_rad);
       CUC(cudaGetLastError());
       k_seed_ipa<<<(unsigned)((ctx->n_pad + 255) / 256), 256, 0, ctx->stream>>>(ctx->cm64, n, ctx->n_pad,
                                                                                  tc_seeds(ctx));
@@ -905,7 +942,10 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
       const int64_t cells = (int64_t)ctx->tc_na * ctx->tc_ntl;
       k_tile_kpmax<<<(unsigned)((cells + 255) / 256), 256, 0, ctx->stream>>>(
           ctx->e0d, ctx->nv32, ctx->nva, ctx->n_pad, ctx->tc_na, n, ctx->tc_ntl, ctx->tc_np, ctx->tc_kp, ctx->kpmax,
-          ctx->tc_vmax);
+          ctx->tc_vmax, ctx->rho);
+      CUC(cudaGetLastError());
+      k_tile_cmmax<<<(unsigned)((ctx->tc_ntl * 32 + 255) / 256), 256, 0, ctx->stream>>>(ctx->e0d, n, ctx->tc_ntl,
+                                                                                        ctx->tc_np, ctx->cmx0);
       CUC(cudaGetLastError());
       CUC(cudaStreamSynchronize(ctx->stream));
       cudaFree(mind);

@@ -222,19 +222,22 @@ __device__ __forceinline__ void st32(uint32_t taddr, const uint32_t (&r)[32]) {
       : "memory");
 }
 
-inline int stages_for(int kpad, int np, int es = 4, int parts = 2) {
+inline int stages_for(int kpad, int np, int es = 4, int parts = 2, size_t list_bytes = 0) {
   const size_t stage = (size_t)parts * np * kpad * es;
-  const size_t budget = 220 * 1024;
+  const size_t budget = 220 * 1024 - list_bytes;
   int st = (int)(budget / stage);
   return st > MAX_STAGES ? MAX_STAGES : st;
 }
 
-inline size_t smem_bytes(int kpad, int np, int es = 4, int parts = 2) {
+// the kept-tile list (uint16 per point tile of the CTA's split) follows the barriers
+inline size_t list_bytes_for(int tps) { return ((size_t)tps * 2 + 15) / 16 * 16; }
+
+inline size_t smem_bytes(int kpad, int np, int es = 4, int parts = 2, size_t list_bytes = 0) {
   const size_t stage = (size_t)parts * np * kpad * es;  // B_hi (, B_lo)
-  size_t ring = stages_for(kpad, np, es, parts) * stage;
+  size_t ring = stages_for(kpad, np, es, parts, list_bytes) * stage;
   const size_t xchg = EPI_WARPGROUPS * 128 * (sizeof(double) + sizeof(float));  // slice exchange reuses the ring
   if (ring < xchg) ring = xchg;
-  return ring + (2 * MAX_STAGES + 8) * sizeof(uint64_t) + 64;
+  return ring + (2 * MAX_STAGES + 8) * sizeof(uint64_t) + 64 + list_bytes;
 }
 
 }  // namespace tc
@@ -367,7 +370,8 @@ __global__ void k_nva(const float* __restrict__ V32, int pitch, int64_t n, int d
 
 // Per 128-candidate block: the anchor minimising max_c |c - mu_a|^2 (ties: lower a).
 __global__ void k_tile_anchor(const float* __restrict__ V32, int pitch, int64_t n, int d,
-                              const float* __restrict__ anchors, int apitch, int na, int* __restrict__ tile_anchor) {
+                              const float* __restrict__ anchors, int apitch, int na, int* __restrict__ tile_anchor,
+                              float* __restrict__ tile_rad) {
   __shared__ float wmax[4];
   const int64_t c = (int64_t)blockIdx.x * 128 + threadIdx.x;
   float best = INFINITY;
@@ -392,7 +396,11 @@ __global__ void k_tile_anchor(const float* __restrict__ V32, int pitch, int64_t 
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) tile_anchor[blockIdx.x] = besta;
+  if (threadIdx.x == 0) {
+    tile_anchor[blockIdx.x] = besta;
+    // R = max_c |c - mu| rounded up (fp32 sum error (d+2)u << 1e-5)
+    if (tile_rad) tile_rad[blockIdx.x] = sqrtf(best) * (1.f + 1e-5f) + 1e-30f;
+  }
 }
 
 // Seeds from the cached minima for every anchor; padded points get -1e30 so
@@ -410,21 +418,50 @@ __global__ void k_seed_ipa(const double* __restrict__ cm64, int64_t n, int64_t n
 // vmax[t] = max |v| over the tile (rounded up).
 __global__ void k_tile_kpmax(const double* __restrict__ e0d, const float* __restrict__ nv32,
                              const float* __restrict__ nva, int64_t stride, int na, int64_t n, int64_t ntiles,
-                             int np, float kp_coef, float* __restrict__ kpmax, float* __restrict__ vmax) {
+                             int np, float kp_coef, float* __restrict__ kpmax, float* __restrict__ vmax,
+                             float* __restrict__ rho) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (int64_t)na * ntiles) return;
   const int a = (int)(i / ntiles);
   const int64_t t = i - (int64_t)a * ntiles;
-  float m = 0.f, vm = 0.f;
+  float m = 0.f, vm = 0.f, rm = INFINITY;
   for (int j = 0; j < np; ++j) {
     const int64_t v = t * np + j;
     if (v < n) {
-      m = fmaxf(m, kp_coef * ((float)e0d[v] + nva[a * stride + v]));
+      const float q = nva[a * stride + v];
+      m = fmaxf(m, kp_coef * ((float)e0d[v] + q));
       vm = fmaxf(vm, nv32[v]);
+      rm = fminf(rm, q);
     }
   }
   kpmax[a * ntiles + t] = m * (1.f + 1e-6f);
   if (a == 0) vmax[t] = sqrtf(vm) * (1.f + 1e-5f);
+  // rho = min_v |v - mu_a| rounded down (nva is the fp64 value rounded to fp32)
+  rho[a * ntiles + t] = sqrtf(rm) * (1.f - 1e-5f);
+}
+
+// cmx[t] = max over the tile's points of the cached minimum (rounded up).
+__global__ void k_tile_cmmax(const double* __restrict__ cm64, int64_t n, int64_t ntiles, int np,
+                             float* __restrict__ cmx) {
+  const int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= ntiles) return;
+  double m = 0.0;
+  for (int j = lane; j < np; j += 32) {
+    const int64_t v = t * np + j;
+    if (v < n) m = fmax(m, cm64[v]);
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffff, m, o));
+  if (lane == 0) cmx[t] = __double2float_ru(m);
+}
+
+// Certified tile-pair pruning: every point of tile t is at least rho - R from
+// every candidate of the block (triangle inequality through the anchor), so
+// when (rho - R)^2 > max cm over the tile no pair can contribute or count.
+// Explicit roundings (no contraction) so every role of the CTA agrees bit for bit.
+__device__ __forceinline__ bool tile_prunable(float rho, float rad, float cmx) {
+  const float gap = __fsub_rn(rho, rad);
+  return gap > 0.f && __fmul_rn(__fmul_rn(gap, gap), 0.99999f) > cmx;
 }
 
 // Anchor data of the tensor screen (kernel argument).
@@ -439,6 +476,12 @@ struct TcAnchors {
   const float* vmax;        // per point tile
   float kc;                 // kc = kc_coef (|mu| |c'| + |c'|^2)
   float kx;                 // per pair MMA term kx |v|max |c'|
+  // tile-pair pruning (nullptr: off): rho[a][t] = min_v |v - mu_a|, rad[block]
+  // = max_c |c - mu_a|, cmx[t] = max cm over the tile (current step)
+  const float* rho;
+  const float* rad;
+  const float* cmx;
+  int list_cap;             // uint16 entries reserved for the kept-tile list
 };
 
 // One CTA: candidates [cand0 + 128*bx, +128) x V tiles [t0, t1) of NP points.
@@ -501,14 +544,45 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  // kept point tiles of this CTA (certified tile-pair pruning, tile_prunable):
+  // every role walks the same compacted list, built once by all threads
+  uint16_t* tlist = nullptr;
+  int ntk = nt;
+  if (an.rho && nt <= an.list_cap) {
+    __shared__ int wsum[THREADS / 32];
+    tlist = reinterpret_cast<uint16_t*>(smem + (size_t)stages * stage_bytes + (2 * MAX_STAGES + 8) * sizeof(uint64_t) +
+                                        64);
+    const float rad = an.rad[crow >> 7];
+    const float* rho = an.rho + (int64_t)an.tile_anchor[crow >> 7] * an.kpstride;
+    int base = 0;
+    for (int c0i = 0; c0i < nt; c0i += THREADS) {
+      const int i = c0i + tid;
+      const bool keep = i < nt && !tile_prunable(rho[t0 + i], rad, an.cmx[t0 + i]);
+      const unsigned bal = __ballot_sync(0xffffffffu, keep);
+      if (lane == 0) wsum[warp] = __popc(bal);
+      __syncthreads();
+      int off = base, tot = 0;
+#pragma unroll 1
+      for (int w = 0; w < THREADS / 32; ++w) {
+        off += w < warp ? wsum[w] : 0;
+        tot += wsum[w];
+      }
+      if (keep) tlist[off + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)i;
+      base += tot;
+      __syncthreads();
+    }
+    ntk = base;
+  }
+  auto TL = [&](int k) -> int { return tlist ? (int)tlist[k] : k; };
+
   if (warp == 0) {
     // ---------------- producer
     if (lane == 0) {
-      for (int it = 0; it < nt; ++it) {
+      for (int it = 0; it < ntk; ++it) {
         const int s = it % stages;
         if (it >= stages) mbar_wait(&sempty[s], ((it / stages) - 1) & 1);
         unsigned char* st = stage0 + s * stage_bytes;
-        const int64_t prow = (int64_t)(t0 + it) * NP;
+        const int64_t prow = (int64_t)(t0 + TL(it)) * NP;
         mbar_arrive_expect_tx(&full[s], stage_bytes);
         bulk_g2s(st, Vhi + prow * kpad * ES, b_bytes, &full[s]);
         if (TM::PARTS == 2) bulk_g2s(st + b_bytes, Vlo + prow * kpad * ES, b_bytes, &full[s]);
@@ -529,7 +603,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     const uint32_t ahi = tmem + COL_AHI, alo = tmem + TM::ALO;
     mbar_wait(aready, 0);
     fence_after();
-    for (int it = b; it < nt && b < NB; it += NB) {
+    for (int it = b; it < ntk && b < NB; it += NB) {
       const int s = it % stages;
       mbar_wait(&full[s], (it / stages) & 1);
       if (it >= NB) mbar_wait(&tempty[b], ((it / NB) - 1) & 1);
@@ -627,13 +701,14 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     float e = 0.f;
     constexpr int NB = TM::NB;
     constexpr int SW = SLICE;  // accumulator columns per thread and tile
-    for (int it = 0; it < nt; ++it) {
+    for (int it = 0; it < ntk; ++it) {
       const int b = it % NB;
+      const int tt = t0 + TL(it);  // point tile
       // this slice's point seeds ip: issued before the accumulator wait so the
       // (L1-broadcast) loads overlap the MMA
       float ipv[SW];
       {
-        const float4* pp4 = reinterpret_cast<const float4*>(ipa + (int64_t)(t0 + it) * NP + half * SLICE);
+        const float4* pp4 = reinterpret_cast<const float4*>(ipa + (int64_t)tt * NP + half * SLICE);
 #pragma unroll
         for (int i = 0; i < SW / 4; ++i) {
           const float4 p = __ldg(pp4 + i);
@@ -645,7 +720,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       }
       // one error quantum per tile: kpmax = max_v kp over the tile (bounds every
       // pair's kp_v; computed at reset, cm only decreases within a run)
-      const float kq = kpa[t0 + it] + fmaf(kxc, __ldg(an.vmax + t0 + it), kc);
+      const float kq = kpa[tt] + fmaf(kxc, __ldg(an.vmax + tt), kc);
       const float thr = -kq;
       mbar_wait(&tfull[b], (it / NB) & 1);
       fence_after();
@@ -672,7 +747,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
 #pragma unroll
           for (int i = 0; i < SW; ++i) {
             if (S[i] + ic > thr) {  // rare: possibly closer than e0
-              const int64_t v = (int64_t)(t0 + it) * NP + half * SLICE + i;
+              const int64_t v = (int64_t)tt * NP + half * SLICE + i;
               if (v < fo.npoints && c < fo.ncands) {
                 const int slot = atomicAdd(fo.count, 1);
                 if (slot < fo.cap) fo.pairs[slot] = make_uint2((unsigned)v, (unsigned)c);

@@ -324,3 +324,23 @@ def test_every_screen_variant_vs_oracle(monkeypatch, variant, prec, d):
     np.testing.assert_allclose(np.cumsum(s.gains), vals, rtol=1e-10)
     if mode == "3":
         assert optimize.last_stats(f)[2] == rung
+
+
+@pytest.mark.parametrize("prune", ["1", "0"])
+@pytest.mark.parametrize("regimes", [5, 50])
+def test_clustered_surrogate_on_anchored_tensor_rung(monkeypatch, prune, regimes):
+    """Injection-molding surrogate (C4's data at reduced N; 50 regimes = the
+    near-tie stress case): the anchored tensor screen keeps the run on rung 0,
+    with and without certified tile-pair pruning, and selects what the oracle
+    selects."""
+    import datasets
+    from paper_2105_12026_b200 import optimize
+    monkeypatch.setenv("EBC200_TC_PRUNE", prune)
+    X = datasets.surrogate(20000, 32, regimes, 0.01, 0).astype(np.float32)
+    f = fn(X, eb.Precision.FP32)
+    s = eb.greedy_maximize(f, eb.OptimizerBudget(k=8))
+    sel, vals, _, _ = oracle.greedy(X.astype(np.float64), 8)
+    assert s.selected == sel
+    np.testing.assert_allclose(np.cumsum(s.gains), vals, rtol=1e-10)
+    if regimes == 5:
+        assert optimize.last_stats(f)[2] == 0
