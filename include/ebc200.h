@@ -129,9 +129,15 @@ int ebc_last_timings(const ebc_ctx* ctx, double* out_ms4);
  * Gram, 1 FFMA Gram, 2 direct, -1 n/a), [3] steps. */
 int ebc_last_stats(const ebc_ctx* ctx, int64_t* out4);
 
+/* Point-candidate pairs the tensor screen actually evaluated since the last
+ * reset / Greedy run (tile pairs kept by the certified tile-pair pruning x
+ * 128 x points per tile).  For bench.py's roofline. */
+int ebc_last_screen_work(const ebc_ctx* ctx, int64_t* out_pairs);
+
 /* Screen configuration: [0] mode (0 direct, 1 FFMA Gram, 2 ladder from FFMA
  * Gram, 3 ladder from the tensor screen), [1] points per tensor tile (0: no
- * tensor screen), [2] tensor operand split (1 BF16 h+m, 0 TF32 hi+lo, -1 n/a),
+ * tensor screen), [2] tensor operand kind (1 BF16 h+m split, 0 TF32 hi+lo split,
+ * 2 FP16 values of fp16-stored grounds, -1 n/a),
  * [3] padded K of the tensor operands. */
 int ebc_screen_info(const ebc_ctx* ctx, int64_t* out4);
 

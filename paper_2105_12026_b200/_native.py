@@ -12,7 +12,8 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libebc200.so")
+# EBC200_LIB_PATH: an alternative in-tree build (development A/B of compile-time variants)
+LIB_PATH = os.environ.get("EBC200_LIB_PATH") or os.path.join(_HERE, "libebc200.so")
 
 EBC_OK, EBC_EINVAL, EBC_EINDEX, EBC_ECUDA, EBC_ECOMM = 0, 1, 2, 3, 4
 EBC_F32, EBC_F16, EBC_F64 = 0, 1, 2
@@ -45,6 +46,7 @@ SIGNATURES = {
     "ebc_last_timings": (ctypes.c_int, [_vp, _f64p]),
     "ebc_last_launches": (_i64, [_vp]),
     "ebc_last_stats": (ctypes.c_int, [_vp, _i64p]),
+    "ebc_last_screen_work": (ctypes.c_int, [_vp, _i64p]),
     "ebc_screen_info": (ctypes.c_int, [_vp, _i64p]),
     "ebc_destroy": (None, [_vp]),
     "ebc_last_error": (ctypes.c_char_p, [_vp]),

@@ -358,7 +358,7 @@ int launch_tc_t(ebc_ctx* ctx, const TcPlan& p, const int* level_now, int level) 
   dim3 grid(p.ncb, p.nsplit);
   TcAnchors an{ctx->anchors, ctx->pitch, ctx->tile_anchor, ctx->pttc, ctx->n_pad, ctx->kpmax, ctx->tc_ntl,
                ctx->tc_vmax, ctx->tc_kc, ctx->tc_kx, p.list_cap ? ctx->rho : nullptr, ctx->tile_rad, ctx->cmx,
-               p.list_cap};
+               p.list_cap, (unsigned long long*)(ctx->stats + 4)};
   kern<<<grid, tc::THREADS, p.smem, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->d, (const unsigned char*)ctx->Vhi,
                                                    (const unsigned char*)ctx->Vlo, an, ctx->kpad, p.stages, ctx->c0,
                                                    p.ntiles, p.tps, (double*)ctx->part_g.p, (float*)ctx->part_e.p,
@@ -376,7 +376,7 @@ int launch_tc_flag_t(ebc_ctx* ctx, const TcPlan& p, const float* Vc, const int* 
   dim3 grid(p.ncb, p.nsplit);
   TcAnchors an{ctx->anchors, ctx->pitch, tanchor, ctx->ipa0, ctx->n_pad, ctx->kpmax, ctx->tc_ntl,
                ctx->tc_vmax, ctx->tc_kc, ctx->tc_kx, p.list_cap ? ctx->rho : nullptr, trad, ctx->cmx0,
-               p.list_cap};
+               p.list_cap, nullptr};
   kern<<<grid, tc::THREADS, p.smem, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->d, (const unsigned char*)ctx->Vhi,
                                                    (const unsigned char*)ctx->Vlo, an, ctx->kpad, p.stages, 0,
                                                    p.ntiles, p.tps, nullptr, nullptr, 0, nullptr, 0, Vc, fo);
@@ -565,7 +565,7 @@ int enqueue_greedy(ebc_ctx* ctx, int k) {
 
 int do_reset(ebc_ctx* ctx) {
   const int blocks = (int)((ctx->n + 255) / 256);
-  CU(cudaMemsetAsync(ctx->stats, 0, 4 * sizeof(long long), ctx->stream));
+  CU(cudaMemsetAsync(ctx->stats, 0, 6 * sizeof(long long), ctx->stream));
   k_reset<<<blocks, 256, 0, ctx->stream>>>(ctx->n, ctx->e0d, ctx->nv32, ctx->pk, ctx->cm64, ctx->pt, ctx->selected,
                                            nullptr, tc_seeds(ctx));
   KCHECK();
@@ -820,8 +820,8 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
   CUC(cudaMemsetAsync(ctx->pt, 0, (size_t)ctx->n_pad * sizeof(float4), ctx->stream));
   CUC(cudaMalloc(&ctx->nv32, (size_t)ctx->n_pad * sizeof(float)));
   CUC(cudaMemsetAsync(ctx->nv32, 0, (size_t)ctx->n_pad * sizeof(float), ctx->stream));
-  CUC(cudaMalloc(&ctx->stats, 4 * sizeof(long long)));
-  CUC(cudaMemsetAsync(ctx->stats, 0, 4 * sizeof(long long), ctx->stream));
+  CUC(cudaMalloc(&ctx->stats, 6 * sizeof(long long)));  // [4]: tensor-screen tile pairs executed
+  CUC(cudaMemsetAsync(ctx->stats, 0, 6 * sizeof(long long), ctx->stream));
   CUC(cudaMalloc(&ctx->level, sizeof(int)));
   CUC(cudaMemsetAsync(ctx->level, 0, sizeof(int), ctx->stream));
   // tensor-core screen: fp32-path grounds whose 128-candidate tile of hi+lo
@@ -1014,6 +1014,15 @@ int ebc_screen_info(const ebc_ctx* ctx, int64_t* out4) {
   out4[1] = ctx->tc_np;
   out4[2] = ctx->tc_np ? ctx->tc_kind : -1;
   out4[3] = ctx->kpad;
+  return EBC_OK;
+}
+
+int ebc_last_screen_work(const ebc_ctx* ctx, int64_t* out_pairs) {
+  if (!ctx || !out_pairs) return fail(nullptr, EBC_EINVAL, "ebc_last_screen_work: NULL argument");
+  long long v[6];
+  if (cudaMemcpy(v, ctx->stats, sizeof(v), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return fail(const_cast<ebc_ctx*>(ctx), EBC_ECUDA, "ebc_last_screen_work: copy failed");
+  *out_pairs = (int64_t)v[4] * tc::M * (ctx->tc_np ? ctx->tc_np : 0);
   return EBC_OK;
 }
 

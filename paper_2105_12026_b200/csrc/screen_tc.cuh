@@ -126,10 +126,26 @@ __device__ __forceinline__ void ld64(uint32_t taddr, float (&v)[64]) {
   for (int i = 0; i < 64; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 template <int W>
 __device__ __forceinline__ void ldcols(uint32_t taddr, float (&v)[W]) {
   if constexpr (W == 64) {
     ld64(taddr, v);
+  } else if constexpr (W == 16) {
+    ld16(taddr, v);
   } else {
     static_assert(W % 32 == 0, "columns per thread: multiple of 32");
 #pragma unroll
@@ -143,7 +159,10 @@ __device__ __forceinline__ void ldcols(uint32_t taddr, float (&v)[W]) {
 }
 
 constexpr int M = 128;        // candidates per CTA (UMMA M)
-constexpr int EPI_WARPGROUPS = 2;  // epilogue warpgroups (slices of the point columns)
+#ifndef EBC200_EPI_WARPGROUPS
+#define EBC200_EPI_WARPGROUPS 2
+#endif
+constexpr int EPI_WARPGROUPS = EBC200_EPI_WARPGROUPS;  // epilogue warpgroups (slices of the point columns)
 constexpr int MMA_WARPS = 3;       // one issuing warp per accumulator buffer (tiles round-robin)
 constexpr int EPI_WARP0 = 1 + MMA_WARPS;
 constexpr int THREADS = 32 * EPI_WARP0 + 128 * EPI_WARPGROUPS;  // producer + MMA warps + epilogue
@@ -230,7 +249,7 @@ inline int stages_for(int kpad, int np, int es = 4, int parts = 2, size_t list_b
 }
 
 // the kept-tile list (uint16 per point tile of the CTA's split) follows the barriers
-inline size_t list_bytes_for(int tps) { return ((size_t)tps * 2 + 15) / 16 * 16; }
+__host__ __device__ constexpr size_t list_bytes_for(int tps) { return ((size_t)tps * 2 + 15) / 16 * 16; }
 
 inline size_t smem_bytes(int kpad, int np, int es = 4, int parts = 2, size_t list_bytes = 0) {
   const size_t stage = (size_t)parts * np * kpad * es;  // B_hi (, B_lo)
@@ -482,6 +501,7 @@ struct TcAnchors {
   const float* rad;
   const float* cmx;
   int list_cap;             // uint16 entries reserved for the kept-tile list
+  unsigned long long* work; // if set: += executed (candidate block, point tile) pairs
 };
 
 // One CTA: candidates [cand0 + 128*bx, +128) x V tiles [t0, t1) of NP points.
@@ -574,6 +594,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     ntk = base;
   }
   auto TL = [&](int k) -> int { return tlist ? (int)tlist[k] : k; };
+  if (an.work && tid == 0) atomicAdd(an.work, (unsigned long long)ntk);
 
   if (warp == 0) {
     // ---------------- producer
@@ -756,19 +777,23 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
           }
         }
       } else if (mb + ic > thr) {
-        float cnt = 0.f;
+        // four independent fp32 partial sums / counts per 32 columns (ILP); each
+        // partial adds 8 terms, so every fp64 fold still covers <= 32 terms
+        // combined by a fixed tree (the finalize bound assumes 32)
+        float cnt4[4] = {0.f, 0.f, 0.f, 0.f};
+        constexpr int GW = SW < 32 ? SW : 32;  // columns per fp64 fold
 #pragma unroll
-        for (int h = 0; h < SW; h += 32) {
-          float g = 0.f;
+        for (int h = 0; h < SW; h += GW) {
+          float g4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-          for (int i = h; i < h + 32; ++i) {
+          for (int i = h; i < h + GW; ++i) {
             const float a = S[i] + ic;
-            g += fmaxf(a, 0.f);
-            cnt += (a > thr) ? 1.f : 0.f;
+            g4[i & 3] += fmaxf(a, 0.f);
+            cnt4[i & 3] += (a > thr) ? 1.f : 0.f;
           }
-          g64 += (double)g;
+          g64 += (double)((g4[0] + g4[1]) + (g4[2] + g4[3]));
         }
-        e = fmaf(cnt, kq, e);
+        e = fmaf((cnt4[0] + cnt4[1]) + (cnt4[2] + cnt4[3]), kq, e);
       }
     }
     if (!FLAG) {

@@ -110,8 +110,17 @@ def last_stats(f: EbcFunction):
     return tuple(int(x) for x in out)
 
 
+def last_screen_work(f: EbcFunction) -> int:
+    """Point-candidate pairs the tensor screen evaluated in the last run (after pruning)."""
+    out = np.zeros(1, dtype=np.int64)
+    _native.check(f._lib.ebc_last_screen_work(f.native_context,
+                                              out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))),
+                  f.native_context)
+    return int(out[0])
+
+
 def screen_info(f: EbcFunction):
-    """(mode, tensor tile points, tensor split 1=BF16/0=TF32/-1, padded K)."""
+    """(mode, tensor tile points, tensor operand kind 1=BF16 split/0=TF32 split/2=FP16/-1, padded K)."""
     out = np.zeros(4, dtype=np.int64)
     _native.check(f._lib.ebc_screen_info(f.native_context, out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))),
                   f.native_context)
