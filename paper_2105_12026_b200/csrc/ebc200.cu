@@ -86,6 +86,7 @@ struct ebc_ctx {
   float* rho = nullptr;             // na x tc_ntl: min |v - mu_a| over the point tile
   float* cmx = nullptr;             // tc_ntl: max cm over the point tile (refreshed every screen)
   float* cmx0 = nullptr;            // tc_ntl: the same at the reset state (cm = d(., e0))
+  bool cmx_fresh = false;           // cmx refreshed by the current step's screen (enqueue-time flag)
   int kpad = 0;
   int tc_np = 0;  // points per tensor tile (0: tensor screen unavailable)
   float tc_kp = 0.f, tc_kc = 0.f, tc_kx = 0.f;  // anchored bound coefficients
@@ -267,11 +268,27 @@ int launch_screen(ebc_ctx* ctx, const ScreenPlan& p, const int* level_now, int l
   return launch_screen_t<ScreenA, MODE>(ctx, p, level_now, level, Vc, fo, ptv);
 }
 
+// The refine may skip certified-unreachable chunks when the tensor screen's
+// anchors exist and cmx was refreshed for this step (run_screen_window).
+bool refine_prune_on(const ebc_ctx* ctx) {
+  return ctx->tc_np && ctx->tc_prune && ctx->screen_mode == 3 && ctx->dtype != EBC_F64 && (RCH % ctx->tc_np) == 0;
+}
+
 template <typename T, bool BIGD>
 int launch_refine(ebc_ctx* ctx, const T* V, int grid, size_t smem, int ng) {
   CU(cudaFuncSetAttribute(k_refine<T, BIGD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024));
+  RefinePrune pr;
+  if (refine_prune_on(ctx) && ctx->cmx_fresh) {
+    pr.rho = ctx->rho;
+    pr.kpstride = ctx->tc_ntl;
+    pr.cmx = ctx->cmx;
+    pr.tile_anchor = ctx->tile_anchor;
+    pr.anchors = ctx->anchors;
+    pr.apitch = ctx->pitch;
+    pr.np = ctx->tc_np;
+  }
   k_refine<T, BIGD><<<grid, RED_THREADS, smem, ctx->stream>>>(V, ctx->pitch, ctx->n, ctx->d, ctx->cm64, ctx->wcount,
-                                                             ctx->wlist, ctx->nchunks, ng, (double*)ctx->part_r.p);
+                                                             ctx->wlist, ctx->nchunks, ng, (double*)ctx->part_r.p, pr);
   KCHECK();
   return EBC_OK;
 }
@@ -421,6 +438,7 @@ int launch_tc(ebc_ctx* ctx, const TcPlan& p, const int* level_now, int level) {
 // |v|^2 + |c|^2, the direct one with cm, so clustered data walks down the ladder.
 // Returns EBC_EINVAL (nothing launched) when no screen tile fits this d.
 int run_screen_window(ebc_ctx* ctx, int eb, int fin_blocks) {
+  ctx->cmx_fresh = false;
   ScreenPlan p;
   int rc = plan_screen(ctx, p);
   if (rc) return rc;
@@ -444,11 +462,12 @@ int run_screen_window(ebc_ctx* ctx, int eb, int fin_blocks) {
     if (!rc) rc = run_finalize_window(ctx, p.nsplit, nterms_ffma, p.tp, fin_blocks, 2.0, nullptr, 0);
   } else {
     if (use_tc) {
-      if (tp.list_cap) {
+      if (tp.list_cap || refine_prune_on(ctx)) {
         k_tile_cmmax<<<(unsigned)((ctx->tc_ntl * 32 + 255) / 256), 256, 0, ctx->stream>>>(ctx->cm64, ctx->n,
                                                                                           ctx->tc_ntl, ctx->tc_np,
                                                                                           ctx->cmx);
         KCHECK();
+        ctx->cmx_fresh = true;  // this step's refine may prune with it
       }
       rc = launch_tc(ctx, tp, ctx->level, 0);
       if (!rc) rc = run_finalize_window(ctx, tp.nsplit, (double)tp.tps * ctx->tc_np, 32, fin_blocks, 2.0,
@@ -479,6 +498,7 @@ int run_step_select(ebc_ctx* ctx, int step, int commit, int64_t* sel_dev) {
   const int64_t ncand = ctx->c1 - ctx->c0;
   CU(cudaMemsetAsync(ctx->wcount, 0, sizeof(int), ctx->stream));
   const int fin_blocks = (int)((ncand + 255) / 256);
+  ctx->cmx_fresh = false;
   int rc = ctx->dtype == EBC_F64 ? EBC_EINVAL : run_screen_window(ctx, eb, fin_blocks);
   if (rc == EBC_EINVAL) rc = run_window_all(ctx, eb, fin_blocks);
   if (rc) return rc;

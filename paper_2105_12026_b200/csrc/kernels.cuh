@@ -622,16 +622,44 @@ __global__ void k_window_all(int64_t c0, int64_t c1, const unsigned char* __rest
 // part_r[w*ng + grp].  A candidate's value never depends on its RW neighbours,
 // its slot in the window, or the number of ranks.
 constexpr int RW = 8;
+
+// Certified tile-pair pruning: every point of tile t is at least rho - R from
+// every candidate of the block (triangle inequality through the anchor), so
+// when (rho - R)^2 > max cm over the tile no pair can contribute or count.
+// Explicit roundings (no contraction) so every role of a CTA agrees bit for bit.
+__device__ __forceinline__ bool tile_prunable(float rho, float rad, float cmx) {
+  const float gap = __fsub_rn(rho, rad);
+  return gap > 0.f && __fmul_rn(__fmul_rn(gap, gap), 0.99999f) > cmx;
+}
+
+// Exact chunk skipping for the refine (tensor-screen anchors, screen_tc.cuh):
+// a chunk whose every point tile is certified out of reach of candidate c
+// ((rho_a[tile] - |c - mu_a|)^2 > max cm over the tile, same test as the
+// screen's tile-pair pruning) has every term max(0, cm - d) exactly 0, so
+// skipping it leaves the fixed-order fp64 sums bit for bit unchanged.
+struct RefinePrune {
+  const float* rho = nullptr;  // na x kpstride (nullptr: off)
+  int64_t kpstride = 0;
+  const float* cmx = nullptr;  // per point tile, current step
+  const int* tile_anchor = nullptr;
+  const float* anchors = nullptr;
+  int apitch = 0;
+  int np = 128;                // points per tile
+};
+
 template <typename T, bool BIGD>
 __global__ void __launch_bounds__(RED_THREADS) k_refine(const T* __restrict__ V, int pitch, int64_t n, int d,
                                                         const double* __restrict__ cm64,
                                                         const int* __restrict__ wcount,
                                                         const int64_t* __restrict__ wlist, int nchunks, int ng,
-                                                        double* __restrict__ part_r) {
+                                                        double* __restrict__ part_r, RefinePrune pr) {
   extern __shared__ double cd[];  // RW * d doubles (BIGD: candidates read through L1 instead)
   __shared__ double red[RW][RED_THREADS];
   __shared__ int64_t cidx[RW];
   __shared__ double tot[RW];
+  __shared__ float crad[RW];   // |c - mu_anchor| rounded up (pruning)
+  __shared__ int canc[RW];
+  __shared__ int live[RW];     // candidate j has a reachable tile in this chunk
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int cpg = (nchunks + ng - 1) / ng;
   const int wc = *wcount;
@@ -651,16 +679,45 @@ __global__ void __launch_bounds__(RED_THREADS) k_refine(const T* __restrict__ V,
     if (tid < RW) {
       tot[tid] = 0.0;
       cidx[tid] = tid < nw ? wlist[wg * RW + tid] : wlist[wg * RW];
+      if (pr.rho) {
+        const int64_t c = cidx[tid];
+        const int a = pr.tile_anchor[c >> 7];
+        const float* mu = pr.anchors + (int64_t)a * pr.apitch;
+        double r2 = 0.0;
+        for (int k = 0; k < d; ++k) {
+          const double x = (double)V[c * pitch + k] - (double)mu[k];
+          r2 = fma(x, x, r2);
+        }
+        canc[tid] = a;
+        crad[tid] = __double2float_ru(sqrt(r2) * (1.0 + 1e-12));
+      }
     }
     __syncthreads();
     const int ch1 = min(nchunks, (grp + 1) * cpg);
     for (int ch = grp * cpg; ch < ch1; ++ch) {
+      if (tid < RW) {
+        int lv = tid < nw;
+        if (lv && pr.rho) {
+          lv = 0;
+          const int tpc = RCH / pr.np;
+          const float* rho = pr.rho + (int64_t)canc[tid] * pr.kpstride;
+          for (int q = 0; q < tpc; ++q) {
+            const int64_t t = (int64_t)ch * tpc + q;
+            if (t * pr.np < n && !tile_prunable(rho[t], crad[tid], pr.cmx[t])) lv = 1;
+          }
+        }
+        live[tid] = lv;
+      }
+      __syncthreads();
+      bool any = false;
+#pragma unroll
+      for (int j = 0; j < RW; ++j) any |= live[j] != 0;
       double acc[RW];
 #pragma unroll
       for (int j = 0; j < RW; ++j) acc[j] = 0.0;
       for (int i = 0; i < RCH / RED_THREADS; ++i) {
         const int64_t v = (int64_t)ch * RCH + tid + (int64_t)i * RED_THREADS;
-        if (v < n) {
+        if (v < n && any) {
           double s[RW];
 #pragma unroll
           for (int j = 0; j < RW; ++j) s[j] = 0.0;
@@ -669,7 +726,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_refine(const T* __restrict__ V,
             const double x = (double)row[k];
 #pragma unroll
             for (int j = 0; j < RW; ++j) {
-              if (j < nw) {  // block-uniform: a short window does not pay for RW
+              if (live[j]) {  // block-uniform: a short window / unreachable chunk does not pay
                 const double cv = BIGD ? (double)__ldg(V + cidx[j] * pitch + k) : cd[j * d + k];
                 const double t = x - cv;
                 s[j] = fma(t, t, s[j]);
@@ -680,7 +737,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_refine(const T* __restrict__ V,
 #pragma unroll
           for (int j = 0; j < RW; ++j) {
             const double t = c - s[j];
-            acc[j] += t > 0.0 ? t : 0.0;
+            if (live[j]) acc[j] += t > 0.0 ? t : 0.0;
           }
         }
       }

@@ -474,14 +474,7 @@ __global__ void k_tile_cmmax(const double* __restrict__ cm64, int64_t n, int64_t
   if (lane == 0) cmx[t] = __double2float_ru(m);
 }
 
-// Certified tile-pair pruning: every point of tile t is at least rho - R from
-// every candidate of the block (triangle inequality through the anchor), so
-// when (rho - R)^2 > max cm over the tile no pair can contribute or count.
-// Explicit roundings (no contraction) so every role of the CTA agrees bit for bit.
-__device__ __forceinline__ bool tile_prunable(float rho, float rad, float cmx) {
-  const float gap = __fsub_rn(rho, rad);
-  return gap > 0.f && __fmul_rn(__fmul_rn(gap, gap), 0.99999f) > cmx;
-}
+// tile_prunable (kernels.cuh): the certified tile-pair test shared with k_refine.
 
 // Anchor data of the tensor screen (kernel argument).
 struct TcAnchors {

@@ -344,3 +344,18 @@ def test_clustered_surrogate_on_anchored_tensor_rung(monkeypatch, prune, regimes
     np.testing.assert_allclose(np.cumsum(s.gains), vals, rtol=1e-10)
     if regimes == 5:
         assert optimize.last_stats(f)[2] == 0
+
+
+def test_pruning_is_bit_identical(monkeypatch):
+    """Tile-pair pruning in the screen and chunk skipping in the exact refine
+    only drop terms certified to be exactly 0: the Greedy record is bit-identical
+    with pruning on and off (and the single-candidate values agree too)."""
+    import datasets
+    X = datasets.surrogate(30000, 32, 5, 0.01, 1).astype(np.float32)
+    out = {}
+    for prune in ("1", "0"):
+        monkeypatch.setenv("EBC200_TC_PRUNE", prune)
+        f = fn(X, eb.Precision.FP32)
+        s = eb.greedy_maximize(f, eb.OptimizerBudget(k=12))
+        out[prune] = (s.selected, s.gains, s.value)
+    assert out["1"] == out["0"]
