@@ -109,6 +109,34 @@ int ebc_shard_advance(ebc_ctx* ctx, int64_t commit_idx, int32_t run_step, int64_
 /* Copy the first `count` entries of the current local window to the host. */
 int ebc_shard_fetch(const ebc_ctx* ctx, int64_t* out_idx, double* out_gain, int64_t count);
 
+/* ---- device-side sharded Greedy: the exchange runs on the GPU (NCCL over
+ * NVLink/NVSwitch), no host round trip per step ----
+ * Replaces the per-step host loop of greedy_maximize (optimize.py:75-88) across
+ * ranks.  Per step every rank screens its candidate range, computes the exact
+ * gains of its certified window, and contributes its local tie set
+ * {c : value_c >= top_r - 1e-12 max(1,|top_r|)} as fixed-size records
+ * (TIE_CAP entries); one ncclAllGather of the records, then every rank applies
+ * the reference rule (optimize.py:83-85) to the identical union and folds the
+ * winner into its cached minima.  The k-step loop is graph-captured like
+ * ebc_greedy.  NCCL is dlopen'ed (libnccl.so.2) on first use.
+ *   ebc_comm_id_bytes / ebc_comm_unique_id -> rank 0 makes the id, the caller
+ *     broadcasts it (e.g. torch.distributed), every rank calls ebc_comm_init;
+ *   ebc_shard_set_range sets the rank's candidate range first;
+ *   ebc_greedy_sharded -> same outputs as ebc_greedy, identical on every rank;
+ *     EBC_ECOMM if a tie set overflowed (caller falls back to ebc_shard_advance). */
+int64_t ebc_comm_id_bytes(void);
+int ebc_comm_unique_id(unsigned char* out_id, int64_t bytes);
+int ebc_comm_init(ebc_ctx* ctx, const unsigned char* id, int64_t bytes, int32_t nranks, int32_t rank);
+int ebc_greedy_sharded(ebc_ctx* ctx, int32_t k, int64_t* out_sel, double* out_val, double* out_gain,
+                       int64_t* out_evals);
+/* Host-fed form of the same step (tests / emulated ranks on one GPU): the local
+ * tie-set records ((TIE_CAP + 1) x {index, gain}, record 0 = {count, 0}) and
+ * the global pick + commit from `world` gathered record blocks. */
+int32_t ebc_tie_cap(void);
+int ebc_shard_tie_step(ebc_ctx* ctx, double* out_rec, double* out_current);
+int ebc_shard_pick_commit(ebc_ctx* ctx, const double* gathered, int32_t world, int32_t step, int64_t* out_best,
+                          double* out_value);
+
 /* Reset the selection state to S = {} (cached minima back to d(., e0)). */
 int ebc_reset(ebc_ctx* ctx);
 

@@ -47,6 +47,13 @@ SIGNATURES = {
     "ebc_last_launches": (_i64, [_vp]),
     "ebc_last_stats": (ctypes.c_int, [_vp, _i64p]),
     "ebc_last_screen_work": (ctypes.c_int, [_vp, _i64p]),
+    "ebc_comm_id_bytes": (ctypes.c_int64, []),
+    "ebc_comm_unique_id": (ctypes.c_int, [ctypes.c_char_p, _i64]),
+    "ebc_comm_init": (ctypes.c_int, [_vp, ctypes.c_char_p, _i64, _i32, _i32]),
+    "ebc_greedy_sharded": (ctypes.c_int, [_vp, _i32, _i64p, _f64p, _f64p, _i64p]),
+    "ebc_tie_cap": (ctypes.c_int32, []),
+    "ebc_shard_tie_step": (ctypes.c_int, [_vp, _f64p, _f64p]),
+    "ebc_shard_pick_commit": (ctypes.c_int, [_vp, _f64p, _i32, _i32, _i64p, _f64p]),
     "ebc_screen_info": (ctypes.c_int, [_vp, _i64p]),
     "ebc_destroy": (None, [_vp]),
     "ebc_last_error": (ctypes.c_char_p, [_vp]),
@@ -89,7 +96,13 @@ def check(rc: int, ctx=None) -> None:
         raise ValueError(msg)
     if rc == EBC_EINDEX:
         raise IndexError(msg)
+    if rc == EBC_ECOMM:
+        raise CommError(msg or "sharded exchange failure")
     raise RuntimeError(msg or f"ebc200 status {rc}")
+
+
+class CommError(RuntimeError):
+    """EBC_ECOMM: the device-side sharded exchange failed or cannot be used."""
 
 
 def device_count() -> int:

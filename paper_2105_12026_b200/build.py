@@ -36,7 +36,7 @@ def build_native(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xptxas", "-v", "-shared", "-Xcompiler", "-fPIC",
-           "-o", LIB, *[os.path.join(CSRC, s) for s in SOURCES]]
+           "-o", LIB, *[os.path.join(CSRC, s) for s in SOURCES], "-ldl"]
     if os.path.exists(LIB):
         os.remove(LIB)  # a failed build must not leave a stale library behind
     proc = subprocess.run(cmd, capture_output=True, text=True)

@@ -7,6 +7,8 @@
 // with the host between steps.
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -29,6 +31,36 @@ using namespace ebc;
 namespace {
 
 thread_local std::string g_err;
+
+// NCCL is loaded on demand (dlopen) so the library itself depends only on the
+// CUDA runtime; in a torch process this resolves to the NCCL torch loaded.
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl_api() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+      api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+      api.AllGather = (decltype(api.AllGather))dlsym(h, "ncclAllGather");
+      api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+      api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+      api.ok = api.GetUniqueId && api.CommInitRank && api.AllGather && api.CommDestroy && api.GetErrorString;
+    }
+  }
+  return api;
+}
 
 struct DevBuf {
   void* p = nullptr;
@@ -111,12 +143,17 @@ struct ebc_ctx {
 
   // CUDA graphs of whole Greedy runs, keyed by k (rebuilt when buffers move)
   struct Graph {
-    int k;
+    int k;  // (k << 1) | sharded
     int64_t epoch;
     int64_t launches;
     cudaGraphExec_t exec;
   };
   std::vector<Graph> graphs;
+  // device-side sharded exchange (NCCL over NVLink, ebc_comm_init)
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+  DevBuf tie_rec, tie_all;
+  int* tie_err = nullptr;
   std::vector<int> eager_ks;  // k values run eagerly once (captured on the next run)
   int64_t alloc_epoch = 0;
   bool use_graphs = true;
@@ -571,6 +608,41 @@ int run_step_select(ebc_ctx* ctx, int step, int commit, int64_t* sel_dev);
 int run_update(ebc_ctx* ctx, int step, double* val_dev, double* gain_dev);
 
 // Reset + the k steps of a Greedy run, all on ctx->stream (no host sync).
+// One sharded Greedy step entirely on the device: local screen + window +
+// exact refine of this rank's candidates, its tie-set records, an NCCL
+// all-gather of the fixed-size records, the identical global pick on every
+// rank, and the cached-min update -- no host round trip (graph-capturable).
+int enqueue_sharded_step(ebc_ctx* ctx, int s, const double2* gathered_host_fed) {
+  if (ctx->c1 > ctx->c0) {
+    int rc = run_step_select(ctx, s, 0, nullptr);
+    if (rc) return rc;
+  } else {
+    CU(cudaMemsetAsync(ctx->wcount, 0, sizeof(int), ctx->stream));
+  }
+  k_tie_records<<<1, 1024, 0, ctx->stream>>>(ctx->wcount, ctx->wlist, ctx->wgain, 1.0 / (double)ctx->n, ctx->cur,
+                                             (double2*)ctx->tie_rec.p);
+  KCHECK();
+  if (!gathered_host_fed) {
+    const NcclApi& api = nccl_api();
+    const ncclResult_t r = api.AllGather(ctx->tie_rec.p, ctx->tie_all.p, (size_t)(TIE_CAP + 1) * 2, ncclFloat64,
+                                         ctx->comm, ctx->stream);
+    if (r != ncclSuccess) return fail(ctx, EBC_ECOMM, std::string("ncclAllGather: ") + api.GetErrorString(r));
+  }
+  k_pick_global<<<1, 1024, 0, ctx->stream>>>((const double2*)ctx->tie_all.p, ctx->nranks, 1.0 / (double)ctx->n,
+                                             ctx->cur, ctx->best, ctx->selected, (int64_t*)ctx->sel_out.p, s,
+                                             ctx->tie_err);
+  KCHECK();
+  return run_update(ctx, s, (double*)ctx->val_out.p, (double*)ctx->gain_out.p);
+}
+
+int enqueue_greedy_sharded(ebc_ctx* ctx, int k) {
+  int rc = do_reset(ctx);
+  if (rc) return rc;
+  CU(cudaMemsetAsync(ctx->tie_err, 0, sizeof(int), ctx->stream));
+  for (int s = 0; s < k && !rc; ++s) rc = enqueue_sharded_step(ctx, s, nullptr);
+  return rc;
+}
+
 int enqueue_greedy(ebc_ctx* ctx, int k) {
   int rc = do_reset(ctx);
   if (rc) return rc;
@@ -607,7 +679,7 @@ void free_ctx(ebc_ctx* c) {
                   c->maxlb, c->wcount, c->wlist, c->wgain, c->ub};
   for (void* p : ptrs)
     if (p) cudaFree(p);
-  DevBuf* bufs[] = {&c->ms_tanchor, &c->ms_trad, &c->part_g, &c->part_e, &c->part_r, &c->sel_out, &c->val_out, &c->gain_out, &c->ms_part,
+  DevBuf* bufs[] = {&c->tie_rec, &c->tie_all, &c->ms_tanchor, &c->ms_trad, &c->part_g, &c->part_e, &c->part_r, &c->sel_out, &c->val_out, &c->gain_out, &c->ms_part,
                     &c->ms_off, &c->ms_idx, &c->ms_out, &c->ms_mbuf, &c->ms_setof, &c->ms_pairs, &c->ms_keys,
                     &c->ms_vals, &c->ms_keys2, &c->ms_vals2, &c->ms_ukeys, &c->ms_uvals, &c->ms_cub};
   void* more[] = {c->pt0, c->ms_count, c->ms_nruns};
@@ -617,6 +689,8 @@ void free_ctx(ebc_ctx* c) {
     if (b->p) cudaFree(b->p);
   for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
   for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+  if (c->comm) nccl_api().CommDestroy(c->comm);
+  if (c->tie_err) cudaFree(c->tie_err);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -1055,7 +1129,14 @@ int ebc_last_stats(const ebc_ctx* ctx, int64_t* out4) {
   return EBC_OK;
 }
 
-int ebc_greedy(ebc_ctx* ctx, int32_t k, int64_t* out_sel, double* out_val, double* out_gain, int64_t* out_evals) {
+}  // extern "C"
+
+namespace {
+
+// Shared driver of ebc_greedy (single device, full candidate range) and
+// ebc_greedy_sharded (this rank's range, device-side NCCL exchange).
+int greedy_run(ebc_ctx* ctx, int32_t k, bool sharded, int64_t* out_sel, double* out_val, double* out_gain,
+               int64_t* out_evals) {
   if (!ctx) return fail(nullptr, EBC_EINVAL, "ebc_greedy: NULL context");
   if (k < 1) return fail(ctx, EBC_EINVAL, "k must be >= 1");
   if (k > ctx->n)
@@ -1063,8 +1144,15 @@ int ebc_greedy(ebc_ctx* ctx, int32_t k, int64_t* out_sel, double* out_val, doubl
   if (!out_sel || !out_val || !out_gain) return fail(ctx, EBC_EINVAL, "ebc_greedy: NULL output buffer");
   CU(cudaSetDevice(ctx->device));
   ctx->launches = 0;
-  ctx->c0 = 0;
-  ctx->c1 = ctx->n;
+  if (!sharded) {
+    ctx->c0 = 0;
+    ctx->c1 = ctx->n;
+  } else {
+    if (!ctx->comm) return fail(ctx, EBC_EINVAL, "ebc_greedy_sharded: no communicator (call ebc_comm_init)");
+    int rc0 = ensure(ctx, ctx->tie_rec, (size_t)(TIE_CAP + 1) * sizeof(double2));
+    if (!rc0) rc0 = ensure(ctx, ctx->tie_all, (size_t)ctx->nranks * (TIE_CAP + 1) * sizeof(double2));
+    if (rc0) return rc0;
+  }
   int rc = ensure(ctx, ctx->sel_out, (size_t)k * sizeof(int64_t));
   if (!rc) rc = ensure(ctx, ctx->val_out, (size_t)k * sizeof(double));
   if (!rc) rc = ensure(ctx, ctx->gain_out, (size_t)k * sizeof(double));
@@ -1084,10 +1172,12 @@ int ebc_greedy(ebc_ctx* ctx, int32_t k, int64_t* out_sel, double* out_val, doubl
   // run stays eager, so a context used once (the e2e path) never pays for
   // capture + instantiation.
   const bool graph_ok = ctx->use_graphs && !ctx->timing;
+  const int key = (k << 1) | (sharded ? 1 : 0);
+  auto enqueue = [&]() { return sharded ? enqueue_greedy_sharded(ctx, k) : enqueue_greedy(ctx, k); };
   ebc_ctx::Graph* cached = nullptr;
   for (auto& g : ctx->graphs)
-    if (g.k == k && g.epoch == ctx->alloc_epoch) cached = &g;
-  const bool seen = std::find(ctx->eager_ks.begin(), ctx->eager_ks.end(), k) != ctx->eager_ks.end();
+    if (g.k == key && g.epoch == ctx->alloc_epoch) cached = &g;
+  const bool seen = std::find(ctx->eager_ks.begin(), ctx->eager_ks.end(), key) != ctx->eager_ks.end();
   if (graph_ok && !cached && seen) {
     const int64_t before = ctx->launches;
     cudaGraph_t graph = nullptr;
@@ -1095,7 +1185,7 @@ int ebc_greedy(ebc_ctx* ctx, int32_t k, int64_t* out_sel, double* out_val, doubl
     bool ok = cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
     const int64_t epoch = ctx->alloc_epoch;
     if (ok) {
-      const int crc = enqueue_greedy(ctx, k);
+      const int crc = enqueue();
       ok = cudaStreamEndCapture(ctx->stream, &graph) == cudaSuccess && crc == EBC_OK && epoch == ctx->alloc_epoch;
     }
     if (ok) ok = cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess;
@@ -1103,13 +1193,13 @@ int ebc_greedy(ebc_ctx* ctx, int32_t k, int64_t* out_sel, double* out_val, doubl
     cudaGetLastError();  // a failed capture only disables graphs
     if (ok) {
       for (auto it = ctx->graphs.begin(); it != ctx->graphs.end();)
-        if (it->k == k) {
+        if (it->k == key) {
           cudaGraphExecDestroy(it->exec);
           it = ctx->graphs.erase(it);
         } else {
           ++it;
         }
-      ctx->graphs.push_back({k, epoch, ctx->launches - before, exec});
+      ctx->graphs.push_back({key, epoch, ctx->launches - before, exec});
       cached = &ctx->graphs.back();
     } else {
       ctx->use_graphs = false;
@@ -1120,15 +1210,20 @@ int ebc_greedy(ebc_ctx* ctx, int32_t k, int64_t* out_sel, double* out_val, doubl
     CU(cudaGraphLaunch(cached->exec, ctx->stream));
     ctx->launches = cached->launches;
   } else {
-    rc = enqueue_greedy(ctx, k);
+    rc = enqueue();
     if (rc) return rc;
-    if (!seen) ctx->eager_ks.push_back(k);
+    if (!seen) ctx->eager_ks.push_back(key);
   }
   CU(cudaEventRecord(tend, ctx->stream));
   CU(cudaMemcpyAsync(out_sel, ctx->sel_out.p, (size_t)k * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaMemcpyAsync(out_val, ctx->val_out.p, (size_t)k * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaMemcpyAsync(out_gain, ctx->gain_out.p, (size_t)k * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  int tie_err = 0;
+  if (sharded) CU(cudaMemcpyAsync(&tie_err, ctx->tie_err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
+  if (tie_err)
+    return fail(ctx, EBC_ECOMM, "sharded Greedy: a rank's tie set exceeded " + std::to_string(TIE_CAP) +
+                                    " records (use the host exchange)");
   if (ctx->timing) {
     for (int st = 0; st < k; ++st) {
       float a = 0, b = 0, c = 0;
@@ -1154,6 +1249,108 @@ int ebc_greedy(ebc_ctx* ctx, int32_t k, int64_t* out_sel, double* out_val, doubl
   }
   for (int s = 0; s < k; ++s)
     if (out_sel[s] < 0) return fail(ctx, EBC_ECUDA, "greedy step " + std::to_string(s) + " found no candidate");
+  return EBC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ebc_greedy(ebc_ctx* ctx, int32_t k, int64_t* out_sel, double* out_val, double* out_gain, int64_t* out_evals) {
+  return greedy_run(ctx, k, false, out_sel, out_val, out_gain, out_evals);
+}
+
+int ebc_comm_unique_id(unsigned char* out_id, int64_t bytes) {
+  if (!out_id || bytes < (int64_t)sizeof(ncclUniqueId)) return fail(nullptr, EBC_EINVAL, "ebc_comm_unique_id: buffer too small");
+  const NcclApi& api = nccl_api();
+  if (!api.ok) return fail(nullptr, EBC_ECOMM, "NCCL (libnccl.so.2) not available");
+  ncclUniqueId id;
+  const ncclResult_t r = api.GetUniqueId(&id);
+  if (r != ncclSuccess) return fail(nullptr, EBC_ECOMM, std::string("ncclGetUniqueId: ") + api.GetErrorString(r));
+  std::memcpy(out_id, &id, sizeof(id));
+  return EBC_OK;
+}
+
+int64_t ebc_comm_id_bytes(void) { return (int64_t)sizeof(ncclUniqueId); }
+
+int ebc_comm_init(ebc_ctx* ctx, const unsigned char* id, int64_t bytes, int32_t nranks, int32_t rank) {
+  if (!ctx || !id || bytes < (int64_t)sizeof(ncclUniqueId)) return fail(ctx, EBC_EINVAL, "ebc_comm_init: bad argument");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(ctx, EBC_EINVAL, "ebc_comm_init: bad rank / world size");
+  const NcclApi& api = nccl_api();
+  if (!api.ok) return fail(ctx, EBC_ECOMM, "NCCL (libnccl.so.2) not available");
+  CU(cudaSetDevice(ctx->device));
+  if (ctx->comm) {
+    api.CommDestroy(ctx->comm);
+    ctx->comm = nullptr;
+  }
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, sizeof(uid));
+  const ncclResult_t r = api.CommInitRank(&ctx->comm, nranks, uid, rank);
+  if (r != ncclSuccess) {
+    ctx->comm = nullptr;
+    return fail(ctx, EBC_ECOMM, std::string("ncclCommInitRank: ") + api.GetErrorString(r));
+  }
+  ctx->nranks = nranks;
+  ctx->rank = rank;
+  if (!ctx->tie_err) CU(cudaMalloc(&ctx->tie_err, sizeof(int)));
+  ++ctx->alloc_epoch;  // graphs captured with another communicator are stale
+  return EBC_OK;
+}
+
+int ebc_greedy_sharded(ebc_ctx* ctx, int32_t k, int64_t* out_sel, double* out_val, double* out_gain,
+                       int64_t* out_evals) {
+  return greedy_run(ctx, k, true, out_sel, out_val, out_gain, out_evals);
+}
+
+int32_t ebc_tie_cap(void) { return TIE_CAP; }
+
+int ebc_shard_tie_step(ebc_ctx* ctx, double* out_rec, double* out_current) {
+  if (!ctx || !out_rec || !out_current) return fail(ctx, EBC_EINVAL, "ebc_shard_tie_step: NULL argument");
+  CU(cudaSetDevice(ctx->device));
+  int rc = ensure(ctx, ctx->tie_rec, (size_t)(TIE_CAP + 1) * sizeof(double2));
+  if (rc) return rc;
+  if (ctx->c1 > ctx->c0) {
+    rc = run_step_select(ctx, 0, 0, nullptr);
+    if (rc) return rc;
+  } else {
+    CU(cudaMemsetAsync(ctx->wcount, 0, sizeof(int), ctx->stream));
+  }
+  k_tie_records<<<1, 1024, 0, ctx->stream>>>(ctx->wcount, ctx->wlist, ctx->wgain, 1.0 / (double)ctx->n, ctx->cur,
+                                             (double2*)ctx->tie_rec.p);
+  KCHECK();
+  CU(cudaMemcpyAsync(out_rec, ctx->tie_rec.p, (size_t)(TIE_CAP + 1) * sizeof(double2), cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CU(cudaMemcpyAsync(out_current, ctx->cur, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return EBC_OK;
+}
+
+int ebc_shard_pick_commit(ebc_ctx* ctx, const double* gathered, int32_t world, int32_t step, int64_t* out_best,
+                          double* out_value) {
+  if (!ctx || !gathered || world < 1 || !out_best || !out_value)
+    return fail(ctx, EBC_EINVAL, "ebc_shard_pick_commit: bad argument");
+  CU(cudaSetDevice(ctx->device));
+  int rc = ensure(ctx, ctx->tie_all, (size_t)world * (TIE_CAP + 1) * sizeof(double2));
+  if (!rc) rc = ensure(ctx, ctx->sel_out, (size_t)(step + 1) * sizeof(int64_t));
+  if (!rc) rc = ensure(ctx, ctx->val_out, (size_t)(step + 1) * sizeof(double));
+  if (!rc) rc = ensure(ctx, ctx->gain_out, (size_t)(step + 1) * sizeof(double));
+  if (rc) return rc;
+  if (!ctx->tie_err) CU(cudaMalloc(&ctx->tie_err, sizeof(int)));
+  CU(cudaMemsetAsync(ctx->tie_err, 0, sizeof(int), ctx->stream));
+  CU(cudaMemcpyAsync(ctx->tie_all.p, gathered, (size_t)world * (TIE_CAP + 1) * sizeof(double2),
+                     cudaMemcpyHostToDevice, ctx->stream));
+  k_pick_global<<<1, 1024, 0, ctx->stream>>>((const double2*)ctx->tie_all.p, world, 1.0 / (double)ctx->n, ctx->cur,
+                                             ctx->best, ctx->selected, (int64_t*)ctx->sel_out.p, step, ctx->tie_err);
+  KCHECK();
+  rc = run_update(ctx, step, (double*)ctx->val_out.p, (double*)ctx->gain_out.p);
+  if (rc) return rc;
+  int err = 0;
+  CU(cudaMemcpyAsync(out_best, ctx->best, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaMemcpyAsync(out_value, ctx->cur, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaMemcpyAsync(&err, ctx->tie_err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  ctx->steps_done += 1;
+  if (err) return fail(ctx, EBC_ECOMM, "tie set exceeded " + std::to_string(TIE_CAP) + " records");
   return EBC_OK;
 }
 

@@ -816,6 +816,92 @@ __global__ void __launch_bounds__(1024) k_pick(const int* __restrict__ wcount, c
   }
 }
 
+// ---------------------------------------------------------------- sharded exchange
+// One rank's contribution to the global argmax: its local tie set
+// T_r = {w in window : value_w >= top_r - 1e-12 max(1, |top_r|)}.  The global
+// window threshold is >= every local one (top - window(top) is monotone in
+// top), so the union of the T_r holds every candidate the reference rule can
+// pick (optimize.py:83-85).  Records: rec[0] = {count, 0}, rec[1 + i] = {index,
+// exact gain}; order inside a rank does not matter (the pick takes the lowest
+// index).  count > TIE_CAP is reported, never truncated silently.
+constexpr int TIE_CAP = 1024;
+
+__global__ void __launch_bounds__(1024) k_tie_records(const int* __restrict__ wcount,
+                                                      const int64_t* __restrict__ wlist,
+                                                      const double* __restrict__ wgain, double inv_n,
+                                                      const double* __restrict__ cur, double2* __restrict__ rec) {
+  __shared__ double smax[1024];
+  __shared__ int fill;
+  const int wc = *wcount;
+  const double f = *cur;
+  double top = -INFINITY;
+  for (int w = threadIdx.x; w < wc; w += blockDim.x) top = fmax(top, __dadd_rn(f, __dmul_rn(wgain[w], inv_n)));
+  smax[threadIdx.x] = top;
+  if (threadIdx.x == 0) fill = 0;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) smax[threadIdx.x] = fmax(smax[threadIdx.x], smax[threadIdx.x + s]);
+    __syncthreads();
+  }
+  top = smax[0];
+  const double thr = top - 1e-12 * fmax(1.0, fabs(top));
+  for (int w = threadIdx.x; w < wc; w += blockDim.x) {
+    if (__dadd_rn(f, __dmul_rn(wgain[w], inv_n)) >= thr) {
+      const int slot = atomicAdd(&fill, 1);
+      if (slot < TIE_CAP) rec[1 + slot] = make_double2((double)wlist[w], wgain[w]);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) rec[0] = make_double2((double)fill, 0.0);
+}
+
+// Global pick over the all-gathered records of `world` ranks (identical input
+// on every rank -> identical winner): top value, reference tie window, lowest
+// index.  Marks the winner selected and records it as step `step`.
+__global__ void __launch_bounds__(1024) k_pick_global(const double2* __restrict__ all, int world, double inv_n,
+                                                      const double* __restrict__ cur, int64_t* __restrict__ best,
+                                                      unsigned char* __restrict__ selected,
+                                                      int64_t* __restrict__ sel_out, int step, int* __restrict__ err) {
+  __shared__ double smax[1024];
+  __shared__ long long smin[1024];
+  const double f = *cur;
+  double top = -INFINITY;
+  for (int r = 0; r < world; ++r) {
+    const double2* rr = all + (int64_t)r * (TIE_CAP + 1);
+    const int cnt = (int)rr[0].x;
+    if (cnt > TIE_CAP && threadIdx.x == 0) *err = 1;
+    for (int i = threadIdx.x; i < min(cnt, TIE_CAP); i += blockDim.x)
+      top = fmax(top, __dadd_rn(f, __dmul_rn(rr[1 + i].y, inv_n)));
+  }
+  smax[threadIdx.x] = top;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) smax[threadIdx.x] = fmax(smax[threadIdx.x], smax[threadIdx.x + s]);
+    __syncthreads();
+  }
+  top = smax[0];
+  const double thr = top - 1e-12 * fmax(1.0, fabs(top));
+  long long bi = LLONG_MAX;
+  for (int r = 0; r < world; ++r) {
+    const double2* rr = all + (int64_t)r * (TIE_CAP + 1);
+    const int cnt = min((int)rr[0].x, TIE_CAP);
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x)
+      if (__dadd_rn(f, __dmul_rn(rr[1 + i].y, inv_n)) >= thr) bi = min(bi, (long long)rr[1 + i].x);
+  }
+  smin[threadIdx.x] = bi;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) smin[threadIdx.x] = min(smin[threadIdx.x], smin[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const long long b = smin[0] == LLONG_MAX ? -1 : smin[0];
+    *best = b;
+    if (b >= 0) selected[b] = 1;
+    if (sel_out) sel_out[step] = b;
+  }
+}
+
 // ---------------------------------------------------------------- K4: cached-min update
 
 // cm64 = min(cm64, d64(., s)); pt = {-cm32, tau}; chunk partials of (e0d - cm64).

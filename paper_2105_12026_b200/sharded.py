@@ -14,6 +14,15 @@ Greedy step:
   4. ``engine.commit(best)`` -- every rank folds the winner into its cached
      minima and recomputes f(S) with the fixed-order fp64 reduction.
 
+Device exchange (the NCCL path, ``greedy_device_exchange``): the same step
+runs without a host round trip -- each rank reduces its window to its local
+tie set {c : value_c >= top_r - 1e-12 max(1,|top_r|)} (a superset of what the
+global rule can pick, since top - window(top) is monotone in top), writes it
+as fixed-size records, one ``ncclAllGather`` inside the step exchanges them,
+and every rank runs the identical device pick; the k-step loop is
+graph-captured (``ebc_greedy_sharded``).  Steps 1-4 above are the host-driven
+fallback (gloo, NCCL missing, or a tie set beyond ``ebc_tie_cap()``).
+
 Why the union of local windows gives the single-GPU answer: a local window
 W_r = {c in shard r : ub_c >= max_{c' in shard r} lb_c' - margin} contains
 every candidate of shard r whose exact value is within the reference tie
@@ -177,9 +186,66 @@ def greedy_sharded_loop(engine, n: int, k: int, group=None, device=None) -> Summ
                    runtime_seconds=time.perf_counter() - t0)
 
 
+def _ensure_device_comm(f, group) -> bool:
+    """NCCL communicator of the library for this EbcFunction (rank 0 makes the
+    unique id, torch.distributed broadcasts it).  False if NCCL is unavailable
+    on any rank -- then every rank uses the host exchange."""
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    key = (id(group), world, rank)
+    if getattr(f, "_comm_key", None) == key:
+        return True
+    lib = f._lib
+    nb = int(lib.ebc_comm_id_bytes())
+    payload = None
+    if rank == 0:
+        buf = ctypes.create_string_buffer(nb)
+        if lib.ebc_comm_unique_id(buf, nb) == _native.EBC_OK:
+            payload = buf.raw
+    obj = [payload]
+    src = dist.get_global_rank(group, 0) if group is not None else 0
+    dist.broadcast_object_list(obj, src=src, group=group)
+    if obj[0] is None:
+        return False
+    _native.check(lib.ebc_comm_init(f.native_context, obj[0], nb, world, rank), f.native_context)
+    f._comm_key = key
+    return True
+
+
+def greedy_device_exchange(f, k: int, c0: int, c1: int) -> Summary:
+    """k sharded Greedy steps with the exchange on the device (ebc_greedy_sharded):
+    one call, no host round trip per step."""
+    lib = f._lib
+    ctx = f.native_context
+    t0 = time.perf_counter()
+    _native.check(lib.ebc_shard_set_range(ctx, c0, c1), ctx)
+    sel = np.empty(k, dtype=np.int64)
+    val = np.empty(k, dtype=np.float64)
+    gain = np.empty(k, dtype=np.float64)
+    evals = ctypes.c_int64()
+    try:
+        _native.check(lib.ebc_greedy_sharded(ctx, k, sel.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                              val.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                              gain.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                              ctypes.byref(evals)), ctx)
+    finally:
+        lib.ebc_shard_set_range(ctx, 0, f.ground.n)
+    return Summary(selected=[int(x) for x in sel], value=float(val[-1]), gains=[float(x) for x in gain],
+                   evaluations=int(evals.value), runtime_seconds=time.perf_counter() - t0)
+
+
 def greedy_maximize_sharded(f, budget: OptimizerBudget, group=None) -> Summary:
     """Greedy over all ranks of `group` (torch.distributed must be initialised;
-    each rank passes its own EbcFunction built on its own GPU from the same data)."""
+    each rank passes its own EbcFunction built on its own GPU from the same data).
+
+    With an NCCL process group the whole k-step loop runs on the devices
+    (ebc_greedy_sharded: NCCL all-gather of fixed-size tie-set records inside
+    the step, graph-captured); otherwise -- gloo, NCCL unavailable,
+    EBC200_DEVICE_EXCHANGE=0, or a tie set larger than ebc_tie_cap() -- the
+    host drives the exchange one step at a time (greedy_sharded_loop)."""
+    import os
+
     import torch
     import torch.distributed as dist
 
@@ -188,8 +254,14 @@ def greedy_maximize_sharded(f, budget: OptimizerBudget, group=None) -> Summary:
         raise ValueError(f"k={budget.k} exceeds ground size {n}")
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     c0, c1 = shard_range(n, rank, world)
+    nccl = dist.get_backend(group) == "nccl"
+    if nccl and os.environ.get("EBC200_DEVICE_EXCHANGE", "1") != "0" and _ensure_device_comm(f, group):
+        try:
+            return greedy_device_exchange(f, int(budget.k), c0, c1)
+        except _native.CommError:
+            pass  # tie-set overflow on some rank (every rank sees the same records): host exchange below
     engine = NativeShardEngine(f, c0, c1)
-    device = f"cuda:{torch.cuda.current_device()}" if dist.get_backend(group) == "nccl" else None
+    device = f"cuda:{torch.cuda.current_device()}" if nccl else None
     try:
         return greedy_sharded_loop(engine, n, int(budget.k), group=group, device=device)
     finally:

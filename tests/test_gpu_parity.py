@@ -359,3 +359,76 @@ def test_pruning_is_bit_identical(monkeypatch):
         s = eb.greedy_maximize(f, eb.OptimizerBudget(k=12))
         out[prune] = (s.selected, s.gains, s.value)
     assert out["1"] == out["0"]
+
+
+# ------------------------------------------------------------ device-side sharded exchange
+
+def _c(arr, ct):
+    import ctypes
+    return arr.ctypes.data_as(ctypes.POINTER(ct))
+
+
+def test_device_exchange_single_rank_matches_greedy():
+    """ebc_greedy_sharded over a one-rank NCCL communicator (the plumbing a
+    multi-GPU run uses: tie-set records, ncclAllGather inside the step, device
+    pick, graph capture on the second run) reproduces ebc_greedy bit for bit."""
+    import ctypes
+    from paper_2105_12026_b200 import _native
+    from paper_2105_12026_b200.sharded import greedy_device_exchange
+    X = np.random.default_rng(17).standard_normal((6000, 40)).astype(np.float32)
+    X[5000] = X[12]  # an exact tie
+    single = eb.greedy_maximize(fn(X, eb.Precision.FP32), eb.OptimizerBudget(k=10))
+    f = fn(X, eb.Precision.FP32)
+    lib = f._lib
+    nb = int(lib.ebc_comm_id_bytes())
+    buf = ctypes.create_string_buffer(nb)
+    _native.check(lib.ebc_comm_unique_id(buf, nb))
+    _native.check(lib.ebc_comm_init(f.native_context, buf.raw, nb, 1, 0), f.native_context)
+    for _ in range(3):  # eager, captured, replayed
+        s = greedy_device_exchange(f, 10, 0, X.shape[0])
+        assert s.selected == single.selected
+        assert s.gains == single.gains and s.value == single.value
+        assert s.evaluations == single.evaluations
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_device_pick_emulated_ranks_bit_identical(world):
+    """The device exchange's kernels (local tie-set records, global pick) with
+    `world` emulated ranks on one GPU, records gathered on the host: the same
+    selection and values as the single-device run, on data with exact ties."""
+    import ctypes
+    from paper_2105_12026_b200 import _native
+    X = np.random.default_rng(23).standard_normal((3000, 24)).astype(np.float32)
+    X[2500] = X[7]
+    X[1999] = X[40]
+    k = 9
+    single = eb.greedy_maximize(fn(X, eb.Precision.FP32), eb.OptimizerBudget(k=k))
+    cap = int(_native.load().ebc_tie_cap())
+    fs = [fn(X, eb.Precision.FP32) for _ in range(world)]
+    for r, f in enumerate(fs):
+        _native.check(f._lib.ebc_shard_set_range(f.native_context, *shard_range(X.shape[0], r, world)))
+        _native.check(f._lib.ebc_reset(f.native_context))
+    sel, vals = [], []
+    for step in range(k):
+        recs = []
+        for f in fs:
+            rec = np.zeros((cap + 1) * 2, dtype=np.float64)
+            cur = ctypes.c_double()
+            _native.check(f._lib.ebc_shard_tie_step(f.native_context, _c(rec, ctypes.c_double), ctypes.byref(cur)),
+                          f.native_context)
+            assert rec[0] <= cap
+            recs.append(rec)
+        gathered = np.concatenate(recs)
+        out = []
+        for f in fs:
+            best = ctypes.c_int64()
+            val = ctypes.c_double()
+            _native.check(f._lib.ebc_shard_pick_commit(f.native_context, _c(gathered, ctypes.c_double), world, step,
+                                                       ctypes.byref(best), ctypes.byref(val)), f.native_context)
+            out.append((best.value, val.value))
+        assert len(set(out)) == 1
+        sel.append(out[0][0])
+        vals.append(out[0][1])
+    assert sel == single.selected
+    assert vals[-1] == single.value
+    assert [b - a for a, b in zip([0.0] + vals[:-1], vals)] == single.gains
