@@ -127,6 +127,9 @@ int ebc_shard_fetch(const ebc_ctx* ctx, int64_t* out_idx, double* out_gain, int6
 int64_t ebc_comm_id_bytes(void);
 int ebc_comm_unique_id(unsigned char* out_id, int64_t bytes);
 int ebc_comm_init(ebc_ctx* ctx, const unsigned char* id, int64_t bytes, int32_t nranks, int32_t rank);
+/* The communicator is per device and process; later contexts on the same device
+ * attach to it without another ncclCommInitRank (EBC_ECOMM if none exists). */
+int ebc_comm_attach(ebc_ctx* ctx);
 int ebc_greedy_sharded(ebc_ctx* ctx, int32_t k, int64_t* out_sel, double* out_val, double* out_gain,
                        int64_t* out_evals);
 /* Host-fed form of the same step (tests / emulated ranks on one GPU): the local

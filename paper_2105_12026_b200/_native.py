@@ -50,6 +50,7 @@ SIGNATURES = {
     "ebc_comm_id_bytes": (ctypes.c_int64, []),
     "ebc_comm_unique_id": (ctypes.c_int, [ctypes.c_char_p, _i64]),
     "ebc_comm_init": (ctypes.c_int, [_vp, ctypes.c_char_p, _i64, _i32, _i32]),
+    "ebc_comm_attach": (ctypes.c_int, [_vp]),
     "ebc_greedy_sharded": (ctypes.c_int, [_vp, _i32, _i64p, _f64p, _f64p, _i64p]),
     "ebc_tie_cap": (ctypes.c_int32, []),
     "ebc_shard_tie_step": (ctypes.c_int, [_vp, _f64p, _f64p]),

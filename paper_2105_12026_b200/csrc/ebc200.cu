@@ -43,6 +43,17 @@ struct NcclApi {
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 
+struct SharedComm {
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+  int64_t generation = 0;
+};
+
+SharedComm& shared_comm(int device) {
+  static SharedComm comms[64];
+  return comms[device & 63];
+}
+
 const NcclApi& nccl_api() {
   static NcclApi api;
   static bool tried = false;
@@ -150,7 +161,8 @@ struct ebc_ctx {
   };
   std::vector<Graph> graphs;
   // device-side sharded exchange (NCCL over NVLink, ebc_comm_init)
-  ncclComm_t comm = nullptr;
+  ncclComm_t comm = nullptr;  // the device's shared communicator (not owned)
+  int64_t comm_gen = -1;
   int nranks = 1, rank = 0;
   DevBuf tie_rec, tie_all;
   int* tie_err = nullptr;
@@ -689,7 +701,6 @@ void free_ctx(ebc_ctx* c) {
     if (b->p) cudaFree(b->p);
   for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
   for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
-  if (c->comm) nccl_api().CommDestroy(c->comm);
   if (c->tie_err) cudaFree(c->tie_err);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -1148,7 +1159,12 @@ int greedy_run(ebc_ctx* ctx, int32_t k, bool sharded, int64_t* out_sel, double* 
     ctx->c0 = 0;
     ctx->c1 = ctx->n;
   } else {
-    if (!ctx->comm) return fail(ctx, EBC_EINVAL, "ebc_greedy_sharded: no communicator (call ebc_comm_init)");
+    const SharedComm& sc = shared_comm(ctx->device);
+    if (!sc.comm) return fail(ctx, EBC_EINVAL, "ebc_greedy_sharded: no communicator (call ebc_comm_init)");
+    if (ctx->comm != sc.comm || ctx->comm_gen != sc.generation) {
+      const int arc = ebc_comm_attach(ctx);
+      if (arc) return arc;
+    }
     int rc0 = ensure(ctx, ctx->tie_rec, (size_t)(TIE_CAP + 1) * sizeof(double2));
     if (!rc0) rc0 = ensure(ctx, ctx->tie_all, (size_t)ctx->nranks * (TIE_CAP + 1) * sizeof(double2));
     if (rc0) return rc0;
@@ -1279,19 +1295,34 @@ int ebc_comm_init(ebc_ctx* ctx, const unsigned char* id, int64_t bytes, int32_t 
   const NcclApi& api = nccl_api();
   if (!api.ok) return fail(ctx, EBC_ECOMM, "NCCL (libnccl.so.2) not available");
   CU(cudaSetDevice(ctx->device));
-  if (ctx->comm) {
-    api.CommDestroy(ctx->comm);
-    ctx->comm = nullptr;
-  }
+  // one communicator per device and process, shared by every context on it
+  // (an EbcFunction per call must not pay ncclCommInitRank each time)
+  SharedComm& sc = shared_comm(ctx->device);
+  if (sc.comm) api.CommDestroy(sc.comm);  // contexts still holding it re-attach below / via ebc_comm_attach
+  sc.comm = nullptr;
   ncclUniqueId uid;
   std::memcpy(&uid, id, sizeof(uid));
-  const ncclResult_t r = api.CommInitRank(&ctx->comm, nranks, uid, rank);
+  const ncclResult_t r = api.CommInitRank(&sc.comm, nranks, uid, rank);
   if (r != ncclSuccess) {
+    sc.comm = nullptr;
     ctx->comm = nullptr;
     return fail(ctx, EBC_ECOMM, std::string("ncclCommInitRank: ") + api.GetErrorString(r));
   }
-  ctx->nranks = nranks;
-  ctx->rank = rank;
+  sc.nranks = nranks;
+  sc.rank = rank;
+  ++sc.generation;
+  return ebc_comm_attach(ctx);
+}
+
+int ebc_comm_attach(ebc_ctx* ctx) {
+  if (!ctx) return fail(nullptr, EBC_EINVAL, "ebc_comm_attach: NULL context");
+  const SharedComm& sc = shared_comm(ctx->device);
+  if (!sc.comm) return fail(ctx, EBC_ECOMM, "no communicator on this device (call ebc_comm_init)");
+  CU(cudaSetDevice(ctx->device));
+  ctx->comm = sc.comm;
+  ctx->comm_gen = sc.generation;
+  ctx->nranks = sc.nranks;
+  ctx->rank = sc.rank;
   if (!ctx->tie_err) CU(cudaMalloc(&ctx->tie_err, sizeof(int)));
   ++ctx->alloc_epoch;  // graphs captured with another communicator are stale
   return EBC_OK;

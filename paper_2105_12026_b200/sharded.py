@@ -193,10 +193,14 @@ def _ensure_device_comm(f, group) -> bool:
     import torch.distributed as dist
 
     rank, world = dist.get_rank(group), dist.get_world_size(group)
-    key = (id(group), world, rank)
+    key = (id(group), world, rank, f.device)
     if getattr(f, "_comm_key", None) == key:
         return True
     lib = f._lib
+    if _COMM_READY.get(key):  # the device's communicator exists: attach, no collective init
+        _native.check(lib.ebc_comm_attach(f.native_context), f.native_context)
+        f._comm_key = key
+        return True
     nb = int(lib.ebc_comm_id_bytes())
     payload = None
     if rank == 0:
@@ -209,8 +213,13 @@ def _ensure_device_comm(f, group) -> bool:
     if obj[0] is None:
         return False
     _native.check(lib.ebc_comm_init(f.native_context, obj[0], nb, world, rank), f.native_context)
+    _COMM_READY.clear()  # a new init replaces the device's communicator
+    _COMM_READY[key] = True
     f._comm_key = key
     return True
+
+
+_COMM_READY: dict = {}  # (group, world, rank, device) -> the library holds a communicator for it
 
 
 def greedy_device_exchange(f, k: int, c0: int, c1: int) -> Summary:

@@ -432,3 +432,16 @@ def test_device_pick_emulated_ranks_bit_identical(world):
     assert sel == single.selected
     assert vals[-1] == single.value
     assert [b - a for a, b in zip([0.0] + vals[:-1], vals)] == single.gains
+
+
+def test_sharded_api_over_one_rank_nccl_group():
+    """greedy_maximize_sharded under a real (one-rank) NCCL process group takes
+    the device-exchange path and matches greedy_maximize (subprocess: keeps the
+    process group out of this interpreter)."""
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, os.path.join(here, "nccl_one_rank.py")], capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "nccl one-rank ok" in r.stdout
