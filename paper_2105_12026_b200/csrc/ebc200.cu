@@ -136,6 +136,9 @@ struct ebc_ctx {
   unsigned char* selected = nullptr;
   double* chunkpart = nullptr;  // nchunks
   unsigned int* counter = nullptr;
+  unsigned int* counter2 = nullptr;  // k_gain_top's last-block ticket
+  int64_t* topc = nullptr;           // candidate with the largest screen bound (ub-only screens)
+  double* toppart = nullptr;         // nchunks: its exact gain's chunk partials
   double* cur = nullptr;
   int64_t* best = nullptr;
   long long* maxlb = nullptr;
@@ -358,14 +361,32 @@ int run_window_all(ebc_ctx* ctx, int eb, int fin_blocks) {
 // accumulators hold t/2).  nterms bounds the terms of one fp32 error
 // accumulator; gterms the fp32 terms summed before each fp64 fold.
 int run_finalize_window(ebc_ctx* ctx, int nsplit, double nterms, int gterms, int fin_blocks, double gscale,
-                        const int* level_now, int level) {
+                        const int* level_now, int level, bool ub_only = false) {
   const double u = 5.960464477539063e-08;
   const double einfl = 1.0 + 2.0 * (nterms + 64.0) * u + 1.0 / 64.0;
   const double gcoef = (gterms + 8) * u;
   k_finalize<<<fin_blocks, 256, 0, ctx->stream>>>(ctx->c0, ctx->c1, nsplit, (double*)ctx->part_g.p,
                                                  (float*)ctx->part_e.p, ctx->n_pad, einfl, gcoef, gscale,
-                                                 ctx->selected, ctx->ub, ctx->maxlb, level_now, level);
+                                                 ctx->selected, ctx->ub, ctx->maxlb, level_now, level, ub_only ? 1 : 0);
   KCHECK();
+  if (ub_only) {
+    // window threshold = exact gain of the candidate with the largest bound
+    k_argmax_ub<<<1, 1024, 0, ctx->stream>>>(ctx->c0, ctx->c1, ctx->ub, ctx->topc, level_now, level);
+    KCHECK();
+    const size_t smem = (size_t)ctx->d * sizeof(double);
+    if (ctx->dtype == EBC_F64) {
+      CU(cudaFuncSetAttribute(k_gain_top<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024));
+      k_gain_top<double><<<ctx->nchunks, RED_THREADS, smem, ctx->stream>>>(
+          ctx->V64, ctx->pitch, ctx->n, ctx->d, ctx->cm64, ctx->topc, ctx->toppart, ctx->counter2, ctx->maxlb,
+          level_now, level);
+    } else {
+      CU(cudaFuncSetAttribute(k_gain_top<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024));
+      k_gain_top<float><<<ctx->nchunks, RED_THREADS, smem, ctx->stream>>>(
+          ctx->V32, ctx->pitch, ctx->n, ctx->d, ctx->cm64, ctx->topc, ctx->toppart, ctx->counter2, ctx->maxlb,
+          level_now, level);
+    }
+    KCHECK();
+  }
   const double margin = (double)ctx->n * 1e-12 * std::max(1.0, std::fabs(ctx->baseline)) * 1.01;
   k_window<<<fin_blocks, 256, 0, ctx->stream>>>(ctx->c0, ctx->c1, ctx->ub, ctx->maxlb, margin, ctx->wcount,
                                                ctx->wlist, level_now, level);
@@ -520,7 +541,7 @@ int run_screen_window(ebc_ctx* ctx, int eb, int fin_blocks) {
       }
       rc = launch_tc(ctx, tp, ctx->level, 0);
       if (!rc) rc = run_finalize_window(ctx, tp.nsplit, (double)tp.tps * ctx->tc_np, 32, fin_blocks, 2.0,
-                                        ctx->level, 0);
+                                        ctx->level, 0, /*ub_only=*/true);
       if (!rc) {
         k_adapt<<<1, 32, 0, ctx->stream>>>(ctx->wcount, ctx->maxlb, ctx->wcap, ctx->level, 0);
         KCHECK();
@@ -687,7 +708,7 @@ int do_reset(ebc_ctx* ctx) {
 void free_ctx(ebc_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
-  void* ptrs[] = {c->V32, c->V64, c->e0d, c->cm64, c->pt, c->nv32, c->level, c->stats, c->Vhi, c->Vlo, c->pttc, c->kpmax, c->anchors, c->nva, c->tile_anchor, c->tc_vmax, c->fps_keys, c->ipa0, c->tile_rad, c->rho, c->cmx, c->cmx0, c->selected, c->chunkpart, c->counter, c->cur, c->best,
+  void* ptrs[] = {c->V32, c->V64, c->e0d, c->cm64, c->pt, c->nv32, c->level, c->stats, c->Vhi, c->Vlo, c->pttc, c->kpmax, c->anchors, c->nva, c->tile_anchor, c->tc_vmax, c->fps_keys, c->ipa0, c->tile_rad, c->rho, c->cmx, c->cmx0, c->selected, c->chunkpart, c->counter, c->counter2, c->topc, c->toppart, c->cur, c->best,
                   c->maxlb, c->wcount, c->wlist, c->wgain, c->ub};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -996,6 +1017,10 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
   CUC(cudaMalloc(&ctx->chunkpart, (size_t)ctx->nchunks * sizeof(double)));
   CUC(cudaMalloc(&ctx->counter, sizeof(unsigned int)));
   CUC(cudaMemsetAsync(ctx->counter, 0, sizeof(unsigned int), ctx->stream));
+  CUC(cudaMalloc(&ctx->counter2, sizeof(unsigned int)));
+  CUC(cudaMemsetAsync(ctx->counter2, 0, sizeof(unsigned int), ctx->stream));
+  CUC(cudaMalloc(&ctx->topc, sizeof(int64_t)));
+  CUC(cudaMalloc(&ctx->toppart, (size_t)ctx->nchunks * sizeof(double)));
   CUC(cudaMalloc(&ctx->cur, sizeof(double)));
   CUC(cudaMemsetAsync(ctx->cur, 0, sizeof(double), ctx->stream));
   CUC(cudaMalloc(&ctx->best, sizeof(int64_t)));

@@ -541,7 +541,8 @@ using ScreenB = ScreenCfg<8, 2, 4, 3, 1>;
 __global__ void k_finalize(int64_t c0, int64_t c1, int nsplit, const double* __restrict__ part_g,
                            const float* __restrict__ part_e, int64_t part_stride, double einfl, double gcoef,
                            double gscale, const unsigned char* __restrict__ selected, double* __restrict__ ub,
-                           long long* __restrict__ maxlb, const int* __restrict__ level_now, int level) {
+                           long long* __restrict__ maxlb, const int* __restrict__ level_now, int level,
+                           int ub_only = 0) {
   if (level_now && *level_now != level) return;
   __shared__ long long smax[256];
   const int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -568,7 +569,85 @@ __global__ void k_finalize(int64_t c0, int64_t c1, int nsplit, const double* __r
     if (threadIdx.x < s) smax[threadIdx.x] = max(smax[threadIdx.x], smax[threadIdx.x + s]);
     __syncthreads();
   }
-  if (threadIdx.x == 0) atomicMax(maxlb, smax[0]);
+  if (threadIdx.x == 0 && !ub_only) atomicMax(maxlb, smax[0]);
+}
+
+// Upper-bound-only screens (the tensor rung: its partials are already sums of
+// max(a + kq, 0), certified upper bounds with no error count): the window
+// threshold is the EXACT gain of the candidate with the largest bound, which is
+// a valid lower bound on the top gain.  Step 1: that candidate (lowest index
+// among equal bounds).
+__global__ void __launch_bounds__(1024) k_argmax_ub(int64_t c0, int64_t c1, const double* __restrict__ ub,
+                                                    int64_t* __restrict__ topc, const int* __restrict__ level_now,
+                                                    int level) {
+  if (level_now && *level_now != level) return;
+  __shared__ double sv[1024];
+  __shared__ long long si[1024];
+  double bv = -INFINITY;
+  long long bi = LLONG_MAX;
+  for (int64_t c = c0 + threadIdx.x; c < c1; c += blockDim.x) {
+    const double u = ub[c - c0];
+    if (u > bv) {  // ascending c per thread: the first maximum is the lowest index
+      bv = u;
+      bi = c;
+    }
+  }
+  sv[threadIdx.x] = bv;
+  si[threadIdx.x] = bi;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      const double ov = sv[threadIdx.x + s];
+      const long long oi = si[threadIdx.x + s];
+      if (ov > sv[threadIdx.x] || (ov == sv[threadIdx.x] && oi < si[threadIdx.x])) {
+        sv[threadIdx.x] = ov;
+        si[threadIdx.x] = oi;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *topc = (sv[0] > -INFINITY) ? si[0] : -1;
+}
+
+// Step 2: exact fp64 gain of topc, sum_v max(0, cm(v) - d64(v, c)) in chunk
+// partials; the last block writes it as the window's lower bound (maxlb key).
+template <typename T>
+__global__ void __launch_bounds__(RED_THREADS) k_gain_top(const T* __restrict__ V, int pitch, int64_t n, int d,
+                                                          const double* __restrict__ cm64,
+                                                          const int64_t* __restrict__ topc,
+                                                          double* __restrict__ part, unsigned int* __restrict__ counter,
+                                                          long long* __restrict__ maxlb,
+                                                          const int* __restrict__ level_now, int level) {
+  if (level_now && *level_now != level) return;
+  extern __shared__ double cd[];
+  __shared__ double sbuf[RED_THREADS];
+  __shared__ bool last;
+  const int64_t s = *topc;
+  if (s >= 0)
+    for (int k = threadIdx.x; k < d; k += blockDim.x) cd[k] = (double)V[s * pitch + k];
+  __syncthreads();
+  double acc = 0.0;
+  if (s >= 0) {
+    for (int i = 0; i < RCH / RED_THREADS; ++i) {
+      const int64_t v = (int64_t)blockIdx.x * RCH + threadIdx.x + (int64_t)i * RED_THREADS;
+      if (v < n) {
+        const double t = cm64[v] - dist64_row(V + v * pitch, cd, d);
+        acc += t > 0.0 ? t : 0.0;
+      }
+    }
+  }
+  const double bs = block_sum_256(acc, sbuf);
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = bs;
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    *maxlb = dkey(chunk_total(part, gridDim.x));
+    *counter = 0u;
+  }
 }
 
 // W = {c : ub_c >= max lb - margin}  (append order is irrelevant: the pick is by

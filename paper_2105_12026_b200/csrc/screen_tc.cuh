@@ -735,7 +735,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       // one error quantum per tile: kpmax = max_v kp over the tile (bounds every
       // pair's kp_v; computed at reset, cm only decreases within a run)
       const float kq = kpa[tt] + fmaf(kxc, __ldg(an.vmax + tt), kc);
-      const float thr = -kq;
+      const float thr = -kq;           // FLAG: possibly closer than e0 iff a > -kq
+      const float icq = ic + kq;       // bound: a + kq = b + icq
       mbar_wait(&tfull[b], (it / NB) & 1);
       fence_after();
       float S[SW];
@@ -769,24 +770,19 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
             }
           }
         }
-      } else if (mb + ic > thr) {
-        // four independent fp32 partial sums / counts per 32 columns (ILP); each
-        // partial adds 8 terms, so every fp64 fold still covers <= 32 terms
-        // combined by a fixed tree (the finalize bound assumes 32)
-        float cnt4[4] = {0.f, 0.f, 0.f, 0.f};
-        constexpr int GW = SW < 32 ? SW : 32;  // columns per fp64 fold
+      } else if (mb + icq > 0.f) {
+        // upper bound only: gain/2 <= sum max(a + kq, 0) with a + kq = fl(b + icq);
+        // fl(. + icq) is monotone, so a slice whose max gives <= 0 adds exactly 0.
+        // Four independent fp32 partial sums per 32 columns (ILP); each partial
+        // adds 8 terms, every fp64 fold covers <= 32 (the finalize bound).
+        constexpr int GW = SW < 32 ? SW : 32;
 #pragma unroll
         for (int h = 0; h < SW; h += GW) {
           float g4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-          for (int i = h; i < h + GW; ++i) {
-            const float a = S[i] + ic;
-            g4[i & 3] += fmaxf(a, 0.f);
-            cnt4[i & 3] += (a > thr) ? 1.f : 0.f;
-          }
+          for (int i = h; i < h + GW; ++i) g4[i & 3] += fmaxf(S[i] + icq, 0.f);
           g64 += (double)((g4[0] + g4[1]) + (g4[2] + g4[3]));
         }
-        e = fmaf((cnt4[0] + cnt4[1]) + (cnt4[2] + cnt4[3]), kq, e);
       }
     }
     if (!FLAG) {
