@@ -1,0 +1,179 @@
+"""Command line front end for the B200 path.
+
+``python -m paper_2105_12026_b200 summarize data.csv -k K`` is the reference's
+``ebcsum summarize`` (cli.py:229-327) with the ``b200`` backend: the same CSV
+contract (rectangular, finite cells, optional header, optional population
+z-score per column), the same e0 kinds, greedy or sieve optimizer, and the same
+JSON document.  ``surrogate`` writes the injection-molding case-study matrix
+(cli.py:111-173 contract) so C4-shaped inputs can be produced without the
+reference.  Exit codes follow the reference's scripting contract (cli.py:1-6):
+0 ok, 1 usage error, 2 data/configuration error, 3 internal error.  The
+reference's ``bench`` sweep and ``layout-audit`` (device-model simulator) are
+out of scope.
+"""
+
+from __future__ import annotations
+
+import argparse
+import csv
+import json
+import math
+import sys
+from typing import List, Optional
+
+import numpy as np
+
+EXIT_OK, EXIT_USAGE, EXIT_DATA, EXIT_INTERNAL = 0, 1, 2, 3
+
+
+class CsvParseError(ValueError):
+    """A CSV cell or row that cannot be turned into finite numbers."""
+
+
+class _UsageError(Exception):
+    pass
+
+
+class _Parser(argparse.ArgumentParser):
+    def error(self, message):  # argparse exits 2; the contract says usage errors are 1
+        raise _UsageError(message)
+
+
+def load_csv(path: str, has_header: bool = False, normalize: bool = False):
+    """Numeric matrix from CSV (reference load_csv contract, cli.py:59-108):
+    blank lines skipped, rectangular rows, every cell a finite float; errors
+    name the 1-based row (and column).  normalize: z-score with the population
+    standard deviation, constant columns left at 0.  Returns (fp64 array, header)."""
+    rows: List[List[float]] = []
+    header: Optional[List[str]] = None
+    width: Optional[int] = None
+    with open(path, newline="") as fh:
+        for line_no, row in enumerate(csv.reader(fh), start=1):
+            if not row:
+                continue
+            if has_header and header is None:
+                header = [tok.strip() for tok in row]
+                continue
+            if width is None:
+                width = len(row)
+            elif len(row) != width:
+                raise CsvParseError(f"row {line_no}: expected {width} columns, got {len(row)}")
+            vals = []
+            for col_no, tok in enumerate(row, start=1):
+                try:
+                    x = float(tok)
+                except ValueError:
+                    raise CsvParseError(f"row {line_no}, column {col_no}: not a number: {tok.strip()!r}") from None
+                if not math.isfinite(x):
+                    raise CsvParseError(f"row {line_no}, column {col_no}: non-finite value {tok.strip()!r}")
+                vals.append(x)
+            rows.append(vals)
+    if not rows:
+        raise CsvParseError(f"{path}: no data rows")
+    data = np.array(rows, dtype=np.float64)
+    if normalize:
+        mu, sd = data.mean(axis=0), data.std(axis=0)
+        out = np.zeros_like(data)
+        live = sd > 0
+        out[:, live] = (data[:, live] - mu[live]) / sd[live]
+        data = out
+    return data, header
+
+
+def _positive_int(text: str) -> int:
+    v = int(text)
+    if v < 1:
+        raise argparse.ArgumentTypeError(f"expected an integer >= 1, got {text}")
+    return v
+
+
+def build_parser() -> argparse.ArgumentParser:
+    from .core import Precision
+
+    parser = _Parser(prog="paper_2105_12026_b200", description="Exemplar-based summarization on B200")
+    sub = parser.add_subparsers(dest="command", required=True, parser_class=_Parser)
+    p = sub.add_parser("summarize", help="select k representatives from a CSV")
+    p.add_argument("input")
+    p.add_argument("-k", type=_positive_int, required=True)
+    p.add_argument("--optimizer", choices=("greedy", "sieve"), default="greedy")
+    p.add_argument("--backend", choices=("b200",), default="b200")
+    p.add_argument("--precision", choices=[m.value for m in Precision], default="fp64")
+    p.add_argument("--e0-kind", choices=("zero", "mean"), default="zero")
+    p.add_argument("--epsilon", type=float, default=0.1)
+    p.add_argument("--seed", type=int, default=0, help="stream order seed (sieve)")
+    p.add_argument("--header", action="store_true")
+    p.add_argument("--normalize", action="store_true")
+    p.add_argument("--output", default=None)
+    p.set_defaults(func=cmd_summarize)
+    p = sub.add_parser("surrogate", help="write the injection-molding surrogate as CSV")
+    p.add_argument("--cycles", type=_positive_int, default=1000)
+    p.add_argument("--dims", type=_positive_int, default=100)
+    p.add_argument("--regimes", type=_positive_int, default=5)
+    p.add_argument("--noise", type=float, default=0.01)
+    p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--output", required=True)
+    p.set_defaults(func=cmd_surrogate)
+    return parser
+
+
+def cmd_summarize(args) -> int:
+    from .core import GroundMatrix, Precision, make_auxiliary_vector
+    from .ebc import EbcFunction
+    from .optimize import OptimizerBudget, greedy_maximize, sieve_stream_maximize
+
+    data, _ = load_csv(args.input, has_header=args.header, normalize=args.normalize)
+    precision = Precision.parse(args.precision)
+    ground = GroundMatrix(data, precision)
+    if args.k > ground.n:
+        raise ValueError(f"k={args.k} exceeds the {ground.n} rows of {args.input}")
+    e0 = make_auxiliary_vector(ground.dims, args.e0_kind, ground)
+    f = EbcFunction(ground, e0)
+    if args.optimizer == "greedy":
+        summary = greedy_maximize(f, OptimizerBudget(k=args.k, backend=args.backend))
+    else:
+        stream = np.random.default_rng(args.seed).permutation(ground.n)
+        summary = sieve_stream_maximize(stream, f, args.k, epsilon=args.epsilon)
+    doc = {"k": args.k, "selected_indices": [int(i) for i in summary.selected],
+           "function_value": summary.value, "gains": [float(g) for g in summary.gains],
+           "backend": args.backend, "precision": precision.value, "runtime_seconds": summary.runtime_seconds}
+    text = json.dumps(doc, indent=2) + "\n"
+    if args.output:
+        with open(args.output, "w") as fh:
+            fh.write(text)
+    else:
+        sys.stdout.write(text)
+    return EXIT_OK
+
+
+def cmd_surrogate(args) -> int:
+    from .surrogate import surrogate
+
+    if args.cycles % args.regimes:
+        raise ValueError("--regimes must divide --cycles")
+    X = surrogate(args.cycles, args.dims, args.regimes, args.noise, args.seed)
+    np.savetxt(args.output, X, delimiter=",", fmt="%.17g")
+    print(f"wrote {X.shape[0]}x{X.shape[1]} surrogate to {args.output}")
+    return EXIT_OK
+
+
+def main(argv=None) -> int:
+    parser = build_parser()
+    try:
+        args = parser.parse_args(argv)
+    except _UsageError as exc:
+        print(f"usage error: {exc}", file=sys.stderr)
+        return EXIT_USAGE
+    except SystemExit as exc:  # --help
+        return int(exc.code or 0)
+    try:
+        return args.func(args)
+    except (ValueError, IndexError, OSError) as exc:
+        print(f"error: {exc}", file=sys.stderr)
+        return EXIT_DATA
+    except Exception as exc:  # pragma: no cover - defensive
+        print(f"internal error: {exc!r}", file=sys.stderr)
+        return EXIT_INTERNAL
+
+
+if __name__ == "__main__":
+    sys.exit(main())
