@@ -758,16 +758,32 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       }
       const float mb = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
       if (FLAG) {
-        if (mb + ic > thr) {
+        // rare: pairs possibly closer than e0.  Warp-aggregated append: one
+        // atomicAdd per warp and tile, each lane writes at its prefix offset.
+        if (__any_sync(0xffffffffu, mb + ic > thr)) {
+          uint64_t msk = 0;
+          const int64_t vb = (int64_t)tt * NP + half * SLICE;
+          if (c < fo.ncands) {
 #pragma unroll
-          for (int i = 0; i < SW; ++i) {
-            if (S[i] + ic > thr) {  // rare: possibly closer than e0
-              const int64_t v = (int64_t)tt * NP + half * SLICE + i;
-              if (v < fo.npoints && c < fo.ncands) {
-                const int slot = atomicAdd(fo.count, 1);
-                if (slot < fo.cap) fo.pairs[slot] = make_uint2((unsigned)v, (unsigned)c);
-              }
-            }
+            for (int i = 0; i < SW; ++i)
+              if (S[i] + ic > thr && vb + i < fo.npoints) msk |= 1ull << i;
+          }
+          const int cnt = __popcll(msk);
+          int incl = cnt;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+          }
+          int base = 0;
+          if (lane == 31 && incl > 0) base = atomicAdd(fo.count, incl);
+          base = __shfl_sync(0xffffffffu, base, 31);
+          int slot = base + incl - cnt;
+          while (msk) {
+            const int i = __ffsll((long long)msk) - 1;
+            msk &= msk - 1;
+            if (slot < fo.cap) fo.pairs[slot] = make_uint2((unsigned)(vb + i), (unsigned)c);
+            ++slot;
           }
         }
       } else if (mb + icq > 0.f) {
