@@ -11,6 +11,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -207,10 +208,13 @@ int fail(ebc_ctx* c, int code, const std::string& msg) {
 
 int ensure(ebc_ctx* ctx, DevBuf& b, size_t bytes) {
   if (b.bytes >= bytes) return EBC_OK;
-  if (b.p) cudaFree(b.p);
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(ctx->stream, &cap) == cudaSuccess && cap != cudaStreamCaptureStatusNone)
+    return fail(ctx, EBC_ECUDA, "buffer growth during graph capture");  // the capture is abandoned, run stays eager
+  if (b.p) cudaFreeAsync(b.p, ctx->stream);
   b.p = nullptr;
   b.bytes = 0;
-  CU(cudaMalloc(&b.p, bytes));
+  CU(cudaMallocAsync((void**)&b.p, bytes, ctx->stream));
   b.bytes = bytes;
   ++ctx->alloc_epoch;  // cached graphs hold the old pointers
   return EBC_OK;
@@ -711,19 +715,22 @@ void free_ctx(ebc_ctx* c) {
   void* ptrs[] = {c->V32, c->V64, c->e0d, c->cm64, c->pt, c->nv32, c->level, c->stats, c->Vhi, c->Vlo, c->pttc, c->kpmax, c->anchors, c->nva, c->tile_anchor, c->tc_vmax, c->fps_keys, c->ipa0, c->tile_rad, c->rho, c->cmx, c->cmx0, c->selected, c->chunkpart, c->counter, c->counter2, c->topc, c->toppart, c->cur, c->best,
                   c->maxlb, c->wcount, c->wlist, c->wgain, c->ub};
   for (void* p : ptrs)
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, c->stream);
   DevBuf* bufs[] = {&c->tie_rec, &c->tie_all, &c->ms_tanchor, &c->ms_trad, &c->part_g, &c->part_e, &c->part_r, &c->sel_out, &c->val_out, &c->gain_out, &c->ms_part,
                     &c->ms_off, &c->ms_idx, &c->ms_out, &c->ms_mbuf, &c->ms_setof, &c->ms_pairs, &c->ms_keys,
                     &c->ms_vals, &c->ms_keys2, &c->ms_vals2, &c->ms_ukeys, &c->ms_uvals, &c->ms_cub};
   void* more[] = {c->pt0, c->ms_count, c->ms_nruns};
   for (void* p : more)
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, c->stream);
   for (DevBuf* b : bufs)
-    if (b->p) cudaFree(b->p);
+    if (b->p) cudaFreeAsync(b->p, c->stream);
   for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
   for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
-  if (c->tie_err) cudaFree(c->tie_err);
-  if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->tie_err) cudaFreeAsync(c->tie_err, c->stream);
+  if (c->stream) {
+    cudaStreamSynchronize(c->stream);
+    cudaStreamDestroy(c->stream);
+  }
   delete c;
 }
 
@@ -736,10 +743,10 @@ int multiset_sparse(ebc_ctx* ctx, int64_t l, int64_t nnz) {
   if (!rc) rc = ensure(ctx, ctx->ms_setof, (size_t)mrows * sizeof(int));
   if (rc) return rc;
   if (!ctx->pt0) {
-    CU(cudaMalloc(&ctx->pt0, (size_t)ctx->n_pad * sizeof(float4)));
+    CU(cudaMallocAsync((void**)&ctx->pt0, (size_t)ctx->n_pad * sizeof(float4), ctx->stream));
     CU(cudaMemsetAsync(ctx->pt0, 0, (size_t)ctx->n_pad * sizeof(float4), ctx->stream));
-    CU(cudaMalloc(&ctx->ms_count, sizeof(int)));
-    CU(cudaMalloc(&ctx->ms_nruns, sizeof(int)));
+    CU(cudaMallocAsync((void**)&ctx->ms_count, sizeof(int), ctx->stream));
+    CU(cudaMallocAsync((void**)&ctx->ms_nruns, sizeof(int), ctx->stream));
     k_make_pt0<<<(unsigned)((ctx->n + 255) / 256), 256, 0, ctx->stream>>>(ctx->n, ctx->e0d, ctx->nv32, ctx->pk,
                                                                           ctx->pt0);
     KCHECK();
@@ -764,7 +771,7 @@ int multiset_sparse(ebc_ctx* ctx, int64_t l, int64_t nnz) {
     rc = ensure(ctx, ctx->ms_tanchor, (size_t)(mrows / 128 + 1) * sizeof(int));
     if (!rc) rc = ensure(ctx, ctx->ms_trad, (size_t)(mrows / 128 + 1) * sizeof(float));
     if (!rc && !ctx->ipa0) {
-      CU(cudaMalloc(&ctx->ipa0, (size_t)ctx->tc_na * ctx->n_pad * sizeof(float)));
+      CU(cudaMallocAsync((void**)&ctx->ipa0, (size_t)ctx->tc_na * ctx->n_pad * sizeof(float), ctx->stream));
       TcSeeds s0 = tc_seeds(ctx);
       s0.ipa = ctx->ipa0;
       k_seed_ipa<<<(unsigned)((ctx->n_pad + 255) / 256), 256, 0, ctx->stream>>>(ctx->e0d, ctx->n, ctx->n_pad, s0);
@@ -906,30 +913,54 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
     }                                                                                               \
   } while (0)
   CUC(cudaSetDevice(device));
-  cudaDeviceProp prop;
-  CUC(cudaGetDeviceProperties(&prop, device));
-  if (prop.major < 10)
+  // single attributes, not cudaGetDeviceProperties (which can cost tens of ms per call)
+  int cc_major = 0, cc_minor = 0, sms = 0;
+  CUC(cudaDeviceGetAttribute(&cc_major, cudaDevAttrComputeCapabilityMajor, device));
+  CUC(cudaDeviceGetAttribute(&cc_minor, cudaDevAttrComputeCapabilityMinor, device));
+  CUC(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  if (cc_major < 10)
     rc = fail(nullptr, EBC_ECUDA,
-              std::string("b200 backend needs an sm_100 device, found ") + prop.name + " sm_" +
-                  std::to_string(prop.major * 10 + prop.minor));
+              "b200 backend needs an sm_100 device, found sm_" + std::to_string(cc_major * 10 + cc_minor));
   if (rc) {
     free_ctx(ctx);
     return rc;
   }
-  ctx->num_sms = prop.multiProcessorCount;
+  ctx->num_sms = sms;
+  {
+    // every device buffer comes from the default stream-ordered pool, which
+    // keeps freed memory (release threshold = max): building and destroying a
+    // context per call (the e2e path) never goes back to the driver's mapper
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
   CUC(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+  // EBC200_PROFILE_CREATE=1: host wall time of the creation phases on stderr
+  const bool prof = getenv("EBC200_PROFILE_CREATE") != nullptr;
+  auto tnow = []() { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+  const double t_begin = tnow();
+  auto mark = [&](const char* what) {
+    if (prof) {
+      cudaStreamSynchronize(ctx->stream);
+      fprintf(stderr, "[ebc_create] %-22s %8.2f ms\n", what, tnow() - t_begin);
+    }
+  };
   const size_t esz = dtype == EBC_F64 ? sizeof(double) : sizeof(float);
   const size_t src_esz = dtype == EBC_F64 ? 8 : (dtype == EBC_F16 ? 2 : 4);
   void* Vdev = nullptr;
-  CUC(cudaMalloc(&Vdev, (size_t)ctx->n_pad * ctx->pitch * esz));
+  CUC(cudaMallocAsync((void**)&Vdev, (size_t)ctx->n_pad * ctx->pitch * esz, ctx->stream));
   CUC(cudaMemsetAsync(Vdev, 0, (size_t)ctx->n_pad * ctx->pitch * esz, ctx->stream));
   if (dtype == EBC_F64)
     ctx->V64 = (double*)Vdev;
   else
     ctx->V32 = (float*)Vdev;
   void* raw = nullptr;
-  CUC(cudaMalloc(&raw, (size_t)n * d * src_esz));
+  CUC(cudaMallocAsync((void**)&raw, (size_t)n * d * src_esz, ctx->stream));
+  mark("allocs V/raw");
   CUC(cudaMemcpyAsync(raw, V, (size_t)n * d * src_esz, cudaMemcpyHostToDevice, ctx->stream));
+  mark("upload");
   {
     const int blocks = 8 * ctx->num_sms;
     if (dtype == EBC_F32)
@@ -940,15 +971,15 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
       k_pad<double, double><<<blocks, 256, 0, ctx->stream>>>((const double*)raw, n, d, ctx->V64, ctx->pitch);
     CUC(cudaGetLastError());
   }
-  CUC(cudaMalloc(&ctx->e0d, (size_t)n * sizeof(double)));
-  CUC(cudaMalloc(&ctx->cm64, (size_t)ctx->n_pad * sizeof(double)));
-  CUC(cudaMalloc(&ctx->pt, (size_t)ctx->n_pad * sizeof(float4)));
+  CUC(cudaMallocAsync((void**)&ctx->e0d, (size_t)n * sizeof(double), ctx->stream));
+  CUC(cudaMallocAsync((void**)&ctx->cm64, (size_t)ctx->n_pad * sizeof(double), ctx->stream));
+  CUC(cudaMallocAsync((void**)&ctx->pt, (size_t)ctx->n_pad * sizeof(float4), ctx->stream));
   CUC(cudaMemsetAsync(ctx->pt, 0, (size_t)ctx->n_pad * sizeof(float4), ctx->stream));
-  CUC(cudaMalloc(&ctx->nv32, (size_t)ctx->n_pad * sizeof(float)));
+  CUC(cudaMallocAsync((void**)&ctx->nv32, (size_t)ctx->n_pad * sizeof(float), ctx->stream));
   CUC(cudaMemsetAsync(ctx->nv32, 0, (size_t)ctx->n_pad * sizeof(float), ctx->stream));
-  CUC(cudaMalloc(&ctx->stats, 6 * sizeof(long long)));  // [4]: tensor-screen tile pairs executed
+  CUC(cudaMallocAsync((void**)&ctx->stats, 6 * sizeof(long long), ctx->stream));  // [4]: tensor-screen tile pairs executed
   CUC(cudaMemsetAsync(ctx->stats, 0, 6 * sizeof(long long), ctx->stream));
-  CUC(cudaMalloc(&ctx->level, sizeof(int)));
+  CUC(cudaMallocAsync((void**)&ctx->level, sizeof(int), ctx->stream));
   CUC(cudaMemsetAsync(ctx->level, 0, sizeof(int), ctx->stream));
   // tensor-core screen: fp32-path grounds whose 128-candidate tile of hi+lo
   // operands plus a 2-stage ring of NP-point tiles fits shared memory
@@ -991,46 +1022,46 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
       ctx->tc_ntl = ctx->n_pad / ctx->tc_np;
       const size_t ve = (size_t)ctx->n_pad * ctx->kpad;
       const size_t nas = (size_t)ctx->tc_na * ctx->n_pad;
-      CUC(cudaMalloc(&ctx->Vhi, ve * es));
-      if (parts == 2) CUC(cudaMalloc(&ctx->Vlo, ve * es));
-      CUC(cudaMalloc(&ctx->pttc, nas * sizeof(float)));
-      CUC(cudaMalloc(&ctx->nva, nas * sizeof(float)));
+      CUC(cudaMallocAsync((void**)&ctx->Vhi, ve * es, ctx->stream));
+      if (parts == 2) CUC(cudaMallocAsync((void**)&ctx->Vlo, ve * es, ctx->stream));
+      CUC(cudaMallocAsync((void**)&ctx->pttc, nas * sizeof(float), ctx->stream));
+      CUC(cudaMallocAsync((void**)&ctx->nva, nas * sizeof(float), ctx->stream));
       CUC(cudaMemsetAsync(ctx->nva, 0, nas * sizeof(float), ctx->stream));
-      CUC(cudaMalloc(&ctx->kpmax, (size_t)ctx->tc_na * ctx->tc_ntl * sizeof(float)));
-      CUC(cudaMalloc(&ctx->tc_vmax, (size_t)ctx->tc_ntl * sizeof(float)));
-      CUC(cudaMalloc(&ctx->anchors, (size_t)ctx->tc_na * ctx->pitch * sizeof(float)));
-      CUC(cudaMalloc(&ctx->tile_anchor, (size_t)(ctx->n_pad / 128 + 1) * sizeof(int)));
+      CUC(cudaMallocAsync((void**)&ctx->kpmax, (size_t)ctx->tc_na * ctx->tc_ntl * sizeof(float), ctx->stream));
+      CUC(cudaMallocAsync((void**)&ctx->tc_vmax, (size_t)ctx->tc_ntl * sizeof(float), ctx->stream));
+      CUC(cudaMallocAsync((void**)&ctx->anchors, (size_t)ctx->tc_na * ctx->pitch * sizeof(float), ctx->stream));
+      CUC(cudaMallocAsync((void**)&ctx->tile_anchor, (size_t)(ctx->n_pad / 128 + 1) * sizeof(int), ctx->stream));
       CUC(cudaMemsetAsync(ctx->tile_anchor, 0, (size_t)(ctx->n_pad / 128 + 1) * sizeof(int), ctx->stream));
-      CUC(cudaMalloc(&ctx->fps_keys, (size_t)(ctx->tc_na + 1) * sizeof(unsigned long long)));
+      CUC(cudaMallocAsync((void**)&ctx->fps_keys, (size_t)(ctx->tc_na + 1) * sizeof(unsigned long long), ctx->stream));
       const char* pr_env = getenv("EBC200_TC_PRUNE");
       ctx->tc_prune = !(pr_env && pr_env[0] == '0');
-      CUC(cudaMalloc(&ctx->tile_rad, (size_t)(ctx->n_pad / 128 + 1) * sizeof(float)));
+      CUC(cudaMallocAsync((void**)&ctx->tile_rad, (size_t)(ctx->n_pad / 128 + 1) * sizeof(float), ctx->stream));
       CUC(cudaMemsetAsync(ctx->tile_rad, 0, (size_t)(ctx->n_pad / 128 + 1) * sizeof(float), ctx->stream));
-      CUC(cudaMalloc(&ctx->rho, (size_t)ctx->tc_na * ctx->tc_ntl * sizeof(float)));
-      CUC(cudaMalloc(&ctx->cmx, (size_t)ctx->tc_ntl * sizeof(float)));
-      CUC(cudaMalloc(&ctx->cmx0, (size_t)ctx->tc_ntl * sizeof(float)));
+      CUC(cudaMallocAsync((void**)&ctx->rho, (size_t)ctx->tc_na * ctx->tc_ntl * sizeof(float), ctx->stream));
+      CUC(cudaMallocAsync((void**)&ctx->cmx, (size_t)ctx->tc_ntl * sizeof(float), ctx->stream));
+      CUC(cudaMallocAsync((void**)&ctx->cmx0, (size_t)ctx->tc_ntl * sizeof(float), ctx->stream));
       CUC(cudaMemsetAsync(ctx->fps_keys, 0, (size_t)(ctx->tc_na + 1) * sizeof(unsigned long long), ctx->stream));
     }
   }
-  CUC(cudaMalloc(&ctx->selected, (size_t)ctx->n_pad));
+  CUC(cudaMallocAsync((void**)&ctx->selected, (size_t)ctx->n_pad, ctx->stream));
   CUC(cudaMemsetAsync(ctx->selected, 0, (size_t)ctx->n_pad, ctx->stream));
-  CUC(cudaMalloc(&ctx->chunkpart, (size_t)ctx->nchunks * sizeof(double)));
-  CUC(cudaMalloc(&ctx->counter, sizeof(unsigned int)));
+  CUC(cudaMallocAsync((void**)&ctx->chunkpart, (size_t)ctx->nchunks * sizeof(double), ctx->stream));
+  CUC(cudaMallocAsync((void**)&ctx->counter, sizeof(unsigned int), ctx->stream));
   CUC(cudaMemsetAsync(ctx->counter, 0, sizeof(unsigned int), ctx->stream));
-  CUC(cudaMalloc(&ctx->counter2, sizeof(unsigned int)));
+  CUC(cudaMallocAsync((void**)&ctx->counter2, sizeof(unsigned int), ctx->stream));
   CUC(cudaMemsetAsync(ctx->counter2, 0, sizeof(unsigned int), ctx->stream));
-  CUC(cudaMalloc(&ctx->topc, sizeof(int64_t)));
-  CUC(cudaMalloc(&ctx->toppart, (size_t)ctx->nchunks * sizeof(double)));
-  CUC(cudaMalloc(&ctx->cur, sizeof(double)));
+  CUC(cudaMallocAsync((void**)&ctx->topc, sizeof(int64_t), ctx->stream));
+  CUC(cudaMallocAsync((void**)&ctx->toppart, (size_t)ctx->nchunks * sizeof(double), ctx->stream));
+  CUC(cudaMallocAsync((void**)&ctx->cur, sizeof(double), ctx->stream));
   CUC(cudaMemsetAsync(ctx->cur, 0, sizeof(double), ctx->stream));
-  CUC(cudaMalloc(&ctx->best, sizeof(int64_t)));
-  CUC(cudaMalloc(&ctx->maxlb, sizeof(long long)));
-  CUC(cudaMalloc(&ctx->wcount, sizeof(int)));
-  CUC(cudaMalloc(&ctx->wlist, (size_t)n * sizeof(int64_t)));
-  CUC(cudaMalloc(&ctx->wgain, (size_t)n * sizeof(double)));
-  CUC(cudaMalloc(&ctx->ub, (size_t)n * sizeof(double)));
+  CUC(cudaMallocAsync((void**)&ctx->best, sizeof(int64_t), ctx->stream));
+  CUC(cudaMallocAsync((void**)&ctx->maxlb, sizeof(long long), ctx->stream));
+  CUC(cudaMallocAsync((void**)&ctx->wcount, sizeof(int), ctx->stream));
+  CUC(cudaMallocAsync((void**)&ctx->wlist, (size_t)n * sizeof(int64_t), ctx->stream));
+  CUC(cudaMallocAsync((void**)&ctx->wgain, (size_t)n * sizeof(double), ctx->stream));
+  CUC(cudaMallocAsync((void**)&ctx->ub, (size_t)n * sizeof(double), ctx->stream));
   double* e0dev = nullptr;
-  CUC(cudaMalloc(&e0dev, (size_t)d * sizeof(double)));
+  CUC(cudaMallocAsync((void**)&e0dev, (size_t)d * sizeof(double), ctx->stream));
   {
     std::vector<double> z;
     const double* src = e0;
@@ -1045,6 +1076,7 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
     k_init<double><<<ctx->nchunks, RED_THREADS, 0, ctx->stream>>>(ctx->V64, ctx->pitch, n, d, e0dev, ctx->pk,
                                                                  ctx->e0d, ctx->cm64, ctx->nv32, ctx->pt, ctx->chunkpart);
   else
+    mark("allocs rest"),
     k_init<float><<<ctx->nchunks, RED_THREADS, 0, ctx->stream>>>(ctx->V32, ctx->pitch, n, d, e0dev, ctx->pk,
                                                                 ctx->e0d, ctx->cm64, ctx->nv32, ctx->pt, ctx->chunkpart);
   CUC(cudaGetLastError());
@@ -1053,7 +1085,7 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
       // anchors (farthest-point sampling from the origin), |v - mu_a|^2, the
       // anchor of each candidate block, seeds and per-tile error quanta
       float* mind = nullptr;
-      CUC(cudaMalloc(&mind, (size_t)n * sizeof(float)));
+      CUC(cudaMallocAsync((void**)&mind, (size_t)n * sizeof(float), ctx->stream));
       for (int a = 0; a < ctx->tc_na; ++a) {
         k_fps_step<<<2 * ctx->num_sms, 256, 0, ctx->stream>>>(ctx->V32, ctx->pitch, n, d, a, ctx->tc_na, mind,
                                                               ctx->fps_keys, ctx->anchors, ctx->pitch);
@@ -1078,7 +1110,8 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
                                                                                         ctx->tc_np, ctx->cmx0);
       CUC(cudaGetLastError());
       CUC(cudaStreamSynchronize(ctx->stream));
-      cudaFree(mind);
+      mark("init + anchors");
+      cudaFreeAsync(mind, ctx->stream);
     }
     if (ctx->tc_kind == tc::KIND_F16)
       k_split_f16<<<8 * ctx->num_sms, 256, 0, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->n_pad, d, ctx->kpad,
@@ -1092,17 +1125,18 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
     CUC(cudaGetLastError());
   }
   double* bl = nullptr;
-  CUC(cudaMalloc(&bl, sizeof(double)));
+  CUC(cudaMallocAsync((void**)&bl, sizeof(double), ctx->stream));
   k_total<<<1, 32, 0, ctx->stream>>>(ctx->chunkpart, ctx->nchunks, 1.0 / (double)n, bl);
   CUC(cudaGetLastError());
   CUC(cudaMemcpyAsync(&ctx->baseline, bl, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   CUC(cudaStreamSynchronize(ctx->stream));
-  cudaFree(bl);
-  cudaFree(e0dev);
-  cudaFree(raw);
+  cudaFreeAsync(bl, ctx->stream);
+  cudaFreeAsync(e0dev, ctx->stream);
+  cudaFreeAsync(raw, ctx->stream);
   ctx->ev.resize(4);
   for (auto& e : ctx->ev) CUC(cudaEventCreate(&e));
 #undef CUC
+  mark("done");
   *out = ctx;
   return EBC_OK;
 }
@@ -1348,7 +1382,7 @@ int ebc_comm_attach(ebc_ctx* ctx) {
   ctx->comm_gen = sc.generation;
   ctx->nranks = sc.nranks;
   ctx->rank = sc.rank;
-  if (!ctx->tie_err) CU(cudaMalloc(&ctx->tie_err, sizeof(int)));
+  if (!ctx->tie_err) CU(cudaMallocAsync((void**)&ctx->tie_err, sizeof(int), ctx->stream));
   ++ctx->alloc_epoch;  // graphs captured with another communicator are stale
   return EBC_OK;
 }
@@ -1391,7 +1425,7 @@ int ebc_shard_pick_commit(ebc_ctx* ctx, const double* gathered, int32_t world, i
   if (!rc) rc = ensure(ctx, ctx->val_out, (size_t)(step + 1) * sizeof(double));
   if (!rc) rc = ensure(ctx, ctx->gain_out, (size_t)(step + 1) * sizeof(double));
   if (rc) return rc;
-  if (!ctx->tie_err) CU(cudaMalloc(&ctx->tie_err, sizeof(int)));
+  if (!ctx->tie_err) CU(cudaMallocAsync((void**)&ctx->tie_err, sizeof(int), ctx->stream));
   CU(cudaMemsetAsync(ctx->tie_err, 0, sizeof(int), ctx->stream));
   CU(cudaMemcpyAsync(ctx->tie_all.p, gathered, (size_t)world * (TIE_CAP + 1) * sizeof(double2),
                      cudaMemcpyHostToDevice, ctx->stream));

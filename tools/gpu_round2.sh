@@ -1,0 +1,12 @@
+# Round evidence: every config's bench line (default C2 with the CPU baseline), C5 timing, launch lists.
+set -x
+mkdir -p gpurun_out
+timeout 900 python bench.py 2>gpurun_out/bench_err_C2.log > gpurun_out/bench_C2.json
+for C in C3 C4 C1; do
+  timeout 900 python bench.py --config $C --no-cpu-baseline 2>gpurun_out/bench_err_$C.log > gpurun_out/bench_$C.json
+done
+timeout 300 python tools/c5_time.py > gpurun_out/c5_time.txt 2>&1
+timeout 600 python bench.py --impl reference --steps 1 --warmup 0 > gpurun_out/bench_ref_C2.json 2>gpurun_out/bench_err_ref.log
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches_c4.csv python tools/profile_run.py C4 20 > /dev/null 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/launches_c5.csv python tools/c5_profile.py > /dev/null 2>&1
+nvidia-smi --query-gpu=name,clocks.max.sm,power.limit --format=csv
