@@ -140,6 +140,7 @@ struct ebc_ctx {
   unsigned int* counter2 = nullptr;  // k_gain_top's last-block ticket
   int64_t* topc = nullptr;           // candidate with the largest screen bound (ub-only screens)
   double* toppart = nullptr;         // nchunks: its exact gain's chunk partials
+  double* terms = nullptr;           // n: e0d - cm64 per point (split K4)
   double* cur = nullptr;
   int64_t* best = nullptr;
   long long* maxlb = nullptr;
@@ -621,10 +622,26 @@ int run_update(ebc_ctx* ctx, int step, double* val_dev, double* gain_dev) {
         ctx->V64, ctx->pitch, ctx->n, ctx->d, ctx->best, ctx->pk, ctx->e0d, ctx->nv32, ctx->cm64, ctx->pt, tc_seeds(ctx), ctx->chunkpart,
         ctx->counter, 1.0 / (double)ctx->n, ctx->cur, val_dev, gain_dev, step);
   } else {
-    CU(cudaFuncSetAttribute(k_update<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024));
-    k_update<float><<<ctx->nchunks, RED_THREADS, smem, ctx->stream>>>(
-        ctx->V32, ctx->pitch, ctx->n, ctx->d, ctx->best, ctx->pk, ctx->e0d, ctx->nv32, ctx->cm64, ctx->pt, tc_seeds(ctx), ctx->chunkpart,
-        ctx->counter, 1.0 / (double)ctx->n, ctx->cur, val_dev, gain_dev, step);
+    // split K4: wide streaming pass over V (a), fixed-structure reduction (b)
+    const int nb = (int)((ctx->n + RED_THREADS - 1) / RED_THREADS);
+    const bool stage = ctx->pitch <= UPDATE_STAGE_PITCH;
+    const size_t dsm = (size_t)((ctx->d + 1) & ~1) * sizeof(double) +
+                       (stage ? (size_t)RED_THREADS * ctx->pitch * sizeof(float) : 0);
+    if (stage) {
+      CU(cudaFuncSetAttribute(k_update_terms<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+      k_update_terms<true><<<nb, RED_THREADS, dsm, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->n, ctx->d, ctx->best,
+                                                                  ctx->pk, ctx->e0d, ctx->nv32, ctx->cm64, ctx->pt,
+                                                                  tc_seeds(ctx), ctx->terms);
+    } else {
+      CU(cudaFuncSetAttribute(k_update_terms<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm + 16));
+      k_update_terms<false><<<nb, RED_THREADS, dsm, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->n, ctx->d, ctx->best,
+                                                                   ctx->pk, ctx->e0d, ctx->nv32, ctx->cm64, ctx->pt,
+                                                                   tc_seeds(ctx), ctx->terms);
+    }
+    KCHECK();
+    k_update_reduce<<<ctx->nchunks, RED_THREADS, 0, ctx->stream>>>(ctx->terms, ctx->n, ctx->chunkpart, ctx->counter,
+                                                                   1.0 / (double)ctx->n, ctx->cur, val_dev, gain_dev,
+                                                                   step, ctx->best);
   }
   KCHECK();
   if (ctx->timing) CU(cudaEventRecord(ctx->ev[eb + 3], ctx->stream));
@@ -712,7 +729,7 @@ int do_reset(ebc_ctx* ctx) {
 void free_ctx(ebc_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
-  void* ptrs[] = {c->V32, c->V64, c->e0d, c->cm64, c->pt, c->nv32, c->level, c->stats, c->Vhi, c->Vlo, c->pttc, c->kpmax, c->anchors, c->nva, c->tile_anchor, c->tc_vmax, c->fps_keys, c->ipa0, c->tile_rad, c->rho, c->cmx, c->cmx0, c->selected, c->chunkpart, c->counter, c->counter2, c->topc, c->toppart, c->cur, c->best,
+  void* ptrs[] = {c->V32, c->V64, c->e0d, c->cm64, c->pt, c->nv32, c->level, c->stats, c->Vhi, c->Vlo, c->pttc, c->kpmax, c->anchors, c->nva, c->tile_anchor, c->tc_vmax, c->fps_keys, c->ipa0, c->tile_rad, c->rho, c->cmx, c->cmx0, c->selected, c->chunkpart, c->counter, c->counter2, c->topc, c->toppart, c->terms, c->cur, c->best,
                   c->maxlb, c->wcount, c->wlist, c->wgain, c->ub};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, c->stream);
@@ -1052,6 +1069,7 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
   CUC(cudaMemsetAsync(ctx->counter2, 0, sizeof(unsigned int), ctx->stream));
   CUC(cudaMallocAsync((void**)&ctx->topc, sizeof(int64_t), ctx->stream));
   CUC(cudaMallocAsync((void**)&ctx->toppart, (size_t)ctx->nchunks * sizeof(double), ctx->stream));
+  CUC(cudaMallocAsync((void**)&ctx->terms, (size_t)ctx->n_pad * sizeof(double), ctx->stream));
   CUC(cudaMallocAsync((void**)&ctx->cur, sizeof(double), ctx->stream));
   CUC(cudaMemsetAsync(ctx->cur, 0, sizeof(double), ctx->stream));
   CUC(cudaMallocAsync((void**)&ctx->best, sizeof(int64_t), ctx->stream));

@@ -50,6 +50,23 @@ __device__ __forceinline__ double chunk_total(const double* part, int nchunks) {
   return s;
 }
 
+// The same left-to-right sum by the last block of a grid: all threads stage
+// the partials through shared memory (coalesced, one L2 round trip per 256),
+// thread 0 adds them in order -- identical bits, no serial L2 latency chain.
+// Called by every thread of the block; result valid in thread 0.
+__device__ __forceinline__ double chunk_total_block(const double* part, int nchunks, double* sbuf) {
+  double s = 0.0;
+  for (int c0 = 0; c0 < nchunks; c0 += RED_THREADS) {
+    const int m = min(RED_THREADS, nchunks - c0);
+    if ((int)threadIdx.x < m) sbuf[threadIdx.x] = __ldcg(part + c0 + threadIdx.x);
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int i = 0; i < m; ++i) s += sbuf[i];
+    __syncthreads();
+  }
+  return s;
+}
+
 // Order-preserving map of a double onto a signed 64-bit key (for atomicMax).
 __device__ __forceinline__ long long dkey(double x) {
   long long b = __double_as_longlong(x);
@@ -66,6 +83,30 @@ __device__ __forceinline__ double dist64_row(const T* __restrict__ row, const do
   double s = 0.0;
   for (int k = 0; k < d; ++k) {
     double t = (double)row[k] - cd[k];
+    s = fma(t, t, s);
+  }
+  return s;
+}
+// fp32 rows (16-byte aligned: the pitch is a multiple of 4): the same sequential
+// operations, fed by 128-bit loads (a thread walks its own row; one LDG.128
+// per 4 dims instead of 4 scalar loads -- K4 is HBM/latency bound).
+__device__ __forceinline__ double dist64_row(const float* __restrict__ row, const double* cd, int d) {
+  const float4* r4 = reinterpret_cast<const float4*>(row);
+  double s = 0.0;
+  int k = 0;
+  for (; k + 4 <= d; k += 4) {
+    const float4 x = __ldg(r4 + (k >> 2));
+    double t = (double)x.x - cd[k];
+    s = fma(t, t, s);
+    t = (double)x.y - cd[k + 1];
+    s = fma(t, t, s);
+    t = (double)x.z - cd[k + 2];
+    s = fma(t, t, s);
+    t = (double)x.w - cd[k + 3];
+    s = fma(t, t, s);
+  }
+  for (; k < d; ++k) {
+    const double t = (double)row[k] - cd[k];
     s = fma(t, t, s);
   }
   return s;
@@ -643,10 +684,13 @@ __global__ void __launch_bounds__(RED_THREADS) k_gain_top(const T* __restrict__ 
     last = atomicAdd(counter, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (last && threadIdx.x == 0) {
+  if (last) {
     __threadfence();
-    *maxlb = dkey(chunk_total(part, gridDim.x));
-    *counter = 0u;
+    const double tot = chunk_total_block(part, gridDim.x, sbuf);
+    if (threadIdx.x == 0) {
+      *maxlb = dkey(tot);
+      *counter = 0u;
+    }
   }
 }
 
@@ -985,6 +1029,35 @@ __global__ void __launch_bounds__(1024) k_pick_global(const double2* __restrict_
 
 // cm64 = min(cm64, d64(., s)); pt = {-cm32, tau}; chunk partials of (e0d - cm64).
 // The last block to finish turns the partials into f(S) and the step record.
+// STAGE (fp32 rows, pitch <= UPDATE_STAGE_PITCH): each 256-point slice of the
+// chunk is a contiguous run of rows; the block copies it into shared memory
+// with coalesced 128-bit loads (the HBM-bound part of K4), then every thread
+// computes its own point's distance from shared memory (LDS.128, conflict-free
+// for an odd number of float4 per row) -- the same fp64 operation sequence.
+constexpr int UPDATE_STAGE_PITCH = 132;
+
+__device__ __forceinline__ double dist64_smem_row(const float* row, const double* cd, int d) {
+  const float4* r4 = reinterpret_cast<const float4*>(row);
+  double s = 0.0;
+  int k = 0;
+  for (; k + 4 <= d; k += 4) {
+    const float4 x = r4[k >> 2];
+    double t = (double)x.x - cd[k];
+    s = fma(t, t, s);
+    t = (double)x.y - cd[k + 1];
+    s = fma(t, t, s);
+    t = (double)x.z - cd[k + 2];
+    s = fma(t, t, s);
+    t = (double)x.w - cd[k + 3];
+    s = fma(t, t, s);
+  }
+  for (; k < d; ++k) {
+    const double t = (double)row[k] - cd[k];
+    s = fma(t, t, s);
+  }
+  return s;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(RED_THREADS) k_update(const T* __restrict__ V, int pitch, int64_t n, int d,
                                                         const int64_t* __restrict__ best, PtCoef pk,
@@ -1003,10 +1076,19 @@ __global__ void __launch_bounds__(RED_THREADS) k_update(const T* __restrict__ V,
   for (int k = threadIdx.x; k < d; k += blockDim.x) cd[k] = (double)V[s * pitch + k];
   __syncthreads();
   double acc = 0.0;
+  // the thread's 4 distances first (independent rows: their loads overlap),
+  // then the updates and the sum in the fixed point order
+  double tv[RCH / RED_THREADS];
+#pragma unroll
+  for (int i = 0; i < RCH / RED_THREADS; ++i) {
+    const int64_t v = (int64_t)blockIdx.x * RCH + threadIdx.x + (int64_t)i * RED_THREADS;
+    tv[i] = v < n ? dist64_row(V + v * pitch, cd, d) : 0.0;
+  }
+#pragma unroll
   for (int i = 0; i < RCH / RED_THREADS; ++i) {
     const int64_t v = (int64_t)blockIdx.x * RCH + threadIdx.x + (int64_t)i * RED_THREADS;
     if (v < n) {
-      const double t = dist64_row(V + v * pitch, cd, d);
+      const double t = tv[i];
       double m = cm64[v];
       if (t < m) {
         m = t;
@@ -1025,14 +1107,99 @@ __global__ void __launch_bounds__(RED_THREADS) k_update(const T* __restrict__ V,
     last = (ticket == gridDim.x - 1);
   }
   __syncthreads();
-  if (last && threadIdx.x == 0) {
+  if (last) {
     __threadfence();
-    const double fnew = chunk_total(fpart, gridDim.x) * inv_n;
-    const double fold = *cur;
-    if (val_out) val_out[step] = fnew;
-    if (gain_out) gain_out[step] = fnew - fold;
-    *cur = fnew;
-    *counter = 0u;
+    const double fnew = chunk_total_block(fpart, gridDim.x, sbuf) * inv_n;
+    if (threadIdx.x == 0) {
+      const double fold = *cur;
+      if (val_out) val_out[step] = fnew;
+      if (gain_out) gain_out[step] = fnew - fold;
+      *cur = fnew;
+      *counter = 0u;
+    }
+  }
+}
+
+
+// K4 for fp32 grounds, split in two so the HBM-bound part gets a wide grid:
+// (a) k_update_terms -- one point per thread, 256-row slices of V staged in
+//     shared memory with coalesced 128-bit loads (pitch <= UPDATE_STAGE_PITCH),
+//     cached-min / seed updates, term[v] = e0d[v] - cm[v];
+// (b) k_update_reduce -- the fixed chunk reduction of the terms (4 points per
+//     thread in order, 256-thread tree, chunks left to right): bit-identical
+//     to the fused kernel above.
+template <bool STAGE>
+__global__ void __launch_bounds__(RED_THREADS) k_update_terms(const float* __restrict__ V, int pitch, int64_t n,
+                                                              int d, const int64_t* __restrict__ best, PtCoef pk,
+                                                              const double* __restrict__ e0d,
+                                                              const float* __restrict__ nv32,
+                                                              double* __restrict__ cm64, float4* __restrict__ pt,
+                                                              TcSeeds seeds, double* __restrict__ terms) {
+  extern __shared__ double cd[];
+  const int64_t s = *best;
+  if (s < 0) return;
+  for (int k = threadIdx.x; k < d; k += blockDim.x) cd[k] = (double)V[s * pitch + k];
+  const int64_t v0 = (int64_t)blockIdx.x * RED_THREADS;
+  const int64_t v = v0 + threadIdx.x;
+  double t = 0.0;
+  if constexpr (STAGE) {
+    float* stage = reinterpret_cast<float*>(cd + ((d + 1) & ~1));  // 16-byte aligned after the candidate
+    const int rows = (int)(n - v0 < RED_THREADS ? n - v0 : RED_THREADS);
+    const float4* src = reinterpret_cast<const float4*>(V + v0 * pitch);
+    float4* dst = reinterpret_cast<float4*>(stage);
+    const int q4 = rows * (pitch >> 2);
+    for (int q = threadIdx.x; q < q4; q += RED_THREADS) dst[q] = __ldcs(src + q);
+    __syncthreads();
+    if (v < n) t = dist64_smem_row(stage + threadIdx.x * pitch, cd, d);
+  } else {
+    __syncthreads();
+    if (v < n) t = dist64_row(V + v * pitch, cd, d);
+  }
+  if (v < n) {
+    double m = cm64[v];
+    if (t < m) {
+      m = t;
+      cm64[v] = m;
+      pt[v] = make_pt((float)m, nv32[v], pk);
+      if (seeds.ipa) write_seeds(seeds, v, (float)m);
+    }
+    terms[v] = e0d[v] - m;
+  }
+}
+
+__global__ void __launch_bounds__(RED_THREADS) k_update_reduce(const double* __restrict__ terms, int64_t n,
+                                                               double* __restrict__ fpart,
+                                                               unsigned int* __restrict__ counter, double inv_n,
+                                                               double* __restrict__ cur, double* __restrict__ val_out,
+                                                               double* __restrict__ gain_out, int step,
+                                                               const int64_t* __restrict__ best) {
+  __shared__ double sbuf[RED_THREADS];
+  __shared__ bool last;
+  if (*best < 0) return;
+  double acc = 0.0;
+#pragma unroll
+  for (int i = 0; i < RCH / RED_THREADS; ++i) {
+    const int64_t v = (int64_t)blockIdx.x * RCH + threadIdx.x + (int64_t)i * RED_THREADS;
+    if (v < n) acc += terms[v];
+  }
+  const double bs = block_sum_256(acc, sbuf);
+  if (threadIdx.x == 0) {
+    fpart[blockIdx.x] = bs;
+    __threadfence();
+    const unsigned int ticket = atomicAdd(counter, 1u);
+    last = (ticket == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    const double fnew = chunk_total_block(fpart, gridDim.x, sbuf) * inv_n;
+    if (threadIdx.x == 0) {
+      const double fold = *cur;
+      if (val_out) val_out[step] = fnew;
+      if (gain_out) gain_out[step] = fnew - fold;
+      *cur = fnew;
+      *counter = 0u;
+    }
   }
 }
 
