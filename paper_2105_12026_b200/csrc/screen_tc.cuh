@@ -159,6 +159,9 @@ __device__ __forceinline__ void ldcols(uint32_t taddr, float (&v)[W]) {
 }
 
 constexpr int M = 128;        // candidates per CTA (UMMA M)
+#ifndef EBC200_EPI_FADD2
+#define EBC200_EPI_FADD2 1
+#endif
 #ifndef EBC200_EPI_WARPGROUPS
 #define EBC200_EPI_WARPGROUPS 2
 #endif
@@ -748,8 +751,17 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       // adds exactly 0 to the gain and to the count, and the tile is skipped --
       // the common case (few points are closer to a candidate than to the summary).
       float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#if EBC200_EPI_FADD2
+#pragma unroll
+      for (int i = 0; i < SW; i += 2) {  // packed FADD2: half the issue slots
+        const float2 r = __fadd2_rn(make_float2(S[i], S[i + 1]), make_float2(ipv[i], ipv[i + 1]));
+        S[i] = r.x;
+        S[i + 1] = r.y;
+      }
+#else
 #pragma unroll
       for (int i = 0; i < SW; ++i) S[i] += ipv[i];
+#endif
 #pragma unroll
       for (int i = 0; i < SW; i += 8) {
         m4[(i / 8) & 3] = fmaxf(m4[(i / 8) & 3], fmaxf(fmaxf(S[i], S[i + 1]), S[i + 2]));
@@ -794,10 +806,21 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         constexpr int GW = SW < 32 ? SW : 32;
 #pragma unroll
         for (int h = 0; h < SW; h += GW) {
+#if EBC200_EPI_FADD2
+          float2 g2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+          const float2 icq2 = make_float2(icq, icq);
+#pragma unroll
+          for (int i = h; i < h + GW; i += 2) {
+            const float2 a = __fadd2_rn(make_float2(S[i], S[i + 1]), icq2);
+            g2[(i >> 1) & 1] = __fadd2_rn(g2[(i >> 1) & 1], make_float2(fmaxf(a.x, 0.f), fmaxf(a.y, 0.f)));
+          }
+          g64 += (double)((g2[0].x + g2[0].y) + (g2[1].x + g2[1].y));
+#else
           float g4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
           for (int i = h; i < h + GW; ++i) g4[i & 3] += fmaxf(S[i] + icq, 0.f);
           g64 += (double)((g4[0] + g4[1]) + (g4[2] + g4[3]));
+#endif
         }
       }
     }
