@@ -156,8 +156,9 @@ int ebc_set_timing(ebc_ctx* ctx, int on);
 int ebc_last_timings(const ebc_ctx* ctx, double* out_ms4);
 
 /* Screen statistics since the last reset / Greedy run: [0] sum of certified
- * window sizes, [1] largest window, [2] screen rung in use at the end (0 tensor
- * Gram, 1 FFMA Gram, 2 direct, -1 n/a), [3] steps. */
+ * window sizes, [1] largest window, [2] screen rung in use at the end (0 fast
+ * tensor Gram with one rounded FP16 product, 1 tensor Gram with the operand kind
+ * of ebc_screen_info [2], 2 FFMA Gram, 3 direct, -1 n/a), [3] steps. */
 int ebc_last_stats(const ebc_ctx* ctx, int64_t* out4);
 
 /* Point-candidate pairs the tensor screen actually evaluated since the last
@@ -168,7 +169,8 @@ int ebc_last_screen_work(const ebc_ctx* ctx, int64_t* out_pairs);
 /* Screen configuration: [0] mode (0 direct, 1 FFMA Gram, 2 ladder from FFMA
  * Gram, 3 ladder from the tensor screen), [1] points per tensor tile (0: no
  * tensor screen), [2] tensor operand kind (1 BF16 h+m split, 0 TF32 hi+lo split,
- * 2 FP16 values of fp16-stored grounds, -1 n/a),
+ * 2 FP16 values of fp16-stored grounds, -1 n/a; rung 0, when enabled, always
+ * uses fp32 values rounded to FP16),
  * [3] padded K of the tensor operands. */
 int ebc_screen_info(const ebc_ctx* ctx, int64_t* out4);
 

@@ -105,7 +105,7 @@ struct ebc_ctx {
   float4* pt = nullptr;
   float* nv32 = nullptr;
   long long* stats = nullptr;  // k_pick: window-size statistics of the last run
-  int* level = nullptr;  // adaptive screen: current rung of the ladder (0 tensor, 1 FFMA Gram, 2 direct)
+  int* level = nullptr;  // adaptive screen: current rung of the ladder (L_FAST .. L_DIRECT)
   PtCoef pk{};
   // screen mode: 0 direct, 1 FFMA Gram, 2 adaptive from FFMA Gram, 3 adaptive from the tensor screen
   int screen_mode = 2;
@@ -114,6 +114,11 @@ struct ebc_ctx {
   void* Vhi = nullptr;
   void* Vlo = nullptr;
   int tc_kind = 1;  // tc::KIND_TF32 / KIND_BF16 (fp32 grounds) / KIND_F16 (fp16 grounds)
+  // fast first rung (fp32 grounds, large d): one rounded FP16 product (tc::KIND_F16R)
+  bool tc_fast = false;
+  void* Vf = nullptr;  // fp16(oscale x) in the UMMA canonical layout
+  float tc_kx_fast = 0.f, tc_oscale = 1.f, tc_sinv2 = 1.f, tc_keta = 0.f, tc_keta2 = 0.f;
+  int wcap_fast = 256;
   float* pttc = nullptr;   // na x n_pad seeds ip_a(v) = (cm32 - |v - mu_a|^2)/2
   float* kpmax = nullptr;  // na x tc_ntl: per (anchor, point tile) max error quantum kp (reset state)
   int tc_na = 1;           // anchors (0 = the origin)
@@ -399,6 +404,11 @@ int run_finalize_window(ebc_ctx* ctx, int nsplit, double nterms, int gterms, int
   return EBC_OK;
 }
 
+// Rungs of the adaptive screen ladder: the fast FP16-rounded
+// tensor screen, the BF16-split (or FP16 / TF32) tensor screen, the FFMA Gram
+// screen, the direct screen.
+enum { L_FAST = 0, L_TC = 1, L_GRAM = 2, L_DIRECT = 3 };
+
 struct TcPlan {
   int ncb, ntiles, tps, nsplit;
   size_t smem;
@@ -407,9 +417,9 @@ struct TcPlan {
 };
 
 int tc_es(int kind) { return kind == tc::KIND_TF32 ? 4 : 2; }
-int tc_parts(int kind) { return kind == tc::KIND_F16 ? 1 : 2; }
+int tc_parts(int kind) { return tc::one_product(kind) ? 1 : 2; }
 
-bool plan_tc(const ebc_ctx* ctx, TcPlan& p) {
+bool plan_tc(const ebc_ctx* ctx, TcPlan& p, int kind) {
   if (!ctx->tc_np || (ctx->c0 % 8) != 0) return false;
   const int64_t ncand = ctx->c1 - ctx->c0;
   p.ncb = (int)((ncand + tc::M - 1) / tc::M);
@@ -428,7 +438,7 @@ bool plan_tc(const ebc_ctx* ctx, TcPlan& p) {
     }
   }
   p.nsplit = (p.ntiles + p.tps - 1) / p.tps;
-  const int es = tc_es(ctx->tc_kind), parts = tc_parts(ctx->tc_kind);
+  const int es = tc_es(kind), parts = tc_parts(kind);
   p.list_cap = 0;
   p.stages = tc::stages_for(ctx->kpad, ctx->tc_np, es, parts);
   if (ctx->tc_prune && p.tps <= 65535) {
@@ -448,10 +458,18 @@ int launch_tc_t(ebc_ctx* ctx, const TcPlan& p, const int* level_now, int level) 
   auto kern = k_screen_tc<NP, KIND>;
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
   dim3 grid(p.ncb, p.nsplit);
+  constexpr bool fast = KIND == tc::KIND_F16R;
   TcAnchors an{ctx->anchors, ctx->pitch, ctx->tile_anchor, ctx->pttc, ctx->n_pad, ctx->kpmax, ctx->tc_ntl,
-               ctx->tc_vmax, ctx->tc_kc, ctx->tc_kx, p.list_cap ? ctx->rho : nullptr, ctx->tile_rad, ctx->cmx,
-               p.list_cap, (unsigned long long*)(ctx->stats + 4)};
-  kern<<<grid, tc::THREADS, p.smem, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->d, (const unsigned char*)ctx->Vhi,
+               ctx->tc_vmax, ctx->tc_kc, fast ? ctx->tc_kx_fast : ctx->tc_kx, p.list_cap ? ctx->rho : nullptr,
+               ctx->tile_rad, ctx->cmx, p.list_cap, (unsigned long long*)(ctx->stats + 4)};
+  if (fast) {
+    an.oscale = ctx->tc_oscale;
+    an.sinv2 = ctx->tc_sinv2;
+    an.keta = ctx->tc_keta;
+    an.keta2 = ctx->tc_keta2;
+  }
+  kern<<<grid, tc::THREADS, p.smem, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->d,
+                                                   (const unsigned char*)(fast ? ctx->Vf : ctx->Vhi),
                                                    (const unsigned char*)ctx->Vlo, an, ctx->kpad, p.stages, ctx->c0,
                                                    p.ntiles, p.tps, (double*)ctx->part_g.p, (float*)ctx->part_e.p,
                                                    ctx->n_pad, level_now, level, nullptr, FlagOut{});
@@ -491,8 +509,11 @@ int launch_tc_flag(ebc_ctx* ctx, const TcPlan& p, const float* Vc, const int* ta
   }
 }
 
-int launch_tc(ebc_ctx* ctx, const TcPlan& p, const int* level_now, int level) {
-  switch (ctx->tc_kind) {
+int launch_tc(ebc_ctx* ctx, const TcPlan& p, const int* level_now, int level, int kind) {
+  switch (kind) {
+    case tc::KIND_F16R:
+      if (ctx->tc_np == 128) return launch_tc_t<128, tc::KIND_F16R>(ctx, p, level_now, level);
+      return launch_tc_t<64, tc::KIND_F16R>(ctx, p, level_now, level);
     case tc::KIND_F16:
       if (ctx->tc_np == 128) return launch_tc_t<128, tc::KIND_F16>(ctx, p, level_now, level);
       return launch_tc_t<64, tc::KIND_F16>(ctx, p, level_now, level);
@@ -517,9 +538,10 @@ int run_screen_window(ebc_ctx* ctx, int eb, int fin_blocks) {
   ScreenPlan p;
   int rc = plan_screen(ctx, p);
   if (rc) return rc;
-  TcPlan tp{};
-  const bool use_tc = ctx->screen_mode == 3 && plan_tc(ctx, tp);
-  const int nsplit_max = std::max(p.nsplit, use_tc ? tp.nsplit : 0);
+  TcPlan tp{}, fp{};
+  const bool use_tc = ctx->screen_mode == 3 && plan_tc(ctx, tp, ctx->tc_kind);
+  const bool use_fast = use_tc && ctx->tc_fast && plan_tc(ctx, fp, tc::KIND_F16R);
+  const int nsplit_max = std::max(std::max(p.nsplit, use_tc ? tp.nsplit : 0), use_fast ? fp.nsplit : 0);
   rc = ensure(ctx, ctx->part_g, (size_t)nsplit_max * ctx->n_pad * sizeof(double));
   if (rc) return rc;
   rc = ensure(ctx, ctx->part_e, (size_t)nsplit_max * ctx->n_pad * sizeof(float));
@@ -537,29 +559,38 @@ int run_screen_window(ebc_ctx* ctx, int eb, int fin_blocks) {
     if (!rc) rc = run_finalize_window(ctx, p.nsplit, nterms_ffma, p.tp, fin_blocks, 2.0, nullptr, 0);
   } else {
     if (use_tc) {
-      if (tp.list_cap || refine_prune_on(ctx)) {
+      if (tp.list_cap || fp.list_cap || refine_prune_on(ctx)) {
         k_tile_cmmax<<<(unsigned)((ctx->tc_ntl * 32 + 255) / 256), 256, 0, ctx->stream>>>(ctx->cm64, ctx->n,
                                                                                           ctx->tc_ntl, ctx->tc_np,
                                                                                           ctx->cmx);
         KCHECK();
         ctx->cmx_fresh = true;  // this step's refine may prune with it
       }
-      rc = launch_tc(ctx, tp, ctx->level, 0);
+      if (use_fast) {
+        rc = launch_tc(ctx, fp, ctx->level, L_FAST, tc::KIND_F16R);
+        if (!rc) rc = run_finalize_window(ctx, fp.nsplit, (double)fp.tps * ctx->tc_np, 32, fin_blocks, 2.0,
+                                          ctx->level, L_FAST, /*ub_only=*/true);
+        if (!rc) {
+          k_adapt<<<1, 32, 0, ctx->stream>>>(ctx->wcount, ctx->maxlb, ctx->wcap_fast, ctx->level, L_FAST);
+          KCHECK();
+        }
+      }
+      if (!rc) rc = launch_tc(ctx, tp, ctx->level, L_TC, ctx->tc_kind);
       if (!rc) rc = run_finalize_window(ctx, tp.nsplit, (double)tp.tps * ctx->tc_np, 32, fin_blocks, 2.0,
-                                        ctx->level, 0, /*ub_only=*/true);
+                                        ctx->level, L_TC, /*ub_only=*/true);
       if (!rc) {
-        k_adapt<<<1, 32, 0, ctx->stream>>>(ctx->wcount, ctx->maxlb, ctx->wcap, ctx->level, 0);
+        k_adapt<<<1, 32, 0, ctx->stream>>>(ctx->wcount, ctx->maxlb, ctx->wcap, ctx->level, L_TC);
         KCHECK();
       }
     }
-    if (!rc) rc = launch_screen<1>(ctx, p, ctx->level, 1);
-    if (!rc) rc = run_finalize_window(ctx, p.nsplit, nterms_ffma, p.tp, fin_blocks, 2.0, ctx->level, 1);
+    if (!rc) rc = launch_screen<1>(ctx, p, ctx->level, L_GRAM);
+    if (!rc) rc = run_finalize_window(ctx, p.nsplit, nterms_ffma, p.tp, fin_blocks, 2.0, ctx->level, L_GRAM);
     if (!rc) {
-      k_adapt<<<1, 32, 0, ctx->stream>>>(ctx->wcount, ctx->maxlb, ctx->wcap, ctx->level, 1);
+      k_adapt<<<1, 32, 0, ctx->stream>>>(ctx->wcount, ctx->maxlb, ctx->wcap, ctx->level, L_GRAM);
       KCHECK();
-      rc = launch_screen<0>(ctx, p, ctx->level, 2);
+      rc = launch_screen<0>(ctx, p, ctx->level, L_DIRECT);
     }
-    if (!rc) rc = run_finalize_window(ctx, p.nsplit, nterms_ffma, p.tp, fin_blocks, 1.0, ctx->level, 2);
+    if (!rc) rc = run_finalize_window(ctx, p.nsplit, nterms_ffma, p.tp, fin_blocks, 1.0, ctx->level, L_DIRECT);
   }
   if (rc) return rc;
   if (ctx->timing) CU(cudaEventRecord(ctx->ev[eb + 1], ctx->stream));
@@ -717,7 +748,7 @@ int do_reset(ebc_ctx* ctx) {
   KCHECK();
   {
     // first rung of the adaptive ladder for this run
-    const int start = (ctx->screen_mode == 3 && ctx->tc_np) ? 0 : 1;
+    const int start = (ctx->screen_mode == 3 && ctx->tc_np) ? (ctx->tc_fast ? L_FAST : L_TC) : L_GRAM;
     k_set_int<<<1, 1, 0, ctx->stream>>>(ctx->level, start);
   }
   KCHECK();
@@ -729,7 +760,7 @@ int do_reset(ebc_ctx* ctx) {
 void free_ctx(ebc_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
-  void* ptrs[] = {c->V32, c->V64, c->e0d, c->cm64, c->pt, c->nv32, c->level, c->stats, c->Vhi, c->Vlo, c->pttc, c->kpmax, c->anchors, c->nva, c->tile_anchor, c->tc_vmax, c->fps_keys, c->ipa0, c->tile_rad, c->rho, c->cmx, c->cmx0, c->selected, c->chunkpart, c->counter, c->counter2, c->topc, c->toppart, c->terms, c->cur, c->best,
+  void* ptrs[] = {c->V32, c->V64, c->e0d, c->cm64, c->pt, c->nv32, c->level, c->stats, c->Vhi, c->Vlo, c->Vf, c->pttc, c->kpmax, c->anchors, c->nva, c->tile_anchor, c->tc_vmax, c->fps_keys, c->ipa0, c->tile_rad, c->rho, c->cmx, c->cmx0, c->selected, c->chunkpart, c->counter, c->counter2, c->topc, c->toppart, c->terms, c->cur, c->best,
                   c->maxlb, c->wcount, c->wlist, c->wgain, c->ub};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, c->stream);
@@ -783,7 +814,7 @@ int multiset_sparse(ebc_ctx* ctx, int64_t l, int64_t nnz) {
   ctx->c1 = nnz;
   FlagOut fo{(uint2*)ctx->ms_pairs.p, ctx->ms_count, cap, ctx->n, nnz};
   TcPlan tp{};
-  if (ctx->ms_mode == 1 && ctx->screen_mode == 3 && plan_tc(ctx, tp)) {
+  if (ctx->ms_mode == 1 && ctx->screen_mode == 3 && plan_tc(ctx, tp, ctx->tc_kind)) {
     // tensor-core flag screen: anchors of the member blocks, reset-state seeds
     rc = ensure(ctx, ctx->ms_tanchor, (size_t)(mrows / 128 + 1) * sizeof(int));
     if (!rc) rc = ensure(ctx, ctx->ms_trad, (size_t)(mrows / 128 + 1) * sizeof(float));
@@ -1031,6 +1062,18 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
       ctx->tc_kp = (float)((d + 8) * u * 1.01);
       ctx->tc_kc = (float)((d + 8) * u * 1.01);
       ctx->tc_kx = (float)((ktc + 4.0 * u) * 1.01);
+      // fast first rung: fp32 grounds whose BF16 split is MMA-bound
+      // (3 kpad/16 K steps of 64 clk > the 1024-clk TMEM read of a 128-point tile)
+      const char* fast_env = getenv("EBC200_TC_FAST");
+      ctx->tc_fast = dtype == EBC_F32 && ctx->tc_kind == tc::KIND_BF16 &&
+                     ((fast_env && fast_env[0]) ? atoi(fast_env) != 0 : ctx->kpad >= 96);
+      if (ctx->tc_fast) {
+        // operand rounding 2^-11 relative per operand -> (2^-10 + 2^-22) |v_k c'_k|;
+        // one product per element accumulated in fp32
+        const double kfast = std::ldexp(1.0, -10) + std::ldexp(1.0, -22) + (ctx->kpad + 16.0) * std::ldexp(1.0, -23);
+        ctx->tc_kx_fast = (float)((kfast + 4.0 * u) * 1.01);
+        ctx->wcap_fast = (int)std::max<int64_t>(256, n / 128);
+      }
       // anchors: the origin plus farthest points (FP16 operands need c' = c exactly: origin only)
       const char* na_env = getenv("EBC200_TC_ANCHORS");
       ctx->tc_na = (na_env && na_env[0]) ? std::max(1, atoi(na_env)) : 32;
@@ -1041,6 +1084,7 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
       const size_t nas = (size_t)ctx->tc_na * ctx->n_pad;
       CUC(cudaMallocAsync((void**)&ctx->Vhi, ve * es, ctx->stream));
       if (parts == 2) CUC(cudaMallocAsync((void**)&ctx->Vlo, ve * es, ctx->stream));
+      if (ctx->tc_fast) CUC(cudaMallocAsync((void**)&ctx->Vf, ve * 2, ctx->stream));
       CUC(cudaMallocAsync((void**)&ctx->pttc, nas * sizeof(float), ctx->stream));
       CUC(cudaMallocAsync((void**)&ctx->nva, nas * sizeof(float), ctx->stream));
       CUC(cudaMemsetAsync(ctx->nva, 0, nas * sizeof(float), ctx->stream));
@@ -1130,6 +1174,27 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
       CUC(cudaStreamSynchronize(ctx->stream));
       mark("init + anchors");
       cudaFreeAsync(mind, ctx->stream);
+      if (ctx->tc_fast) {
+        // operand scale s = 2^e: every |s c'_k| <= s (|c| + |mu|) <= 2 s max|v| <= 2^15
+        // (fp16 max 65504); |e| <= 60 keeps s^2 and 1/s^2 normal in fp32
+        std::vector<float> vm((size_t)ctx->tc_ntl);
+        CUC(cudaMemcpy(vm.data(), ctx->tc_vmax, vm.size() * sizeof(float), cudaMemcpyDeviceToHost));
+        float vmx = 0.f;
+        for (float x : vm) vmx = std::max(vmx, x);
+        int e = vmx > 0.f ? (int)std::floor(std::log2(std::ldexp(1.0, 14) / (double)vmx)) : 0;
+        e = std::max(-60, std::min(60, e));
+        ctx->tc_oscale = (float)std::ldexp(1.0, e);
+        ctx->tc_sinv2 = (float)std::ldexp(1.0, -2 * e);
+        // subnormal half-spacing 2^-25 in scaled units: per element |err| <= 2^-11 |x| + eta
+        const double eta = std::ldexp(1.0, -25 - e);
+        ctx->tc_keta = (float)(eta * std::sqrt((double)d) * (1.0 + std::ldexp(1.0, -11)) * 1.02);
+        ctx->tc_keta2 = (float)((double)d * eta * eta * 1.02 + 1e-38);
+      }
+    }
+    if (ctx->tc_fast) {
+      k_split_f16<<<8 * ctx->num_sms, 256, 0, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->n_pad, d, ctx->kpad,
+                                                            (__half*)ctx->Vf, ctx->tc_oscale);
+      CUC(cudaGetLastError());
     }
     if (ctx->tc_kind == tc::KIND_F16)
       k_split_f16<<<8 * ctx->num_sms, 256, 0, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->n_pad, d, ctx->kpad,

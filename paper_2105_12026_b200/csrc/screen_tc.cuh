@@ -60,8 +60,13 @@ __host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
 // Operand kinds of the tensor screen.
 //   KIND_TF32: 3xTF32 split (kind::tf32), KIND_BF16: 3-product BF16 split
 //   (kind::f16), KIND_F16: FP16-stored grounds, one exact FP16 product per
-//   element (fp16 x fp16 has 22 significant bits: exact in the fp32 accumulator).
-enum { KIND_TF32 = 0, KIND_BF16 = 1, KIND_F16 = 2 };
+//   element (fp16 x fp16 has 22 significant bits: exact in the fp32 accumulator),
+//   KIND_F16R: fp32 grounds scaled by s = 2^e and ROUNDED to fp16, one product
+//   per element: relative operand error 2^-11 each, so the certified bound is
+//   ~2^-10 |v| |c'| per pair (vs ~2^-16 for the BF16 split) at a third of the
+//   MMA work -- the first rung when the BF16 split is MMA-bound (large d).
+enum { KIND_TF32 = 0, KIND_BF16 = 1, KIND_F16 = 2, KIND_F16R = 3 };
+__host__ __device__ constexpr bool one_product(int kind) { return kind == KIND_F16 || kind == KIND_F16R; }
 
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
   asm volatile(
@@ -177,7 +182,7 @@ struct TmemMap {
   static constexpr int NB = W16 ? 3 : 2;
   static constexpr uint32_t ALO = W16 ? 64 : 128;
   static constexpr uint32_t ACC = W16 ? 128 : 256;
-  static constexpr int PARTS = KIND == KIND_F16 ? 1 : 2;  // operand parts per point tile
+  static constexpr int PARTS = one_product(KIND) ? 1 : 2;  // operand parts per point tile
   static constexpr int ES = W16 ? 2 : 4;                  // operand element bytes
 };
 constexpr int MAX_STAGES = 4;
@@ -303,9 +308,10 @@ __global__ void k_split_bf16(const float* __restrict__ V32, int pitch, int64_t n
   }
 }
 
-// FP16 grounds: V (exactly widened to fp32) back to fp16, same blocked layout.
+// FP16 grounds: V (exactly widened to fp32) back to fp16, same blocked layout
+// (scale 1: exact).  KIND_F16R: fp16(scale * x), scale a power of two.
 __global__ void k_split_f16(const float* __restrict__ V32, int pitch, int64_t nrows, int d, int kpad,
-                            __half* __restrict__ hi) {
+                            __half* __restrict__ hi, float scale = 1.f) {
   const int KC = kpad / 8;
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t total = nrows * kpad;
@@ -314,7 +320,7 @@ __global__ void k_split_f16(const float* __restrict__ V32, int pitch, int64_t nr
     const int k = (int)(i - v * kpad);
     const float x = k < d ? V32[v * pitch + k] : 0.f;
     const int64_t off = (((v >> 3) * KC + (k >> 3)) * 8 + (v & 7)) * 8 + (k & 7);
-    hi[off] = __float2half_rn(x);
+    hi[off] = __float2half_rn(x * scale);
   }
 }
 
@@ -498,6 +504,13 @@ struct TcAnchors {
   const float* cmx;
   int list_cap;             // uint16 entries reserved for the kept-tile list
   unsigned long long* work; // if set: += executed (candidate block, point tile) pairs
+  // KIND_F16R: operands are fp16(oscale * x), the accumulator holds oscale^2 v.c';
+  // keta = sqrt(d) x (fp16 subnormal half-spacing 2^-25) / oscale x 1.02, the
+  // absolute underflow term of the operand rounding (per |c'| and per |v|max)
+  float oscale = 1.f;
+  float sinv2 = 1.f;
+  float keta = 0.f;
+  float keta2 = 0.f;  // d eta^2
 };
 
 // One CTA: candidates [cand0 + 128*bx, +128) x V tiles [t0, t1) of NP points.
@@ -611,7 +624,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     // overlap the other's queued MMAs.  The whole warp walks the loop
     // (warp-uniform operands stay in uniform registers), one elected lane issues.
     constexpr uint32_t idesc =
-        KIND == KIND_F16 ? idesc_f16(M, NP) : (KIND == KIND_BF16 ? idesc_bf16(M, NP) : idesc_tf32(M, NP));
+        one_product(KIND) ? idesc_f16(M, NP) : (KIND == KIND_BF16 ? idesc_bf16(M, NP) : idesc_tf32(M, NP));
     const uint32_t sbo = (uint32_t)kpad * 8 * ES;  // 8 rows x kpad elements
     const int ksteps = kpad / (BF ? 16 : 8);       // 32 bytes of K per instruction
     constexpr int NB = TM::NB;
@@ -633,7 +646,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       if (elect_one()) {
 #pragma unroll 4
         for (int j = 0; j < ksteps; ++j) {
-          if (KIND == KIND_F16)
+          if (one_product(KIND))
             mma1_f16_ts(dt, ahi + 8 * j, dhi + 16 * j, idesc, j > 0);
           else if (KIND == KIND_BF16)
             mma3_bf16_ts(dt, ahi + 8 * j, alo + 8 * j, dhi + 16 * j, dlo + 16 * j, idesc, j > 0);
@@ -675,12 +688,13 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         uint32_t rh[32], rl[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
-          if (KIND == KIND_F16) {
-            // FP16 operands only with the origin anchor (c' = c, exactly fp16)
+          if (one_product(KIND)) {
+            // KIND_F16: origin anchor only (c' = c, exactly fp16, oscale 1);
+            // KIND_F16R: fp16(oscale c'), the rounding is in the bound
             const int k = blk * 64 + 2 * i;
             const float x0 = cprime(k), x1 = cprime(k + 1);
-            rh[i] = (uint32_t)__half_as_ushort(__float2half_rn(x0)) |
-                    ((uint32_t)__half_as_ushort(__float2half_rn(x1)) << 16);
+            rh[i] = (uint32_t)__half_as_ushort(__float2half_rn(x0 * an.oscale)) |
+                    ((uint32_t)__half_as_ushort(__float2half_rn(x1 * an.oscale)) << 16);
             rl[i] = 0u;
           } else if (BF) {
             // column = packed pair (k = 2i, 2i+1), low half = even k
@@ -710,8 +724,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     // kpmax[a][tile] + kc + kx |v|max(tile) |c'|  (DESIGN.md §4 "anchored tensor screen")
     const float cn = sqrtf(cn2) * (1.f + 1e-5f);
     const float ic = -(mc + 0.5f * cn2);
-    const float kc = an.kc * (sqrtf(mn2) * (1.f + 1e-5f) * cn + cn2);
-    const float kxc = an.kx * cn;
+    const float kc = fmaf(an.keta, cn, an.kc * (sqrtf(mn2) * (1.f + 1e-5f) * cn + cn2)) + an.keta2;
+    const float kxc = fmaf(an.kx, cn, an.keta);
     const float* ipa = an.ipa + (int64_t)anc * an.ipstride;
     const float* kpa = an.kpmax + (int64_t)anc * an.kpstride;
     double g64 = 0.0;
@@ -752,13 +766,27 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       // the common case (few points are closer to a candidate than to the summary).
       float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #if EBC200_EPI_FADD2
+      if (KIND == KIND_F16R) {
+        // S sinv2 is exact (power of two): fl(S sinv2 + ip) in one packed FFMA2
+        const float2 sv2 = make_float2(an.sinv2, an.sinv2);
 #pragma unroll
-      for (int i = 0; i < SW; i += 2) {  // packed FADD2: half the issue slots
-        const float2 r = __fadd2_rn(make_float2(S[i], S[i + 1]), make_float2(ipv[i], ipv[i + 1]));
-        S[i] = r.x;
-        S[i + 1] = r.y;
+        for (int i = 0; i < SW; i += 2) {
+          const float2 r = __ffma2_rn(make_float2(S[i], S[i + 1]), sv2, make_float2(ipv[i], ipv[i + 1]));
+          S[i] = r.x;
+          S[i + 1] = r.y;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < SW; i += 2) {  // packed FADD2: half the issue slots
+          const float2 r = __fadd2_rn(make_float2(S[i], S[i + 1]), make_float2(ipv[i], ipv[i + 1]));
+          S[i] = r.x;
+          S[i + 1] = r.y;
+        }
       }
 #else
+      if (KIND == KIND_F16R)
+#pragma unroll
+        for (int i = 0; i < SW; ++i) S[i] *= an.sinv2;
 #pragma unroll
       for (int i = 0; i < SW; ++i) S[i] += ipv[i];
 #endif

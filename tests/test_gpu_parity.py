@@ -299,7 +299,7 @@ def test_sieve_validation_and_empty_stream():
 # ------------------------------------------------------------ every screen implementation
 
 @pytest.mark.parametrize("d", [32, 100])
-@pytest.mark.parametrize("variant", ["tc-tf32", "tc-bf16", "tc-f16", "ffma-gram", "direct"])
+@pytest.mark.parametrize("variant", ["tc-f16r", "tc-tf32", "tc-bf16", "tc-f16", "ffma-gram", "direct"])
 @pytest.mark.parametrize("prec", ["fp32", "fp16-storage"])
 def test_every_screen_variant_vs_oracle(monkeypatch, variant, prec, d):
     """Each rung of the adaptive ladder and each tensor operand kind, forced by
@@ -308,10 +308,14 @@ def test_every_screen_variant_vs_oracle(monkeypatch, variant, prec, d):
     from paper_2105_12026_b200 import optimize
     if variant == "tc-f16" and prec != "fp16-storage":
         pytest.skip("FP16 operands only for fp16-stored grounds")
-    mode, kind, rung = {"tc-tf32": ("3", "0", 0), "tc-bf16": ("3", "1", 0), "tc-f16": ("3", "2", 0),
-                        "ffma-gram": ("1", "", 1), "direct": ("0", "", 2)}[variant]
+    if variant == "tc-f16r" and prec != "fp32":
+        pytest.skip("the fast rounded-FP16 rung is for fp32 grounds")
+    # rungs: 0 fast (fp32 rounded to FP16), 1 tensor (operand kind), 2 FFMA Gram, 3 direct
+    mode, kind, rung = {"tc-f16r": ("3", "1", 0), "tc-tf32": ("3", "0", 1), "tc-bf16": ("3", "1", 1),
+                        "tc-f16": ("3", "2", 1), "ffma-gram": ("1", "", 2), "direct": ("0", "", 3)}[variant]
     monkeypatch.setenv("EBC200_SCREEN_MODE", mode)
     monkeypatch.setenv("EBC200_TC_KIND", kind)
+    monkeypatch.setenv("EBC200_TC_FAST", "1" if variant == "tc-f16r" else "0")
     rng = np.random.default_rng(100 + d)
     X = rng.standard_normal((4000, d)).astype(np.float32)
     g = eb.GroundMatrix(X, PREC[prec])
@@ -343,7 +347,7 @@ def test_clustered_surrogate_on_anchored_tensor_rung(monkeypatch, prune, regimes
     assert s.selected == sel
     np.testing.assert_allclose(np.cumsum(s.gains), vals, rtol=1e-10)
     if regimes == 5:
-        assert optimize.last_stats(f)[2] == 0
+        assert optimize.last_stats(f)[2] == 1  # d = 32: BF16-split tensor rung (no fast rung)
 
 
 def test_pruning_is_bit_identical(monkeypatch):
@@ -445,3 +449,19 @@ def test_sharded_api_over_one_rank_nccl_group():
                        timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "nccl one-rank ok" in r.stdout
+
+
+def test_fast_rung_falls_back_on_clustered_data(monkeypatch):
+    """The fast rung (fp32 rounded to FP16, ~2^-10 |v||c'| per pair) forced on
+    clustered data, where its certified window is wide: the ladder hands the
+    step to the BF16-split rung and the selection is still the oracle's."""
+    import datasets
+    from paper_2105_12026_b200 import optimize
+    monkeypatch.setenv("EBC200_TC_FAST", "1")
+    X = datasets.surrogate(20000, 32, 5, 0.01, 0).astype(np.float32)
+    f = fn(X, eb.Precision.FP32)
+    s = eb.greedy_maximize(f, eb.OptimizerBudget(k=8))
+    sel, vals, _, _ = oracle.greedy(X.astype(np.float64), 8)
+    assert s.selected == sel
+    np.testing.assert_allclose(np.cumsum(s.gains), vals, rtol=1e-10)
+    assert optimize.last_stats(f)[2] in (0, 1)
