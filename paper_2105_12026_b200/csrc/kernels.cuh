@@ -112,6 +112,50 @@ __device__ __forceinline__ double dist64_row(const float* __restrict__ row, cons
   return s;
 }
 
+// The 4 points a reduction thread owns (v0 + i * RED_THREADS, i = 0..3), their
+// fp64 distances to one candidate computed as 4 interleaved chains: each chain is
+// exactly dist64_row's operation sequence (bit-identical), but the 4 independent
+// DFMA chains and row loads overlap (the single-chain form is latency-bound).
+template <typename T>
+__device__ __forceinline__ void dist64_rows4(const T* __restrict__ V, int pitch, int64_t v0, int64_t n,
+                                             const double* cd, int d, double (&s)[4]) {
+  const T* row[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t v = v0 + (int64_t)i * 256;
+    row[i] = V + (v < n ? v : v0) * pitch;  // out-of-range points recompute row v0 (discarded)
+    s[i] = 0.0;
+  }
+  int k = 0;
+  if constexpr (sizeof(T) == 4) {
+    for (; k + 4 <= d; k += 4) {
+      float4 x[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) x[i] = __ldg(reinterpret_cast<const float4*>(row[i]) + (k >> 2));
+      const double c0 = cd[k], c1 = cd[k + 1], c2 = cd[k + 2], c3 = cd[k + 3];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        double t = (double)x[i].x - c0;
+        s[i] = fma(t, t, s[i]);
+        t = (double)x[i].y - c1;
+        s[i] = fma(t, t, s[i]);
+        t = (double)x[i].z - c2;
+        s[i] = fma(t, t, s[i]);
+        t = (double)x[i].w - c3;
+        s[i] = fma(t, t, s[i]);
+      }
+    }
+  }
+  for (; k < d; ++k) {
+    const double ck = cd[k];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const double t = (double)row[i][k] - ck;
+      s[i] = fma(t, t, s[i]);
+    }
+  }
+}
+
 // ---------------------------------------------------------------- per-point screen data
 
 // pt[v] = {-cm32, tau, ip, kp}: the direct screen seeds its accumulator with
@@ -668,11 +712,16 @@ __global__ void __launch_bounds__(RED_THREADS) k_gain_top(const T* __restrict__ 
     for (int k = threadIdx.x; k < d; k += blockDim.x) cd[k] = (double)V[s * pitch + k];
   __syncthreads();
   double acc = 0.0;
+  static_assert(RCH / RED_THREADS == 4 && RED_THREADS == 256, "dist64_rows4 layout");
   if (s >= 0) {
+    const int64_t v0 = (int64_t)blockIdx.x * RCH + threadIdx.x;
+    double dd[4];
+    if (v0 < n) dist64_rows4(V, pitch, v0, n, cd, d, dd);
+#pragma unroll
     for (int i = 0; i < RCH / RED_THREADS; ++i) {
-      const int64_t v = (int64_t)blockIdx.x * RCH + threadIdx.x + (int64_t)i * RED_THREADS;
+      const int64_t v = v0 + (int64_t)i * RED_THREADS;
       if (v < n) {
-        const double t = cm64[v] - dist64_row(V + v * pitch, cd, d);
+        const double t = cm64[v] - dd[i];
         acc += t > 0.0 ? t : 0.0;
       }
     }
@@ -838,29 +887,49 @@ __global__ void __launch_bounds__(RED_THREADS) k_refine(const T* __restrict__ V,
       double acc[RW];
 #pragma unroll
       for (int j = 0; j < RW; ++j) acc[j] = 0.0;
-      for (int i = 0; i < RCH / RED_THREADS; ++i) {
-        const int64_t v = (int64_t)ch * RCH + tid + (int64_t)i * RED_THREADS;
-        if (v < n && any) {
-          double s[RW];
+      const int64_t v0 = (int64_t)ch * RCH + tid;
+      if (v0 < n && any) {
+        // the thread's 4 points as 4 interleaved chains per candidate: each
+        // (point, candidate) chain is the same sequential fp64 operation
+        // sequence as before (bit-identical), the 4 x RW chains overlap
+        unsigned lm = 0;  // block-uniform: a short window / unreachable chunk does not pay
 #pragma unroll
-          for (int j = 0; j < RW; ++j) s[j] = 0.0;
-          const T* row = V + v * pitch;
-          for (int k = 0; k < d; ++k) {
-            const double x = (double)row[k];
+        for (int j = 0; j < RW; ++j) lm |= (live[j] ? 1u : 0u) << j;
+        const T* row[4];
+        double s[4][RW];
 #pragma unroll
-            for (int j = 0; j < RW; ++j) {
-              if (live[j]) {  // block-uniform: a short window / unreachable chunk does not pay
-                const double cv = BIGD ? (double)__ldg(V + cidx[j] * pitch + k) : cd[j * d + k];
-                const double t = x - cv;
-                s[j] = fma(t, t, s[j]);
+        for (int i = 0; i < 4; ++i) {
+          const int64_t v = v0 + (int64_t)i * RED_THREADS;
+          row[i] = V + (v < n ? v : v0) * pitch;
+#pragma unroll
+          for (int j = 0; j < RW; ++j) s[i][j] = 0.0;
+        }
+        for (int k = 0; k < d; ++k) {
+          double x[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) x[i] = (double)row[i][k];
+#pragma unroll
+          for (int j = 0; j < RW; ++j) {
+            if (lm >> j & 1u) {
+              const double cv = BIGD ? (double)__ldg(V + cidx[j] * pitch + k) : cd[j * d + k];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const double t = x[i] - cv;
+                s[i][j] = fma(t, t, s[i][j]);
               }
             }
           }
-          const double c = cm64[v];
+        }
 #pragma unroll
-          for (int j = 0; j < RW; ++j) {
-            const double t = c - s[j];
-            if (live[j]) acc[j] += t > 0.0 ? t : 0.0;
+        for (int i = 0; i < 4; ++i) {
+          const int64_t v = v0 + (int64_t)i * RED_THREADS;
+          if (v < n) {
+            const double c = cm64[v];
+#pragma unroll
+            for (int j = 0; j < RW; ++j) {
+              const double t = c - s[i][j];
+              if (lm >> j & 1u) acc[j] += t > 0.0 ? t : 0.0;
+            }
           }
         }
       }
