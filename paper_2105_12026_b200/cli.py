@@ -7,9 +7,10 @@ z-score per column), the same e0 kinds, greedy or sieve optimizer, and the same
 JSON document.  ``surrogate`` writes the injection-molding case-study matrix
 (cli.py:111-173 contract) so C4-shaped inputs can be produced without the
 reference.  Exit codes follow the reference's scripting contract (cli.py:1-6):
-0 ok, 1 usage error, 2 data/configuration error, 3 internal error.  The
-reference's ``bench`` sweep and ``layout-audit`` (device-model simulator) are
-out of scope.
+0 ok, 1 usage error, 2 data/configuration error, 3 internal error.  ``bench``
+is the reference's N / l / k sweep (cli.py:252-267, 330-342; ``sweep.py``) with
+the ``b200`` backend.  The reference's ``layout-audit`` (device-model
+simulator) is out of scope.
 """
 
 from __future__ import annotations
@@ -87,6 +88,16 @@ def _positive_int(text: str) -> int:
     return v
 
 
+def _int_list(text: str) -> List[int]:
+    try:
+        vals = [int(tok) for tok in text.split(",") if tok.strip()]
+    except ValueError:
+        raise argparse.ArgumentTypeError(f"expected comma-separated integers, got {text!r}") from None
+    if not vals:
+        raise argparse.ArgumentTypeError("empty value list")
+    return vals
+
+
 def build_parser() -> argparse.ArgumentParser:
     from .core import Precision
 
@@ -105,6 +116,20 @@ def build_parser() -> argparse.ArgumentParser:
     p.add_argument("--normalize", action="store_true")
     p.add_argument("--output", default=None)
     p.set_defaults(func=cmd_summarize)
+    p = sub.add_parser("bench", help="sweep one axis and report runtimes/speedups")
+    p.add_argument("--axis", choices=("N", "l", "k"), default="N")
+    p.add_argument("--values", type=_int_list, default=None, help="comma-separated axis values (defaults per axis)")
+    p.add_argument("--n", type=_positive_int, default=50000)
+    p.add_argument("--l", type=_positive_int, default=5000)
+    p.add_argument("-k", type=_positive_int, default=10)
+    p.add_argument("--dims", type=_positive_int, default=100)
+    p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--precision", choices=[m.value for m in Precision], default="fp32")
+    p.add_argument("--backends", default="b200", help="comma list of name[:threads]")
+    p.add_argument("--repeats", type=_positive_int, default=15)
+    p.add_argument("--format", choices=("csv", "markdown"), default="csv")
+    p.add_argument("--output", default=None)
+    p.set_defaults(func=cmd_bench)
     p = sub.add_parser("surrogate", help="write the injection-molding surrogate as CSV")
     p.add_argument("--cycles", type=_positive_int, default=1000)
     p.add_argument("--dims", type=_positive_int, default=100)
@@ -153,6 +178,24 @@ def cmd_surrogate(args) -> int:
     X = surrogate(args.cycles, args.dims, args.regimes, args.noise, args.seed)
     np.savetxt(args.output, X, delimiter=",", fmt="%.17g")
     print(f"wrote {X.shape[0]}x{X.shape[1]} surrogate to {args.output}")
+    return EXIT_OK
+
+
+def cmd_bench(args) -> int:
+    from .core import Precision
+    from .sweep import DEFAULT_AXIS_VALUES, ProblemSpec, emit_report, run_sweep
+
+    values = args.values if args.values else DEFAULT_AXIS_VALUES[args.axis]
+    base = ProblemSpec(n=args.n, l=args.l, k=args.k, dims=args.dims, seed=args.seed,
+                       precision=Precision.parse(args.precision))
+    backends = [tok.strip() for tok in args.backends.split(",") if tok.strip()]
+    report = run_sweep(args.axis, values, base, backends, repeats=args.repeats)
+    text = emit_report(report, format=args.format)
+    if args.output:
+        with open(args.output, "w") as fh:
+            fh.write(text)
+    else:
+        sys.stdout.write(text)
     return EXIT_OK
 
 
