@@ -118,6 +118,11 @@ struct ebc_ctx {
   bool tc_fast = false;
   void* Vf = nullptr;  // fp16(oscale x) in the UMMA canonical layout
   float tc_kx_fast = 0.f, tc_oscale = 1.f, tc_sinv2 = 1.f, tc_keta = 0.f, tc_keta2 = 0.f;
+  // seeds folded into the MMA for the one-product FP16 rung (rung 0 for fp32
+  // grounds, rung 1 for fp16-stored grounds): DESIGN.md §4
+  bool tc_mseed = false;
+  float tc_kpscale = 1.f;
+  int* tile_anchor0 = nullptr;  // all-zero block anchors (the origin) for rung 0 with folded seeds
   int wcap_fast = 256;
   float* pttc = nullptr;   // na x n_pad seeds ip_a(v) = (cm32 - |v - mu_a|^2)/2
   float* kpmax = nullptr;  // na x tc_ntl: per (anchor, point tile) max error quantum kp (reset state)
@@ -455,13 +460,24 @@ bool plan_tc(const ebc_ctx* ctx, TcPlan& p, int kind) {
 
 template <int NP, int KIND>
 int launch_tc_t(ebc_ctx* ctx, const TcPlan& p, const int* level_now, int level) {
-  auto kern = k_screen_tc<NP, KIND>;
+  constexpr bool one = tc::one_product(KIND);
+  const bool ms = one && ctx->tc_mseed;
+  auto kern = ms ? k_screen_tc<NP, KIND, false, one> : k_screen_tc<NP, KIND>;
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
   dim3 grid(p.ncb, p.nsplit);
   constexpr bool fast = KIND == tc::KIND_F16R;
-  TcAnchors an{ctx->anchors, ctx->pitch, ctx->tile_anchor, ctx->pttc, ctx->n_pad, ctx->kpmax, ctx->tc_ntl,
-               ctx->tc_vmax, ctx->tc_kc, fast ? ctx->tc_kx_fast : ctx->tc_kx, p.list_cap ? ctx->rho : nullptr,
-               ctx->tile_rad, ctx->cmx, p.list_cap, (unsigned long long*)(ctx->stats + 4)};
+  // folded seeds use the origin anchor: rung 0 (anchored otherwise) gets the
+  // all-zero anchor map and no tile-pair pruning (its radii belong to the
+  // chosen anchors); fp16-stored grounds have the origin as their only anchor
+  const bool origin_only = ms && fast;
+  TcAnchors an{ctx->anchors, ctx->pitch, origin_only ? ctx->tile_anchor0 : ctx->tile_anchor, ctx->pttc, ctx->n_pad,
+               ctx->kpmax, ctx->tc_ntl, ctx->tc_vmax, ctx->tc_kc, fast ? ctx->tc_kx_fast : ctx->tc_kx,
+               (p.list_cap && !origin_only) ? ctx->rho : nullptr, ctx->tile_rad, ctx->cmx, p.list_cap,
+               (unsigned long long*)(ctx->stats + 4)};
+  if (ms) {
+    an.kpscale = ctx->tc_kpscale;
+    an.keta2 = (float)std::ldexp(1.0, -24);  // seed split residual (fp16 subnormal), unscaled operands
+  }
   if (fast) {
     an.oscale = ctx->tc_oscale;
     an.sinv2 = ctx->tc_sinv2;
@@ -640,6 +656,12 @@ TcSeeds tc_seeds(const ebc_ctx* ctx) {
     s.nva = ctx->nva;
     s.na = ctx->tc_na;
     s.stride = ctx->n_pad;
+    if (ctx->tc_mseed) {
+      s.ops = (__half*)(ctx->tc_fast ? ctx->Vf : ctx->Vhi);
+      s.kpad = ctx->kpad;
+      s.d = ctx->d;
+      s.s2 = ctx->tc_fast ? ctx->tc_oscale * ctx->tc_oscale : 1.f;
+    }
   }
   return s;
 }
@@ -760,7 +782,7 @@ int do_reset(ebc_ctx* ctx) {
 void free_ctx(ebc_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
-  void* ptrs[] = {c->V32, c->V64, c->e0d, c->cm64, c->pt, c->nv32, c->level, c->stats, c->Vhi, c->Vlo, c->Vf, c->pttc, c->kpmax, c->anchors, c->nva, c->tile_anchor, c->tc_vmax, c->fps_keys, c->ipa0, c->tile_rad, c->rho, c->cmx, c->cmx0, c->selected, c->chunkpart, c->counter, c->counter2, c->topc, c->toppart, c->terms, c->cur, c->best,
+  void* ptrs[] = {c->V32, c->V64, c->e0d, c->cm64, c->pt, c->nv32, c->level, c->stats, c->Vhi, c->Vlo, c->Vf, c->tile_anchor0, c->pttc, c->kpmax, c->anchors, c->nva, c->tile_anchor, c->tc_vmax, c->fps_keys, c->ipa0, c->tile_rad, c->rho, c->cmx, c->cmx0, c->selected, c->chunkpart, c->counter, c->counter2, c->topc, c->toppart, c->terms, c->cur, c->best,
                   c->maxlb, c->wcount, c->wlist, c->wgain, c->ub};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, c->stream);
@@ -822,6 +844,7 @@ int multiset_sparse(ebc_ctx* ctx, int64_t l, int64_t nnz) {
       CU(cudaMallocAsync((void**)&ctx->ipa0, (size_t)ctx->tc_na * ctx->n_pad * sizeof(float), ctx->stream));
       TcSeeds s0 = tc_seeds(ctx);
       s0.ipa = ctx->ipa0;
+      s0.ops = nullptr;  // reset-state seeds only; the operand's folded seeds track the run
       k_seed_ipa<<<(unsigned)((ctx->n_pad + 255) / 256), 256, 0, ctx->stream>>>(ctx->e0d, ctx->n, ctx->n_pad, s0);
       KCHECK();
     }
@@ -1190,6 +1213,41 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
         ctx->tc_keta = (float)(eta * std::sqrt((double)d) * (1.0 + std::ldexp(1.0, -11)) * 1.02);
         ctx->tc_keta2 = (float)((double)d * eta * eta * 1.02 + 1e-38);
       }
+      // seeds folded into the MMA: the one-product rung with three
+      // spare K columns; scaled seeds |s^2 ip| <= s^2 (max e0d + max |v|^2)/2 <= 2^14
+      const bool one_rung = ctx->tc_fast || ctx->tc_kind == tc::KIND_F16;
+      const char* ms_env = getenv("EBC200_TC_MSEED");
+      if (one_rung && ctx->kpad - d >= 3 && !(ms_env && ms_env[0] == '0')) {
+        std::vector<double> e0h((size_t)n);
+        std::vector<float> nvh((size_t)n);
+        CUC(cudaMemcpy(e0h.data(), ctx->e0d, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost));
+        CUC(cudaMemcpy(nvh.data(), ctx->nv32, (size_t)n * sizeof(float), cudaMemcpyDeviceToHost));
+        double me = 0.0, mv = 0.0;
+        for (int64_t i = 0; i < n; ++i) {
+          me = std::max(me, e0h[(size_t)i]);
+          mv = std::max(mv, (double)nvh[(size_t)i]);
+        }
+        const double bip = 0.5 * (me + mv) * 1.01 + 1e-30;
+        if (ctx->tc_fast) {
+          const int e2 = (int)std::floor(0.5 * std::log2(std::ldexp(1.0, 14) / bip));
+          const int e = std::max(-60, std::min(e2, (int)std::lround(std::log2((double)ctx->tc_oscale))));
+          ctx->tc_oscale = (float)std::ldexp(1.0, e);
+          ctx->tc_sinv2 = (float)std::ldexp(1.0, -2 * e);
+          const double eta = std::ldexp(1.0, -25 - e);
+          ctx->tc_keta = (float)(eta * std::sqrt((double)d) * (1.0 + std::ldexp(1.0, -11)) * 1.02);
+          ctx->tc_keta2 = (float)((double)d * eta * eta * 1.02 + std::ldexp(1.0, -24 - 2 * e) + 1e-38);
+          ctx->tc_mseed = true;
+        } else {
+          ctx->tc_mseed = bip <= 16384.0;  // fp16-stored grounds: unscaled seeds must fit fp16
+        }
+        // in-MMA fp32 accumulation of the seed parts: (kpad + 16 + 8) 2^-23 |ip| on top
+        // of the (d + 8) u (cm + |v|^2) seed/final-add quantum kpmax
+        ctx->tc_kpscale = (float)((1.0 + (ctx->kpad + 24.0) / (d + 8.0)) * 1.01);
+        if (ctx->tc_mseed && ctx->tc_fast) {
+          CUC(cudaMallocAsync((void**)&ctx->tile_anchor0, (size_t)(ctx->n_pad / 128 + 1) * sizeof(int), ctx->stream));
+          CUC(cudaMemsetAsync(ctx->tile_anchor0, 0, (size_t)(ctx->n_pad / 128 + 1) * sizeof(int), ctx->stream));
+        }
+      }
     }
     if (ctx->tc_fast) {
       k_split_f16<<<8 * ctx->num_sms, 256, 0, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->n_pad, d, ctx->kpad,
@@ -1206,6 +1264,12 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
       k_split_tf32<<<8 * ctx->num_sms, 256, 0, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->n_pad, d, ctx->kpad,
                                                              (float*)ctx->Vhi, (float*)ctx->Vlo);
     CUC(cudaGetLastError());
+    if (ctx->tc_mseed) {
+      // the splits zero K columns >= d: write the folded seeds after them
+      k_seed_ipa<<<(unsigned)((ctx->n_pad + 255) / 256), 256, 0, ctx->stream>>>(ctx->cm64, n, ctx->n_pad,
+                                                                                 tc_seeds(ctx));
+      CUC(cudaGetLastError());
+    }
   }
   double* bl = nullptr;
   CUC(cudaMallocAsync((void**)&bl, sizeof(double), ctx->stream));

@@ -17,6 +17,7 @@
 // across GPUs, and the empty set evaluates to exactly 0.0.
 #pragma once
 #include <cfloat>
+#include <cuda_fp16.h>
 #include <cstdint>
 
 #include "ptx.cuh"
@@ -177,10 +178,34 @@ struct TcSeeds {
   const float* nva = nullptr;  // na x stride
   int na = 0;
   int64_t stride = 0;
+  // seeds folded into the MMA (one-product FP16 kinds): the origin
+  // seed ip_0(v), scaled by s2 = s^2 and split into three FP16 parts, sits in K
+  // columns d, d+1, d+2 of the point operand (UMMA canonical K-major layout,
+  // kpad columns); the candidate operand holds 1 there
+  __half* ops = nullptr;
+  int kpad = 0;
+  int d = 0;
+  float s2 = 1.f;
 };
+
+__device__ __forceinline__ int64_t umma_off(int64_t v, int k, int kpad) {
+  return (((v >> 3) * (kpad >> 3) + (k >> 3)) * 8 + (v & 7)) * 8 + (k & 7);
+}
+
+// X ~ p1 + p2 + p3 (each part the FP16 rounding of the remainder, |X| <= 2^14)
+__device__ __forceinline__ void write_seed_parts(const TcSeeds& s, int64_t v, float x) {
+  const __half p1 = __float2half_rn(x);
+  const float r1 = x - __half2float(p1);  // exact (fp32 holds x - p1)
+  const __half p2 = __float2half_rn(r1);
+  const __half p3 = __float2half_rn(r1 - __half2float(p2));
+  s.ops[umma_off(v, s.d, s.kpad)] = p1;
+  s.ops[umma_off(v, s.d + 1, s.kpad)] = p2;
+  s.ops[umma_off(v, s.d + 2, s.kpad)] = p3;
+}
 
 __device__ __forceinline__ void write_seeds(const TcSeeds& s, int64_t v, float cm32) {
   for (int a = 0; a < s.na; ++a) s.ipa[a * s.stride + v] = (cm32 - s.nva[a * s.stride + v]) * 0.5f;
+  if (s.ops) write_seed_parts(s, v, s.ipa[v] * s.s2);  // anchor 0 = the origin
 }
 
 // ---------------------------------------------------------------- K0: init

@@ -435,10 +435,14 @@ __global__ void k_tile_anchor(const float* __restrict__ V32, int pitch, int64_t 
 // they can never contribute (a = S + ip + ic stays hugely negative).
 __global__ void k_seed_ipa(const double* __restrict__ cm64, int64_t n, int64_t n_pad, TcSeeds seeds) {
   const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (v < n)
+  if (v < n) {
     write_seeds(seeds, v, (float)cm64[v]);
-  else if (v < n_pad)
+  } else if (v < n_pad) {
     for (int a = 0; a < seeds.na; ++a) seeds.ipa[a * seeds.stride + v] = -1e30f;
+    // MMA seeds: -2^14 / s2 <= -(max |ip|), far below any -kq (the candidate side
+    // of the origin form, ic = -|c|^2/2, is <= 0)
+    if (seeds.ops) write_seed_parts(seeds, v, -16384.f);
+  }
 }
 
 // kpmax[a][t] = max over the NP points of tile t of kp = KP (cm32 + nva_a) at
@@ -511,6 +515,9 @@ struct TcAnchors {
   float sinv2 = 1.f;
   float keta = 0.f;
   float keta2 = 0.f;  // d eta^2
+  // MS: the per-tile seed/final-add quantum kpmax is scaled by kpscale to cover
+  // the in-MMA fp32 accumulation of the seed parts ((kpad + 24) 2^-23 |ip|)
+  float kpscale = 1.f;
 };
 
 // One CTA: candidates [cand0 + 128*bx, +128) x V tiles [t0, t1) of NP points.
@@ -521,7 +528,11 @@ struct TcAnchors {
 // FLAG: work-matrix flag screen (multiset.cuh) -- candidates are the gathered
 // member rows Vc, seeds are the reset state (cm = d(., e0)), and every pair that
 // is possibly closer than e0 (a > -kq) is appended to fo instead of summed.
-template <int NP, int KIND, bool FLAG = false>
+// MS: seeds folded into the MMA (one-product FP16 kinds; TcSeeds): K columns
+// d..d+2 of the point operand hold the scaled origin seed in three FP16 parts,
+// the candidate operand holds 1 there, so the accumulator is s^2 (ip_0 + v.c)
+// and the epilogue neither loads nor adds seeds.  Origin anchor only.
+template <int NP, int KIND, bool FLAG = false, bool MS = false>
 __global__ void __launch_bounds__(tc::THREADS, 1)
     k_screen_tc(const float* __restrict__ V32, int pitch, int d, const unsigned char* __restrict__ Vhi,
                 const unsigned char* __restrict__ Vlo, TcAnchors an,
@@ -667,7 +678,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     const int cl = q * 32 + lane;
     const int64_t c = crow + cl;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    const int anc = an.tile_anchor[crow >> 7];  // anchor of this candidate block
+    const int anc = MS ? 0 : an.tile_anchor[crow >> 7];  // anchor of this candidate block
     const float* mu = an.mu + (int64_t)anc * an.apitch;
     float cn2 = 0.f, mc = 0.f, mn2 = 0.f;
     {
@@ -693,8 +704,11 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
             // KIND_F16R: fp16(oscale c'), the rounding is in the bound
             const int k = blk * 64 + 2 * i;
             const float x0 = cprime(k), x1 = cprime(k + 1);
-            rh[i] = (uint32_t)__half_as_ushort(__float2half_rn(x0 * an.oscale)) |
-                    ((uint32_t)__half_as_ushort(__float2half_rn(x1 * an.oscale)) << 16);
+            // MS: 1 in the seed columns d..d+2
+            const float y0 = (MS && k >= d && k < d + 3) ? 1.f : x0 * an.oscale;
+            const float y1 = (MS && k + 1 >= d && k + 1 < d + 3) ? 1.f : x1 * an.oscale;
+            rh[i] = (uint32_t)__half_as_ushort(__float2half_rn(y0)) |
+                    ((uint32_t)__half_as_ushort(__float2half_rn(y1)) << 16);
             rl[i] = 0u;
           } else if (BF) {
             // column = packed pair (k = 2i, 2i+1), low half = even k
@@ -737,8 +751,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       const int tt = t0 + TL(it);  // point tile
       // this slice's point seeds ip: issued before the accumulator wait so the
       // (L1-broadcast) loads overlap the MMA
-      float ipv[SW];
-      {
+      float ipv[MS ? 1 : SW];
+      if constexpr (!MS) {
         const float4* pp4 = reinterpret_cast<const float4*>(ipa + (int64_t)tt * NP + half * SLICE);
 #pragma unroll
         for (int i = 0; i < SW / 4; ++i) {
@@ -751,7 +765,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       }
       // one error quantum per tile: kpmax = max_v kp over the tile (bounds every
       // pair's kp_v; computed at reset, cm only decreases within a run)
-      const float kq = kpa[tt] + fmaf(kxc, __ldg(an.vmax + tt), kc);
+      const float kq = fmaf(kpa[tt], an.kpscale, fmaf(kxc, __ldg(an.vmax + tt), kc));
       const float thr = -kq;           // FLAG: possibly closer than e0 iff a > -kq
       const float icq = ic + kq;       // bound: a + kq = b + icq
       mbar_wait(&tfull[b], (it / NB) & 1);
@@ -765,6 +779,10 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       // adds exactly 0 to the gain and to the count, and the tile is skipped --
       // the common case (few points are closer to a candidate than to the summary).
       float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+      if constexpr (MS) {
+        // the accumulator already holds s^2 b: the max tree runs on it raw and
+        // max_i fl(S_i s^-2 + icq) = fl(max_i S_i s^-2 + icq) (exact power of two)
+      } else {
 #if EBC200_EPI_FADD2
       if (KIND == KIND_F16R) {
         // S sinv2 is exact (power of two): fl(S sinv2 + ip) in one packed FFMA2
@@ -790,13 +808,15 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
 #pragma unroll
       for (int i = 0; i < SW; ++i) S[i] += ipv[i];
 #endif
+      }
 #pragma unroll
       for (int i = 0; i < SW; i += 8) {
         m4[(i / 8) & 3] = fmaxf(m4[(i / 8) & 3], fmaxf(fmaxf(S[i], S[i + 1]), S[i + 2]));
         m4[(i / 8) & 3] = fmaxf(m4[(i / 8) & 3], fmaxf(fmaxf(S[i + 3], S[i + 4]), S[i + 5]));
         m4[(i / 8) & 3] = fmaxf(m4[(i / 8) & 3], fmaxf(S[i + 6], S[i + 7]));
       }
-      const float mb = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+      const float mb = MS ? fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * an.sinv2
+                          : fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
       if (FLAG) {
         // rare: pairs possibly closer than e0.  Warp-aggregated append: one
         // atomicAdd per warp and tile, each lane writes at its prefix offset.
@@ -838,15 +858,17 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
           float2 g2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
           const float2 icq2 = make_float2(icq, icq);
 #pragma unroll
+          const float2 sv2 = make_float2(an.sinv2, an.sinv2);
           for (int i = h; i < h + GW; i += 2) {
-            const float2 a = __fadd2_rn(make_float2(S[i], S[i + 1]), icq2);
+            const float2 a = MS ? __ffma2_rn(make_float2(S[i], S[i + 1]), sv2, icq2)
+                                : __fadd2_rn(make_float2(S[i], S[i + 1]), icq2);
             g2[(i >> 1) & 1] = __fadd2_rn(g2[(i >> 1) & 1], make_float2(fmaxf(a.x, 0.f), fmaxf(a.y, 0.f)));
           }
           g64 += (double)((g2[0].x + g2[0].y) + (g2[1].x + g2[1].y));
 #else
           float g4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-          for (int i = h; i < h + GW; ++i) g4[i & 3] += fmaxf(S[i] + icq, 0.f);
+          for (int i = h; i < h + GW; ++i) g4[i & 3] += fmaxf((MS ? S[i] * an.sinv2 : S[i]) + icq, 0.f);
           g64 += (double)((g4[0] + g4[1]) + (g4[2] + g4[3]));
 #endif
         }

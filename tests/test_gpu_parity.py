@@ -465,3 +465,30 @@ def test_fast_rung_falls_back_on_clustered_data(monkeypatch):
     assert s.selected == sel
     np.testing.assert_allclose(np.cumsum(s.gains), vals, rtol=1e-10)
     assert optimize.last_stats(f)[2] in (0, 1)
+
+
+@pytest.mark.parametrize("d", [13, 14, 29, 100])
+@pytest.mark.parametrize("prec", ["fp32", "fp16-storage"])
+def test_seeds_folded_into_the_mma_are_exact(monkeypatch, prec, d):
+    """The one-product FP16 rung with the seeds in three spare K columns (d = 13,
+    29, 100: kpad - d >= 3) or in the epilogue (d = 14: two spare columns, and
+    the EBC200_TC_MSEED=0 switch) gives the oracle's selection and bit-identical
+    exact gains either way."""
+    from paper_2105_12026_b200 import optimize
+    monkeypatch.setenv("EBC200_TC_FAST", "1")
+    monkeypatch.setenv("EBC200_SCREEN_MODE", "3")  # the tensor ladder also below d = 24
+    rng = np.random.default_rng(300 + d)
+    X = (rng.standard_normal((3000, d)) * 2.5 + 1.0).astype(np.float32 if prec == "fp32" else np.float16)
+    g = eb.GroundMatrix(X, PREC[prec])
+    sel, vals, _, _ = oracle.greedy(g.as_float64(), 6)
+    out = {}
+    for ms in ("1", "0"):
+        monkeypatch.setenv("EBC200_TC_MSEED", ms)
+        f = eb.EbcFunction(g)
+        s = eb.greedy_maximize(f, eb.OptimizerBudget(k=6))
+        assert s.selected == sel
+        np.testing.assert_allclose(np.cumsum(s.gains), vals, rtol=1e-10)
+        assert optimize.last_stats(f)[2] == (0 if prec == "fp32" else 1)
+        out[ms] = (s.selected, s.gains)
+        f.close()
+    assert out["1"] == out["0"]
