@@ -182,6 +182,8 @@ struct ebc_ctx {
   DevBuf tie_rec, tie_all;
   int* tie_err = nullptr;
   std::vector<int> eager_ks;  // k values run eagerly once (captured on the next run)
+  std::vector<int> eager_lv;  // the deepest ladder rung each of those eager runs reached
+  int ladder_max = 3;         // deepest rung enqueued (L_DIRECT except while capturing)
   int64_t alloc_epoch = 0;
   bool use_graphs = true;
   // timing / accounting
@@ -582,31 +584,41 @@ int run_screen_window(ebc_ctx* ctx, int eb, int fin_blocks) {
         KCHECK();
         ctx->cmx_fresh = true;  // this step's refine may prune with it
       }
+      // ladder_max < L_DIRECT only while capturing a graph of a run whose eager
+      // pass never went below that rung: the rungs below are not enqueued and the
+      // last enqueued rung keeps its window however wide (still exact -- the
+      // refine evaluates any window; only speed is at stake)
       if (use_fast) {
         rc = launch_tc(ctx, fp, ctx->level, L_FAST, tc::KIND_F16R);
         if (!rc) rc = run_finalize_window(ctx, fp.nsplit, (double)fp.tps * ctx->tc_np, 32, fin_blocks, 2.0,
                                           ctx->level, L_FAST, /*ub_only=*/true);
-        if (!rc) {
+        if (!rc && ctx->ladder_max > L_FAST) {
           k_adapt<<<1, 32, 0, ctx->stream>>>(ctx->wcount, ctx->maxlb, ctx->wcap_fast, ctx->level, L_FAST);
           KCHECK();
         }
       }
-      if (!rc) rc = launch_tc(ctx, tp, ctx->level, L_TC, ctx->tc_kind);
-      if (!rc) rc = run_finalize_window(ctx, tp.nsplit, (double)tp.tps * ctx->tc_np, 32, fin_blocks, 2.0,
-                                        ctx->level, L_TC, /*ub_only=*/true);
-      if (!rc) {
-        k_adapt<<<1, 32, 0, ctx->stream>>>(ctx->wcount, ctx->maxlb, ctx->wcap, ctx->level, L_TC);
+      if (ctx->ladder_max >= L_TC) {
+        if (!rc) rc = launch_tc(ctx, tp, ctx->level, L_TC, ctx->tc_kind);
+        if (!rc) rc = run_finalize_window(ctx, tp.nsplit, (double)tp.tps * ctx->tc_np, 32, fin_blocks, 2.0,
+                                          ctx->level, L_TC, /*ub_only=*/true);
+        if (!rc && ctx->ladder_max > L_TC) {
+          k_adapt<<<1, 32, 0, ctx->stream>>>(ctx->wcount, ctx->maxlb, ctx->wcap, ctx->level, L_TC);
+          KCHECK();
+        }
+      }
+    }
+    if (ctx->ladder_max >= L_GRAM) {
+      if (!rc) rc = launch_screen<1>(ctx, p, ctx->level, L_GRAM);
+      if (!rc) rc = run_finalize_window(ctx, p.nsplit, nterms_ffma, p.tp, fin_blocks, 2.0, ctx->level, L_GRAM);
+      if (!rc && ctx->ladder_max > L_GRAM) {
+        k_adapt<<<1, 32, 0, ctx->stream>>>(ctx->wcount, ctx->maxlb, ctx->wcap, ctx->level, L_GRAM);
         KCHECK();
       }
     }
-    if (!rc) rc = launch_screen<1>(ctx, p, ctx->level, L_GRAM);
-    if (!rc) rc = run_finalize_window(ctx, p.nsplit, nterms_ffma, p.tp, fin_blocks, 2.0, ctx->level, L_GRAM);
-    if (!rc) {
-      k_adapt<<<1, 32, 0, ctx->stream>>>(ctx->wcount, ctx->maxlb, ctx->wcap, ctx->level, L_GRAM);
-      KCHECK();
-      rc = launch_screen<0>(ctx, p, ctx->level, L_DIRECT);
+    if (ctx->ladder_max >= L_DIRECT) {
+      if (!rc) rc = launch_screen<0>(ctx, p, ctx->level, L_DIRECT);
+      if (!rc) rc = run_finalize_window(ctx, p.nsplit, nterms_ffma, p.tp, fin_blocks, 1.0, ctx->level, L_DIRECT);
     }
-    if (!rc) rc = run_finalize_window(ctx, p.nsplit, nterms_ffma, p.tp, fin_blocks, 1.0, ctx->level, L_DIRECT);
   }
   if (rc) return rc;
   if (ctx->timing) CU(cudaEventRecord(ctx->ev[eb + 1], ctx->stream));
@@ -1407,7 +1419,12 @@ int greedy_run(ebc_ctx* ctx, int32_t k, bool sharded, int64_t* out_sel, double* 
     bool ok = cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
     const int64_t epoch = ctx->alloc_epoch;
     if (ok) {
+      // a Greedy run is a deterministic function of (V, e0, k): replays take the
+      // eager run's path down the ladder, so the graph holds only those rungs
+      const size_t ki = (size_t)(std::find(ctx->eager_ks.begin(), ctx->eager_ks.end(), key) - ctx->eager_ks.begin());
+      ctx->ladder_max = ki < ctx->eager_lv.size() ? std::max(0, std::min(3, ctx->eager_lv[ki])) : 3;
       const int crc = enqueue();
+      ctx->ladder_max = 3;
       ok = cudaStreamEndCapture(ctx->stream, &graph) == cudaSuccess && crc == EBC_OK && epoch == ctx->alloc_epoch;
     }
     if (ok) ok = cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess;
@@ -1434,8 +1451,10 @@ int greedy_run(ebc_ctx* ctx, int32_t k, bool sharded, int64_t* out_sel, double* 
   } else {
     rc = enqueue();
     if (rc) return rc;
-    if (!seen) ctx->eager_ks.push_back(key);
   }
+  long long lv_end = 3;
+  if (!(graph_ok && cached) && !seen)
+    CU(cudaMemcpyAsync(&lv_end, ctx->stats + 2, sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaEventRecord(tend, ctx->stream));
   CU(cudaMemcpyAsync(out_sel, ctx->sel_out.p, (size_t)k * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaMemcpyAsync(out_val, ctx->val_out.p, (size_t)k * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
@@ -1443,6 +1462,10 @@ int greedy_run(ebc_ctx* ctx, int32_t k, bool sharded, int64_t* out_sel, double* 
   int tie_err = 0;
   if (sharded) CU(cudaMemcpyAsync(&tie_err, ctx->tie_err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
+  if (!(graph_ok && cached) && !seen) {
+    ctx->eager_ks.push_back(key);
+    ctx->eager_lv.push_back(lv_end < 0 ? 3 : (int)lv_end);
+  }
   if (tie_err)
     return fail(ctx, EBC_ECOMM, "sharded Greedy: a rank's tie set exceeded " + std::to_string(TIE_CAP) +
                                     " records (use the host exchange)");
