@@ -149,7 +149,7 @@ struct ebc_ctx {
   unsigned int* counter = nullptr;
   unsigned int* counter2 = nullptr;  // k_gain_top's last-block ticket
   int64_t* topc = nullptr;           // candidate with the largest screen bound (ub-only screens)
-  double* toppart = nullptr;         // nchunks: its exact gain's chunk partials
+  double* toppart = nullptr;         // 4 nchunks: its exact gain's partials (argmax scratch before)
   double* terms = nullptr;           // n: e0d - cm64 per point (split K4)
   double* cur = nullptr;
   int64_t* best = nullptr;
@@ -388,17 +388,21 @@ int run_finalize_window(ebc_ctx* ctx, int nsplit, double nterms, int gterms, int
   KCHECK();
   if (ub_only) {
     // window threshold = exact gain of the candidate with the largest bound
-    k_argmax_ub<<<1, 1024, 0, ctx->stream>>>(ctx->c0, ctx->c1, ctx->ub, ctx->topc, level_now, level);
+    // grid <= ceil(ncand / 1024) <= nchunks: its (value, index) partials fit the
+    // 4 nchunks doubles of toppart, which k_gain_top overwrites afterwards
+    const int ag = (int)std::max<int64_t>(1, std::min<int64_t>(2 * ctx->num_sms, (ctx->c1 - ctx->c0 + 1023) / 1024));
+    k_argmax_ub<<<ag, 256, 0, ctx->stream>>>(ctx->c0, ctx->c1, ctx->ub, ctx->topc, ctx->toppart, ctx->counter2,
+                                            level_now, level);
     KCHECK();
     const size_t smem = (size_t)ctx->d * sizeof(double);
     if (ctx->dtype == EBC_F64) {
       CU(cudaFuncSetAttribute(k_gain_top<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024));
-      k_gain_top<double><<<ctx->nchunks, RED_THREADS, smem, ctx->stream>>>(
+      k_gain_top<double><<<(unsigned)((ctx->n + RED_THREADS - 1) / RED_THREADS), RED_THREADS, smem, ctx->stream>>>(
           ctx->V64, ctx->pitch, ctx->n, ctx->d, ctx->cm64, ctx->topc, ctx->toppart, ctx->counter2, ctx->maxlb,
           level_now, level);
     } else {
       CU(cudaFuncSetAttribute(k_gain_top<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024));
-      k_gain_top<float><<<ctx->nchunks, RED_THREADS, smem, ctx->stream>>>(
+      k_gain_top<float><<<(unsigned)((ctx->n + RED_THREADS - 1) / RED_THREADS), RED_THREADS, smem, ctx->stream>>>(
           ctx->V32, ctx->pitch, ctx->n, ctx->d, ctx->cm64, ctx->topc, ctx->toppart, ctx->counter2, ctx->maxlb,
           level_now, level);
     }
@@ -1147,7 +1151,7 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
   CUC(cudaMallocAsync((void**)&ctx->counter2, sizeof(unsigned int), ctx->stream));
   CUC(cudaMemsetAsync(ctx->counter2, 0, sizeof(unsigned int), ctx->stream));
   CUC(cudaMallocAsync((void**)&ctx->topc, sizeof(int64_t), ctx->stream));
-  CUC(cudaMallocAsync((void**)&ctx->toppart, (size_t)ctx->nchunks * sizeof(double), ctx->stream));
+  CUC(cudaMallocAsync((void**)&ctx->toppart, (size_t)ctx->nchunks * 4 * sizeof(double), ctx->stream));
   CUC(cudaMallocAsync((void**)&ctx->terms, (size_t)ctx->n_pad * sizeof(double), ctx->stream));
   CUC(cudaMallocAsync((void**)&ctx->cur, sizeof(double), ctx->stream));
   CUC(cudaMemsetAsync(ctx->cur, 0, sizeof(double), ctx->stream));

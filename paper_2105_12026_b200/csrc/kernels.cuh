@@ -687,36 +687,70 @@ __global__ void k_finalize(int64_t c0, int64_t c1, int nsplit, const double* __r
 // threshold is the EXACT gain of the candidate with the largest bound, which is
 // a valid lower bound on the top gain.  Step 1: that candidate (lowest index
 // among equal bounds).
-__global__ void __launch_bounds__(1024) k_argmax_ub(int64_t c0, int64_t c1, const double* __restrict__ ub,
-                                                    int64_t* __restrict__ topc, const int* __restrict__ level_now,
-                                                    int level) {
+__device__ __forceinline__ bool ub_better(double v, long long i, double bv, long long bi) {
+  return v > bv || (v == bv && i < bi);
+}
+
+// Grid-wide: every block reduces a strided share of the candidates to its
+// (largest bound, lowest index) pair in part/pidx, the last block to finish
+// reduces those (any order gives the same pair: the comparison is a total order).
+__global__ void __launch_bounds__(256) k_argmax_ub(int64_t c0, int64_t c1, const double* __restrict__ ub,
+                                                   int64_t* __restrict__ topc, double* __restrict__ part,
+                                                   unsigned int* __restrict__ counter,
+                                                   const int* __restrict__ level_now, int level) {
   if (level_now && *level_now != level) return;
-  __shared__ double sv[1024];
-  __shared__ long long si[1024];
+  __shared__ double sv[256];
+  __shared__ long long si[256];
+  __shared__ bool last;
+  long long* pidx = reinterpret_cast<long long*>(part + gridDim.x);
   double bv = -INFINITY;
   long long bi = LLONG_MAX;
-  for (int64_t c = c0 + threadIdx.x; c < c1; c += blockDim.x) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < c1; c += stride) {
     const double u = ub[c - c0];
     if (u > bv) {  // ascending c per thread: the first maximum is the lowest index
       bv = u;
       bi = c;
     }
   }
-  sv[threadIdx.x] = bv;
-  si[threadIdx.x] = bi;
-  __syncthreads();
-  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s) {
-      const double ov = sv[threadIdx.x + s];
-      const long long oi = si[threadIdx.x + s];
-      if (ov > sv[threadIdx.x] || (ov == sv[threadIdx.x] && oi < si[threadIdx.x])) {
-        sv[threadIdx.x] = ov;
-        si[threadIdx.x] = oi;
-      }
-    }
+  auto block_reduce = [&]() {
+    sv[threadIdx.x] = bv;
+    si[threadIdx.x] = bi;
     __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+      if (threadIdx.x < s && ub_better(sv[threadIdx.x + s], si[threadIdx.x + s], sv[threadIdx.x], si[threadIdx.x])) {
+        sv[threadIdx.x] = sv[threadIdx.x + s];
+        si[threadIdx.x] = si[threadIdx.x + s];
+      }
+      __syncthreads();
+    }
+  };
+  block_reduce();
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = sv[0];
+    pidx[blockIdx.x] = si[0];
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
   }
-  if (threadIdx.x == 0) *topc = (sv[0] > -INFINITY) ? si[0] : -1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  bv = -INFINITY;
+  bi = LLONG_MAX;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+    const double v = __ldcg(part + b);
+    const long long i = __ldcg(pidx + b);
+    if (ub_better(v, i, bv, bi)) {
+      bv = v;
+      bi = i;
+    }
+  }
+  __syncthreads();
+  block_reduce();
+  if (threadIdx.x == 0) {
+    *topc = (sv[0] > -INFINITY) ? si[0] : -1;
+    *counter = 0u;
+  }
 }
 
 // Step 2: exact fp64 gain of topc, sum_v max(0, cm(v) - d64(v, c)) in chunk
@@ -737,18 +771,13 @@ __global__ void __launch_bounds__(RED_THREADS) k_gain_top(const T* __restrict__ 
     for (int k = threadIdx.x; k < d; k += blockDim.x) cd[k] = (double)V[s * pitch + k];
   __syncthreads();
   double acc = 0.0;
-  static_assert(RCH / RED_THREADS == 4 && RED_THREADS == 256, "dist64_rows4 layout");
   if (s >= 0) {
-    const int64_t v0 = (int64_t)blockIdx.x * RCH + threadIdx.x;
-    double dd[4];
-    if (v0 < n) dist64_rows4(V, pitch, v0, n, cd, d, dd);
-#pragma unroll
-    for (int i = 0; i < RCH / RED_THREADS; ++i) {
-      const int64_t v = v0 + (int64_t)i * RED_THREADS;
-      if (v < n) {
-        const double t = cm64[v] - dd[i];
-        acc += t > 0.0 ? t : 0.0;
-      }
+    // one point per thread, RED_THREADS points per block (a threshold, not a
+    // reported value: its summation structure is free, only deterministic)
+    const int64_t v = (int64_t)blockIdx.x * RED_THREADS + threadIdx.x;
+    if (v < n) {
+      const double t = cm64[v] - dist64_row(V + v * pitch, cd, d);
+      acc = t > 0.0 ? t : 0.0;
     }
   }
   const double bs = block_sum_256(acc, sbuf);
@@ -929,10 +958,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_refine(const T* __restrict__ V,
 #pragma unroll
           for (int j = 0; j < RW; ++j) s[i][j] = 0.0;
         }
-        for (int k = 0; k < d; ++k) {
-          double x[4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) x[i] = (double)row[i][k];
+        auto step = [&](int k, const double (&x)[4]) {
 #pragma unroll
           for (int j = 0; j < RW; ++j) {
             if (lm >> j & 1u) {
@@ -944,6 +970,35 @@ __global__ void __launch_bounds__(RED_THREADS) k_refine(const T* __restrict__ V,
               }
             }
           }
+        };
+        int k = 0;
+        if constexpr (sizeof(T) == 4) {
+          // fp32 rows are 16-byte aligned (pitch % 4 == 0): one LDG.128 per row
+          // and 4 dims, the four rows' loads in flight together
+          for (; k + 4 <= d; k += 4) {
+            float4 q[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) q[i] = __ldg(reinterpret_cast<const float4*>(row[i]) + (k >> 2));
+            double x[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) x[i] = (double)q[i].x;
+            step(k, x);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) x[i] = (double)q[i].y;
+            step(k + 1, x);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) x[i] = (double)q[i].z;
+            step(k + 2, x);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) x[i] = (double)q[i].w;
+            step(k + 3, x);
+          }
+        }
+        for (; k < d; ++k) {
+          double x[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) x[i] = (double)row[i][k];
+          step(k, x);
         }
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
