@@ -123,6 +123,14 @@ struct ebc_ctx {
   bool tc_mseed = false;
   float tc_kpscale = 1.f;
   int* tile_anchor0 = nullptr;  // all-zero block anchors (the origin) for rung 0 with folded seeds
+  // all-positive (block, tile) pairs of rung 1 summed from tile aggregates (k_screen_agg)
+  bool tc_agg = false;
+  float* rhomax = nullptr;  // na x tc_ntl: max |v - mu_a| over the tile
+  float* cmn = nullptr;     // tc_ntl: min cm over the tile (current step)
+  float* vsum = nullptr;    // tc_ntl x pitch: sum of the tile's points
+  float* vsn = nullptr;     // tc_ntl: |vsum|
+  double* ipsum = nullptr;  // na x tc_ntl: sum of the tile's seeds (current step)
+  DevBuf part_a;            // nsplit x n_pad aggregate partials
   int wcap_fast = 256;
   float* pttc = nullptr;   // na x n_pad seeds ip_a(v) = (cm32 - |v - mu_a|^2)/2
   float* kpmax = nullptr;  // na x tc_ntl: per (anchor, point tile) max error quantum kp (reset state)
@@ -378,13 +386,14 @@ int run_window_all(ebc_ctx* ctx, int eb, int fin_blocks) {
 // accumulators hold t/2).  nterms bounds the terms of one fp32 error
 // accumulator; gterms the fp32 terms summed before each fp64 fold.
 int run_finalize_window(ebc_ctx* ctx, int nsplit, double nterms, int gterms, int fin_blocks, double gscale,
-                        const int* level_now, int level, bool ub_only = false) {
+                        const int* level_now, int level, bool ub_only = false, const double* part_a = nullptr) {
   const double u = 5.960464477539063e-08;
   const double einfl = 1.0 + 2.0 * (nterms + 64.0) * u + 1.0 / 64.0;
   const double gcoef = (gterms + 8) * u;
   k_finalize<<<fin_blocks, 256, 0, ctx->stream>>>(ctx->c0, ctx->c1, nsplit, (double*)ctx->part_g.p,
                                                  (float*)ctx->part_e.p, ctx->n_pad, einfl, gcoef, gscale,
-                                                 ctx->selected, ctx->ub, ctx->maxlb, level_now, level, ub_only ? 1 : 0);
+                                                 ctx->selected, ctx->ub, ctx->maxlb, level_now, level, ub_only ? 1 : 0,
+                                                 part_a);
   KCHECK();
   if (ub_only) {
     // window threshold = exact gain of the candidate with the largest bound
@@ -480,6 +489,10 @@ int launch_tc_t(ebc_ctx* ctx, const TcPlan& p, const int* level_now, int level) 
                ctx->kpmax, ctx->tc_ntl, ctx->tc_vmax, ctx->tc_kc, fast ? ctx->tc_kx_fast : ctx->tc_kx,
                (p.list_cap && !origin_only) ? ctx->rho : nullptr, ctx->tile_rad, ctx->cmx, p.list_cap,
                (unsigned long long*)(ctx->stats + 4)};
+  if (!one && ctx->tc_agg && p.list_cap) {
+    an.rhomax = ctx->rhomax;
+    an.cmn = ctx->cmn;
+  }
   if (ms) {
     an.kpscale = ctx->tc_kpscale;
     an.keta2 = (float)std::ldexp(1.0, -24);  // seed split residual (fp16 subnormal), unscaled operands
@@ -548,6 +561,33 @@ int launch_tc(ebc_ctx* ctx, const TcPlan& p, const int* level_now, int level, in
   }
 }
 
+// All-positive (block, tile) pairs of rung 1 from tile aggregates (same plan and
+// anchors as the rung-1 screen launch).
+int launch_tc_agg(ebc_ctx* ctx, const TcPlan& p) {
+  TcAnchors an{ctx->anchors, ctx->pitch, ctx->tile_anchor, ctx->pttc, ctx->n_pad, ctx->kpmax, ctx->tc_ntl,
+               ctx->tc_vmax, ctx->tc_kc, ctx->tc_kx, ctx->rho, ctx->tile_rad, ctx->cmx, p.list_cap, nullptr};
+  an.rhomax = ctx->rhomax;
+  an.cmn = ctx->cmn;
+  // c' in 32 registers when it fits (padded dims of vsum are zero), else in smem;
+  // the all-positive tile list (uint16 per tile of the split) follows
+  const bool regs = ctx->d <= 32;  // reads 32 floats per vsum row: zeros times c' past d (32-float tail pad)
+  const size_t smem = (regs ? 0 : (size_t)ctx->d * 128 * sizeof(float)) + ((size_t)p.tps * 2 + 16);
+  dim3 grid(p.ncb, p.nsplit);
+  if (regs) {
+    CU(cudaFuncSetAttribute(k_screen_agg<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_screen_agg<32><<<grid, 128, smem, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->d, an, ctx->c0, p.ntiles, p.tps,
+                                                       ctx->tc_np, ctx->n, ctx->ipsum, ctx->vsum, ctx->vsn,
+                                                       (double*)ctx->part_a.p, ctx->n_pad, ctx->level, L_TC);
+  } else {
+    CU(cudaFuncSetAttribute(k_screen_agg<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_screen_agg<0><<<grid, 128, smem, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->d, an, ctx->c0, p.ntiles, p.tps,
+                                                      ctx->tc_np, ctx->n, ctx->ipsum, ctx->vsum, ctx->vsn,
+                                                      (double*)ctx->part_a.p, ctx->n_pad, ctx->level, L_TC);
+  }
+  KCHECK();
+  return EBC_OK;
+}
+
 // fp32 screen of the candidate range + certified window.
 // Modes: 0 direct form; 1 FFMA Gram form (v.c on the FMA pipe); 2 adaptive
 // ladder FFMA Gram -> direct; 3 adaptive ladder tensor-core Gram -> FFMA Gram
@@ -581,12 +621,20 @@ int run_screen_window(ebc_ctx* ctx, int eb, int fin_blocks) {
     if (!rc) rc = run_finalize_window(ctx, p.nsplit, nterms_ffma, p.tp, fin_blocks, 2.0, nullptr, 0);
   } else {
     if (use_tc) {
+      const bool agg = ctx->tc_agg && tp.list_cap && ctx->ladder_max >= L_TC;
       if (tp.list_cap || fp.list_cap || refine_prune_on(ctx)) {
-        k_tile_cmmax<<<(unsigned)((ctx->tc_ntl * 32 + 255) / 256), 256, 0, ctx->stream>>>(ctx->cm64, ctx->n,
-                                                                                          ctx->tc_ntl, ctx->tc_np,
-                                                                                          ctx->cmx);
+        k_tile_cmmax<<<(unsigned)((ctx->tc_ntl * 32 + 255) / 256), 256, 0, ctx->stream>>>(
+            ctx->cm64, ctx->n, ctx->tc_ntl, ctx->tc_np, ctx->cmx, agg ? ctx->cmn : nullptr);
         KCHECK();
         ctx->cmx_fresh = true;  // this step's refine may prune with it
+      }
+      if (agg) {
+        rc = ensure(ctx, ctx->part_a, (size_t)tp.nsplit * ctx->n_pad * sizeof(double));
+        if (rc) return rc;
+        const int64_t cells = (int64_t)ctx->tc_na * ctx->tc_ntl;
+        k_tile_ipsum<<<(unsigned)((cells * 32 + 255) / 256), 256, 0, ctx->stream>>>(
+            ctx->pttc, ctx->n_pad, ctx->tc_na, ctx->n, ctx->tc_ntl, ctx->tc_np, ctx->ipsum);
+        KCHECK();
       }
       // ladder_max < L_DIRECT only while capturing a graph of a run whose eager
       // pass never went below that rung: the rungs below are not enqueued and the
@@ -603,8 +651,9 @@ int run_screen_window(ebc_ctx* ctx, int eb, int fin_blocks) {
       }
       if (ctx->ladder_max >= L_TC) {
         if (!rc) rc = launch_tc(ctx, tp, ctx->level, L_TC, ctx->tc_kind);
+        if (!rc && agg) rc = launch_tc_agg(ctx, tp);
         if (!rc) rc = run_finalize_window(ctx, tp.nsplit, (double)tp.tps * ctx->tc_np, 32, fin_blocks, 2.0,
-                                          ctx->level, L_TC, /*ub_only=*/true);
+                                          ctx->level, L_TC, /*ub_only=*/true, agg ? (double*)ctx->part_a.p : nullptr);
         if (!rc && ctx->ladder_max > L_TC) {
           k_adapt<<<1, 32, 0, ctx->stream>>>(ctx->wcount, ctx->maxlb, ctx->wcap, ctx->level, L_TC);
           KCHECK();
@@ -798,11 +847,11 @@ int do_reset(ebc_ctx* ctx) {
 void free_ctx(ebc_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
-  void* ptrs[] = {c->V32, c->V64, c->e0d, c->cm64, c->pt, c->nv32, c->level, c->stats, c->Vhi, c->Vlo, c->Vf, c->tile_anchor0, c->pttc, c->kpmax, c->anchors, c->nva, c->tile_anchor, c->tc_vmax, c->fps_keys, c->ipa0, c->tile_rad, c->rho, c->cmx, c->cmx0, c->selected, c->chunkpart, c->counter, c->counter2, c->topc, c->toppart, c->terms, c->cur, c->best,
+  void* ptrs[] = {c->V32, c->V64, c->e0d, c->cm64, c->pt, c->nv32, c->level, c->stats, c->Vhi, c->Vlo, c->Vf, c->tile_anchor0, c->rhomax, c->cmn, c->vsum, c->vsn, c->ipsum, c->pttc, c->kpmax, c->anchors, c->nva, c->tile_anchor, c->tc_vmax, c->fps_keys, c->ipa0, c->tile_rad, c->rho, c->cmx, c->cmx0, c->selected, c->chunkpart, c->counter, c->counter2, c->topc, c->toppart, c->terms, c->cur, c->best,
                   c->maxlb, c->wcount, c->wlist, c->wgain, c->ub};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, c->stream);
-  DevBuf* bufs[] = {&c->tie_rec, &c->tie_all, &c->ms_tanchor, &c->ms_trad, &c->part_g, &c->part_e, &c->part_r, &c->sel_out, &c->val_out, &c->gain_out, &c->ms_part,
+  DevBuf* bufs[] = {&c->tie_rec, &c->tie_all, &c->ms_tanchor, &c->ms_trad, &c->part_g, &c->part_e, &c->part_a, &c->part_r, &c->sel_out, &c->val_out, &c->gain_out, &c->ms_part,
                     &c->ms_off, &c->ms_idx, &c->ms_out, &c->ms_mbuf, &c->ms_setof, &c->ms_pairs, &c->ms_keys,
                     &c->ms_vals, &c->ms_keys2, &c->ms_vals2, &c->ms_ukeys, &c->ms_uvals, &c->ms_cub};
   void* more[] = {c->pt0, c->ms_count, c->ms_nruns};
@@ -1138,6 +1187,19 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
       CUC(cudaMallocAsync((void**)&ctx->tile_rad, (size_t)(ctx->n_pad / 128 + 1) * sizeof(float), ctx->stream));
       CUC(cudaMemsetAsync(ctx->tile_rad, 0, (size_t)(ctx->n_pad / 128 + 1) * sizeof(float), ctx->stream));
       CUC(cudaMallocAsync((void**)&ctx->rho, (size_t)ctx->tc_na * ctx->tc_ntl * sizeof(float), ctx->stream));
+      {
+        const char* ag_env = getenv("EBC200_TC_AGG");
+        ctx->tc_agg = ctx->tc_prune && ctx->tc_kind != tc::KIND_F16 && ctx->tc_na > 1 && d <= 128 &&
+                      !(ag_env && ag_env[0] == '0');
+      }
+      if (ctx->tc_agg) {
+        CUC(cudaMallocAsync((void**)&ctx->rhomax, (size_t)ctx->tc_na * ctx->tc_ntl * sizeof(float), ctx->stream));
+        CUC(cudaMallocAsync((void**)&ctx->cmn, (size_t)ctx->tc_ntl * sizeof(float), ctx->stream));
+        CUC(cudaMallocAsync((void**)&ctx->vsum, ((size_t)ctx->tc_ntl * ctx->pitch + 32) * sizeof(float), ctx->stream));
+        CUC(cudaMemsetAsync(ctx->vsum + (size_t)ctx->tc_ntl * ctx->pitch, 0, 32 * sizeof(float), ctx->stream));
+        CUC(cudaMallocAsync((void**)&ctx->vsn, (size_t)ctx->tc_ntl * sizeof(float), ctx->stream));
+        CUC(cudaMallocAsync((void**)&ctx->ipsum, (size_t)ctx->tc_na * ctx->tc_ntl * sizeof(double), ctx->stream));
+      }
       CUC(cudaMallocAsync((void**)&ctx->cmx, (size_t)ctx->tc_ntl * sizeof(float), ctx->stream));
       CUC(cudaMallocAsync((void**)&ctx->cmx0, (size_t)ctx->tc_ntl * sizeof(float), ctx->stream));
       CUC(cudaMemsetAsync(ctx->fps_keys, 0, (size_t)(ctx->tc_na + 1) * sizeof(unsigned long long), ctx->stream));
@@ -1205,7 +1267,11 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
       const int64_t cells = (int64_t)ctx->tc_na * ctx->tc_ntl;
       k_tile_kpmax<<<(unsigned)((cells + 255) / 256), 256, 0, ctx->stream>>>(
           ctx->e0d, ctx->nv32, ctx->nva, ctx->n_pad, ctx->tc_na, n, ctx->tc_ntl, ctx->tc_np, ctx->tc_kp, ctx->kpmax,
-          ctx->tc_vmax, ctx->rho);
+          ctx->tc_vmax, ctx->rho, ctx->rhomax);
+      CUC(cudaGetLastError());
+      if (ctx->tc_agg)
+        k_tile_vsum<<<(unsigned)ctx->tc_ntl, 128, 0, ctx->stream>>>(ctx->V32, ctx->pitch, n, d, ctx->tc_np, ctx->vsum,
+                                                                   ctx->vsn);
       CUC(cudaGetLastError());
       k_tile_cmmax<<<(unsigned)((ctx->tc_ntl * 32 + 255) / 256), 256, 0, ctx->stream>>>(ctx->e0d, n, ctx->tc_ntl,
                                                                                         ctx->tc_np, ctx->cmx0);

@@ -652,7 +652,7 @@ __global__ void k_finalize(int64_t c0, int64_t c1, int nsplit, const double* __r
                            const float* __restrict__ part_e, int64_t part_stride, double einfl, double gcoef,
                            double gscale, const unsigned char* __restrict__ selected, double* __restrict__ ub,
                            long long* __restrict__ maxlb, const int* __restrict__ level_now, int level,
-                           int ub_only = 0) {
+                           int ub_only = 0, const double* __restrict__ part_a = nullptr) {
   if (level_now && *level_now != level) return;
   __shared__ long long smax[256];
   const int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -665,7 +665,14 @@ __global__ void k_finalize(int64_t c0, int64_t c1, int nsplit, const double* __r
     }
     g *= gscale;
     e *= gscale;
-    const double eps = e * einfl + gcoef * g + 1e-300;
+    double eps = e * einfl + gcoef * g + 1e-300;
+    if (part_a) {  // all-positive tiles (k_screen_agg): certified upper bounds already
+      double ga = 0.0;
+      for (int s = 0; s < nsplit; ++s) ga += part_a[s * part_stride + c];
+      ga *= gscale;
+      g += ga;
+      eps += 1e-12 * fabs(ga);
+    }
     if (selected[c]) {
       ub[c - c0] = -INFINITY;
     } else {

@@ -451,12 +451,12 @@ __global__ void k_seed_ipa(const double* __restrict__ cm64, int64_t n, int64_t n
 __global__ void k_tile_kpmax(const double* __restrict__ e0d, const float* __restrict__ nv32,
                              const float* __restrict__ nva, int64_t stride, int na, int64_t n, int64_t ntiles,
                              int np, float kp_coef, float* __restrict__ kpmax, float* __restrict__ vmax,
-                             float* __restrict__ rho) {
+                             float* __restrict__ rho, float* __restrict__ rhomax = nullptr) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (int64_t)na * ntiles) return;
   const int a = (int)(i / ntiles);
   const int64_t t = i - (int64_t)a * ntiles;
-  float m = 0.f, vm = 0.f, rm = INFINITY;
+  float m = 0.f, vm = 0.f, rm = INFINITY, rx = 0.f;
   for (int j = 0; j < np; ++j) {
     const int64_t v = t * np + j;
     if (v < n) {
@@ -464,8 +464,11 @@ __global__ void k_tile_kpmax(const double* __restrict__ e0d, const float* __rest
       m = fmaxf(m, kp_coef * ((float)e0d[v] + q));
       vm = fmaxf(vm, nv32[v]);
       rm = fminf(rm, q);
+      rx = fmaxf(rx, q);
     }
   }
+  // rhomax = max_v |v - mu_a| rounded up (all-positive tile test, k_screen_agg)
+  if (rhomax) rhomax[a * ntiles + t] = sqrtf(rx) * (1.f + 1e-5f) + 1e-30f;
   kpmax[a * ntiles + t] = m * (1.f + 1e-6f);
   if (a == 0) vmax[t] = sqrtf(vm) * (1.f + 1e-5f);
   // rho = min_v |v - mu_a| rounded down (nva is the fp64 value rounded to fp32)
@@ -474,17 +477,86 @@ __global__ void k_tile_kpmax(const double* __restrict__ e0d, const float* __rest
 
 // cmx[t] = max over the tile's points of the cached minimum (rounded up).
 __global__ void k_tile_cmmax(const double* __restrict__ cm64, int64_t n, int64_t ntiles, int np,
-                             float* __restrict__ cmx) {
+                             float* __restrict__ cmx, float* __restrict__ cmn = nullptr) {
   const int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (t >= ntiles) return;
-  double m = 0.0;
+  double m = 0.0, mn = INFINITY;
   for (int j = lane; j < np; j += 32) {
     const int64_t v = t * np + j;
-    if (v < n) m = fmax(m, cm64[v]);
+    if (v < n) {
+      m = fmax(m, cm64[v]);
+      mn = fmin(mn, cm64[v]);
+    }
   }
-  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffff, m, o));
-  if (lane == 0) cmx[t] = __double2float_ru(m);
+  for (int o = 16; o > 0; o >>= 1) {
+    m = fmax(m, __shfl_xor_sync(0xffffffff, m, o));
+    mn = fmin(mn, __shfl_xor_sync(0xffffffff, mn, o));
+  }
+  if (lane == 0) {
+    cmx[t] = __double2float_ru(m);
+    if (cmn) cmn[t] = __double2float_rd(mn);  // min cm over the tile, rounded down
+  }
+}
+
+// ---------------------------------------------------------------- all-positive tiles
+// A (candidate block, point tile) pair whose every pair is certified to have
+// d(v, c) < cm(v) -- (max_v |v - mu| + max_c |c - mu|)^2 < min_v cm(v), the
+// triangle inequality through the block's anchor -- has max(0, a) = a for every
+// pair, so its contribution to the gain is the LINEAR sum
+//   sum_v a_v = sum_v ip_mu(v) + c'.(sum_v v) + n_t ic
+// computed from per-tile aggregates (k_screen_agg) instead of 128 x 128 MMA
+// terms.  Early Greedy steps on clustered data (C4) are dominated by such
+// tiles: at step 0 cm = |v|^2 exceeds every inter-regime distance.
+__device__ __forceinline__ bool tile_allpos(float rhomax, float rad, float cmn) {
+  const float r = __fadd_ru(rhomax, rad);
+  return __fmul_ru(__fmul_ru(r, r), 1.00001f) < cmn;
+}
+
+// vsum[t][k] = sum of the tile's (real) points, fp64 accumulation rounded to
+// fp32; vsn[t] = |vsum[t]| rounded up.  One block per tile.
+__global__ void k_tile_vsum(const float* __restrict__ V32, int pitch, int64_t n, int d, int np,
+                            float* __restrict__ vsum, float* __restrict__ vsn) {
+  __shared__ double nrm[32];
+  const int64_t t = blockIdx.x;
+  double q = 0.0;
+  for (int k = threadIdx.x; k < pitch; k += blockDim.x) {
+    double acc = 0.0;
+    if (k < d)
+      for (int j = 0; j < np; ++j) {
+        const int64_t v = t * np + j;
+        if (v < n) acc += (double)V32[v * pitch + k];
+      }
+    const float f = (float)acc;
+    vsum[t * pitch + k] = f;
+    q += (double)f * (double)f;
+  }
+  for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffff, q, o);
+  if ((threadIdx.x & 31) == 0) nrm[threadIdx.x >> 5] = q;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += nrm[w];
+    vsn[t] = (float)(sqrt(tot) * (1.0 + 1e-6)) + 1e-30f;
+  }
+}
+
+// ipsum[a][t] = sum over the tile's real points of the fp32 seeds ip_a(v) (fp64,
+// fixed order).  One warp per (anchor, tile).
+__global__ void k_tile_ipsum(const float* __restrict__ ipa, int64_t stride, int na, int64_t n, int64_t ntiles,
+                             int np, double* __restrict__ ipsum) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= (int64_t)na * ntiles) return;
+  const int a = (int)(w / ntiles);
+  const int64_t t = w - (int64_t)a * ntiles;
+  double s = 0.0;
+  for (int j = lane; j < np; j += 32) {
+    const int64_t v = t * np + j;
+    if (v < n) s += (double)ipa[a * stride + v];
+  }
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffff, s, o);
+  if (lane == 0) ipsum[w] = s;
 }
 
 // tile_prunable (kernels.cuh): the certified tile-pair test shared with k_refine.
@@ -508,6 +580,10 @@ struct TcAnchors {
   const float* cmx;
   int list_cap;             // uint16 entries reserved for the kept-tile list
   unsigned long long* work; // if set: += executed (candidate block, point tile) pairs
+  // all-positive tiles handled by k_screen_agg (nullptr: off): rhomax[a][t] =
+  // max_v |v - mu_a|, cmn[t] = min cm over the tile (current step)
+  const float* rhomax = nullptr;
+  const float* cmn = nullptr;
   // KIND_F16R: operands are fp16(oscale * x), the accumulator holds oscale^2 v.c';
   // keta = sqrt(d) x (fp16 subnormal half-spacing 2^-25) / oscale x 1.02, the
   // absolute underflow term of the operand rounding (per |c'| and per |v|max)
@@ -597,7 +673,9 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     int base = 0;
     for (int c0i = 0; c0i < nt; c0i += THREADS) {
       const int i = c0i + tid;
-      const bool keep = i < nt && !tile_prunable(rho[t0 + i], rad, an.cmx[t0 + i]);
+      bool keep = i < nt && !tile_prunable(rho[t0 + i], rad, an.cmx[t0 + i]);
+      if (keep && an.rhomax)  // summed from aggregates by k_screen_agg instead
+        keep = !tile_allpos(an.rhomax[(int64_t)an.tile_anchor[crow >> 7] * an.kpstride + t0 + i], rad, an.cmn[t0 + i]);
       const unsigned bal = __ballot_sync(0xffffffffu, keep);
       if (lane == 0) wsum[warp] = __popc(bal);
       __syncthreads();
@@ -900,6 +978,109 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   __syncthreads();
   fence_after();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+}
+
+
+// All-positive (block, tile) pairs of the tensor screen (tile_allpos): the
+// block's upper-bound contribution from tile aggregates.  Same plan and grid as
+// k_screen_tc, one thread per candidate; only where the screen used its kept-tile
+// list (it then skipped exactly these tiles).  Per tile:
+//   sum_v (a_v + kq) <= ipsum_a[t] + c'.vsum[t] + n_t (ic + kq) + (d + 2) u |c'| |vsum[t]|
+// with the screen's own per-pair quantum kq (it bounds the fp32 seed, c' and ic
+// roundings) and the fp32 dot's error; accumulated in fp64.
+template <int DR>  // DR > 0: c' held in DR registers (d <= DR); 0: c' in shared memory
+__global__ void __launch_bounds__(128) k_screen_agg(const float* __restrict__ V32, int pitch, int d, TcAnchors an,
+                                                    int64_t cand0, int ntiles, int tiles_per_split, int np, int64_t n,
+                                                    const double* __restrict__ ipsum, const float* __restrict__ vsum,
+                                                    const float* __restrict__ vsn, double* __restrict__ part_a,
+                                                    int64_t part_stride, const int* __restrict__ level_now,
+                                                    int level) {
+  if (level_now && *level_now != level) return;
+  extern __shared__ float cs[];  // DR == 0: c' of the block, [k][thread]; then the tile list
+  __shared__ int wsum[4];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int t0 = blockIdx.y * tiles_per_split;
+  const int t1 = min(ntiles, t0 + tiles_per_split);
+  const int nt = t1 - t0;
+  const int64_t crow = cand0 + (int64_t)blockIdx.x * 128;
+  const int64_t c = crow + tid;
+  double acc = 0.0;
+  if (an.rho && an.rhomax && nt <= an.list_cap) {
+    const int anc = an.tile_anchor[crow >> 7];
+    const float rad = an.rad[crow >> 7];
+    const float* rho = an.rho + (int64_t)anc * an.kpstride;
+    const float* rhx = an.rhomax + (int64_t)anc * an.kpstride;
+    // the block's all-positive tiles, classified once (same tests as the screen)
+    uint16_t* tl = reinterpret_cast<uint16_t*>(cs + (DR > 0 ? 0 : 128 * d));
+    int nl = 0;
+    for (int i0 = 0; i0 < nt; i0 += 128) {
+      const int i = i0 + tid;
+      const bool on = i < nt && !tile_prunable(rho[t0 + i], rad, an.cmx[t0 + i]) &&
+                      tile_allpos(rhx[t0 + i], rad, an.cmn[t0 + i]);
+      const unsigned bal = __ballot_sync(0xffffffffu, on);
+      if (lane == 0) wsum[warp] = __popc(bal);
+      __syncthreads();
+      int off = nl;
+      for (int w = 0; w < warp; ++w) off += wsum[w];
+      if (on) tl[off + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)i;
+      nl += wsum[0] + wsum[1] + wsum[2] + wsum[3];
+      __syncthreads();
+    }
+    if (nl > 0) {
+      const float* mu = an.mu + (int64_t)anc * an.apitch;
+      const float* row = V32 + c * pitch;
+      float cn2 = 0.f, mc = 0.f, mn2 = 0.f;
+      float cp[DR > 0 ? DR : 1];
+#pragma unroll
+      for (int k = 0; k < (DR > 0 ? DR : 1); ++k) cp[k] = 0.f;
+      for (int k = 0; k < d; ++k) {  // the screen's c' = fl(c - mu) and its sums, same order
+        const float m = mu[k];
+        const float x = row[k] - m;
+        cn2 = fmaf(x, x, cn2);
+        mc = fmaf(m, x, mc);
+        mn2 = fmaf(m, m, mn2);
+        if constexpr (DR > 0) {
+#pragma unroll
+          for (int q = 0; q < DR; ++q)
+            if (q == k) cp[q] = x;
+        } else {
+          cs[k * 128 + tid] = x;
+        }
+      }
+      const float cn = sqrtf(cn2) * (1.f + 1e-5f);
+      const float ic = -(mc + 0.5f * cn2);
+      const float kc = an.kc * (sqrtf(mn2) * (1.f + 1e-5f) * cn + cn2);
+      const float kxc = an.kx * cn;
+      const float* kpa = an.kpmax + (int64_t)anc * an.kpstride;
+      const double* ips = ipsum + (int64_t)anc * an.kpstride;
+      const double edot = (double)(d + 2) * 5.960464477539063e-08 * 1.01 * (double)cn;
+      for (int li = 0; li < nl; ++li) {
+        const int t = t0 + tl[li];
+        const float* vs = vsum + (int64_t)t * pitch;
+        float dot;
+        if constexpr (DR > 0) {
+          // four independent partial dots over 128-bit (warp-broadcast) loads
+          float p4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int k = 0; k < DR; k += 4) {
+            const float4 w4 = __ldg(reinterpret_cast<const float4*>(vs) + (k >> 2));
+            p4[0] = fmaf(cp[k], w4.x, p4[0]);
+            p4[1] = fmaf(cp[k + 1], w4.y, p4[1]);
+            p4[2] = fmaf(cp[k + 2], w4.z, p4[2]);
+            p4[3] = fmaf(cp[k + 3], w4.w, p4[3]);
+          }
+          dot = (p4[0] + p4[1]) + (p4[2] + p4[3]);
+        } else {
+          dot = 0.f;
+          for (int k = 0; k < d; ++k) dot = fmaf(cs[k * 128 + tid], __ldg(vs + k), dot);
+        }
+        const float kq = kpa[t] + fmaf(kxc, __ldg(an.vmax + t), kc);
+        const int64_t nt_pts = min((int64_t)np, n - (int64_t)t * np);
+        acc += ips[t] + (double)dot + (double)nt_pts * ((double)ic + (double)kq) + edot * (double)vsn[t];
+      }
+    }
+  }
+  part_a[blockIdx.y * part_stride + c] = acc;
 }
 
 }  // namespace ebc

@@ -492,3 +492,22 @@ def test_seeds_folded_into_the_mma_are_exact(monkeypatch, prec, d):
         out[ms] = (s.selected, s.gains)
         f.close()
     assert out["1"] == out["0"]
+
+
+def test_all_positive_tiles_from_aggregates_are_exact(monkeypatch):
+    """Rung 1 sums the certified all-positive (block, tile) pairs of the early
+    steps from tile aggregates (k_screen_agg) instead of MMA terms: same
+    selection as the oracle and bit-identical exact gains with the path off."""
+    import datasets
+    X = datasets.surrogate(40000, 32, 5, 0.01, 3).astype(np.float32)
+    sel, vals, _, _ = oracle.greedy(X.astype(np.float64), 10)
+    out = {}
+    for agg in ("1", "0"):
+        monkeypatch.setenv("EBC200_TC_AGG", agg)
+        f = fn(X, eb.Precision.FP32)
+        s = eb.greedy_maximize(f, eb.OptimizerBudget(k=10))
+        assert s.selected == sel
+        np.testing.assert_allclose(np.cumsum(s.gains), vals, rtol=1e-10)
+        out[agg] = (s.selected, s.gains)
+        f.close()
+    assert out["1"] == out["0"]
