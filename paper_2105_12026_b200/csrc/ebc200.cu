@@ -972,7 +972,7 @@ int multiset_sparse(ebc_ctx* ctx, int64_t l, int64_t nnz) {
   } else {
     CU(cudaMemsetAsync(ctx->ms_nruns, 0, sizeof(int), ctx->stream));
   }
-  k_sparse_set_sum<<<(unsigned)l, RED_THREADS, 0, ctx->stream>>>(
+  k_sparse_set_sum<<<(unsigned)((l * 32 + 255) / 256), 256, 0, ctx->stream>>>(
       (const unsigned long long*)ctx->ms_ukeys.p, (const double*)ctx->ms_uvals.p, ctx->ms_nruns, ctx->n, l,
       1.0 / (double)ctx->n, (double*)ctx->ms_out.p);
   KCHECK();

@@ -77,47 +77,67 @@ struct DMax {
   __device__ __forceinline__ double operator()(double a, double b) const { return a > b ? a : b; }
 };
 
-// One block per set: the dense chunk reduction over its (sparse) terms.
-__global__ void __launch_bounds__(RED_THREADS) k_sparse_set_sum(const unsigned long long* __restrict__ ukeys,
-                                                                const double* __restrict__ uvals,
-                                                                const int* __restrict__ nruns, int64_t n, int64_t l,
-                                                                double inv_n, double* __restrict__ out) {
-  __shared__ double sbuf[RED_THREADS];
-  __shared__ int64_t range[2];
-  const int64_t j = blockIdx.x;
+// One WARP per set: the dense chunk reduction over its (sparse) terms.
+// block_sum_256's tree (level s: t < s adds t + s, s = 128 .. 1) is replayed by
+// one warp: lane l holds the partials of threads l + 32 m (m = 0..7); levels
+// 128/64/32 pair them inside the lane (m with m + 4, m + 2, m + 1), levels
+// 16..1 are the shuffle-down steps.  Every tree node is the same single fp64
+// add of the same two operands as in the block form, so each chunk sum -- and
+// the set's left-to-right total -- is bit-identical to the dense kernel.
+__global__ void __launch_bounds__(256) k_sparse_set_sum(const unsigned long long* __restrict__ ukeys,
+                                                        const double* __restrict__ uvals,
+                                                        const int* __restrict__ nruns, int64_t n, int64_t l,
+                                                        double inv_n, double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (j >= l) return;
   const int64_t R = *nruns;
-  if (threadIdx.x < 2) {
-    // first run with key >= (j + threadIdx.x) * n
-    const unsigned long long target = (unsigned long long)(j + threadIdx.x) * (unsigned long long)n;
+  // [r0, r1): runs with key in [j n, (j + 1) n) (lanes 0 and 1 search, then broadcast)
+  int64_t found = 0;
+  if (lane < 2) {
+    const unsigned long long target = (unsigned long long)(j + lane) * (unsigned long long)n;
     int64_t lo = 0, hi = R;
     while (lo < hi) {
       const int64_t mid = (lo + hi) >> 1;
       if (ukeys[mid] < target) lo = mid + 1; else hi = mid;
     }
-    range[threadIdx.x] = lo;
+    found = lo;
   }
-  __syncthreads();
-  const int64_t r0 = range[0], r1 = range[1];
+  const int64_t r0 = __shfl_sync(0xffffffffu, found, 0), r1 = __shfl_sync(0xffffffffu, found, 1);
   const unsigned long long base = (unsigned long long)j * (unsigned long long)n;
   double total = 0.0;
   int64_t r = r0;
   while (r < r1) {
-    const int64_t v0 = (int64_t)(ukeys[r] - base);
-    const int64_t ch = v0 / RCH;
-    // runs of this chunk: [r, re)
+    const int64_t ch = (int64_t)(ukeys[r] - base) / RCH;
+    // runs of this chunk: [r, re) (every lane walks the same runs)
     int64_t re = r;
     while (re < r1 && (int64_t)(ukeys[re] - base) / RCH == ch) ++re;
-    // thread t accumulates its points t + 256 i (i ascending) exactly like k_multiset
-    double acc = 0.0;
+    // thread t's accumulator (points t + 256 i, i ascending) lives in lane t % 32, slot t / 32
+    double v[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     for (int64_t q = r; q < re; ++q) {
-      const int64_t off = (int64_t)(ukeys[q] - base) - ch * RCH;
-      if ((int)(off % RED_THREADS) == (int)threadIdx.x) acc += uvals[q];
+      const int t = (int)(((int64_t)(ukeys[q] - base) - ch * RCH) % RED_THREADS);
+      if ((t & 31) == lane) {
+        const int m = t >> 5;
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          if (i == m) v[i] += uvals[q];
+      }
     }
-    total += block_sum_256(acc, sbuf);
+#pragma unroll
+    for (int m = 0; m < 4; ++m) v[m] += v[m + 4];  // s = 128
+#pragma unroll
+    for (int m = 0; m < 2; ++m) v[m] += v[m + 2];  // s = 64
+    v[0] += v[1];                                   // s = 32
+    double x = v[0];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {  // s = 16 .. 1
+      const double y = __shfl_down_sync(0xffffffffu, x, o);
+      if (lane < o) x += y;
+    }
+    total += __shfl_sync(0xffffffffu, x, 0);
     r = re;
   }
-  if (threadIdx.x == 0) out[j] = total * inv_n;
+  if (lane == 0) out[j] = total * inv_n;
 }
 
 }  // namespace ebc
