@@ -60,7 +60,8 @@ def evaluate_multiset_batched(f: EbcFunction, multiset: EvalMultiset, threads: i
     in multiset order, IndexError naming the first offending set."""
     if threads < 1:
         raise ValueError("threads must be >= 1")
-    multiset.validate_indices(f.ground.n)
+    # index validation (validate_indices, core.py:137-143) happens in the C-ABI
+    # before any launch, with the reference's message for the first bad index
     return f.evaluate_multiset(multiset)
 
 
