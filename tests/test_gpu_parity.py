@@ -511,3 +511,26 @@ def test_all_positive_tiles_from_aggregates_are_exact(monkeypatch):
         out[agg] = (s.selected, s.gains)
         f.close()
     assert out["1"] == out["0"]
+
+
+@pytest.mark.parametrize("case", ["fp32-d100", "fp16-d100", "surrogate-d32"])
+def test_nonzero_e0_on_the_tensor_rungs(case):
+    """A non-zero auxiliary vector e0 (ebc.py:55-71) shifts every seed, the
+    folded-seed scale bound (max d(v, e0)) and the all-positive tile test; the
+    selection and gains still equal the oracle's."""
+    import datasets
+    rng = np.random.default_rng(77)
+    if case == "surrogate-d32":
+        X = datasets.surrogate(20000, 32, 5, 0.01, 4).astype(np.float32)
+        prec = eb.Precision.FP32
+        e0 = X.mean(axis=0).astype(np.float64) + 0.5
+    else:
+        X = rng.standard_normal((4000, 100)).astype(np.float32 if case == "fp32-d100" else np.float16)
+        prec = eb.Precision.FP32 if case == "fp32-d100" else eb.Precision.FP16_STORAGE
+        e0 = rng.standard_normal(100) * 0.7 + 0.3
+    g = eb.GroundMatrix(X, prec)
+    f = eb.EbcFunction(g, e0=e0)
+    s = eb.greedy_maximize(f, eb.OptimizerBudget(k=8))
+    sel, vals, _, _ = oracle.greedy(g.as_float64(), 8, e0=e0)
+    assert s.selected == sel
+    np.testing.assert_allclose(np.cumsum(s.gains), vals, rtol=1e-10)
