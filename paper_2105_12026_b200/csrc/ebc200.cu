@@ -434,6 +434,7 @@ struct TcPlan {
   size_t smem;
   int stages;
   int list_cap;  // kept-tile list entries (0: pruning off)
+  int kq_cap;    // per-tile {kpmax, vmax} entries staged in smem (0: read per tile)
 };
 
 int tc_es(int kind) { return kind == tc::KIND_TF32 ? 4 : 2; }
@@ -459,17 +460,20 @@ bool plan_tc(const ebc_ctx* ctx, TcPlan& p, int kind) {
   }
   p.nsplit = (p.ntiles + p.tps - 1) / p.tps;
   const int es = tc_es(kind), parts = tc_parts(kind);
+  // per-tile {kpmax, vmax} staged in smem ahead of the kept-tile list (<= 16 KB)
+  p.kq_cap = p.tps <= 2048 ? p.tps : 0;
+  const size_t kqb = (size_t)p.kq_cap * 8;
   p.list_cap = 0;
-  p.stages = tc::stages_for(ctx->kpad, ctx->tc_np, es, parts);
+  p.stages = tc::stages_for(ctx->kpad, ctx->tc_np, es, parts, kqb);
   if (ctx->tc_prune && p.tps <= 65535) {
     const size_t lb = tc::list_bytes_for(p.tps);
-    const int st = tc::stages_for(ctx->kpad, ctx->tc_np, es, parts, lb);
+    const int st = tc::stages_for(ctx->kpad, ctx->tc_np, es, parts, lb + kqb);
     if (st >= 2 && st >= p.stages - 1) {  // keep the ring at least as deep, minus one stage at most
       p.list_cap = p.tps;
       p.stages = st;
     }
   }
-  p.smem = tc::smem_bytes(ctx->kpad, ctx->tc_np, es, parts, p.list_cap ? tc::list_bytes_for(p.tps) : 0);
+  p.smem = tc::smem_bytes(ctx->kpad, ctx->tc_np, es, parts, (p.list_cap ? tc::list_bytes_for(p.tps) : 0) + kqb);
   return true;
 }
 
@@ -487,7 +491,7 @@ int launch_tc_t(ebc_ctx* ctx, const TcPlan& p, const int* level_now, int level) 
   const bool origin_only = ms && fast;
   TcAnchors an{ctx->anchors, ctx->pitch, origin_only ? ctx->tile_anchor0 : ctx->tile_anchor, ctx->pttc, ctx->n_pad,
                ctx->kpmax, ctx->tc_ntl, ctx->tc_vmax, ctx->tc_kc, fast ? ctx->tc_kx_fast : ctx->tc_kx,
-               (p.list_cap && !origin_only) ? ctx->rho : nullptr, ctx->tile_rad, ctx->cmx, p.list_cap,
+               (p.list_cap && !origin_only) ? ctx->rho : nullptr, ctx->tile_rad, ctx->cmx, p.list_cap, p.kq_cap,
                (unsigned long long*)(ctx->stats + 4)};
   if (!one && ctx->tc_agg && p.list_cap) {
     an.rhomax = ctx->rhomax;
@@ -521,7 +525,7 @@ int launch_tc_flag_t(ebc_ctx* ctx, const TcPlan& p, const float* Vc, const int* 
   dim3 grid(p.ncb, p.nsplit);
   TcAnchors an{ctx->anchors, ctx->pitch, tanchor, ctx->ipa0, ctx->n_pad, ctx->kpmax, ctx->tc_ntl,
                ctx->tc_vmax, ctx->tc_kc, ctx->tc_kx, p.list_cap ? ctx->rho : nullptr, trad, ctx->cmx0,
-               p.list_cap, nullptr};
+               p.list_cap, p.kq_cap, nullptr};
   kern<<<grid, tc::THREADS, p.smem, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->d, (const unsigned char*)ctx->Vhi,
                                                    (const unsigned char*)ctx->Vlo, an, ctx->kpad, p.stages, 0,
                                                    p.ntiles, p.tps, nullptr, nullptr, 0, nullptr, 0, Vc, fo);
@@ -565,7 +569,7 @@ int launch_tc(ebc_ctx* ctx, const TcPlan& p, const int* level_now, int level, in
 // anchors as the rung-1 screen launch).
 int launch_tc_agg(ebc_ctx* ctx, const TcPlan& p) {
   TcAnchors an{ctx->anchors, ctx->pitch, ctx->tile_anchor, ctx->pttc, ctx->n_pad, ctx->kpmax, ctx->tc_ntl,
-               ctx->tc_vmax, ctx->tc_kc, ctx->tc_kx, ctx->rho, ctx->tile_rad, ctx->cmx, p.list_cap, nullptr};
+               ctx->tc_vmax, ctx->tc_kc, ctx->tc_kx, ctx->rho, ctx->tile_rad, ctx->cmx, p.list_cap, 0, nullptr};
   an.rhomax = ctx->rhomax;
   an.cmn = ctx->cmn;
   // c' in 32 registers when it fits (padded dims of vsum are zero), else in smem;

@@ -579,6 +579,7 @@ struct TcAnchors {
   const float* rad;
   const float* cmx;
   int list_cap;             // uint16 entries reserved for the kept-tile list
+  int kq_cap;               // float2 {kpmax, vmax} entries staged in smem per CTA (0: read per tile)
   unsigned long long* work; // if set: += executed (candidate block, point tile) pairs
   // all-positive tiles handled by k_screen_agg (nullptr: off): rhomax[a][t] =
   // max_v |v - mu_a|, cmn[t] = min cm over the tile (current step)
@@ -662,12 +663,21 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
 
   // kept point tiles of this CTA (certified tile-pair pruning, tile_prunable):
   // every role walks the same compacted list, built once by all threads
+  // per-tile error-quantum inputs {kpmax[anchor][t], vmax[t]} of the CTA's tile
+  // range, staged once so the epilogue's per-tile quantum is a shared-memory read
+  float2* kqs = reinterpret_cast<float2*>(smem + (size_t)stages * stage_bytes + (2 * MAX_STAGES + 8) * sizeof(uint64_t) + 64);
+  const bool kq_staged = nt <= an.kq_cap;
+  if (kq_staged) {
+    const int a0 = MS ? 0 : an.tile_anchor[crow >> 7];
+    const float* kpg = an.kpmax + (int64_t)a0 * an.kpstride;
+    for (int i = tid; i < nt; i += THREADS) kqs[i] = make_float2(kpg[t0 + i], an.vmax[t0 + i]);
+    __syncthreads();  // kq_staged is uniform over the CTA
+  }
   uint16_t* tlist = nullptr;
   int ntk = nt;
   if (an.rho && nt <= an.list_cap) {
     __shared__ int wsum[THREADS / 32];
-    tlist = reinterpret_cast<uint16_t*>(smem + (size_t)stages * stage_bytes + (2 * MAX_STAGES + 8) * sizeof(uint64_t) +
-                                        64);
+    tlist = reinterpret_cast<uint16_t*>(reinterpret_cast<unsigned char*>(kqs) + (size_t)an.kq_cap * sizeof(float2));
     const float rad = an.rad[crow >> 7];
     const float* rho = an.rho + (int64_t)an.tile_anchor[crow >> 7] * an.kpstride;
     int base = 0;
@@ -843,7 +853,16 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       }
       // one error quantum per tile: kpmax = max_v kp over the tile (bounds every
       // pair's kp_v; computed at reset, cm only decreases within a run)
-      const float kq = fmaf(kpa[tt], an.kpscale, fmaf(kxc, __ldg(an.vmax + tt), kc));
+      float kpt, vmt;
+      if (kq_staged) {
+        const float2 q2 = kqs[tt - t0];
+        kpt = q2.x;
+        vmt = q2.y;
+      } else {
+        kpt = kpa[tt];
+        vmt = __ldg(an.vmax + tt);
+      }
+      const float kq = fmaf(kpt, an.kpscale, fmaf(kxc, vmt, kc));
       const float thr = -kq;           // FLAG: possibly closer than e0 iff a > -kq
       const float icq = ic + kq;       // bound: a + kq = b + icq
       mbar_wait(&tfull[b], (it / NB) & 1);
