@@ -204,7 +204,20 @@ __device__ __forceinline__ void write_seed_parts(const TcSeeds& s, int64_t v, fl
 }
 
 __device__ __forceinline__ void write_seeds(const TcSeeds& s, int64_t v, float cm32) {
-  for (int a = 0; a < s.na; ++a) s.ipa[a * s.stride + v] = (cm32 - s.nva[a * s.stride + v]) * 0.5f;
+  constexpr int NA_MAX = 32;
+  if (s.na <= NA_MAX) {
+    // all |v - mu_a|^2 loads in flight before the first store: one memory
+    // latency per updated point instead of one per anchor
+    float q[NA_MAX];
+#pragma unroll
+    for (int a = 0; a < NA_MAX; ++a)
+      if (a < s.na) q[a] = __ldg(s.nva + a * s.stride + v);
+#pragma unroll
+    for (int a = 0; a < NA_MAX; ++a)
+      if (a < s.na) s.ipa[a * s.stride + v] = (cm32 - q[a]) * 0.5f;
+  } else {
+    for (int a = 0; a < s.na; ++a) s.ipa[a * s.stride + v] = (cm32 - s.nva[a * s.stride + v]) * 0.5f;
+  }
   if (s.ops) write_seed_parts(s, v, s.ipa[v] * s.s2);  // anchor 0 = the origin
 }
 
