@@ -281,10 +281,12 @@ def run_ours(args):
         torch.cuda.synchronize(dev)
         barrier()
         times_ms.append(ev0.elapsed_time(ev1))
+        # NCCL path: the whole run is one native call (graph); host-driven
+        # (gloo) path: the count of the last per-step native call
+        launches += optimize.last_launches(f)
         if not distributed:
             t = optimize.last_timings(f)
             screen_ms.append(t[0])
-            launches += optimize.last_launches(f)
             stats = optimize.last_stats(f)
             work.append(optimize.last_screen_work(f))
         if ref_sel is not None and s.selected != ref_sel:
@@ -416,7 +418,9 @@ def run_ours(args):
             line["cpu_baseline"] = {"value": rate, "unit": "point-candidate evals/s", "cores": threads,
                                     "kind": "port", "sample": desc}
     else:
-        line["gpu_launches"] = None
+        line["gpu_launches"] = int(launches)
+        if dist.get_backend() != "nccl":
+            line["gpu_launches_note"] = "host-driven exchange: rank 0's last native step call per run"
     print(json.dumps(line), flush=True)
     if distributed:
         dist.destroy_process_group()
