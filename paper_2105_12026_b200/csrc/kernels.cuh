@@ -44,10 +44,20 @@ __device__ __forceinline__ double block_sum_256(double v, double* sbuf) {
   return r;
 }
 
-// Sequential left-to-right sum of chunk partials (one thread).
+// Sequential left-to-right sum of chunk partials (one thread).  Loads go out
+// 16 at a time ahead of their (still strictly ordered) adds: one memory latency
+// per 16 partials instead of one per partial.
 __device__ __forceinline__ double chunk_total(const double* part, int nchunks) {
   double s = 0.0;
-  for (int c = 0; c < nchunks; ++c) s += part[c];
+  int c = 0;
+  for (; c + 16 <= nchunks; c += 16) {
+    double x[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) x[i] = __ldcg(part + c + i);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) s += x[i];
+  }
+  for (; c < nchunks; ++c) s += __ldcg(part + c);
   return s;
 }
 
