@@ -1523,7 +1523,14 @@ int greedy_run(ebc_ctx* ctx, int32_t k, bool sharded, int64_t* out_sel, double* 
     CU(cudaGraphLaunch(cached->exec, ctx->stream));
     ctx->launches = cached->launches;
   } else {
+    // a repeated eager run (timing mode: per-step events, no graph) takes the
+    // first run's path down the ladder, like a replayed graph
+    if (seen) {
+      const size_t ki = (size_t)(std::find(ctx->eager_ks.begin(), ctx->eager_ks.end(), key) - ctx->eager_ks.begin());
+      ctx->ladder_max = ki < ctx->eager_lv.size() ? std::max(0, std::min(3, ctx->eager_lv[ki])) : 3;
+    }
     rc = enqueue();
+    ctx->ladder_max = 3;
     if (rc) return rc;
   }
   long long lv_end = 3;
