@@ -130,6 +130,9 @@ struct ebc_ctx {
   float* vsum = nullptr;    // tc_ntl x pitch: sum of the tile's points
   float* vsn = nullptr;     // tc_ntl: |vsum|
   double* ipsum = nullptr;  // na x tc_ntl: sum of the tile's seeds (current step)
+  float* rhomin = nullptr;  // tc_ntl: min over anchors of rhomax
+  float radmin = 0.f;       // min candidate-block radius
+  int* agg_any = nullptr;   // this step: some tile can be all-positive
   DevBuf part_a;            // nsplit x n_pad aggregate partials
   int wcap_fast = 256;
   float* pttc = nullptr;   // na x n_pad seeds ip_a(v) = (cm32 - |v - mu_a|^2)/2
@@ -581,12 +584,12 @@ int launch_tc_agg(ebc_ctx* ctx, const TcPlan& p) {
     CU(cudaFuncSetAttribute(k_screen_agg<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_screen_agg<32><<<grid, 128, smem, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->d, an, ctx->c0, p.ntiles, p.tps,
                                                        ctx->tc_np, ctx->n, ctx->ipsum, ctx->vsum, ctx->vsn,
-                                                       (double*)ctx->part_a.p, ctx->n_pad, ctx->level, L_TC);
+                                                       (double*)ctx->part_a.p, ctx->n_pad, ctx->level, L_TC, ctx->agg_any);
   } else {
     CU(cudaFuncSetAttribute(k_screen_agg<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_screen_agg<0><<<grid, 128, smem, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->d, an, ctx->c0, p.ntiles, p.tps,
                                                       ctx->tc_np, ctx->n, ctx->ipsum, ctx->vsum, ctx->vsn,
-                                                      (double*)ctx->part_a.p, ctx->n_pad, ctx->level, L_TC);
+                                                      (double*)ctx->part_a.p, ctx->n_pad, ctx->level, L_TC, ctx->agg_any);
   }
   KCHECK();
   return EBC_OK;
@@ -636,8 +639,10 @@ int run_screen_window(ebc_ctx* ctx, int eb, int fin_blocks) {
         rc = ensure(ctx, ctx->part_a, (size_t)tp.nsplit * ctx->n_pad * sizeof(double));
         if (rc) return rc;
         const int64_t cells = (int64_t)ctx->tc_na * ctx->tc_ntl;
+        CU(cudaMemsetAsync(ctx->agg_any, 0, sizeof(int), ctx->stream));
         k_tile_ipsum<<<(unsigned)((cells * 32 + 255) / 256), 256, 0, ctx->stream>>>(
-            ctx->pttc, ctx->n_pad, ctx->tc_na, ctx->n, ctx->tc_ntl, ctx->tc_np, ctx->ipsum);
+            ctx->pttc, ctx->n_pad, ctx->tc_na, ctx->n, ctx->tc_ntl, ctx->tc_np, ctx->ipsum, ctx->rhomin, ctx->radmin,
+            ctx->cmn, ctx->agg_any);
         KCHECK();
       }
       // ladder_max < L_DIRECT only while capturing a graph of a run whose eager
@@ -851,7 +856,7 @@ int do_reset(ebc_ctx* ctx) {
 void free_ctx(ebc_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
-  void* ptrs[] = {c->V32, c->V64, c->e0d, c->cm64, c->pt, c->nv32, c->level, c->stats, c->Vhi, c->Vlo, c->Vf, c->tile_anchor0, c->rhomax, c->cmn, c->vsum, c->vsn, c->ipsum, c->pttc, c->kpmax, c->anchors, c->nva, c->tile_anchor, c->tc_vmax, c->fps_keys, c->ipa0, c->tile_rad, c->rho, c->cmx, c->cmx0, c->selected, c->chunkpart, c->counter, c->counter2, c->topc, c->toppart, c->terms, c->cur, c->best,
+  void* ptrs[] = {c->V32, c->V64, c->e0d, c->cm64, c->pt, c->nv32, c->level, c->stats, c->Vhi, c->Vlo, c->Vf, c->tile_anchor0, c->rhomax, c->cmn, c->vsum, c->vsn, c->ipsum, c->rhomin, c->agg_any, c->pttc, c->kpmax, c->anchors, c->nva, c->tile_anchor, c->tc_vmax, c->fps_keys, c->ipa0, c->tile_rad, c->rho, c->cmx, c->cmx0, c->selected, c->chunkpart, c->counter, c->counter2, c->topc, c->toppart, c->terms, c->cur, c->best,
                   c->maxlb, c->wcount, c->wlist, c->wgain, c->ub};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, c->stream);
@@ -1203,6 +1208,8 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
         CUC(cudaMemsetAsync(ctx->vsum + (size_t)ctx->tc_ntl * ctx->pitch, 0, 32 * sizeof(float), ctx->stream));
         CUC(cudaMallocAsync((void**)&ctx->vsn, (size_t)ctx->tc_ntl * sizeof(float), ctx->stream));
         CUC(cudaMallocAsync((void**)&ctx->ipsum, (size_t)ctx->tc_na * ctx->tc_ntl * sizeof(double), ctx->stream));
+        CUC(cudaMallocAsync((void**)&ctx->rhomin, (size_t)ctx->tc_ntl * sizeof(float), ctx->stream));
+        CUC(cudaMallocAsync((void**)&ctx->agg_any, sizeof(int), ctx->stream));
       }
       CUC(cudaMallocAsync((void**)&ctx->cmx, (size_t)ctx->tc_ntl * sizeof(float), ctx->stream));
       CUC(cudaMallocAsync((void**)&ctx->cmx0, (size_t)ctx->tc_ntl * sizeof(float), ctx->stream));
@@ -1273,9 +1280,13 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
           ctx->e0d, ctx->nv32, ctx->nva, ctx->n_pad, ctx->tc_na, n, ctx->tc_ntl, ctx->tc_np, ctx->tc_kp, ctx->kpmax,
           ctx->tc_vmax, ctx->rho, ctx->rhomax);
       CUC(cudaGetLastError());
-      if (ctx->tc_agg)
+      if (ctx->tc_agg) {
         k_tile_vsum<<<(unsigned)ctx->tc_ntl, 128, 0, ctx->stream>>>(ctx->V32, ctx->pitch, n, d, ctx->tc_np, ctx->vsum,
                                                                    ctx->vsn);
+        CUC(cudaGetLastError());
+        k_tile_rhomin<<<(unsigned)((ctx->tc_ntl + 255) / 256), 256, 0, ctx->stream>>>(ctx->rhomax, ctx->tc_na,
+                                                                                       ctx->tc_ntl, ctx->rhomin);
+      }
       CUC(cudaGetLastError());
       k_tile_cmmax<<<(unsigned)((ctx->tc_ntl * 32 + 255) / 256), 256, 0, ctx->stream>>>(ctx->e0d, n, ctx->tc_ntl,
                                                                                         ctx->tc_np, ctx->cmx0);
@@ -1283,6 +1294,14 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
       CUC(cudaStreamSynchronize(ctx->stream));
       mark("init + anchors");
       cudaFreeAsync(mind, ctx->stream);
+      if (ctx->tc_agg) {
+        // smallest candidate-block radius (k_tile_ipsum's any-block screen)
+        std::vector<float> rad((size_t)((n + 127) / 128));
+        CUC(cudaMemcpy(rad.data(), ctx->tile_rad, rad.size() * sizeof(float), cudaMemcpyDeviceToHost));
+        float rm = INFINITY;
+        for (float r : rad) rm = std::min(rm, r);
+        ctx->radmin = rm;
+      }
       if (ctx->tc_fast) {
         // operand scale s = 2^e: every |s c'_k| <= s (|c| + |mu|) <= 2 s max|v| <= 2^15
         // (fp16 max 65504); |e| <= 60 keeps s^2 and 1/s^2 normal in fp32

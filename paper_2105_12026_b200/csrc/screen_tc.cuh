@@ -515,6 +515,15 @@ __device__ __forceinline__ bool tile_allpos(float rhomax, float rad, float cmn) 
 
 // vsum[t][k] = sum of the tile's (real) points, fp64 accumulation rounded to
 // fp32; vsn[t] = |vsum[t]| rounded up.  One block per tile.
+// rhomin[t] = min over anchors of rhomax[a][t] (the any-block screen of k_tile_ipsum)
+__global__ void k_tile_rhomin(const float* __restrict__ rhomax, int na, int64_t ntiles, float* __restrict__ rhomin) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ntiles) return;
+  float m = INFINITY;
+  for (int a = 0; a < na; ++a) m = fminf(m, rhomax[a * ntiles + t]);
+  rhomin[t] = m;
+}
+
 __global__ void k_tile_vsum(const float* __restrict__ V32, int pitch, int64_t n, int d, int np,
                             float* __restrict__ vsum, float* __restrict__ vsn) {
   __shared__ double nrm[32];
@@ -543,13 +552,21 @@ __global__ void k_tile_vsum(const float* __restrict__ V32, int pitch, int64_t n,
 
 // ipsum[a][t] = sum over the tile's real points of the fp32 seeds ip_a(v) (fp64,
 // fixed order).  One warp per (anchor, tile).
+// Only tiles that can be all-positive for SOME block are summed: tile_allpos is
+// monotone in (rhomax, rad), so (min over anchors of rhomax[a][t], min block
+// radius) failing it rules the tile out for every block (its ipsum is never
+// read); *anyflag records whether any tile passed (k_screen_agg exits early
+// otherwise -- the late steps of a run).
 __global__ void k_tile_ipsum(const float* __restrict__ ipa, int64_t stride, int na, int64_t n, int64_t ntiles,
-                             int np, double* __restrict__ ipsum) {
+                             int np, double* __restrict__ ipsum, const float* __restrict__ rhomin, float radmin,
+                             const float* __restrict__ cmn, int* __restrict__ anyflag) {
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= (int64_t)na * ntiles) return;
   const int a = (int)(w / ntiles);
   const int64_t t = w - (int64_t)a * ntiles;
+  if (!tile_allpos(rhomin[t], radmin, cmn[t])) return;
+  if (a == 0 && lane == 0) atomicOr(anyflag, 1);
   double s = 0.0;
   for (int j = lane; j < np; j += 32) {
     const int64_t v = t * np + j;
@@ -1013,8 +1030,12 @@ __global__ void __launch_bounds__(128) k_screen_agg(const float* __restrict__ V3
                                                     const double* __restrict__ ipsum, const float* __restrict__ vsum,
                                                     const float* __restrict__ vsn, double* __restrict__ part_a,
                                                     int64_t part_stride, const int* __restrict__ level_now,
-                                                    int level) {
+                                                    int level, const int* __restrict__ anyflag) {
   if (level_now && *level_now != level) return;
+  if (*anyflag == 0) {  // no tile can be all-positive this step
+    part_a[blockIdx.y * part_stride + cand0 + (int64_t)blockIdx.x * 128 + threadIdx.x] = 0.0;
+    return;
+  }
   extern __shared__ float cs[];  // DR == 0: c' of the block, [k][thread]; then the tile list
   __shared__ int wsum[4];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
