@@ -121,6 +121,7 @@ struct ebc_ctx {
   // seeds folded into the MMA for the one-product FP16 rung (rung 0 for fp32
   // grounds, rung 1 for fp16-stored grounds): DESIGN.md §4
   bool tc_mseed = false;
+  bool tc_mb2 = false;  // folded-seed rung: two candidate blocks per CTA (EBC200_TC_MB2)
   float tc_kpscale = 1.f;
   int* tile_anchor0 = nullptr;  // all-zero block anchors (the origin) for rung 0 with folded seeds
   // all-positive (block, tile) pairs of rung 1 summed from tile aggregates (k_screen_agg)
@@ -509,6 +510,30 @@ int launch_tc_t(ebc_ctx* ctx, const TcPlan& p, const int* level_now, int level) 
     an.sinv2 = ctx->tc_sinv2;
     an.keta = ctx->tc_keta;
     an.keta2 = ctx->tc_keta2;
+  }
+  if constexpr (one && NP == 128) {
+    if (ms && ctx->tc_mb2) {
+      // two candidate blocks per CTA on 64-point tiles: the same
+      // split of the point range (twice the tiles per split), half the CTAs
+      auto k2 = k_screen_tc<64, KIND, false, true, 2>;
+      const int tps2 = 2 * p.tps, nt2 = 2 * p.ntiles;
+      const int kqc = tps2 <= 4096 ? tps2 : 0;
+      const size_t kqb = (size_t)kqc * 8;
+      const int st = tc::stages_for(ctx->kpad, 64, 2, 1, kqb);
+      const size_t sm = tc::smem_bytes(ctx->kpad, 64, 2, 1, kqb);
+      CU(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      an.rho = nullptr;  // no tile-pair pruning in the two-block shape
+      an.list_cap = 0;
+      an.kq_cap = kqc;
+      dim3 g2((p.ncb + 1) / 2, p.nsplit);
+      k2<<<g2, tc::THREADS, sm, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->d,
+                                               (const unsigned char*)(fast ? ctx->Vf : ctx->Vhi),
+                                               (const unsigned char*)ctx->Vlo, an, ctx->kpad, st, ctx->c0, nt2, tps2,
+                                               (double*)ctx->part_g.p, (float*)ctx->part_e.p, ctx->n_pad, level_now,
+                                               level, nullptr, FlagOut{});
+      KCHECK();
+      return EBC_OK;
+    }
   }
   kern<<<grid, tc::THREADS, p.smem, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->d,
                                                    (const unsigned char*)(fast ? ctx->Vf : ctx->Vhi),
@@ -1344,6 +1369,10 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
           ctx->tc_mseed = true;
         } else {
           ctx->tc_mseed = bip <= 16384.0;  // fp16-stored grounds: unscaled seeds must fit fp16
+        }
+        {
+          const char* mb = getenv("EBC200_TC_MB2");
+          ctx->tc_mb2 = ctx->tc_np == 128 && !(mb && mb[0] == '0');
         }
         // in-MMA fp32 accumulation of the seed parts: (kpad + 16 + 8) 2^-23 |ip| on top
         // of the (d + 8) u (cm + |v|^2) seed/final-add quantum kpmax

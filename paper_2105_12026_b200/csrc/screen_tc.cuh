@@ -626,7 +626,13 @@ struct TcAnchors {
 // d..d+2 of the point operand hold the scaled origin seed in three FP16 parts,
 // the candidate operand holds 1 there, so the accumulator is s^2 (ip_0 + v.c)
 // and the epilogue neither loads nor adds seeds.  Origin anchor only.
-template <int NP, int KIND, bool FLAG = false, bool MS = false>
+// MB = 2 (one-product kinds with folded seeds only, NP = 64): the CTA screens
+// TWO candidate blocks against each 64-point tile -- A of block h in TMEM
+// columns [64h, 64h + 56), its three accumulators at 128 + (3h + b) 64 -- so every
+// point tile fetched from L2 serves 256 candidates (half the L2 -> SM traffic
+// per pair); epilogue warpgroup h owns block h.  Per-tile host arrays are at
+// 128-point granularity (index >> 1).
+template <int NP, int KIND, bool FLAG = false, bool MS = false, int MB = 1>
 __global__ void __launch_bounds__(tc::THREADS, 1)
     k_screen_tc(const float* __restrict__ V32, int pitch, int d, const unsigned char* __restrict__ Vhi,
                 const unsigned char* __restrict__ Vlo, TcAnchors an,
@@ -654,7 +660,9 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   const int t0 = blockIdx.y * tiles_per_split;
   const int t1 = min(ntiles, t0 + tiles_per_split);
   const int nt = t1 - t0;
-  const int64_t crow = cand0 + (int64_t)blockIdx.x * M;
+  static_assert(MB == 1 || (MB == 2 && NP == 64 && MS && !FLAG && EPI_WARPGROUPS == 2), "two-block CTA shape");
+  constexpr int TSH = MB == 2 ? 1 : 0;  // per-tile host arrays: 128-point tiles
+  const int64_t crow = cand0 + (int64_t)blockIdx.x * M * MB;
 
   if (tid == 0) {
     for (int s = 0; s < stages; ++s) {
@@ -687,7 +695,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   if (kq_staged) {
     const int a0 = MS ? 0 : an.tile_anchor[crow >> 7];
     const float* kpg = an.kpmax + (int64_t)a0 * an.kpstride;
-    for (int i = tid; i < nt; i += THREADS) kqs[i] = make_float2(kpg[t0 + i], an.vmax[t0 + i]);
+    for (int i = tid; i < nt; i += THREADS) kqs[i] = make_float2(kpg[(t0 + i) >> TSH], an.vmax[(t0 + i) >> TSH]);
     __syncthreads();  // kq_staged is uniform over the CTA
   }
   uint16_t* tlist = nullptr;
@@ -746,6 +754,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     constexpr int NB = TM::NB;
     const int b = warp - 1;
     const uint32_t dt = tmem + TM::ACC + (uint32_t)(b * NP);
+    const uint32_t dt2 = tmem + TM::ACC + (uint32_t)((NB + b) * NP);  // MB = 2: block 1's buffer b
     const uint32_t ahi = tmem + COL_AHI, alo = tmem + TM::ALO;
     mbar_wait(aready, 0);
     fence_after();
@@ -762,8 +771,10 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       if (elect_one()) {
 #pragma unroll 4
         for (int j = 0; j < ksteps; ++j) {
-          if (one_product(KIND))
+          if (one_product(KIND)) {
             mma1_f16_ts(dt, ahi + 8 * j, dhi + 16 * j, idesc, j > 0);
+            if (MB == 2) mma1_f16_ts(dt2, ahi + 64 + 8 * j, dhi + 16 * j, idesc, j > 0);
+          }
           else if (KIND == KIND_BF16)
             mma3_bf16_ts(dt, ahi + 8 * j, alo + 8 * j, dhi + 16 * j, dlo + 16 * j, idesc, j > 0);
           else
@@ -779,9 +790,9 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     // (TMEM lane) x one slice of the tile's point columns
     const int q = warp & 3;                    // TMEM lane quadrant of this warp
     const int half = (warp - EPI_WARP0) >> 2;  // which slice of the NP columns
-    constexpr int SLICE = NP / EPI_WARPGROUPS;
+    constexpr int SLICE = MB == 2 ? NP : NP / EPI_WARPGROUPS;
     const int cl = q * 32 + lane;
-    const int64_t c = crow + cl;
+    const int64_t c = crow + (MB == 2 ? (int64_t)half * M : 0) + cl;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     const int anc = MS ? 0 : an.tile_anchor[crow >> 7];  // anchor of this candidate block
     const float* mu = an.mu + (int64_t)anc * an.apitch;
@@ -789,7 +800,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     {
       // A of this candidate into TMEM: slice 0 writes hi [0,128), the last slice lo [128,256)
       const float* row = (FLAG ? Vc : V32) + c * pitch;
-      const bool do_hi = half == 0, do_lo = TM::PARTS == 2 && half == EPI_WARPGROUPS - 1;
+      const bool do_hi = MB == 2 || half == 0, do_lo = TM::PARTS == 2 && half == EPI_WARPGROUPS - 1;
       auto cprime = [&](int k) -> float {  // c' = fl(c - mu), accumulating |c'|^2, mu.c', |mu|^2
         if (k >= d) return 0.f;
         const float m = mu[k];
@@ -832,7 +843,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
             rl[i] = __float_as_uint(x - __uint_as_float(h));
           }
         }
-        if (do_hi) st32(tmem + lane_off + COL_AHI + blk * 32, rh);
+        if (do_hi) st32(tmem + lane_off + COL_AHI + (MB == 2 ? half * 64 : 0) + blk * 32, rh);
         if (do_lo) st32(tmem + lane_off + TM::ALO + blk * 32, rl);
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -876,8 +887,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         kpt = q2.x;
         vmt = q2.y;
       } else {
-        kpt = kpa[tt];
-        vmt = __ldg(an.vmax + tt);
+        kpt = kpa[tt >> TSH];
+        vmt = __ldg(an.vmax + (tt >> TSH));
       }
       const float kq = fmaf(kpt, an.kpscale, fmaf(kxc, vmt, kc));
       const float thr = -kq;           // FLAG: possibly closer than e0 iff a > -kq
@@ -885,7 +896,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       mbar_wait(&tfull[b], (it / NB) & 1);
       fence_after();
       float S[SW];
-      ldcols<SW>(tmem + lane_off + TM::ACC + (uint32_t)(b * NP + half * SLICE), S);
+      ldcols<SW>(tmem + lane_off + TM::ACC +
+                 (uint32_t)(MB == 2 ? (half * NB + b) * NP : b * NP + half * SLICE), S);
       fence_before();
       mbar_arrive(&tempty[b]);  // this thread's columns of the buffer are in registers
       // b = S + ip per pair, a = b + ic.  fl(b + ic) is monotone in b, so
@@ -988,7 +1000,10 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         }
       }
     }
-    if (!FLAG) {
+    if (!FLAG && MB == 2) {  // each warpgroup owns its block's candidates outright
+      part_g[blockIdx.y * part_stride + c] = g64;
+      part_e[blockIdx.y * part_stride + c] = e;
+    } else if (!FLAG) {
     // combine the slices of each candidate in slice order (named barrier over
     // the epilogue warps only)
     double* xg = reinterpret_cast<double*>(stage0);  // the ring is idle once every tile is consumed
