@@ -161,11 +161,13 @@ def test_repeatable_and_reset():
     assert a.selected == b.selected and a.gains == b.gains
 
 
-@pytest.mark.parametrize("world", [2, 3, 8])
-def test_emulated_sharding_bit_identical(world):
+@pytest.mark.parametrize("world,d", [(2, 20), (3, 20), (8, 20), (3, 100), (5, 100)])
+def test_emulated_sharding_bit_identical(world, d):
     """G candidate shards (one context each, all on this GPU) + the host pick
-    rule must give the single-device selection and values bit for bit."""
-    X = np.random.default_rng(9).standard_normal((2500, 20)).astype(np.float32)
+    rule must give the single-device selection and values bit for bit.  d = 100
+    runs the folded-seed FP16 rung with two candidate blocks per CTA on shards
+    with odd block counts."""
+    X = np.random.default_rng(9).standard_normal((3100 if d == 100 else 2500, d)).astype(np.float32)
     X[2000] = X[3]
     k = 8
     single = eb.greedy_maximize(fn(X, eb.Precision.FP32), eb.OptimizerBudget(k=k))
@@ -534,3 +536,25 @@ def test_nonzero_e0_on_the_tensor_rungs(case):
     sel, vals, _, _ = oracle.greedy(g.as_float64(), 8, e0=e0)
     assert s.selected == sel
     np.testing.assert_allclose(np.cumsum(s.gains), vals, rtol=1e-10)
+
+
+@pytest.mark.parametrize("n", [3100, 1000])
+@pytest.mark.parametrize("prec", ["fp32", "fp16-storage"])
+def test_two_block_cta_odd_block_counts(monkeypatch, n, prec):
+    """The two-block CTA of the folded-seed rung on candidate ranges with an odd
+    number of 128-candidate blocks (the last CTA's second block lies in the
+    zero padding): oracle selection, and bit-identical to the one-block shape."""
+    rng = np.random.default_rng(n)
+    X = rng.standard_normal((n, 100)).astype(np.float32 if prec == "fp32" else np.float16)
+    g = eb.GroundMatrix(X, PREC[prec])
+    sel, vals, _, _ = oracle.greedy(g.as_float64(), 6)
+    out = {}
+    for mb in ("1", "0"):
+        monkeypatch.setenv("EBC200_TC_MB2", mb)
+        f = eb.EbcFunction(g)
+        s = eb.greedy_maximize(f, eb.OptimizerBudget(k=6))
+        assert s.selected == sel
+        np.testing.assert_allclose(np.cumsum(s.gains), vals, rtol=1e-10)
+        out[mb] = (s.selected, s.gains)
+        f.close()
+    assert out["1"] == out["0"]
