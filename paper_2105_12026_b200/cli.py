@@ -112,6 +112,9 @@ def build_parser() -> argparse.ArgumentParser:
     p.add_argument("--e0-kind", choices=("zero", "mean"), default="zero")
     p.add_argument("--epsilon", type=float, default=0.1)
     p.add_argument("--seed", type=int, default=0, help="stream order seed (sieve)")
+    # accepted for scripts written against the reference (cli.py:247); the device
+    # evaluator has no host thread pool, so the value (and $EBCSUM_THREADS) is ignored
+    p.add_argument("--threads", type=_positive_int, default=None, help="ignored by the b200 backend")
     p.add_argument("--header", action="store_true")
     p.add_argument("--normalize", action="store_true")
     p.add_argument("--output", default=None)
@@ -134,6 +137,7 @@ def build_parser() -> argparse.ArgumentParser:
     p.add_argument("--cycles", type=_positive_int, default=1000)
     p.add_argument("--dims", type=_positive_int, default=100)
     p.add_argument("--regimes", type=_positive_int, default=5)
+    p.add_argument("--cycles-per-regime", type=_positive_int, default=200)
     p.add_argument("--noise", type=float, default=0.01)
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--output", required=True)
@@ -171,13 +175,12 @@ def cmd_summarize(args) -> int:
 
 
 def cmd_surrogate(args) -> int:
-    from .surrogate import surrogate
+    from . import surrogate
 
-    if args.cycles % args.regimes:
-        raise ValueError("--regimes must divide --cycles")
-    X = surrogate(args.cycles, args.dims, args.regimes, args.noise, args.seed)
-    np.savetxt(args.output, X, delimiter=",", fmt="%.17g")
-    print(f"wrote {X.shape[0]}x{X.shape[1]} surrogate to {args.output}")
+    data_path, lp = surrogate.write(args.output, args.cycles, args.dims, args.regimes, args.cycles_per_regime,
+                                    args.noise, args.seed)
+    print(f"wrote {args.cycles}x{args.dims} surrogate to {data_path}")
+    print(f"wrote regime labels to {lp}")
     return EXIT_OK
 
 

@@ -79,6 +79,13 @@ struct DevBuf {
   size_t bytes = 0;
 };
 
+struct ScopedEvent {
+  cudaEvent_t e = nullptr;
+  ~ScopedEvent() {
+    if (e) cudaEventDestroy(e);
+  }
+};
+
 }  // namespace
 
 struct ebc_ctx {
@@ -182,6 +189,7 @@ struct ebc_ctx {
   // CUDA graphs of whole Greedy runs, keyed by k (rebuilt when buffers move)
   struct Graph {
     int k;  // (k << 1) | sharded
+    int64_t c0, c1;  // the candidate range the graph's kernel arguments and grids hold
     int64_t epoch;
     int64_t launches;
     cudaGraphExec_t exec;
@@ -193,8 +201,14 @@ struct ebc_ctx {
   int nranks = 1, rank = 0;
   DevBuf tie_rec, tie_all;
   int* tie_err = nullptr;
-  std::vector<int> eager_ks;  // k values run eagerly once (captured on the next run)
-  std::vector<int> eager_lv;  // the deepest ladder rung each of those eager runs reached
+  // runs made eagerly once (captured on the next run with the same key and
+  // candidate range) and the deepest ladder rung each of them reached
+  struct Eager {
+    int k;
+    int64_t c0, c1;
+    int lv;
+  };
+  std::vector<Eager> eager;
   int ladder_max = 3;         // deepest rung enqueued (L_DIRECT except while capturing)
   int64_t alloc_epoch = 0;
   bool use_graphs = true;
@@ -445,7 +459,9 @@ int tc_es(int kind) { return kind == tc::KIND_TF32 ? 4 : 2; }
 int tc_parts(int kind) { return tc::one_product(kind) ? 1 : 2; }
 
 bool plan_tc(const ebc_ctx* ctx, TcPlan& p, int kind) {
-  if (!ctx->tc_np || (ctx->c0 % 8) != 0) return false;
+  // the screen reads each candidate block's anchor and radius as
+  // tile_anchor/tile_rad[crow >> 7]: blocks must start on a 128-row boundary
+  if (!ctx->tc_np || (ctx->c0 % tc::M) != 0) return false;
   const int64_t ncand = ctx->c1 - ctx->c0;
   p.ncb = (int)((ncand + tc::M - 1) / tc::M);
   p.ntiles = (int)((ctx->n + ctx->tc_np - 1) / ctx->tc_np);
@@ -1518,9 +1534,10 @@ int greedy_run(ebc_ctx* ctx, int32_t k, bool sharded, int64_t* out_sel, double* 
     if (rc) return rc;
   }
   double acc_ms[4] = {0, 0, 0, 0};
-  cudaEvent_t tstart = nullptr, tend = nullptr;
-  CU(cudaEventCreate(&tstart));
-  CU(cudaEventCreate(&tend));
+  ScopedEvent ts, te;  // destroyed on every return path
+  CU(cudaEventCreate(&ts.e));
+  CU(cudaEventCreate(&te.e));
+  cudaEvent_t tstart = ts.e, tend = te.e;
   CU(cudaEventRecord(tstart, ctx->stream));
   // The k-step loop has no host decision in it, so the second run with the
   // same k is captured as a CUDA graph and launched; later runs replay it (one
@@ -1532,8 +1549,12 @@ int greedy_run(ebc_ctx* ctx, int32_t k, bool sharded, int64_t* out_sel, double* 
   auto enqueue = [&]() { return sharded ? enqueue_greedy_sharded(ctx, k) : enqueue_greedy(ctx, k); };
   ebc_ctx::Graph* cached = nullptr;
   for (auto& g : ctx->graphs)
-    if (g.k == key && g.epoch == ctx->alloc_epoch) cached = &g;
-  const bool seen = std::find(ctx->eager_ks.begin(), ctx->eager_ks.end(), key) != ctx->eager_ks.end();
+    if (g.k == key && g.c0 == ctx->c0 && g.c1 == ctx->c1 && g.epoch == ctx->alloc_epoch) cached = &g;
+  const ebc_ctx::Eager* er = nullptr;
+  for (const auto& e : ctx->eager)
+    if (e.k == key && e.c0 == ctx->c0 && e.c1 == ctx->c1) er = &e;
+  const bool seen = er != nullptr;
+  const int seen_lv = er ? std::max(0, std::min(3, er->lv)) : 3;
   if (graph_ok && !cached && seen) {
     const int64_t before = ctx->launches;
     cudaGraph_t graph = nullptr;
@@ -1543,8 +1564,7 @@ int greedy_run(ebc_ctx* ctx, int32_t k, bool sharded, int64_t* out_sel, double* 
     if (ok) {
       // a Greedy run is a deterministic function of (V, e0, k): replays take the
       // eager run's path down the ladder, so the graph holds only those rungs
-      const size_t ki = (size_t)(std::find(ctx->eager_ks.begin(), ctx->eager_ks.end(), key) - ctx->eager_ks.begin());
-      ctx->ladder_max = ki < ctx->eager_lv.size() ? std::max(0, std::min(3, ctx->eager_lv[ki])) : 3;
+      ctx->ladder_max = seen_lv;
       const int crc = enqueue();
       ctx->ladder_max = 3;
       ok = cudaStreamEndCapture(ctx->stream, &graph) == cudaSuccess && crc == EBC_OK && epoch == ctx->alloc_epoch;
@@ -1554,13 +1574,13 @@ int greedy_run(ebc_ctx* ctx, int32_t k, bool sharded, int64_t* out_sel, double* 
     cudaGetLastError();  // a failed capture only disables graphs
     if (ok) {
       for (auto it = ctx->graphs.begin(); it != ctx->graphs.end();)
-        if (it->k == key) {
+        if (it->k == key && it->c0 == ctx->c0 && it->c1 == ctx->c1) {
           cudaGraphExecDestroy(it->exec);
           it = ctx->graphs.erase(it);
         } else {
           ++it;
         }
-      ctx->graphs.push_back({key, epoch, ctx->launches - before, exec});
+      ctx->graphs.push_back({key, ctx->c0, ctx->c1, epoch, ctx->launches - before, exec});
       cached = &ctx->graphs.back();
     } else {
       ctx->use_graphs = false;
@@ -1573,10 +1593,7 @@ int greedy_run(ebc_ctx* ctx, int32_t k, bool sharded, int64_t* out_sel, double* 
   } else {
     // a repeated eager run (timing mode: per-step events, no graph) takes the
     // first run's path down the ladder, like a replayed graph
-    if (seen) {
-      const size_t ki = (size_t)(std::find(ctx->eager_ks.begin(), ctx->eager_ks.end(), key) - ctx->eager_ks.begin());
-      ctx->ladder_max = ki < ctx->eager_lv.size() ? std::max(0, std::min(3, ctx->eager_lv[ki])) : 3;
-    }
+    if (seen) ctx->ladder_max = seen_lv;
     rc = enqueue();
     ctx->ladder_max = 3;
     if (rc) return rc;
@@ -1591,10 +1608,7 @@ int greedy_run(ebc_ctx* ctx, int32_t k, bool sharded, int64_t* out_sel, double* 
   int tie_err = 0;
   if (sharded) CU(cudaMemcpyAsync(&tie_err, ctx->tie_err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
-  if (!(graph_ok && cached) && !seen) {
-    ctx->eager_ks.push_back(key);
-    ctx->eager_lv.push_back(lv_end < 0 ? 3 : (int)lv_end);
-  }
+  if (!(graph_ok && cached) && !seen) ctx->eager.push_back({key, ctx->c0, ctx->c1, lv_end < 0 ? 3 : (int)lv_end});
   if (tie_err)
     return fail(ctx, EBC_ECOMM, "sharded Greedy: a rank's tie set exceeded " + std::to_string(TIE_CAP) +
                                     " records (use the host exchange)");
@@ -1611,8 +1625,6 @@ int greedy_run(ebc_ctx* ctx, int32_t k, bool sharded, int64_t* out_sel, double* 
   }
   float tot = 0;
   CU(cudaEventElapsedTime(&tot, tstart, tend));
-  cudaEventDestroy(tstart);
-  cudaEventDestroy(tend);
   acc_ms[3] = tot;
   for (int i = 0; i < 4; ++i) ctx->last_ms[i] = acc_ms[i];
   ctx->steps_done = k;
@@ -1724,6 +1736,8 @@ int ebc_shard_pick_commit(ebc_ctx* ctx, const double* gathered, int32_t world, i
   if (!rc) rc = ensure(ctx, ctx->val_out, (size_t)(step + 1) * sizeof(double));
   if (!rc) rc = ensure(ctx, ctx->gain_out, (size_t)(step + 1) * sizeof(double));
   if (rc) return rc;
+  if (!rc && ctx->timing) rc = ensure_events(ctx, 4 * (size_t)(step + 1));  // run_update records slot 4 step + 3
+  if (rc) return rc;
   if (!ctx->tie_err) CU(cudaMallocAsync((void**)&ctx->tie_err, sizeof(int), ctx->stream));
   CU(cudaMemsetAsync(ctx->tie_err, 0, sizeof(int), ctx->stream));
   CU(cudaMemcpyAsync(ctx->tie_all.p, gathered, (size_t)world * (TIE_CAP + 1) * sizeof(double2),
@@ -1748,6 +1762,10 @@ int ebc_shard_set_range(ebc_ctx* ctx, int64_t c0, int64_t c1) {
   if (c0 < 0 || c1 < c0 || c1 > ctx->n)
     return fail(ctx, EBC_EINVAL,
                 "candidate range [" + std::to_string(c0) + ", " + std::to_string(c1) + ") outside [0, n)");
+  if (c0 < c1 && (c0 % tc::M) != 0)
+    return fail(ctx, EBC_EINVAL,
+                "candidate range start " + std::to_string(c0) + " is not a multiple of " + std::to_string(tc::M));
+  // cached graphs and eager ladder records are keyed by the range (greedy_run)
   ctx->c0 = c0;
   ctx->c1 = c1;
   return EBC_OK;
@@ -1874,11 +1892,10 @@ int ebc_eval_multiset(ebc_ctx* ctx, const int64_t* offsets, const int64_t* idx, 
   if (!rc) rc = ensure(ctx, ctx->ms_out, (size_t)l * sizeof(double));
   if (rc) return rc;
   const int64_t batch = std::min<int64_t>(l, 65535);
-  rc = ensure(ctx, ctx->ms_part, (size_t)l * ctx->nchunks * sizeof(double));
-  if (rc) return rc;
-  cudaEvent_t a, b;
-  CU(cudaEventCreate(&a));
-  CU(cudaEventCreate(&b));
+  ScopedEvent ea, eb;  // destroyed on every return path
+  CU(cudaEventCreate(&ea.e));
+  CU(cudaEventCreate(&eb.e));
+  cudaEvent_t a = ea.e, b = eb.e;
   CU(cudaMemcpyAsync(ctx->ms_off.p, offsets, (size_t)(l + 1) * sizeof(int64_t), cudaMemcpyHostToDevice,
                      ctx->stream));
   if (nnz > 0)
@@ -1898,6 +1915,11 @@ int ebc_eval_multiset(ebc_ctx* ctx, const int64_t* offsets, const int64_t* idx, 
       if (rc == EBC_OK) done = true;
       else if (rc != EBC_EINVAL) return rc;
     }
+  }
+  if (!done) {
+    // dense fallback: l x nchunks partials, allocated only when it runs
+    rc = ensure(ctx, ctx->ms_part, (size_t)l * ctx->nchunks * sizeof(double));
+    if (rc) return rc;
   }
   for (int64_t s0 = 0; !done && s0 < l; s0 += batch) {
     const int64_t nb = std::min<int64_t>(batch, l - s0);
@@ -1923,8 +1945,6 @@ int ebc_eval_multiset(ebc_ctx* ctx, const int64_t* offsets, const int64_t* idx, 
   CU(cudaStreamSynchronize(ctx->stream));
   float ms = 0;
   CU(cudaEventElapsedTime(&ms, a, b));
-  cudaEventDestroy(a);
-  cudaEventDestroy(b);
   ctx->last_ms[0] = ms;
   ctx->last_ms[1] = 0;
   ctx->last_ms[2] = 0;

@@ -8,6 +8,9 @@ tests/test_oracle.py (in the container that has the reference).
 
 from __future__ import annotations
 
+from pathlib import Path
+from typing import Tuple
+
 import numpy as np
 
 
@@ -27,6 +30,39 @@ def _regime_curve(dims: int, regime: int) -> np.ndarray:
     tail = t >= 0.85
     curve[tail] = plateau * np.exp(-(t[tail] - 0.85) / 0.05)
     return curve
+
+
+def check_spec(n_cycles: int, dims: int, n_regimes: int, cycles_per_regime: int, noise_scale: float) -> None:
+    """SurrogateSpec's validation and messages (cli.py:121-131)."""
+    if min(n_cycles, dims, n_regimes, cycles_per_regime) < 1:
+        raise ValueError("all surrogate counts must be >= 1")
+    if n_regimes * cycles_per_regime != n_cycles:
+        raise ValueError(f"n_regimes * cycles_per_regime must equal n_cycles "
+                         f"({n_regimes} * {cycles_per_regime} != {n_cycles})")
+    if noise_scale < 0:
+        raise ValueError("noise_scale must be >= 0")
+
+
+def labels(n_regimes: int, cycles_per_regime: int) -> np.ndarray:
+    """Per-row regime labels of the regime-ordered blocks (cli.py:165)."""
+    return np.repeat(np.arange(n_regimes), cycles_per_regime)
+
+
+def labels_path(output: str) -> str:
+    """The regime-label sidecar next to `output`: stem + "_labels" (cli.py:176-178)."""
+    p = Path(output)
+    return str(p.with_name(p.stem + "_labels" + (p.suffix or ".csv")))
+
+
+def write(output: str, n_cycles: int, dims: int, n_regimes: int, cycles_per_regime: int,
+          noise_scale: float = 0.01, seed: int = 0) -> Tuple[str, str]:
+    """Surrogate CSV plus the regime-label sidecar (cli.py:181-187); returns both paths."""
+    check_spec(n_cycles, dims, n_regimes, cycles_per_regime, noise_scale)
+    X = surrogate(n_cycles, dims, n_regimes, noise_scale, seed)
+    np.savetxt(output, X, delimiter=",", fmt="%.17g")
+    lp = labels_path(output)
+    np.savetxt(lp, labels(n_regimes, cycles_per_regime), fmt="%d")
+    return output, lp
 
 
 def surrogate(n_cycles: int, dims: int, n_regimes: int, noise_scale: float = 0.01,

@@ -107,6 +107,32 @@ def test_multiset_validation_and_csr():
         ms.validate_indices(3)
 
 
+def test_multiset_sets_are_read_only():
+    """The CSR arrays are built once; the sets they mirror cannot change under them."""
+    ms = eb.EvalMultiset([[3, 1], [2]])
+    off, idx = ms.csr()
+    for mutate in (lambda: ms.sets[0].append(5), lambda: ms.sets.__setitem__(0, [0]),
+                   lambda: ms.sets[1].__setitem__(0, 0), lambda: ms.sets.append([1])):
+        with pytest.raises(TypeError, match="read-only"):
+            mutate()
+    assert ms.sets == [[3, 1], [2]] and ms.csr()[1] is idx
+    assert ms.sets[0] + [7] == [3, 1, 7]  # building a new list from a set still works
+    with pytest.raises(ValueError):
+        idx[0] = 9
+
+
+def test_ground_compute_view():
+    """GroundMatrix.compute_view (reference core.py:82-92): widened to the
+    arithmetic dtype, cached, read-only."""
+    X = np.arange(6, dtype=np.float64).reshape(3, 2) / 3
+    g16 = eb.GroundMatrix(X, eb.Precision.FP16_STORAGE)
+    v = g16.compute_view()
+    assert v.dtype == np.float32 and v is g16.compute_view() and not v.flags.writeable
+    np.testing.assert_array_equal(v, g16.data.astype(np.float32))
+    g64 = eb.GroundMatrix(X)
+    assert g64.compute_view() is g64.data
+
+
 def test_budget_validation():
     # test_optimize.py:11-18 of the reference
     with pytest.raises(ValueError):

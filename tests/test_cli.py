@@ -53,9 +53,32 @@ def test_exit_codes_usage_and_data(tmp_path, capsys):
 def test_surrogate_writer_matches_generator(tmp_path):
     from paper_2105_12026_b200.surrogate import surrogate
     out = tmp_path / "s.csv"
-    assert cli.main(["surrogate", "--cycles", "50", "--dims", "8", "--output", str(out)]) == cli.EXIT_OK
+    assert cli.main(["surrogate", "--cycles", "50", "--dims", "8", "--cycles-per-regime", "10",
+                     "--output", str(out)]) == cli.EXIT_OK
     data, _ = cli.load_csv(str(out))
     np.testing.assert_array_equal(data, surrogate(50, 8, 5, 0.01, 0))
+    # the regime-label sidecar (reference cli.py:176-187): stem + "_labels"
+    lab = np.loadtxt(tmp_path / "s_labels.csv", dtype=np.int64)
+    np.testing.assert_array_equal(lab, np.repeat(np.arange(5), 10))
+
+
+def test_surrogate_spec_contract(tmp_path, capsys):
+    """SurrogateSpec validation (reference cli.py:121-131): the default
+    --cycles-per-regime is 200, so --cycles 1000 --regimes 5 is the default case
+    and any product mismatch is a data error naming both sides."""
+    out = str(tmp_path / "d.csv")
+    assert cli.main(["surrogate", "--dims", "4", "--output", out]) == cli.EXIT_OK
+    assert np.loadtxt(out, delimiter=",").shape == (1000, 4)
+    assert cli.main(["surrogate", "--cycles", "100", "--regimes", "5", "--output", out]) == cli.EXIT_DATA
+    assert "n_regimes * cycles_per_regime must equal n_cycles (5 * 200 != 100)" in capsys.readouterr().err
+    assert cli.main(["surrogate", "--noise", "-1", "--output", out]) == cli.EXIT_DATA
+
+
+def test_summarize_accepts_reference_threads_flag():
+    """--threads (reference cli.py:247) parses; the device path ignores it."""
+    args = cli.build_parser().parse_args(["summarize", "x.csv", "-k", "2", "--threads", "4"])
+    assert args.threads == 4
+    assert cli.main(["summarize", "x.csv", "-k", "2", "--threads", "0"]) == cli.EXIT_USAGE
 
 
 @pytest.mark.gpu

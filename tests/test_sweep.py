@@ -84,6 +84,20 @@ def test_run_sweep_validates_before_touching_the_device():
         sweep.run_sweep("l", [3], base, ["b200"], repeats=0)
     with pytest.raises(ValueError, match="unknown backend"):
         sweep.run_sweep("l", [3], base, ["batched:4"])
+    with pytest.raises(ValueError, match="thread count"):
+        sweep.run_sweep("l", [3], base, ["ref-batched:0"])
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_SRC), reason="reference not present (GPU box)")
+def test_run_sweep_reference_cpu_columns(monkeypatch):
+    """The CPU baseline columns run the reference package's own backends."""
+    monkeypatch.setenv("EBCSUM_PATH", REF_SRC)
+    base = sweep.ProblemSpec(n=300, l=8, k=3, dims=4, seed=1)
+    rep = sweep.run_sweep("l", [4, 8], base, ["ref-naive", "ref-batched:2"], repeats=2)
+    assert rep.backends == ["ref-naive", "ref-batched:2"]
+    assert all(len(rep.runtimes[(v, b)]) == 2 for v in (4, 8) for b in rep.backends)
+    c = {(x.baseline, x.subject): x for x in rep.comparisons}
+    assert c[("ref-naive", "ref-naive")].mean == 1.0
 
 
 def test_cli_bench_exit_codes(capsys):
@@ -96,8 +110,9 @@ def test_cli_bench_exit_codes(capsys):
 @pytest.mark.gpu
 def test_run_sweep_on_the_device(tmp_path):
     base = sweep.ProblemSpec(n=600, l=16, k=4, dims=8, seed=2)
-    rep = sweep.run_sweep("l", [8, 16], base, ["b200", "b200:4"], repeats=2)
-    assert set(rep.runtimes) == {(8, "b200"), (8, "b200:4"), (16, "b200"), (16, "b200:4")}
+    cols = ["b200", "b200:4"] + (["ref-batched:2"] if sweep._reference_package() is not None else [])
+    rep = sweep.run_sweep("l", [8, 16], base, cols, repeats=2)
+    assert set(rep.runtimes) == {(v, b) for v in (8, 16) for b in cols}
     assert all(len(v) == 2 and min(v) > 0 for v in rep.runtimes.values())
     out = tmp_path / "sweep.md"
     assert cli.main(["bench", "--axis", "k", "--values", "2,5", "--n", "400", "--l", "20", "--dims", "6",
