@@ -3,16 +3,25 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
 
 One *step* = one full Greedy(k) run of the configured workload (default C2:
-k=50, N=100,000, d=100, fp32, Gaussian seed 1) with V already
-resident in HBM.  value = point-candidate distance evaluations per second,
-E = N * sum_{s<k} (N - s) per run, over all ranks.  For N>1 (torchrun, one rank
-per GPU) candidates are sharded across ranks (strong scaling: the same total
-work), with an all-gather of (index, gain) records per Greedy step.
+k=50, N=100,000, d=100, fp32, Gaussian seed 1; --config C4 is
+the north star's scaling configuration) with V already resident in HBM.
+value = point-candidate distance evaluations per second, E = N * sum_{s<k}
+(N - s) per run, over all ranks.
+
+Multi-GPU: one rank per GPU.  Under torchrun (WORLD_SIZE set) every rank
+builds its own context and the candidates are sharded across ranks (strong
+scaling: the same total work), with the per-step exchange on the devices (NCCL
+all-gather of 128-B tie-set frontiers) and an end-of-run cross-rank check of
+the selection.  ``--gpus N`` without torchrun re-launches itself as N ranks
+(torch.distributed.run on 127.0.0.1) and fails if fewer than N GPUs are
+visible.
 
 Timing: W untimed warm-up runs; then K runs, each bracketed by a barrier and
 device syncs, timed with CUDA events recorded on the library's own stream;
-max over ranks.  L2 (126 MB) is flushed before every timed run.  SM clocks
-are sampled with nvidia-smi during the timed region.
+max over ranks.  The timed runs are CUDA-graph replays with the per-step
+kernel-family events captured inside the graph (the roofline's screen time).
+L2 (126 MB) is flushed before every timed run.  SM clocks are sampled with
+nvidia-smi during the timed region.
 
 `e2e` runs the same workload through the public API from host data every
 step: EbcFunction(GroundMatrix) (host->device copy of V + baseline) then
@@ -218,6 +227,95 @@ def run_reference(args):
 
 # ------------------------------------------------------------------ our arm
 
+def tensor_roofline(info, rung, d, work_pairs, screen_ms, E):
+    """Roofline object of the tensor screen: 2 P d flops per evaluated pair (P
+    products) over the screen's own time, against the measured BF16 peak."""
+    kind = 3 if rung == 0 else int(info[2])
+    kname = {0: "3xTF32 kind::tf32", 1: "BF16x3 kind::f16", 2: "FP16x1 kind::f16",
+             3: "FP16x1-rounded kind::f16"}[kind]
+    nprod = 1 if kind in (2, 3) else 3
+    peaks = load_measured_peaks()
+    # the screen runs inside a long step (a whole Greedy run, >= 100 ms of
+    # back-to-back launches): the SUSTAINED measured BF16 figure is its peak
+    # (B200_PROFILING / task contract); the burst figure is reported beside it
+    burst = peaks.get("bf16_tflops") if peaks else None
+    sust = peaks.get("bf16_tflops_sustained") if peaks else None
+    bf16 = sust or burst
+    base = bf16 if bf16 else 1590.0
+    tpeak = base / 2.0 if kind == 0 else base
+    wexec = float(work_pairs) if work_pairs and work_pairs > 0 else float(E)
+    tach = 2.0 * nprod * d * wexec / (screen_ms * 1e-3) / 1e12
+    return {
+        "bound": "tensor",
+        "kernel": "k_screen_tc (tcgen05 %s anchored Gram screen, TMEM operands and accumulators)" % kname,
+        "achieved": tach, "peak": tpeak, "unit": "TFLOP/s", "frac": tach / tpeak,
+        "peak_burst": (burst / 2.0 if kind == 0 else burst) if burst else None,
+        "frac_vs_burst": (tach / (burst / 2.0 if kind == 0 else burst)) if burst else None,
+        "peak_source": (("MEASURED_PEAKS.json bf16_tflops_sustained" if sust else
+                         "MEASURED_PEAKS.json bf16_tflops") if bf16 else "fallback 1.59 PF bf16")
+                       + (" / 2 (TF32)" if kind == 0 else "") + "; nominal dense BF16 = 2250 TFLOP/s",
+        "work": "%dd tensor flops per evaluated point-candidate pair (%d product%s, d not padded)"
+                % (2 * nprod, nprod, "s of the split" if nprod > 1 else " of the fp16 values"),
+        "pairs_evaluated": wexec, "pairs_evaluated_frac_of_E": wexec / E,
+        "tmem_read": {"achieved": 4.0 * wexec / (screen_ms * 1e-3) / 1e9,
+                      "peak": TMEM_LD_BPC * 148 * 1.965e9 / 1e9, "unit": "GB/s",
+                      "frac": (4.0 * wexec / (screen_ms * 1e-3)) / (TMEM_LD_BPC * 148 * 1.965e9),
+                      "work": "4 B fp32 accumulator per point-candidate pair; peak = tcgen05.ld throughput "
+                              "measured with 8 loading warps per SM (the screen's epilogue), "
+                              "335 B/clk/SM x 148 SM x 1.965 GHz (profiles/r01_microbench_tmem_ld.txt)"},
+        "screen_rung": rung,
+        "screen_info": {"mode": info[0], "tile_points": info[1],
+                        "operands": {0: "tf32 split", 1: "bf16 split", 2: "fp16",
+                                     3: "fp32 rounded to fp16 (scaled)"}[kind], "kpad": info[3]},
+    }
+
+
+def screen_roofline(info, rung, d, work_pairs, screen_ms, step_ms, E, config):
+    """Roofline of the dominant kernel (the candidate screen) for one GPU's share
+    of the run: its evaluated pairs over its own time (CUDA events on the
+    library stream inside the timed region)."""
+    achieved = 2.0 * d * E / (screen_ms * 1e-3)
+    fma_equiv = {"achieved": achieved / 1e12, "peak": PEAK_FP32_OPS / 1e12, "unit": "TFLOP/s",
+                 "frac": achieved / PEAK_FP32_OPS,
+                 "work": "W = 2d FP32 FMA-pipe ops per point-candidate pair (SURVEY.md §8(d)), not redefined; "
+                         "peak = 148 SM x 128 lanes x 1.965 GHz (nominal)"}
+    traffic, _prof = load_profile_traffic(config)
+    if rung in (0, 1):
+        line = tensor_roofline(info, rung, d, work_pairs, screen_ms, E)
+        line["traffic"] = traffic
+        line["fma_equiv"] = dict(fma_equiv, flag="frac > 1.0 expected: tensor cores vs the FP32 FMA roofline")
+    else:
+        line = {"bound": "fma", "kernel": "k_screen (fused distance->min->sum on the FP32 FMA pipe)",
+                "achieved": fma_equiv["achieved"], "peak": fma_equiv["peak"], "unit": "TFLOP/s",
+                "frac": fma_equiv["frac"], "traffic": traffic, "work": fma_equiv["work"],
+                "flag": ("frac > 1.0: the Gram rung issues d FFMA per pair against the direct-form W = 2d"
+                         if achieved > PEAK_FP32_OPS else None), "screen_rung": rung}
+    line["screen_ms_per_step"] = screen_ms
+    line["screen_share_of_step"] = screen_ms / step_ms
+    return line
+
+
+def update_roofline(n_pts, d, k, update_ms):
+    """Second ceiling named by the north star: the cached-min update (K4) is
+    HBM-bound; algorithmic bytes per step = N (4 pitch + 8 cm + 8 e0d + 8 term)
+    (the seed refresh of changed points not counted), against the measured HBM
+    copy bandwidth; its time is the update family per step (CUDA events)."""
+    peaks = load_measured_peaks()
+    hbm = (peaks or {}).get("hbm_gbs")
+    per_step_ms = update_ms / k
+    pitch = (d + 3) // 4 * 4
+    if (pitch // 4) % 2 == 0:
+        pitch += 4
+    ubytes = n_pts * (4.0 * pitch + 24.0)
+    ach = ubytes / (per_step_ms * 1e-3) / 1e9
+    return {"bound": "hbm", "kernel": "k_update_fused (cached-min update + fixed-order f(S), one launch)",
+            "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": (ach / hbm) if hbm else None,
+            "bytes_per_step": ubytes, "us_per_step": per_step_ms * 1e3,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if hbm else None,
+            "note": "V may be partly L2-resident between steps (40-64 MB vs 126 MB L2); algorithmic bytes, "
+                    "not DRAM bytes"}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -228,17 +326,24 @@ def run_ours(args):
     ndev = torch.cuda.device_count()
     if ndev < 1:
         raise RuntimeError("bench.py needs a CUDA device (the b200 path has no CPU fallback)")
+    if world != args.gpus:
+        raise RuntimeError(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
+    shared_gpu = os.environ.get("EBC_BENCH_SHARE_GPU") == "1"
+    if world > ndev and not shared_gpu:
+        raise RuntimeError(f"{world} ranks but only {ndev} visible GPU(s): one rank per GPU "
+                           f"(EBC_BENCH_SHARE_GPU=1 runs the gloo test mode)")
     dev_index = local_rank % ndev
     torch.cuda.set_device(dev_index)
     dev = torch.device("cuda", dev_index)
     distributed = world > 1
     if distributed:
-        backend = "nccl" if world <= ndev else "gloo"  # gloo only for >1 rank per GPU (test boxes)
+        backend = "nccl" if world <= ndev else "gloo"  # gloo only in the shared-GPU test mode
         dist.init_process_group(backend, device_id=dev if backend == "nccl" else None)
     os.environ["EBC200_DEVICE"] = str(dev_index)
+    nccl = distributed and dist.get_backend() == "nccl"
 
     import paper_2105_12026_b200 as eb
-    from paper_2105_12026_b200 import _native, optimize
+    from paper_2105_12026_b200 import optimize
     from paper_2105_12026_b200.sharded import greedy_maximize_sharded
 
     X, k = workload(args.config)
@@ -249,26 +354,27 @@ def run_ours(args):
     lib_stream = torch.cuda.ExternalStream(f._lib.ebc_stream(f.native_context), device=dev)
     budget = eb.OptimizerBudget(k=k)
 
-    def one_run():
+    def one_run(fx=f):
         if distributed:
-            return greedy_maximize_sharded(f, budget)
-        return eb.greedy_maximize(f, budget)
+            return greedy_maximize_sharded(fx, budget)
+        return eb.greedy_maximize(fx, budget)
 
     def barrier():
         if distributed:
             dist.barrier()
 
-    # warm-up
+    # per-step CUDA events of the kernel families are captured into the run's
+    # graph, so warm-up (eager run, capture) and the timed replays share one key
+    optimize.set_timing(f, True)
     ref_sel = None
     for _ in range(args.warmup):
-        s = one_run()
-        ref_sel = s.selected
+        ref_sel = one_run().selected
 
-    optimize.set_timing(f, True)
     clocks = ClockSampler(dev_index)
     clocks.start()
     times_ms, screen_ms, update_ms, launches, work = [], [], [], 0, []
     stats = None
+    timed_families = (not distributed) or nccl
     for _ in range(args.steps):
         flush_l2(torch, dev)
         torch.cuda.synchronize(dev)
@@ -284,7 +390,7 @@ def run_ours(args):
         # NCCL path: the whole run is one native call (graph); host-driven
         # (gloo) path: the count of the last per-step native call
         launches += optimize.last_launches(f)
-        if not distributed:
+        if timed_families:
             t = optimize.last_timings(f)
             screen_ms.append(t[0])
             update_ms.append(t[2])
@@ -295,15 +401,15 @@ def run_ours(args):
     clk = clocks.stop()
     optimize.set_timing(f, False)
 
-    step_ms = float(np.mean(times_ms))
-    if distributed:
-        t = torch.tensor([step_ms], dtype=torch.float64, device=dev if dist.get_backend() == "nccl" else "cpu")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        step_ms = float(t.item())
     E = evals_per_run(n, k)
-    value = E / (step_ms * 1e-3)
+    mine = {"step_ms": float(np.mean(times_ms)), "launches": int(launches),
+            "screen_ms": float(np.mean(screen_ms)) if screen_ms else None,
+            "update_ms": float(np.mean(update_ms)) if update_ms else None,
+            "work": float(np.mean(work)) if work else None, "stats": stats,
+            "selected": s.selected, "value": s.value}
 
-    # e2e through the public API from host data (one rank's view; rank 0 reports)
+    # e2e through the public API from host data: EbcFunction(GroundMatrix) (V
+    # host->device) + greedy_maximize(_sharded) (results device->host), wall clock
     e2e_ms = []
     h2d = X.nbytes + d * 8
     d2h = k * 3 * 8 + 8
@@ -311,142 +417,93 @@ def run_ours(args):
         barrier()
         t0 = time.perf_counter()
         f2 = eb.EbcFunction(g, device=dev_index)
-        s2 = greedy_maximize_sharded(f2, budget) if distributed else eb.greedy_maximize(f2, budget)
+        one_run(f2)
         t1 = time.perf_counter()
         barrier()
         e2e_ms.append((t1 - t0) * 1e3)
         f2.close()
-    e2e_step = float(np.median(e2e_ms))
+    mine["e2e_ms"] = float(np.median(e2e_ms))
+
+    ranks = [mine]
     if distributed:
-        t = torch.tensor([e2e_step], dtype=torch.float64, device=dev if dist.get_backend() == "nccl" else "cpu")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_step = float(t.item())
+        ranks = [None] * world
+        dist.all_gather_object(ranks, mine)
+    if any(r["selected"] != mine["selected"] or r["value"] != mine["value"] for r in ranks):
+        raise RuntimeError("ranks disagree on the selection")
 
     if rank != 0:
         if distributed:
             dist.destroy_process_group()
         return 0
 
+    step_ms = max(r["step_ms"] for r in ranks)  # device time, max over ranks
+    e2e_step = max(r["e2e_ms"] for r in ranks)
+    value = E / (step_ms * 1e-3)
     line = {
         "metric": METRIC, "value": value, "unit": "point-candidate evals/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32" if prec is eb.Precision.FP32 else "f16-storage/f32",
         "data": "synthetic (seeded Gaussian / surrogate, tests/golden/datasets.py)",
         "config": {"workload": CONFIG_DESC[args.config], "config_id": args.config, "N": n, "d": d, "k": k,
-                   "evals_per_step": E, "parallelism": f"candidate-sharded x{world}" if distributed else "1 GPU",
-                   "l2": "flushed (256 MB write) before every timed run; V is 40-64 MB"},
+                   "evals_per_step": E,
+                   "parallelism": (f"candidate-sharded x{world} ({'NCCL device exchange' if nccl else 'gloo host exchange'})"
+                                   if distributed else "1 GPU"),
+                   "l2": "flushed (256 MB write) before every timed run; V is 40-64 MB",
+                   "timed_runs": "CUDA-graph replays (per-step family events captured in the graph)"},
         "selected_head": s.selected[:5], "summary_value": s.value,
         "clocks": clk,
         "e2e": {"value": E / (e2e_step * 1e-3), "unit": "point-candidate evals/s", "ms_per_step": e2e_step,
-                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "path": "EbcFunction(GroundMatrix) + greedy_maximize via libebc200.so C-ABI, pageable host buffers"},
+                "h2d_bytes_per_step": int(h2d) * world, "d2h_bytes_per_step": int(d2h) * world,
+                "path": "EbcFunction(GroundMatrix) + greedy_maximize%s via libebc200.so C-ABI, pageable host buffers"
+                        % ("_sharded (every rank uploads V)" if distributed else "")},
+        "gpu_launches": int(sum(r["launches"] for r in ranks)),
     }
-    if not distributed:
-        scr = float(np.mean(screen_ms))
-        ops = 2.0 * d * E
-        achieved = ops / (scr * 1e-3)
-        traffic, prof = load_profile_traffic(args.config)
-        rung = stats[2] if stats else -1
-        fma_equiv = {"achieved": achieved / 1e12, "peak": PEAK_FP32_OPS / 1e12, "unit": "TFLOP/s",
-                     "frac": achieved / PEAK_FP32_OPS,
-                     "work": "W = 2d FP32 FMA-pipe ops per point-candidate pair (SURVEY.md §8(d)), not redefined; "
-                             "peak = 148 SM x 128 lanes x 1.965 GHz (nominal)"}
-        if rung in (0, 1):
-            # tensor rung.  BF16 split (kind::f16): 3 products = 6d flops per pair
-            # against the driver-measured dense BF16 peak; FP16 grounds (kind::f16,
-            # one exact product) 2d flops per pair, same peak; TF32 split
-            # (kind::tf32, half the BF16 rate on sm_100): 6d against measured BF16 / 2
-            # rung 0 = the fast rung (fp32 values rounded to FP16, one product)
-            info = optimize.screen_info(f)
-            kind = 3 if rung == 0 else int(info[2])
-            kname = {0: "3xTF32 kind::tf32", 1: "BF16x3 kind::f16", 2: "FP16x1 kind::f16",
-                     3: "FP16x1-rounded kind::f16"}[kind]
-            nprod = 1 if kind in (2, 3) else 3
-            peaks = load_measured_peaks()
-            # the screen runs inside a long step (a whole Greedy run, >= 100 ms of
-            # back-to-back launches): the SUSTAINED measured BF16 figure is its peak
-            # (B200_PROFILING / task contract); the burst figure is reported beside it
-            burst = peaks.get("bf16_tflops") if peaks else None
-            sust = peaks.get("bf16_tflops_sustained") if peaks else None
-            bf16 = sust or burst
-            base = bf16 if bf16 else 1590.0
-            tpeak = base / 2.0 if kind == 0 else base
-            # pairs the screen actually evaluated: executed 128 x 128 tiles after the
-            # certified tile-pair pruning (padding included); E counts every pair
-            wexec = float(np.mean(work)) if work and np.mean(work) > 0 else float(E)
-            tach = 2.0 * nprod * d * wexec / (scr * 1e-3) / 1e12
-            line["roofline"] = {
-                "bound": "tensor",
-                "kernel": "k_screen_tc (tcgen05 %s anchored Gram screen, TMEM operands and accumulators)" % kname,
-                "achieved": tach, "peak": tpeak, "unit": "TFLOP/s", "frac": tach / tpeak,
-                "peak_burst": (burst / 2.0 if kind == 0 else burst) if burst else None,
-                "frac_vs_burst": (tach / (burst / 2.0 if kind == 0 else burst)) if burst else None,
-                "peak_source": (("MEASURED_PEAKS.json bf16_tflops_sustained" if sust else
-                                 "MEASURED_PEAKS.json bf16_tflops") if bf16 else "fallback 1.59 PF bf16")
-                               + (" / 2 (TF32)" if kind == 0 else "") + "; nominal dense BF16 = 2250 TFLOP/s",
-                "traffic": traffic,
-                "work": "%dd tensor flops per evaluated point-candidate pair (%d product%s, d not padded)"
-                        % (2 * nprod, nprod, "s of the split" if nprod > 1 else " of the fp16 values"),
-                "fma_equiv": dict(fma_equiv, flag="frac > 1.0 expected: tensor cores vs the FP32 FMA roofline"),
-                # second ceiling of the same kernel: every pair's fp32 accumulator is
-                # read once from TMEM (tcgen05.ld), 64 B/clk/SM
-                "pairs_evaluated": wexec, "pairs_evaluated_frac_of_E": wexec / E,
-                "tmem_read": {"achieved": 4.0 * wexec / (scr * 1e-3) / 1e9,
-                              "peak": TMEM_LD_BPC * 148 * 1.965e9 / 1e9, "unit": "GB/s",
-                              "frac": (4.0 * wexec / (scr * 1e-3)) / (TMEM_LD_BPC * 148 * 1.965e9),
-                              "work": "4 B fp32 accumulator per point-candidate pair; peak = tcgen05.ld throughput "
-                                      "measured with 8 loading warps per SM (the screen's epilogue), "
-                                      "335 B/clk/SM x 148 SM x 1.965 GHz (profiles/r01_microbench_tmem_ld.txt)"},
-                "screen_ms_per_step": scr, "screen_share_of_step": scr / step_ms, "screen_rung": rung,
-                "screen_info": {"mode": info[0], "tile_points": info[1],
-                                "operands": {0: "tf32 split", 1: "bf16 split", 2: "fp16",
-                                             3: "fp32 rounded to fp16 (scaled)"}[kind], "kpad": info[3]},
-            }
-        else:
-            line["roofline"] = {
-                "bound": "fma", "kernel": "k_screen (fused distance->min->sum on the FP32 FMA pipe)",
-                "achieved": fma_equiv["achieved"], "peak": fma_equiv["peak"], "unit": "TFLOP/s",
-                "frac": fma_equiv["frac"], "traffic": traffic, "work": fma_equiv["work"],
-                "flag": ("frac > 1.0: the Gram rung issues d FFMA per pair against the direct-form W = 2d"
-                         if achieved > PEAK_FP32_OPS else None),
-                "screen_ms_per_step": scr, "screen_share_of_step": scr / step_ms, "screen_rung": rung,
-            }
-        line["window"] = {"sum": stats[0], "max": stats[1], "steps": stats[3]} if stats else None
-        # second ceiling named by the north star: the cached-min update (K4) is
-        # HBM-bound; algorithmic bytes per step = N (4 pitch + 8 cm + 8 e0d + 8
-        # term) plus the seed refresh of changed points (not counted), against
-        # the measured HBM copy bandwidth; its time is the update family per step
-        # (k_update_terms + the fixed-order reduction)
-        if update_ms and np.mean(update_ms) > 0:
-            peaks = load_measured_peaks()
-            hbm = (peaks or {}).get("hbm_gbs")
-            per_step_ms = float(np.mean(update_ms)) / k
-            n_pts = X.shape[0]
-            pitch = (d + 3) // 4 * 4
-            if (pitch // 4) % 2 == 0:
-                pitch += 4
-            ubytes = n_pts * (4.0 * pitch + 24.0)
-            ach = ubytes / (per_step_ms * 1e-3) / 1e9
-            line["update_roofline"] = {
-                "bound": "hbm", "kernel": "k_update_terms + k_update_reduce (cached-min update, fixed-order f(S))",
-                "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": (ach / hbm) if hbm else None,
-                "bytes_per_step": ubytes, "us_per_step": per_step_ms * 1e3,
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if hbm else None,
-                "note": "V may be partly L2-resident between steps (40-64 MB vs 126 MB L2); algorithmic bytes, not DRAM bytes"}
-        line["gpu_launches"] = int(launches)
-        if rank == 0 and not args.no_cpu_baseline:
-            threads = len(os.sched_getaffinity(0))
-            rate, desc = cpu_sample(X.astype(np.float64), threads, float(os.environ.get("EBC_CPU_SECONDS", "10")))
-            line["cpu_baseline"] = {"value": rate, "unit": "point-candidate evals/s", "cores": threads,
-                                    "kind": "port", "sample": desc}
-    else:
-        line["gpu_launches"] = int(launches)
-        if dist.get_backend() != "nccl":
-            line["gpu_launches_note"] = "host-driven exchange: rank 0's last native step call per run"
+    if distributed:
+        line["per_rank_ms_per_step"] = [r["step_ms"] for r in ranks]
+    if timed_families and all(r["screen_ms"] for r in ranks):
+        info = optimize.screen_info(f)
+        # one GPU's share: the slowest rank's screen over that rank's own pairs
+        slow = max(range(world), key=lambda r: ranks[r]["screen_ms"])
+        rr = ranks[slow]
+        rung = rr["stats"][2] if rr["stats"] else -1
+        e_rank = E / world
+        line["roofline"] = screen_roofline(info, rung, d, rr["work"], rr["screen_ms"], rr["step_ms"], e_rank,
+                                           args.config)
+        if distributed:
+            line["roofline"]["rank"] = slow
+            line["roofline"]["per_rank_frac"] = [
+                screen_roofline(info, (q["stats"] or [0, 0, -1])[2], d, q["work"], q["screen_ms"], q["step_ms"],
+                                e_rank, args.config)["frac"] for q in ranks]
+        line["window"] = {"sum": rr["stats"][0], "max": rr["stats"][1], "steps": rr["stats"][3]} if rr["stats"] else None
+        if rr["update_ms"]:
+            line["update_roofline"] = update_roofline(n, d, k, rr["update_ms"])
+    if not args.no_cpu_baseline:
+        threads = len(os.sched_getaffinity(0))
+        rate, desc = cpu_sample(X.astype(np.float64), threads, float(os.environ.get("EBC_CPU_SECONDS", "10")))
+        line["cpu_baseline"] = {"value": rate, "unit": "point-candidate evals/s", "cores": threads,
+                                "kind": "port", "sample": desc}
     print(json.dumps(line), flush=True)
     if distributed:
         dist.destroy_process_group()
     return 0
+
+
+def spawn_ranks(args, argv):
+    """--gpus N > 1 outside torchrun: re-launch this script as N ranks, one per
+    GPU (torch.distributed.run on 127.0.0.1); refuses to oversubscribe GPUs."""
+    import socket
+
+    import torch
+    ndev = torch.cuda.device_count()
+    if args.gpus > ndev and os.environ.get("EBC_BENCH_SHARE_GPU") != "1":
+        log(f"error: --gpus {args.gpus} needs {args.gpus} GPUs, {ndev} visible")
+        return 2
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
+    return subprocess.call(cmd)
 
 
 def main(argv=None):
@@ -457,12 +514,17 @@ def main(argv=None):
     ap.add_argument("--config", default=os.environ.get("EBC_BENCH_CONFIG", "C2"), choices=sorted(CONFIG_DESC))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    args = ap.parse_args(argv)
+    raw = list(sys.argv[1:] if argv is None else argv)
+    args = ap.parse_args(raw)
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
     if args.warmup < 3:
         log("note: warm-up raised to the contract minimum of 3")
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args, raw)
     return run_ours(args)
 
 

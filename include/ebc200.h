@@ -84,6 +84,7 @@ int ebc_greedy(ebc_ctx* ctx, int32_t k, int64_t* out_sel, double* out_val, doubl
  *   (host exchange across ranks; global pick, see paper_2105_12026_b200/sharded.py)
  *   ebc_shard_commit -> fold the globally chosen index into the cached minima.
  */
+/* c0 must be a multiple of 128 (the screens' candidate block) unless c0 == c1. */
 int ebc_shard_set_range(ebc_ctx* ctx, int64_t c0, int64_t c1);
 
 /* Screen + refine the local candidates for the current step.  Writes up to
@@ -113,17 +114,23 @@ int ebc_shard_fetch(const ebc_ctx* ctx, int64_t* out_idx, double* out_gain, int6
  * NVLink/NVSwitch), no host round trip per step ----
  * Replaces the per-step host loop of greedy_maximize (optimize.py:75-88) across
  * ranks.  Per step every rank screens its candidate range, computes the exact
- * gains of its certified window, and contributes its local tie set
- * {c : value_c >= top_r - 1e-12 max(1,|top_r|)} as fixed-size records
- * (TIE_CAP entries); one ncclAllGather of the records, then every rank applies
- * the reference rule (optimize.py:83-85) to the identical union and folds the
- * winner into its cached minima.  The k-step loop is graph-captured like
- * ebc_greedy.  NCCL is dlopen'ed (libnccl.so.2) on first use.
+ * gains of its certified window, reduces its local tie set
+ * {c : value_c >= top_r - 1e-12 max(1,|top_r|)} to its index-ordered Pareto
+ * frontier (at most TIE_CAP = ebc_tie_cap() records of {index, gain} plus a
+ * count: 128 B per rank), one ncclAllGather of the records, then every rank
+ * applies the reference rule (optimize.py:83-85) to the identical union and
+ * folds the winner into its cached minima.  After the last step the ranks
+ * all-gather a 64-bit hash of (selection, values, gains) and fail on any
+ * mismatch.  The k-step loop is graph-captured like ebc_greedy.  NCCL is
+ * dlopen'ed (libnccl.so.2) on first use.
  *   ebc_comm_id_bytes / ebc_comm_unique_id -> rank 0 makes the id, the caller
  *     broadcasts it (e.g. torch.distributed), every rank calls ebc_comm_init;
- *   ebc_shard_set_range sets the rank's candidate range first;
+ *   ebc_shard_set_range sets the rank's candidate range first (the start must
+ *     be a multiple of 128, the candidate block of the screens, unless empty);
  *   ebc_greedy_sharded -> same outputs as ebc_greedy, identical on every rank;
- *     EBC_ECOMM if a tie set overflowed (caller falls back to ebc_shard_advance). */
+ *     EBC_ECOMM if a frontier overflowed (ebc_comm_status bit 0: the caller
+ *     falls back to ebc_shard_advance) or the ranks disagree (bit 1: a bug,
+ *     never a fallback). */
 int64_t ebc_comm_id_bytes(void);
 int ebc_comm_unique_id(unsigned char* out_id, int64_t bytes);
 int ebc_comm_init(ebc_ctx* ctx, const unsigned char* id, int64_t bytes, int32_t nranks, int32_t rank);
@@ -132,8 +139,10 @@ int ebc_comm_init(ebc_ctx* ctx, const unsigned char* id, int64_t bytes, int32_t 
 int ebc_comm_attach(ebc_ctx* ctx);
 int ebc_greedy_sharded(ebc_ctx* ctx, int32_t k, int64_t* out_sel, double* out_val, double* out_gain,
                        int64_t* out_evals);
+/* Flags of the last ebc_greedy_sharded: 1 frontier overflow, 2 cross-rank mismatch. */
+int ebc_comm_status(const ebc_ctx* ctx, int32_t* out_flags);
 /* Host-fed form of the same step (tests / emulated ranks on one GPU): the local
- * tie-set records ((TIE_CAP + 1) x {index, gain}, record 0 = {count, 0}) and
+ * frontier records ((TIE_CAP + 1) x {index, gain}, record 0 = {count, 0}) and
  * the global pick + commit from `world` gathered record blocks. */
 int32_t ebc_tie_cap(void);
 int ebc_shard_tie_step(ebc_ctx* ctx, double* out_rec, double* out_current);

@@ -53,6 +53,7 @@ SIGNATURES = {
     "ebc_comm_attach": (ctypes.c_int, [_vp]),
     "ebc_greedy_sharded": (ctypes.c_int, [_vp, _i32, _i64p, _f64p, _f64p, _i64p]),
     "ebc_tie_cap": (ctypes.c_int32, []),
+    "ebc_comm_status": (ctypes.c_int, [_vp, ctypes.POINTER(_i32)]),
     "ebc_shard_tie_step": (ctypes.c_int, [_vp, _f64p, _f64p]),
     "ebc_shard_pick_commit": (ctypes.c_int, [_vp, _f64p, _i32, _i32, _i64p, _f64p]),
     "ebc_screen_info": (ctypes.c_int, [_vp, _i64p]),

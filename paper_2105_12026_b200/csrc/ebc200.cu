@@ -188,7 +188,7 @@ struct ebc_ctx {
 
   // CUDA graphs of whole Greedy runs, keyed by k (rebuilt when buffers move)
   struct Graph {
-    int k;  // (k << 1) | sharded
+    int k;  // (k << 2) | (timing << 1) | sharded
     int64_t c0, c1;  // the candidate range the graph's kernel arguments and grids hold
     int64_t epoch;
     int64_t launches;
@@ -199,8 +199,9 @@ struct ebc_ctx {
   ncclComm_t comm = nullptr;  // the device's shared communicator (not owned)
   int64_t comm_gen = -1;
   int nranks = 1, rank = 0;
-  DevBuf tie_rec, tie_all;
+  DevBuf tie_rec, tie_all, sel_hash;
   int* tie_err = nullptr;
+  int comm_status = 0;  // flags of the last sharded run: 1 frontier overflow, 2 cross-rank mismatch
   // runs made eagerly once (captured on the next run with the same key and
   // candidate range) and the deepest ladder rung each of them reached
   struct Eager {
@@ -212,6 +213,7 @@ struct ebc_ctx {
   int ladder_max = 3;         // deepest rung enqueued (L_DIRECT except while capturing)
   int64_t alloc_epoch = 0;
   bool use_graphs = true;
+  bool capturing = false;  // a Greedy run is being captured into a graph
   // timing / accounting
   bool timing = false;
   std::vector<cudaEvent_t> ev;
@@ -244,6 +246,14 @@ int fail(ebc_ctx* c, int code, const std::string& msg) {
       return fail(ctx, EBC_ECUDA, std::string("kernel launch failed: ") + cudaGetErrorString(e_) + \
                                       " at " + __FILE__ + ":" + std::to_string(__LINE__));         \
   } while (0)
+
+// Per-step family events (timing mode).  While a run is being captured they
+// become external event record nodes (cudaEventRecordExternal), which keep
+// their timestamps on every replay; outside capture a plain record.
+cudaError_t record_step_event(ebc_ctx* ctx, cudaEvent_t e) {
+  return ctx->capturing ? cudaEventRecordWithFlags(e, ctx->stream, cudaEventRecordExternal)
+                        : cudaEventRecord(e, ctx->stream);
+}
 
 int ensure(ebc_ctx* ctx, DevBuf& b, size_t bytes) {
   if (b.bytes >= bytes) return EBC_OK;
@@ -392,8 +402,8 @@ int launch_refine(ebc_ctx* ctx, const T* V, int grid, size_t smem, int ng) {
 // candidate goes straight to the exact fp64 refine.
 int run_window_all(ebc_ctx* ctx, int eb, int fin_blocks) {
   if (ctx->timing) {
-    CU(cudaEventRecord(ctx->ev[eb + 0], ctx->stream));
-    CU(cudaEventRecord(ctx->ev[eb + 1], ctx->stream));
+    CU(record_step_event(ctx, ctx->ev[eb + 0]));
+    CU(record_step_event(ctx, ctx->ev[eb + 1]));
   }
   k_window_all<<<fin_blocks, 256, 0, ctx->stream>>>(ctx->c0, ctx->c1, ctx->selected, ctx->wcount, ctx->wlist);
   KCHECK();
@@ -656,7 +666,7 @@ int run_screen_window(ebc_ctx* ctx, int eb, int fin_blocks) {
   if (rc) return rc;
   rc = ensure(ctx, ctx->part_e, (size_t)nsplit_max * ctx->n_pad * sizeof(float));
   if (rc) return rc;
-  if (ctx->timing) CU(cudaEventRecord(ctx->ev[eb + 0], ctx->stream));
+  if (ctx->timing) CU(record_step_event(ctx, ctx->ev[eb + 0]));
   // lower bounds are clamped at 0 (every gain is a sum of max(0, .) terms), so
   // key 0 (= +0.0) is a valid neutral element for the max
   CU(cudaMemsetAsync(ctx->maxlb, 0, sizeof(long long), ctx->stream));
@@ -724,7 +734,7 @@ int run_screen_window(ebc_ctx* ctx, int eb, int fin_blocks) {
     }
   }
   if (rc) return rc;
-  if (ctx->timing) CU(cudaEventRecord(ctx->ev[eb + 1], ctx->stream));
+  if (ctx->timing) CU(record_step_event(ctx, ctx->ev[eb + 1]));
   return EBC_OK;
 }
 
@@ -760,7 +770,7 @@ int run_step_select(ebc_ctx* ctx, int step, int commit, int64_t* sel_dev) {
                                       1.0 / (double)ctx->n, ctx->cur, ctx->wgain, ctx->best, commit, step,
                                       ctx->selected, sel_dev, ctx->stats, ctx->level);
   KCHECK();
-  if (ctx->timing) CU(cudaEventRecord(ctx->ev[eb + 2], ctx->stream));
+  if (ctx->timing) CU(record_step_event(ctx, ctx->ev[eb + 2]));
   return EBC_OK;
 }
 
@@ -812,7 +822,7 @@ int run_update(ebc_ctx* ctx, int step, double* val_dev, double* gain_dev) {
                                                                    step, ctx->best);
   }
   KCHECK();
-  if (ctx->timing) CU(cudaEventRecord(ctx->ev[eb + 3], ctx->stream));
+  if (ctx->timing) CU(record_step_event(ctx, ctx->ev[eb + 3]));
   return EBC_OK;
 }
 
@@ -862,7 +872,20 @@ int enqueue_greedy_sharded(ebc_ctx* ctx, int k) {
   if (rc) return rc;
   CU(cudaMemsetAsync(ctx->tie_err, 0, sizeof(int), ctx->stream));
   for (int s = 0; s < k && !rc; ++s) rc = enqueue_sharded_step(ctx, s, nullptr);
-  return rc;
+  if (rc) return rc;
+  // consistency guard: every rank must hold the same selection, values and
+  // gains; a disagreement (err bit 2) fails the call instead of returning
+  // rank-dependent results
+  unsigned long long* h = (unsigned long long*)ctx->sel_hash.p;
+  k_sel_hash<<<1, 32, 0, ctx->stream>>>((const int64_t*)ctx->sel_out.p, (const double*)ctx->val_out.p,
+                                        (const double*)ctx->gain_out.p, k, h);
+  KCHECK();
+  const NcclApi& api = nccl_api();
+  const ncclResult_t r = api.AllGather(h, h + 1, 1, ncclUint64, ctx->comm, ctx->stream);
+  if (r != ncclSuccess) return fail(ctx, EBC_ECOMM, std::string("ncclAllGather: ") + api.GetErrorString(r));
+  k_sel_hash_check<<<1, 32, 0, ctx->stream>>>(h + 1, ctx->nranks, ctx->tie_err);
+  KCHECK();
+  return EBC_OK;
 }
 
 int enqueue_greedy(ebc_ctx* ctx, int k) {
@@ -901,7 +924,7 @@ void free_ctx(ebc_ctx* c) {
                   c->maxlb, c->wcount, c->wlist, c->wgain, c->ub};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, c->stream);
-  DevBuf* bufs[] = {&c->tie_rec, &c->tie_all, &c->ms_tanchor, &c->ms_trad, &c->part_g, &c->part_e, &c->part_a, &c->part_r, &c->sel_out, &c->val_out, &c->gain_out, &c->ms_part,
+  DevBuf* bufs[] = {&c->tie_rec, &c->tie_all, &c->sel_hash, &c->ms_tanchor, &c->ms_trad, &c->part_g, &c->part_e, &c->part_a, &c->part_r, &c->sel_out, &c->val_out, &c->gain_out, &c->ms_part,
                     &c->ms_off, &c->ms_idx, &c->ms_out, &c->ms_mbuf, &c->ms_setof, &c->ms_pairs, &c->ms_keys,
                     &c->ms_vals, &c->ms_keys2, &c->ms_vals2, &c->ms_ukeys, &c->ms_uvals, &c->ms_cub};
   void* more[] = {c->pt0, c->ms_count, c->ms_nruns};
@@ -1523,6 +1546,7 @@ int greedy_run(ebc_ctx* ctx, int32_t k, bool sharded, int64_t* out_sel, double* 
     }
     int rc0 = ensure(ctx, ctx->tie_rec, (size_t)(TIE_CAP + 1) * sizeof(double2));
     if (!rc0) rc0 = ensure(ctx, ctx->tie_all, (size_t)ctx->nranks * (TIE_CAP + 1) * sizeof(double2));
+    if (!rc0) rc0 = ensure(ctx, ctx->sel_hash, (size_t)(ctx->nranks + 1) * sizeof(unsigned long long));
     if (rc0) return rc0;
   }
   int rc = ensure(ctx, ctx->sel_out, (size_t)k * sizeof(int64_t));
@@ -1544,8 +1568,11 @@ int greedy_run(ebc_ctx* ctx, int32_t k, bool sharded, int64_t* out_sel, double* 
   // launch instead of ~10 per step: matters for small N, e.g. C1).  The first
   // run stays eager, so a context used once (the e2e path) never pays for
   // capture + instantiation.
-  const bool graph_ok = ctx->use_graphs && !ctx->timing;
-  const int key = (k << 1) | (sharded ? 1 : 0);
+  // timing mode captures the per-step event records into the graph too
+  // (external event record nodes: cudaEventRecordExternal, which keep timing),
+  // so timed runs are replays like the untimed product path
+  const bool graph_ok = ctx->use_graphs;
+  const int key = (k << 2) | (ctx->timing ? 2 : 0) | (sharded ? 1 : 0);
   auto enqueue = [&]() { return sharded ? enqueue_greedy_sharded(ctx, k) : enqueue_greedy(ctx, k); };
   ebc_ctx::Graph* cached = nullptr;
   for (auto& g : ctx->graphs)
@@ -1565,7 +1592,9 @@ int greedy_run(ebc_ctx* ctx, int32_t k, bool sharded, int64_t* out_sel, double* 
       // a Greedy run is a deterministic function of (V, e0, k): replays take the
       // eager run's path down the ladder, so the graph holds only those rungs
       ctx->ladder_max = seen_lv;
+      ctx->capturing = true;
       const int crc = enqueue();
+      ctx->capturing = false;
       ctx->ladder_max = 3;
       ok = cudaStreamEndCapture(ctx->stream, &graph) == cudaSuccess && crc == EBC_OK && epoch == ctx->alloc_epoch;
     }
@@ -1609,8 +1638,11 @@ int greedy_run(ebc_ctx* ctx, int32_t k, bool sharded, int64_t* out_sel, double* 
   if (sharded) CU(cudaMemcpyAsync(&tie_err, ctx->tie_err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
   if (!(graph_ok && cached) && !seen) ctx->eager.push_back({key, ctx->c0, ctx->c1, lv_end < 0 ? 3 : (int)lv_end});
+  ctx->comm_status = tie_err;
+  if (tie_err & 2)
+    return fail(ctx, EBC_ECOMM, "sharded Greedy: ranks disagree on the selection (end-of-run hash mismatch)");
   if (tie_err)
-    return fail(ctx, EBC_ECOMM, "sharded Greedy: a rank's tie set exceeded " + std::to_string(TIE_CAP) +
+    return fail(ctx, EBC_ECOMM, "sharded Greedy: a rank's tie-set frontier exceeded " + std::to_string(TIE_CAP) +
                                     " records (use the host exchange)");
   if (ctx->timing) {
     for (int st = 0; st < k; ++st) {
@@ -1704,6 +1736,12 @@ int ebc_greedy_sharded(ebc_ctx* ctx, int32_t k, int64_t* out_sel, double* out_va
 }
 
 int32_t ebc_tie_cap(void) { return TIE_CAP; }
+
+int ebc_comm_status(const ebc_ctx* ctx, int32_t* out_flags) {
+  if (!ctx || !out_flags) return fail(nullptr, EBC_EINVAL, "ebc_comm_status: NULL argument");
+  *out_flags = ctx->comm_status;
+  return EBC_OK;
+}
 
 int ebc_shard_tie_step(ebc_ctx* ctx, double* out_rec, double* out_current) {
   if (!ctx || !out_rec || !out_current) return fail(ctx, EBC_EINVAL, "ebc_shard_tie_step: NULL argument");

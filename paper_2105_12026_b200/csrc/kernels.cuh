@@ -1119,42 +1119,80 @@ __global__ void __launch_bounds__(1024) k_pick(const int* __restrict__ wcount, c
 }
 
 // ---------------------------------------------------------------- sharded exchange
-// One rank's contribution to the global argmax: its local tie set
-// T_r = {w in window : value_w >= top_r - 1e-12 max(1, |top_r|)}.  The global
-// window threshold is >= every local one (top - window(top) is monotone in
-// top), so the union of the T_r holds every candidate the reference rule can
-// pick (optimize.py:83-85).  Records: rec[0] = {count, 0}, rec[1 + i] = {index,
-// exact gain}; order inside a rank does not matter (the pick takes the lowest
-// index).  count > TIE_CAP is reported, never truncated silently.
-constexpr int TIE_CAP = 1024;
+// One rank's contribution to the global argmax.  Its local tie set
+// T_r = {w in window : value_w >= top_r - 1e-12 max(1, |top_r|)} holds every
+// candidate of the rank the reference rule can pick (the global threshold is
+// >= every local one: top - window(top) is monotone in top, optimize.py:83-85).
+// Of T_r only the index-ordered Pareto frontier is sent: c is kept iff every
+// candidate of T_r with a lower index has a strictly lower value.  The global
+// winner (lowest index with value >= the global threshold) is never dominated
+// -- a dominating candidate would be eligible with a lower index -- so the
+// union of the frontiers decides exactly as the union of the T_r would.  Exact
+// duplicates collapse to their lowest index, so the frontier is almost always
+// one entry.  Records: rec[0] = {count, 0}, rec[1 + i] = {index, exact gain}
+// in increasing index (and value) order; a frontier longer than TIE_CAP is
+// reported as count TIE_CAP + 1 (the caller falls back to the host exchange),
+// never truncated silently.  TIE_CAP + 1 records = 128 B per rank and step.
+constexpr int TIE_CAP = 7;
 
 __global__ void __launch_bounds__(1024) k_tie_records(const int* __restrict__ wcount,
                                                       const int64_t* __restrict__ wlist,
                                                       const double* __restrict__ wgain, double inv_n,
                                                       const double* __restrict__ cur, double2* __restrict__ rec) {
   __shared__ double smax[1024];
-  __shared__ int fill;
+  __shared__ long long sidx[1024];
+  __shared__ double sgain[1024];
+  const int t = threadIdx.x;
   const int wc = *wcount;
   const double f = *cur;
   double top = -INFINITY;
-  for (int w = threadIdx.x; w < wc; w += blockDim.x) top = fmax(top, __dadd_rn(f, __dmul_rn(wgain[w], inv_n)));
-  smax[threadIdx.x] = top;
-  if (threadIdx.x == 0) fill = 0;
+  for (int w = t; w < wc; w += blockDim.x) top = fmax(top, __dadd_rn(f, __dmul_rn(wgain[w], inv_n)));
+  smax[t] = top;
   __syncthreads();
   for (int s = blockDim.x / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s) smax[threadIdx.x] = fmax(smax[threadIdx.x], smax[threadIdx.x + s]);
+    if (t < s) smax[t] = fmax(smax[t], smax[t + s]);
     __syncthreads();
   }
   top = smax[0];
   const double thr = top - 1e-12 * fmax(1.0, fabs(top));
-  for (int w = threadIdx.x; w < wc; w += blockDim.x) {
-    if (__dadd_rn(f, __dmul_rn(wgain[w], inv_n)) >= thr) {
-      const int slot = atomicAdd(&fill, 1);
-      if (slot < TIE_CAP) rec[1 + slot] = make_double2((double)wlist[w], wgain[w]);
+  double prev = -INFINITY;  // value of the last frontier entry
+  int cnt = 0;
+  for (int it = 0; it <= TIE_CAP; ++it) {
+    // next frontier entry: the lowest index whose value beats the previous entry
+    long long bi = LLONG_MAX;
+    double bg = 0.0;
+    for (int w = t; w < wc; w += blockDim.x) {
+      const double g = wgain[w];
+      const double val = __dadd_rn(f, __dmul_rn(g, inv_n));
+      const long long id = (long long)wlist[w];
+      if (val >= thr && val > prev && id < bi) {
+        bi = id;
+        bg = g;
+      }
     }
+    sidx[t] = bi;
+    sgain[t] = bg;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+      if (t < s && sidx[t + s] < sidx[t]) {
+        sidx[t] = sidx[t + s];
+        sgain[t] = sgain[t + s];
+      }
+      __syncthreads();
+    }
+    bi = sidx[0];
+    bg = sgain[0];
+    __syncthreads();
+    if (bi == LLONG_MAX) break;
+    if (it == TIE_CAP) {
+      cnt = TIE_CAP + 1;  // overflow: reported, not truncated
+      break;
+    }
+    if (t == 0) rec[1 + it] = make_double2((double)bi, bg);
+    cnt = it + 1;
+    prev = __dadd_rn(f, __dmul_rn(bg, inv_n));
   }
-  __syncthreads();
-  if (threadIdx.x == 0) rec[0] = make_double2((double)fill, 0.0);
+  if (t == 0) rec[0] = make_double2((double)cnt, 0.0);
 }
 
 // Global pick over the all-gathered records of `world` ranks (identical input
@@ -1171,7 +1209,7 @@ __global__ void __launch_bounds__(1024) k_pick_global(const double2* __restrict_
   for (int r = 0; r < world; ++r) {
     const double2* rr = all + (int64_t)r * (TIE_CAP + 1);
     const int cnt = (int)rr[0].x;
-    if (cnt > TIE_CAP && threadIdx.x == 0) *err = 1;
+    if (cnt > TIE_CAP && threadIdx.x == 0) *err |= 1;
     for (int i = threadIdx.x; i < min(cnt, TIE_CAP); i += blockDim.x)
       top = fmax(top, __dadd_rn(f, __dmul_rn(rr[1 + i].y, inv_n)));
   }
@@ -1202,6 +1240,33 @@ __global__ void __launch_bounds__(1024) k_pick_global(const double2* __restrict_
     if (b >= 0) selected[b] = 1;
     if (sel_out) sel_out[step] = b;
   }
+}
+
+// End-of-run consistency guard of the sharded Greedy: a 64-bit hash of the k
+// selected indices and the bits of their values and gains; every rank
+// all-gathers the hashes and flags (err bit 2) any rank that disagrees.
+__global__ void k_sel_hash(const int64_t* __restrict__ sel, const double* __restrict__ val,
+                           const double* __restrict__ gain, int k, unsigned long long* __restrict__ out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  unsigned long long h = 0xcbf29ce484222325ull;  // FNV-1a over 64-bit words
+  auto mix = [&](unsigned long long x) {
+    for (int b = 0; b < 8; ++b) {
+      h ^= (x >> (8 * b)) & 0xffull;
+      h *= 0x100000001b3ull;
+    }
+  };
+  for (int s = 0; s < k; ++s) {
+    mix((unsigned long long)sel[s]);
+    mix((unsigned long long)__double_as_longlong(val[s]));
+    mix((unsigned long long)__double_as_longlong(gain[s]));
+  }
+  *out = h;
+}
+
+__global__ void k_sel_hash_check(const unsigned long long* __restrict__ all, int world, int* __restrict__ err) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  for (int r = 1; r < world; ++r)
+    if (all[r] != all[0]) *err |= 2;
 }
 
 // ---------------------------------------------------------------- K4: cached-min update

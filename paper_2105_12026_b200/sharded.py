@@ -17,11 +17,15 @@ Greedy step:
 Device exchange (the NCCL path, ``greedy_device_exchange``): the same step
 runs without a host round trip -- each rank reduces its window to its local
 tie set {c : value_c >= top_r - 1e-12 max(1,|top_r|)} (a superset of what the
-global rule can pick, since top - window(top) is monotone in top), writes it
-as fixed-size records, one ``ncclAllGather`` inside the step exchanges them,
-and every rank runs the identical device pick; the k-step loop is
-graph-captured (``ebc_greedy_sharded``).  Steps 1-4 above are the host-driven
-fallback (gloo, NCCL missing, or a tie set beyond ``ebc_tie_cap()``).
+global rule can pick, since top - window(top) is monotone in top) and that to
+its index-ordered Pareto frontier (the only members the lowest-index rule can
+need; exact duplicates collapse to one), writes at most ``ebc_tie_cap()``
+16-byte records, one ``ncclAllGather`` inside the step exchanges them (128 B
+per rank), and every rank runs the identical device pick; the k-step loop is
+graph-captured (``ebc_greedy_sharded``) and ends with an all-gather of a hash of
+the selection that fails the call if any rank disagrees.  Steps 1-4 above are
+the host-driven fallback (gloo, NCCL missing, or a frontier beyond
+``ebc_tie_cap()`` records).
 
 Why the union of local windows gives the single-GPU answer: a local window
 W_r = {c in shard r : ub_c >= max_{c' in shard r} lb_c' - margin} contains
@@ -182,8 +186,34 @@ def greedy_sharded_loop(engine, n: int, k: int, group=None, device=None) -> Summ
         gains.append(newval - current)
         current = newval
         selected.append(best)
+    check_ranks_agree(selected, gains, current, group=group)
     return Summary(selected=selected, value=current, gains=gains, evaluations=evaluations,
                    runtime_seconds=time.perf_counter() - t0)
+
+
+def selection_digest(selected: Sequence[int], gains: Sequence[float], value: float) -> bytes:
+    """Digest of a Greedy result (indices and the exact bits of gains and value)."""
+    import hashlib
+    h = hashlib.sha256()
+    h.update(np.asarray(selected, dtype=np.int64).tobytes())
+    h.update(np.asarray(gains, dtype=np.float64).tobytes())
+    h.update(np.float64(value).tobytes())
+    return h.digest()
+
+
+def check_ranks_agree(selected, gains, value, group=None) -> None:
+    """End-of-run guard of the host-driven exchange: every rank must hold the
+    same result; raises RuntimeError (never returns rank-dependent results)."""
+    import torch.distributed as dist
+
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return
+    mine = selection_digest(selected, gains, value)
+    all_d = [None] * dist.get_world_size(group)
+    dist.all_gather_object(all_d, mine, group=group)
+    if any(d != all_d[0] for d in all_d):
+        bad = [r for r, d in enumerate(all_d) if d != all_d[0]]
+        raise RuntimeError(f"sharded Greedy: ranks {bad} disagree with rank 0 on the selection")
 
 
 def _ensure_device_comm(f, group) -> bool:
@@ -268,7 +298,11 @@ def greedy_maximize_sharded(f, budget: OptimizerBudget, group=None) -> Summary:
         try:
             return greedy_device_exchange(f, int(budget.k), c0, c1)
         except _native.CommError:
-            pass  # tie-set overflow on some rank (every rank sees the same records): host exchange below
+            flags = ctypes.c_int32()
+            _native.check(f._lib.ebc_comm_status(f.native_context, ctypes.byref(flags)), f.native_context)
+            if flags.value & 2:
+                raise  # the ranks disagree: a bug, never papered over by a fallback
+            # a frontier overflow (every rank sees the same records): host exchange below
     engine = NativeShardEngine(f, c0, c1)
     device = f"cuda:{torch.cuda.current_device()}" if nccl else None
     try:

@@ -397,6 +397,80 @@ def test_device_exchange_single_rank_matches_greedy():
         assert s.evaluations == single.evaluations
 
 
+def _one_rank_comm(f):
+    import ctypes
+    from paper_2105_12026_b200 import _native
+    lib = f._lib
+    nb = int(lib.ebc_comm_id_bytes())
+    buf = ctypes.create_string_buffer(nb)
+    _native.check(lib.ebc_comm_unique_id(buf, nb))
+    _native.check(lib.ebc_comm_init(f.native_context, buf.raw, nb, 1, 0), f.native_context)
+
+
+def test_sharded_graphs_are_keyed_by_candidate_range():
+    """A captured sharded run holds its candidate range in its kernel arguments:
+    changing the range with the same k must not replay the old graph (each
+    range runs eager -> captured -> replayed and keeps its own answer), and
+    misaligned range starts are refused."""
+    from paper_2105_12026_b200 import _native
+    from paper_2105_12026_b200.sharded import greedy_device_exchange
+    X = np.random.default_rng(29).standard_normal((6000, 40)).astype(np.float32)
+    f = fn(X, eb.Precision.FP32)
+    _one_rank_comm(f)
+    with pytest.raises(ValueError, match="not a multiple of 128"):
+        _native.check(f._lib.ebc_shard_set_range(f.native_context, 8, 6000), f.native_context)
+    _native.check(f._lib.ebc_shard_set_range(f.native_context, 6000, 6000), f.native_context)  # empty: any start
+    full = [greedy_device_exchange(f, 6, 0, 6000).selected for _ in range(3)]
+    part = [greedy_device_exchange(f, 6, 0, 1024).selected for _ in range(3)]
+    again = greedy_device_exchange(f, 6, 0, 6000).selected
+    assert full[0] == full[1] == full[2] == again == eb.greedy_maximize(fn(X, eb.Precision.FP32),
+                                                                         eb.OptimizerBudget(k=6)).selected
+    assert part[0] == part[1] == part[2] and all(i < 1024 for i in part[0])
+    assert part[0] != full[0]
+
+
+def test_tie_frontier_collapses_duplicates():
+    """Exact duplicates of the winner on one rank: the frontier records hold
+    one entry for them (the lowest index), so the 128-byte record never
+    overflows on duplicate-heavy data and the pick is the reference's."""
+    import ctypes
+    from paper_2105_12026_b200 import _native
+    X = np.random.default_rng(31).standard_normal((4096, 24)).astype(np.float32)
+    top = eb.greedy_maximize(fn(X, eb.Precision.FP32), eb.OptimizerBudget(k=1)).selected[0]
+    X[1000:1040] = X[top]  # 40 exact copies of the first winner
+    want = oracle.greedy(X.astype(np.float64), 3)[0]
+    f = fn(X, eb.Precision.FP32)
+    cap = int(_native.load().ebc_tie_cap())
+    assert cap == 7
+    rec = np.zeros((cap + 1) * 2, dtype=np.float64)
+    cur = ctypes.c_double()
+    _native.check(f._lib.ebc_reset(f.native_context))
+    _native.check(f._lib.ebc_shard_tie_step(f.native_context, _c(rec, ctypes.c_double), ctypes.byref(cur)),
+                  f.native_context)
+    assert rec[0] == 1 and int(rec[2]) == min(top, 1000) == want[0]
+    _one_rank_comm(f)
+    from paper_2105_12026_b200.sharded import greedy_device_exchange
+    assert greedy_device_exchange(f, 3, 0, 4096).selected == want
+
+
+def test_timing_mode_replays_the_graph():
+    """Timing mode captures the per-step family events into the run's graph:
+    timed runs are replays (fewer host launches) with valid family times."""
+    from paper_2105_12026_b200 import optimize
+    X = np.random.default_rng(37).standard_normal((20000, 100)).astype(np.float32)
+    f = fn(X, eb.Precision.FP32)
+    optimize.set_timing(f, True)
+    sels, tims = [], []
+    for _ in range(4):
+        sels.append(eb.greedy_maximize(f, eb.OptimizerBudget(k=5)).selected)
+        tims.append(optimize.last_timings(f))
+    assert all(s == sels[0] for s in sels)
+    for t in tims:
+        assert t[0] > 0 and t[2] > 0 and t[0] + t[1] + t[2] <= t[3] * 1.05 + 0.05
+    optimize.set_timing(f, False)
+    assert eb.greedy_maximize(f, eb.OptimizerBudget(k=5)).selected == sels[0]
+
+
 @pytest.mark.parametrize("world", [2, 3, 8])
 def test_device_pick_emulated_ranks_bit_identical(world):
     """The device exchange's kernels (local tie-set records, global pick) with
