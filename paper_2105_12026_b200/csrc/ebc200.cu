@@ -170,6 +170,10 @@ struct ebc_ctx {
   int64_t* topc = nullptr;           // candidate with the largest screen bound (ub-only screens)
   double* toppart = nullptr;         // 4 nchunks: its exact gain's partials (argmax scratch before)
   double* terms = nullptr;           // n: e0d - cm64 per point (split K4)
+  // fused K4 (k_update_fused; false: split K4) and its counters
+  // ([0] chunks done, [1..] per-chunk tickets)
+  bool uf_on = false;
+  unsigned int* uf_ctr = nullptr;
   double* cur = nullptr;
   int64_t* best = nullptr;
   long long* maxlb = nullptr;
@@ -799,6 +803,15 @@ int run_update(ebc_ctx* ctx, int step, double* val_dev, double* gain_dev) {
     k_update<double><<<ctx->nchunks, RED_THREADS, smem, ctx->stream>>>(
         ctx->V64, ctx->pitch, ctx->n, ctx->d, ctx->best, ctx->pk, ctx->e0d, ctx->nv32, ctx->cm64, ctx->pt, tc_seeds(ctx), ctx->chunkpart,
         ctx->counter, 1.0 / (double)ctx->n, ctx->cur, val_dev, gain_dev, step);
+  } else if (ctx->uf_on) {
+    // fused K4: one launch, one bulk-copied 256-row slice per block, f(S) by
+    // the block that completes the last chunk (DESIGN.md §4 K4)
+    const size_t dsm = (((size_t)ctx->d * 8 + 15) & ~(size_t)15) + (size_t)UF_ROWS * (ctx->pitch * 4 + 16);
+    CU(cudaFuncSetAttribute(k_update_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+    UpdateCounters uc{ctx->uf_ctr + 1, ctx->uf_ctr};
+    k_update_fused<<<(unsigned)((ctx->n + UF_ROWS - 1) / UF_ROWS), UF_ROWS, dsm, ctx->stream>>>(
+        ctx->V32, ctx->pitch, ctx->n, ctx->d, ctx->best, ctx->pk, ctx->e0d, ctx->nv32, ctx->cm64, ctx->pt,
+        tc_seeds(ctx), ctx->terms, ctx->chunkpart, uc, 1.0 / (double)ctx->n, ctx->cur, val_dev, gain_dev, step);
   } else {
     // split K4: wide streaming pass over V (a), fixed-structure reduction (b)
     const int nb = (int)((ctx->n + RED_THREADS - 1) / RED_THREADS);
@@ -920,7 +933,7 @@ int do_reset(ebc_ctx* ctx) {
 void free_ctx(ebc_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
-  void* ptrs[] = {c->V32, c->V64, c->e0d, c->cm64, c->pt, c->nv32, c->level, c->stats, c->Vhi, c->Vlo, c->Vf, c->tile_anchor0, c->rhomax, c->cmn, c->vsum, c->vsn, c->ipsum, c->rhomin, c->agg_any, c->pttc, c->kpmax, c->anchors, c->nva, c->tile_anchor, c->tc_vmax, c->fps_keys, c->ipa0, c->tile_rad, c->rho, c->cmx, c->cmx0, c->selected, c->chunkpart, c->counter, c->counter2, c->topc, c->toppart, c->terms, c->cur, c->best,
+  void* ptrs[] = {c->V32, c->V64, c->e0d, c->cm64, c->pt, c->nv32, c->level, c->stats, c->Vhi, c->Vlo, c->Vf, c->tile_anchor0, c->rhomax, c->cmn, c->vsum, c->vsn, c->ipsum, c->rhomin, c->agg_any, c->pttc, c->kpmax, c->anchors, c->nva, c->tile_anchor, c->tc_vmax, c->fps_keys, c->ipa0, c->tile_rad, c->rho, c->cmx, c->cmx0, c->selected, c->chunkpart, c->counter, c->counter2, c->topc, c->toppart, c->terms, c->cur, c->best, c->uf_ctr,
                   c->maxlb, c->wcount, c->wlist, c->wgain, c->ub};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, c->stream);
@@ -1180,7 +1193,7 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
       k_pad<double, double><<<blocks, 256, 0, ctx->stream>>>((const double*)raw, n, d, ctx->V64, ctx->pitch);
     CUC(cudaGetLastError());
   }
-  CUC(cudaMallocAsync((void**)&ctx->e0d, (size_t)n * sizeof(double), ctx->stream));
+  CUC(cudaMallocAsync((void**)&ctx->e0d, (size_t)ctx->n_pad * sizeof(double), ctx->stream));  // K4 stages whole slices
   CUC(cudaMallocAsync((void**)&ctx->cm64, (size_t)ctx->n_pad * sizeof(double), ctx->stream));
   CUC(cudaMallocAsync((void**)&ctx->pt, (size_t)ctx->n_pad * sizeof(float4), ctx->stream));
   CUC(cudaMemsetAsync(ctx->pt, 0, (size_t)ctx->n_pad * sizeof(float4), ctx->stream));
@@ -1290,6 +1303,17 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
   CUC(cudaMallocAsync((void**)&ctx->topc, sizeof(int64_t), ctx->stream));
   CUC(cudaMallocAsync((void**)&ctx->toppart, (size_t)ctx->nchunks * 4 * sizeof(double), ctx->stream));
   CUC(cudaMallocAsync((void**)&ctx->terms, (size_t)ctx->n_pad * sizeof(double), ctx->stream));
+  if (dtype != EBC_F64) {
+    // fused K4 when a 256-row slice fits shared memory (pitch <= ~200 floats)
+    const size_t dsm = (((size_t)d * 8 + 15) & ~(size_t)15) + (size_t)UF_ROWS * (ctx->pitch * 4 + 16);
+    const char* uf_env = getenv("EBC200_UPDATE_FUSED");
+    if (dsm <= 220 * 1024 && !(uf_env && uf_env[0] == '0')) {
+      ctx->uf_on = true;
+      const size_t cb = (size_t)(1 + ctx->nchunks) * sizeof(unsigned int);
+      CUC(cudaMallocAsync((void**)&ctx->uf_ctr, cb, ctx->stream));
+      CUC(cudaMemsetAsync(ctx->uf_ctr, 0, cb, ctx->stream));
+    }
+  }
   CUC(cudaMallocAsync((void**)&ctx->cur, sizeof(double), ctx->stream));
   CUC(cudaMemsetAsync(ctx->cur, 0, sizeof(double), ctx->stream));
   CUC(cudaMallocAsync((void**)&ctx->best, sizeof(int64_t), ctx->stream));

@@ -1447,6 +1447,109 @@ __global__ void __launch_bounds__(RED_THREADS) k_update_reduce(const double* __r
   }
 }
 
+// K4 fused (fp32 grounds): ONE launch per step streams V once and produces
+// f(S) with exactly the fixed reduction structure of k_update_reduce.
+//
+// * One block per slice of UF_ROWS = 256 consecutive rows, one row per thread.
+//   The slice (contiguous in HBM), its cm64 run and its e0d run arrive by three
+//   cp.async.bulk copies on one mbarrier -- no register staging; several
+//   blocks per SM keep ~200 KB per SM in flight.
+// * Per row: the fp64 distance to the winner s in dist64_smem_row's operation
+//   order, cm64 / pt / anchored-seed refresh for points whose minimum changed,
+//   term[v] = e0d[v] - cm64[v] (to L2).
+// * Chunk c (RCH = 1024 points = 4 slices): the block taking the chunk's last
+//   ticket sums its terms in k_update_reduce's fixed order (thread u adds terms
+//   u, u+256, u+512, u+768 left to right, then block_sum_256's tree) --
+//   bit-identical; the block completing the last chunk adds the chunk partials
+//   left to right (chunk_total_block) and records f(S).  Tickets are reset by
+//   their last taker, so graph replays need no memset.
+constexpr int UF_ROWS = RED_THREADS;
+static_assert(RCH % UF_ROWS == 0, "a chunk is a whole number of slices");
+
+struct UpdateCounters {
+  unsigned int* chunk_ticket;  // nchunks
+  unsigned int* chunks_done;   // 1
+};
+
+__global__ void __launch_bounds__(UF_ROWS) k_update_fused(
+    const float* __restrict__ V, int pitch, int64_t n, int d, const int64_t* __restrict__ best, PtCoef pk,
+    const double* __restrict__ e0d, const float* __restrict__ nv32, double* __restrict__ cm64,
+    float4* __restrict__ pt, TcSeeds seeds, double* __restrict__ terms, double* __restrict__ fpart,
+    UpdateCounters ctr, double inv_n, double* __restrict__ cur, double* __restrict__ val_out,
+    double* __restrict__ gain_out, int step) {
+  extern __shared__ __align__(16) unsigned char uf_smem[];
+  __shared__ uint64_t full;
+  __shared__ double sbuf[RED_THREADS];
+  __shared__ int flag;
+  const int64_t s = *best;
+  if (s < 0) return;
+  const int t = threadIdx.x;
+  const int id = blockIdx.x;
+  const int nslices = gridDim.x;
+  const int nchunks = (int)((n + RCH - 1) / RCH);
+  // rows < n_pad: always a full slice; cm64 / e0d are allocated n_pad long
+  const uint32_t row_bytes = (uint32_t)UF_ROWS * pitch * 4;
+  double* cd = reinterpret_cast<double*>(uf_smem);
+  unsigned char* stage = uf_smem + (((size_t)d * 8 + 15) & ~(size_t)15);
+  if (t == 0) {
+    mbar_init(&full, 1);
+    fence_mbar_init();
+    mbar_arrive_expect_tx(&full, row_bytes + 2 * UF_ROWS * 8);
+    bulk_g2s(stage, V + (int64_t)id * UF_ROWS * pitch, row_bytes, &full);
+    bulk_g2s(stage + row_bytes, cm64 + (int64_t)id * UF_ROWS, UF_ROWS * 8, &full);
+    bulk_g2s(stage + row_bytes + UF_ROWS * 8, e0d + (int64_t)id * UF_ROWS, UF_ROWS * 8, &full);
+  }
+  for (int k = t; k < d; k += UF_ROWS) cd[k] = (double)V[s * pitch + k];
+  __syncthreads();
+  mbar_wait(&full, 0);
+  const int64_t v = (int64_t)id * UF_ROWS + t;
+  if (v < n) {
+    const double dist = dist64_smem_row(reinterpret_cast<const float*>(stage) + (size_t)t * pitch, cd, d);
+    double m = reinterpret_cast<const double*>(stage + row_bytes)[t];
+    if (dist < m) {
+      m = dist;
+      cm64[v] = m;
+      pt[v] = make_pt((float)m, nv32[v], pk);
+      if (seeds.ipa) write_seeds(seeds, v, (float)m);
+    }
+    terms[v] = reinterpret_cast<const double*>(stage + row_bytes + UF_ROWS * 8)[t] - m;
+  }
+  __syncthreads();
+  const int c = id / (RCH / UF_ROWS);
+  if (t == 0) {
+    __threadfence();  // the block's terms (ordered by the barrier) before the ticket
+    const int in_chunk = min(RCH / UF_ROWS, nslices - c * (RCH / UF_ROWS));
+    flag = atomicAdd(ctr.chunk_ticket + c, 1u) == (unsigned int)(in_chunk - 1);
+  }
+  __syncthreads();
+  if (!flag) return;
+  __threadfence();
+  double acc = 0.0;
+#pragma unroll
+  for (int i = 0; i < RCH / RED_THREADS; ++i) {
+    const int64_t u = (int64_t)c * RCH + t + (int64_t)i * RED_THREADS;
+    if (u < n) acc += __ldcg(terms + u);
+  }
+  const double bs = block_sum_256(acc, sbuf);
+  if (t == 0) {
+    ctr.chunk_ticket[c] = 0u;
+    fpart[c] = bs;
+    __threadfence();
+    flag = atomicAdd(ctr.chunks_done, 1u) == (unsigned int)(nchunks - 1);
+  }
+  __syncthreads();
+  if (!flag) return;
+  __threadfence();
+  const double fnew = chunk_total_block(fpart, nchunks, sbuf) * inv_n;
+  if (t == 0) {
+    const double fold = *cur;
+    if (val_out) val_out[step] = fnew;
+    if (gain_out) gain_out[step] = fnew - fold;
+    *cur = fnew;
+    *ctr.chunks_done = 0u;
+  }
+}
+
 // ---------------------------------------------------------------- K2: multiset (work matrix)
 
 // part[j*nchunks + ch] = sum over chunk ch of (e0d[v] - min(e0d[v], min_{s in S_j} d64(v, s))).

@@ -453,6 +453,26 @@ def test_tie_frontier_collapses_duplicates():
     assert greedy_device_exchange(f, 3, 0, 4096).selected == want
 
 
+@pytest.mark.parametrize("n,d", [(5000, 100), (20000 + 77, 32), (1031, 7), (130, 200)])
+def test_fused_update_bit_identical_to_split(monkeypatch, n, d):
+    """K4 as one launch (bulk-copied slices taken dynamically, chunk sums by the
+    block completing each chunk) gives bit-identical values and gains to the
+    split two-kernel form, over repeated runs (eager, captured, replayed: the
+    in-kernel counters reset themselves) and ragged N."""
+    X = np.random.default_rng(n + d).standard_normal((n, d)).astype(np.float32)
+    runs = {}
+    for fused in ("1", "0"):
+        monkeypatch.setenv("EBC200_UPDATE_FUSED", fused)
+        f = fn(X, eb.Precision.FP32)
+        runs[fused] = [eb.greedy_maximize(f, eb.OptimizerBudget(k=7)) for _ in range(3)]
+    for a in runs["1"] + runs["0"]:
+        b = runs["0"][0]
+        assert a.selected == b.selected and a.gains == b.gains and a.value == b.value
+    sel, vals, _, _ = oracle.greedy(X.astype(np.float64), 7)
+    assert runs["1"][0].selected == sel
+    np.testing.assert_allclose(np.cumsum(runs["1"][0].gains), vals, rtol=1e-11)
+
+
 def test_timing_mode_replays_the_graph():
     """Timing mode captures the per-step family events into the run's graph:
     timed runs are replays (fewer host launches) with valid family times."""
