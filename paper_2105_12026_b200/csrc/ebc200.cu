@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <climits>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -112,7 +113,9 @@ struct ebc_ctx {
   float4* pt = nullptr;
   float* nv32 = nullptr;
   long long* stats = nullptr;  // k_pick: window-size statistics of the last run
-  int* level = nullptr;  // adaptive screen: current rung of the ladder (L_FAST .. L_DIRECT)
+  // adaptive screen: [0] the rung this step's kernels run (-1: a lazy step
+  // decided without a screen), [1] the run's current rung (L_FAST .. L_DIRECT)
+  int* level = nullptr;
   PtCoef pk{};
   // screen mode: 0 direct, 1 FFMA Gram, 2 adaptive from FFMA Gram, 3 adaptive from the tensor screen
   int screen_mode = 2;
@@ -181,6 +184,14 @@ struct ebc_ctx {
   int64_t* wlist = nullptr;  // n
   double* wgain = nullptr;   // n
   double* ub = nullptr;      // n
+  // lazy Greedy (kernels.cuh k_lazy_mark): ubp[c - c0] bounds c's current gain
+  // (+inf after a reset); bflag: this step's re-screened 128-candidate blocks
+  double* ubp = nullptr;           // n
+  unsigned char* bflag = nullptr;  // ceil(n / 128) + 2
+  bool lazy_on = true;             // EBC200_LAZY=0: every step screens every candidate
+  int lazy_cap = 256;              // EBC200_LAZY_CAP: stale candidates decided by the exact refine alone
+  bool ubp_seeded = false;         // enqueue-time: a full step has run since the reset
+  const unsigned char* step_bflag = nullptr;  // enqueue-time: bflag during a lazy step, else nullptr
   DevBuf part_g, part_e, part_r, sel_out, val_out, gain_out, ms_part, ms_off, ms_idx, ms_out;
   // sparse work-matrix path
   DevBuf ms_tanchor, ms_trad;
@@ -425,7 +436,7 @@ int run_finalize_window(ebc_ctx* ctx, int nsplit, double nterms, int gterms, int
   k_finalize<<<fin_blocks, 256, 0, ctx->stream>>>(ctx->c0, ctx->c1, nsplit, (double*)ctx->part_g.p,
                                                  (float*)ctx->part_e.p, ctx->n_pad, einfl, gcoef, gscale,
                                                  ctx->selected, ctx->ub, ctx->maxlb, level_now, level, ub_only ? 1 : 0,
-                                                 part_a);
+                                                 part_a, ctx->step_bflag, ctx->lazy_on ? ctx->ubp : nullptr);
   KCHECK();
   if (ub_only) {
     // window threshold = exact gain of the candidate with the largest bound
@@ -531,6 +542,7 @@ int launch_tc_t(ebc_ctx* ctx, const TcPlan& p, const int* level_now, int level) 
     an.rhomax = ctx->rhomax;
     an.cmn = ctx->cmn;
   }
+  an.bflag = ctx->step_bflag;
   if (ms) {
     an.kpscale = ctx->tc_kpscale;
     an.keta2 = (float)std::ldexp(1.0, -24);  // seed split residual (fp16 subnormal), unscaled operands
@@ -630,6 +642,7 @@ int launch_tc_agg(ebc_ctx* ctx, const TcPlan& p) {
                ctx->tc_vmax, ctx->tc_kc, ctx->tc_kx, ctx->rho, ctx->tile_rad, ctx->cmx, p.list_cap, 0, nullptr};
   an.rhomax = ctx->rhomax;
   an.cmn = ctx->cmn;
+  an.bflag = ctx->step_bflag;
   // c' in 32 registers when it fits (padded dims of vsum are zero), else in smem;
   // the all-positive tile list (uint16 per tile of the split) follows
   const bool regs = ctx->d <= 32;  // reads 32 floats per vsum row: zeros times c' past d (32-float tail pad)
@@ -673,7 +686,7 @@ int run_screen_window(ebc_ctx* ctx, int eb, int fin_blocks) {
   if (ctx->timing) CU(record_step_event(ctx, ctx->ev[eb + 0]));
   // lower bounds are clamped at 0 (every gain is a sum of max(0, .) terms), so
   // key 0 (= +0.0) is a valid neutral element for the max
-  CU(cudaMemsetAsync(ctx->maxlb, 0, sizeof(long long), ctx->stream));
+  if (!ctx->step_bflag) CU(cudaMemsetAsync(ctx->maxlb, 0, sizeof(long long), ctx->stream));
   const double nterms_ffma = (double)p.tps * p.tp * 8 * 2;
   if (ctx->screen_mode == 0) {
     rc = launch_screen<0>(ctx, p, nullptr, 0);
@@ -697,7 +710,7 @@ int run_screen_window(ebc_ctx* ctx, int eb, int fin_blocks) {
         CU(cudaMemsetAsync(ctx->agg_any, 0, sizeof(int), ctx->stream));
         k_tile_ipsum<<<(unsigned)((cells * 32 + 255) / 256), 256, 0, ctx->stream>>>(
             ctx->pttc, ctx->n_pad, ctx->tc_na, ctx->n, ctx->tc_ntl, ctx->tc_np, ctx->ipsum, ctx->rhomin, ctx->radmin,
-            ctx->cmn, ctx->agg_any);
+            ctx->cmn, ctx->agg_any, ctx->level);
         KCHECK();
       }
       // ladder_max < L_DIRECT only while capturing a graph of a run whose eager
@@ -742,6 +755,30 @@ int run_screen_window(ebc_ctx* ctx, int eb, int fin_blocks) {
   return EBC_OK;
 }
 
+// Lazy prologue, step 1: maxlb = exact gain of the candidate with the largest
+// stale bound ubp (lowest index among equal bounds, selected ones skipped).
+int run_lazy_top(ebc_ctx* ctx) {
+  const int ag = (int)std::max<int64_t>(1, std::min<int64_t>(2 * ctx->num_sms, (ctx->c1 - ctx->c0 + 1023) / 1024));
+  k_argmax_ub<<<ag, 256, 0, ctx->stream>>>(ctx->c0, ctx->c1, ctx->ubp, ctx->topc, ctx->toppart, ctx->counter2,
+                                          nullptr, 0, ctx->selected);
+  KCHECK();
+  const size_t smem = (size_t)ctx->d * sizeof(double);
+  const unsigned g = (unsigned)((ctx->n + RED_THREADS - 1) / RED_THREADS);
+  if (ctx->dtype == EBC_F64) {
+    CU(cudaFuncSetAttribute(k_gain_top<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024));
+    k_gain_top<double><<<g, RED_THREADS, smem, ctx->stream>>>(ctx->V64, ctx->pitch, ctx->n, ctx->d, ctx->cm64,
+                                                             ctx->topc, ctx->toppart, ctx->counter2, ctx->maxlb,
+                                                             nullptr, 0);
+  } else {
+    CU(cudaFuncSetAttribute(k_gain_top<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024));
+    k_gain_top<float><<<g, RED_THREADS, smem, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->n, ctx->d, ctx->cm64,
+                                                            ctx->topc, ctx->toppart, ctx->counter2, ctx->maxlb,
+                                                            nullptr, 0);
+  }
+  KCHECK();
+  return EBC_OK;
+}
+
 // One step's candidate screen + certified window + exact refine + pick.
 // commit: single-device mode (mark the winner, record it as step `step`).
 int run_step_select(ebc_ctx* ctx, int step, int commit, int64_t* sel_dev) {
@@ -750,8 +787,33 @@ int run_step_select(ebc_ctx* ctx, int step, int commit, int64_t* sel_dev) {
   CU(cudaMemsetAsync(ctx->wcount, 0, sizeof(int), ctx->stream));
   const int fin_blocks = (int)((ncand + 255) / 256);
   ctx->cmx_fresh = false;
-  int rc = ctx->dtype == EBC_F64 ? EBC_EINVAL : run_screen_window(ctx, eb, fin_blocks);
-  if (rc == EBC_EINVAL) rc = run_window_all(ctx, eb, fin_blocks);
+  ScreenPlan sp;
+  const bool has_screen = ctx->dtype != EBC_F64 && plan_screen(ctx, sp) == EBC_OK;
+  const bool lazy = ctx->lazy_on && ctx->ubp_seeded;
+  int rc = EBC_OK;
+  if (lazy) {
+    // lazy prologue (kernels.cuh k_lazy_mark): lb = exact gain of the best
+    // stale bound, list the stale candidates, flag their blocks, pick the mode
+    CU(cudaMemsetAsync(ctx->maxlb, 0, sizeof(long long), ctx->stream));
+    CU(cudaMemsetAsync(ctx->bflag, 0, (size_t)((ncand + tc::M - 1) / tc::M + 2), ctx->stream));
+    rc = run_lazy_top(ctx);
+    if (rc) return rc;
+    const double margin = (double)ctx->n * 1e-12 * std::max(1.0, std::fabs(ctx->baseline)) * 1.01;
+    k_lazy_mark<<<fin_blocks, 256, 0, ctx->stream>>>(ctx->c0, ctx->c1, ctx->ubp, ctx->selected, ctx->maxlb, margin,
+                                                     ctx->wcount, ctx->wlist, ctx->bflag);
+    KCHECK();
+    k_lazy_plan<<<1, 32, 0, ctx->stream>>>(ctx->wcount, has_screen ? ctx->lazy_cap : INT_MAX, ctx->level, ctx->stats);
+    KCHECK();
+    ctx->step_bflag = ctx->bflag;
+  }
+  if (has_screen) rc = run_screen_window(ctx, eb, fin_blocks);
+  else if (!lazy) rc = run_window_all(ctx, eb, fin_blocks);
+  else if (ctx->timing) {
+    CU(record_step_event(ctx, ctx->ev[eb + 0]));
+    CU(record_step_event(ctx, ctx->ev[eb + 1]));
+  }
+  ctx->step_bflag = nullptr;
+  if (ctx->lazy_on) ctx->ubp_seeded = true;
   if (rc) return rc;
   // exact fp64 gains of the window
   // point-chunk groups per window candidate: as many as 256 MB of partials allow
@@ -772,7 +834,8 @@ int run_step_select(ebc_ctx* ctx, int step, int commit, int64_t* sel_dev) {
   if (rc) return rc;
   k_pick<<<1, 1024, 0, ctx->stream>>>(ctx->wcount, ctx->wlist, ng, (double*)ctx->part_r.p,
                                       1.0 / (double)ctx->n, ctx->cur, ctx->wgain, ctx->best, commit, step,
-                                      ctx->selected, sel_dev, ctx->stats, ctx->level);
+                                      ctx->selected, sel_dev, ctx->stats, ctx->level,
+                                      ctx->lazy_on ? ctx->ubp : nullptr, ctx->c0);
   KCHECK();
   if (ctx->timing) CU(record_step_event(ctx, ctx->ev[eb + 2]));
   return EBC_OK;
@@ -915,7 +978,7 @@ int enqueue_greedy(ebc_ctx* ctx, int k) {
 
 int do_reset(ebc_ctx* ctx) {
   const int blocks = (int)((ctx->n + 255) / 256);
-  CU(cudaMemsetAsync(ctx->stats, 0, 6 * sizeof(long long), ctx->stream));
+  CU(cudaMemsetAsync(ctx->stats, 0, 8 * sizeof(long long), ctx->stream));
   k_reset<<<blocks, 256, 0, ctx->stream>>>(ctx->n, ctx->e0d, ctx->nv32, ctx->pk, ctx->cm64, ctx->pt, ctx->selected,
                                            nullptr, tc_seeds(ctx));
   KCHECK();
@@ -923,8 +986,15 @@ int do_reset(ebc_ctx* ctx) {
     // first rung of the adaptive ladder for this run
     const int start = (ctx->screen_mode == 3 && ctx->tc_np) ? (ctx->tc_fast ? L_FAST : L_TC) : L_GRAM;
     k_set_int<<<1, 1, 0, ctx->stream>>>(ctx->level, start);
+    k_set_int<<<1, 1, 0, ctx->stream>>>(ctx->level + 1, start);
   }
   KCHECK();
+  if (ctx->lazy_on) {
+    k_fill_f64<<<(unsigned)std::min<int64_t>(4 * ctx->num_sms, (ctx->n + 255) / 256), 256, 0, ctx->stream>>>(
+        ctx->ubp, ctx->n, INFINITY);
+    KCHECK();
+  }
+  ctx->ubp_seeded = false;
   CU(cudaMemsetAsync(ctx->cur, 0, sizeof(double), ctx->stream));
   ctx->steps_done = 0;
   return EBC_OK;
@@ -934,7 +1004,7 @@ void free_ctx(ebc_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   void* ptrs[] = {c->V32, c->V64, c->e0d, c->cm64, c->pt, c->nv32, c->level, c->stats, c->Vhi, c->Vlo, c->Vf, c->tile_anchor0, c->rhomax, c->cmn, c->vsum, c->vsn, c->ipsum, c->rhomin, c->agg_any, c->pttc, c->kpmax, c->anchors, c->nva, c->tile_anchor, c->tc_vmax, c->fps_keys, c->ipa0, c->tile_rad, c->rho, c->cmx, c->cmx0, c->selected, c->chunkpart, c->counter, c->counter2, c->topc, c->toppart, c->terms, c->cur, c->best, c->uf_ctr,
-                  c->maxlb, c->wcount, c->wlist, c->wgain, c->ub};
+                  c->maxlb, c->wcount, c->wlist, c->wgain, c->ub, c->ubp, c->bflag};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, c->stream);
   DevBuf* bufs[] = {&c->tie_rec, &c->tie_all, &c->sel_hash, &c->ms_tanchor, &c->ms_trad, &c->part_g, &c->part_e, &c->part_a, &c->part_r, &c->sel_out, &c->val_out, &c->gain_out, &c->ms_part,
@@ -1199,10 +1269,11 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
   CUC(cudaMemsetAsync(ctx->pt, 0, (size_t)ctx->n_pad * sizeof(float4), ctx->stream));
   CUC(cudaMallocAsync((void**)&ctx->nv32, (size_t)ctx->n_pad * sizeof(float), ctx->stream));
   CUC(cudaMemsetAsync(ctx->nv32, 0, (size_t)ctx->n_pad * sizeof(float), ctx->stream));
-  CUC(cudaMallocAsync((void**)&ctx->stats, 6 * sizeof(long long), ctx->stream));  // [4]: tensor-screen tile pairs executed
-  CUC(cudaMemsetAsync(ctx->stats, 0, 6 * sizeof(long long), ctx->stream));
-  CUC(cudaMallocAsync((void**)&ctx->level, sizeof(int), ctx->stream));
-  CUC(cudaMemsetAsync(ctx->level, 0, sizeof(int), ctx->stream));
+  // [4]: tensor-screen tile pairs executed; [5..7] lazy steps (k_lazy_plan)
+  CUC(cudaMallocAsync((void**)&ctx->stats, 8 * sizeof(long long), ctx->stream));
+  CUC(cudaMemsetAsync(ctx->stats, 0, 8 * sizeof(long long), ctx->stream));
+  CUC(cudaMallocAsync((void**)&ctx->level, 2 * sizeof(int), ctx->stream));
+  CUC(cudaMemsetAsync(ctx->level, 0, 2 * sizeof(int), ctx->stream));
   // tensor-core screen: fp32-path grounds whose 128-candidate tile of hi+lo
   // operands plus a 2-stage ring of NP-point tiles fits shared memory
   if (dtype != EBC_F64 && ctx->screen_mode == 3) {
@@ -1322,6 +1393,14 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
   CUC(cudaMallocAsync((void**)&ctx->wlist, (size_t)n * sizeof(int64_t), ctx->stream));
   CUC(cudaMallocAsync((void**)&ctx->wgain, (size_t)n * sizeof(double), ctx->stream));
   CUC(cudaMallocAsync((void**)&ctx->ub, (size_t)n * sizeof(double), ctx->stream));
+  CUC(cudaMallocAsync((void**)&ctx->ubp, (size_t)n * sizeof(double), ctx->stream));
+  CUC(cudaMallocAsync((void**)&ctx->bflag, (size_t)((n + tc::M - 1) / tc::M + 2), ctx->stream));
+  {
+    const char* lz = getenv("EBC200_LAZY");
+    ctx->lazy_on = !(lz && lz[0] == '0');
+    const char* lc = getenv("EBC200_LAZY_CAP");
+    if (lc && lc[0]) ctx->lazy_cap = std::max(0, atoi(lc));
+  }
   double* e0dev = nullptr;
   CUC(cudaMallocAsync((void**)&e0dev, (size_t)d * sizeof(double), ctx->stream));
   {
@@ -1527,10 +1606,22 @@ int ebc_screen_info(const ebc_ctx* ctx, int64_t* out4) {
 
 int ebc_last_screen_work(const ebc_ctx* ctx, int64_t* out_pairs) {
   if (!ctx || !out_pairs) return fail(nullptr, EBC_EINVAL, "ebc_last_screen_work: NULL argument");
-  long long v[6];
+  long long v[8];
   if (cudaMemcpy(v, ctx->stats, sizeof(v), cudaMemcpyDeviceToHost) != cudaSuccess)
     return fail(const_cast<ebc_ctx*>(ctx), EBC_ECUDA, "ebc_last_screen_work: copy failed");
   *out_pairs = (int64_t)v[4] * tc::M * (ctx->tc_np ? ctx->tc_np : 0);
+  return EBC_OK;
+}
+
+int ebc_last_lazy_stats(const ebc_ctx* ctx, int64_t* out4) {
+  if (!ctx || !out4) return fail(nullptr, EBC_EINVAL, "ebc_last_lazy_stats: NULL argument");
+  long long v[8];
+  if (cudaMemcpy(v, ctx->stats, sizeof(v), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return fail(const_cast<ebc_ctx*>(ctx), EBC_ECUDA, "ebc_last_lazy_stats: copy failed");
+  out4[0] = ctx->lazy_on ? 1 : 0;
+  out4[1] = v[7];
+  out4[2] = v[5];
+  out4[3] = v[6];
   return EBC_OK;
 }
 

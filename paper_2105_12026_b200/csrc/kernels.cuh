@@ -675,12 +675,17 @@ __global__ void k_finalize(int64_t c0, int64_t c1, int nsplit, const double* __r
                            const float* __restrict__ part_e, int64_t part_stride, double einfl, double gcoef,
                            double gscale, const unsigned char* __restrict__ selected, double* __restrict__ ub,
                            long long* __restrict__ maxlb, const int* __restrict__ level_now, int level,
-                           int ub_only = 0, const double* __restrict__ part_a = nullptr) {
+                           int ub_only = 0, const double* __restrict__ part_a = nullptr,
+                           const unsigned char* __restrict__ bflag = nullptr, double* __restrict__ ubp = nullptr) {
   if (level_now && *level_now != level) return;
   __shared__ long long smax[256];
   const int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   long long key = dkey(-INFINITY);
-  if (c < c1) {
+  // lazy step (bflag set): only the flagged 128-candidate blocks were screened;
+  // the others hold stale partials and are out of the window (k_lazy_mark)
+  if (c < c1 && bflag && !bflag[(c - c0) >> 7]) {
+    ub[c - c0] = -INFINITY;
+  } else if (c < c1) {
     double g = 0.0, e = 0.0;
     for (int s = 0; s < nsplit; ++s) {
       g += part_g[s * part_stride + c];
@@ -701,6 +706,7 @@ __global__ void k_finalize(int64_t c0, int64_t c1, int nsplit, const double* __r
     } else {
       ub[c - c0] = g + eps;
       key = dkey(fmax(g - eps, 0.0));
+      if (ubp) ubp[c - c0] = fmin(ubp[c - c0], g + eps);  // both bound the current gain
     }
   }
   smax[threadIdx.x] = key;
@@ -727,7 +733,8 @@ __device__ __forceinline__ bool ub_better(double v, long long i, double bv, long
 __global__ void __launch_bounds__(256) k_argmax_ub(int64_t c0, int64_t c1, const double* __restrict__ ub,
                                                    int64_t* __restrict__ topc, double* __restrict__ part,
                                                    unsigned int* __restrict__ counter,
-                                                   const int* __restrict__ level_now, int level) {
+                                                   const int* __restrict__ level_now, int level,
+                                                   const unsigned char* __restrict__ selected = nullptr) {
   if (level_now && *level_now != level) return;
   __shared__ double sv[256];
   __shared__ long long si[256];
@@ -737,7 +744,7 @@ __global__ void __launch_bounds__(256) k_argmax_ub(int64_t c0, int64_t c1, const
   long long bi = LLONG_MAX;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < c1; c += stride) {
-    const double u = ub[c - c0];
+    const double u = (selected && selected[c]) ? -INFINITY : ub[c - c0];
     if (u > bv) {  // ascending c per thread: the first maximum is the lowest index
       bv = u;
       bi = c;
@@ -821,7 +828,9 @@ __global__ void __launch_bounds__(RED_THREADS) k_gain_top(const T* __restrict__ 
     __threadfence();
     const double tot = chunk_total_block(part, gridDim.x, sbuf);
     if (threadIdx.x == 0) {
-      *maxlb = dkey(tot);
+      // max with the bound already there (0 after the step's reset, or the lazy
+      // prologue's exact gain of the best stale bound): both are lower bounds
+      *maxlb = max(*maxlb, dkey(tot));
       *counter = 0u;
     }
   }
@@ -852,7 +861,8 @@ __global__ void k_adapt(int* __restrict__ wcount, long long* __restrict__ maxlb,
                         int level) {
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     if (*level_now == level && *wcount > cap) {
-      *level_now = level + 1;
+      level_now[0] = level + 1;
+      level_now[1] = level + 1;  // the run's rung (level_now[0] gates this step's kernels)
       *wcount = 0;
       *maxlb = 0;
     }
@@ -866,6 +876,70 @@ __global__ void k_window_all(int64_t c0, int64_t c1, const unsigned char* __rest
   if (c < c1 && !selected[c]) {
     int slot = atomicAdd(wcount, 1);
     wlist[slot] = c;
+  }
+}
+
+// ---------------------------------------------------------------- lazy Greedy (DESIGN.md §4 "Lazy steps")
+// f is monotone submodular, so a candidate's gain can only shrink as S grows:
+// gain_{s+1}(c) = sum_v max(0, cm_{s+1}(v) - d(v, c)) with cm only decreasing,
+// and the computed fp64 sums inherit it term by term (every term is monotone in
+// cm, fixed-order rounding is monotone).  ubp[c] keeps the tightest bound seen
+// for c: the screen's certified upper bound (k_finalize) or its exact fp64
+// gain (k_pick).  A later step needs to look only at the STALE candidates
+//   ubp[c] >= lb - margin - 1e-9 |lb|,   lb = exact gain of argmax_c ubp[c],
+// every other candidate is out of the reference's tie window for certain
+// (the same margin as k_window plus a rounding allowance between k_gain_top's
+// and k_refine's summation orders).  k_lazy_mark lists them (the window if
+// they are few) and flags their 128-candidate blocks (what the screen re-runs
+// if they are many).
+
+__global__ void k_fill_f64(double* __restrict__ p, int64_t n, double v) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+__global__ void __launch_bounds__(256) k_lazy_mark(int64_t c0, int64_t c1, const double* __restrict__ ubp,
+                                                   const unsigned char* __restrict__ selected,
+                                                   const long long* __restrict__ maxlb, double margin,
+                                                   int* __restrict__ wcount, int64_t* __restrict__ wlist,
+                                                   unsigned char* __restrict__ bflag) {
+  const int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  bool stale = false;
+  if (c < c1 && !selected[c]) {
+    const double lb = dkey_inv(*maxlb);
+    stale = ubp[c - c0] >= lb - margin - 1e-9 * fabs(lb);
+  }
+  // warp-aggregated append (append order is irrelevant: k_pick decides by exact
+  // value and lowest index)
+  const unsigned bal = __ballot_sync(0xffffffffu, stale);
+  if (!bal) return;
+  int base = 0;
+  if (lane == 0) base = atomicAdd(wcount, __popc(bal));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (stale) {
+    wlist[base + __popc(bal & ((1u << lane) - 1u))] = c;
+    bflag[(c - c0) >> 7] = 1;
+  }
+}
+
+// Mode of a lazy step.  Few stale candidates (<= cap, or no screen exists for
+// this ground): they ARE the window -- the screen kernels see level -1 and
+// exit, the exact refine decides.  Otherwise the screen re-runs over the
+// flagged blocks only (level[0] = the run's rung) and builds the window itself.
+// stats: [5] steps decided without a screen, [6] stale candidates, [7] lazy steps.
+__global__ void k_lazy_plan(int* __restrict__ wcount, int cap, int* __restrict__ level, long long* __restrict__ stats) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    const int cnt = *wcount;
+    stats[6] += cnt;
+    stats[7] += 1;
+    if (cnt <= cap) {
+      level[0] = -1;
+      stats[5] += 1;
+    } else {
+      level[0] = level[1];
+      *wcount = 0;
+    }
   }
 }
 
@@ -1071,7 +1145,8 @@ __global__ void __launch_bounds__(1024) k_pick(const int* __restrict__ wcount, c
                                                const double* __restrict__ cur, double* __restrict__ wgain,
                                                int64_t* __restrict__ best, int commit, int step,
                                                unsigned char* __restrict__ selected, int64_t* __restrict__ sel_out,
-                                               long long* __restrict__ stats, const int* __restrict__ level_now) {
+                                               long long* __restrict__ stats, const int* __restrict__ level_now,
+                                               double* __restrict__ ubp = nullptr, int64_t c0 = 0) {
   __shared__ double smax[1024];
   __shared__ long long smin[1024];
   const int wc = *wcount;
@@ -1080,6 +1155,7 @@ __global__ void __launch_bounds__(1024) k_pick(const int* __restrict__ wcount, c
   for (int w = threadIdx.x; w < wc; w += blockDim.x) {
     const double gsum = chunk_total(part_r + (int64_t)w * ng, ng);
     wgain[w] = gsum;
+    if (ubp) ubp[wlist[w] - c0] = gsum;  // the exact gain bounds every later one (submodularity)
     const double val = __dadd_rn(f, __dmul_rn(gsum, inv_n));  // no FMA contraction: host pick() matches
     top = fmax(top, val);
   }
@@ -1108,7 +1184,7 @@ __global__ void __launch_bounds__(1024) k_pick(const int* __restrict__ wcount, c
     if (stats) {  // [0] sum of window sizes, [1] max window, [2] screen rung, [3] steps
       stats[0] += wc;
       stats[1] = max(stats[1], (long long)wc);
-      stats[2] = level_now ? *level_now : -1;
+      stats[2] = level_now ? level_now[1] : -1;
       stats[3] += 1;
     }
     if (commit && b >= 0) {

@@ -559,7 +559,9 @@ __global__ void k_tile_vsum(const float* __restrict__ V32, int pitch, int64_t n,
 // otherwise -- the late steps of a run).
 __global__ void k_tile_ipsum(const float* __restrict__ ipa, int64_t stride, int na, int64_t n, int64_t ntiles,
                              int np, double* __restrict__ ipsum, const float* __restrict__ rhomin, float radmin,
-                             const float* __restrict__ cmn, int* __restrict__ anyflag) {
+                             const float* __restrict__ cmn, int* __restrict__ anyflag,
+                             const int* __restrict__ level_now = nullptr) {
+  if (level_now && *level_now < 0) return;  // lazy step decided without a screen
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= (int64_t)na * ntiles) return;
@@ -612,6 +614,9 @@ struct TcAnchors {
   // MS: the per-tile seed/final-add quantum kpmax is scaled by kpscale to cover
   // the in-MMA fp32 accumulation of the seed parts ((kpad + 24) 2^-23 |ip|)
   float kpscale = 1.f;
+  // lazy step (kernels.cuh k_lazy_mark): screen only the 128-candidate blocks
+  // flagged here (nullptr: every block); indexed by (crow - cand0) >> 7
+  const unsigned char* bflag = nullptr;
 };
 
 // One CTA: candidates [cand0 + 128*bx, +128) x V tiles [t0, t1) of NP points.
@@ -663,6 +668,10 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   static_assert(MB == 1 || (MB == 2 && NP == 64 && MS && !FLAG && EPI_WARPGROUPS == 2), "two-block CTA shape");
   constexpr int TSH = MB == 2 ? 1 : 0;  // per-tile host arrays: 128-point tiles
   const int64_t crow = cand0 + (int64_t)blockIdx.x * M * MB;
+  if (an.bflag) {  // CTA-uniform: exits before any barrier or TMEM allocation
+    const int64_t b0 = (int64_t)blockIdx.x * MB;
+    if (!an.bflag[b0] && (MB == 1 || !an.bflag[b0 + 1])) return;
+  }
 
   if (tid == 0) {
     for (int s = 0; s < stages; ++s) {
@@ -1047,6 +1056,7 @@ __global__ void __launch_bounds__(128) k_screen_agg(const float* __restrict__ V3
                                                     int64_t part_stride, const int* __restrict__ level_now,
                                                     int level, const int* __restrict__ anyflag) {
   if (level_now && *level_now != level) return;
+  if (an.bflag && !an.bflag[blockIdx.x]) return;  // lazy step: block not re-screened
   if (*anyflag == 0) {  // no tile can be all-positive this step
     part_a[blockIdx.y * part_stride + cand0 + (int64_t)blockIdx.x * 128 + threadIdx.x] = 0.0;
     return;
