@@ -871,14 +871,13 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     float e = 0.f;
     constexpr int NB = TM::NB;
     constexpr int SW = SLICE;  // accumulator columns per thread and tile
-    for (int it = 0; it < ntk; ++it) {
-      const int b = it % NB;
-      const int tt = t0 + TL(it);  // point tile
-      // this slice's point seeds ip: issued before the accumulator wait so the
-      // (L1-broadcast) loads overlap the MMA
-      float ipv[MS ? 1 : SW];
+    // this slice's point seeds ip, software-pipelined one tile ahead: tile it+1's
+    // loads are issued as soon as tile it's seed add has consumed the registers,
+    // so their L2 latency hides behind the rest of tile it's epilogue
+    float ipv[MS ? 1 : SW];
+    auto load_seeds = [&](int itn) {
       if constexpr (!MS) {
-        const float4* pp4 = reinterpret_cast<const float4*>(ipa + (int64_t)tt * NP + half * SLICE);
+        const float4* pp4 = reinterpret_cast<const float4*>(ipa + (int64_t)(t0 + TL(itn)) * NP + half * SLICE);
 #pragma unroll
         for (int i = 0; i < SW / 4; ++i) {
           const float4 p = __ldg(pp4 + i);
@@ -888,6 +887,11 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
           ipv[4 * i + 3] = p.w;
         }
       }
+    };
+    if (ntk > 0) load_seeds(0);
+    for (int it = 0; it < ntk; ++it) {
+      const int b = it % NB;
+      const int tt = t0 + TL(it);  // point tile
       // one error quantum per tile: kpmax = max_v kp over the tile (bounds every
       // pair's kp_v; computed at reset, cm only decreases within a run)
       float kpt, vmt;
@@ -899,9 +903,6 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         kpt = kpa[tt >> TSH];
         vmt = __ldg(an.vmax + (tt >> TSH));
       }
-      const float kq = fmaf(kpt, an.kpscale, fmaf(kxc, vmt, kc));
-      const float thr = -kq;           // FLAG: possibly closer than e0 iff a > -kq
-      const float icq = ic + kq;       // bound: a + kq = b + icq
       mbar_wait(&tfull[b], (it / NB) & 1);
       fence_after();
       float S[SW];
@@ -909,6 +910,14 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
                  (uint32_t)(MB == 2 ? (half * NB + b) * NP : b * NP + half * SLICE), S);
       fence_before();
       mbar_arrive(&tempty[b]);  // this thread's columns of the buffer are in registers
+      // the quantum is formed only now: its inputs share a load scoreboard with
+      // the seed loads, and an FFMA scheduled before the tcgen05.ld held the
+      // load's issue behind them (ncu, C4: 13% of stall samples).  vmt + 0*S[0]
+      // (exactly vmt: S is finite) makes the FFMA depend on the TMEM load.
+      const float vmt_after = __fadd_rn(vmt, __fmul_rn(S[0], 0.f));
+      const float kq = fmaf(kpt, an.kpscale, fmaf(kxc, vmt_after, kc));
+      const float thr = -kq;           // FLAG: possibly closer than e0 iff a > -kq
+      const float icq = ic + kq;       // bound: a + kq = b + icq
       // b = S + ip per pair, a = b + ic.  fl(b + ic) is monotone in b, so
       // max_i a_i = fl(max_i b_i + ic): when that is <= thr (< 0) every pair
       // adds exactly 0 to the gain and to the count, and the tile is skipped --
@@ -943,6 +952,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
 #pragma unroll
       for (int i = 0; i < SW; ++i) S[i] += ipv[i];
 #endif
+      if (it + 1 < ntk) load_seeds(it + 1);  // ipv is free again
       }
 #pragma unroll
       for (int i = 0; i < SW; i += 8) {

@@ -41,6 +41,8 @@ def config_data(name: str) -> np.ndarray:
         return x.astype(np.float16) if name == "C3" else x
     if name == "C4":
         return surrogate(500_000, 32, 5, 0.01, 0).astype(np.float32)
+    if name == "C4S50":  # the 50-regime near-tie stress case of C4
+        return surrogate(500_000, 32, 50, 0.01, 0).astype(np.float32)
     if name == "C5":
         return c5_problem()[0]
     raise KeyError(name)
@@ -55,4 +57,4 @@ def c5_problem(n: int = 200_000, d: int = 64, l: int = 4096, size: int = 10, see
     return x, sets
 
 
-CONFIG_K = {"C1": 10, "C2": 50, "C3": 50, "C4": 20}
+CONFIG_K = {"C1": 10, "C2": 50, "C3": 50, "C4": 20, "C4S50": 20}
