@@ -70,6 +70,13 @@ int ebc_baseline(const ebc_ctx* ctx, double* out);
 int ebc_eval_multiset(ebc_ctx* ctx, const int64_t* offsets, const int64_t* idx, int64_t l,
                       double* out_f, int64_t* out_bad_set, int64_t* out_bad_index);
 
+/* k-medoids loss of explicit representatives: mean over the ground rows of the
+ * exact fp64 squared distance to the nearest of the r representatives
+ * (reps: r x d row-major fp64, finite), the ground values widened exactly to
+ * fp64.  EBC_EINVAL for r < 1 or a non-finite representative (the reference's
+ * messages).  Replaces: k_medoids_loss (ebc.py:21-43). */
+int ebc_kmedoids_loss(ebc_ctx* ctx, const double* reps, int64_t r, double* out);
+
 /* Full Greedy(k) on this device: k steps of screen -> certified fp64 refine ->
  * argmax with the reference tie window -> cached-min update, no host sync
  * between steps.  out_sel/out_val/out_gain receive k entries (out_val[s] is

@@ -50,6 +50,7 @@ def _load():
                                           _i64p, _f64p, _f64p, _i64p]
         lib.ebc_oracle_step_values.argtypes = [_f64p, ctypes.c_int64, ctypes.c_int, _f64p, _i64p, ctypes.c_int,
                                                _i64p, ctypes.c_int64, _f64p]
+        lib.ebc_oracle_kmedoids.argtypes = [_f64p, ctypes.c_int64, ctypes.c_int, _f64p, ctypes.c_int64, _f64p]
         lib.ebc_oracle_set_threads.argtypes = [ctypes.c_int]
         lib.ebc_oracle_num_threads.restype = ctypes.c_int
         lib.ebc_oracle_sqdist.restype = ctypes.c_double
@@ -140,3 +141,15 @@ def step_values(V, selected: Sequence[int], candidates: Sequence[int], e0=None) 
     if rc:
         raise ValueError("oracle step_values: invalid argument")
     return out
+
+
+def kmedoids_loss(V, reps) -> float:
+    """k_medoids_loss(GroundMatrix(V), reps) of the reference (ebc.py:21-43), fp64."""
+    V64 = _as64(V)
+    n, d = V64.shape
+    R = np.ascontiguousarray(np.atleast_2d(np.asarray(reps, dtype=np.float64)))
+    out = ctypes.c_double()
+    rc = _load().ebc_oracle_kmedoids(_p(V64), n, d, _p(R), R.shape[0], ctypes.byref(out))
+    if rc:
+        raise ValueError("oracle kmedoids_loss: invalid argument")
+    return float(out.value)

@@ -284,3 +284,26 @@ int ebc_oracle_step_values(const double* V, int64_t n, int d, const double* e0,
   free(VT);
   return 0;
 }
+
+/* k-medoids loss of explicit representatives (ebc.py:21-43): per ground row the
+ * minimum over reps of the exact fp64 distance (starting from +inf), summed left
+ * to right (_ordered_sum, ebc.py:13-18), divided by n. */
+int ebc_oracle_kmedoids(const double* V, int64_t n, int d, const double* reps, int64_t r, double* out) {
+  if (!V || !reps || !out || n < 1 || d < 1 || r < 1) return 1;
+  double* mins = (double*)malloc((size_t)n * sizeof(double));
+  if (!mins) return 1;
+#pragma omp parallel for schedule(static)
+  for (int64_t v = 0; v < n; ++v) {
+    double m = INFINITY;
+    for (int64_t j = 0; j < r; ++j) {
+      const double t = sqdist(V + v * d, reps + j * d, d);
+      if (t < m) m = t;
+    }
+    mins[v] = m;
+  }
+  double s = 0.0;
+  for (int64_t v = 0; v < n; ++v) s += mins[v];
+  free(mins);
+  *out = s / (double)n;
+  return 0;
+}

@@ -11,16 +11,16 @@ default) computing on an sm_100a GPU through libebc200.so.
 
 from .core import (Dissimilarity, EvalMultiset, GroundMatrix, Precision, SquaredEuclidean, Summary,
                    make_auxiliary_vector, squared_euclidean)
-from .ebc import EbcFunction
+from .ebc import EbcFunction, k_medoids_loss
 from .optimize import (BACKENDS, OptimizerBudget, evaluate_multiset_batched, evaluate_with_backend,
                        greedy_maximize, parse_backend_spec, sieve_stream_maximize)
-from .sharded import greedy_maximize_sharded
+from .sharded import evaluate_multiset_sharded, greedy_maximize_sharded
 
 __version__ = "0.1.0"
 
 __all__ = [
     "Dissimilarity", "EvalMultiset", "GroundMatrix", "Precision", "SquaredEuclidean", "Summary",
-    "make_auxiliary_vector", "squared_euclidean", "EbcFunction", "BACKENDS", "OptimizerBudget",
+    "make_auxiliary_vector", "squared_euclidean", "EbcFunction", "k_medoids_loss", "BACKENDS", "OptimizerBudget",
     "evaluate_multiset_batched", "evaluate_with_backend", "greedy_maximize", "parse_backend_spec",
-    "greedy_maximize_sharded", "sieve_stream_maximize",
+    "greedy_maximize_sharded", "evaluate_multiset_sharded", "sieve_stream_maximize",
 ]

@@ -35,6 +35,7 @@ SIGNATURES = {
     "ebc_baseline": (ctypes.c_int, [_vp, _f64p]),
     "ebc_eval_multiset": (ctypes.c_int, [_vp, _i64p, _i64p, _i64, _f64p, _i64p, _i64p]),
     "ebc_greedy": (ctypes.c_int, [_vp, _i32, _i64p, _f64p, _f64p, _i64p]),
+    "ebc_kmedoids_loss": (ctypes.c_int, [_vp, _f64p, _i64, _f64p]),
     "ebc_shard_set_range": (ctypes.c_int, [_vp, _i64, _i64]),
     "ebc_shard_step": (ctypes.c_int, [_vp, _i64p, _f64p, _i64, _i64p, _f64p]),
     "ebc_shard_commit": (ctypes.c_int, [_vp, _i64, _f64p]),

@@ -2012,6 +2012,49 @@ int ebc_shard_commit(ebc_ctx* ctx, int64_t s, double* out_value) {
   return EBC_OK;
 }
 
+int ebc_kmedoids_loss(ebc_ctx* ctx, const double* reps, int64_t r, double* out) {
+  if (!ctx) return fail(nullptr, EBC_EINVAL, "ebc_kmedoids_loss: NULL context");
+  if (!reps || !out) return fail(ctx, EBC_EINVAL, "ebc_kmedoids_loss: NULL argument");
+  if (r < 1) return fail(ctx, EBC_EINVAL, "the loss is undefined for an empty representative set");
+  for (int64_t i = 0; i < r * ctx->d; ++i)
+    if (!std::isfinite(reps[i])) return fail(ctx, EBC_EINVAL, "representatives must be finite");
+  CU(cudaSetDevice(ctx->device));
+  ctx->launches = 0;
+  int rc = ensure(ctx, ctx->ms_part, (size_t)r * ctx->d * sizeof(double));
+  if (rc) return rc;
+  CU(cudaMemcpyAsync(ctx->ms_part.p, reps, (size_t)r * ctx->d * sizeof(double), cudaMemcpyHostToDevice,
+                     ctx->stream));
+  // representatives staged in shared memory, up to 48 KB per pass
+  const int per = (int)std::max<int64_t>(1, std::min<int64_t>(r, 6144 / ctx->d));
+  const unsigned grid = (unsigned)((ctx->n + RED_THREADS - 1) / RED_THREADS);
+  for (int64_t r0 = 0; r0 < r; r0 += per) {
+    const int r1 = (int)std::min<int64_t>(r, r0 + per);
+    const size_t smem = (size_t)(r1 - r0) * ctx->d * sizeof(double);
+    if (ctx->dtype == EBC_F64) {
+      CU(cudaFuncSetAttribute(k_kmed_min<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      k_kmed_min<double><<<grid, RED_THREADS, smem, ctx->stream>>>(ctx->V64, ctx->pitch, ctx->n, ctx->d,
+                                                                   (const double*)ctx->ms_part.p, (int)r0, r1,
+                                                                   ctx->terms, r0 == 0);
+    } else {
+      CU(cudaFuncSetAttribute(k_kmed_min<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      k_kmed_min<float><<<grid, RED_THREADS, smem, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->n, ctx->d,
+                                                                  (const double*)ctx->ms_part.p, (int)r0, r1,
+                                                                  ctx->terms, r0 == 0);
+    }
+    KCHECK();
+  }
+  k_sum_chunks<<<ctx->nchunks, RED_THREADS, 0, ctx->stream>>>(ctx->terms, ctx->n, ctx->chunkpart);
+  KCHECK();
+  rc = ensure(ctx, ctx->ms_out, sizeof(double));
+  if (rc) return rc;
+  double* dout = (double*)ctx->ms_out.p;
+  k_mean<<<1, 1, 0, ctx->stream>>>(ctx->chunkpart, ctx->nchunks, (double)ctx->n, dout);
+  KCHECK();
+  CU(cudaMemcpyAsync(out, dout, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return EBC_OK;
+}
+
 int ebc_eval_multiset(ebc_ctx* ctx, const int64_t* offsets, const int64_t* idx, int64_t l, double* out_f,
                       int64_t* out_bad_set, int64_t* out_bad_index) {
   if (!ctx) return fail(nullptr, EBC_EINVAL, "ebc_eval_multiset: NULL context");

@@ -320,6 +320,11 @@ __global__ void k_total(const double* __restrict__ part, int nchunks, double sca
   if (threadIdx.x == 0 && blockIdx.x == 0) *out = chunk_total(part, nchunks) * scale;
 }
 
+// out = (sum of the chunk partials, left to right) / n -- ebc.py:43's division
+__global__ void k_mean(const double* __restrict__ part, int nchunks, double n, double* __restrict__ out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) *out = chunk_total(part, nchunks) / n;
+}
+
 // ---------------------------------------------------------------- K1: screen
 //
 // gain32[c] = sum_v max(0, cm32[v] - d32(v, c)) for a tile of candidates, with
@@ -877,6 +882,41 @@ __global__ void k_window_all(int64_t c0, int64_t c1, const unsigned char* __rest
     int slot = atomicAdd(wcount, 1);
     wlist[slot] = c;
   }
+}
+
+// ---------------------------------------------------------------- k-medoids loss (ebc.py:21-43)
+// mins[v] = min over the explicit representatives [r0, r1) of the exact fp64
+// direct distance (core.py:236-251), folded into the running minimum of earlier
+// representative chunks (first chunk: from +inf, ebc.py:42 initial=np.inf).
+template <typename T>
+__global__ void __launch_bounds__(RED_THREADS) k_kmed_min(const T* __restrict__ V, int pitch, int64_t n, int d,
+                                                          const double* __restrict__ reps, int r0, int r1,
+                                                          double* __restrict__ mins, int first) {
+  extern __shared__ double sr[];  // (r1 - r0) x d
+  const int nr = r1 - r0;
+  for (int i = threadIdx.x; i < nr * d; i += blockDim.x) sr[i] = reps[(int64_t)r0 * d + i];
+  __syncthreads();
+  const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= n) return;
+  double m = first ? INFINITY : mins[v];
+  for (int r = 0; r < nr; ++r) m = fmin(m, dist64_row(V + v * pitch, sr + (int64_t)r * d, d));
+  mins[v] = m;
+}
+
+// part[chunk] = fixed-order sum of x over the chunk (the k_init structure:
+// RCH points per block, RCH / RED_THREADS points per thread in order, the
+// fixed 256-thread tree); k_total then adds the chunks left to right.
+__global__ void __launch_bounds__(RED_THREADS) k_sum_chunks(const double* __restrict__ x, int64_t n,
+                                                            double* __restrict__ part) {
+  __shared__ double sbuf[RED_THREADS];
+  const int64_t base = (int64_t)blockIdx.x * RCH;
+  double acc = 0.0;
+  for (int i = 0; i < RCH / RED_THREADS; ++i) {
+    const int64_t v = base + threadIdx.x + (int64_t)i * RED_THREADS;
+    if (v < n) acc += x[v];
+  }
+  const double s = block_sum_256(acc, sbuf);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
 // ---------------------------------------------------------------- lazy Greedy (DESIGN.md §4 "Lazy steps")

@@ -129,6 +129,35 @@ class EbcFunction:
             pass
 
 
+def k_medoids_loss(ground: GroundMatrix, reps, distance: Optional[Dissimilarity] = None) -> float:
+    """Mean distance of every ground observation to its nearest representative
+    (ebc.py:21-43): ``reps`` are explicit vectors of the ground dimensionality,
+    the loss is computed in fp64 on the device (exact direct distances from the
+    stored values, per-row minimum from +inf, fixed-order sum, / n).  The ground
+    keeps one device context for these calls (created on first use)."""
+    reps_arr = np.atleast_2d(np.asarray(reps, dtype=np.float64))
+    if reps_arr.size == 0:
+        raise ValueError("the loss is undefined for an empty representative set")
+    if reps_arr.shape[1] != ground.dims:
+        raise ValueError(f"representative dimensionality {reps_arr.shape[1]} does not match "
+                         f"ground dims {ground.dims}")
+    if not np.all(np.isfinite(reps_arr)):
+        raise ValueError("representatives must be finite")
+    if distance is not None and not isinstance(distance, SquaredEuclidean):
+        raise ValueError(f"the b200 backend only implements squared Euclidean distance, "
+                         f"got {type(distance).__name__}")
+    f = getattr(ground, "_b200_kmedoids", None)
+    if f is None:
+        f = EbcFunction(ground)
+        ground._b200_kmedoids = f
+    reps_arr = np.ascontiguousarray(reps_arr)
+    out = ctypes.c_double()
+    rc = f._lib.ebc_kmedoids_loss(f._ctx, reps_arr.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                  reps_arr.shape[0], ctypes.byref(out))
+    _native.check(rc, f._ctx)
+    return float(out.value)
+
+
 def _two_sets(indices, e):
     base = [int(i) for i in indices]
     idx = np.asarray(base + base + [int(e)], dtype=np.int64)

@@ -309,3 +309,79 @@ def greedy_maximize_sharded(f, budget: OptimizerBudget, group=None) -> Summary:
         return greedy_sharded_loop(engine, n, int(budget.k), group=group, device=device)
     finally:
         engine.close()
+
+
+# ---------------------------------------------------------------- work-matrix sharding (C5)
+# the sets of a multiset are independent units.  Rank r
+# evaluates a contiguous range of sets [j0, j1) on its own GPU (V replicated),
+# the fp64 values are all-gathered in rank order.  A set's value is a
+# fixed-order reduction over the points that does not depend on which rank (or
+# how many) evaluates it, so the gathered vector is bit-identical to the
+# single-GPU call (batched.py:180-240 evaluates the same sets in one process).
+
+def set_range(offsets: np.ndarray, rank: int, world: int) -> Tuple[int, int]:
+    """Contiguous set range of `rank`, balanced by work: each set weighs its
+    member count + 1 (a set costs one pass over the points per member; the +1
+    keeps runs of empty sets from piling onto one rank)."""
+    offsets = np.asarray(offsets, dtype=np.int64)
+    l = offsets.size - 1
+    w = np.diff(offsets) + 1
+    cum = np.concatenate([[0], np.cumsum(w)])
+    total = int(cum[-1])
+    bounds = [int(np.searchsorted(cum, (r * total + world - 1) // world, side="left")) for r in range(world + 1)]
+    bounds[0], bounds[-1] = 0, l
+    j0 = min(l, bounds[rank])
+    j1 = min(l, max(j0, bounds[rank + 1]))
+    return j0, j1
+
+
+def _first_bad_index(offsets: np.ndarray, idx: np.ndarray, n: int):
+    """(set, index) of the first out-of-range member in set order, or None."""
+    bad = np.nonzero((idx < 0) | (idx >= n))[0]
+    if bad.size == 0:
+        return None
+    p = int(bad[0])
+    j = int(np.searchsorted(offsets, p, side="right") - 1)
+    return j, int(idx[p])
+
+
+def evaluate_multiset_sharded(f, multiset, group=None, evaluate=None) -> np.ndarray:
+    """f(S_j) for every set, fp64, in multiset order, the sets split across the
+    ranks of `group` (torch.distributed must be initialised; every rank passes
+    the same multiset and its own EbcFunction on its own GPU).  Out-of-range
+    indices raise the reference's IndexError (core.py:140-143) on every rank,
+    before any device work.  ``evaluate(offsets, idx, l)`` overrides the local
+    evaluator (tests); default: the rank's device (ebc_eval_multiset)."""
+    import torch
+    import torch.distributed as dist
+
+    offsets, idx = multiset.csr()
+    offsets = np.asarray(offsets, dtype=np.int64)
+    idx = np.asarray(idx, dtype=np.int64)
+    n = f.ground.n if f is not None else None
+    if n is not None:
+        bad = _first_bad_index(offsets, idx, n)
+        if bad is not None:
+            raise IndexError(f"set {bad[0]}: index {bad[1]} out of range for ground size {n}")
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    l = offsets.size - 1
+    ranges = [set_range(offsets, r, world) for r in range(world)]
+    j0, j1 = ranges[rank]
+    if evaluate is None:
+        evaluate = f._eval_csr
+    local = np.zeros(0)
+    if j1 > j0:
+        lo = offsets[j0:j1 + 1] - offsets[j0]
+        local = np.asarray(evaluate(lo, idx[offsets[j0]:offsets[j1]], j1 - j0), dtype=np.float64)
+    nccl = dist.get_backend(group) == "nccl"
+    dev = torch.device(f"cuda:{torch.cuda.current_device()}") if nccl else torch.device("cpu")
+    m = max(b - a for a, b in ranges) or 1
+    buf = torch.zeros(m, dtype=torch.float64, device=dev)
+    if local.size:
+        buf[: local.size] = torch.from_numpy(local).to(dev)
+    parts = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(parts, buf, group=group)
+    out = np.empty(l, dtype=np.float64)
+    for r, (a, b) in enumerate(ranges):
+        out[a:b] = parts[r][: b - a].cpu().numpy()
+    return out

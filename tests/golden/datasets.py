@@ -58,3 +58,28 @@ def c5_problem(n: int = 200_000, d: int = 64, l: int = 4096, size: int = 10, see
 
 
 CONFIG_K = {"C1": 10, "C2": 50, "C3": 50, "C4": 20, "C4S50": 20}
+
+
+def kmedoids_cases():
+    """Seeded k_medoids_loss inputs (tests/golden/make_golden_kmedoids.py pairs
+    each with the reference's loss): (precision name, data fp64, reps fp64)."""
+    rng = np.random.default_rng(2105)
+    precs = ["fp32", "fp16-storage", "fp64"]
+    half = {"fp32": np.float32, "fp16-storage": np.float16, "fp64": np.float64}
+    out = []
+    for i in range(18):
+        n = int(rng.integers(1, 3000))
+        d = int(rng.integers(1, 70))
+        r = int(rng.integers(1, 40))
+        prec = precs[i % 3]
+        scale = float(rng.choice([0.01, 1.0, 30.0]))
+        data = rng.standard_normal((n, d)) * scale + float(rng.choice([0.0, 5.0]))
+        if i % 4 == 0:  # representatives taken from the stored ground rows (exact zeros there)
+            stored = data.astype(half[prec]).astype(np.float64)
+            reps = stored[rng.choice(n, size=min(r, n), replace=False)]
+        else:
+            reps = rng.standard_normal((r, d)) * scale
+        out.append((prec, data, reps))
+    two = np.array([[0.0, 1.0], [0.0, -1.0]])
+    out.append(("fp64", two, np.array([[0.0, 0.0]])))  # test_ebc.py:29-30: (1 + 1) / 2
+    return out

@@ -194,3 +194,27 @@ def test_surrogate_restatement_matches_reference_generator():
     X, _ = generate_surrogate(SurrogateSpec(n_cycles=600, dims=32, n_regimes=5, cycles_per_regime=120,
                                             noise_scale=0.01, seed=0))
     assert np.array_equal(X, datasets.surrogate(600, 32, 5, 0.01, 0))
+
+
+def test_kmedoids_validation_before_any_device_work():
+    """k_medoids_loss raises the reference's ValueErrors (ebc.py:31-40) on the host."""
+    g = eb.GroundMatrix(np.zeros((3, 2)), eb.Precision.FP64)
+    with pytest.raises(ValueError, match="empty representative set"):
+        eb.k_medoids_loss(g, np.empty((0, 2)))
+    with pytest.raises(ValueError, match="representative dimensionality 3 does not match ground dims 2"):
+        eb.k_medoids_loss(g, [[1.0, 2.0, 3.0]])
+    with pytest.raises(ValueError, match="representatives must be finite"):
+        eb.k_medoids_loss(g, [[1.0, np.nan]])
+
+
+def test_set_ranges_partition_in_order():
+    from paper_2105_12026_b200.sharded import set_range
+    rng = np.random.default_rng(3)
+    for _ in range(50):
+        lens = rng.integers(0, 20, size=int(rng.integers(1, 60)))
+        off = np.concatenate([[0], np.cumsum(lens)])
+        for world in (1, 2, 3, 5, 8, 13):
+            rs = [set_range(off, r, world) for r in range(world)]
+            assert rs[0][0] == 0 and rs[-1][1] == len(lens)
+            for (a, b), (c, _) in zip(rs, rs[1:]):
+                assert a <= b == c

@@ -652,3 +652,57 @@ def test_two_block_cta_odd_block_counts(monkeypatch, n, prec):
         out[mb] = (s.selected, s.gains)
         f.close()
     assert out["1"] == out["0"]
+
+
+# ------------------------------------------------------------ k-medoids loss (ebc.py:21-43)
+
+def test_kmedoids_hand_values():
+    """test_ebc.py:19-38 of the reference: exact small answers."""
+    two = eb.GroundMatrix(np.array([[0.0, 1.0], [0.0, -1.0]]), eb.Precision.FP64)
+    assert eb.k_medoids_loss(two, [[0.0, 0.0]]) == 1.0
+    assert eb.k_medoids_loss(two, [[0.0, 1.0], [0.0, -1.0]]) == 0.0
+    g = eb.GroundMatrix(np.array([[0.0, 0.0], [2.0, 0.0]]), eb.Precision.FP64)
+    assert eb.k_medoids_loss(g, [[0.0, 0.0]]) == 2.0
+
+
+def test_kmedoids_matches_reference_goldens():
+    import sys
+    sys.path.insert(0, GOLDEN_DIR)
+    import datasets
+    want = json.load(open(os.path.join(GOLDEN_DIR, "reference_kmedoids.json")))["losses"]
+    for (prec, data, reps), w in zip(datasets.kmedoids_cases(), want):
+        got = eb.k_medoids_loss(eb.GroundMatrix(data, PREC[prec]), reps)
+        assert abs(got - w) <= 1e-12 * max(1.0, abs(w)), (prec, data.shape, reps.shape, got, w)
+
+
+def test_kmedoids_full_size_vs_oracle():
+    """C2-sized ground, many representatives (several shared-memory passes)."""
+    X = np.random.default_rng(11).standard_normal((100_000, 100)).astype(np.float32)
+    reps = np.random.default_rng(12).standard_normal((300, 100))
+    got = eb.k_medoids_loss(eb.GroundMatrix(X, eb.Precision.FP32), reps)
+    want = oracle.kmedoids_loss(X.astype(np.float64), reps)
+    assert abs(got - want) <= 1e-12 * abs(want)
+
+
+# ------------------------------------------------------------ work-matrix sharding (C5, SURVEY §8(e) row 2)
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_sharded_multiset_emulated_ranks_bit_identical(world):
+    """Each emulated rank evaluates its contiguous set range through the C-ABI;
+    the concatenation must equal the single-call values bit for bit."""
+    from paper_2105_12026_b200.sharded import set_range
+    rng = np.random.default_rng(5)
+    X = rng.standard_normal((50_000, 64)).astype(np.float32)
+    sets = [rng.choice(50_000, size=int(rng.integers(0, 14)), replace=False).tolist() for _ in range(700)]
+    f = fn(X, eb.Precision.FP32)
+    ms = eb.EvalMultiset(sets)
+    full = eb.evaluate_with_backend(f, ms)
+    off, idx = ms.csr()
+    parts = []
+    for r in range(world):
+        j0, j1 = set_range(off, r, world)
+        if j1 > j0:
+            parts.append(f._eval_csr(off[j0:j1 + 1] - off[j0], idx[off[j0]:off[j1]], j1 - j0))
+    assert np.array_equal(np.concatenate(parts), full)
+    want = oracle.eval_multiset(X.astype(np.float64), sets)
+    assert max_scaled_diff(full, want) <= 1e-12

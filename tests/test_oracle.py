@@ -68,3 +68,16 @@ def test_step_values_consistent_with_greedy():
     sel, vals, _, _ = oracle.greedy(V, 4)
     v = oracle.step_values(V, sel[:3], [sel[3]])
     assert v[0] == vals[3]
+
+
+def test_oracle_kmedoids_matches_reference():
+    """k_medoids_loss (ebc.py:21-43): reference-produced losses on seeded inputs."""
+    import json
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(__file__), "golden"))
+    import datasets
+    want = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "reference_kmedoids.json")))["losses"]
+    store = {"fp32": np.float32, "fp16-storage": np.float16, "fp64": np.float64}
+    for (prec, data, reps), w in zip(datasets.kmedoids_cases(), want):
+        got = oracle.kmedoids_loss(data.astype(store[prec]).astype(np.float64), reps)
+        assert abs(got - w) <= 1e-14 * max(1.0, abs(w)), (prec, data.shape, got, w)

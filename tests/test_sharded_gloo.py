@@ -96,3 +96,62 @@ def test_sharded_greedy_matches_single_process(world):
         np.testing.assert_allclose(np.cumsum(g), vals, rtol=1e-12)
     # all ranks agree exactly
     assert len({tuple(r[1]) for r in res}) == 1 and len({r[2] for r in res}) == 1
+
+
+# ---------------------------------------------------------------- work-matrix (C5) sharding
+
+class _StubFunction:
+    """Carries the ground size for the sharded multiset driver's index check;
+    the device evaluator is replaced by the oracle on the rank's slice."""
+
+    class _G:
+        def __init__(self, n):
+            self.n = n
+
+    def __init__(self, n):
+        self.ground = self._G(n)
+
+
+def _ms_worker(rank, world, port, V, sets, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2105_12026_b200 import EvalMultiset
+        from paper_2105_12026_b200.sharded import evaluate_multiset_sharded
+
+        def local_eval(offsets, idx, l):
+            return oracle.eval_multiset(V, [idx[offsets[j]:offsets[j + 1]].tolist() for j in range(l)])
+
+        ms = EvalMultiset(sets)
+        vals = evaluate_multiset_sharded(_StubFunction(V.shape[0]), ms, evaluate=local_eval)
+        err = None
+        try:
+            evaluate_multiset_sharded(_StubFunction(V.shape[0]), EvalMultiset(sets + [[0, V.shape[0] + 3]]),
+                                      evaluate=local_eval)
+        except IndexError as e:
+            err = str(e)
+        q.put((rank, vals.tolist(), err))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_multiset_matches_single_process(world):
+    rng = np.random.default_rng(23)
+    V = rng.standard_normal((400, 5))
+    sets = [rng.choice(400, size=int(rng.integers(0, 12)), replace=False).tolist() for _ in range(37)]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ms_worker, args=(r, world, port, V, sets, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = oracle.eval_multiset(V, sets)
+    for rank, vals, err in res:
+        assert np.array_equal(np.asarray(vals), want), f"rank {rank}"  # bit-identical to one process
+        assert err == f"set {len(sets)}: index {V.shape[0] + 3} out of range for ground size {V.shape[0]}"
