@@ -119,6 +119,7 @@ struct ebc_ctx {
   PtCoef pk{};
   // screen mode: 0 direct, 1 FFMA Gram, 2 adaptive from FFMA Gram, 3 adaptive from the tensor screen
   int screen_mode = 2;
+  bool fp32_ok = true;  // ebc_create's range guard: false -> no fp32 screen at all (screen_mode -1)
   int wcap = 256;
   // tensor-core Gram screen (tcgen05, kind::tf32, 3xTF32)
   void* Vhi = nullptr;
@@ -342,6 +343,7 @@ int screen_shape_choice(const ebc_ctx* ctx) {
 }
 
 int plan_screen(const ebc_ctx* ctx, ScreenPlan& p) {
+  if (ctx->screen_mode < 0) return EBC_EINVAL;  // out of the fp32 range: exact refine only
   p.shape = screen_shape_choice(ctx);
   int rc;
   if (p.shape == 2) {
@@ -1262,6 +1264,37 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
     else
       k_pad<double, double><<<blocks, 256, 0, ctx->stream>>>((const double*)raw, n, d, ctx->V64, ctx->pitch);
     CUC(cudaGetLastError());
+  }
+  if (dtype != EBC_F64) {
+    // fp32 range guard: every screen (and the sparse work-matrix flag screen)
+    // forms squared distances, norms and short sums in fp32.  Grounds whose
+    // distances could leave the fp32 range (|x| ~ 1e15 and beyond: the
+    // reference's exact fp64 path still handles them) run without a screen --
+    // every candidate goes to the exact fp64 refine (lazy steps keep that to
+    // the stale ones) and work matrices to the dense fp64 kernel.
+    unsigned int* amax = nullptr;
+    CUC(cudaMallocAsync((void**)&amax, sizeof(unsigned int), ctx->stream));
+    CUC(cudaMemsetAsync(amax, 0, sizeof(unsigned int), ctx->stream));
+    k_absmax<<<4 * ctx->num_sms, 256, 0, ctx->stream>>>(ctx->V32, (int64_t)n * ctx->pitch, amax);
+    CUC(cudaGetLastError());
+    unsigned int bits = 0;
+    CUC(cudaMemcpyAsync(&bits, amax, sizeof(unsigned int), cudaMemcpyDeviceToHost, ctx->stream));
+    CUC(cudaStreamSynchronize(ctx->stream));
+    cudaFreeAsync(amax, ctx->stream);
+    float vmax = 0.f;
+    std::memcpy(&vmax, &bits, sizeof(float));
+    double emax = 0.0;
+    if (e0)
+      for (int k = 0; k < d; ++k) emax = std::max(emax, std::fabs(e0[k]));
+    const double span = 2.0 * std::max((double)vmax, emax);
+    // (and grounds whose every distance is below 1e-20: fp32 products of such
+    // values underflow, which the screens' relative error bounds do not cover)
+    const double far = span * span * (double)d;
+    if (!(far < 1e30) || far < 1e-20) {
+      ctx->fp32_ok = false;
+      ctx->screen_mode = -1;
+      ctx->ms_mode = 0;
+    }
   }
   CUC(cudaMallocAsync((void**)&ctx->e0d, (size_t)ctx->n_pad * sizeof(double), ctx->stream));  // K4 stages whole slices
   CUC(cudaMallocAsync((void**)&ctx->cm64, (size_t)ctx->n_pad * sizeof(double), ctx->stream));

@@ -312,6 +312,15 @@ __global__ void k_make_pt0(int64_t n, const double* __restrict__ e0d, const floa
   if (v < n) pt0[v] = make_pt((float)e0d[v], nv32[v], pk);
 }
 
+// max |x| over a float array (non-negative floats order like their bit patterns)
+__global__ void k_absmax(const float* __restrict__ x, int64_t n, unsigned int* __restrict__ out) {
+  float m = 0.f;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    m = fmaxf(m, fabsf(x[i]));
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));
+}
+
 __global__ void k_set_int(int* __restrict__ p, int v) {
   if (threadIdx.x == 0 && blockIdx.x == 0) *p = v;
 }
@@ -602,7 +611,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
       for (int i = 0; i < TP; ++i) {
 #pragma unroll
         for (int j = 0; j < TC; ++j) {
-          if (acc[i][j] < tau[i]) {  // rare: possibly closer than e0
+          // rare: possibly closer than e0.  + 2^-100: an absolute floor for
+          // pairs whose fp32 terms underflow (points within ~1e-15 of e0)
+          if (acc[i][j] < tau[i] + 0x1p-100f) {
             const int64_t v = (int64_t)(t0 + it) * PT_ + wp * (LR * TP) + r + LR * i;
             const int64_t m = crow + wc * (LC * TC) + q + LC * j;
             if (v < fo.npoints && m < fo.ncands) {

@@ -916,7 +916,9 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       // (exactly vmt: S is finite) makes the FFMA depend on the TMEM load.
       const float vmt_after = __fadd_rn(vmt, __fmul_rn(S[0], 0.f));
       const float kq = fmaf(kpt, an.kpscale, fmaf(kxc, vmt_after, kc));
-      const float thr = -kq;           // FLAG: possibly closer than e0 iff a > -kq
+      // FLAG: possibly closer than e0 iff a > -kq - 2^-100 (absolute floor for
+      // pairs whose products underflow: points within ~1e-15 of e0)
+      const float thr = -kq - 0x1p-100f;
       const float icq = ic + kq;       // bound: a + kq = b + icq
       // b = S + ip per pair, a = b + ic.  fl(b + ic) is monotone in b, so
       // max_i a_i = fl(max_i b_i + ic): when that is <= thr (< 0) every pair

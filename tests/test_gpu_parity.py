@@ -706,3 +706,95 @@ def test_sharded_multiset_emulated_ranks_bit_identical(world):
     assert np.array_equal(np.concatenate(parts), full)
     want = oracle.eval_multiset(X.astype(np.float64), sets)
     assert max_scaled_diff(full, want) <= 1e-12
+
+
+# ------------------------------------------------------------ parity hardening (VERDICT r01 "What's weak" 2-4)
+
+@pytest.mark.parametrize("kind", ["huge", "mixed", "tiny", "huge_e0"])
+def test_extreme_dynamic_range_vs_oracle(kind):
+    """GroundMatrix accepts any finite value (core.py:73-77).  Distances beyond
+    the fp32 range make ebc_create drop every fp32 screen (exact fp64 refine
+    only); tiny values keep the screens, whose absolute tie margin covers the
+    underflow.  Either way: the oracle's selection and values."""
+    rng = np.random.default_rng(31)
+    X = rng.standard_normal((2500, 32))
+    e0 = None
+    if kind == "huge":
+        X *= 1e20
+    elif kind == "mixed":
+        X[:, :16] *= 1e-30
+        X[:, 16:] *= 1e30
+    elif kind == "tiny":
+        X *= 1e-30
+    else:
+        e0 = np.full(32, 3e18)
+    X32 = X.astype(np.float32)
+    f = fn(X32, eb.Precision.FP32, e0=e0)
+    k = 8
+    s = eb.greedy_maximize(f, eb.OptimizerBudget(k=k))
+    sel, vals, gains, ev = oracle.greedy(X32.astype(np.float64), k, e0=e0)
+    assert s.selected == sel
+    assert abs(s.value - vals[-1]) <= 1e-12 * max(abs(vals[-1]), 1e-300)
+    sets = [rng.choice(2500, size=int(rng.integers(0, 9)), replace=False).tolist() for _ in range(40)]
+    got = eb.evaluate_with_backend(f, eb.EvalMultiset(sets))
+    want = oracle.eval_multiset(X32.astype(np.float64), sets, e0=e0)
+    assert np.all(np.abs(got - want) <= 1e-12 * np.maximum(np.abs(want), 1e-300))
+
+
+def test_fp64_storage_greedy_20k_vs_oracle():
+    """FP64 grounds have no fp32 screen: step 0 refines every candidate, the
+    lazy steps after it only the stale ones."""
+    X = np.random.default_rng(41).standard_normal((20_000, 16))
+    k = 8
+    s = eb.greedy_maximize(fn(X, eb.Precision.FP64), eb.OptimizerBudget(k=k))
+    sel, vals, gains, ev = oracle.greedy(X, k)
+    assert s.selected == sel
+    np.testing.assert_allclose(np.cumsum(s.gains), vals, rtol=1e-12)
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_duplicates_straddling_shard_boundaries_c2_scale(world):
+    """C2-sized ground with exact copies of the first winner placed on both
+    sides of a shard boundary (and in the last shard): every emulated rank
+    count must pick the lowest copy first (optimize.py:83-85) and match the
+    single-device run bit for bit."""
+    import datasets
+    X = datasets.config_data("C2").copy()
+    n = X.shape[0]
+    top = _oracle_golden("C2")["selected"][0]
+    c0, _ = shard_range(n, 1, world)
+    dups = [c0 - 1, c0, n - 1]
+    for i in dups:
+        X[i] = X[top]
+    k = 6
+    single = eb.greedy_maximize(fn(X, eb.Precision.FP32), eb.OptimizerBudget(k=k))
+    assert single.selected[0] == min(dups + [top])
+    fs = [fn(X, eb.Precision.FP32) for _ in range(world)]
+    engines = [NativeShardEngine(f, *shard_range(n, r, world)) for r, f in enumerate(fs)]
+    sel = []
+    parts = [e.advance(-1, True) for e in engines]
+    for step in range(k):
+        cur = parts[0][2]
+        best, _ = pick(np.concatenate([p[0] for p in parts]), np.concatenate([p[1] for p in parts]), cur, n)
+        parts = [e.advance(best, step + 1 < k) for e in engines]
+        sel.append(best)
+    assert sel == single.selected
+    for e in engines:
+        e.close()
+
+
+@pytest.mark.parametrize("mode", ["1", "2"])
+def test_multiset_points_within_underflow_of_e0(monkeypatch, mode):
+    """A cluster of points ~1e-30 from e0 inside normal-scale data: the flag
+    screens' absolute floor must send their pairs to the exact fp64 terms
+    (values of sets made of those points are ~1e-60, compared relatively)."""
+    monkeypatch.setenv("EBC200_MULTISET_MODE", mode)
+    rng = np.random.default_rng(43)
+    X = rng.standard_normal((6000, 32)).astype(np.float32)
+    X[:64] = (rng.standard_normal((64, 32)) * 1e-30).astype(np.float32)
+    f = fn(X, eb.Precision.FP32)
+    sets = [rng.choice(64, size=int(rng.integers(1, 6)), replace=False).tolist() for _ in range(30)]
+    sets += [rng.choice(6000, size=5, replace=False).tolist() for _ in range(10)]
+    got = eb.evaluate_with_backend(f, eb.EvalMultiset(sets))
+    want = oracle.eval_multiset(X.astype(np.float64), sets)
+    assert np.all(np.abs(got - want) <= 1e-12 * np.abs(want)), (got[:5], want[:5])
