@@ -193,7 +193,7 @@ int ebc_screen_info(const ebc_ctx* ctx, int64_t* out4);
 /* Lazy Greedy statistics of the last run: [0] lazy steps enabled (EBC200_LAZY),
  * [1] lazy steps (every step after the first), [2] of those decided by the
  * exact refine of the stale candidates alone (no screen launch did work),
- * [3] sum of stale candidates over the lazy steps.  A lazy step re-examines
+ * [3] candidates re-examined by the lazy steps (first batches + stale lists).  A lazy step re-examines
  * only candidates whose last bound (screen upper bound or exact gain) can
  * still reach the reference tie window: gains only shrink as S grows
  * (submodularity), so the selection is unchanged. */

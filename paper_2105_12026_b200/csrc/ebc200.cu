@@ -160,6 +160,7 @@ struct ebc_ctx {
   // certified tile-pair pruning of the tensor screen
   bool tc_prune = true;
   float* tile_rad = nullptr;        // per 128-row candidate block: max |c - mu_anchor|
+  float* crad = nullptr;            // per candidate: |c - mu_anchor| rounded up (refine pruning)
   float* rho = nullptr;             // na x tc_ntl: min |v - mu_a| over the point tile
   float* cmx = nullptr;             // tc_ntl: max cm over the point tile (refreshed every screen)
   float* cmx0 = nullptr;            // tc_ntl: the same at the reset state (cm = d(., e0))
@@ -185,13 +186,27 @@ struct ebc_ctx {
   int64_t* wlist = nullptr;  // n
   double* wgain = nullptr;   // n
   double* ub = nullptr;      // n
-  // lazy Greedy (kernels.cuh k_lazy_mark): ubp[c - c0] bounds c's current gain
+  // lazy Greedy (kernels.cuh k_lazy_topk / k_lazy_mark2): ubp[c - c0] bounds c's current gain
   // (+inf after a reset); bflag: this step's re-screened 128-candidate blocks
   double* ubp = nullptr;           // n
   unsigned char* bflag = nullptr;  // ceil(n / 128) + 2
   bool lazy_on = true;             // EBC200_LAZY=0: every step screens every candidate
   int lazy_cap = 256;              // EBC200_LAZY_CAP: stale candidates decided by the exact refine alone
   bool ubp_seeded = false;         // enqueue-time: a full step has run since the reset
+  bool cmx_valid = false;          // enqueue-time: cmx computed since the reset (an upper bound of cm's tile maxima)
+  int64_t* slist = nullptr;        // n: this step's stale candidates (k_lazy_mark2)
+  int* scount = nullptr;
+  void* lazy_part = nullptr;       // 2 num_sms x TK 64-bit keys: k_lazy_topk's block lists
+  double* ub_next = nullptr;       // best stale bound outside the first batch
+  int lazy_batch = 4;              // EBC200_LAZY_BATCH (1..RW): candidates refined first in a lazy step
+  unsigned int* counter3 = nullptr;  // k_refine's finalize ticket
+  bool refine2 = true;             // EBC200_REFINE2=0: the lazy batch on the classic k_refine
+  DevBuf rterms;                   // RW x n_pad per-point terms of the two-phase refine
+  // CUDA-graph conditional nodes for the undecided part of a lazy step (captured
+  // runs only: an eager run gates those kernels on level[0] instead)
+  bool use_cond = true;            // EBC200_GRAPH_COND=0: plain gated kernels in graphs too
+  cudaStream_t side[2] = {nullptr, nullptr};  // capture streams of conditional bodies
+  bool screen_events_outside = false;  // the step's family events are recorded by the caller
   const unsigned char* step_bflag = nullptr;  // enqueue-time: bflag during a lazy step, else nullptr
   DevBuf part_g, part_e, part_r, sel_out, val_out, gain_out, ms_part, ms_off, ms_idx, ms_out;
   // sparse work-matrix path
@@ -393,11 +408,13 @@ int launch_screen(ebc_ctx* ctx, const ScreenPlan& p, const int* level_now, int l
 // The refine may skip certified-unreachable chunks when the tensor screen's
 // anchors exist and cmx was refreshed for this step (run_screen_window).
 bool refine_prune_on(const ebc_ctx* ctx) {
-  return ctx->tc_np && ctx->tc_prune && ctx->screen_mode == 3 && ctx->dtype != EBC_F64 && (RCH % ctx->tc_np) == 0;
+  return ctx->tc_np && ctx->tc_prune && ctx->screen_mode == 3 && ctx->dtype != EBC_F64 && (RCH % ctx->tc_np) == 0 &&
+         ctx->crad;
 }
 
 template <typename T, bool BIGD>
-int launch_refine(ebc_ctx* ctx, const T* V, int grid, size_t smem, int ng) {
+int launch_refine(ebc_ctx* ctx, const T* V, int grid, size_t smem, int ng, const int* skip_level,
+                  const RefineFinal& fin) {
   CU(cudaFuncSetAttribute(k_refine<T, BIGD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024));
   RefinePrune pr;
   if (refine_prune_on(ctx) && ctx->cmx_fresh) {
@@ -408,9 +425,11 @@ int launch_refine(ebc_ctx* ctx, const T* V, int grid, size_t smem, int ng) {
     pr.anchors = ctx->anchors;
     pr.apitch = ctx->pitch;
     pr.np = ctx->tc_np;
+    pr.crad = ctx->crad;
   }
   k_refine<T, BIGD><<<grid, RED_THREADS, smem, ctx->stream>>>(V, ctx->pitch, ctx->n, ctx->d, ctx->cm64, ctx->wcount,
-                                                             ctx->wlist, ctx->nchunks, ng, (double*)ctx->part_r.p, pr);
+                                                             ctx->wlist, ctx->nchunks, ng, (double*)ctx->part_r.p, pr,
+                                                             skip_level, fin);
   KCHECK();
   return EBC_OK;
 }
@@ -685,17 +704,19 @@ int run_screen_window(ebc_ctx* ctx, int eb, int fin_blocks) {
   if (rc) return rc;
   rc = ensure(ctx, ctx->part_e, (size_t)nsplit_max * ctx->n_pad * sizeof(float));
   if (rc) return rc;
-  if (ctx->timing) CU(record_step_event(ctx, ctx->ev[eb + 0]));
+  if (ctx->timing && !ctx->screen_events_outside) CU(record_step_event(ctx, ctx->ev[eb + 0]));
   // lower bounds are clamped at 0 (every gain is a sum of max(0, .) terms), so
   // key 0 (= +0.0) is a valid neutral element for the max
   if (!ctx->step_bflag) CU(cudaMemsetAsync(ctx->maxlb, 0, sizeof(long long), ctx->stream));
   const double nterms_ffma = (double)p.tps * p.tp * 8 * 2;
-  if (ctx->screen_mode == 0) {
-    rc = launch_screen<0>(ctx, p, nullptr, 0);
-    if (!rc) rc = run_finalize_window(ctx, p.nsplit, nterms_ffma, p.tp, fin_blocks, 1.0, nullptr, 0);
-  } else if (ctx->screen_mode == 1) {
-    rc = launch_screen<1>(ctx, p, nullptr, 0);
-    if (!rc) rc = run_finalize_window(ctx, p.nsplit, nterms_ffma, p.tp, fin_blocks, 2.0, nullptr, 0);
+  if (ctx->screen_mode == 0 || ctx->screen_mode == 1) {
+    // single-rung modes: level[] holds L_GRAM for the whole run (do_reset), so
+    // the gate only switches the pass off in lazy steps decided without it
+    if (ctx->screen_mode == 0) rc = launch_screen<0>(ctx, p, ctx->level, L_GRAM);
+    else rc = launch_screen<1>(ctx, p, ctx->level, L_GRAM);
+    if (!rc)
+      rc = run_finalize_window(ctx, p.nsplit, nterms_ffma, p.tp, fin_blocks, ctx->screen_mode == 0 ? 1.0 : 2.0,
+                               ctx->level, L_GRAM);
   } else {
     if (use_tc) {
       const bool agg = ctx->tc_agg && tp.list_cap && ctx->ladder_max >= L_TC;
@@ -753,93 +774,220 @@ int run_screen_window(ebc_ctx* ctx, int eb, int fin_blocks) {
     }
   }
   if (rc) return rc;
-  if (ctx->timing) CU(record_step_event(ctx, ctx->ev[eb + 1]));
-  return EBC_OK;
-}
-
-// Lazy prologue, step 1: maxlb = exact gain of the candidate with the largest
-// stale bound ubp (lowest index among equal bounds, selected ones skipped).
-int run_lazy_top(ebc_ctx* ctx) {
-  const int ag = (int)std::max<int64_t>(1, std::min<int64_t>(2 * ctx->num_sms, (ctx->c1 - ctx->c0 + 1023) / 1024));
-  k_argmax_ub<<<ag, 256, 0, ctx->stream>>>(ctx->c0, ctx->c1, ctx->ubp, ctx->topc, ctx->toppart, ctx->counter2,
-                                          nullptr, 0, ctx->selected);
-  KCHECK();
-  const size_t smem = (size_t)ctx->d * sizeof(double);
-  const unsigned g = (unsigned)((ctx->n + RED_THREADS - 1) / RED_THREADS);
-  if (ctx->dtype == EBC_F64) {
-    CU(cudaFuncSetAttribute(k_gain_top<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024));
-    k_gain_top<double><<<g, RED_THREADS, smem, ctx->stream>>>(ctx->V64, ctx->pitch, ctx->n, ctx->d, ctx->cm64,
-                                                             ctx->topc, ctx->toppart, ctx->counter2, ctx->maxlb,
-                                                             nullptr, 0);
-  } else {
-    CU(cudaFuncSetAttribute(k_gain_top<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024));
-    k_gain_top<float><<<g, RED_THREADS, smem, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->n, ctx->d, ctx->cm64,
-                                                            ctx->topc, ctx->toppart, ctx->counter2, ctx->maxlb,
-                                                            nullptr, 0);
-  }
-  KCHECK();
+  if (ctx->timing && !ctx->screen_events_outside) CU(record_step_event(ctx, ctx->ev[eb + 1]));
   return EBC_OK;
 }
 
 // One step's candidate screen + certified window + exact refine + pick.
 // commit: single-device mode (mark the winner, record it as step `step`).
+// Exact fp64 gains of the window (wcount / wlist) into part_r, then the pick
+// in the refine's last block (fin); skip_level: the kernel exits when it reads
+// -2 there (lazy step decided by the first batch).
+int enqueue_refine(ebc_ctx* ctx, int ng, const int* skip_level, const RefineFinal& fin) {
+  const int rgrid = 4 * ctx->num_sms;
+  const bool bigd = (size_t)RW * ctx->d * sizeof(double) > 160 * 1024;
+  const size_t rsmem = bigd ? 0 : (size_t)RW * ctx->d * sizeof(double);
+  if (ctx->dtype == EBC_F64)
+    return bigd ? launch_refine<double, true>(ctx, ctx->V64, rgrid, rsmem, ng, skip_level, fin)
+                : launch_refine<double, false>(ctx, ctx->V64, rgrid, rsmem, ng, skip_level, fin);
+  return bigd ? launch_refine<float, true>(ctx, ctx->V32, rgrid, rsmem, ng, skip_level, fin)
+              : launch_refine<float, false>(ctx, ctx->V32, rgrid, rsmem, ng, skip_level, fin);
+}
+
+// Two-phase refine of a window of at most RW candidates (the lazy first batch):
+// per-point terms, then the classic reduction replayed on them (kernels.cuh).
+int enqueue_refine_short(ebc_ctx* ctx, int ng, const RefineFinal& fin) {
+  RefinePrune pr;
+  if (refine_prune_on(ctx) && ctx->cmx_fresh) {
+    pr.rho = ctx->rho;
+    pr.kpstride = ctx->tc_ntl;
+    pr.cmx = ctx->cmx;
+    pr.tile_anchor = ctx->tile_anchor;
+    pr.anchors = ctx->anchors;
+    pr.apitch = ctx->pitch;
+    pr.np = ctx->tc_np;
+    pr.crad = ctx->crad;
+  }
+  const size_t smem = (size_t)RW * ctx->d * sizeof(double);
+  if (smem > 200 * 1024) return enqueue_refine(ctx, ng, nullptr, fin);
+  int rc = ensure(ctx, ctx->rterms, (size_t)RW * ctx->n_pad * sizeof(double));
+  if (rc) return rc;
+  const unsigned grid = (unsigned)((ctx->n + RED_THREADS - 1) / RED_THREADS);
+  if (ctx->dtype == EBC_F64) {
+    CU(cudaFuncSetAttribute(k_refine_terms<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_refine_terms<double><<<grid, RED_THREADS, smem, ctx->stream>>>(ctx->V64, ctx->pitch, ctx->n, ctx->d, ctx->cm64,
+                                                                    ctx->wcount, ctx->wlist, (double*)ctx->rterms.p,
+                                                                    ctx->n_pad, pr);
+  } else {
+    CU(cudaFuncSetAttribute(k_refine_terms<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_refine_terms<float><<<grid, RED_THREADS, smem, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->n, ctx->d, ctx->cm64,
+                                                                   ctx->wcount, ctx->wlist, (double*)ctx->rterms.p,
+                                                                   ctx->n_pad, pr);
+  }
+  KCHECK();
+  k_refine_sums<<<ng, RED_THREADS, 0, ctx->stream>>>((const double*)ctx->rterms.p, ctx->n_pad, ctx->n, ctx->wcount,
+                                                     ctx->wlist, ctx->nchunks, ng, (double*)ctx->part_r.p, fin);
+  KCHECK();
+  return EBC_OK;
+}
+
+// Conditional graph nodes (captured runs): a handle of the graph ctx->stream is
+// capturing into (0 outside capture), and a scope that inserts an IF node with
+// it and captures the body on a side stream until the scope closes.
+cudaGraphConditionalHandle cond_handle(ebc_ctx* ctx) {
+  if (!ctx->capturing || !ctx->use_cond) return 0;
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  cudaGraph_t g = nullptr;
+  if (cudaStreamGetCaptureInfo(ctx->stream, &st, nullptr, &g, nullptr, nullptr) != cudaSuccess ||
+      st != cudaStreamCaptureStatusActive)
+    return 0;
+  cudaGraphConditionalHandle h = 0;
+  if (cudaGraphConditionalHandleCreate(&h, g, 0, cudaGraphCondAssignDefault) != cudaSuccess) return 0;
+  return h;
+}
+
+struct CondScope {
+  ebc_ctx* ctx = nullptr;
+  cudaStream_t saved = nullptr;
+  ~CondScope() { close(); }
+  cudaError_t open(ebc_ctx* c, cudaGraphConditionalHandle h, int depth) {
+    if (!h) return cudaSuccess;
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    cudaGraph_t g = nullptr;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    cudaError_t e = cudaStreamGetCaptureInfo(c->stream, &st, nullptr, &g, &deps, &nd);
+    if (e != cudaSuccess) return e;
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeIf;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cn = nullptr;
+    if ((e = cudaGraphAddNode(&cn, g, deps, nd, &cp)) != cudaSuccess) return e;
+    if ((e = cudaStreamUpdateCaptureDependencies(c->stream, &cn, 1, cudaStreamSetCaptureDependencies)) != cudaSuccess)
+      return e;
+    if ((e = cudaStreamBeginCaptureToGraph(c->side[depth], cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeThreadLocal)) != cudaSuccess)
+      return e;
+    ctx = c;
+    saved = c->stream;
+    c->stream = c->side[depth];
+    return cudaSuccess;
+  }
+  cudaError_t close() {
+    if (!ctx) return cudaSuccess;
+    cudaGraph_t body = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(ctx->stream, &body);
+    ctx->stream = saved;
+    ctx = nullptr;
+    return e;
+  }
+};
+
+RefineFinal step_final(ebc_ctx* ctx, int commit, int step, int64_t* sel_dev) {
+  RefineFinal f;
+  f.counter = ctx->counter3;
+  f.wgain = ctx->wgain;
+  f.inv_n = 1.0 / (double)ctx->n;
+  f.cur = ctx->cur;
+  f.best = ctx->best;
+  f.commit = commit;
+  f.step = step;
+  f.selected = ctx->selected;
+  f.sel_out = sel_dev;
+  f.stats = ctx->stats;
+  f.level = ctx->level;
+  f.ubp = ctx->lazy_on ? ctx->ubp : nullptr;
+  f.c0 = ctx->c0;
+  return f;
+}
+
+// One step's selection: screen + certified window + exact refine + pick, or a
+// lazy step (DESIGN.md §4 "Lazy steps"): the lazy_batch best stale bounds are
+// refined first and decide the step when they hold the whole stale set;
+// otherwise (a conditional graph node in captured runs, kernels gated on
+// level[0] in eager runs) the stale set is listed and either refined directly
+// or its blocks re-screened.  commit: single-device mode (mark the winner,
+// record it as step `step`).
 int run_step_select(ebc_ctx* ctx, int step, int commit, int64_t* sel_dev) {
   const int eb = 4 * step;  // event slot of this step
   const int64_t ncand = ctx->c1 - ctx->c0;
-  CU(cudaMemsetAsync(ctx->wcount, 0, sizeof(int), ctx->stream));
   const int fin_blocks = (int)((ncand + 255) / 256);
   ctx->cmx_fresh = false;
   ScreenPlan sp;
   const bool has_screen = ctx->dtype != EBC_F64 && plan_screen(ctx, sp) == EBC_OK;
   const bool lazy = ctx->lazy_on && ctx->ubp_seeded;
-  int rc = EBC_OK;
-  if (lazy) {
-    // lazy prologue (kernels.cuh k_lazy_mark): lb = exact gain of the best
-    // stale bound, list the stale candidates, flag their blocks, pick the mode
-    CU(cudaMemsetAsync(ctx->maxlb, 0, sizeof(long long), ctx->stream));
-    CU(cudaMemsetAsync(ctx->bflag, 0, (size_t)((ncand + tc::M - 1) / tc::M + 2), ctx->stream));
-    rc = run_lazy_top(ctx);
-    if (rc) return rc;
-    const double margin = (double)ctx->n * 1e-12 * std::max(1.0, std::fabs(ctx->baseline)) * 1.01;
-    k_lazy_mark<<<fin_blocks, 256, 0, ctx->stream>>>(ctx->c0, ctx->c1, ctx->ubp, ctx->selected, ctx->maxlb, margin,
-                                                     ctx->wcount, ctx->wlist, ctx->bflag);
-    KCHECK();
-    k_lazy_plan<<<1, 32, 0, ctx->stream>>>(ctx->wcount, has_screen ? ctx->lazy_cap : INT_MAX, ctx->level, ctx->stats);
-    KCHECK();
-    ctx->step_bflag = ctx->bflag;
-  }
-  if (has_screen) rc = run_screen_window(ctx, eb, fin_blocks);
-  else if (!lazy) rc = run_window_all(ctx, eb, fin_blocks);
-  else if (ctx->timing) {
-    CU(record_step_event(ctx, ctx->ev[eb + 0]));
-    CU(record_step_event(ctx, ctx->ev[eb + 1]));
-  }
-  ctx->step_bflag = nullptr;
-  if (ctx->lazy_on) ctx->ubp_seeded = true;
-  if (rc) return rc;
-  // exact fp64 gains of the window
+  if (!lazy) CU(cudaMemsetAsync(ctx->wcount, 0, sizeof(int), ctx->stream));  // a lazy step's k_lazy_topk writes it
   // point-chunk groups per window candidate: as many as 256 MB of partials allow
   // (a short window is latency-bound: more groups = more blocks in flight)
   const int64_t ng_mem = (int64_t)(256ull << 20) / (8 * (ctx->n + RW));
   const int ng = (int)std::max<int64_t>(1, std::min<int64_t>(ctx->nchunks, std::max<int64_t>(32, ng_mem)));
-  rc = ensure(ctx, ctx->part_r, (size_t)(ctx->n + RW) * ng * sizeof(double));
+  int rc = ensure(ctx, ctx->part_r, (size_t)(ctx->n + RW) * ng * sizeof(double));
   if (rc) return rc;
-  const int rgrid = 4 * ctx->num_sms;
-  const bool bigd = (size_t)RW * ctx->d * sizeof(double) > 160 * 1024;
-  const size_t rsmem = bigd ? 0 : (size_t)RW * ctx->d * sizeof(double);
-  if (ctx->dtype == EBC_F64)
-    rc = bigd ? launch_refine<double, true>(ctx, ctx->V64, rgrid, rsmem, ng)
-              : launch_refine<double, false>(ctx, ctx->V64, rgrid, rsmem, ng);
-  else
-    rc = bigd ? launch_refine<float, true>(ctx, ctx->V32, rgrid, rsmem, ng)
-              : launch_refine<float, false>(ctx, ctx->V32, rgrid, rsmem, ng);
-  if (rc) return rc;
-  k_pick<<<1, 1024, 0, ctx->stream>>>(ctx->wcount, ctx->wlist, ng, (double*)ctx->part_r.p,
-                                      1.0 / (double)ctx->n, ctx->cur, ctx->wgain, ctx->best, commit, step,
-                                      ctx->selected, sel_dev, ctx->stats, ctx->level,
-                                      ctx->lazy_on ? ctx->ubp : nullptr, ctx->c0);
+  RefineFinal fin = step_final(ctx, commit, step, sel_dev);
+  if (!lazy) {
+    rc = has_screen ? run_screen_window(ctx, eb, fin_blocks) : run_window_all(ctx, eb, fin_blocks);
+    if (rc) return rc;
+    if (ctx->lazy_on) ctx->ubp_seeded = true;
+    if (ctx->cmx_fresh) ctx->cmx_valid = true;
+    rc = enqueue_refine(ctx, ng, nullptr, fin);
+    if (rc) return rc;
+    if (ctx->timing) CU(record_step_event(ctx, ctx->ev[eb + 2]));
+    return EBC_OK;
+  }
+  // lazy step: the first batch (k_lazy_topk) and its refine, which decides
+  // (it also sets maxlb = lb and zeroes scount; no memset nodes on this path)
+  const int ag = (int)std::max<int64_t>(1, std::min<int64_t>(2 * ctx->num_sms, (ncand + 1023) / 1024));
+  k_lazy_topk<<<ag, 256, 0, ctx->stream>>>(ctx->c0, ctx->c1, ctx->ubp, ctx->selected, ctx->lazy_batch,
+                                          (unsigned long long*)ctx->lazy_part, ctx->counter2, ctx->wcount, ctx->wlist,
+                                          ctx->ub_next);
   KCHECK();
-  if (ctx->timing) CU(record_step_event(ctx, ctx->ev[eb + 2]));
+  const cudaGraphConditionalHandle hrest = cond_handle(ctx);
+  const double margin = (double)ctx->n * 1e-12 * std::max(1.0, std::fabs(ctx->baseline)) * 1.01;
+  RefineFinal fb = fin;
+  fb.batch = 1;
+  fb.ub_next = ctx->ub_next;
+  fb.margin = margin;
+  fb.maxlb = ctx->maxlb;
+  fb.scount = ctx->scount;
+  fb.hrest = hrest;
+  ctx->cmx_fresh = ctx->cmx_valid;  // an earlier step's tile maxima still bound cm (it only decreases)
+  rc = ctx->refine2 ? enqueue_refine_short(ctx, ng, fb) : enqueue_refine(ctx, ng, nullptr, fb);
+  if (rc) return rc;
+  ctx->cmx_fresh = false;
+  {
+    // undecided step (level[0] == -3): stale set -> mode -> screen / refine
+    CondScope ca;
+    CU(ca.open(ctx, hrest, 0));
+    CU(cudaMemsetAsync(ctx->bflag, 0, (size_t)((ncand + tc::M - 1) / tc::M + 2), ctx->stream));
+    k_lazy_mark2<<<fin_blocks, 256, 0, ctx->stream>>>(ctx->c0, ctx->c1, ctx->ubp, ctx->selected, ctx->maxlb,
+                                                      margin, ctx->scount, ctx->slist, ctx->bflag, ctx->level);
+    KCHECK();
+    const cudaGraphConditionalHandle hs = has_screen ? cond_handle(ctx) : 0;
+    k_lazy_plan2<<<1, 256, 0, ctx->stream>>>(ctx->scount, ctx->slist, has_screen ? ctx->lazy_cap : INT_MAX,
+                                             ctx->wcount, ctx->wlist, ctx->level, ctx->stats, hs);
+    KCHECK();
+    if (has_screen) {
+      CondScope cb;
+      CU(cb.open(ctx, hs, 1));
+      ctx->step_bflag = ctx->bflag;
+      ctx->screen_events_outside = true;
+      rc = run_screen_window(ctx, eb, fin_blocks);
+      ctx->step_bflag = nullptr;
+      ctx->screen_events_outside = false;
+      if (rc) return rc;
+      CU(cb.close());
+    }
+    // the window's refine and pick (mode -1: the stale list; re-screened: the window)
+    ctx->cmx_fresh = ctx->cmx_valid;
+    rc = enqueue_refine(ctx, ng, ctx->level, fin);
+    if (rc) return rc;
+    CU(ca.close());
+  }
+  // lazy steps record only eb + 1 (here) and eb + 3 (after the update): greedy_run
+  // reads [prev eb + 3, eb + 1] as the step's selection time
+  if (ctx->timing) CU(record_step_event(ctx, ctx->ev[eb + 1]));
   return EBC_OK;
 }
 
@@ -997,6 +1145,7 @@ int do_reset(ebc_ctx* ctx) {
     KCHECK();
   }
   ctx->ubp_seeded = false;
+  ctx->cmx_valid = false;
   CU(cudaMemsetAsync(ctx->cur, 0, sizeof(double), ctx->stream));
   ctx->steps_done = 0;
   return EBC_OK;
@@ -1005,11 +1154,12 @@ int do_reset(ebc_ctx* ctx) {
 void free_ctx(ebc_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
-  void* ptrs[] = {c->V32, c->V64, c->e0d, c->cm64, c->pt, c->nv32, c->level, c->stats, c->Vhi, c->Vlo, c->Vf, c->tile_anchor0, c->rhomax, c->cmn, c->vsum, c->vsn, c->ipsum, c->rhomin, c->agg_any, c->pttc, c->kpmax, c->anchors, c->nva, c->tile_anchor, c->tc_vmax, c->fps_keys, c->ipa0, c->tile_rad, c->rho, c->cmx, c->cmx0, c->selected, c->chunkpart, c->counter, c->counter2, c->topc, c->toppart, c->terms, c->cur, c->best, c->uf_ctr,
-                  c->maxlb, c->wcount, c->wlist, c->wgain, c->ub, c->ubp, c->bflag};
+  void* ptrs[] = {c->V32, c->V64, c->e0d, c->cm64, c->pt, c->nv32, c->level, c->stats, c->Vhi, c->Vlo, c->Vf, c->tile_anchor0, c->rhomax, c->cmn, c->vsum, c->vsn, c->ipsum, c->rhomin, c->agg_any, c->pttc, c->kpmax, c->anchors, c->nva, c->tile_anchor, c->tc_vmax, c->fps_keys, c->ipa0, c->tile_rad, c->crad, c->rho, c->cmx, c->cmx0, c->selected, c->chunkpart, c->counter, c->counter2, c->topc, c->toppart, c->terms, c->cur, c->best, c->uf_ctr,
+                  c->maxlb, c->wcount, c->wlist, c->wgain, c->ub, c->ubp, c->bflag, c->slist, c->scount,
+                  c->lazy_part, c->ub_next, c->counter3};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, c->stream);
-  DevBuf* bufs[] = {&c->tie_rec, &c->tie_all, &c->sel_hash, &c->ms_tanchor, &c->ms_trad, &c->part_g, &c->part_e, &c->part_a, &c->part_r, &c->sel_out, &c->val_out, &c->gain_out, &c->ms_part,
+  DevBuf* bufs[] = {&c->tie_rec, &c->tie_all, &c->sel_hash, &c->ms_tanchor, &c->ms_trad, &c->part_g, &c->part_e, &c->part_a, &c->part_r, &c->rterms, &c->sel_out, &c->val_out, &c->gain_out, &c->ms_part,
                     &c->ms_off, &c->ms_idx, &c->ms_out, &c->ms_mbuf, &c->ms_setof, &c->ms_pairs, &c->ms_keys,
                     &c->ms_vals, &c->ms_keys2, &c->ms_vals2, &c->ms_ukeys, &c->ms_uvals, &c->ms_cub};
   void* more[] = {c->pt0, c->ms_count, c->ms_nruns};
@@ -1024,6 +1174,8 @@ void free_ctx(ebc_ctx* c) {
     cudaStreamSynchronize(c->stream);
     cudaStreamDestroy(c->stream);
   }
+  for (cudaStream_t ss : c->side)
+    if (ss) cudaStreamDestroy(ss);
   delete c;
 }
 
@@ -1231,6 +1383,8 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
     }
   }
   CUC(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+  CUC(cudaStreamCreateWithFlags(&ctx->side[0], cudaStreamNonBlocking));
+  CUC(cudaStreamCreateWithFlags(&ctx->side[1], cudaStreamNonBlocking));
   // EBC200_PROFILE_CREATE=1: host wall time of the creation phases on stderr
   const bool prof = getenv("EBC200_PROFILE_CREATE") != nullptr;
   auto tnow = []() { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
@@ -1302,7 +1456,7 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
   CUC(cudaMemsetAsync(ctx->pt, 0, (size_t)ctx->n_pad * sizeof(float4), ctx->stream));
   CUC(cudaMallocAsync((void**)&ctx->nv32, (size_t)ctx->n_pad * sizeof(float), ctx->stream));
   CUC(cudaMemsetAsync(ctx->nv32, 0, (size_t)ctx->n_pad * sizeof(float), ctx->stream));
-  // [4]: tensor-screen tile pairs executed; [5..7] lazy steps (k_lazy_plan)
+  // [4]: tensor-screen tile pairs executed; [5..7] lazy steps (k_lazy_plan2)
   CUC(cudaMallocAsync((void**)&ctx->stats, 8 * sizeof(long long), ctx->stream));
   CUC(cudaMemsetAsync(ctx->stats, 0, 8 * sizeof(long long), ctx->stream));
   CUC(cudaMallocAsync((void**)&ctx->level, 2 * sizeof(int), ctx->stream));
@@ -1428,6 +1582,20 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
   CUC(cudaMallocAsync((void**)&ctx->ub, (size_t)n * sizeof(double), ctx->stream));
   CUC(cudaMallocAsync((void**)&ctx->ubp, (size_t)n * sizeof(double), ctx->stream));
   CUC(cudaMallocAsync((void**)&ctx->bflag, (size_t)((n + tc::M - 1) / tc::M + 2), ctx->stream));
+  CUC(cudaMallocAsync((void**)&ctx->slist, (size_t)n * sizeof(int64_t), ctx->stream));
+  CUC(cudaMallocAsync((void**)&ctx->scount, sizeof(int), ctx->stream));
+  CUC(cudaMallocAsync(&ctx->lazy_part, (size_t)2 * ctx->num_sms * TK * sizeof(unsigned long long), ctx->stream));
+  CUC(cudaMallocAsync((void**)&ctx->ub_next, sizeof(double), ctx->stream));
+  CUC(cudaMallocAsync((void**)&ctx->counter3, sizeof(unsigned int), ctx->stream));
+  CUC(cudaMemsetAsync(ctx->counter3, 0, sizeof(unsigned int), ctx->stream));
+  {
+    const char* lb = getenv("EBC200_LAZY_BATCH");
+    if (lb && lb[0]) ctx->lazy_batch = std::max(1, std::min(RW, atoi(lb)));
+    const char* r2 = getenv("EBC200_REFINE2");
+    if (r2 && r2[0] == '0') ctx->refine2 = false;
+    const char* gc = getenv("EBC200_GRAPH_COND");
+    if (gc && gc[0] == '0') ctx->use_cond = false;
+  }
   {
     const char* lz = getenv("EBC200_LAZY");
     ctx->lazy_on = !(lz && lz[0] == '0');
@@ -1471,6 +1639,11 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
       k_tile_anchor<<<(unsigned)((n + 127) / 128), 128, 0, ctx->stream>>>(ctx->V32, ctx->pitch, n, d, ctx->anchors,
                                                                           ctx->pitch, ctx->tc_na, ctx->tile_anchor,
                                                                           ctx->tile_rad);
+      CUC(cudaGetLastError());
+      CUC(cudaMallocAsync((void**)&ctx->crad, (size_t)n * sizeof(float), ctx->stream));
+      k_cand_rad<float><<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(ctx->V32, ctx->pitch, n, d,
+                                                                             ctx->tile_anchor, ctx->anchors,
+                                                                             ctx->pitch, ctx->crad);
       CUC(cudaGetLastError());
       k_seed_ipa<<<(unsigned)((ctx->n_pad + 255) / 256), 256, 0, ctx->stream>>>(ctx->cm64, n, ctx->n_pad,
                                                                                  tc_seeds(ctx));
@@ -1795,6 +1968,14 @@ int greedy_run(ebc_ctx* ctx, int32_t k, bool sharded, int64_t* out_sel, double* 
   if (ctx->timing) {
     for (int st = 0; st < k; ++st) {
       float a = 0, b = 0, c = 0;
+      if (ctx->lazy_on && st > 0) {
+        // lazy step: selection (batch, and the screen when re-run) + update
+        CU(cudaEventElapsedTime(&a, ctx->ev[4 * (st - 1) + 3], ctx->ev[4 * st + 1]));
+        CU(cudaEventElapsedTime(&c, ctx->ev[4 * st + 1], ctx->ev[4 * st + 3]));
+        acc_ms[0] += a;
+        acc_ms[2] += c;
+        continue;
+      }
       CU(cudaEventElapsedTime(&a, ctx->ev[4 * st + 0], ctx->ev[4 * st + 1]));
       CU(cudaEventElapsedTime(&b, ctx->ev[4 * st + 1], ctx->ev[4 * st + 2]));
       CU(cudaEventElapsedTime(&c, ctx->ev[4 * st + 2], ctx->ev[4 * st + 3]));

@@ -698,7 +698,7 @@ __global__ void k_finalize(int64_t c0, int64_t c1, int nsplit, const double* __r
   const int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   long long key = dkey(-INFINITY);
   // lazy step (bflag set): only the flagged 128-candidate blocks were screened;
-  // the others hold stale partials and are out of the window (k_lazy_mark)
+  // the others hold stale partials and are out of the window (k_lazy_mark2)
   if (c < c1 && bflag && !bflag[(c - c0) >> 7]) {
     ub[c - c0] = -INFINITY;
   } else if (c < c1) {
@@ -937,60 +937,177 @@ __global__ void __launch_bounds__(RED_THREADS) k_sum_chunks(const double* __rest
 // cm, fixed-order rounding is monotone).  ubp[c] keeps the tightest bound seen
 // for c: the screen's certified upper bound (k_finalize) or its exact fp64
 // gain (k_pick).  A later step needs to look only at the STALE candidates
-//   ubp[c] >= lb - margin - 1e-9 |lb|,   lb = exact gain of argmax_c ubp[c],
+//   ubp[c] >= lb - margin - 1e-9 |lb|,   lb = a current exact gain (below),
 // every other candidate is out of the reference's tie window for certain
-// (the same margin as k_window plus a rounding allowance between k_gain_top's
-// and k_refine's summation orders).  k_lazy_mark lists them (the window if
-// they are few) and flags their 128-candidate blocks (what the screen re-runs
-// if they are many).
+// (the same margin as k_window plus a rounding allowance for the different
+// summation orders of the exact sums).  The lower bound comes from refining
+// the RW best stale bounds first (k_lazy_topk); k_lazy_mark2 lists the stale
+// set and flags its 128-candidate blocks; k_lazy_plan2 picks the mode.
 
 __global__ void k_fill_f64(double* __restrict__ p, int64_t n, double v) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     p[i] = v;
 }
 
-__global__ void __launch_bounds__(256) k_lazy_mark(int64_t c0, int64_t c1, const double* __restrict__ ubp,
-                                                   const unsigned char* __restrict__ selected,
-                                                   const long long* __restrict__ maxlb, double margin,
-                                                   int* __restrict__ wcount, int64_t* __restrict__ wlist,
-                                                   unsigned char* __restrict__ bflag) {
+constexpr int RW = 8;  // refine window group (k_refine): candidates sharing each V row read
+
+// Lazy fast path: the LB (<= RW) candidates with the largest stale bounds
+// (ubp descending, index ascending; selected ones skipped) are refined first.
+// Their best exact gain is the step's lower bound lb; the stale set is a
+// prefix of this order, so if the best bound OUTSIDE the batch (ub_next) is
+// already below the stale threshold, the batch holds the whole stale set and
+// the step is decided by that one refine (C2: almost every step after the
+// first).  Grid-wide top-(LB+1): per-thread sorted lists, warp merges by
+// shuffles, the last block merges the blocks' lists ((value, index) is a
+// total order, so any merge order gives the same result).
+constexpr int LB_MAX = RW;
+constexpr int TK = LB_MAX + 1;  // entries kept per list: the batch + the best outside it
+// (bound, index) as one 64-bit key: the bound rounded UP to fp32 in the high word
+// (non-negative floats order like their bits), ~index in the low word (lower
+// index wins ties), 0 = empty.  Rounding up keeps the batch test conservative:
+// every candidate outside the batch has ubp <= its key's bound <= ub_next.
+__device__ __forceinline__ unsigned long long top_key(double ub, int64_t c) {
+  const float f = __double2float_ru(fmax(ub, 0.0));
+  return ((unsigned long long)__float_as_uint(f) << 32) | (unsigned long long)(0xFFFFFFFFu - (unsigned)c);
+}
+__device__ __forceinline__ void top_insert(unsigned long long (&l)[TK], unsigned long long k) {
+  if (k <= l[TK - 1]) return;
+#pragma unroll
+  for (int p = TK - 1; p > 0; --p) l[p] = k > l[p - 1] ? l[p - 1] : (k > l[p] ? k : l[p]);
+  if (k > l[0]) l[0] = k;
+}
+// TK rounds of a warp max over the lanes' list heads (keys are unique); the
+// winner lane pops.  Lane 0 writes the warp's sorted top-TK to out.
+__device__ __forceinline__ void warp_topk(unsigned long long (&l)[TK], unsigned long long* out) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll 1
+  for (int r = 0; r < TK; ++r) {
+    unsigned long long b = l[0];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long x = __shfl_xor_sync(0xffffffffu, b, o);
+      b = x > b ? x : b;
+    }
+    if (lane == 0) out[r] = b;
+    if (b != 0ull && l[0] == b) {
+#pragma unroll
+      for (int p = 0; p < TK - 1; ++p) l[p] = l[p + 1];
+      l[TK - 1] = 0ull;
+    }
+  }
+}
+
+// Writes the batch to wlist[0..m) (m = min(lb, unselected candidates)),
+// *wcount = m and *ub_next = the (rounded-up) best bound outside it (-inf if none).
+__global__ void __launch_bounds__(256) k_lazy_topk(int64_t c0, int64_t c1, const double* __restrict__ ubp,
+                                                   const unsigned char* __restrict__ selected, int lb,
+                                                   unsigned long long* __restrict__ part,
+                                                   unsigned int* __restrict__ counter, int* __restrict__ wcount,
+                                                   int64_t* __restrict__ wlist, double* __restrict__ ub_next) {
+  __shared__ unsigned long long wt[9 * TK];  // 8 warp lists + the merged one
+  __shared__ bool last;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned long long l[TK];
+#pragma unroll
+  for (int j = 0; j < TK; ++j) l[j] = 0ull;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < c1; c += stride)
+    if (!selected[c]) top_insert(l, top_key(ubp[c - c0], c - c0));
+  warp_topk(l, wt + warp * TK);
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int j = 0; j < TK; ++j) l[j] = 0ull;
+    for (int q = lane; q < 8 * TK; q += 32) top_insert(l, wt[q]);
+    warp_topk(l, part + (int64_t)blockIdx.x * TK);
+    if (lane == 0) {
+      __threadfence();
+      last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    }
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+#pragma unroll
+  for (int j = 0; j < TK; ++j) l[j] = 0ull;
+  const int total = (int)gridDim.x * TK;
+  constexpr int PT = 12;  // independent loads per thread (2 x 148 blocks x TK < 12 x 256)
+  unsigned long long x[PT];
+#pragma unroll
+  for (int j = 0; j < PT; ++j) {
+    const int q = threadIdx.x + j * blockDim.x;
+    x[j] = q < total ? __ldcg(part + q) : 0ull;
+  }
+#pragma unroll
+  for (int j = 0; j < PT; ++j) top_insert(l, x[j]);
+  for (int q = threadIdx.x + PT * blockDim.x; q < total; q += blockDim.x) top_insert(l, __ldcg(part + q));
+  warp_topk(l, wt + warp * TK);
+  __syncthreads();
+  if (warp != 0) return;
+#pragma unroll
+  for (int j = 0; j < TK; ++j) l[j] = 0ull;
+  for (int q = lane; q < 8 * TK; q += 32) top_insert(l, wt[q]);
+  warp_topk(l, wt + 8 * TK);
+  __syncwarp();
+  if (lane == 0) {
+    const unsigned long long* fin = wt + 8 * TK;
+    int m = 0;
+    for (int j = 0; j < lb; ++j)
+      if (fin[j]) wlist[m++] = c0 + (int64_t)(0xFFFFFFFFu - (unsigned)(fin[j] & 0xFFFFFFFFull));
+    *wcount = m;
+    *ub_next = fin[lb] ? (double)__uint_as_float((unsigned)(fin[lb] >> 32)) : -INFINITY;
+    *counter = 0u;
+  }
+}
+
+// Undecided lazy step (level[0] == -3): list the stale candidates
+// ubp[c] >= lb - margin - 1e-9 |lb| (lb = *maxlb, the batch's best exact gain)
+// in slist (count *scount) and flag their 128-candidate blocks.
+__global__ void __launch_bounds__(256) k_lazy_mark2(int64_t c0, int64_t c1, const double* __restrict__ ubp,
+                                                    const unsigned char* __restrict__ selected,
+                                                    const long long* __restrict__ maxlb, double margin,
+                                                    int* __restrict__ scount, int64_t* __restrict__ slist,
+                                                    unsigned char* __restrict__ bflag, const int* __restrict__ level) {
+  if (*level != -3) return;
+  const double lb = dkey_inv(*maxlb);
   const int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   bool stale = false;
-  if (c < c1 && !selected[c]) {
-    const double lb = dkey_inv(*maxlb);
-    stale = ubp[c - c0] >= lb - margin - 1e-9 * fabs(lb);
-  }
-  // warp-aggregated append (append order is irrelevant: k_pick decides by exact
-  // value and lowest index)
+  if (c < c1 && !selected[c]) stale = ubp[c - c0] >= lb - margin - 1e-9 * fabs(lb);
   const unsigned bal = __ballot_sync(0xffffffffu, stale);
   if (!bal) return;
   int base = 0;
-  if (lane == 0) base = atomicAdd(wcount, __popc(bal));
+  if (lane == 0) base = atomicAdd(scount, __popc(bal));
   base = __shfl_sync(0xffffffffu, base, 0);
   if (stale) {
-    wlist[base + __popc(bal & ((1u << lane) - 1u))] = c;
+    slist[base + __popc(bal & ((1u << lane) - 1u))] = c;
     bflag[(c - c0) >> 7] = 1;
   }
 }
 
-// Mode of a lazy step.  Few stale candidates (<= cap, or no screen exists for
-// this ground): they ARE the window -- the screen kernels see level -1 and
-// exit, the exact refine decides.  Otherwise the screen re-runs over the
-// flagged blocks only (level[0] = the run's rung) and builds the window itself.
-// stats: [5] steps decided without a screen, [6] stale candidates, [7] lazy steps.
-__global__ void k_lazy_plan(int* __restrict__ wcount, int cap, int* __restrict__ level, long long* __restrict__ stats) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    const int cnt = *wcount;
+// Mode of an undecided lazy step (level[0] == -3), written to level[0]:
+//   -1  few stale candidates (<= cap, or no screen): they are the window of
+//       the second refine (copied into wlist);
+//   rung  many: the flagged blocks are re-screened and the screen builds the
+//       window (hs: the screen's conditional graph node, when captured).
+// stats: [5] lazy steps decided without a screen, [6] candidates re-examined.
+__global__ void __launch_bounds__(256) k_lazy_plan2(const int* __restrict__ scount,
+                                                    const int64_t* __restrict__ slist, int cap,
+                                                    int* __restrict__ wcount, int64_t* __restrict__ wlist,
+                                                    int* __restrict__ level, long long* __restrict__ stats,
+                                                    cudaGraphConditionalHandle hs) {
+  if (level[0] != -3) return;
+  const int cnt = *scount;
+  const bool few = cnt <= cap;
+  if (few)
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) wlist[i] = slist[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
     stats[6] += cnt;
-    stats[7] += 1;
-    if (cnt <= cap) {
-      level[0] = -1;
-      stats[5] += 1;
-    } else {
-      level[0] = level[1];
-      *wcount = 0;
-    }
+    stats[5] += few ? 1 : 0;  // decided without a screen
+    level[0] = few ? -1 : level[1];
+    *wcount = few ? cnt : 0;
+    if (hs) cudaGraphSetConditional(hs, few ? 0u : 1u);
   }
 }
 
@@ -1002,7 +1119,6 @@ __global__ void k_lazy_plan(int* __restrict__ wcount, int cap, int* __restrict__
 // sequential per lane, then a butterfly); chunks are added left to right into
 // part_r[w*ng + grp].  A candidate's value never depends on its RW neighbours,
 // its slot in the window, or the number of ranks.
-constexpr int RW = 8;
 
 // Certified tile-pair pruning: every point of tile t is at least rho - R from
 // every candidate of the block (triangle inequality through the anchor), so
@@ -1026,14 +1142,140 @@ struct RefinePrune {
   const float* anchors = nullptr;
   int apitch = 0;
   int np = 128;                // points per tile
+  const float* crad = nullptr; // per candidate |c - mu_anchor| rounded up (k_cand_rad, at create)
 };
+
+// crad[c] = |c - mu_a|, a = the anchor of c's 128-row block, in fp64 and rounded
+// up (the refine's pruning radius; computed once at create instead of per unit).
+template <typename T>
+__global__ void k_cand_rad(const T* __restrict__ V, int pitch, int64_t n, int d, const int* __restrict__ tile_anchor,
+                           const float* __restrict__ anchors, int apitch, float* __restrict__ crad) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  const float* mu = anchors + (int64_t)tile_anchor[c >> 7] * apitch;
+  double r2 = 0.0;
+  for (int k = 0; k < d; ++k) {
+    const double x = (double)V[c * pitch + k] - (double)mu[k];
+    r2 = fma(x, x, r2);
+  }
+  crad[c] = __double2float_ru(sqrt(r2) * (1.0 + 1e-12));
+}
+
+// The pick, folded into the refine's last block (the block whose ticket
+// completes the grid): exact gains of the window, the reference argmax rule
+// (optimize.py:83-85: top = max value; window = 1e-12 max(1,|top|); best =
+// lowest index with value >= top - window; value = f(S) + gain/N) and, with
+// `commit`, the selection.  A lazy first batch (`batch`) first decides whether
+// it holds the whole stale set (best bound outside it below the threshold):
+// if so it picks and marks the step decided (level[0] = -2), otherwise it
+// marks it undecided (-3) and leaves the pick to the second refine.
+struct RefineFinal {
+  unsigned int* counter = nullptr;  // nullptr: no finalize (the caller picks)
+  double* wgain = nullptr;
+  double inv_n = 0.0;
+  const double* cur = nullptr;
+  int64_t* best = nullptr;
+  int commit = 0, step = 0;
+  unsigned char* selected = nullptr;
+  int64_t* sel_out = nullptr;
+  long long* stats = nullptr;   // [0] window sum [1] max [2] rung [3] steps [5] decided lazy steps [7] lazy steps
+  int* level = nullptr;         // [0] this step's gate, [1] the run's rung
+  double* ubp = nullptr;        // lazy bounds: exact gains of the window
+  int64_t c0 = 0;
+  int batch = 0;
+  const double* ub_next = nullptr;
+  double margin = 0.0;
+  long long* maxlb = nullptr;
+  int* scount = nullptr;                 // zeroed for the undecided path's k_lazy_mark2
+  cudaGraphConditionalHandle hrest = 0;  // the undecided-step conditional node (graph capture)
+};
+
+__device__ void refine_finalize(const RefineFinal& F, int wc, const int64_t* __restrict__ wlist,
+                                const double* __restrict__ part_r, int ng, double* sred, long long* sidx) {
+  const int tid = threadIdx.x;
+  const double f = *F.cur;
+  double top = -INFINITY, gmax = 0.0;
+  // short windows: every partial loaded by the whole block first (one memory
+  // round trip), then each candidate's left-to-right sum from shared memory --
+  // the same additions in the same order as chunk_total
+  const bool staged = wc <= (int)blockDim.x && (int64_t)wc * ng <= 2 * (int64_t)blockDim.x;
+  if (staged) {
+    for (int i = tid; i < wc * ng; i += blockDim.x) sred[i] = __ldcg(part_r + i);
+    __syncthreads();
+  }
+  double gs = 0.0;
+  if (staged && tid < wc)
+    for (int q = 0; q < ng; ++q) gs += sred[tid * ng + q];
+  __syncthreads();
+  for (int w = tid; w < wc; w += blockDim.x) {
+    const double gsum = staged ? gs : chunk_total(part_r + (int64_t)w * ng, ng);
+    F.wgain[w] = gsum;
+    if (F.ubp) F.ubp[wlist[w] - F.c0] = gsum;  // the exact gain bounds every later one (submodularity)
+    top = fmax(top, __dadd_rn(f, __dmul_rn(gsum, F.inv_n)));  // no FMA contraction: host pick() matches
+    gmax = fmax(gmax, gsum);
+  }
+  sred[tid] = top;
+  sred[blockDim.x + tid] = gmax;
+  __syncthreads();
+  for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+    if (tid < st) {
+      sred[tid] = fmax(sred[tid], sred[tid + st]);
+      sred[blockDim.x + tid] = fmax(sred[blockDim.x + tid], sred[blockDim.x + tid + st]);
+    }
+    __syncthreads();
+  }
+  top = sred[0];
+  if (F.batch) {
+    __shared__ int sdone;
+    if (tid == 0) {
+      const double lb = sred[blockDim.x];
+      const int done = *F.ub_next < lb - F.margin - 1e-9 * fabs(lb);
+      *F.maxlb = dkey(lb);
+      F.stats[7] += 1;
+      F.stats[5] += done;
+      F.stats[6] += wc;
+      F.level[0] = done ? -2 : -3;
+      *F.scount = 0;
+      if (F.hrest) cudaGraphSetConditional(F.hrest, done ? 0u : 1u);
+      sdone = done;
+    }
+    __syncthreads();
+    if (!sdone) return;
+  }
+  const double window = 1e-12 * fmax(1.0, fabs(top));
+  long long bi = LLONG_MAX;
+  for (int w = tid; w < wc; w += blockDim.x) {
+    const double val = __dadd_rn(f, __dmul_rn(F.wgain[w], F.inv_n));
+    if (val >= top - window) bi = min(bi, (long long)wlist[w]);
+  }
+  sidx[tid] = bi;
+  __syncthreads();
+  for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+    if (tid < st) sidx[tid] = min(sidx[tid], sidx[tid + st]);
+    __syncthreads();
+  }
+  if (tid == 0) {
+    const long long b = sidx[0] == LLONG_MAX ? -1 : sidx[0];
+    *F.best = b;
+    F.stats[0] += wc;
+    F.stats[1] = max(F.stats[1], (long long)wc);
+    F.stats[2] = F.level ? F.level[1] : -1;
+    F.stats[3] += 1;
+    if (F.commit && b >= 0) {
+      F.selected[b] = 1;
+      F.sel_out[F.step] = b;
+    }
+  }
+}
 
 template <typename T, bool BIGD>
 __global__ void __launch_bounds__(RED_THREADS) k_refine(const T* __restrict__ V, int pitch, int64_t n, int d,
                                                         const double* __restrict__ cm64,
                                                         const int* __restrict__ wcount,
                                                         const int64_t* __restrict__ wlist, int nchunks, int ng,
-                                                        double* __restrict__ part_r, RefinePrune pr) {
+                                                        double* __restrict__ part_r, RefinePrune pr,
+                                                        const int* __restrict__ skip_level, RefineFinal fin) {
+  if (skip_level && *skip_level == -2) return;  // lazy step already decided by the first batch
   extern __shared__ double cd[];  // RW * d doubles (BIGD: candidates read through L1 instead)
   __shared__ double red[RW][RED_THREADS];
   __shared__ int64_t cidx[RW];
@@ -1062,15 +1304,8 @@ __global__ void __launch_bounds__(RED_THREADS) k_refine(const T* __restrict__ V,
       cidx[tid] = tid < nw ? wlist[wg * RW + tid] : wlist[wg * RW];
       if (pr.rho) {
         const int64_t c = cidx[tid];
-        const int a = pr.tile_anchor[c >> 7];
-        const float* mu = pr.anchors + (int64_t)a * pr.apitch;
-        double r2 = 0.0;
-        for (int k = 0; k < d; ++k) {
-          const double x = (double)V[c * pitch + k] - (double)mu[k];
-          r2 = fma(x, x, r2);
-        }
-        canc[tid] = a;
-        crad[tid] = __double2float_ru(sqrt(r2) * (1.0 + 1e-12));
+        canc[tid] = pr.tile_anchor[c >> 7];
+        crad[tid] = pr.crad[c];
       }
     }
     __syncthreads();
@@ -1129,7 +1364,41 @@ __global__ void __launch_bounds__(RED_THREADS) k_refine(const T* __restrict__ V,
         int k = 0;
         if constexpr (sizeof(T) == 4) {
           // fp32 rows are 16-byte aligned (pitch % 4 == 0): one LDG.128 per row
-          // and 4 dims, the four rows' loads in flight together
+          // and 4 dims; 8 dims per iteration keep the 8 loads of the four rows
+          // in flight together (the refine of a short window is latency-bound)
+          for (; k + 8 <= d; k += 8) {
+            float4 q[4], r[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              q[i] = __ldg(reinterpret_cast<const float4*>(row[i]) + (k >> 2));
+              r[i] = __ldg(reinterpret_cast<const float4*>(row[i]) + (k >> 2) + 1);
+            }
+            double x[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) x[i] = (double)q[i].x;
+            step(k, x);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) x[i] = (double)q[i].y;
+            step(k + 1, x);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) x[i] = (double)q[i].z;
+            step(k + 2, x);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) x[i] = (double)q[i].w;
+            step(k + 3, x);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) x[i] = (double)r[i].x;
+            step(k + 4, x);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) x[i] = (double)r[i].y;
+            step(k + 5, x);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) x[i] = (double)r[i].z;
+            step(k + 6, x);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) x[i] = (double)r[i].w;
+            step(k + 7, x);
+          }
           for (; k + 4 <= d; k += 4) {
             float4 q[4];
 #pragma unroll
@@ -1184,65 +1453,156 @@ __global__ void __launch_bounds__(RED_THREADS) k_refine(const T* __restrict__ V,
     }
     if (tid < nw) part_r[(int64_t)(wg * RW + tid) * ng + grp] = tot[tid];
   }
+  if (!fin.counter) return;
+  __shared__ bool last;
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    last = atomicAdd(fin.counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (tid == 0) *fin.counter = 0u;
+  refine_finalize(fin, wc, wlist, part_r, ng, &red[0][0], reinterpret_cast<long long*>(&red[2][0]));
 }
 static_assert(RW == RED_THREADS / 32, "one reducing warp per window candidate");
 
-// Exact gains of W, the reference argmax rule (optimize.py:83-85):
-//   top = max value; window = 1e-12*max(1,|top|); best = lowest index with
-//   value >= top - window; value = f(S) + gain/N.
-// commit != 0: mark the winner selected and record it as step `step`.
-__global__ void __launch_bounds__(1024) k_pick(const int* __restrict__ wcount, const int64_t* __restrict__ wlist,
-                                               int ng, const double* __restrict__ part_r, double inv_n,
-                                               const double* __restrict__ cur, double* __restrict__ wgain,
-                                               int64_t* __restrict__ best, int commit, int step,
-                                               unsigned char* __restrict__ selected, int64_t* __restrict__ sel_out,
-                                               long long* __restrict__ stats, const int* __restrict__ level_now,
-                                               double* __restrict__ ubp = nullptr, int64_t c0 = 0) {
-  __shared__ double smax[1024];
-  __shared__ long long smin[1024];
-  const int wc = *wcount;
-  const double f = *cur;
-  double top = -INFINITY;
-  for (int w = threadIdx.x; w < wc; w += blockDim.x) {
-    const double gsum = chunk_total(part_r + (int64_t)w * ng, ng);
-    wgain[w] = gsum;
-    if (ubp) ubp[wlist[w] - c0] = gsum;  // the exact gain bounds every later one (submodularity)
-    const double val = __dadd_rn(f, __dmul_rn(gsum, inv_n));  // no FMA contraction: host pick() matches
-    top = fmax(top, val);
+// Two-phase refine of a short window (<= RW candidates: the lazy first batch).
+// The classic k_refine gives each (window group, chunk group) unit to one block,
+// so a short window runs on nchunks blocks with 4 points per thread and the
+// row loads on its critical path.  Here (a) every point is one thread
+// (k_refine_terms: term[j][v] = max(0, cm(v) - d64(v, c_j)), the same
+// sequential fp64 operations per (point, candidate); certified-unreachable
+// tiles store 0, exactly what the classic computes there), then (b) one block
+// per chunk group replays the classic reduction on the stored terms: per
+// thread its 4 points in order, the same 8-sequential + butterfly warp sums,
+// chunks left to right (k_refine_sums) -- bit-identical partials, so the two
+// refines are interchangeable for any candidate.
+template <typename T>
+__global__ void __launch_bounds__(RED_THREADS) k_refine_terms(const T* __restrict__ V, int pitch, int64_t n, int d,
+                                                              const double* __restrict__ cm64,
+                                                              const int* __restrict__ wcount,
+                                                              const int64_t* __restrict__ wlist,
+                                                              double* __restrict__ terms, int64_t tstride,
+                                                              RefinePrune pr) {
+  extern __shared__ double cd[];  // RW * d doubles
+  __shared__ int lmask[4];        // live candidates of each of the block's point tiles (256 / np)
+  const int tid = threadIdx.x;
+  const int wc = min(RW, *wcount);
+  for (int i = tid; i < RW * d; i += blockDim.x) {
+    const int j = i / d, k = i - j * d;
+    cd[i] = j < wc ? (double)V[wlist[j] * pitch + k] : 0.0;
   }
-  smax[threadIdx.x] = top;
+  if (tid < RED_THREADS / pr.np) {
+    unsigned m = (1u << wc) - 1u;
+    const int64_t t = (int64_t)blockIdx.x * (RED_THREADS / pr.np) + tid;
+    if (pr.rho && t * pr.np < n) {
+      m = 0;
+      for (int j = 0; j < wc; ++j) {
+        const int64_t c = wlist[j];
+        const float* rho = pr.rho + (int64_t)pr.tile_anchor[c >> 7] * pr.kpstride;
+        if (!tile_prunable(rho[t], pr.crad[c], pr.cmx[t])) m |= 1u << j;
+      }
+    }
+    lmask[tid] = (int)m;
+  }
   __syncthreads();
-  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s) smax[threadIdx.x] = fmax(smax[threadIdx.x], smax[threadIdx.x + s]);
+  const int64_t v = (int64_t)blockIdx.x * RED_THREADS + tid;
+  if (v >= n) return;
+  const unsigned lm = (unsigned)lmask[tid / pr.np];
+  double s[RW];
+#pragma unroll
+  for (int j = 0; j < RW; ++j) s[j] = 0.0;
+  const T* row = V + v * pitch;
+  auto step = [&](int k, double x) {
+#pragma unroll
+    for (int j = 0; j < RW; ++j)
+      if (lm >> j & 1u) {
+        const double t = x - cd[j * d + k];
+        s[j] = fma(t, t, s[j]);
+      }
+  };
+  int k = 0;
+  if constexpr (sizeof(T) == 4) {
+    for (; k + 16 <= d; k += 16) {  // 4 x LDG.128 in flight per iteration
+      float4 q[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) q[i] = __ldg(reinterpret_cast<const float4*>(row) + (k >> 2) + i);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        step(k + 4 * i, (double)q[i].x);
+        step(k + 4 * i + 1, (double)q[i].y);
+        step(k + 4 * i + 2, (double)q[i].z);
+        step(k + 4 * i + 3, (double)q[i].w);
+      }
+    }
+    for (; k + 4 <= d; k += 4) {
+      const float4 q = __ldg(reinterpret_cast<const float4*>(row) + (k >> 2));
+      step(k, (double)q.x);
+      step(k + 1, (double)q.y);
+      step(k + 2, (double)q.z);
+      step(k + 3, (double)q.w);
+    }
+  }
+  for (; k < d; ++k) step(k, (double)row[k]);
+  const double c = cm64[v];
+#pragma unroll
+  for (int j = 0; j < RW; ++j)
+    if (j < wc) {
+      const double t = c - s[j];
+      terms[(int64_t)j * tstride + v] = (lm >> j & 1u) && t > 0.0 ? t : 0.0;
+    }
+}
+
+__global__ void __launch_bounds__(RED_THREADS) k_refine_sums(const double* __restrict__ terms, int64_t tstride,
+                                                             int64_t n, const int* __restrict__ wcount,
+                                                             const int64_t* __restrict__ wlist, int nchunks, int ng,
+                                                             double* __restrict__ part_r, RefineFinal fin) {
+  __shared__ double red[RW][RED_THREADS];
+  __shared__ double tot[RW];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wc = min(RW, *wcount);
+  const int cpg = (nchunks + ng - 1) / ng;
+  const int grp = blockIdx.x;
+  if (tid < RW) tot[tid] = 0.0;
+  const int ch1 = min(nchunks, (grp + 1) * cpg);
+  for (int ch = grp * cpg; ch < ch1; ++ch) {
+    const int64_t v0 = (int64_t)ch * RCH + tid;
+#pragma unroll
+    for (int j = 0; j < RW; ++j) {
+      double acc = 0.0;
+      if (j < wc)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int64_t v = v0 + (int64_t)i * RED_THREADS;
+          if (v < n) acc += __ldcg(terms + (int64_t)j * tstride + v);
+        }
+      red[j][tid] = acc;
+    }
+    __syncthreads();
+    {
+      double x = 0.0;
+#pragma unroll
+      for (int q = 0; q < RED_THREADS / 32; ++q) x += red[warp][lane * (RED_THREADS / 32) + q];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      if (lane == 0) tot[warp] += x;
+    }
     __syncthreads();
   }
-  top = smax[0];
-  const double window = 1e-12 * fmax(1.0, fabs(top));
-  long long bi = LLONG_MAX;
-  for (int w = threadIdx.x; w < wc; w += blockDim.x) {
-    const double val = __dadd_rn(f, __dmul_rn(wgain[w], inv_n));
-    if (val >= top - window) bi = min(bi, (long long)wlist[w]);
-  }
-  smin[threadIdx.x] = bi;
+  if (tid < wc) part_r[(int64_t)tid * ng + grp] = tot[tid];
+  __shared__ bool last;
   __syncthreads();
-  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s) smin[threadIdx.x] = min(smin[threadIdx.x], smin[threadIdx.x + s]);
-    __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    last = atomicAdd(fin.counter, 1u) == gridDim.x - 1;
   }
-  if (threadIdx.x == 0) {
-    const long long b = smin[0] == LLONG_MAX ? -1 : smin[0];
-    *best = b;
-    if (stats) {  // [0] sum of window sizes, [1] max window, [2] screen rung, [3] steps
-      stats[0] += wc;
-      stats[1] = max(stats[1], (long long)wc);
-      stats[2] = level_now ? level_now[1] : -1;
-      stats[3] += 1;
-    }
-    if (commit && b >= 0) {
-      selected[b] = 1;
-      sel_out[step] = b;
-    }
-  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (tid == 0) *fin.counter = 0u;
+  refine_finalize(fin, wc, wlist, part_r, ng, &red[0][0], reinterpret_cast<long long*>(&red[2][0]));
 }
 
 // ---------------------------------------------------------------- sharded exchange
