@@ -201,12 +201,16 @@ struct ebc_ctx {
   int lazy_batch = 4;              // EBC200_LAZY_BATCH (1..RW): candidates refined first in a lazy step
   unsigned int* counter3 = nullptr;  // k_refine's finalize ticket
   bool refine2 = true;             // EBC200_REFINE2=0: the lazy batch on the classic k_refine
-  DevBuf rterms;                   // RW x n_pad per-point terms of the two-phase refine
+  DevBuf rterms;                   // RW x nchunks chunk sums of the short refine
   // CUDA-graph conditional nodes for the undecided part of a lazy step (captured
   // runs only: an eager run gates those kernels on level[0] instead)
   bool use_cond = true;            // EBC200_GRAPH_COND=0: plain gated kernels in graphs too
   cudaStream_t side[2] = {nullptr, nullptr};  // capture streams of conditional bodies
   bool screen_events_outside = false;  // the step's family events are recorded by the caller
+  // eager (uncaptured) lazy steps read the step's mode back (one 4-byte copy
+  // into pinned memory) and enqueue only the kernels that will do work
+  bool eager_sync = true;          // EBC200_EAGER_SYNC=0: enqueue everything, gated on the device
+  int* mode_host = nullptr;        // pinned
   const unsigned char* step_bflag = nullptr;  // enqueue-time: bflag during a lazy step, else nullptr
   DevBuf part_g, part_e, part_r, sel_out, val_out, gain_out, ms_part, ms_off, ms_idx, ms_out;
   // sparse work-matrix path
@@ -794,8 +798,8 @@ int enqueue_refine(ebc_ctx* ctx, int ng, const int* skip_level, const RefineFina
               : launch_refine<float, false>(ctx, ctx->V32, rgrid, rsmem, ng, skip_level, fin);
 }
 
-// Two-phase refine of a window of at most RW candidates (the lazy first batch):
-// per-point terms, then the classic reduction replayed on them (kernels.cuh).
+// Refine of a window of at most RW candidates (the lazy first batch): one
+// RCH-thread block per chunk, the classic reduction replayed (kernels.cuh).
 int enqueue_refine_short(ebc_ctx* ctx, int ng, const RefineFinal& fin) {
   RefinePrune pr;
   if (refine_prune_on(ctx) && ctx->cmx_fresh) {
@@ -808,25 +812,21 @@ int enqueue_refine_short(ebc_ctx* ctx, int ng, const RefineFinal& fin) {
     pr.np = ctx->tc_np;
     pr.crad = ctx->crad;
   }
-  const size_t smem = (size_t)RW * ctx->d * sizeof(double);
-  if (smem > 200 * 1024) return enqueue_refine(ctx, ng, nullptr, fin);
-  int rc = ensure(ctx, ctx->rterms, (size_t)RW * ctx->n_pad * sizeof(double));
+  const size_t smem = (size_t)RW * (ctx->d + RCH) * sizeof(double);
+  if (smem > 180 * 1024) return enqueue_refine(ctx, ng, nullptr, fin);
+  int rc = ensure(ctx, ctx->rterms, (size_t)RW * ctx->nchunks * sizeof(double));
   if (rc) return rc;
-  const unsigned grid = (unsigned)((ctx->n + RED_THREADS - 1) / RED_THREADS);
   if (ctx->dtype == EBC_F64) {
-    CU(cudaFuncSetAttribute(k_refine_terms<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_refine_terms<double><<<grid, RED_THREADS, smem, ctx->stream>>>(ctx->V64, ctx->pitch, ctx->n, ctx->d, ctx->cm64,
-                                                                    ctx->wcount, ctx->wlist, (double*)ctx->rterms.p,
-                                                                    ctx->n_pad, pr);
+    CU(cudaFuncSetAttribute(k_refine_short<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_refine_short<double><<<ctx->nchunks, SHORT_THREADS, smem, ctx->stream>>>(
+        ctx->V64, ctx->pitch, ctx->n, ctx->d, ctx->cm64, ctx->wcount, ctx->wlist, ctx->nchunks, ng,
+        (double*)ctx->rterms.p, (double*)ctx->part_r.p, pr, fin);
   } else {
-    CU(cudaFuncSetAttribute(k_refine_terms<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_refine_terms<float><<<grid, RED_THREADS, smem, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->n, ctx->d, ctx->cm64,
-                                                                   ctx->wcount, ctx->wlist, (double*)ctx->rterms.p,
-                                                                   ctx->n_pad, pr);
+    CU(cudaFuncSetAttribute(k_refine_short<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_refine_short<float><<<ctx->nchunks, SHORT_THREADS, smem, ctx->stream>>>(
+        ctx->V32, ctx->pitch, ctx->n, ctx->d, ctx->cm64, ctx->wcount, ctx->wlist, ctx->nchunks, ng,
+        (double*)ctx->rterms.p, (double*)ctx->part_r.p, pr, fin);
   }
-  KCHECK();
-  k_refine_sums<<<ng, RED_THREADS, 0, ctx->stream>>>((const double*)ctx->rterms.p, ctx->n_pad, ctx->n, ctx->wcount,
-                                                     ctx->wlist, ctx->nchunks, ng, (double*)ctx->part_r.p, fin);
   KCHECK();
   return EBC_OK;
 }
@@ -956,7 +956,16 @@ int run_step_select(ebc_ctx* ctx, int step, int commit, int64_t* sel_dev) {
   rc = ctx->refine2 ? enqueue_refine_short(ctx, ng, fb) : enqueue_refine(ctx, ng, nullptr, fb);
   if (rc) return rc;
   ctx->cmx_fresh = false;
-  {
+  const bool sync = !ctx->capturing && ctx->eager_sync;
+  auto read_mode = [&]() -> int {
+    if (cudaMemcpyAsync(ctx->mode_host, ctx->level, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
+        cudaStreamSynchronize(ctx->stream) != cudaSuccess)
+      return -4;
+    return *ctx->mode_host;
+  };
+  int mode = sync ? read_mode() : -3;
+  if (mode == -4) return fail(ctx, EBC_ECUDA, "lazy step: mode read-back failed");
+  if (mode != -2) {
     // undecided step (level[0] == -3): stale set -> mode -> screen / refine
     CondScope ca;
     CU(ca.open(ctx, hrest, 0));
@@ -968,7 +977,11 @@ int run_step_select(ebc_ctx* ctx, int step, int commit, int64_t* sel_dev) {
     k_lazy_plan2<<<1, 256, 0, ctx->stream>>>(ctx->scount, ctx->slist, has_screen ? ctx->lazy_cap : INT_MAX,
                                              ctx->wcount, ctx->wlist, ctx->level, ctx->stats, hs);
     KCHECK();
-    if (has_screen) {
+    if (sync) {
+      mode = read_mode();
+      if (mode == -4) return fail(ctx, EBC_ECUDA, "lazy step: mode read-back failed");
+    }
+    if (has_screen && mode != -1) {
       CondScope cb;
       CU(cb.open(ctx, hs, 1));
       ctx->step_bflag = ctx->bflag;
@@ -1176,6 +1189,7 @@ void free_ctx(ebc_ctx* c) {
   }
   for (cudaStream_t ss : c->side)
     if (ss) cudaStreamDestroy(ss);
+  if (c->mode_host) cudaFreeHost(c->mode_host);
   delete c;
 }
 
@@ -1593,6 +1607,9 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
     if (lb && lb[0]) ctx->lazy_batch = std::max(1, std::min(RW, atoi(lb)));
     const char* r2 = getenv("EBC200_REFINE2");
     if (r2 && r2[0] == '0') ctx->refine2 = false;
+    const char* es = getenv("EBC200_EAGER_SYNC");
+    if (es && es[0] == '0') ctx->eager_sync = false;
+    CUC(cudaMallocHost((void**)&ctx->mode_host, sizeof(int)));
     const char* gc = getenv("EBC200_GRAPH_COND");
     if (gc && gc[0] == '0') ctx->use_cond = false;
   }

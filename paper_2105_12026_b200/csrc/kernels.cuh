@@ -1190,37 +1190,43 @@ struct RefineFinal {
   cudaGraphConditionalHandle hrest = 0;  // the undecided-step conditional node (graph capture)
 };
 
-__device__ void refine_finalize(const RefineFinal& F, int wc, const int64_t* __restrict__ wlist,
-                                const double* __restrict__ part_r, int ng, double* sred, long long* sidx) {
+// nt: the participating threads (the first nt of the block; every thread of
+// the block must call it -- it synchronises the block)
+__device__ void refine_finalize_n(const RefineFinal& F, int wc, const int64_t* __restrict__ wlist,
+                                  const double* __restrict__ part_r, int ng, double* sred, long long* sidx,
+                                  int nt) {
   const int tid = threadIdx.x;
+  const bool on = tid < nt;
   const double f = *F.cur;
   double top = -INFINITY, gmax = 0.0;
   // short windows: every partial loaded by the whole block first (one memory
   // round trip), then each candidate's left-to-right sum from shared memory --
   // the same additions in the same order as chunk_total
-  const bool staged = wc <= (int)blockDim.x && (int64_t)wc * ng <= 2 * (int64_t)blockDim.x;
+  const bool staged = wc <= nt && (int64_t)wc * ng <= 2 * (int64_t)nt;
   if (staged) {
-    for (int i = tid; i < wc * ng; i += blockDim.x) sred[i] = __ldcg(part_r + i);
+    for (int i = tid; i < wc * ng && on; i += nt) sred[i] = __ldcg(part_r + i);
     __syncthreads();
   }
   double gs = 0.0;
   if (staged && tid < wc)
     for (int q = 0; q < ng; ++q) gs += sred[tid * ng + q];
   __syncthreads();
-  for (int w = tid; w < wc; w += blockDim.x) {
+  for (int w = tid; w < wc && on; w += nt) {
     const double gsum = staged ? gs : chunk_total(part_r + (int64_t)w * ng, ng);
     F.wgain[w] = gsum;
     if (F.ubp) F.ubp[wlist[w] - F.c0] = gsum;  // the exact gain bounds every later one (submodularity)
     top = fmax(top, __dadd_rn(f, __dmul_rn(gsum, F.inv_n)));  // no FMA contraction: host pick() matches
     gmax = fmax(gmax, gsum);
   }
-  sred[tid] = top;
-  sred[blockDim.x + tid] = gmax;
+  if (on) {
+    sred[tid] = top;
+    sred[nt + tid] = gmax;
+  }
   __syncthreads();
-  for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+  for (int st = nt / 2; st > 0; st >>= 1) {
     if (tid < st) {
       sred[tid] = fmax(sred[tid], sred[tid + st]);
-      sred[blockDim.x + tid] = fmax(sred[blockDim.x + tid], sred[blockDim.x + tid + st]);
+      sred[nt + tid] = fmax(sred[nt + tid], sred[nt + tid + st]);
     }
     __syncthreads();
   }
@@ -1228,7 +1234,7 @@ __device__ void refine_finalize(const RefineFinal& F, int wc, const int64_t* __r
   if (F.batch) {
     __shared__ int sdone;
     if (tid == 0) {
-      const double lb = sred[blockDim.x];
+      const double lb = sred[nt];
       const int done = *F.ub_next < lb - F.margin - 1e-9 * fabs(lb);
       *F.maxlb = dkey(lb);
       F.stats[7] += 1;
@@ -1244,13 +1250,13 @@ __device__ void refine_finalize(const RefineFinal& F, int wc, const int64_t* __r
   }
   const double window = 1e-12 * fmax(1.0, fabs(top));
   long long bi = LLONG_MAX;
-  for (int w = tid; w < wc; w += blockDim.x) {
+  for (int w = tid; w < wc && on; w += nt) {
     const double val = __dadd_rn(f, __dmul_rn(F.wgain[w], F.inv_n));
     if (val >= top - window) bi = min(bi, (long long)wlist[w]);
   }
-  sidx[tid] = bi;
+  if (on) sidx[tid] = bi;
   __syncthreads();
-  for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+  for (int st = nt / 2; st > 0; st >>= 1) {
     if (tid < st) sidx[tid] = min(sidx[tid], sidx[tid + st]);
     __syncthreads();
   }
@@ -1266,6 +1272,12 @@ __device__ void refine_finalize(const RefineFinal& F, int wc, const int64_t* __r
       F.sel_out[F.step] = b;
     }
   }
+}
+
+__device__ __forceinline__ void refine_finalize(const RefineFinal& F, int wc, const int64_t* __restrict__ wlist,
+                                                const double* __restrict__ part_r, int ng, double* sred,
+                                                long long* sidx) {
+  refine_finalize_n(F, wc, wlist, part_r, ng, sred, sidx, blockDim.x);
 }
 
 template <typename T, bool BIGD>
@@ -1468,35 +1480,43 @@ __global__ void __launch_bounds__(RED_THREADS) k_refine(const T* __restrict__ V,
 }
 static_assert(RW == RED_THREADS / 32, "one reducing warp per window candidate");
 
-// Two-phase refine of a short window (<= RW candidates: the lazy first batch).
-// The classic k_refine gives each (window group, chunk group) unit to one block,
-// so a short window runs on nchunks blocks with 4 points per thread and the
-// row loads on its critical path.  Here (a) every point is one thread
-// (k_refine_terms: term[j][v] = max(0, cm(v) - d64(v, c_j)), the same
-// sequential fp64 operations per (point, candidate); certified-unreachable
-// tiles store 0, exactly what the classic computes there), then (b) one block
-// per chunk group replays the classic reduction on the stored terms: per
-// thread its 4 points in order, the same 8-sequential + butterfly warp sums,
-// chunks left to right (k_refine_sums) -- bit-identical partials, so the two
-// refines are interchangeable for any candidate.
+// Refine of a short window (<= RW candidates: the lazy first batch), one block
+// of RCH threads per chunk.  The classic k_refine gives each (window group,
+// chunk group) unit to a 256-thread block (4 points per thread, the row loads
+// on its critical path), so a short window runs latency-bound on nchunks
+// blocks.  Here every point is one thread: term(v, j) = max(0, cm(v) -
+// d64(v, c_j)) with the same sequential fp64 operations per (point, candidate)
+// (certified-unreachable tiles give 0, exactly what the classic computes
+// there); then the classic chunk reduction replayed in shared memory -- thread
+// t < 256 adds the terms of points t, t+256, t+512, t+768 in order, the same
+// 8-sequential + butterfly warp sums -- and the chunk sums are combined by the
+// last block in the classic order (chunks of a group left to right, then the
+// groups): bit-identical partials, so both refines serve any candidate.
+constexpr int SHORT_THREADS = RCH;
 template <typename T>
-__global__ void __launch_bounds__(RED_THREADS) k_refine_terms(const T* __restrict__ V, int pitch, int64_t n, int d,
-                                                              const double* __restrict__ cm64,
-                                                              const int* __restrict__ wcount,
-                                                              const int64_t* __restrict__ wlist,
-                                                              double* __restrict__ terms, int64_t tstride,
-                                                              RefinePrune pr) {
-  extern __shared__ double cd[];  // RW * d doubles
-  __shared__ int lmask[4];        // live candidates of each of the block's point tiles (256 / np)
-  const int tid = threadIdx.x;
+__global__ void __launch_bounds__(SHORT_THREADS, 1) k_refine_short(const T* __restrict__ V, int pitch, int64_t n,
+                                                                   int d, const double* __restrict__ cm64,
+                                                                   const int* __restrict__ wcount,
+                                                                   const int64_t* __restrict__ wlist, int nchunks,
+                                                                   int ng, double* __restrict__ xch,
+                                                                   double* __restrict__ part_r, RefinePrune pr,
+                                                                   RefineFinal fin) {
+  extern __shared__ double dsm[];  // cd: RW * d doubles, then terms [RW][RCH]
+  double* cd = dsm;
+  double* tr = dsm + RW * d;
+  __shared__ double red[RW][RED_THREADS];
+  __shared__ int lmask[RCH / 64];  // live candidates per point tile of the chunk
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int wc = min(RW, *wcount);
+  const int ch = blockIdx.x;
   for (int i = tid; i < RW * d; i += blockDim.x) {
     const int j = i / d, k = i - j * d;
     cd[i] = j < wc ? (double)V[wlist[j] * pitch + k] : 0.0;
   }
-  if (tid < RED_THREADS / pr.np) {
+  const int tpc = RCH / pr.np;
+  if (tid < tpc) {
     unsigned m = (1u << wc) - 1u;
-    const int64_t t = (int64_t)blockIdx.x * (RED_THREADS / pr.np) + tid;
+    const int64_t t = (int64_t)ch * tpc + tid;
     if (pr.rho && t * pr.np < n) {
       m = 0;
       for (int j = 0; j < wc; ++j) {
@@ -1508,90 +1528,73 @@ __global__ void __launch_bounds__(RED_THREADS) k_refine_terms(const T* __restric
     lmask[tid] = (int)m;
   }
   __syncthreads();
-  const int64_t v = (int64_t)blockIdx.x * RED_THREADS + tid;
-  if (v >= n) return;
+  const int64_t v = (int64_t)ch * RCH + tid;
   const unsigned lm = (unsigned)lmask[tid / pr.np];
   double s[RW];
 #pragma unroll
   for (int j = 0; j < RW; ++j) s[j] = 0.0;
-  const T* row = V + v * pitch;
-  auto step = [&](int k, double x) {
+  if (v < n && lm) {
+    const T* row = V + v * pitch;
+    auto step = [&](int k, double x) {
 #pragma unroll
-    for (int j = 0; j < RW; ++j)
-      if (lm >> j & 1u) {
-        const double t = x - cd[j * d + k];
-        s[j] = fma(t, t, s[j]);
+      for (int j = 0; j < RW; ++j)
+        if (lm >> j & 1u) {
+          const double t = x - cd[j * d + k];
+          s[j] = fma(t, t, s[j]);
+        }
+    };
+    int k = 0;
+    if constexpr (sizeof(T) == 4) {
+      for (; k + 16 <= d; k += 16) {  // 4 x LDG.128 in flight
+        float4 q[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) q[i] = __ldg(reinterpret_cast<const float4*>(row) + (k >> 2) + i);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          step(k + 4 * i, (double)q[i].x);
+          step(k + 4 * i + 1, (double)q[i].y);
+          step(k + 4 * i + 2, (double)q[i].z);
+          step(k + 4 * i + 3, (double)q[i].w);
+        }
       }
-  };
-  int k = 0;
-  if constexpr (sizeof(T) == 4) {
-    for (; k + 16 <= d; k += 16) {  // 4 x LDG.128 in flight per iteration
-      float4 q[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) q[i] = __ldg(reinterpret_cast<const float4*>(row) + (k >> 2) + i);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        step(k + 4 * i, (double)q[i].x);
-        step(k + 4 * i + 1, (double)q[i].y);
-        step(k + 4 * i + 2, (double)q[i].z);
-        step(k + 4 * i + 3, (double)q[i].w);
+      for (; k + 4 <= d; k += 4) {
+        const float4 q = __ldg(reinterpret_cast<const float4*>(row) + (k >> 2));
+        step(k, (double)q.x);
+        step(k + 1, (double)q.y);
+        step(k + 2, (double)q.z);
+        step(k + 3, (double)q.w);
       }
     }
-    for (; k + 4 <= d; k += 4) {
-      const float4 q = __ldg(reinterpret_cast<const float4*>(row) + (k >> 2));
-      step(k, (double)q.x);
-      step(k + 1, (double)q.y);
-      step(k + 2, (double)q.z);
-      step(k + 3, (double)q.w);
-    }
+    for (; k < d; ++k) step(k, (double)row[k]);
   }
-  for (; k < d; ++k) step(k, (double)row[k]);
-  const double c = cm64[v];
+  const double c = v < n ? cm64[v] : 0.0;
 #pragma unroll
-  for (int j = 0; j < RW; ++j)
-    if (j < wc) {
-      const double t = c - s[j];
-      terms[(int64_t)j * tstride + v] = (lm >> j & 1u) && t > 0.0 ? t : 0.0;
-    }
-}
-
-__global__ void __launch_bounds__(RED_THREADS) k_refine_sums(const double* __restrict__ terms, int64_t tstride,
-                                                             int64_t n, const int* __restrict__ wcount,
-                                                             const int64_t* __restrict__ wlist, int nchunks, int ng,
-                                                             double* __restrict__ part_r, RefineFinal fin) {
-  __shared__ double red[RW][RED_THREADS];
-  __shared__ double tot[RW];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int wc = min(RW, *wcount);
-  const int cpg = (nchunks + ng - 1) / ng;
-  const int grp = blockIdx.x;
-  if (tid < RW) tot[tid] = 0.0;
-  const int ch1 = min(nchunks, (grp + 1) * cpg);
-  for (int ch = grp * cpg; ch < ch1; ++ch) {
-    const int64_t v0 = (int64_t)ch * RCH + tid;
+  for (int j = 0; j < RW; ++j) {
+    const double t = c - s[j];
+    tr[j * RCH + tid] = (lm >> j & 1u) && t > 0.0 ? t : 0.0;
+  }
+  __syncthreads();
+  // the classic reduction: thread t < 256 adds its 4 points in order
+  if (tid < RED_THREADS) {
 #pragma unroll
     for (int j = 0; j < RW; ++j) {
       double acc = 0.0;
       if (j < wc)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int64_t v = v0 + (int64_t)i * RED_THREADS;
-          if (v < n) acc += __ldcg(terms + (int64_t)j * tstride + v);
-        }
+        for (int i = 0; i < RCH / RED_THREADS; ++i)
+          if ((int64_t)ch * RCH + tid + i * RED_THREADS < n) acc += tr[j * RCH + tid + i * RED_THREADS];
       red[j][tid] = acc;
     }
-    __syncthreads();
-    {
-      double x = 0.0;
-#pragma unroll
-      for (int q = 0; q < RED_THREADS / 32; ++q) x += red[warp][lane * (RED_THREADS / 32) + q];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-      if (lane == 0) tot[warp] += x;
-    }
-    __syncthreads();
   }
-  if (tid < wc) part_r[(int64_t)tid * ng + grp] = tot[tid];
+  __syncthreads();
+  if (warp < RW) {
+    double x = 0.0;
+#pragma unroll
+    for (int q = 0; q < RED_THREADS / 32; ++q) x += red[warp][lane * (RED_THREADS / 32) + q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0 && warp < wc) xch[(int64_t)warp * nchunks + ch] = x;
+  }
   __shared__ bool last;
   __syncthreads();
   if (tid == 0) {
@@ -1602,7 +1605,17 @@ __global__ void __launch_bounds__(RED_THREADS) k_refine_sums(const double* __res
   if (!last) return;
   __threadfence();
   if (tid == 0) *fin.counter = 0u;
-  refine_finalize(fin, wc, wlist, part_r, ng, &red[0][0], reinterpret_cast<long long*>(&red[2][0]));
+  // group partials in the classic order: tot = 0; tot += chunk sums left to right
+  const int cpg = (nchunks + ng - 1) / ng;
+  for (int i = tid; i < wc * ng; i += blockDim.x) {
+    const int w = i / ng, grp = i - w * ng;
+    double tot = 0.0;
+    const int c1 = min(nchunks, (grp + 1) * cpg);
+    for (int q = grp * cpg; q < c1; ++q) tot += __ldcg(xch + (int64_t)w * nchunks + q);
+    part_r[(int64_t)w * ng + grp] = tot;
+  }
+  __syncthreads();
+  refine_finalize_n(fin, wc, wlist, part_r, ng, &red[0][0], reinterpret_cast<long long*>(&red[2][0]), RED_THREADS);
 }
 
 // ---------------------------------------------------------------- sharded exchange
