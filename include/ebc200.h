@@ -70,6 +70,21 @@ int ebc_baseline(const ebc_ctx* ctx, double* out);
 int ebc_eval_multiset(ebc_ctx* ctx, const int64_t* offsets, const int64_t* idx, int64_t l,
                       double* out_f, int64_t* out_bad_set, int64_t* out_bad_index);
 
+/* ---- threshold sieves (sieve_stream_maximize, optimize.py:140-197) ----
+ * Each live sieve occupies a slot holding its cached minima over S_r u {e0}
+ * (N doubles), so one streamed element costs one distance pass shared by all
+ * sieves.  Values equal ebc_eval_multiset's on the same sets bit for bit.
+ *   ebc_sieve_reserve: storage for `slots` sieves (a new reservation starts
+ *     from scratch: slot contents are not kept);
+ *   ebc_sieve_step: (1) reset the reset slots to S = {}, (2) fold ground
+ *     index commit_e into the commit slots (the previous element's admissions;
+ *     commit_e < 0: none), (3) if e >= 0: *out_single = f({e}) and
+ *     out_values[i] = f(S_r u {e}) for r = eval_slots[i].  One host round trip. */
+int ebc_sieve_reserve(ebc_ctx* ctx, int32_t slots);
+int ebc_sieve_step(ebc_ctx* ctx, int64_t commit_e, const int32_t* commit_slots, int32_t n_commit,
+                   const int32_t* reset_slots, int32_t n_reset, int64_t e, const int32_t* eval_slots,
+                   int32_t n_eval, double* out_single, double* out_values);
+
 /* k-medoids loss of explicit representatives: mean over the ground rows of the
  * exact fp64 squared distance to the nearest of the r representatives
  * (reps: r x d row-major fp64, finite), the ground values widened exactly to

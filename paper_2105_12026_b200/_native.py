@@ -25,6 +25,7 @@ _i64 = ctypes.c_int64
 _i32 = ctypes.c_int32
 _f64p = ctypes.POINTER(ctypes.c_double)
 _i64p = ctypes.POINTER(ctypes.c_int64)
+_i32p = ctypes.POINTER(ctypes.c_int32)
 _vp = ctypes.c_void_p
 
 # name -> (restype, argtypes); mirrors include/ebc200.h
@@ -36,6 +37,8 @@ SIGNATURES = {
     "ebc_eval_multiset": (ctypes.c_int, [_vp, _i64p, _i64p, _i64, _f64p, _i64p, _i64p]),
     "ebc_greedy": (ctypes.c_int, [_vp, _i32, _i64p, _f64p, _f64p, _i64p]),
     "ebc_kmedoids_loss": (ctypes.c_int, [_vp, _f64p, _i64, _f64p]),
+    "ebc_sieve_reserve": (ctypes.c_int, [_vp, _i32]),
+    "ebc_sieve_step": (ctypes.c_int, [_vp, _i64, _i32p, _i32, _i32p, _i32, _i64, _i32p, _i32, _f64p, _f64p]),
     "ebc_shard_set_range": (ctypes.c_int, [_vp, _i64, _i64]),
     "ebc_shard_step": (ctypes.c_int, [_vp, _i64p, _f64p, _i64, _i64p, _f64p]),
     "ebc_shard_commit": (ctypes.c_int, [_vp, _i64, _f64p]),

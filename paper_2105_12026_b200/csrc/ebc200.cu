@@ -211,6 +211,11 @@ struct ebc_ctx {
   // into pinned memory) and enqueue only the kernels that will do work
   bool eager_sync = true;          // EBC200_EAGER_SYNC=0: enqueue everything, gated on the device
   int* mode_host = nullptr;        // pinned
+  // threshold sieves (ebc_sieve_*): cached minima per slot
+  DevBuf sv_cm, sv_de, sv_slots, sv_part, sv_out;
+  int sv_nslots = 0;
+  int* sv_slots_host = nullptr;    // pinned staging of the slot lists
+  double* sv_out_host = nullptr;   // pinned staging of the values
   const unsigned char* step_bflag = nullptr;  // enqueue-time: bflag during a lazy step, else nullptr
   DevBuf part_g, part_e, part_r, sel_out, val_out, gain_out, ms_part, ms_off, ms_idx, ms_out;
   // sparse work-matrix path
@@ -1172,7 +1177,7 @@ void free_ctx(ebc_ctx* c) {
                   c->lazy_part, c->ub_next, c->counter3};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, c->stream);
-  DevBuf* bufs[] = {&c->tie_rec, &c->tie_all, &c->sel_hash, &c->ms_tanchor, &c->ms_trad, &c->part_g, &c->part_e, &c->part_a, &c->part_r, &c->rterms, &c->sel_out, &c->val_out, &c->gain_out, &c->ms_part,
+  DevBuf* bufs[] = {&c->tie_rec, &c->tie_all, &c->sel_hash, &c->ms_tanchor, &c->ms_trad, &c->part_g, &c->part_e, &c->part_a, &c->part_r, &c->rterms, &c->sv_cm, &c->sv_de, &c->sv_slots, &c->sv_part, &c->sv_out, &c->sel_out, &c->val_out, &c->gain_out, &c->ms_part,
                     &c->ms_off, &c->ms_idx, &c->ms_out, &c->ms_mbuf, &c->ms_setof, &c->ms_pairs, &c->ms_keys,
                     &c->ms_vals, &c->ms_keys2, &c->ms_vals2, &c->ms_ukeys, &c->ms_uvals, &c->ms_cub};
   void* more[] = {c->pt0, c->ms_count, c->ms_nruns};
@@ -1190,6 +1195,8 @@ void free_ctx(ebc_ctx* c) {
   for (cudaStream_t ss : c->side)
     if (ss) cudaStreamDestroy(ss);
   if (c->mode_host) cudaFreeHost(c->mode_host);
+  if (c->sv_slots_host) cudaFreeHost(c->sv_slots_host);
+  if (c->sv_out_host) cudaFreeHost(c->sv_out_host);
   delete c;
 }
 
@@ -2240,6 +2247,90 @@ int ebc_shard_commit(ebc_ctx* ctx, int64_t s, double* out_value) {
   CU(cudaStreamSynchronize(ctx->stream));
   ctx->steps_done += 1;
   if (out_value) *out_value = v;
+  return EBC_OK;
+}
+
+int ebc_sieve_reserve(ebc_ctx* ctx, int32_t slots) {
+  if (!ctx) return fail(nullptr, EBC_EINVAL, "ebc_sieve_reserve: NULL context");
+  if (slots < 1) return fail(ctx, EBC_EINVAL, "ebc_sieve_reserve: slots must be >= 1");
+  CU(cudaSetDevice(ctx->device));
+  int rc = ensure(ctx, ctx->sv_cm, (size_t)slots * ctx->n_pad * sizeof(double));
+  if (!rc) rc = ensure(ctx, ctx->sv_de, (size_t)ctx->n_pad * sizeof(double));
+  if (!rc) rc = ensure(ctx, ctx->sv_slots, (size_t)3 * (slots + 1) * sizeof(int));
+  if (!rc) rc = ensure(ctx, ctx->sv_part, (size_t)(slots + 1) * ctx->nchunks * sizeof(double));
+  if (!rc) rc = ensure(ctx, ctx->sv_out, (size_t)(slots + 1) * sizeof(double));
+  if (rc) return rc;
+  if (slots > ctx->sv_nslots) {
+    if (ctx->sv_slots_host) cudaFreeHost(ctx->sv_slots_host);
+    if (ctx->sv_out_host) cudaFreeHost(ctx->sv_out_host);
+    ctx->sv_slots_host = nullptr;
+    ctx->sv_out_host = nullptr;
+    CU(cudaMallocHost((void**)&ctx->sv_slots_host, (size_t)3 * (slots + 1) * sizeof(int)));
+    CU(cudaMallocHost((void**)&ctx->sv_out_host, (size_t)(slots + 1) * sizeof(double)));
+    ctx->sv_nslots = slots;
+  }
+  return EBC_OK;
+}
+
+int ebc_sieve_step(ebc_ctx* ctx, int64_t commit_e, const int32_t* commit_slots, int32_t n_commit,
+                   const int32_t* reset_slots, int32_t n_reset, int64_t e, const int32_t* eval_slots,
+                   int32_t n_eval, double* out_single, double* out_values) {
+  if (!ctx) return fail(nullptr, EBC_EINVAL, "ebc_sieve_step: NULL context");
+  if (n_commit < 0 || n_reset < 0 || n_eval < 0 || (n_commit && !commit_slots) || (n_reset && !reset_slots) ||
+      (n_eval && (!eval_slots || !out_values)) || (e >= 0 && !out_single))
+    return fail(ctx, EBC_EINVAL, "ebc_sieve_step: bad slot lists");
+  if (n_commit > ctx->sv_nslots || n_reset > ctx->sv_nslots || n_eval > ctx->sv_nslots)
+    return fail(ctx, EBC_EINVAL, "ebc_sieve_step: more slots than reserved");
+  if (commit_e >= ctx->n || e >= ctx->n)
+    return fail(ctx, EBC_EINDEX, "index " + std::to_string(std::max(commit_e, e)) + " out of range for ground size " +
+                                     std::to_string(ctx->n));
+  int* hs = ctx->sv_slots_host;
+  for (int i = 0; i < n_commit; ++i) hs[i] = commit_slots[i];
+  for (int i = 0; i < n_reset; ++i) hs[n_commit + i] = reset_slots[i];
+  for (int i = 0; i < n_eval; ++i) hs[n_commit + n_reset + i] = eval_slots[i];
+  for (int i = 0; i < n_commit + n_reset + n_eval; ++i)
+    if (hs[i] < 0 || hs[i] >= ctx->sv_nslots) return fail(ctx, EBC_EINVAL, "ebc_sieve_step: slot out of range");
+  CU(cudaSetDevice(ctx->device));
+  ctx->launches = 0;
+  int* ds = (int*)ctx->sv_slots.p;
+  const int tot = n_commit + n_reset + n_eval;
+  if (tot) CU(cudaMemcpyAsync(ds, hs, (size_t)tot * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+  double* cm = (double*)ctx->sv_cm.p;
+  double* de = (double*)ctx->sv_de.p;
+  const size_t smem = (size_t)2 * ctx->d * sizeof(double);
+  const unsigned grid = (unsigned)((ctx->n + RED_THREADS - 1) / RED_THREADS);
+  if (n_commit || n_reset || e >= 0) {
+    if (ctx->dtype == EBC_F64) {
+      CU(cudaFuncSetAttribute(k_sieve_points<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024));
+      k_sieve_points<double><<<grid, RED_THREADS, smem, ctx->stream>>>(ctx->V64, ctx->pitch, ctx->n, ctx->d, ctx->e0d,
+                                                                      cm, ctx->n_pad, n_commit ? commit_e : -1, ds,
+                                                                      n_commit, n_reset, e, de);
+    } else {
+      CU(cudaFuncSetAttribute(k_sieve_points<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024));
+      k_sieve_points<float><<<grid, RED_THREADS, smem, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->n, ctx->d, ctx->e0d,
+                                                                     cm, ctx->n_pad, n_commit ? commit_e : -1, ds,
+                                                                     n_commit, n_reset, e, de);
+    }
+    KCHECK();
+  }
+  if (e < 0) {
+    CU(cudaStreamSynchronize(ctx->stream));
+    return EBC_OK;
+  }
+  double* part = (double*)ctx->sv_part.p;
+  dim3 g2((unsigned)ctx->nchunks, (unsigned)((n_eval + 1 + 7) / 8));
+  k_sieve_sums<<<g2, RED_THREADS, 0, ctx->stream>>>(ctx->n, ctx->e0d, cm, ctx->n_pad, de, ds + n_commit + n_reset,
+                                                   n_eval, ctx->nchunks, part);
+  KCHECK();
+  k_multiset_final<<<(unsigned)((n_eval + 1 + 127) / 128), 128, 0, ctx->stream>>>(part, n_eval + 1, ctx->nchunks,
+                                                                                  1.0 / (double)ctx->n,
+                                                                                  (double*)ctx->sv_out.p);
+  KCHECK();
+  CU(cudaMemcpyAsync(ctx->sv_out_host, ctx->sv_out.p, (size_t)(n_eval + 1) * sizeof(double), cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  *out_single = ctx->sv_out_host[0];
+  for (int i = 0; i < n_eval; ++i) out_values[i] = ctx->sv_out_host[1 + i];
   return EBC_OK;
 }
 

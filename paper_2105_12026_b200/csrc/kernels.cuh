@@ -895,6 +895,83 @@ __global__ void k_window_all(int64_t c0, int64_t c1, const unsigned char* __rest
   }
 }
 
+// ---------------------------------------------------------------- threshold sieves (optimize.py:140-197)
+// Every live sieve r keeps its cached minima cm_r(v) = min over S_r u {e0} of
+// d64(v, .) (N doubles per slot), so a streamed element e costs one distance
+// pass d64(., e) shared by all sieves plus one min/sum pass per sieve, instead
+// of re-evaluating every member of every sieve.  The value of S_r u {e} is
+//   sum_v (e0d(v) - min(cm_r(v), d(v, e))) / N
+// with exactly k_multiset's per-point operations (fmin is exact and order-free)
+// and reduction (4 points per thread in order, block_sum_256, chunk_total,
+// x 1/N), so it is bit-identical to evaluating the set on the work-matrix path.
+
+// Per point: reset the reset slots to S = {} (cm = e0d), fold commit_e into the
+// commit slots, and d_e(v) = d64(v, e) for the evaluation.
+template <typename T>
+__global__ void __launch_bounds__(RED_THREADS) k_sieve_points(const T* __restrict__ V, int pitch, int64_t n, int d,
+                                                              const double* __restrict__ e0d,
+                                                              double* __restrict__ cm, int64_t cstride,
+                                                              int64_t commit_e, const int* __restrict__ slots,
+                                                              int n_commit, int n_reset, int64_t e,
+                                                              double* __restrict__ de) {
+  extern __shared__ double rows[];  // commit row, then e's row (fp64)
+  for (int k = threadIdx.x; k < d; k += blockDim.x) {
+    rows[k] = commit_e >= 0 ? (double)V[commit_e * pitch + k] : 0.0;
+    rows[d + k] = e >= 0 ? (double)V[e * pitch + k] : 0.0;
+  }
+  __syncthreads();
+  const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= n) return;
+  // resets first: a sieve created at the previous element may also have admitted it
+  if (n_reset > 0) {
+    const double b = e0d[v];
+    for (int q = 0; q < n_reset; ++q) cm[(int64_t)slots[n_commit + q] * cstride + v] = b;
+  }
+  if (commit_e >= 0 && n_commit > 0) {
+    const double dc = dist64_row(V + v * pitch, rows, d);
+    for (int q = 0; q < n_commit; ++q) {
+      double* c = cm + (int64_t)slots[q] * cstride + v;
+      *c = fmin(*c, dc);
+    }
+  }
+  if (e >= 0) de[v] = dist64_row(V + v * pitch, rows + d, d);
+}
+
+// part[s][chunk] for the evaluation slots (s = 0: the singleton {e}; s >= 1:
+// S_r u {e} of slot eval[s - 1]), 8 per block row.
+__global__ void __launch_bounds__(RED_THREADS) k_sieve_sums(int64_t n, const double* __restrict__ e0d,
+                                                            const double* __restrict__ cm, int64_t cstride,
+                                                            const double* __restrict__ de,
+                                                            const int* __restrict__ eval, int n_eval, int nchunks,
+                                                            double* __restrict__ part) {
+  __shared__ double sbuf[RED_THREADS];
+  const int ch = blockIdx.x;
+  double acc[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+  const int s0 = blockIdx.y * 8;
+  for (int i = 0; i < RCH / RED_THREADS; ++i) {
+    const int64_t v = (int64_t)ch * RCH + threadIdx.x + (int64_t)i * RED_THREADS;
+    if (v < n) {
+      const double base = e0d[v], dv = de[v];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int sidx = s0 + q;
+        if (sidx <= n_eval) {
+          const double c = sidx == 0 ? base : cm[(int64_t)eval[sidx - 1] * cstride + v];
+          acc[q] += base - fmin(c, dv);
+        }
+      }
+    }
+  }
+#pragma unroll 1
+  for (int q = 0; q < 8; ++q) {
+    if (s0 + q > n_eval) break;  // block-uniform
+    const double bs = block_sum_256(acc[q], sbuf);
+    if (threadIdx.x == 0) part[(int64_t)(s0 + q) * nchunks + ch] = bs;
+  }
+}
+
 // ---------------------------------------------------------------- k-medoids loss (ebc.py:21-43)
 // mins[v] = min over the explicit representatives [r0, r1) of the exact fp64
 // direct distance (core.py:236-251), folded into the running minimum of earlier

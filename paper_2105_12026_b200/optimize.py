@@ -13,7 +13,7 @@ import ctypes
 import math
 import time
 from dataclasses import dataclass
-from typing import Tuple
+from typing import List, Tuple
 
 import numpy as np
 
@@ -136,6 +136,60 @@ def set_timing(f: EbcFunction, on: bool) -> None:
     _native.check(f._lib.ebc_set_timing(f.native_context, 1 if on else 0), f.native_context)
 
 
+class _SieveSlots:
+    """Device slots of the live sieves (ebc_sieve_*): each holds the sieve's
+    cached minima; commits of the previous element and resets of new sieves
+    ride along with the next evaluation call (one round trip per element)."""
+
+    def __init__(self, f: EbcFunction, cap: int):
+        self.f = f
+        self.cap = 0
+        self.free: List[int] = []
+        self.pending_e = -1
+        self.pending_commit: List[int] = []
+        self.pending_reset: List[int] = []
+        self._grow(cap)
+
+    def _grow(self, cap: int) -> None:
+        if cap > self.cap:
+            _native.check(self.f._lib.ebc_sieve_reserve(self.f.native_context, cap), self.f.native_context)
+            self.free.extend(range(self.cap, cap))
+            self.cap = cap
+
+    def new_slot(self) -> int:
+        if not self.free:  # the grid never holds more than log(2k)/log(1+eps) + 2 sieves
+            raise RuntimeError("sieve slots exhausted")
+        slot = self.free.pop()
+        self.pending_reset.append(slot)
+        return slot
+
+    def release(self, slot: int) -> None:
+        if slot in self.pending_reset:
+            self.pending_reset.remove(slot)
+        if slot in self.pending_commit:
+            self.pending_commit.remove(slot)
+        self.free.append(slot)
+
+    def commit(self, slots: List[int], e: int) -> None:
+        self.pending_e = e
+        self.pending_commit = list(slots)
+
+    def _arr(self, xs):
+        return (ctypes.c_int32 * max(1, len(xs)))(*xs)
+
+    def step(self, e: int, eval_slots: List[int]):
+        ce = self.pending_e if self.pending_commit else -1
+        out_single = ctypes.c_double()
+        vals = (ctypes.c_double * max(1, len(eval_slots)))()
+        rc = self.f._lib.ebc_sieve_step(self.f.native_context, ce, self._arr(self.pending_commit),
+                                        len(self.pending_commit), self._arr(self.pending_reset),
+                                        len(self.pending_reset), e, self._arr(eval_slots), len(eval_slots),
+                                        ctypes.byref(out_single), vals)
+        _native.check(rc, self.f.native_context)
+        self.pending_e, self.pending_commit, self.pending_reset = -1, [], []
+        return float(out_single.value), [float(vals[i]) for i in range(len(eval_slots))]
+
+
 def sieve_stream_maximize(stream, f: EbcFunction, k: int, epsilon: float = 0.1) -> Summary:
     """Single-pass threshold-sieve maximization (optimize.py:140-197 contract).
 
@@ -145,9 +199,13 @@ def sieve_stream_maximize(stream, f: EbcFunction, k: int, epsilon: float = 0.1) 
     f(S+e) - f(S) >= (tau/2 - f(S)) / (k - |S|).  The best sieve is returned;
     an empty stream gives an empty summary of value 0.
 
-    Device work per element: one evaluation of {e} and one batched work-matrix
-    evaluation of {S_r u {e}} over every live sieve r that can still admit e
-    (sieve decisions for one element are independent, so they batch).
+    Device work per element (one host round trip, ebc_sieve_step): the previous
+    element folded into the cached minima of the sieves that admitted it, the
+    distance pass d(., e), f({e}) and f(S_r u {e}) for every live sieve that
+    can still admit e -- O(N d + N R) instead of re-evaluating every member.
+    The singleton value is needed before the live set is known (a new maximum
+    moves the threshold grid), so every live sieve is evaluated with it and
+    only those the reference would examine are used.
     """
     if k < 1:
         raise ValueError("k must be >= 1")
@@ -155,37 +213,44 @@ def sieve_stream_maximize(stream, f: EbcFunction, k: int, epsilon: float = 0.1) 
         raise ValueError("epsilon must lie in (0, 1)")
     t0 = time.perf_counter()
     log_base = math.log1p(epsilon)
-    sieves: dict = {}      # exponent -> [threshold, selected, value, gains]
+    sieves: dict = {}      # exponent -> [threshold, selected, value, gains, slot]
     best_single = 0.0
     evaluations = 0
     n = f.ground.n
+    slots = _SieveSlots(f, int(math.log(2.0 * k) / log_base) + 3)
     for raw in stream:
         e = int(raw)
         if not 0 <= e < n:
             raise IndexError(f"index {e} out of range for ground size {n}")
-        single = f.value([e])
+        cand = [ex for ex in sorted(sieves) if len(sieves[ex][1]) < k and e not in sieves[ex][1]]
+        single, vals = slots.step(e, [sieves[ex][4] for ex in cand])
         evaluations += 1
+        by_ex = dict(zip(cand, vals))
         if single > best_single:
             best_single = single
             lo = math.ceil(math.log(best_single) / log_base - 1e-12)
             hi = math.floor(math.log(2.0 * k * best_single) / log_base + 1e-12)
             for ex in [x for x in sieves if x < lo or x > hi]:
-                del sieves[ex]
+                slots.release(sieves.pop(ex)[4])
             for ex in range(lo, hi + 1):
-                sieves.setdefault(ex, [(1.0 + epsilon) ** ex, [], 0.0, []])
+                if ex not in sieves:
+                    sieves[ex] = [(1.0 + epsilon) ** ex, [], 0.0, [], slots.new_slot()]
+                    by_ex[ex] = single  # S = {} : f(S u {e}) = f({e}), bit for bit
         live = [ex for ex in sorted(sieves) if len(sieves[ex][1]) < k and e not in sieves[ex][1]]
         if not live:
             continue
-        values = f.evaluate_multiset(EvalMultiset([sieves[ex][1] + [e] for ex in live]))
         evaluations += len(live)
-        for ex, val in zip(live, values):
+        admitted = []
+        for ex in live:
             sv = sieves[ex]
-            gain = float(val) - sv[2]
+            gain = float(by_ex[ex]) - sv[2]
             need = (sv[0] / 2.0 - sv[2]) / (k - len(sv[1]))
             if gain >= need:
                 sv[1].append(e)
                 sv[2] += gain
                 sv[3].append(gain)
+                admitted.append(sv[4])
+        slots.commit(admitted, e)
     runtime = time.perf_counter() - t0
     if not sieves:
         return Summary(selected=[], value=0.0, gains=[], evaluations=evaluations, runtime_seconds=runtime)

@@ -862,3 +862,52 @@ def test_lazy_stats_report_batch_decided_steps():
                   f.native_context)
     assert out[0] == 1 and out[1] == k - 1
     assert 0 < out[2] <= out[1]  # Gaussian data: most steps decided by the first batch
+
+
+def _sieve_by_multisets(stream, f, k, epsilon):
+    """The threshold sieve of optimize.py:140-197 evaluated set by set on the
+    work-matrix path (the pre-slot implementation): the reference for the
+    cached-minima sieve, which must reproduce it bit for bit."""
+    import math
+    log_base = math.log1p(epsilon)
+    sieves, m, ev = {}, 0.0, 0
+    for e in stream:
+        single = f.value([e])
+        ev += 1
+        if single > m:
+            m = single
+            lo = math.ceil(math.log(m) / log_base - 1e-12)
+            hi = math.floor(math.log(2.0 * k * m) / log_base + 1e-12)
+            for x in [x for x in sieves if x < lo or x > hi]:
+                del sieves[x]
+            for x in range(lo, hi + 1):
+                sieves.setdefault(x, [(1.0 + epsilon) ** x, [], 0.0, []])
+        live = [x for x in sorted(sieves) if len(sieves[x][1]) < k and e not in sieves[x][1]]
+        if not live:
+            continue
+        vals = f.evaluate_multiset(eb.EvalMultiset([sieves[x][1] + [e] for x in live]))
+        ev += len(live)
+        for x, val in zip(live, vals):
+            sv = sieves[x]
+            gain = float(val) - sv[2]
+            if gain >= (sv[0] / 2.0 - sv[2]) / (k - len(sv[1])):
+                sv[1].append(e)
+                sv[2] += gain
+                sv[3].append(gain)
+    best = max((sieves[x] for x in sorted(sieves)), key=lambda sv: sv[2])
+    return best[1], best[2], best[3], ev
+
+
+@pytest.mark.parametrize("kind", ["surrogate", "gauss"])
+def test_sieve_cached_minima_bit_identical_to_multisets(kind):
+    import datasets
+    if kind == "surrogate":
+        X = datasets.surrogate(20_000, 32, 5, 0.01, 7).astype(np.float32)
+    else:
+        X = np.random.default_rng(61).standard_normal((20_000, 48)).astype(np.float32)
+    f = fn(X, eb.Precision.FP32)
+    stream = np.random.default_rng(62).permutation(20_000)[:1500].tolist()
+    stream += stream[:50]  # repeated elements: skipped by the sieves that hold them
+    s = eb.sieve_stream_maximize(stream, f, k=10, epsilon=0.1)
+    sel, val, gains, ev = _sieve_by_multisets(stream, f, 10, 0.1)
+    assert s.selected == sel and s.value == val and s.gains == gains and s.evaluations == ev
