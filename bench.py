@@ -57,6 +57,7 @@ CONFIG_DESC = {
     "C2": "Greedy k=50 EBC, synthetic Gaussian N=100,000 d=100 fp32",
     "C3": "Greedy k=50 EBC, synthetic Gaussian N=100,000 d=100 fp16 storage",
     "C4": "Greedy k=20 EBC, injection-molding surrogate N=500,000 d=32 fp32",
+    "C5": "work-matrix evaluation, 4,096 sets x 10 members, synthetic Gaussian N=200,000 d=64 fp32",
 }
 METRIC = "Greedy EBC point-candidate distance evals/s (wall time & FMA roofline)"
 
@@ -191,6 +192,33 @@ def workload(config: str):
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
+        return 0
+    if args.config == "C5":
+        import oracle
+        X, sets = datasets.c5_problem()
+        threads = len(os.sched_getaffinity(0))
+        oracle.set_threads(threads)
+        V = X.astype(np.float64)
+        rates = []
+        for i in range(args.warmup + args.steps):
+            m = 64 if i < args.warmup else 512
+            t0 = time.perf_counter()
+            oracle.eval_multiset(V, sets[:m])
+            dt = time.perf_counter() - t0
+            if i >= args.warmup:
+                rates.append(X.shape[0] * 10 * m / dt)
+        value = float(np.median(rates))
+        work = float(X.shape[0]) * sum(len(x) for x in sets)
+        print(json.dumps({
+            "impl": "reference", "metric": "work-matrix point-member distance evals/s", "value": value,
+            "unit": "point-member evals/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * work / value, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded Gaussian, tests/golden/datasets.c5_problem)",
+            "config": {"workload": CONFIG_DESC["C5"], "config_id": "C5", "parallelism": "host threads"},
+            "cpu_baseline": {"value": value, "unit": "point-member evals/s", "cores": threads, "kind": "port",
+                             "sample": "first 512 sets of the 4,096 per step"},
+            "e2e": {"value": value, "unit": "point-member evals/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}), flush=True)
         return 0
     X, k = workload(args.config)
     V = X.astype(np.float64)
@@ -363,49 +391,77 @@ def run_ours(args):
         if distributed:
             dist.barrier()
 
-    # per-step CUDA events of the kernel families are captured into the run's
-    # graph, so warm-up (eager run, capture) and the timed replays share one key
-    optimize.set_timing(f, True)
+    def timed(fx, runs, families):
+        """`runs` graph replays of fx, each after an L2 flush, bracketed by
+        barriers + syncs, CUDA events on the library stream."""
+        ms, scr, upd, wk, st, launches, last = [], [], [], [], None, 0, None
+        for _ in range(runs):
+            flush_l2(torch, dev)
+            torch.cuda.synchronize(dev)
+            barrier()
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev0.record(lib_stream)
+            last = one_run(fx)
+            ev1.record(lib_stream)
+            torch.cuda.synchronize(dev)
+            barrier()
+            ms.append(ev0.elapsed_time(ev1))
+            # NCCL path: the whole run is one native call (graph); host-driven
+            # (gloo) path: the count of the last per-step native call
+            launches += optimize.last_launches(fx)
+            if families:
+                t = optimize.last_timings(fx)
+                scr.append(t[0])
+                upd.append(t[2])
+                st = optimize.last_stats(fx)
+                wk.append(optimize.last_screen_work(fx))
+            if ref_sel is not None and last.selected != ref_sel:
+                raise RuntimeError("selection changed between runs")
+        return ms, scr, upd, wk, st, launches, last
+
+    # (a) the product path as a user runs it (lazy steps, no timing events in
+    # the graph): ms_per_step / value
     ref_sel = None
     for _ in range(args.warmup):
         ref_sel = one_run().selected
-
     clocks = ClockSampler(dev_index)
     clocks.start()
-    times_ms, screen_ms, update_ms, launches, work = [], [], [], 0, []
-    stats = None
-    timed_families = (not distributed) or nccl
-    for _ in range(args.steps):
-        flush_l2(torch, dev)
-        torch.cuda.synchronize(dev)
-        barrier()
-        ev0 = torch.cuda.Event(enable_timing=True)
-        ev1 = torch.cuda.Event(enable_timing=True)
-        ev0.record(lib_stream)
-        s = one_run()
-        ev1.record(lib_stream)
-        torch.cuda.synchronize(dev)
-        barrier()
-        times_ms.append(ev0.elapsed_time(ev1))
-        # NCCL path: the whole run is one native call (graph); host-driven
-        # (gloo) path: the count of the last per-step native call
-        launches += optimize.last_launches(f)
-        if timed_families:
-            t = optimize.last_timings(f)
-            screen_ms.append(t[0])
-            update_ms.append(t[2])
-            stats = optimize.last_stats(f)
-            work.append(optimize.last_screen_work(f))
-        if ref_sel is not None and s.selected != ref_sel:
-            raise RuntimeError("selection changed between runs")
+    times_ms, _, _, _, _, launches, s = timed(f, args.steps, False)
     clk = clocks.stop()
+    timed_families = (not distributed) or nccl
+    lazy = optimize.last_lazy_stats(f)
+    # (b) the same runs with per-step family events captured in the graph:
+    # selection vs cached-min update time (update_roofline)
+    optimize.set_timing(f, True)
+    for _ in range(3):
+        one_run()
+    _, sel_ms, update_ms, _, stats, _, _ = timed(f, 2, timed_families)
     optimize.set_timing(f, False)
+    # (c) the dominant kernel's roofline: the tensor screen measured on a
+    # context whose every step screens every candidate (EBC200_LAZY=0; the lazy
+    # run screens fully only at step 0 and in re-screened steps), and that
+    # run's time for reference
+    os.environ["EBC200_LAZY"] = "0"
+    try:
+        fk = eb.EbcFunction(g, device=dev_index)
+    finally:
+        del os.environ["EBC200_LAZY"]
+    optimize.set_timing(fk, True)
+    for _ in range(3):
+        one_run(fk)
+    full_ms, screen_ms, _, work, full_stats, _, sk = timed(fk, 2, timed_families)
+    if sk.selected != s.selected or sk.value != s.value:
+        raise RuntimeError("lazy and full-screen runs disagree")
+    fk.close()
 
     E = evals_per_run(n, k)
     mine = {"step_ms": float(np.mean(times_ms)), "launches": int(launches),
             "screen_ms": float(np.mean(screen_ms)) if screen_ms else None,
             "update_ms": float(np.mean(update_ms)) if update_ms else None,
-            "work": float(np.mean(work)) if work else None, "stats": stats,
+            "sel_ms": float(np.mean(sel_ms)) if sel_ms else None,
+            "full_ms": float(np.mean(full_ms)), "full_stats": full_stats,
+            "work": float(np.mean(work)) if work else None, "stats": stats, "lazy": lazy,
             "selected": s.selected, "value": s.value}
 
     # e2e through the public API from host data: EbcFunction(GroundMatrix) (V
@@ -449,7 +505,9 @@ def run_ours(args):
                    "parallelism": (f"candidate-sharded x{world} ({'NCCL device exchange' if nccl else 'gloo host exchange'})"
                                    if distributed else "1 GPU"),
                    "l2": "flushed (256 MB write) before every timed run; V is 40-64 MB",
-                   "timed_runs": "CUDA-graph replays (per-step family events captured in the graph)"},
+                   "timed_runs": "CUDA-graph replays of the product path (no timing events in the graph); "
+                                 "kernel-family times and the screen roofline from separate event-instrumented "
+                                 "replays"},
         "selected_head": s.selected[:5], "summary_value": s.value,
         "clocks": clk,
         "e2e": {"value": E / (e2e_step * 1e-3), "unit": "point-candidate evals/s", "ms_per_step": e2e_step,
@@ -462,26 +520,156 @@ def run_ours(args):
         line["per_rank_ms_per_step"] = [r["step_ms"] for r in ranks]
     if timed_families and all(r["screen_ms"] for r in ranks):
         info = optimize.screen_info(f)
-        # one GPU's share: the slowest rank's screen over that rank's own pairs
+        # one GPU's share: the slowest rank's screen over that rank's own pairs,
+        # measured on the full-screen (EBC200_LAZY=0) run of the same workload
         slow = max(range(world), key=lambda r: ranks[r]["screen_ms"])
         rr = ranks[slow]
-        rung = rr["stats"][2] if rr["stats"] else -1
+        fst = rr["full_stats"]
+        rung = fst[2] if fst else -1
         e_rank = E / world
-        line["roofline"] = screen_roofline(info, rung, d, rr["work"], rr["screen_ms"], rr["step_ms"], e_rank,
+        line["roofline"] = screen_roofline(info, rung, d, rr["work"], rr["screen_ms"], rr["full_ms"], e_rank,
                                            args.config)
+        line["roofline"]["measured_on"] = ("full-screen run of the same workload (EBC200_LAZY=0: every step screens "
+                                           "every candidate); the product run screens fully at step 0 and in "
+                                           "re-screened lazy steps only")
         if distributed:
             line["roofline"]["rank"] = slow
             line["roofline"]["per_rank_frac"] = [
-                screen_roofline(info, (q["stats"] or [0, 0, -1])[2], d, q["work"], q["screen_ms"], q["step_ms"],
+                screen_roofline(info, (q["full_stats"] or [0, 0, -1])[2], d, q["work"], q["screen_ms"], q["full_ms"],
                                 e_rank, args.config)["frac"] for q in ranks]
         line["window"] = {"sum": rr["stats"][0], "max": rr["stats"][1], "steps": rr["stats"][3]} if rr["stats"] else None
         if rr["update_ms"]:
             line["update_roofline"] = update_roofline(n, d, k, rr["update_ms"])
+    lz = mine["lazy"]
+    line["lazy"] = {
+        "enabled": bool(lz[0]), "lazy_steps": lz[1], "decided_without_screen": lz[2],
+        "candidates_reexamined": lz[3],
+        "full_screen_ms_per_step": max(r["full_ms"] for r in ranks),
+        "speedup_vs_full_screen": max(r["full_ms"] for r in ranks) / step_ms,
+        "rule": "a step re-examines only candidates whose last certified bound (screen upper bound or exact gain) "
+                "can still reach the reference tie window (gains only shrink: f is submodular); selections, values "
+                "and gains are bit-identical to the full-screen run (checked here and in tests)",
+    }
     if not args.no_cpu_baseline:
         threads = len(os.sched_getaffinity(0))
         rate, desc = cpu_sample(X.astype(np.float64), threads, float(os.environ.get("EBC_CPU_SECONDS", "10")))
         line["cpu_baseline"] = {"value": rate, "unit": "point-candidate evals/s", "cores": threads,
                                 "kind": "port", "sample": desc}
+    print(json.dumps(line), flush=True)
+    if distributed:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_multiset(args):
+    """C5: one step = one evaluate_with_backend of the 4,096-set work matrix
+    (batched.py:180-240); N > 1: the sets split across ranks
+    (evaluate_multiset_sharded, fp64 values all-gathered)."""
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    ndev = torch.cuda.device_count()
+    if ndev < 1:
+        raise RuntimeError("bench.py needs a CUDA device (the b200 path has no CPU fallback)")
+    dev_index = local_rank % ndev
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
+    distributed = world > 1
+    if distributed:
+        backend = "nccl" if world <= ndev else "gloo"
+        dist.init_process_group(backend, device_id=dev if backend == "nccl" else None)
+    os.environ["EBC200_DEVICE"] = str(dev_index)
+    import paper_2105_12026_b200 as eb
+    from paper_2105_12026_b200 import optimize
+    from paper_2105_12026_b200.sharded import evaluate_multiset_sharded
+
+    X, sets = datasets.c5_problem()
+    n, d = X.shape
+    g = eb.GroundMatrix(X, eb.Precision.FP32)
+    f = eb.EbcFunction(g, device=dev_index)
+    ms = eb.EvalMultiset(sets)
+    lib_stream = torch.cuda.ExternalStream(f._lib.ebc_stream(f.native_context), device=dev)
+
+    def one(fx=f):
+        return evaluate_multiset_sharded(fx, ms) if distributed else eb.evaluate_with_backend(fx, ms)
+
+    def barrier():
+        if distributed:
+            dist.barrier()
+
+    ref = None
+    for _ in range(args.warmup):
+        ref = one()
+    clocks = ClockSampler(dev_index)
+    clocks.start()
+    times, launches = [], 0
+    for _ in range(args.steps):
+        flush_l2(torch, dev)
+        torch.cuda.synchronize(dev)
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(lib_stream)
+        vals = one()
+        e1.record(lib_stream)
+        torch.cuda.synchronize(dev)
+        barrier()
+        times.append(e0.elapsed_time(e1))
+        launches += optimize.last_launches(f)
+        if not np.array_equal(vals, ref):
+            raise RuntimeError("values changed between runs")
+    clk = clocks.stop()
+    e2e = []
+    for _ in range(max(1, min(args.steps, 3))):
+        barrier()
+        t0 = time.perf_counter()
+        f2 = eb.EbcFunction(g, device=dev_index)
+        one(f2)
+        e2e.append((time.perf_counter() - t0) * 1e3)
+        barrier()
+        f2.close()
+    mine = {"ms": float(np.mean(times)), "e2e": float(np.median(e2e)), "launches": launches}
+    ranks = [mine]
+    if distributed:
+        ranks = [None] * world
+        dist.all_gather_object(ranks, mine)
+    if rank != 0:
+        if distributed:
+            dist.destroy_process_group()
+        return 0
+    ms_step = max(r["ms"] for r in ranks)
+    e2e_step = max(r["e2e"] for r in ranks)
+    work = float(n) * sum(len(x) for x in sets)  # point-member distance evaluations per step
+    line = {
+        "metric": "work-matrix point-member distance evals/s", "value": work / (ms_step * 1e-3),
+        "unit": "point-member evals/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic (seeded Gaussian, tests/golden/datasets.c5_problem)",
+        "config": {"workload": CONFIG_DESC["C5"], "config_id": "C5", "N": n, "d": d, "sets": len(sets),
+                   "members": 10, "parallelism": f"set-sharded x{world}" if distributed else "1 GPU",
+                   "l2": "flushed (256 MB write) before every timed call",
+                   "timed_runs": "whole evaluate_with_backend calls (CSR upload, device work, values back)"},
+        "clocks": clk,
+        "e2e": {"value": work / (e2e_step * 1e-3), "unit": "point-member evals/s", "ms_per_step": e2e_step,
+                "h2d_bytes_per_step": int(X.nbytes + 8 * (len(sets) + 1 + sum(len(x) for x in sets))),
+                "d2h_bytes_per_step": 8 * len(sets)},
+        "gpu_launches": int(sum(r["launches"] for r in ranks)),
+        "roofline": None,
+        "roofline_note": "dominant kernel: the tensor flag screen (profiles/r01_screen_tc_flag_c5_ncu_summary.txt)",
+    }
+    if not args.no_cpu_baseline:
+        import oracle
+        threads = len(os.sched_getaffinity(0))
+        oracle.set_threads(threads)
+        m = 256
+        t0 = time.perf_counter()
+        oracle.eval_multiset(X.astype(np.float64), sets[:m])
+        dt = time.perf_counter() - t0
+        line["cpu_baseline"] = {"value": n * 10 * m / dt, "unit": "point-member evals/s", "cores": threads,
+                                "kind": "port", "sample": f"first {m} sets, {dt:.1f}s"}
     print(json.dumps(line), flush=True)
     if distributed:
         dist.destroy_process_group()
@@ -525,6 +713,8 @@ def main(argv=None):
         return run_reference(args)
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         return spawn_ranks(args, raw)
+    if args.config == "C5":
+        return run_multiset(args)
     return run_ours(args)
 
 

@@ -111,6 +111,14 @@ def last_stats(f: EbcFunction):
     return tuple(int(x) for x in out)
 
 
+def last_lazy_stats(f: EbcFunction):
+    """(lazy steps on, lazy steps, steps decided without a screen, candidates re-examined) of the last run."""
+    out = np.zeros(4, dtype=np.int64)
+    _native.check(f._lib.ebc_last_lazy_stats(f.native_context, out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))),
+                  f.native_context)
+    return tuple(int(x) for x in out)
+
+
 def last_screen_work(f: EbcFunction) -> int:
     """Point-candidate pairs the tensor screen evaluated in the last run (after pruning)."""
     out = np.zeros(1, dtype=np.int64)
