@@ -200,8 +200,10 @@ def _oracle_golden(name):
         return json.load(fh)
 
 
-@pytest.mark.parametrize("name", ["C2", "C3", "C4"])
+@pytest.mark.parametrize("name", ["C2", "C3", "C4", "C4S50"])
 def test_full_config_greedy_vs_oracle(name):
+    """Full-size BASELINE configs against the oracle golden (C4S50: SURVEY
+    §8(d)'s 50-regime near-tie stress case of C4, N=500k, k=20)."""
     import datasets
     gold = _oracle_golden(name)
     X = datasets.config_data(name)
