@@ -36,6 +36,10 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
       : "memory");
 }
 
+#ifndef EBC200_MBAR_SUSPEND_NS
+#define EBC200_MBAR_SUSPEND_NS 0  // measured: no change on the C2 / C4 screens (spins are not the limit)
+#endif
+
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
@@ -48,9 +52,30 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 
+// try_wait with a suspend-time hint: a waiting warp is parked by the hardware
+// until the phase completes (or the hint expires) instead of re-issuing the
+// test -- a spinning producer/MMA warp otherwise takes issue slots from the
+// epilogue warps of its scheduler (ncu, C4 screen: ~80 spins per tile)
+__device__ __forceinline__ bool mbar_try_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(EBC200_MBAR_SUSPEND_NS)
+      : "memory");
+  return ok != 0;
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if EBC200_MBAR_SUSPEND_NS > 0
+  while (!mbar_try_wait_sleep(bar, parity)) {
+  }
+#else
   while (!mbar_try_wait(bar, parity)) {
   }
+#endif
 }
 
 // Bulk copy global -> shared (bytes % 16 == 0, both addresses 16-B aligned);
