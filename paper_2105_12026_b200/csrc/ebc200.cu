@@ -178,6 +178,7 @@ struct ebc_ctx {
   // fused K4 (k_update_fused; false: split K4) and its counters
   // ([0] chunks done, [1..] per-chunk tickets)
   bool uf_on = false;
+  int uf_rows = 256;  // EBC200_UPDATE_ROWS: 64, 128 or 256 rows per fused-update block (measured equal)
   unsigned int* uf_ctr = nullptr;
   double* cur = nullptr;
   int64_t* best = nullptr;
@@ -1035,14 +1036,26 @@ int run_update(ebc_ctx* ctx, int step, double* val_dev, double* gain_dev) {
         ctx->V64, ctx->pitch, ctx->n, ctx->d, ctx->best, ctx->pk, ctx->e0d, ctx->nv32, ctx->cm64, ctx->pt, tc_seeds(ctx), ctx->chunkpart,
         ctx->counter, 1.0 / (double)ctx->n, ctx->cur, val_dev, gain_dev, step);
   } else if (ctx->uf_on) {
-    // fused K4: one launch, one bulk-copied 256-row slice per block, f(S) by
-    // the block that completes the last chunk (DESIGN.md §4 K4)
-    const size_t dsm = (((size_t)ctx->d * 8 + 15) & ~(size_t)15) + (size_t)UF_ROWS * (ctx->pitch * 4 + 16);
-    CU(cudaFuncSetAttribute(k_update_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+    // fused K4: one launch, one bulk-copied slice per block (EBC200_UPDATE_ROWS
+    // rows, 256 by default; 64 and 128 measured the same on C2 and C4), f(S) by
+    // the block that completes the last chunk
+    // (DESIGN.md §4 K4)
+    const size_t head = ((size_t)ctx->d * 8 + 15) & ~(size_t)15;
+    const int rows = ctx->uf_rows;
+    const size_t dsm = head + (size_t)rows * (ctx->pitch * 4 + 16);
     UpdateCounters uc{ctx->uf_ctr + 1, ctx->uf_ctr};
-    k_update_fused<<<(unsigned)((ctx->n + UF_ROWS - 1) / UF_ROWS), UF_ROWS, dsm, ctx->stream>>>(
-        ctx->V32, ctx->pitch, ctx->n, ctx->d, ctx->best, ctx->pk, ctx->e0d, ctx->nv32, ctx->cm64, ctx->pt,
-        tc_seeds(ctx), ctx->terms, ctx->chunkpart, uc, 1.0 / (double)ctx->n, ctx->cur, val_dev, gain_dev, step);
+    const unsigned grid = (unsigned)((ctx->n + rows - 1) / rows);
+    auto go = [&](auto kern) -> int {
+      CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+      kern<<<grid, rows, dsm, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->n, ctx->d, ctx->best, ctx->pk, ctx->e0d,
+                                             ctx->nv32, ctx->cm64, ctx->pt, tc_seeds(ctx), ctx->terms,
+                                             ctx->chunkpart, uc, 1.0 / (double)ctx->n, ctx->cur, val_dev, gain_dev,
+                                             step);
+      return EBC_OK;
+    };
+    const int grc = rows == 64 ? go(k_update_fused<64>) : (rows == 128 ? go(k_update_fused<128>)
+                                                                      : go(k_update_fused<256>));
+    if (grc) return grc;
   } else {
     // split K4: wide streaming pass over V (a), fixed-structure reduction (b)
     const int nb = (int)((ctx->n + RED_THREADS - 1) / RED_THREADS);
@@ -1586,6 +1599,8 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
     // fused K4 when a 256-row slice fits shared memory (pitch <= ~200 floats)
     const size_t dsm = (((size_t)d * 8 + 15) & ~(size_t)15) + (size_t)UF_ROWS * (ctx->pitch * 4 + 16);
     const char* uf_env = getenv("EBC200_UPDATE_FUSED");
+    const char* ur_env = getenv("EBC200_UPDATE_ROWS");
+    if (ur_env && (atoi(ur_env) == 128 || atoi(ur_env) == 256 || atoi(ur_env) == 64)) ctx->uf_rows = atoi(ur_env);
     if (dsm <= 220 * 1024 && !(uf_env && uf_env[0] == '0')) {
       ctx->uf_on = true;
       const size_t cb = (size_t)(1 + ctx->nchunks) * sizeof(unsigned int);

@@ -2048,12 +2048,21 @@ struct UpdateCounters {
   unsigned int* chunks_done;   // 1
 };
 
-__global__ void __launch_bounds__(UF_ROWS) k_update_fused(
+// UFR = rows per slice = threads per block (64, 128 or 256).  Smaller slices
+// mean more, smaller blocks per SM, so one block's copy overlaps another's
+// compute (the 256-row form waits for its 110 KB slice at C2 and runs 1.3
+// waves of 2 blocks per SM).  A chunk's sum is always the 256-thread structure
+// of k_update_reduce: with UFR < 256 every thread plays 256 / UFR of its
+// virtual threads, the same additions in the same order.
+template <int UFR>
+__global__ void __launch_bounds__(UFR) k_update_fused(
     const float* __restrict__ V, int pitch, int64_t n, int d, const int64_t* __restrict__ best, PtCoef pk,
     const double* __restrict__ e0d, const float* __restrict__ nv32, double* __restrict__ cm64,
     float4* __restrict__ pt, TcSeeds seeds, double* __restrict__ terms, double* __restrict__ fpart,
     UpdateCounters ctr, double inv_n, double* __restrict__ cur, double* __restrict__ val_out,
     double* __restrict__ gain_out, int step) {
+  static_assert(RED_THREADS % UFR == 0 && RCH % UFR == 0, "slices tile the chunk reduction");
+  constexpr int VT = RED_THREADS / UFR;  // virtual reduction threads per thread
   extern __shared__ __align__(16) unsigned char uf_smem[];
   __shared__ uint64_t full;
   __shared__ double sbuf[RED_THREADS];
@@ -2065,21 +2074,21 @@ __global__ void __launch_bounds__(UF_ROWS) k_update_fused(
   const int nslices = gridDim.x;
   const int nchunks = (int)((n + RCH - 1) / RCH);
   // rows < n_pad: always a full slice; cm64 / e0d are allocated n_pad long
-  const uint32_t row_bytes = (uint32_t)UF_ROWS * pitch * 4;
+  const uint32_t row_bytes = (uint32_t)UFR * pitch * 4;
   double* cd = reinterpret_cast<double*>(uf_smem);
   unsigned char* stage = uf_smem + (((size_t)d * 8 + 15) & ~(size_t)15);
   if (t == 0) {
     mbar_init(&full, 1);
     fence_mbar_init();
-    mbar_arrive_expect_tx(&full, row_bytes + 2 * UF_ROWS * 8);
-    bulk_g2s(stage, V + (int64_t)id * UF_ROWS * pitch, row_bytes, &full);
-    bulk_g2s(stage + row_bytes, cm64 + (int64_t)id * UF_ROWS, UF_ROWS * 8, &full);
-    bulk_g2s(stage + row_bytes + UF_ROWS * 8, e0d + (int64_t)id * UF_ROWS, UF_ROWS * 8, &full);
+    mbar_arrive_expect_tx(&full, row_bytes + 2 * UFR * 8);
+    bulk_g2s(stage, V + (int64_t)id * UFR * pitch, row_bytes, &full);
+    bulk_g2s(stage + row_bytes, cm64 + (int64_t)id * UFR, UFR * 8, &full);
+    bulk_g2s(stage + row_bytes + UFR * 8, e0d + (int64_t)id * UFR, UFR * 8, &full);
   }
-  for (int k = t; k < d; k += UF_ROWS) cd[k] = (double)V[s * pitch + k];
+  for (int k = t; k < d; k += UFR) cd[k] = (double)V[s * pitch + k];
   __syncthreads();
   mbar_wait(&full, 0);
-  const int64_t v = (int64_t)id * UF_ROWS + t;
+  const int64_t v = (int64_t)id * UFR + t;
   if (v < n) {
     const double dist = dist64_smem_row(reinterpret_cast<const float*>(stage) + (size_t)t * pitch, cd, d);
     double m = reinterpret_cast<const double*>(stage + row_bytes)[t];
@@ -2089,25 +2098,39 @@ __global__ void __launch_bounds__(UF_ROWS) k_update_fused(
       pt[v] = make_pt((float)m, nv32[v], pk);
       if (seeds.ipa) write_seeds(seeds, v, (float)m);
     }
-    terms[v] = reinterpret_cast<const double*>(stage + row_bytes + UF_ROWS * 8)[t] - m;
+    terms[v] = reinterpret_cast<const double*>(stage + row_bytes + UFR * 8)[t] - m;
   }
   __syncthreads();
-  const int c = id / (RCH / UF_ROWS);
+  const int c = id / (RCH / UFR);
   if (t == 0) {
     __threadfence();  // the block's terms (ordered by the barrier) before the ticket
-    const int in_chunk = min(RCH / UF_ROWS, nslices - c * (RCH / UF_ROWS));
+    const int in_chunk = min(RCH / UFR, nslices - c * (RCH / UFR));
     flag = atomicAdd(ctr.chunk_ticket + c, 1u) == (unsigned int)(in_chunk - 1);
   }
   __syncthreads();
   if (!flag) return;
   __threadfence();
-  double acc = 0.0;
+  // virtual thread u = t + q UFR: its 4 points u, u+256, u+512, u+768 in order
 #pragma unroll
-  for (int i = 0; i < RCH / RED_THREADS; ++i) {
-    const int64_t u = (int64_t)c * RCH + t + (int64_t)i * RED_THREADS;
-    if (u < n) acc += __ldcg(terms + u);
+  for (int q = 0; q < VT; ++q) {
+    const int u = t + q * UFR;
+    double acc = 0.0;
+#pragma unroll
+    for (int i = 0; i < RCH / RED_THREADS; ++i) {
+      const int64_t w = (int64_t)c * RCH + u + (int64_t)i * RED_THREADS;
+      if (w < n) acc += __ldcg(terms + w);
+    }
+    sbuf[u] = acc;
   }
-  const double bs = block_sum_256(acc, sbuf);
+  __syncthreads();
+  // block_sum_256's tree over the virtual threads
+#pragma unroll
+  for (int st = RED_THREADS / 2; st > 0; st >>= 1) {
+    for (int u = t; u < st; u += UFR) sbuf[u] += sbuf[u + st];
+    __syncthreads();
+  }
+  const double bs = sbuf[0];
+  __syncthreads();
   if (t == 0) {
     ctr.chunk_ticket[c] = 0u;
     fpart[c] = bs;
@@ -2117,7 +2140,17 @@ __global__ void __launch_bounds__(UF_ROWS) k_update_fused(
   __syncthreads();
   if (!flag) return;
   __threadfence();
-  const double fnew = chunk_total_block(fpart, nchunks, sbuf) * inv_n;
+  // chunk partials left to right (chunk_total_block with this block's width)
+  double fsum = 0.0;
+  for (int c0 = 0; c0 < nchunks; c0 += UFR) {
+    const int m = min(UFR, nchunks - c0);
+    if (t < m) sbuf[t] = __ldcg(fpart + c0 + t);
+    __syncthreads();
+    if (t == 0)
+      for (int i = 0; i < m; ++i) fsum += sbuf[i];
+    __syncthreads();
+  }
+  const double fnew = fsum * inv_n;
   if (t == 0) {
     const double fold = *cur;
     if (val_out) val_out[step] = fnew;
