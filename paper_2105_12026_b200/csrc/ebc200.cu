@@ -41,6 +41,8 @@ struct NcclApi {
   ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
@@ -67,9 +69,11 @@ const NcclApi& nccl_api() {
       api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
       api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
       api.AllGather = (decltype(api.AllGather))dlsym(h, "ncclAllGather");
+      api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
       api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
       api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
-      api.ok = api.GetUniqueId && api.CommInitRank && api.AllGather && api.CommDestroy && api.GetErrorString;
+      api.ok = api.GetUniqueId && api.CommInitRank && api.AllGather && api.AllReduce && api.CommDestroy &&
+               api.GetErrorString;
     }
   }
   return api;
@@ -208,6 +212,8 @@ struct ebc_ctx {
   bool use_cond = true;            // EBC200_GRAPH_COND=0: plain gated kernels in graphs too
   cudaStream_t side[2] = {nullptr, nullptr};  // capture streams of conditional bodies
   bool screen_events_outside = false;  // the step's family events are recorded by the caller
+  bool in_sharded_run = false;     // enqueue-time: inside enqueue_greedy_sharded (lazy steps use the global bound)
+  bool force_global_lb = false;    // EBC200_GLOBAL_LB=1: the all-reduce path even on one rank (tests)
   // eager (uncaptured) lazy steps read the step's mode back (one 4-byte copy
   // into pinned memory) and enqueue only the kernels that will do work
   bool eager_sync = true;          // EBC200_EAGER_SYNC=0: enqueue everything, gated on the device
@@ -951,8 +957,13 @@ int run_step_select(ebc_ctx* ctx, int step, int commit, int64_t* sel_dev) {
   KCHECK();
   const cudaGraphConditionalHandle hrest = cond_handle(ctx);
   const double margin = (double)ctx->n * 1e-12 * std::max(1.0, std::fabs(ctx->baseline)) * 1.01;
+  // device-sharded runs: the batch's bound is all-reduced (max) across the
+  // ranks before the decision, so every rank's stale set is its share of the
+  // single-device one (a rank whose own candidates are all weak would
+  // otherwise re-screen them against its own low bound)
+  const bool global_lb = ctx->in_sharded_run && ctx->comm && (ctx->nranks > 1 || ctx->force_global_lb);
   RefineFinal fb = fin;
-  fb.batch = 1;
+  fb.batch = global_lb ? 2 : 1;
   fb.ub_next = ctx->ub_next;
   fb.margin = margin;
   fb.maxlb = ctx->maxlb;
@@ -961,6 +972,13 @@ int run_step_select(ebc_ctx* ctx, int step, int commit, int64_t* sel_dev) {
   ctx->cmx_fresh = ctx->cmx_valid;  // an earlier step's tile maxima still bound cm (it only decreases)
   rc = ctx->refine2 ? enqueue_refine_short(ctx, ng, fb) : enqueue_refine(ctx, ng, nullptr, fb);
   if (rc) return rc;
+  if (global_lb) {
+    const NcclApi& api = nccl_api();
+    const ncclResult_t r = api.AllReduce(ctx->maxlb, ctx->maxlb, 1, ncclInt64, ncclMax, ctx->comm, ctx->stream);
+    if (r != ncclSuccess) return fail(ctx, EBC_ECOMM, std::string("ncclAllReduce: ") + api.GetErrorString(r));
+    k_lazy_decide<<<1, 32, 0, ctx->stream>>>(ctx->maxlb, ctx->ub_next, margin, ctx->level, ctx->stats, hrest);
+    KCHECK();
+  }
   ctx->cmx_fresh = false;
   const bool sync = !ctx->capturing && ctx->eager_sync;
   auto read_mode = [&]() -> int {
@@ -1107,6 +1125,13 @@ int enqueue_sharded_step(ebc_ctx* ctx, int s, const double2* gathered_host_fed) 
     if (rc) return rc;
   } else {
     CU(cudaMemsetAsync(ctx->wcount, 0, sizeof(int), ctx->stream));
+    if (ctx->lazy_on && s > 0 && ctx->nranks > 1 && !gathered_host_fed) {
+      // the other ranks' lazy steps all-reduce their batch bound: take part with 0
+      CU(cudaMemsetAsync(ctx->maxlb, 0, sizeof(long long), ctx->stream));
+      const NcclApi& api = nccl_api();
+      const ncclResult_t r = api.AllReduce(ctx->maxlb, ctx->maxlb, 1, ncclInt64, ncclMax, ctx->comm, ctx->stream);
+      if (r != ncclSuccess) return fail(ctx, EBC_ECOMM, std::string("ncclAllReduce: ") + api.GetErrorString(r));
+    }
   }
   k_tie_records<<<1, 1024, 0, ctx->stream>>>(ctx->wcount, ctx->wlist, ctx->wgain, 1.0 / (double)ctx->n, ctx->cur,
                                              (double2*)ctx->tie_rec.p);
@@ -1128,7 +1153,9 @@ int enqueue_greedy_sharded(ebc_ctx* ctx, int k) {
   int rc = do_reset(ctx);
   if (rc) return rc;
   CU(cudaMemsetAsync(ctx->tie_err, 0, sizeof(int), ctx->stream));
+  ctx->in_sharded_run = true;
   for (int s = 0; s < k && !rc; ++s) rc = enqueue_sharded_step(ctx, s, nullptr);
+  ctx->in_sharded_run = false;
   if (rc) return rc;
   // consistency guard: every rank must hold the same selection, values and
   // gains; a disagreement (err bit 2) fails the call instead of returning
@@ -1629,6 +1656,8 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
     if (lb && lb[0]) ctx->lazy_batch = std::max(1, std::min(RW, atoi(lb)));
     const char* r2 = getenv("EBC200_REFINE2");
     if (r2 && r2[0] == '0') ctx->refine2 = false;
+    const char* gl = getenv("EBC200_GLOBAL_LB");
+    ctx->force_global_lb = gl && gl[0] == '1';
     const char* es = getenv("EBC200_EAGER_SYNC");
     if (es && es[0] == '0') ctx->eager_sync = false;
     CUC(cudaMallocHost((void**)&ctx->mode_host, sizeof(int)));

@@ -1137,6 +1137,22 @@ __global__ void __launch_bounds__(256) k_lazy_topk(int64_t c0, int64_t c1, const
   }
 }
 
+// Device-sharded lazy step: the decision of the batch refine's finalize, made
+// with the bound all-reduced (max) across the ranks.  Decided (-2): the batch
+// is the rank's window (its exact gains are in wgain; no local pick is needed,
+// the ranks exchange tie-set frontiers of their windows).
+__global__ void k_lazy_decide(const long long* __restrict__ maxlb, const double* __restrict__ ub_next, double margin,
+                              int* __restrict__ level, long long* __restrict__ stats,
+                              cudaGraphConditionalHandle hrest) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    const double lb = dkey_inv(*maxlb);
+    const int done = *ub_next < lb - margin - 1e-9 * fabs(lb);
+    level[0] = done ? -2 : -3;
+    stats[5] += done;
+    if (hrest) cudaGraphSetConditional(hrest, done ? 0u : 1u);
+  }
+}
+
 // Undecided lazy step (level[0] == -3): list the stale candidates
 // ubp[c] >= lb - margin - 1e-9 |lb| (lb = *maxlb, the batch's best exact gain)
 // in slist (count *scount) and flag their 128-candidate blocks.
@@ -1308,6 +1324,16 @@ __device__ void refine_finalize_n(const RefineFinal& F, int wc, const int64_t* _
     __syncthreads();
   }
   top = sred[0];
+  if (F.batch == 2) {  // sharded: the decision waits for the global bound (k_lazy_decide)
+    if (tid == 0) {
+      *F.maxlb = dkey(sred[nt]);
+      F.stats[7] += 1;
+      F.stats[6] += wc;
+      F.level[0] = -3;
+      *F.scount = 0;  // for k_lazy_mark2 if the step stays undecided
+    }
+    return;
+  }
   if (F.batch) {
     __shared__ int sdone;
     if (tid == 0) {

@@ -376,16 +376,26 @@ def _c(arr, ct):
     return arr.ctypes.data_as(ctypes.POINTER(ct))
 
 
-def test_device_exchange_single_rank_matches_greedy():
+@pytest.mark.parametrize("global_lb,data", [(False, "gauss"), (True, "gauss"), (False, "surrogate"),
+                                            (True, "surrogate")])
+def test_device_exchange_single_rank_matches_greedy(monkeypatch, global_lb, data):
     """ebc_greedy_sharded over a one-rank NCCL communicator (the plumbing a
     multi-GPU run uses: tie-set records, ncclAllGather inside the step, device
-    pick, graph capture on the second run) reproduces ebc_greedy bit for bit."""
+    pick, graph capture on the second run; with global_lb the lazy steps'
+    ncclAllReduce of the batch bound and the separate decision kernel)
+    reproduces ebc_greedy bit for bit."""
     import ctypes
+    import datasets
     from paper_2105_12026_b200 import _native
     from paper_2105_12026_b200.sharded import greedy_device_exchange
-    X = np.random.default_rng(17).standard_normal((6000, 40)).astype(np.float32)
-    X[5000] = X[12]  # an exact tie
+    if data == "gauss":
+        X = np.random.default_rng(17).standard_normal((6000, 40)).astype(np.float32)
+        X[5000] = X[12]  # an exact tie
+    else:
+        X = datasets.surrogate(20_000, 32, 5, 0.01, 9).astype(np.float32)
     single = eb.greedy_maximize(fn(X, eb.Precision.FP32), eb.OptimizerBudget(k=10))
+    if global_lb:
+        monkeypatch.setenv("EBC200_GLOBAL_LB", "1")
     f = fn(X, eb.Precision.FP32)
     lib = f._lib
     nb = int(lib.ebc_comm_id_bytes())
