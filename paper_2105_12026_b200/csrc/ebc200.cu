@@ -199,7 +199,8 @@ struct ebc_ctx {
   int lazy_cap = 256;              // EBC200_LAZY_CAP: stale candidates decided by the exact refine alone
   bool ubp_seeded = false;         // enqueue-time: a full step has run since the reset
   bool cmx_valid = false;          // enqueue-time: cmx computed since the reset (an upper bound of cm's tile maxima)
-  int64_t* slist = nullptr;        // n: this step's stale candidates (k_lazy_mark2)
+  int64_t* slist = nullptr;        // n: this step's stale candidates in index order (k_lazy_write)
+  int* bcnt = nullptr;             // ceil(n / 256) + 1: per-block stale counts, then offsets
   int* scount = nullptr;
   void* lazy_part = nullptr;       // 2 num_sms x TK 64-bit keys: k_lazy_topk's block lists
   double* ub_next = nullptr;       // best stale bound outside the first batch
@@ -214,6 +215,13 @@ struct ebc_ctx {
   bool screen_events_outside = false;  // the step's family events are recorded by the caller
   bool in_sharded_run = false;     // enqueue-time: inside enqueue_greedy_sharded (lazy steps use the global bound)
   bool force_global_lb = false;    // EBC200_GLOBAL_LB=1: the all-reduce path even on one rank (tests)
+  // gathered lazy re-screens (kernels.cuh k_lazy_plan2): the stale set packed
+  // into fresh 128-candidate blocks when the flagged blocks are sparse
+  bool gather_on = false;          // EBC200_GATHER=0: always re-screen the flagged blocks
+  int64_t gath_cap = 0;            // candidates a gathered re-screen holds
+  float* Vg = nullptr;             // gath_cap x pitch
+  int* g_anchor = nullptr;         // per gathered block
+  float* g_rad = nullptr;
   // eager (uncaptured) lazy steps read the step's mode back (one 4-byte copy
   // into pinned memory) and enqueue only the kernels that will do work
   bool eager_sync = true;          // EBC200_EAGER_SYNC=0: enqueue everything, gated on the device
@@ -796,6 +804,90 @@ int run_screen_window(ebc_ctx* ctx, int eb, int fin_blocks) {
 
 // One step's candidate screen + certified window + exact refine + pick.
 // commit: single-device mode (mark the winner, record it as step `step`).
+// Gathered lazy re-screen (level[0] == L_GATHER): the stale candidates packed
+// into gath_cap rows, their own block anchors and radii, the split-rung tensor
+// screen over them (no all-positive aggregates), bounds per slot, then the
+// usual argmax -> exact top gain -> window chain.  Every kernel is gated on
+// L_GATHER (eager runs) and the whole section sits in a conditional node
+// (captured runs).
+template <int NP, int KIND>
+int launch_tc_gathered_t(ebc_ctx* ctx, const TcPlan& p) {
+  auto kern = k_screen_tc<NP, KIND>;
+  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
+  TcAnchors an{ctx->anchors, ctx->pitch, ctx->g_anchor, ctx->pttc, ctx->n_pad, ctx->kpmax, ctx->tc_ntl,
+               ctx->tc_vmax, ctx->tc_kc, ctx->tc_kx, p.list_cap ? ctx->rho : nullptr, ctx->g_rad, ctx->cmx,
+               p.list_cap, p.kq_cap, (unsigned long long*)(ctx->stats + 4)};
+  an.ncand_dev = ctx->scount;
+  dim3 grid(p.ncb, p.nsplit);
+  kern<<<grid, tc::THREADS, p.smem, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->d, (const unsigned char*)ctx->Vhi,
+                                                   (const unsigned char*)ctx->Vlo, an, ctx->kpad, p.stages, 0,
+                                                   p.ntiles, p.tps, (double*)ctx->part_g.p, (float*)ctx->part_e.p,
+                                                   ctx->n_pad, ctx->level, L_GATHER, ctx->Vg, FlagOut{});
+  KCHECK();
+  return EBC_OK;
+}
+
+int run_gathered_window(ebc_ctx* ctx, int fin_blocks) {
+  TcPlan gp{};
+  const int64_t s0 = ctx->c0, s1 = ctx->c1;
+  ctx->c0 = 0;
+  ctx->c1 = ctx->gath_cap;
+  const bool ok = plan_tc(ctx, gp, ctx->tc_kind);
+  ctx->c0 = s0;
+  ctx->c1 = s1;
+  if (!ok) return fail(ctx, EBC_ECUDA, "gathered re-screen: no tensor plan");
+  int rc = ensure(ctx, ctx->part_g, (size_t)gp.nsplit * ctx->n_pad * sizeof(double));
+  if (!rc) rc = ensure(ctx, ctx->part_e, (size_t)gp.nsplit * ctx->n_pad * sizeof(float));
+  if (rc) return rc;
+  const int64_t ncand = ctx->c1 - ctx->c0;
+  // tile maxima of the current cached minima (pruning)
+  k_tile_cmmax<<<(unsigned)((ctx->tc_ntl * 32 + 255) / 256), 256, 0, ctx->stream>>>(ctx->cm64, ctx->n, ctx->tc_ntl,
+                                                                                  ctx->tc_np, ctx->cmx, nullptr);
+  KCHECK();
+  k_gather_rows<<<8 * ctx->num_sms, 256, 0, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->slist, ctx->scount,
+                                                          (int)ctx->gath_cap, ctx->Vg, ctx->ub, ncand, ctx->level,
+                                                          L_GATHER);
+  KCHECK();
+  k_tile_anchor<<<(unsigned)(ctx->gath_cap / tc::M), 128, 0, ctx->stream>>>(ctx->Vg, ctx->pitch, ctx->gath_cap, ctx->d,
+                                                                          ctx->anchors, ctx->pitch, ctx->tc_na,
+                                                                          ctx->g_anchor, ctx->g_rad, ctx->scount,
+                                                                          ctx->level, L_GATHER);
+  KCHECK();
+  switch (ctx->tc_kind) {
+    case tc::KIND_BF16:
+      rc = ctx->tc_np == 128 ? launch_tc_gathered_t<128, tc::KIND_BF16>(ctx, gp)
+                             : launch_tc_gathered_t<64, tc::KIND_BF16>(ctx, gp);
+      break;
+    default:
+      rc = ctx->tc_np == 128 ? launch_tc_gathered_t<128, tc::KIND_TF32>(ctx, gp)
+                             : launch_tc_gathered_t<64, tc::KIND_TF32>(ctx, gp);
+  }
+  if (rc) return rc;
+  const double u = 5.960464477539063e-08;
+  const double nterms = (double)gp.tps * ctx->tc_np;
+  const double einfl = 1.0 + 2.0 * (nterms + 64.0) * u + 1.0 / 64.0;
+  const double gcoef = (32 + 8) * u;
+  k_finalize_gathered<<<(unsigned)((ctx->gath_cap + 255) / 256), 256, 0, ctx->stream>>>(
+      ctx->scount, ctx->slist, ctx->c0, gp.nsplit, (const double*)ctx->part_g.p, (const float*)ctx->part_e.p,
+      ctx->n_pad, einfl, gcoef, 2.0, ctx->selected, ctx->ub, ctx->ubp, ctx->level, L_GATHER);
+  KCHECK();
+  const int ag = (int)std::max<int64_t>(1, std::min<int64_t>(2 * ctx->num_sms, (ncand + 1023) / 1024));
+  k_argmax_ub<<<ag, 256, 0, ctx->stream>>>(ctx->c0, ctx->c1, ctx->ub, ctx->topc, ctx->toppart, ctx->counter2,
+                                          ctx->level, L_GATHER);
+  KCHECK();
+  const size_t smem = (size_t)ctx->d * sizeof(double);
+  CU(cudaFuncSetAttribute(k_gain_top<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024));
+  k_gain_top<float><<<(unsigned)((ctx->n + RED_THREADS - 1) / RED_THREADS), RED_THREADS, smem, ctx->stream>>>(
+      ctx->V32, ctx->pitch, ctx->n, ctx->d, ctx->cm64, ctx->topc, ctx->toppart, ctx->counter2, ctx->maxlb,
+      ctx->level, L_GATHER);
+  KCHECK();
+  const double margin = (double)ctx->n * 1e-12 * std::max(1.0, std::fabs(ctx->baseline)) * 1.01;
+  k_window<<<fin_blocks, 256, 0, ctx->stream>>>(ctx->c0, ctx->c1, ctx->ub, ctx->maxlb, margin, ctx->wcount,
+                                               ctx->wlist, ctx->level, L_GATHER);
+  KCHECK();
+  return EBC_OK;
+}
+
 // Exact fp64 gains of the window (wcount / wlist) into part_r, then the pick
 // in the refine's last block (fin); skip_level: the kernel exits when it reads
 // -2 there (lazy step decided by the first batch).
@@ -995,17 +1087,42 @@ int run_step_select(ebc_ctx* ctx, int step, int commit, int64_t* sel_dev) {
     CU(ca.open(ctx, hrest, 0));
     CU(cudaMemsetAsync(ctx->bflag, 0, (size_t)((ncand + tc::M - 1) / tc::M + 2), ctx->stream));
     k_lazy_mark2<<<fin_blocks, 256, 0, ctx->stream>>>(ctx->c0, ctx->c1, ctx->ubp, ctx->selected, ctx->maxlb,
-                                                      margin, ctx->scount, ctx->slist, ctx->bflag, ctx->level);
+                                                      margin, ctx->bcnt, ctx->bflag, ctx->level);
+    KCHECK();
+    k_lazy_scan<<<1, 1024, 0, ctx->stream>>>(ctx->bcnt, fin_blocks, ctx->scount, ctx->level);
+    KCHECK();
+    k_lazy_write<<<fin_blocks, 256, 0, ctx->stream>>>(ctx->c0, ctx->c1, ctx->ubp, ctx->selected, ctx->maxlb,
+                                                      margin, ctx->bcnt, ctx->slist, ctx->level);
     KCHECK();
     const cudaGraphConditionalHandle hs = has_screen ? cond_handle(ctx) : 0;
+    const bool can_gather = has_screen && ctx->gather_on && ctx->ladder_max >= L_TC;
+    const cudaGraphConditionalHandle hg = can_gather ? cond_handle(ctx) : 0;
     k_lazy_plan2<<<1, 256, 0, ctx->stream>>>(ctx->scount, ctx->slist, has_screen ? ctx->lazy_cap : INT_MAX,
-                                             ctx->wcount, ctx->wlist, ctx->level, ctx->stats, hs);
+                                             ctx->wcount, ctx->wlist, ctx->level, ctx->stats, hs, ctx->bflag,
+                                             (int)((ncand + tc::M - 1) / tc::M),
+                                             can_gather ? (int)ctx->gath_cap : 0, (int)L_TC, hg);
     KCHECK();
     if (sync) {
       mode = read_mode();
       if (mode == -4) return fail(ctx, EBC_ECUDA, "lazy step: mode read-back failed");
+      if (getenv("EBC200_LAZY_TRACE")) {  // development aid: stale-set shape per eager lazy step
+        int cnt = 0;
+        std::vector<unsigned char> fl((size_t)((ncand + tc::M - 1) / tc::M));
+        cudaMemcpy(&cnt, ctx->scount, sizeof(int), cudaMemcpyDeviceToHost);
+        cudaMemcpy(fl.data(), ctx->bflag, fl.size(), cudaMemcpyDeviceToHost);
+        size_t nb = 0;
+        for (unsigned char b : fl) nb += b != 0;
+        fprintf(stderr, "[lazy] step %d mode %d stale %d blocks %zu of %zu\n", step, mode, cnt, nb, fl.size());
+      }
     }
-    if (has_screen && mode != -1) {
+    if (can_gather && (mode == -3 || mode == L_GATHER)) {
+      CondScope cg;
+      CU(cg.open(ctx, hg, 1));
+      rc = run_gathered_window(ctx, fin_blocks);
+      if (rc) return rc;
+      CU(cg.close());
+    }
+    if (has_screen && mode != -1 && mode != L_GATHER) {
       CondScope cb;
       CU(cb.open(ctx, hs, 1));
       ctx->step_bflag = ctx->bflag;
@@ -1214,7 +1331,7 @@ void free_ctx(ebc_ctx* c) {
   cudaSetDevice(c->device);
   void* ptrs[] = {c->V32, c->V64, c->e0d, c->cm64, c->pt, c->nv32, c->level, c->stats, c->Vhi, c->Vlo, c->Vf, c->tile_anchor0, c->rhomax, c->cmn, c->vsum, c->vsn, c->ipsum, c->rhomin, c->agg_any, c->pttc, c->kpmax, c->anchors, c->nva, c->tile_anchor, c->tc_vmax, c->fps_keys, c->ipa0, c->tile_rad, c->crad, c->rho, c->cmx, c->cmx0, c->selected, c->chunkpart, c->counter, c->counter2, c->topc, c->toppart, c->terms, c->cur, c->best, c->uf_ctr,
                   c->maxlb, c->wcount, c->wlist, c->wgain, c->ub, c->ubp, c->bflag, c->slist, c->scount,
-                  c->lazy_part, c->ub_next, c->counter3};
+                  c->lazy_part, c->ub_next, c->counter3, c->bcnt, c->Vg, c->g_anchor, c->g_rad};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, c->stream);
   DevBuf* bufs[] = {&c->tie_rec, &c->tie_all, &c->sel_hash, &c->ms_tanchor, &c->ms_trad, &c->part_g, &c->part_e, &c->part_a, &c->part_r, &c->rterms, &c->sv_cm, &c->sv_de, &c->sv_slots, &c->sv_part, &c->sv_out, &c->sel_out, &c->val_out, &c->gain_out, &c->ms_part,
@@ -1647,6 +1764,7 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
   CUC(cudaMallocAsync((void**)&ctx->bflag, (size_t)((n + tc::M - 1) / tc::M + 2), ctx->stream));
   CUC(cudaMallocAsync((void**)&ctx->slist, (size_t)n * sizeof(int64_t), ctx->stream));
   CUC(cudaMallocAsync((void**)&ctx->scount, sizeof(int), ctx->stream));
+  CUC(cudaMallocAsync((void**)&ctx->bcnt, (size_t)((n + 255) / 256 + 1) * sizeof(int), ctx->stream));
   CUC(cudaMallocAsync(&ctx->lazy_part, (size_t)2 * ctx->num_sms * TK * sizeof(unsigned long long), ctx->stream));
   CUC(cudaMallocAsync((void**)&ctx->ub_next, sizeof(double), ctx->stream));
   CUC(cudaMallocAsync((void**)&ctx->counter3, sizeof(unsigned int), ctx->stream));
@@ -1669,6 +1787,15 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
     ctx->lazy_on = !(lz && lz[0] == '0');
     const char* lc = getenv("EBC200_LAZY_CAP");
     if (lc && lc[0]) ctx->lazy_cap = std::max(0, atoi(lc));
+    const char* ge = getenv("EBC200_GATHER");
+    ctx->gather_on = ctx->lazy_on && ctx->tc_np && ctx->screen_mode == 3 && !ctx->tc_fast &&
+                     (ctx->tc_kind == tc::KIND_BF16 || ctx->tc_kind == tc::KIND_TF32) && !(ge && ge[0] == '0');
+    if (ctx->gather_on) {
+      ctx->gath_cap = std::min<int64_t>((n + tc::M - 1) / tc::M * tc::M, 65536);
+      CUC(cudaMallocAsync((void**)&ctx->Vg, (size_t)ctx->gath_cap * ctx->pitch * sizeof(float), ctx->stream));
+      CUC(cudaMallocAsync((void**)&ctx->g_anchor, (size_t)(ctx->gath_cap / tc::M + 1) * sizeof(int), ctx->stream));
+      CUC(cudaMallocAsync((void**)&ctx->g_rad, (size_t)(ctx->gath_cap / tc::M + 1) * sizeof(float), ctx->stream));
+    }
   }
   double* e0dev = nullptr;
   CUC(cudaMallocAsync((void**)&e0dev, (size_t)d * sizeof(double), ctx->stream));

@@ -1156,26 +1156,81 @@ __global__ void k_lazy_decide(const long long* __restrict__ maxlb, const double*
 // Undecided lazy step (level[0] == -3): list the stale candidates
 // ubp[c] >= lb - margin - 1e-9 |lb| (lb = *maxlb, the batch's best exact gain)
 // in slist (count *scount) and flag their 128-candidate blocks.
+// The stale set in INDEX ORDER (three passes: per-256-block counts, one-block
+// scan, ordered writes) -- a gathered re-screen packs neighbouring candidates
+// into the same 128-candidate block, which keeps the block anchors close and
+// the tile pruning effective.
+__device__ __forceinline__ bool lazy_is_stale(int64_t c, int64_t c0, int64_t c1, const double* __restrict__ ubp,
+                                              const unsigned char* __restrict__ selected, double thr) {
+  return c < c1 && !selected[c] && ubp[c - c0] >= thr;
+}
+
 __global__ void __launch_bounds__(256) k_lazy_mark2(int64_t c0, int64_t c1, const double* __restrict__ ubp,
                                                     const unsigned char* __restrict__ selected,
                                                     const long long* __restrict__ maxlb, double margin,
-                                                    int* __restrict__ scount, int64_t* __restrict__ slist,
-                                                    unsigned char* __restrict__ bflag, const int* __restrict__ level) {
+                                                    int* __restrict__ bcnt, unsigned char* __restrict__ bflag,
+                                                    const int* __restrict__ level) {
+  __shared__ int wsum[8];
   if (*level != -3) return;
   const double lb = dkey_inv(*maxlb);
+  const double thr = lb - margin - 1e-9 * fabs(lb);
   const int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int lane = threadIdx.x & 31;
-  bool stale = false;
-  if (c < c1 && !selected[c]) stale = ubp[c - c0] >= lb - margin - 1e-9 * fabs(lb);
+  const bool stale = lazy_is_stale(c, c0, c1, ubp, selected, thr);
+  if (stale) bflag[(c - c0) >> 7] = 1;
   const unsigned bal = __ballot_sync(0xffffffffu, stale);
-  if (!bal) return;
-  int base = 0;
-  if (lane == 0) base = atomicAdd(scount, __popc(bal));
-  base = __shfl_sync(0xffffffffu, base, 0);
-  if (stale) {
-    slist[base + __popc(bal & ((1u << lane) - 1u))] = c;
-    bflag[(c - c0) >> 7] = 1;
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = __popc(bal);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int w = 0; w < 8; ++w) t += wsum[w];
+    bcnt[blockIdx.x] = t;
   }
+}
+
+__global__ void __launch_bounds__(1024) k_lazy_scan(int* __restrict__ bcnt, int nb, int* __restrict__ scount,
+                                                    const int* __restrict__ level) {
+  __shared__ int sx[1024];
+  __shared__ int carry;
+  if (*level != -3) return;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int b0 = 0; b0 < nb; b0 += 1024) {
+    const int b = b0 + threadIdx.x;
+    const int x = b < nb ? bcnt[b] : 0;
+    sx[threadIdx.x] = x;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {  // inclusive scan (Hillis-Steele)
+      const int y = threadIdx.x >= o ? sx[threadIdx.x - o] : 0;
+      __syncthreads();
+      sx[threadIdx.x] += y;
+      __syncthreads();
+    }
+    if (b < nb) bcnt[b] = carry + sx[threadIdx.x] - x;  // exclusive offset, in place
+    __syncthreads();
+    if (threadIdx.x == 0) carry += sx[1023];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *scount = carry;
+}
+
+__global__ void __launch_bounds__(256) k_lazy_write(int64_t c0, int64_t c1, const double* __restrict__ ubp,
+                                                    const unsigned char* __restrict__ selected,
+                                                    const long long* __restrict__ maxlb, double margin,
+                                                    const int* __restrict__ boff, int64_t* __restrict__ slist,
+                                                    const int* __restrict__ level) {
+  __shared__ int wsum[8];
+  if (*level != -3) return;
+  const double lb = dkey_inv(*maxlb);
+  const double thr = lb - margin - 1e-9 * fabs(lb);
+  const int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool stale = lazy_is_stale(c, c0, c1, ubp, selected, thr);
+  const unsigned bal = __ballot_sync(0xffffffffu, stale);
+  if (lane == 0) wsum[warp] = __popc(bal);
+  __syncthreads();
+  int off = boff[blockIdx.x];
+  for (int w = 0; w < warp; ++w) off += wsum[w];
+  if (stale) slist[off + __popc(bal & ((1u << lane) - 1u))] = c;
 }
 
 // Mode of an undecided lazy step (level[0] == -3), written to level[0]:
@@ -1184,23 +1239,85 @@ __global__ void __launch_bounds__(256) k_lazy_mark2(int64_t c0, int64_t c1, cons
 //   rung  many: the flagged blocks are re-screened and the screen builds the
 //       window (hs: the screen's conditional graph node, when captured).
 // stats: [5] lazy steps decided without a screen, [6] candidates re-examined.
+constexpr int L_GATHER = 8;  // level[0] of a gathered re-screen (matches no rung: the block screens skip)
 __global__ void __launch_bounds__(256) k_lazy_plan2(const int* __restrict__ scount,
                                                     const int64_t* __restrict__ slist, int cap,
                                                     int* __restrict__ wcount, int64_t* __restrict__ wlist,
                                                     int* __restrict__ level, long long* __restrict__ stats,
-                                                    cudaGraphConditionalHandle hs) {
+                                                    cudaGraphConditionalHandle hs,
+                                                    const unsigned char* __restrict__ bflag = nullptr, int nblocks = 0,
+                                                    int gather_cap = 0, int gather_rung = -1,
+                                                    cudaGraphConditionalHandle hg = 0) {
+  __shared__ int nfl;
   if (level[0] != -3) return;
   const int cnt = *scount;
   const bool few = cnt <= cap;
   if (few)
     for (int i = threadIdx.x; i < cnt; i += blockDim.x) wlist[i] = slist[i];
+  // gathered re-screen: the stale set compacted into fresh 128-candidate blocks
+  // when the flagged blocks are less than half full (scattered stale sets)
+  if (threadIdx.x == 0) nfl = 0;
+  __syncthreads();
+  bool gather = false;
+  if (!few && gather_cap > 0 && cnt <= gather_cap && level[1] == gather_rung) {
+    int m = 0;
+    for (int b = threadIdx.x; b < nblocks; b += blockDim.x) m += bflag[b] != 0;
+    atomicAdd(&nfl, m);
+    __syncthreads();
+    gather = (int64_t)nfl * 128 > 2 * (int64_t)cnt;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     stats[6] += cnt;
     stats[5] += few ? 1 : 0;  // decided without a screen
-    level[0] = few ? -1 : level[1];
+    level[0] = few ? -1 : (gather ? L_GATHER : level[1]);
     *wcount = few ? cnt : 0;
-    if (hs) cudaGraphSetConditional(hs, few ? 0u : 1u);
+    if (hs) cudaGraphSetConditional(hs, (few || gather) ? 0u : 1u);
+    if (hg) cudaGraphSetConditional(hg, gather ? 1u : 0u);
+  }
+}
+
+// Gathered re-screen: the stale candidates' rows packed into Vg (rows past the
+// count up to the block boundary zeroed), ub = -inf for every candidate (the
+// gathered finalize writes the re-screened ones).
+__global__ void k_gather_rows(const float* __restrict__ V32, int pitch, const int64_t* __restrict__ slist,
+                              const int* __restrict__ scount, int cap, float* __restrict__ Vg,
+                              double* __restrict__ ub, int64_t ncand, const int* __restrict__ level_now, int level) {
+  if (*level_now != level) return;
+  const int cnt = min(*scount, cap);
+  const int64_t rows = ((int64_t)cnt + 127) / 128 * 128;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows * pitch; i += stride) {
+    const int64_t r = i / pitch;
+    const int k = (int)(i - r * pitch);
+    Vg[i] = r < cnt ? V32[slist[r] * pitch + k] : 0.f;
+  }
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < ncand; c += stride) ub[c] = -INFINITY;
+}
+
+// Bounds of the gathered candidates (k_finalize's ub-only formula per slot).
+__global__ void k_finalize_gathered(const int* __restrict__ scount, const int64_t* __restrict__ slist, int64_t c0,
+                                    int nsplit, const double* __restrict__ part_g, const float* __restrict__ part_e,
+                                    int64_t part_stride, double einfl, double gcoef, double gscale,
+                                    const unsigned char* __restrict__ selected, double* __restrict__ ub,
+                                    double* __restrict__ ubp, const int* __restrict__ level_now, int level) {
+  if (*level_now != level) return;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= *scount) return;
+  const int64_t c = slist[i];
+  double g = 0.0, e = 0.0;
+  for (int s = 0; s < nsplit; ++s) {
+    g += part_g[s * part_stride + i];
+    e += (double)part_e[s * part_stride + i];
+  }
+  g *= gscale;
+  e *= gscale;
+  const double eps = e * einfl + gcoef * g + 1e-300;
+  if (selected[c]) {
+    ub[c - c0] = -INFINITY;
+  } else {
+    ub[c - c0] = g + eps;
+    ubp[c - c0] = fmin(ubp[c - c0], g + eps);
   }
 }
 
@@ -1279,7 +1396,7 @@ struct RefineFinal {
   const double* ub_next = nullptr;
   double margin = 0.0;
   long long* maxlb = nullptr;
-  int* scount = nullptr;                 // zeroed for the undecided path's k_lazy_mark2
+  int* scount = nullptr;                 // zeroed for the undecided path
   cudaGraphConditionalHandle hrest = 0;  // the undecided-step conditional node (graph capture)
 };
 
@@ -1330,7 +1447,7 @@ __device__ void refine_finalize_n(const RefineFinal& F, int wc, const int64_t* _
       F.stats[7] += 1;
       F.stats[6] += wc;
       F.level[0] = -3;
-      *F.scount = 0;  // for k_lazy_mark2 if the step stays undecided
+      *F.scount = 0;  // for the undecided path
     }
     return;
   }

@@ -402,7 +402,12 @@ __global__ void k_nva(const float* __restrict__ V32, int pitch, int64_t n, int d
 // Per 128-candidate block: the anchor minimising max_c |c - mu_a|^2 (ties: lower a).
 __global__ void k_tile_anchor(const float* __restrict__ V32, int pitch, int64_t n, int d,
                               const float* __restrict__ anchors, int apitch, int na, int* __restrict__ tile_anchor,
-                              float* __restrict__ tile_rad) {
+                              float* __restrict__ tile_rad, const int* __restrict__ n_dev = nullptr,
+                              const int* __restrict__ level_now = nullptr, int level = 0) {
+  // n_dev: a device-side row count (gathered lazy re-screens; blocks past it exit)
+  if (level_now && *level_now != level) return;
+  if (n_dev) n = min(n, (int64_t)*n_dev);
+  if ((int64_t)blockIdx.x * 128 >= n) return;
   __shared__ float wmax[4];
   const int64_t c = (int64_t)blockIdx.x * 128 + threadIdx.x;
   float best = INFINITY;
@@ -620,6 +625,7 @@ struct TcAnchors {
   // lazy step (kernels.cuh k_lazy_mark): screen only the 128-candidate blocks
   // flagged here (nullptr: every block); indexed by (crow - cand0) >> 7
   const unsigned char* bflag = nullptr;
+  const int* ncand_dev = nullptr;  // gathered candidates (Vc rows): CTAs of blocks past the count exit
 };
 
 // One CTA: candidates [cand0 + 128*bx, +128) x V tiles [t0, t1) of NP points.
@@ -675,6 +681,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     const int64_t b0 = (int64_t)blockIdx.x * MB;
     if (!an.bflag[b0] && (MB == 1 || !an.bflag[b0 + 1])) return;
   }
+  if (an.ncand_dev && crow >= (int64_t)*an.ncand_dev) return;
 
   if (tid == 0) {
     for (int s = 0; s < stages; ++s) {
@@ -811,7 +818,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     float cn2 = 0.f, mc = 0.f, mn2 = 0.f;
     {
       // A of this candidate into TMEM: slice 0 writes hi [0,128), the last slice lo [128,256)
-      const float* row = (FLAG ? Vc : V32) + c * pitch;
+      const float* row = (Vc ? Vc : V32) + c * pitch;  // Vc: gathered candidate rows
       const bool do_hi = MB == 2 || half == 0, do_lo = TM::PARTS == 2 && half == EPI_WARPGROUPS - 1;
       auto cprime = [&](int k) -> float {  // c' = fl(c - mu), accumulating |c'|^2, mu.c', |mu|^2
         if (k >= d) return 0.f;

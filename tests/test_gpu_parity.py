@@ -842,8 +842,9 @@ def test_lazy_steps_bit_identical_to_full_screens(monkeypatch, kind):
     X, prec, k = _lazy_case(kind)
     runs = {}
     for name, env in (("lazy", {}), ("full", {"EBC200_LAZY": "0"}), ("classic", {"EBC200_REFINE2": "0"}),
-                      ("nocond", {"EBC200_GRAPH_COND": "0"})):
-        for key in ("EBC200_LAZY", "EBC200_REFINE2", "EBC200_GRAPH_COND"):
+                      ("nocond", {"EBC200_GRAPH_COND": "0"}), ("nogather", {"EBC200_GATHER": "0"}),
+                      ("noeagersync", {"EBC200_EAGER_SYNC": "0"})):
+        for key in ("EBC200_LAZY", "EBC200_REFINE2", "EBC200_GRAPH_COND", "EBC200_GATHER", "EBC200_EAGER_SYNC"):
             monkeypatch.delenv(key, raising=False)
         for key, val in env.items():
             monkeypatch.setenv(key, val)
