@@ -2606,14 +2606,15 @@ int ebc_eval_multiset(ebc_ctx* ctx, const int64_t* offsets, const int64_t* idx, 
     }
   }
   if (!done) {
-    // dense fallback: l x nchunks partials, allocated only when it runs
-    rc = ensure(ctx, ctx->ms_part, (size_t)l * ctx->nchunks * sizeof(double));
+    // dense fallback: partials of one batch of sets at a time (batch x nchunks),
+    // allocated only when it runs; each batch is finished before the next
+    rc = ensure(ctx, ctx->ms_part, (size_t)std::min<int64_t>(l, batch) * ctx->nchunks * sizeof(double));
     if (rc) return rc;
   }
   for (int64_t s0 = 0; !done && s0 < l; s0 += batch) {
     const int64_t nb = std::min<int64_t>(batch, l - s0);
     dim3 grid(ctx->nchunks, (unsigned)nb);
-    double* part = (double*)ctx->ms_part.p + s0 * ctx->nchunks;
+    double* part = (double*)ctx->ms_part.p;  // k_multiset indexes it by (set - s0)
     if (ctx->dtype == EBC_F64)
       k_multiset<double><<<grid, RED_THREADS, 0, ctx->stream>>>(ctx->V64, ctx->pitch, ctx->n, ctx->d, ctx->e0d,
                                                                (const int64_t*)ctx->ms_off.p,
@@ -2623,10 +2624,8 @@ int ebc_eval_multiset(ebc_ctx* ctx, const int64_t* offsets, const int64_t* idx, 
                                                               (const int64_t*)ctx->ms_off.p,
                                                               (const int64_t*)ctx->ms_idx.p, s0, ctx->nchunks, part);
     KCHECK();
-  }
-  if (!done) {
-    k_multiset_final<<<(unsigned)((l + 255) / 256), 256, 0, ctx->stream>>>(
-        (const double*)ctx->ms_part.p, l, ctx->nchunks, 1.0 / (double)ctx->n, (double*)ctx->ms_out.p);
+    k_multiset_final<<<(unsigned)((nb + 255) / 256), 256, 0, ctx->stream>>>(
+        part, nb, ctx->nchunks, 1.0 / (double)ctx->n, (double*)ctx->ms_out.p + s0);
     KCHECK();
   }
   CU(cudaEventRecord(b, ctx->stream));
