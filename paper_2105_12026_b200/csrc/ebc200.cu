@@ -18,6 +18,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <mutex>
 #include <vector>
 
 #include "../../include/ebc200.h"
@@ -77,6 +78,40 @@ const NcclApi& nccl_api() {
     }
   }
   return api;
+}
+
+// Small pinned host words for per-step read-backs, carved from one
+// process-wide page-locked slab: cudaMallocHost costs milliseconds, far more
+// than the rest of a context's creation (EbcFunction in the e2e path).
+struct PinnedWords {
+  std::mutex mu;
+  int* slab = nullptr;
+  std::vector<int> free_slots;
+  static constexpr int SLOTS = 4096;
+  int* take() {
+    std::lock_guard<std::mutex> lock(mu);
+    if (!slab) {
+      if (cudaMallocHost((void**)&slab, SLOTS * sizeof(int) * 16) != cudaSuccess) {
+        slab = nullptr;
+        return nullptr;
+      }
+      for (int i = SLOTS - 1; i >= 0; --i) free_slots.push_back(i);
+    }
+    if (free_slots.empty()) return nullptr;
+    const int i = free_slots.back();
+    free_slots.pop_back();
+    return slab + (size_t)i * 16;  // one 64-byte line per slot
+  }
+  bool give(int* p) {
+    std::lock_guard<std::mutex> lock(mu);
+    if (!slab || p < slab || p >= slab + (size_t)SLOTS * 16) return false;
+    free_slots.push_back((int)((p - slab) / 16));
+    return true;
+  }
+};
+PinnedWords& pinned_words() {
+  static PinnedWords pw;
+  return pw;
 }
 
 struct DevBuf {
@@ -1351,7 +1386,7 @@ void free_ctx(ebc_ctx* c) {
   }
   for (cudaStream_t ss : c->side)
     if (ss) cudaStreamDestroy(ss);
-  if (c->mode_host) cudaFreeHost(c->mode_host);
+  if (c->mode_host && !pinned_words().give(c->mode_host)) cudaFreeHost(c->mode_host);
   if (c->sv_slots_host) cudaFreeHost(c->sv_slots_host);
   if (c->sv_out_host) cudaFreeHost(c->sv_out_host);
   delete c;
@@ -1597,6 +1632,7 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
       k_pad<double, double><<<blocks, 256, 0, ctx->stream>>>((const double*)raw, n, d, ctx->V64, ctx->pitch);
     CUC(cudaGetLastError());
   }
+  mark("pad");
   if (dtype != EBC_F64) {
     // fp32 range guard: every screen (and the sparse work-matrix flag screen)
     // forms squared distances, norms and short sums in fp32.  Grounds whose
@@ -1639,6 +1675,7 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
   CUC(cudaMemsetAsync(ctx->stats, 0, 8 * sizeof(long long), ctx->stream));
   CUC(cudaMallocAsync((void**)&ctx->level, 2 * sizeof(int), ctx->stream));
   CUC(cudaMemsetAsync(ctx->level, 0, 2 * sizeof(int), ctx->stream));
+  mark("range guard");
   // tensor-core screen: fp32-path grounds whose 128-candidate tile of hi+lo
   // operands plus a 2-stage ring of NP-point tiles fits shared memory
   if (dtype != EBC_F64 && ctx->screen_mode == 3) {
@@ -1692,6 +1729,7 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
       ctx->tc_ntl = ctx->n_pad / ctx->tc_np;
       const size_t ve = (size_t)ctx->n_pad * ctx->kpad;
       const size_t nas = (size_t)ctx->tc_na * ctx->n_pad;
+      mark("tc plan");
       CUC(cudaMallocAsync((void**)&ctx->Vhi, ve * es, ctx->stream));
       if (parts == 2) CUC(cudaMallocAsync((void**)&ctx->Vlo, ve * es, ctx->stream));
       if (ctx->tc_fast) CUC(cudaMallocAsync((void**)&ctx->Vf, ve * 2, ctx->stream));
@@ -1729,6 +1767,7 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
       CUC(cudaMemsetAsync(ctx->fps_keys, 0, (size_t)(ctx->tc_na + 1) * sizeof(unsigned long long), ctx->stream));
     }
   }
+  mark("tc allocs");
   CUC(cudaMallocAsync((void**)&ctx->selected, (size_t)ctx->n_pad, ctx->stream));
   CUC(cudaMemsetAsync(ctx->selected, 0, (size_t)ctx->n_pad, ctx->stream));
   CUC(cudaMallocAsync((void**)&ctx->chunkpart, (size_t)ctx->nchunks * sizeof(double), ctx->stream));
@@ -1752,6 +1791,7 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
       CUC(cudaMemsetAsync(ctx->uf_ctr, 0, cb, ctx->stream));
     }
   }
+  mark("misc allocs");
   CUC(cudaMallocAsync((void**)&ctx->cur, sizeof(double), ctx->stream));
   CUC(cudaMemsetAsync(ctx->cur, 0, sizeof(double), ctx->stream));
   CUC(cudaMallocAsync((void**)&ctx->best, sizeof(int64_t), ctx->stream));
@@ -1778,7 +1818,8 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
     ctx->force_global_lb = gl && gl[0] == '1';
     const char* es = getenv("EBC200_EAGER_SYNC");
     if (es && es[0] == '0') ctx->eager_sync = false;
-    CUC(cudaMallocHost((void**)&ctx->mode_host, sizeof(int)));
+    ctx->mode_host = pinned_words().take();
+    if (!ctx->mode_host) CUC(cudaMallocHost((void**)&ctx->mode_host, sizeof(int)));
     const char* gc = getenv("EBC200_GRAPH_COND");
     if (gc && gc[0] == '0') ctx->use_cond = false;
   }
@@ -1817,6 +1858,7 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
     k_init<float><<<ctx->nchunks, RED_THREADS, 0, ctx->stream>>>(ctx->V32, ctx->pitch, n, d, e0dev, ctx->pk,
                                                                 ctx->e0d, ctx->cm64, ctx->nv32, ctx->pt, ctx->chunkpart);
   CUC(cudaGetLastError());
+  mark("init");
   if (ctx->tc_np) {
     {
       // anchors (farthest-point sampling from the origin), |v - mu_a|^2, the
@@ -1828,6 +1870,7 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
                                                               ctx->fps_keys, ctx->anchors, ctx->pitch);
         CUC(cudaGetLastError());
       }
+      mark("fps anchors");
       k_nva<<<8 * ctx->num_sms, 256, 0, ctx->stream>>>(ctx->V32, ctx->pitch, n, d, ctx->anchors, ctx->pitch,
                                                        ctx->tc_na, ctx->nva, ctx->n_pad);
       CUC(cudaGetLastError());
