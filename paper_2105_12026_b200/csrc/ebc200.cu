@@ -18,7 +18,9 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <atomic>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include "../../include/ebc200.h"
@@ -112,6 +114,66 @@ struct PinnedWords {
 PinnedWords& pinned_words() {
   static PinnedWords pw;
   return pw;
+}
+
+// Upload of the caller's pageable rows (ebc_create): host threads copy each
+// chunk into one of two process-wide pinned staging buffers while the previous
+// chunk's DMA runs (the driver's pageable path stages through one thread).
+// Returns false (nothing enqueued) when staging is unavailable.
+bool staged_upload(cudaStream_t stream, void* dst, const void* src, size_t bytes) {
+  constexpr size_t CH = 8u << 20;
+  static std::mutex mu;
+  static unsigned char* stage[2] = {nullptr, nullptr};
+  static cudaEvent_t done[2] = {nullptr, nullptr};
+  std::lock_guard<std::mutex> lock(mu);
+  if (!stage[0]) {
+    if (cudaMallocHost((void**)&stage[0], 2 * CH) != cudaSuccess) {
+      stage[0] = nullptr;
+      return false;
+    }
+    stage[1] = stage[0] + CH;
+    if (cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming) != cudaSuccess)
+      return false;
+  }
+  const size_t nch = (bytes + CH - 1) / CH;
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const int T = (int)std::min<unsigned>(8, hw);
+  std::atomic<int64_t> allowed{std::min<int64_t>(2, (int64_t)nch) - 1};  // highest chunk a worker may fill
+  std::vector<std::atomic<int>> filled(nch);
+  for (auto& f : filled) f.store(0);
+  auto worker = [&](int t) {
+    for (size_t i = 0; i < nch; ++i) {
+      while (allowed.load(std::memory_order_acquire) < (int64_t)i) std::this_thread::yield();
+      const size_t off = i * CH, len = std::min(CH, bytes - off);
+      const size_t a = len * t / T, b = len * (t + 1) / T;
+      std::memcpy(stage[i & 1] + a, static_cast<const unsigned char*>(src) + off + a, b - a);
+      filled[i].fetch_add(1, std::memory_order_acq_rel);
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < T; ++t) pool.emplace_back(worker, t);
+  bool ok = true;
+  // thread 0 of the copy is this one, interleaved with the DMA issue
+  for (size_t i = 0; i < nch; ++i) {
+    const size_t off = i * CH, len = std::min(CH, bytes - off);
+    const size_t b0 = len / T;
+    std::memcpy(stage[i & 1], static_cast<const unsigned char*>(src) + off, b0);
+    filled[i].fetch_add(1, std::memory_order_acq_rel);
+    while (filled[i].load(std::memory_order_acquire) < T) std::this_thread::yield();
+    ok = ok && cudaMemcpyAsync(static_cast<unsigned char*>(dst) + off, stage[i & 1], len, cudaMemcpyHostToDevice,
+                               stream) == cudaSuccess;
+    ok = ok && cudaEventRecord(done[i & 1], stream) == cudaSuccess;
+    if (i + 2 < nch) {  // buffer (i & 1) is reused by chunk i + 2 once this DMA is done
+      ok = ok && cudaEventSynchronize(done[i & 1]) == cudaSuccess;
+      allowed.store((int64_t)i + 2, std::memory_order_release);
+    }
+  }
+  for (auto& th : pool) th.join();
+  // the staging buffers are shared: the last DMAs finish before the next caller
+  ok = ok && cudaEventSynchronize(done[(nch - 1) & 1]) == cudaSuccess;
+  if (nch > 1) ok = ok && cudaEventSynchronize(done[nch & 1]) == cudaSuccess;
+  return ok;
 }
 
 struct DevBuf {
@@ -1620,7 +1682,12 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
   void* raw = nullptr;
   CUC(cudaMallocAsync((void**)&raw, (size_t)n * d * src_esz, ctx->stream));
   mark("allocs V/raw");
-  CUC(cudaMemcpyAsync(raw, V, (size_t)n * d * src_esz, cudaMemcpyHostToDevice, ctx->stream));
+  {
+    const size_t bytes = (size_t)n * d * src_esz;
+    const char* su = getenv("EBC200_STAGED_UPLOAD");
+    const bool staged = bytes >= (16u << 20) && !(su && su[0] == '0') && staged_upload(ctx->stream, raw, V, bytes);
+    if (!staged) CUC(cudaMemcpyAsync(raw, V, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  }
   mark("upload");
   {
     const int blocks = 8 * ctx->num_sms;
