@@ -124,18 +124,24 @@ bool staged_upload(cudaStream_t stream, void* dst, const void* src, size_t bytes
   constexpr size_t CH = 8u << 20;
   static std::mutex mu;
   static unsigned char* stage[2] = {nullptr, nullptr};
-  static cudaEvent_t done[2] = {nullptr, nullptr};
   std::lock_guard<std::mutex> lock(mu);
-  if (!stage[0]) {
-    if (cudaMallocHost((void**)&stage[0], 2 * CH) != cudaSuccess) {
+  if (!stage[0]) {  // page-locked once per process (portable across devices)
+    if (cudaHostAlloc((void**)&stage[0], 2 * CH, cudaHostAllocPortable) != cudaSuccess) {
       stage[0] = nullptr;
       return false;
     }
     stage[1] = stage[0] + CH;
-    if (cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming) != cudaSuccess)
-      return false;
   }
+  // events of the calling device (a process may upload to several devices)
+  struct Ev {
+    cudaEvent_t e = nullptr;
+    ~Ev() {
+      if (e) cudaEventDestroy(e);
+    }
+  } done[2];
+  if (cudaEventCreateWithFlags(&done[0].e, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&done[1].e, cudaEventDisableTiming) != cudaSuccess)
+    return false;
   const size_t nch = (bytes + CH - 1) / CH;
   const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
   const int T = (int)std::min<unsigned>(8, hw);
@@ -163,16 +169,17 @@ bool staged_upload(cudaStream_t stream, void* dst, const void* src, size_t bytes
     while (filled[i].load(std::memory_order_acquire) < T) std::this_thread::yield();
     ok = ok && cudaMemcpyAsync(static_cast<unsigned char*>(dst) + off, stage[i & 1], len, cudaMemcpyHostToDevice,
                                stream) == cudaSuccess;
-    ok = ok && cudaEventRecord(done[i & 1], stream) == cudaSuccess;
+    ok = ok && cudaEventRecord(done[i & 1].e, stream) == cudaSuccess;
     if (i + 2 < nch) {  // buffer (i & 1) is reused by chunk i + 2 once this DMA is done
-      ok = ok && cudaEventSynchronize(done[i & 1]) == cudaSuccess;
+      ok = ok && cudaEventSynchronize(done[i & 1].e) == cudaSuccess;
       allowed.store((int64_t)i + 2, std::memory_order_release);
     }
   }
   for (auto& th : pool) th.join();
   // the staging buffers are shared: the last DMAs finish before the next caller
-  ok = ok && cudaEventSynchronize(done[(nch - 1) & 1]) == cudaSuccess;
-  if (nch > 1) ok = ok && cudaEventSynchronize(done[nch & 1]) == cudaSuccess;
+  ok = ok && cudaEventSynchronize(done[(nch - 1) & 1].e) == cudaSuccess;
+  if (nch > 1) ok = ok && cudaEventSynchronize(done[nch & 1].e) == cudaSuccess;
+  if (!ok) cudaStreamSynchronize(stream);  // no DMA may still read the shared staging
   return ok;
 }
 
