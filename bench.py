@@ -58,6 +58,7 @@ CONFIG_DESC = {
     "C3": "Greedy k=50 EBC, synthetic Gaussian N=100,000 d=100 fp16 storage",
     "C4": "Greedy k=20 EBC, injection-molding surrogate N=500,000 d=32 fp32",
     "C5": "work-matrix evaluation, 4,096 sets x 10 members, synthetic Gaussian N=200,000 d=64 fp32",
+    "C4S50": "Greedy k=20 EBC, 50-regime surrogate N=500,000 d=32 fp32 (SURVEY 8(d) near-tie stress case)",
 }
 METRIC = "Greedy EBC point-candidate distance evals/s (wall time & FMA roofline)"
 

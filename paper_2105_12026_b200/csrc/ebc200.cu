@@ -229,6 +229,7 @@ struct ebc_ctx {
   int screen_mode = 2;
   bool fp32_ok = true;  // ebc_create's range guard: false -> no fp32 screen at all (screen_mode -1)
   int wcap = 256;
+  int wcap_tc = 256;  // the anchored tensor rung's window cap (EBC200_WCAP_TC)
   // tensor-core Gram screen (tcgen05, kind::tf32, 3xTF32)
   void* Vhi = nullptr;
   void* Vlo = nullptr;
@@ -883,7 +884,7 @@ int run_screen_window(ebc_ctx* ctx, int eb, int fin_blocks) {
         if (!rc) rc = run_finalize_window(ctx, tp.nsplit, (double)tp.tps * ctx->tc_np, 32, fin_blocks, 2.0,
                                           ctx->level, L_TC, /*ub_only=*/true, agg ? (double*)ctx->part_a.p : nullptr);
         if (!rc && ctx->ladder_max > L_TC) {
-          k_adapt<<<1, 32, 0, ctx->stream>>>(ctx->wcount, ctx->maxlb, ctx->wcap, ctx->level, L_TC);
+          k_adapt<<<1, 32, 0, ctx->stream>>>(ctx->wcount, ctx->maxlb, ctx->wcap_tc, ctx->level, L_TC);
           KCHECK();
         }
       }
@@ -1622,6 +1623,14 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
     ctx->pk.gram_k = (float)(0.5 * (d + 4) * u * (1.0 + 1.0 / 512));
     ctx->gram_kc = (float)(1.5 * (d + 4) * u * (1.0 + 1.0 / 512));
     ctx->wcap = (int)std::max<int64_t>(256, n / 64);
+    // the anchored tensor rung keeps windows up to N/8: on near-tied clustered
+    // data (C4's 50-regime stress case) no FFMA rung narrows them, and refining
+    // even N/8 candidates exactly costs far less than an FFMA re-screen
+    ctx->wcap_tc = (int)std::max<int64_t>(256, n / 8);
+    {
+      const char* wc = getenv("EBC200_WCAP_TC");
+      if (wc && wc[0]) ctx->wcap_tc = std::max(1, atoi(wc));
+    }
     ctx->screen_mode = d >= 24 ? 3 : 0;
     const char* gg = getenv("EBC200_GRAPHS");
     if (gg && gg[0] == '0') ctx->use_graphs = false;
