@@ -310,6 +310,8 @@ struct ebc_ctx {
   void* lazy_part = nullptr;       // 2 num_sms x TK 64-bit keys: k_lazy_topk's block lists
   double* ub_next = nullptr;       // best stale bound outside the first batch
   int lazy_batch = 4;              // EBC200_LAZY_BATCH (1..RW): candidates refined first in a lazy step
+  bool probe_on = true;            // EBC200_LAZY_PROBE=0: no ring-probe batch on undecided steps
+  ProbeBuf probe;                  // k_lazy_rings: ring winners, ticket, the probe list
   unsigned int* counter3 = nullptr;  // k_refine's finalize ticket
   bool refine2 = true;             // EBC200_REFINE2=0: the lazy batch on the classic k_refine
   DevBuf rterms;                   // RW x nchunks chunk sums of the short refine
@@ -793,22 +795,13 @@ int launch_tc_agg(ebc_ctx* ctx, const TcPlan& p) {
   an.rhomax = ctx->rhomax;
   an.cmn = ctx->cmn;
   an.bflag = ctx->step_bflag;
-  // c' in 32 registers when it fits (padded dims of vsum are zero), else in smem;
-  // the all-positive tile list (uint16 per tile of the split) follows
-  const bool regs = ctx->d <= 32;  // reads 32 floats per vsum row: zeros times c' past d (32-float tail pad)
-  const size_t smem = (regs ? 0 : (size_t)ctx->d * 128 * sizeof(float)) + ((size_t)p.tps * 2 + 16);
+  // W (d doubles) and its 128 group partials, then the all-positive tile list
+  const size_t smem = ((size_t)ctx->d + 128) * sizeof(double) + ((size_t)p.tps * 2 + 16);
   dim3 grid(p.ncb, p.nsplit);
-  if (regs) {
-    CU(cudaFuncSetAttribute(k_screen_agg<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_screen_agg<32><<<grid, 128, smem, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->d, an, ctx->c0, p.ntiles, p.tps,
-                                                       ctx->tc_np, ctx->n, ctx->ipsum, ctx->vsum, ctx->vsn,
-                                                       (double*)ctx->part_a.p, ctx->n_pad, ctx->level, L_TC, ctx->agg_any);
-  } else {
-    CU(cudaFuncSetAttribute(k_screen_agg<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_screen_agg<0><<<grid, 128, smem, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->d, an, ctx->c0, p.ntiles, p.tps,
-                                                      ctx->tc_np, ctx->n, ctx->ipsum, ctx->vsum, ctx->vsn,
-                                                      (double*)ctx->part_a.p, ctx->n_pad, ctx->level, L_TC, ctx->agg_any);
-  }
+  CU(cudaFuncSetAttribute(k_screen_agg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_screen_agg<<<grid, 128, smem, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->d, an, ctx->c0, p.ntiles, p.tps,
+                                                 ctx->tc_np, ctx->n, ctx->ipsum, ctx->vsum, ctx->vsn,
+                                                 (double*)ctx->part_a.p, ctx->n_pad, ctx->level, L_TC, ctx->agg_any);
   KCHECK();
   return EBC_OK;
 }
@@ -1009,7 +1002,12 @@ int enqueue_refine(ebc_ctx* ctx, int ng, const int* skip_level, const RefineFina
 
 // Refine of a window of at most RW candidates (the lazy first batch): one
 // RCH-thread block per chunk, the classic reduction replayed (kernels.cuh).
-int enqueue_refine_short(ebc_ctx* ctx, int ng, const RefineFinal& fin) {
+int enqueue_refine_short(ebc_ctx* ctx, int ng, const RefineFinal& fin, const int* wcount = nullptr,
+                         const int64_t* wlist = nullptr) {
+  if (!wcount) {
+    wcount = ctx->wcount;
+    wlist = ctx->wlist;
+  }
   RefinePrune pr;
   if (refine_prune_on(ctx) && ctx->cmx_fresh) {
     pr.rho = ctx->rho;
@@ -1022,18 +1020,21 @@ int enqueue_refine_short(ebc_ctx* ctx, int ng, const RefineFinal& fin) {
     pr.crad = ctx->crad;
   }
   const size_t smem = (size_t)RW * (ctx->d + RCH) * sizeof(double);
-  if (smem > 180 * 1024) return enqueue_refine(ctx, ng, nullptr, fin);
+  if (smem > 180 * 1024) {
+    if (wcount != ctx->wcount) return EBC_EINVAL;  // callers check short_refine_fits first
+    return enqueue_refine(ctx, ng, nullptr, fin);
+  }
   int rc = ensure(ctx, ctx->rterms, (size_t)RW * ctx->nchunks * sizeof(double));
   if (rc) return rc;
   if (ctx->dtype == EBC_F64) {
     CU(cudaFuncSetAttribute(k_refine_short<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_refine_short<double><<<ctx->nchunks, SHORT_THREADS, smem, ctx->stream>>>(
-        ctx->V64, ctx->pitch, ctx->n, ctx->d, ctx->cm64, ctx->wcount, ctx->wlist, ctx->nchunks, ng,
+        ctx->V64, ctx->pitch, ctx->n, ctx->d, ctx->cm64, wcount, wlist, ctx->nchunks, ng,
         (double*)ctx->rterms.p, (double*)ctx->part_r.p, pr, fin);
   } else {
     CU(cudaFuncSetAttribute(k_refine_short<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_refine_short<float><<<ctx->nchunks, SHORT_THREADS, smem, ctx->stream>>>(
-        ctx->V32, ctx->pitch, ctx->n, ctx->d, ctx->cm64, ctx->wcount, ctx->wlist, ctx->nchunks, ng,
+        ctx->V32, ctx->pitch, ctx->n, ctx->d, ctx->cm64, wcount, wlist, ctx->nchunks, ng,
         (double*)ctx->rterms.p, (double*)ctx->part_r.p, pr, fin);
   }
   KCHECK();
@@ -1190,6 +1191,22 @@ int run_step_select(ebc_ctx* ctx, int step, int commit, int64_t* sel_dev) {
     // undecided step (level[0] == -3): stale set -> mode -> screen / refine
     CondScope ca;
     CU(ca.open(ctx, hrest, 0));
+    if (ctx->probe_on && has_screen && ctx->refine2 && (size_t)RW * (ctx->d + RCH) * sizeof(double) <= 180 * 1024) {
+      // probe batch: ring winners around the last selected centre raise lb
+      // (k_lazy_rings) before the stale set is listed
+      k_lazy_rings<<<ag, 256, (size_t)ctx->d * sizeof(float), ctx->stream>>>(
+          ctx->c0, ctx->c1, ctx->V32, ctx->pitch, ctx->d, ctx->best, ctx->ubp, ctx->selected, ctx->level, ctx->probe,
+          RW);
+      KCHECK();
+      RefineFinal fp = fin;
+      fp.batch = 3;
+      fp.commit = 0;
+      fp.maxlb = ctx->maxlb;
+      ctx->cmx_fresh = ctx->cmx_valid;
+      rc = enqueue_refine_short(ctx, ng, fp, ctx->probe.pcount, ctx->probe.plist);
+      ctx->cmx_fresh = false;
+      if (rc) return rc;
+    }
     CU(cudaMemsetAsync(ctx->bflag, 0, (size_t)((ncand + tc::M - 1) / tc::M + 2), ctx->stream));
     k_lazy_mark2<<<fin_blocks, 256, 0, ctx->stream>>>(ctx->c0, ctx->c1, ctx->ubp, ctx->selected, ctx->maxlb,
                                                       margin, ctx->bcnt, ctx->bflag, ctx->level);
@@ -1436,7 +1453,7 @@ void free_ctx(ebc_ctx* c) {
   cudaSetDevice(c->device);
   void* ptrs[] = {c->V32, c->V64, c->e0d, c->cm64, c->pt, c->nv32, c->level, c->stats, c->Vhi, c->Vlo, c->Vf, c->tile_anchor0, c->rhomax, c->cmn, c->vsum, c->vsn, c->ipsum, c->rhomin, c->agg_any, c->pttc, c->kpmax, c->anchors, c->nva, c->tile_anchor, c->tc_vmax, c->fps_keys, c->ipa0, c->tile_rad, c->crad, c->rho, c->cmx, c->cmx0, c->selected, c->chunkpart, c->counter, c->counter2, c->topc, c->toppart, c->terms, c->cur, c->best, c->uf_ctr,
                   c->maxlb, c->wcount, c->wlist, c->wgain, c->ub, c->ubp, c->bflag, c->slist, c->scount,
-                  c->lazy_part, c->ub_next, c->counter3, c->bcnt, c->Vg, c->g_anchor, c->g_rad};
+                  c->lazy_part, c->ub_next, c->counter3, c->bcnt, c->Vg, c->g_anchor, c->g_rad, c->probe.rkey};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, c->stream);
   DevBuf* bufs[] = {&c->tie_rec, &c->tie_all, &c->sel_hash, &c->ms_tanchor, &c->ms_trad, &c->part_g, &c->part_e, &c->part_a, &c->part_r, &c->rterms, &c->sv_cm, &c->sv_de, &c->sv_slots, &c->sv_part, &c->sv_out, &c->sel_out, &c->val_out, &c->gain_out, &c->ms_part,
@@ -1893,6 +1910,19 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
   CUC(cudaMallocAsync((void**)&ctx->counter3, sizeof(unsigned int), ctx->stream));
   CUC(cudaMemsetAsync(ctx->counter3, 0, sizeof(unsigned int), ctx->stream));
   {
+    // ring keys | ticket | count | list (one allocation, zeroed once; k_lazy_rings re-zeroes)
+    const size_t pbytes = NRING * 8 + 8 + 8 + RW * 8;
+    unsigned char* pbm = nullptr;
+    CUC(cudaMallocAsync((void**)&pbm, pbytes, ctx->stream));
+    CUC(cudaMemsetAsync(pbm, 0, pbytes, ctx->stream));
+    ctx->probe.rkey = (unsigned long long*)pbm;
+    ctx->probe.counter = (unsigned int*)(pbm + NRING * 8);
+    ctx->probe.pcount = (int*)(pbm + NRING * 8 + 8);
+    ctx->probe.plist = (int64_t*)(pbm + NRING * 8 + 16);
+    const char* pe = getenv("EBC200_LAZY_PROBE");
+    if (pe && pe[0] == '0') ctx->probe_on = false;
+  }
+  {
     const char* lb = getenv("EBC200_LAZY_BATCH");
     if (lb && lb[0]) ctx->lazy_batch = std::max(1, std::min(RW, atoi(lb)));
     const char* r2 = getenv("EBC200_REFINE2");
@@ -1915,7 +1945,12 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
     ctx->gather_on = ctx->lazy_on && ctx->tc_np && ctx->screen_mode == 3 && !ctx->tc_fast &&
                      (ctx->tc_kind == tc::KIND_BF16 || ctx->tc_kind == tc::KIND_TF32) && !(ge && ge[0] == '0');
     if (ctx->gather_on) {
-      ctx->gath_cap = std::min<int64_t>((n + tc::M - 1) / tc::M * tc::M, 65536);
+      // up to a quarter of the candidates (at least 64k): late steps of C4 with the
+      // probe batch list ~100k scattered stale candidates over every block
+      const int64_t gq = std::max<int64_t>(65536, (n / 4 + tc::M - 1) / tc::M * tc::M);
+      ctx->gath_cap = std::min<int64_t>((n + tc::M - 1) / tc::M * tc::M, gq);
+      const char* gc = getenv("EBC200_GATHER_CAP");
+      if (gc && gc[0]) ctx->gath_cap = std::min<int64_t>(ctx->gath_cap, std::max(tc::M, atoi(gc) / tc::M * tc::M));
       CUC(cudaMallocAsync((void**)&ctx->Vg, (size_t)ctx->gath_cap * ctx->pitch * sizeof(float), ctx->stream));
       CUC(cudaMallocAsync((void**)&ctx->g_anchor, (size_t)(ctx->gath_cap / tc::M + 1) * sizeof(int), ctx->stream));
       CUC(cudaMallocAsync((void**)&ctx->g_rad, (size_t)(ctx->gath_cap / tc::M + 1) * sizeof(float), ctx->stream));

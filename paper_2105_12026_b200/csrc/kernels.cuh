@@ -1153,6 +1153,100 @@ __global__ void k_lazy_decide(const long long* __restrict__ maxlb, const double*
   }
 }
 
+// Probe batch of an undecided lazy step (level[0] == -3).  The first batch is
+// the top stale bounds, and on clustered data those are the neighbours of the
+// centre just selected: their gains collapsed, lb comes out tiny and nearly
+// every candidate stays stale (C4 steps 2-7).  Any candidate's exact gain is a
+// valid lb, so a second batch is drawn for diversity: candidates are binned in
+// rings of |c - s|^2 around the last selected s (two binary exponents per ring),
+// the best stale bound of each ring is kept, and the np ring winners with the
+// largest bounds are refined (k_refine_short, RefineFinal batch 3: lb = max).
+// Which candidates are probed never affects the result, only how many stay stale.
+constexpr int NRING = 128;
+struct ProbeBuf {
+  unsigned long long* rkey = nullptr;  // NRING ring winners (top_key), zero between steps
+  unsigned int* counter = nullptr;
+  int* pcount = nullptr;
+  int64_t* plist = nullptr;            // RW
+};
+__global__ void __launch_bounds__(256) k_lazy_rings(int64_t c0, int64_t c1, const float* __restrict__ V32, int pitch,
+                                                    int d, const int64_t* __restrict__ best,
+                                                    const double* __restrict__ ubp,
+                                                    const unsigned char* __restrict__ selected,
+                                                    const int* __restrict__ level, ProbeBuf pb, int np) {
+  extern __shared__ float ssv[];  // d floats: the last selected row
+  __shared__ unsigned long long sk[NRING];
+  __shared__ bool last;
+  for (int i = threadIdx.x; i < NRING; i += blockDim.x) sk[i] = 0ull;
+  const bool on = *level == -3;
+  const int64_t sb = on ? *best : -1;
+  if (sb >= 0)
+    for (int k = threadIdx.x; k < d; k += blockDim.x) ssv[k] = V32[sb * pitch + k];
+  __syncthreads();
+  if (sb >= 0) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < c1; c += stride) {
+      if (selected[c]) continue;
+      const float4* row = reinterpret_cast<const float4*>(V32 + c * pitch);
+      float a0 = 0.f, a1 = 0.f;
+      int k = 0;
+      for (; k + 4 <= d; k += 4) {
+        const float4 q = __ldg(row + (k >> 2));
+        const float x0 = q.x - ssv[k], x1 = q.y - ssv[k + 1], x2 = q.z - ssv[k + 2], x3 = q.w - ssv[k + 3];
+        a0 = fmaf(x0, x0, fmaf(x1, x1, a0));
+        a1 = fmaf(x2, x2, fmaf(x3, x3, a1));
+      }
+      for (; k < d; ++k) {
+        const float x = V32[c * pitch + k] - ssv[k];
+        a0 = fmaf(x, x, a0);
+      }
+      const int ring = (int)(__float_as_uint(a0 + a1) >> 24) & (NRING - 1);
+      const unsigned long long key = top_key(ubp[c - c0], c - c0);
+      if (key > sk[ring]) atomicMax(&sk[ring], key);
+    }
+  }
+  __syncthreads();
+  for (int r = threadIdx.x; r < NRING; r += blockDim.x)
+    if (sk[r]) atomicMax(pb.rkey + r, sk[r]);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(pb.counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last || threadIdx.x >= 32) return;
+  __threadfence();
+  // warp 0: the np largest ring winners (keys are unique), rings cleared for the next step
+  const int lane = threadIdx.x;
+  unsigned long long l[NRING / 32];
+#pragma unroll
+  for (int j = 0; j < NRING / 32; ++j) {
+    l[j] = __ldcg(pb.rkey + lane + 32 * j);
+    pb.rkey[lane + 32 * j] = 0ull;
+  }
+  int m = 0;
+  for (int r = 0; r < np; ++r) {
+    unsigned long long b = 0ull;
+#pragma unroll
+    for (int j = 0; j < NRING / 32; ++j) b = l[j] > b ? l[j] : b;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long x = __shfl_xor_sync(0xffffffffu, b, o);
+      b = x > b ? x : b;
+    }
+    if (b == 0ull) break;
+#pragma unroll
+    for (int j = 0; j < NRING / 32; ++j)
+      if (l[j] == b) l[j] = 0ull;
+    if (lane == 0) pb.plist[m] = c0 + (int64_t)(0xFFFFFFFFu - (unsigned)(b & 0xFFFFFFFFull));
+    ++m;
+  }
+  if (lane == 0) {
+    *pb.pcount = m;
+    *pb.counter = 0u;
+  }
+}
+
 // Undecided lazy step (level[0] == -3): list the stale candidates
 // ubp[c] >= lb - margin - 1e-9 |lb| (lb = *maxlb, the batch's best exact gain)
 // in slist (count *scount) and flag their 128-candidate blocks.
@@ -1441,6 +1535,14 @@ __device__ void refine_finalize_n(const RefineFinal& F, int wc, const int64_t* _
     __syncthreads();
   }
   top = sred[0];
+  if (F.batch == 3) {  // probe batch (k_lazy_rings): raises lb, decides nothing
+    if (tid == 0 && wc > 0) {
+      const long long k = dkey(sred[nt]);
+      if (k > *F.maxlb) *F.maxlb = k;
+      F.stats[6] += wc;
+    }
+    return;
+  }
   if (F.batch == 2) {  // sharded: the decision waits for the global bound (k_lazy_decide)
     if (tid == 0) {
       *F.maxlb = dkey(sred[nt]);

@@ -1084,10 +1084,17 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
 // block's upper-bound contribution from tile aggregates.  Same plan and grid as
 // k_screen_tc, one thread per candidate; only where the screen used its kept-tile
 // list (it then skipped exactly these tiles).  Per tile:
-//   sum_v (a_v + kq) <= ipsum_a[t] + c'.vsum[t] + n_t (ic + kq) + (d + 2) u |c'| |vsum[t]|
-// with the screen's own per-pair quantum kq (it bounds the fp32 seed, c' and ic
-// roundings) and the fp32 dot's error; accumulated in fp64.
-template <int DR>  // DR > 0: c' held in DR registers (d <= DR); 0: c' in shared memory
+//   sum_v (a_v + kq) <= ipsum_a[t] + c'.vsum[t] + n_t (ic + kq_t) + (d + 2) u |c'| |vsum[t]|
+// with the screen's own per-pair quantum kq_t (it bounds the fp32 seed, c' and
+// ic roundings); the last term covers vsum's fp32 rounding and an
+// fp32 dot.  The terms are linear in the tile, so the CTA first sums the
+// block's all-positive tiles (fixed order, fp64): W = sum vsum[t], sum ipsum,
+// sum n_t, sum n_t kpmax[t], sum n_t vmax[t], sum |vsum[t]| -- then each
+// candidate needs ONE fp64 dot c'.W instead of one fp32 dot per tile (C4 step 0:
+// every pair all-positive, 9.8 ms -> see DESIGN.md).  The fp64 sums and dot
+// err by < (nl + d + 2) 2^-53 |c'| sum |vsum[t]|, far inside the kept (d + 2) u
+// term; kq_t = fl32(kpmax + fl32(kxc vmax + kc)) (non-negative terms) is
+// bounded by its exact value times (1 + 2^-21).
 __global__ void __launch_bounds__(128) k_screen_agg(const float* __restrict__ V32, int pitch, int d, TcAnchors an,
                                                     int64_t cand0, int ntiles, int tiles_per_split, int np, int64_t n,
                                                     const double* __restrict__ ipsum, const float* __restrict__ vsum,
@@ -1100,8 +1107,12 @@ __global__ void __launch_bounds__(128) k_screen_agg(const float* __restrict__ V3
     part_a[blockIdx.y * part_stride + cand0 + (int64_t)blockIdx.x * 128 + threadIdx.x] = 0.0;
     return;
   }
-  extern __shared__ float cs[];  // DR == 0: c' of the block, [k][thread]; then the tile list
+  extern __shared__ __align__(16) double agg_sm[];  // W[d], Wp[128], then the tile list
+  double* W = agg_sm;
+  double* Wp = agg_sm + d;
+  uint16_t* tl = reinterpret_cast<uint16_t*>(agg_sm + d + 128);
   __shared__ int wsum[4];
+  __shared__ double red[5][4];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int t0 = blockIdx.y * tiles_per_split;
   const int t1 = min(ntiles, t0 + tiles_per_split);
@@ -1115,7 +1126,6 @@ __global__ void __launch_bounds__(128) k_screen_agg(const float* __restrict__ V3
     const float* rho = an.rho + (int64_t)anc * an.kpstride;
     const float* rhx = an.rhomax + (int64_t)anc * an.kpstride;
     // the block's all-positive tiles, classified once (same tests as the screen)
-    uint16_t* tl = reinterpret_cast<uint16_t*>(cs + (DR > 0 ? 0 : 128 * d));
     int nl = 0;
     for (int i0 = 0; i0 < nt; i0 += 128) {
       const int i = i0 + tid;
@@ -1131,57 +1141,69 @@ __global__ void __launch_bounds__(128) k_screen_agg(const float* __restrict__ V3
       __syncthreads();
     }
     if (nl > 0) {
+      const float* kpa = an.kpmax + (int64_t)anc * an.kpstride;
+      const double* ips = ipsum + (int64_t)anc * an.kpstride;
+      // the block's scalar sums: per-thread strided partials, butterfly, warps in order
+      double sv[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+      for (int li = tid; li < nl; li += 128) {
+        const int t = t0 + tl[li];
+        const double nt_pts = (double)min((int64_t)np, n - (int64_t)t * np);
+        sv[0] += ips[t];
+        sv[1] += nt_pts;
+        sv[2] += nt_pts * (double)kpa[t];
+        sv[3] += nt_pts * (double)__ldg(an.vmax + t);
+        sv[4] += (double)vsn[t];
+      }
+#pragma unroll
+      for (int j = 0; j < 5; ++j) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sv[j] += __shfl_xor_sync(0xffffffffu, sv[j], o);
+        if (lane == 0) red[j][warp] = sv[j];
+      }
+      // W = sum of the tiles' vsum rows: groups of d threads take every T-th tile
+      if (d <= 128) {
+        const int T = 128 / d, g = tid / d, k = tid - g * d;
+        if (g < T) {
+          double p = 0.0;
+          for (int li = g; li < nl; li += T) p += (double)__ldg(vsum + (int64_t)(t0 + tl[li]) * pitch + k);
+          Wp[g * d + k] = p;
+        }
+        __syncthreads();
+        if (tid < d) {
+          double w = 0.0;
+          for (int q = 0; q < T; ++q) w += Wp[q * d + tid];
+          W[tid] = w;
+        }
+      } else {
+        for (int k = tid; k < d; k += 128) {
+          double p = 0.0;
+          for (int li = 0; li < nl; ++li) p += (double)__ldg(vsum + (int64_t)(t0 + tl[li]) * pitch + k);
+          W[k] = p;
+        }
+      }
+      __syncthreads();
+      double S[5];
+#pragma unroll
+      for (int j = 0; j < 5; ++j) S[j] = ((red[j][0] + red[j][1]) + red[j][2]) + red[j][3];
       const float* mu = an.mu + (int64_t)anc * an.apitch;
       const float* row = V32 + c * pitch;
       float cn2 = 0.f, mc = 0.f, mn2 = 0.f;
-      float cp[DR > 0 ? DR : 1];
-#pragma unroll
-      for (int k = 0; k < (DR > 0 ? DR : 1); ++k) cp[k] = 0.f;
+      double dot = 0.0;
       for (int k = 0; k < d; ++k) {  // the screen's c' = fl(c - mu) and its sums, same order
         const float m = mu[k];
         const float x = row[k] - m;
         cn2 = fmaf(x, x, cn2);
         mc = fmaf(m, x, mc);
         mn2 = fmaf(m, m, mn2);
-        if constexpr (DR > 0) {
-#pragma unroll
-          for (int q = 0; q < DR; ++q)
-            if (q == k) cp[q] = x;
-        } else {
-          cs[k * 128 + tid] = x;
-        }
+        dot = fma((double)x, W[k], dot);
       }
       const float cn = sqrtf(cn2) * (1.f + 1e-5f);
       const float ic = -(mc + 0.5f * cn2);
       const float kc = an.kc * (sqrtf(mn2) * (1.f + 1e-5f) * cn + cn2);
       const float kxc = an.kx * cn;
-      const float* kpa = an.kpmax + (int64_t)anc * an.kpstride;
-      const double* ips = ipsum + (int64_t)anc * an.kpstride;
       const double edot = (double)(d + 2) * 5.960464477539063e-08 * 1.01 * (double)cn;
-      for (int li = 0; li < nl; ++li) {
-        const int t = t0 + tl[li];
-        const float* vs = vsum + (int64_t)t * pitch;
-        float dot;
-        if constexpr (DR > 0) {
-          // four independent partial dots over 128-bit (warp-broadcast) loads
-          float p4[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-          for (int k = 0; k < DR; k += 4) {
-            const float4 w4 = __ldg(reinterpret_cast<const float4*>(vs) + (k >> 2));
-            p4[0] = fmaf(cp[k], w4.x, p4[0]);
-            p4[1] = fmaf(cp[k + 1], w4.y, p4[1]);
-            p4[2] = fmaf(cp[k + 2], w4.z, p4[2]);
-            p4[3] = fmaf(cp[k + 3], w4.w, p4[3]);
-          }
-          dot = (p4[0] + p4[1]) + (p4[2] + p4[3]);
-        } else {
-          dot = 0.f;
-          for (int k = 0; k < d; ++k) dot = fmaf(cs[k * 128 + tid], __ldg(vs + k), dot);
-        }
-        const float kq = kpa[t] + fmaf(kxc, __ldg(an.vmax + t), kc);
-        const int64_t nt_pts = min((int64_t)np, n - (int64_t)t * np);
-        acc += ips[t] + (double)dot + (double)nt_pts * ((double)ic + (double)kq) + edot * (double)vsn[t];
-      }
+      const double kqs = (S[2] + (double)kxc * S[3] + (double)kc * S[1]) * (1.0 + 0x1p-21);
+      acc = S[0] + dot + (double)ic * S[1] + kqs + edot * S[4];
     }
   }
   part_a[blockIdx.y * part_stride + c] = acc;
