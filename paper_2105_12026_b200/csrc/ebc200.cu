@@ -312,6 +312,8 @@ struct ebc_ctx {
   int lazy_batch = 4;              // EBC200_LAZY_BATCH (1..RW): candidates refined first in a lazy step
   bool probe_on = true;            // EBC200_LAZY_PROBE=0: no ring-probe batch on undecided steps
   ProbeBuf probe;                  // k_lazy_rings: ring winners, ticket, the probe list
+  bool nb_on = false;              // EBC200_LAZY_NEARBOUND=0: no near-centre bound (k_lazy_nearbound)
+  ChunkGeo geo;                    // per-chunk mean / radius / e0 sums for the near-centre bound
   unsigned int* counter3 = nullptr;  // k_refine's finalize ticket
   bool refine2 = true;             // EBC200_REFINE2=0: the lazy batch on the classic k_refine
   DevBuf rterms;                   // RW x nchunks chunk sums of the short refine
@@ -1207,6 +1209,18 @@ int run_step_select(ebc_ctx* ctx, int step, int commit, int64_t* sel_dev) {
       ctx->cmx_fresh = false;
       if (rc) return rc;
     }
+    if (ctx->nb_on && has_screen) {
+      // near-centre bound: the neighbours of the centre just selected leave the
+      // stale set without a screen (k_lazy_nearbound)
+      const bool regs = ctx->d <= 32;
+      const size_t nsm = ((size_t)ctx->geo.dp * (NB_TILE + 1) + (regs ? 0 : (size_t)ctx->d * NB_CPB)) * sizeof(float);
+      auto kern = regs ? k_lazy_nearbound<32> : k_lazy_nearbound<0>;
+      CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nsm));
+      kern<<<(unsigned)((ncand + NB_CPB - 1) / NB_CPB), 256, nsm, ctx->stream>>>(
+          ctx->c0, ctx->c1, ctx->V32, ctx->pitch, ctx->d, ctx->best, ctx->ubp, ctx->selected, ctx->maxlb, margin,
+          ctx->level, ctx->geo, ctx->chunkpart, ctx->n);
+      KCHECK();
+    }
     CU(cudaMemsetAsync(ctx->bflag, 0, (size_t)((ncand + tc::M - 1) / tc::M + 2), ctx->stream));
     k_lazy_mark2<<<fin_blocks, 256, 0, ctx->stream>>>(ctx->c0, ctx->c1, ctx->ubp, ctx->selected, ctx->maxlb,
                                                       margin, ctx->bcnt, ctx->bflag, ctx->level);
@@ -1453,7 +1467,8 @@ void free_ctx(ebc_ctx* c) {
   cudaSetDevice(c->device);
   void* ptrs[] = {c->V32, c->V64, c->e0d, c->cm64, c->pt, c->nv32, c->level, c->stats, c->Vhi, c->Vlo, c->Vf, c->tile_anchor0, c->rhomax, c->cmn, c->vsum, c->vsn, c->ipsum, c->rhomin, c->agg_any, c->pttc, c->kpmax, c->anchors, c->nva, c->tile_anchor, c->tc_vmax, c->fps_keys, c->ipa0, c->tile_rad, c->crad, c->rho, c->cmx, c->cmx0, c->selected, c->chunkpart, c->counter, c->counter2, c->topc, c->toppart, c->terms, c->cur, c->best, c->uf_ctr,
                   c->maxlb, c->wcount, c->wlist, c->wgain, c->ub, c->ubp, c->bflag, c->slist, c->scount,
-                  c->lazy_part, c->ub_next, c->counter3, c->bcnt, c->Vg, c->g_anchor, c->g_rad, c->probe.rkey};
+                  c->lazy_part, c->ub_next, c->counter3, c->bcnt, c->Vg, c->g_anchor, c->g_rad, c->probe.rkey,
+                  c->geo.mu, c->geo.r, c->geo.mn, c->geo.e0s, c->geo.muf};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, c->stream);
   DevBuf* bufs[] = {&c->tie_rec, &c->tie_all, &c->sel_hash, &c->ms_tanchor, &c->ms_trad, &c->part_g, &c->part_e, &c->part_a, &c->part_r, &c->rterms, &c->sv_cm, &c->sv_de, &c->sv_slots, &c->sv_part, &c->sv_out, &c->sel_out, &c->val_out, &c->gain_out, &c->ms_part,
@@ -1977,6 +1992,22 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
                                                                 ctx->e0d, ctx->cm64, ctx->nv32, ctx->pt, ctx->chunkpart);
   CUC(cudaGetLastError());
   mark("init");
+  {
+    const char* nb = getenv("EBC200_LAZY_NEARBOUND");
+    ctx->nb_on = ctx->lazy_on && dtype != EBC_F64 && d <= 256 && !(nb && nb[0] == '0');
+    if (ctx->nb_on) {
+      ctx->geo.nchunks = (int)ctx->nchunks;
+      CUC(cudaMallocAsync((void**)&ctx->geo.mu, (size_t)ctx->nchunks * d * sizeof(double), ctx->stream));
+      CUC(cudaMallocAsync((void**)&ctx->geo.r, (size_t)ctx->nchunks * sizeof(double), ctx->stream));
+      CUC(cudaMallocAsync((void**)&ctx->geo.mn, (size_t)ctx->nchunks * sizeof(double), ctx->stream));
+      CUC(cudaMallocAsync((void**)&ctx->geo.e0s, (size_t)ctx->nchunks * sizeof(double), ctx->stream));
+      ctx->geo.dp = (d + 3) / 4 * 4;
+      CUC(cudaMallocAsync((void**)&ctx->geo.muf, (size_t)ctx->nchunks * ctx->geo.dp * sizeof(float), ctx->stream));
+      k_chunk_geo<<<(unsigned)ctx->nchunks, 256, (size_t)d * sizeof(double), ctx->stream>>>(ctx->V32, ctx->pitch, n,
+                                                                                          d, ctx->e0d, ctx->geo);
+      CUC(cudaGetLastError());
+    }
+  }
   if (ctx->tc_np) {
     {
       // anchors (farthest-point sampling from the origin), |v - mu_a|^2, the

@@ -1247,6 +1247,207 @@ __global__ void __launch_bounds__(256) k_lazy_rings(int64_t c0, int64_t c1, cons
   }
 }
 
+// Chunk geometry for the near-centre bound (k_lazy_nearbound), once per
+// context: per RCH-point chunk T its fp64 mean mu_T, radius r_T >= max |v - mu_T|
+// (rounded up), |mu_T|, the sum of e0d over it, and its point count.
+struct ChunkGeo {
+  double* mu = nullptr;   // nchunks x d
+  double* r = nullptr;    // nchunks
+  double* mn = nullptr;   // nchunks: |mu_T|
+  double* e0s = nullptr;  // nchunks: sum of e0d (fixed order)
+  float* muf = nullptr;   // nchunks x dp: mu_T rounded to fp32 (zero padded)
+  int dp = 0;
+  int nchunks = 0;
+};
+__global__ void __launch_bounds__(256) k_chunk_geo(const float* __restrict__ V32, int pitch, int64_t n, int d,
+                                                   const double* __restrict__ e0d, ChunkGeo g) {
+  extern __shared__ double cmu[];  // d
+  __shared__ double red[8];
+  const int ch = blockIdx.x, tid = threadIdx.x;
+  const int64_t v0 = (int64_t)ch * RCH;
+  const int np = (int)min((int64_t)RCH, n - v0);
+  for (int k = tid; k < d; k += blockDim.x) {
+    double s = 0.0;
+    for (int j = 0; j < np; ++j) s += (double)V32[(v0 + j) * pitch + k];
+    cmu[k] = s / (double)np;
+    g.mu[(int64_t)ch * d + k] = cmu[k];
+  }
+  for (int k = tid; k < g.dp; k += blockDim.x) g.muf[(int64_t)ch * g.dp + k] = k < d ? (float)cmu[k] : 0.f;
+  __syncthreads();
+  double rmax = 0.0, es = 0.0;
+  for (int j = tid; j < np; j += blockDim.x) {
+    double q = 0.0;
+    for (int k = 0; k < d; ++k) {
+      const double x = (double)V32[(v0 + j) * pitch + k] - cmu[k];
+      q = fma(x, x, q);
+    }
+    rmax = fmax(rmax, q);
+    es += e0d[v0 + j];
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+    es += __shfl_xor_sync(0xffffffffu, es, o);
+  }
+  if ((tid & 31) == 0) red[tid >> 5] = rmax;
+  __syncthreads();
+  if (tid == 0) {
+    double m = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, red[w]);
+    g.r[ch] = sqrt(m) * (1.0 + 1e-9);
+    double q = 0.0;
+    for (int k = 0; k < d; ++k) q = fma(cmu[k], cmu[k], q);
+    g.mn[ch] = sqrt(q) * (1.0 + 1e-9);
+  }
+  __syncthreads();
+  if ((tid & 31) == 0) red[tid >> 5] = es;
+  __syncthreads();
+  if (tid == 0) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+    g.e0s[ch] = s;
+  }
+}
+
+// Near-centre bound of an undecided lazy step (level[0] == -3), for every stale
+// candidate c (ubp >= the stale threshold).  With s the centre just selected,
+// cm(v) <= d(v, s), so
+//   gain(c) = sum_v max(0, cm(v) - d(v, c)) <= sum_v min(cm(v), max(0, d(v, s) - d(v, c)))
+// and d(v, s) - d(v, c) = 2 v.u + |s|^2 - |c|^2 (u = c - s) is linear in v: over
+// a chunk T, v.u <= mu_T.u + r_T |u|.  Hence
+//   gain(c) <= sum_T min(CM_T, n_T max(0, 2 mu_T.u + 2 r_T |u| + |s|^2 - |c|^2 + m_T))
+// with CM_T = sum of cm over T (= sum e0d - the update's chunk partial) and m_T
+// covering the fp64 roundings of d64 and of this evaluation.  Candidates next
+// to s (whose gains just collapsed -- on clustered data a whole cluster) get a
+// bound far below lb and leave the stale set without a screen; the bound is
+// stored in ubp (it bounds every later gain too).  A candidate whose partial
+// sum already reaches the threshold stops early and stays stale.
+constexpr int NB_CPB = 64;  // candidates per block (4 chunk groups of 64 threads)
+// The dot mu_T.u runs in fp32 (mu_T rounded to fp32 in muf, u = fl32(c - s)):
+// |error| <= (d + 4) 2^-24 |u| |mu_T| (products, partial sums, both roundings),
+// added to the bound.  Each candidate visits the chunks starting at its own
+// (on index-ordered clustered data its own cluster first, where a candidate far
+// from s reaches the threshold after a few chunks and stops).
+// Chunks are staged through shared memory NB_TILE at a time (fp32 means, the
+// per-chunk scalars, this step's CM_T), so the inner loop is shared-memory
+// broadcasts and FMAs; the block stops when every candidate has stopped.
+constexpr int NB_TILE = 64;
+template <int DR>  // DR > 0: u in DR registers (d <= DR); 0: u in shared memory
+__global__ void __launch_bounds__(256) k_lazy_nearbound(int64_t c0, int64_t c1, const float* __restrict__ V32,
+                                                        int pitch, int d, const int64_t* __restrict__ best,
+                                                        double* __restrict__ ubp,
+                                                        const unsigned char* __restrict__ selected,
+                                                        const long long* __restrict__ maxlb, double margin,
+                                                        const int* __restrict__ level, ChunkGeo g,
+                                                        const double* __restrict__ fpart, int64_t n) {
+  extern __shared__ float nbs[];  // s[dp], mu tile [NB_TILE][dp], then (DR == 0) u[d][NB_CPB]
+  __shared__ double part[4][NB_CPB];
+  __shared__ double tr[NB_TILE], tm[NB_TILE], tcm[NB_TILE], tn[NB_TILE];
+  __shared__ int stop[NB_CPB];
+  if (*level != -3) return;
+  const int tid = threadIdx.x, j = tid & (NB_CPB - 1), grp = tid >> 6;
+  const int dp = g.dp;
+  const int64_t c = c0 + (int64_t)blockIdx.x * NB_CPB + j;
+  const double lb = dkey_inv(*maxlb);
+  const double thr = lb - margin - 1e-9 * fabs(lb);
+  const bool stale = c < c1 && !selected[c] && ubp[c - c0] >= thr;
+  if (!__syncthreads_or(stale)) return;
+  const int64_t sb = *best;
+  float* sv = nbs;
+  float* mt = nbs + dp;
+  float* us = mt + NB_TILE * dp;
+  for (int k = tid; k < d; k += blockDim.x) sv[k] = V32[sb * pitch + k];
+  if (tid < NB_CPB) stop[tid] = 0;
+  __syncthreads();
+  // u = fl32(c - s) (registers or smem), |u| from the exact differences, |c|^2, |s|^2
+  float ur[DR > 0 ? DR : 1];
+  double q = 0.0, cc = 0.0, s2 = 0.0;
+  for (int k = 0; k < d; ++k) {
+    const float x = stale ? V32[c * pitch + k] : 0.f;
+    const double du = (double)x - (double)sv[k];
+    q = fma(du, du, q);
+    cc = fma((double)x, (double)x, cc);
+    s2 = fma((double)sv[k], (double)sv[k], s2);
+    const float uf = x - sv[k];
+    if constexpr (DR > 0) {
+#pragma unroll
+      for (int r = 0; r < DR; ++r)
+        if (r == k) ur[r] = uf;
+    } else if (grp == 0) {
+      us[k * NB_CPB + j] = uf;
+    }
+  }
+  if constexpr (DR > 0) {
+#pragma unroll
+    for (int r = 0; r < DR; ++r)
+      if (r >= d) ur[r] = 0.f;
+  }
+  if (!stale && grp == 0) stop[j] = 1;
+  const double un = sqrt(q) * (1.0 + 1e-12);
+  const double mrel = 2.0 * (4e-12 + 1e-15 * (double)(d + 1));  // (a + b)^2 <= 2 a^2 + 2 b^2
+  const double snc = fmax(sqrt(s2), sqrt(cc)) + un;
+  const double cst = s2 - cc + mrel * snc * snc;  // per candidate
+  const double kdot = 2.0 * (double)(d + 4) * 0x1p-24 * 1.01 * un;
+  const double un2 = 2.0 * un;
+  const int tstart = (int)min((int64_t)g.nchunks - 1, max((int64_t)0, (c0 + (int64_t)blockIdx.x * NB_CPB) / RCH));
+  double acc = 0.0;
+  bool mystop = !stale;
+  for (int i0 = 0; i0 < g.nchunks; i0 += NB_TILE) {
+    const int nt = min(NB_TILE, g.nchunks - i0);
+    __syncthreads();  // previous tile consumed; stop flags visible
+    if (__syncthreads_and(stop[j] != 0)) break;
+    for (int e = tid; e < nt * dp; e += blockDim.x) {
+      const int ti = e / dp, k = e - ti * dp;
+      int T = tstart + i0 + ti;
+      if (T >= g.nchunks) T -= g.nchunks;
+      mt[e] = __ldg(g.muf + (int64_t)T * dp + k);
+    }
+    if (tid < nt) {
+      int T = tstart + i0 + tid;
+      if (T >= g.nchunks) T -= g.nchunks;
+      const double rT = g.r[T], mnT = g.mn[T], e0s = g.e0s[T];
+      tr[tid] = rT;
+      tm[tid] = mnT;
+      tcm[tid] = e0s - __ldcg(fpart + T) + 1e-12 * e0s;
+      tn[tid] = (double)min((int64_t)RCH, n - (int64_t)T * RCH);
+    }
+    __syncthreads();
+    if (mystop || stop[j]) continue;
+    for (int ti = grp; ti < nt; ti += 4) {
+      const float* mu = mt + ti * dp;
+      float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+      if constexpr (DR > 0) {
+#pragma unroll
+        for (int k = 0; k < DR; k += 4) {
+          if (k >= dp) break;
+          const float4 m4 = *reinterpret_cast<const float4*>(mu + k);
+          a0 = fmaf(ur[k], m4.x, a0);
+          a1 = fmaf(ur[k + 1], m4.y, a1);
+          a2 = fmaf(ur[k + 2], m4.z, a2);
+          a3 = fmaf(ur[k + 3], m4.w, a3);
+        }
+      } else {
+        for (int k = 0; k < d; ++k) a0 = fmaf(us[k * NB_CPB + j], mu[k], a0);
+      }
+      const float dot = (a0 + a1) + (a2 + a3);
+      const double rT = tr[ti], mnT = tm[ti];
+      const double MT = mnT + rT;
+      const double ell = fma(2.0, (double)dot, fma(rT, un2, fma(mnT, kdot, fma(mrel * MT, MT, cst))));
+      if (ell > 0.0) acc += fmin(tcm[ti], tn[ti] * ell);
+    }
+    if (acc >= thr) {  // cannot leave the stale set: stop every group of the candidate
+      mystop = true;
+      stop[j] = 1;
+    }
+  }
+  __syncthreads();
+  part[grp][j] = acc;
+  __syncthreads();
+  if (grp == 0 && stale && !stop[j]) {
+    const double b = (((part[0][j] + part[1][j]) + part[2][j]) + part[3][j]) * (1.0 + 1e-12);
+    if (b < ubp[c - c0]) ubp[c - c0] = b;
+  }
+}
+
 // Undecided lazy step (level[0] == -3): list the stale candidates
 // ubp[c] >= lb - margin - 1e-9 |lb| (lb = *maxlb, the batch's best exact gain)
 // in slist (count *scount) and flag their 128-candidate blocks.
