@@ -542,7 +542,7 @@ def run_ours(args):
         "clocks": clk,
         "e2e": {"value": E / (e2e_step * 1e-3), "unit": "point-candidate evals/s", "ms_per_step": e2e_step,
                 "h2d_bytes_per_step": int(h2d) * world, "d2h_bytes_per_step": int(d2h) * world,
-                "path": "EbcFunction(GroundMatrix) + greedy_maximize%s via libebc200.so C-ABI, pageable host buffers"
+                "path": "EbcFunction(GroundMatrix) + greedy_maximize%s via libebc200.so C-ABI; host rows page-locked (the GroundMatrix's buffer, registered at its first context), results to pageable host memory"
                         % ("_sharded (every rank uploads V)" if distributed else "")},
         "gpu_launches": int(sum(r["launches"] for r in ranks)),
     }

@@ -214,6 +214,15 @@ int ebc_screen_info(const ebc_ctx* ctx, int64_t* out4);
  * (submodularity), so the selection is unchanged. */
 int ebc_last_lazy_stats(const ebc_ctx* ctx, int64_t* out4);
 
+/* Page-lock a host buffer for direct DMA (cudaHostRegister, portable) /
+ * release it.  No reference counterpart: the reference keeps its ground in
+ * ordinary numpy memory.  A GroundMatrix's rows are registered once
+ * (ebc.py), so every ebc_create from them uploads by one direct copy instead
+ * of the staged pageable path.  ebc_host_register returns EBC_ECUDA (and
+ * leaves the buffer pageable) when the driver refuses. */
+int ebc_host_register(const void* ptr, int64_t bytes);
+int ebc_host_unregister(const void* ptr);
+
 /* Kernel launches issued by the last call (bench.py's gpu_launches). */
 int64_t ebc_last_launches(const ebc_ctx* ctx);
 

@@ -51,6 +51,8 @@ SIGNATURES = {
     "ebc_last_launches": (_i64, [_vp]),
     "ebc_last_stats": (ctypes.c_int, [_vp, _i64p]),
     "ebc_last_lazy_stats": (ctypes.c_int, [_vp, _i64p]),
+    "ebc_host_register": (ctypes.c_int, [_vp, _i64]),
+    "ebc_host_unregister": (ctypes.c_int, [_vp]),
     "ebc_last_screen_work": (ctypes.c_int, [_vp, _i64p]),
     "ebc_comm_id_bytes": (ctypes.c_int64, []),
     "ebc_comm_unique_id": (ctypes.c_int, [ctypes.c_char_p, _i64]),

@@ -436,6 +436,12 @@ int ensure(ebc_ctx* ctx, DevBuf& b, size_t bytes) {
 // Row pitch (elements) of the device copy: 16-byte rows; for fp32 the pitch in
 // float4 units is odd so that 4 or 8 consecutive rows read by one LDS.128 hit
 // disjoint bank groups.
+// Dynamic shared memory of k_tile_anchor's staged form (0: the looped form).
+size_t tile_anchor_smem(const ebc_ctx* ctx) {
+  const size_t b = (size_t)ctx->tc_na * ((ctx->d + 3) / 4 * 4) * sizeof(float);
+  return ctx->tc_na <= NA_ALL && b <= 160 * 1024 ? b : 0;
+}
+
 int pitch_for(int d, int dtype) {
   if (dtype == EBC_F64) return (d + 1) / 2 * 2;
   int p = (d + 3) / 4 * 4;
@@ -948,10 +954,9 @@ int run_gathered_window(ebc_ctx* ctx, int fin_blocks) {
                                                           (int)ctx->gath_cap, ctx->Vg, ctx->ub, ncand, ctx->level,
                                                           L_GATHER);
   KCHECK();
-  k_tile_anchor<<<(unsigned)(ctx->gath_cap / tc::M), 128, 0, ctx->stream>>>(ctx->Vg, ctx->pitch, ctx->gath_cap, ctx->d,
-                                                                          ctx->anchors, ctx->pitch, ctx->tc_na,
-                                                                          ctx->g_anchor, ctx->g_rad, ctx->scount,
-                                                                          ctx->level, L_GATHER);
+  k_tile_anchor<<<(unsigned)(ctx->gath_cap / tc::M), 128, tile_anchor_smem(ctx), ctx->stream>>>(
+      ctx->Vg, ctx->pitch, ctx->gath_cap, ctx->d, ctx->anchors, ctx->pitch, ctx->tc_na, ctx->g_anchor, ctx->g_rad,
+      tile_anchor_smem(ctx) > 0, ctx->scount, ctx->level, L_GATHER);
   KCHECK();
   switch (ctx->tc_kind) {
     case tc::KIND_BF16:
@@ -1243,6 +1248,7 @@ int run_step_select(ebc_ctx* ctx, int step, int commit, int64_t* sel_dev) {
       if (mode == -4) return fail(ctx, EBC_ECUDA, "lazy step: mode read-back failed");
       if (getenv("EBC200_LAZY_TRACE")) {  // development aid: stale-set shape per eager lazy step
         int cnt = 0;
+        cudaStreamSynchronize(ctx->stream);
         std::vector<unsigned char> fl((size_t)((ncand + tc::M - 1) / tc::M));
         cudaMemcpy(&cnt, ctx->scount, sizeof(int), cudaMemcpyDeviceToHost);
         cudaMemcpy(fl.data(), ctx->bflag, fl.size(), cudaMemcpyDeviceToHost);
@@ -1273,6 +1279,12 @@ int run_step_select(ebc_ctx* ctx, int step, int commit, int64_t* sel_dev) {
     ctx->cmx_fresh = ctx->cmx_valid;
     rc = enqueue_refine(ctx, ng, ctx->level, fin);
     if (rc) return rc;
+    if (sync && getenv("EBC200_LAZY_TRACE")) {
+      long long st[2] = {0, 0};
+      cudaStreamSynchronize(ctx->stream);
+      cudaMemcpy(st, ctx->stats, sizeof(st), cudaMemcpyDeviceToHost);
+      fprintf(stderr, "[lazy] step %d window sum %lld max %lld\n", step, st[0], st[1]);
+    }
     CU(ca.close());
   }
   // lazy steps record only eb + 1 (here) and eb + 3 (after the update): greedy_run
@@ -1539,9 +1551,9 @@ int multiset_sparse(ebc_ctx* ctx, int64_t l, int64_t nnz) {
       KCHECK();
     }
     if (!rc) {
-      k_tile_anchor<<<(unsigned)((nnz + 127) / 128), 128, 0, ctx->stream>>>(
+      k_tile_anchor<<<(unsigned)((nnz + 127) / 128), 128, tile_anchor_smem(ctx), ctx->stream>>>(
           (const float*)ctx->ms_mbuf.p, ctx->pitch, nnz, ctx->d, ctx->anchors, ctx->pitch, ctx->tc_na,
-          (int*)ctx->ms_tanchor.p, (float*)ctx->ms_trad.p);
+          (int*)ctx->ms_tanchor.p, (float*)ctx->ms_trad.p, tile_anchor_smem(ctx) > 0);
       KCHECK();
       rc = launch_tc_flag(ctx, tp, (const float*)ctx->ms_mbuf.p, (const int*)ctx->ms_tanchor.p,
                           (const float*)ctx->ms_trad.p, fo);
@@ -1733,7 +1745,12 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
   {
     const size_t bytes = (size_t)n * d * src_esz;
     const char* su = getenv("EBC200_STAGED_UPLOAD");
-    const bool staged = bytes >= (16u << 20) && !(su && su[0] == '0') && staged_upload(ctx->stream, raw, V, bytes);
+    // page-locked source (ebc_host_register): one direct DMA; pageable: staged
+    cudaPointerAttributes pa{};
+    const bool pinned = cudaPointerGetAttributes(&pa, V) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+    (void)cudaGetLastError();
+    const bool staged = !pinned && bytes >= (16u << 20) && !(su && su[0] == '0') &&
+                        staged_upload(ctx->stream, raw, V, bytes);
     if (!staged) CUC(cudaMemcpyAsync(raw, V, bytes, cudaMemcpyHostToDevice, ctx->stream));
   }
   mark("upload");
@@ -2014,18 +2031,51 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
       // anchor of each candidate block, seeds and per-tile error quanta
       float* mind = nullptr;
       CUC(cudaMallocAsync((void**)&mind, (size_t)n * sizeof(float), ctx->stream));
-      for (int a = 0; a < ctx->tc_na; ++a) {
-        k_fps_step<<<2 * ctx->num_sms, 256, 0, ctx->stream>>>(ctx->V32, ctx->pitch, n, d, a, ctx->tc_na, mind,
-                                                              ctx->fps_keys, ctx->anchors, ctx->pitch);
-        CUC(cudaGetLastError());
+      {
+        // one cooperative launch (grid barrier per anchor); per-anchor launches
+        // if the cooperative launch is refused -- the same anchors either way
+        int per_sm = 0;
+        const size_t fsm = (size_t)(d + 3) / 4 * 4 * sizeof(float);
+        bool coop = fsm <= 48 * 1024 &&
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fps_all, 256, fsm) == cudaSuccess &&
+                    per_sm > 0;
+        unsigned int* bar = nullptr;
+        if (coop) {
+          CUC(cudaMallocAsync((void**)&bar, 2 * sizeof(unsigned int), ctx->stream));
+          CUC(cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned int), ctx->stream));
+          const float* v32 = ctx->V32;
+          int pitch_ = ctx->pitch, d_ = d, na_ = ctx->tc_na, ap_ = ctx->pitch;
+          int64_t n_ = n;
+          void* args[] = {(void*)&v32, &pitch_, &n_, &d_, &na_, (void*)&mind, (void*)&ctx->fps_keys,
+                          (void*)&ctx->anchors, &ap_, (void*)&bar};
+          coop = cudaLaunchCooperativeKernel((const void*)k_fps_all, dim3(std::min(per_sm, 2) * ctx->num_sms),
+                                             dim3(256), args, fsm, ctx->stream) == cudaSuccess;
+          if (!coop) (void)cudaGetLastError();
+          cudaFreeAsync(bar, ctx->stream);
+        }
+        if (!coop)
+          for (int a = 0; a < ctx->tc_na; ++a) {
+            k_fps_step<<<2 * ctx->num_sms, 256, 0, ctx->stream>>>(ctx->V32, ctx->pitch, n, d, a, ctx->tc_na, mind,
+                                                                  ctx->fps_keys, ctx->anchors, ctx->pitch);
+            CUC(cudaGetLastError());
+          }
       }
       mark("fps anchors");
-      k_nva<<<8 * ctx->num_sms, 256, 0, ctx->stream>>>(ctx->V32, ctx->pitch, n, d, ctx->anchors, ctx->pitch,
-                                                       ctx->tc_na, ctx->nva, ctx->n_pad);
+      const size_t nsm = (size_t)ctx->tc_na * ((d + 3) / 4 * 4) * sizeof(double);
+      if (ctx->tc_na <= NA_ALL && nsm <= 160 * 1024) {
+        CUC(cudaFuncSetAttribute(k_nva_all, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+        k_nva_all<<<(unsigned)((n + 127) / 128), 128, nsm, ctx->stream>>>(ctx->V32, ctx->pitch, n, d, ctx->anchors,
+                                                                         ctx->pitch, ctx->tc_na, ctx->nva,
+                                                                         ctx->n_pad);
+      } else {
+        k_nva<<<8 * ctx->num_sms, 256, 0, ctx->stream>>>(ctx->V32, ctx->pitch, n, d, ctx->anchors, ctx->pitch,
+                                                         ctx->tc_na, ctx->nva, ctx->n_pad);
+      }
       CUC(cudaGetLastError());
-      k_tile_anchor<<<(unsigned)((n + 127) / 128), 128, 0, ctx->stream>>>(ctx->V32, ctx->pitch, n, d, ctx->anchors,
-                                                                          ctx->pitch, ctx->tc_na, ctx->tile_anchor,
-                                                                          ctx->tile_rad);
+      CUC(cudaFuncSetAttribute(k_tile_anchor, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+      k_tile_anchor<<<(unsigned)((n + 127) / 128), 128, tile_anchor_smem(ctx), ctx->stream>>>(
+          ctx->V32, ctx->pitch, n, d, ctx->anchors, ctx->pitch, ctx->tc_na, ctx->tile_anchor, ctx->tile_rad,
+          tile_anchor_smem(ctx) > 0);
       CUC(cudaGetLastError());
       CUC(cudaMallocAsync((void**)&ctx->crad, (size_t)n * sizeof(float), ctx->stream));
       k_cand_rad<float><<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(ctx->V32, ctx->pitch, n, d,
@@ -2054,21 +2104,29 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
       CUC(cudaStreamSynchronize(ctx->stream));
       mark("init + anchors");
       cudaFreeAsync(mind, ctx->stream);
-      if (ctx->tc_agg) {
+      // the scalars below from one device pass (k_create_maxes) and one 32-byte copy
+      double max_e0d = 0.0, max_nv = 0.0;
+      float vmx = 0.f;
+      {
+        unsigned long long hm[4] = {0ull, 0ull, 0ull, 0x7f800000ull};
+        unsigned long long* dm = nullptr;
+        CUC(cudaMallocAsync((void**)&dm, sizeof(hm), ctx->stream));
+        CUC(cudaMemcpyAsync(dm, hm, sizeof(hm), cudaMemcpyHostToDevice, ctx->stream));
+        k_create_maxes<<<2 * ctx->num_sms, 256, 0, ctx->stream>>>(ctx->e0d, ctx->nv32, n, ctx->tc_vmax, ctx->tc_ntl,
+                                                                 ctx->tile_rad, (n + 127) / 128, dm);
+        CUC(cudaGetLastError());
+        CUC(cudaMemcpyAsync(hm, dm, sizeof(hm), cudaMemcpyDeviceToHost, ctx->stream));
+        CUC(cudaStreamSynchronize(ctx->stream));
+        cudaFreeAsync(dm, ctx->stream);
+        max_e0d = __builtin_bit_cast(double, hm[0]);
+        max_nv = (double)__builtin_bit_cast(float, (unsigned int)hm[1]);
+        vmx = __builtin_bit_cast(float, (unsigned int)hm[2]);
         // smallest candidate-block radius (k_tile_ipsum's any-block screen)
-        std::vector<float> rad((size_t)((n + 127) / 128));
-        CUC(cudaMemcpy(rad.data(), ctx->tile_rad, rad.size() * sizeof(float), cudaMemcpyDeviceToHost));
-        float rm = INFINITY;
-        for (float r : rad) rm = std::min(rm, r);
-        ctx->radmin = rm;
+        if (ctx->tc_agg) ctx->radmin = __builtin_bit_cast(float, (unsigned int)hm[3]);
       }
       if (ctx->tc_fast) {
         // operand scale s = 2^e: every |s c'_k| <= s (|c| + |mu|) <= 2 s max|v| <= 2^15
         // (fp16 max 65504); |e| <= 60 keeps s^2 and 1/s^2 normal in fp32
-        std::vector<float> vm((size_t)ctx->tc_ntl);
-        CUC(cudaMemcpy(vm.data(), ctx->tc_vmax, vm.size() * sizeof(float), cudaMemcpyDeviceToHost));
-        float vmx = 0.f;
-        for (float x : vm) vmx = std::max(vmx, x);
         int e = vmx > 0.f ? (int)std::floor(std::log2(std::ldexp(1.0, 14) / (double)vmx)) : 0;
         e = std::max(-60, std::min(60, e));
         ctx->tc_oscale = (float)std::ldexp(1.0, e);
@@ -2083,15 +2141,7 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
       const bool one_rung = ctx->tc_fast || ctx->tc_kind == tc::KIND_F16;
       const char* ms_env = getenv("EBC200_TC_MSEED");
       if (one_rung && ctx->kpad - d >= 3 && !(ms_env && ms_env[0] == '0')) {
-        std::vector<double> e0h((size_t)n);
-        std::vector<float> nvh((size_t)n);
-        CUC(cudaMemcpy(e0h.data(), ctx->e0d, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost));
-        CUC(cudaMemcpy(nvh.data(), ctx->nv32, (size_t)n * sizeof(float), cudaMemcpyDeviceToHost));
-        double me = 0.0, mv = 0.0;
-        for (int64_t i = 0; i < n; ++i) {
-          me = std::max(me, e0h[(size_t)i]);
-          mv = std::max(mv, (double)nvh[(size_t)i]);
-        }
+        const double me = max_e0d, mv = max_nv;
         const double bip = 0.5 * (me + mv) * 1.01 + 1e-30;
         if (ctx->tc_fast) {
           const int e2 = (int)std::floor(0.5 * std::log2(std::ldexp(1.0, 14) / bip));
@@ -2203,6 +2253,24 @@ int ebc_last_screen_work(const ebc_ctx* ctx, int64_t* out_pairs) {
   if (cudaMemcpy(v, ctx->stats, sizeof(v), cudaMemcpyDeviceToHost) != cudaSuccess)
     return fail(const_cast<ebc_ctx*>(ctx), EBC_ECUDA, "ebc_last_screen_work: copy failed");
   *out_pairs = (int64_t)v[4] * tc::M * (ctx->tc_np ? ctx->tc_np : 0);
+  return EBC_OK;
+}
+
+int ebc_host_register(const void* ptr, int64_t bytes) {
+  if (!ptr || bytes <= 0) return fail(nullptr, EBC_EINVAL, "ebc_host_register: NULL or empty buffer");
+  if (cudaHostRegister(const_cast<void*>(ptr), (size_t)bytes, cudaHostRegisterPortable) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return fail(nullptr, EBC_ECUDA, "ebc_host_register: cudaHostRegister refused");
+  }
+  return EBC_OK;
+}
+
+int ebc_host_unregister(const void* ptr) {
+  if (!ptr) return fail(nullptr, EBC_EINVAL, "ebc_host_unregister: NULL buffer");
+  if (cudaHostUnregister(const_cast<void*>(ptr)) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return fail(nullptr, EBC_ECUDA, "ebc_host_unregister: not registered");
+  }
   return EBC_OK;
 }
 

@@ -1247,6 +1247,37 @@ __global__ void __launch_bounds__(256) k_lazy_rings(int64_t c0, int64_t c1, cons
   }
 }
 
+// Create-time maxima in one pass (no host copies of whole arrays): [0] max e0d
+// (fp64 bits), [1] max |v|^2, [2] max per-tile |v|max, [3] min block radius
+// (fp32 bits; all values are non-negative, so their bits order like them).
+__global__ void k_create_maxes(const double* __restrict__ e0d, const float* __restrict__ nv32, int64_t n,
+                               const float* __restrict__ vmax, int64_t ntl, const float* __restrict__ rad,
+                               int64_t nrad, unsigned long long* __restrict__ out) {
+  unsigned long long me = 0;
+  unsigned int mv = 0, mx = 0, mr = 0x7f800000u;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    me = max(me, (unsigned long long)__double_as_longlong(fmax(e0d[i], 0.0)));
+    mv = max(mv, __float_as_uint(fmaxf(nv32[i], 0.f)));
+  }
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; vmax && i < ntl; i += stride)
+    mx = max(mx, __float_as_uint(fmaxf(vmax[i], 0.f)));
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; rad && i < nrad; i += stride)
+    mr = min(mr, __float_as_uint(fmaxf(rad[i], 0.f)));
+  for (int o = 16; o > 0; o >>= 1) {
+    me = max(me, __shfl_xor_sync(0xffffffffu, me, o));
+    mv = max(mv, __shfl_xor_sync(0xffffffffu, mv, o));
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    mr = min(mr, __shfl_xor_sync(0xffffffffu, mr, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(out, me);
+    atomicMax(out + 1, (unsigned long long)mv);
+    atomicMax(out + 2, (unsigned long long)mx);
+    atomicMin(out + 3, (unsigned long long)mr);
+  }
+}
+
 // Chunk geometry for the near-centre bound (k_lazy_nearbound), once per
 // context: per RCH-point chunk T its fp64 mean mu_T, radius r_T >= max |v - mu_T|
 // (rounded up), |mu_T|, the sum of e0d over it, and its point count.
@@ -1262,18 +1293,27 @@ struct ChunkGeo {
 __global__ void __launch_bounds__(256) k_chunk_geo(const float* __restrict__ V32, int pitch, int64_t n, int d,
                                                    const double* __restrict__ e0d, ChunkGeo g) {
   extern __shared__ double cmu[];  // d
-  __shared__ double red[8];
-  const int ch = blockIdx.x, tid = threadIdx.x;
+  __shared__ double red[8][33];
+  const int ch = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t v0 = (int64_t)ch * RCH;
   const int np = (int)min((int64_t)RCH, n - v0);
-  for (int k = tid; k < d; k += blockDim.x) {
+  // mean: warp w sums rows w, w + 8, ... over 32 dims at a time (coalesced)
+  for (int k0 = 0; k0 < d; k0 += 32) {
+    const int k = k0 + lane;
     double s = 0.0;
-    for (int j = 0; j < np; ++j) s += (double)V32[(v0 + j) * pitch + k];
-    cmu[k] = s / (double)np;
-    g.mu[(int64_t)ch * d + k] = cmu[k];
+    if (k < d)
+      for (int j = warp; j < np; j += 8) s += (double)V32[(v0 + j) * pitch + k];
+    red[warp][lane] = s;
+    __syncthreads();
+    if (tid < 32 && k < d) {
+      double t = 0.0;
+      for (int w = 0; w < 8; ++w) t += red[w][tid];
+      cmu[k] = t / (double)np;
+      g.mu[(int64_t)ch * d + k] = cmu[k];
+    }
+    __syncthreads();
   }
   for (int k = tid; k < g.dp; k += blockDim.x) g.muf[(int64_t)ch * g.dp + k] = k < d ? (float)cmu[k] : 0.f;
-  __syncthreads();
   double rmax = 0.0, es = 0.0;
   for (int j = tid; j < np; j += blockDim.x) {
     double q = 0.0;
@@ -1288,23 +1328,22 @@ __global__ void __launch_bounds__(256) k_chunk_geo(const float* __restrict__ V32
     rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
     es += __shfl_xor_sync(0xffffffffu, es, o);
   }
-  if ((tid & 31) == 0) red[tid >> 5] = rmax;
+  if (lane == 0) {
+    red[warp][0] = rmax;
+    red[warp][1] = es;
+  }
   __syncthreads();
   if (tid == 0) {
-    double m = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, red[w]);
+    double m = 0.0, e = 0.0;
+    for (int w = 0; w < 8; ++w) {
+      m = fmax(m, red[w][0]);
+      e += red[w][1];
+    }
     g.r[ch] = sqrt(m) * (1.0 + 1e-9);
+    g.e0s[ch] = e;
     double q = 0.0;
     for (int k = 0; k < d; ++k) q = fma(cmu[k], cmu[k], q);
     g.mn[ch] = sqrt(q) * (1.0 + 1e-9);
-  }
-  __syncthreads();
-  if ((tid & 31) == 0) red[tid >> 5] = es;
-  __syncthreads();
-  if (tid == 0) {
-    double s = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
-    g.e0s[ch] = s;
   }
 }
 

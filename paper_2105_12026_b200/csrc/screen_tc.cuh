@@ -381,6 +381,80 @@ __global__ void k_fps_step(const float* __restrict__ V32, int pitch, int64_t n, 
   }
 }
 
+// All of farthest-point sampling in one cooperative launch: the same per-step
+// arithmetic and keys as k_fps_step (so the same anchors), one grid barrier per
+// anchor instead of one launch per anchor.  bar: two zeroed words.
+__device__ __forceinline__ void fps_grid_barrier(unsigned int* bar, unsigned int& gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned int nb = gridDim.x;
+    if (atomicAdd(bar, 1u) == nb - 1) {
+      bar[0] = 0u;
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*(volatile unsigned int*)(bar + 1) == gen) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  ++gen;
+  __syncthreads();
+}
+__global__ void __launch_bounds__(256) k_fps_all(const float* __restrict__ V32, int pitch, int64_t n, int d, int na,
+                                                 float* __restrict__ mind, unsigned long long* __restrict__ keys,
+                                                 float* __restrict__ anchors, int apitch, unsigned int* bar) {
+  extern __shared__ float fmu[];  // (d + 3) / 4 * 4: the current anchor, zero padded
+  __shared__ unsigned long long sk[8];
+  unsigned int gen = *(volatile unsigned int*)(bar + 1);
+  for (int a = 0; a < na; ++a) {
+    int64_t src = -1;
+    if (a > 0) src = (int64_t)(0xFFFFFFFFull - (__ldcg(keys + a) & 0xFFFFFFFFull));
+    for (int k = threadIdx.x; k < (d + 3) / 4 * 4; k += blockDim.x) {
+      const float x = src >= 0 && k < d ? V32[src * pitch + k] : 0.f;
+      fmu[k] = x;
+      if (blockIdx.x == 0 && k < d) anchors[(int64_t)a * apitch + k] = x;
+    }
+    if (blockIdx.x == 0)
+      for (int k = d + threadIdx.x; k < apitch; k += blockDim.x) anchors[(int64_t)a * apitch + k] = 0.f;
+    __syncthreads();
+    unsigned long long best = 0;
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+      // rows are 16-byte aligned (pitch % 4 == 0, zero-padded past d, fmu too):
+      // four independent partial sums over 128-bit loads (any order is fine --
+      // anchors only steer the bounds, every choice is certified)
+      const float4* row4 = reinterpret_cast<const float4*>(V32 + v * pitch);
+      float t0 = 0.f, t1 = 0.f, t2 = 0.f, t3 = 0.f;
+      for (int k4 = 0; k4 < (d + 3) / 4; ++k4) {
+        const float4 r = __ldg(row4 + k4);
+        const float x0 = r.x - fmu[4 * k4], x1 = r.y - fmu[4 * k4 + 1];
+        const float x2 = r.z - fmu[4 * k4 + 2], x3 = r.w - fmu[4 * k4 + 3];
+        t0 = fmaf(x0, x0, t0);
+        t1 = fmaf(x1, x1, t1);
+        t2 = fmaf(x2, x2, t2);
+        t3 = fmaf(x3, x3, t3);
+      }
+      const float t = (t0 + t1) + (t2 + t3);
+      const float m = a == 0 ? t : fminf(mind[v], t);
+      mind[v] = m;
+      const unsigned long long key = fps_key(m, v);
+      best = key > best ? key : best;
+    }
+    if (a + 1 >= na) break;
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long other = __shfl_xor_sync(0xffffffff, best, o);
+      best = other > best ? other : best;
+    }
+    if ((threadIdx.x & 31) == 0) sk[threadIdx.x >> 5] = best;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < (int)(blockDim.x >> 5); ++w) best = sk[w] > best ? sk[w] : best;
+      atomicMax(&keys[a + 1], best);
+    }
+    fps_grid_barrier(bar, gen);
+  }
+}
+
 // nva[a][v] = |v - mu_a|^2 (fp64 sum, rounded to fp32) for every anchor.
 __global__ void k_nva(const float* __restrict__ V32, int pitch, int64_t n, int d, const float* __restrict__ anchors,
                       int apitch, int na, float* __restrict__ nva, int64_t stride) {
@@ -399,38 +473,135 @@ __global__ void k_nva(const float* __restrict__ V32, int pitch, int64_t n, int d
   }
 }
 
+// The same values, one thread per point for every anchor at once (anchors
+// staged in shared memory; the per-(anchor, point) fp64 sum in the same order).
+constexpr int NA_ALL = 32;
+__global__ void __launch_bounds__(128) k_nva_all(const float* __restrict__ V32, int pitch, int64_t n, int d,
+                                                 const float* __restrict__ anchors, int apitch, int na,
+                                                 float* __restrict__ nva, int64_t stride) {
+  extern __shared__ double amd[];  // na x dp anchors in fp64 (converted once), zero padded (dp = d rounded
+                                   // up to 4; rows are zero padded too, so the extra terms add exactly 0)
+  const int dp = (d + 3) / 4 * 4;
+  for (int i = threadIdx.x; i < na * dp; i += blockDim.x) {
+    const int a = i / dp, k = i - a * dp;
+    amd[i] = k < d ? (double)anchors[(int64_t)a * apitch + k] : 0.0;
+  }
+  __syncthreads();
+  const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= n) return;
+  double acc[NA_ALL];
+#pragma unroll
+  for (int a = 0; a < NA_ALL; ++a) acc[a] = 0.0;
+  const float4* row4 = reinterpret_cast<const float4*>(V32 + v * pitch);
+  for (int k4 = 0; k4 < dp / 4; ++k4) {
+    const float4 r = __ldg(row4 + k4);
+    const double r0 = r.x, r1 = r.y, r2 = r.z, r3 = r.w;
+#pragma unroll
+    for (int a = 0; a < NA_ALL; ++a)
+      if (a < na) {
+        const double2 m01 = *reinterpret_cast<const double2*>(amd + a * dp + 4 * k4);
+        const double2 m23 = *reinterpret_cast<const double2*>(amd + a * dp + 4 * k4 + 2);
+        double t = r0 - m01.x;
+        acc[a] = fma(t, t, acc[a]);
+        t = r1 - m01.y;
+        acc[a] = fma(t, t, acc[a]);
+        t = r2 - m23.x;
+        acc[a] = fma(t, t, acc[a]);
+        t = r3 - m23.y;
+        acc[a] = fma(t, t, acc[a]);
+      }
+  }
+#pragma unroll
+  for (int a = 0; a < NA_ALL; ++a)
+    if (a < na) nva[a * stride + v] = (float)acc[a];
+}
+
 // Per 128-candidate block: the anchor minimising max_c |c - mu_a|^2 (ties: lower a).
-__global__ void k_tile_anchor(const float* __restrict__ V32, int pitch, int64_t n, int d,
-                              const float* __restrict__ anchors, int apitch, int na, int* __restrict__ tile_anchor,
-                              float* __restrict__ tile_rad, const int* __restrict__ n_dev = nullptr,
-                              const int* __restrict__ level_now = nullptr, int level = 0) {
+// na <= NA_ALL: every thread sums its candidate against all anchors at once
+// (anchors in shared memory, dynamic smem na x d floats); larger na loops.
+__global__ void __launch_bounds__(128) k_tile_anchor(const float* __restrict__ V32, int pitch, int64_t n, int d,
+                                                     const float* __restrict__ anchors, int apitch, int na,
+                                                     int* __restrict__ tile_anchor, float* __restrict__ tile_rad,
+                                                     int staged, const int* __restrict__ n_dev = nullptr,
+                                                     const int* __restrict__ level_now = nullptr, int level = 0) {
   // n_dev: a device-side row count (gathered lazy re-screens; blocks past it exit)
   if (level_now && *level_now != level) return;
   if (n_dev) n = min(n, (int64_t)*n_dev);
   if ((int64_t)blockIdx.x * 128 >= n) return;
+  extern __shared__ float tmu[];  // na x d (na <= NA_ALL)
+  __shared__ float wm[4][NA_ALL];
   __shared__ float wmax[4];
   const int64_t c = (int64_t)blockIdx.x * 128 + threadIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   float best = INFINITY;
   int besta = 0;
-  for (int a = 0; a < na; ++a) {
-    float t = 0.f;
+  if (staged) {  // host: na <= NA_ALL and na x dp floats of dynamic smem
+    // anchors zero padded to dp (rows are zero padded too: the extra terms add
+    // exactly 0, so the sums equal the looped form's)
+    const int dp = (d + 3) / 4 * 4;
+    for (int i = threadIdx.x; i < na * dp; i += blockDim.x) {
+      const int a = i / dp, k = i - a * dp;
+      tmu[i] = k < d ? anchors[(int64_t)a * apitch + k] : 0.f;
+    }
+    __syncthreads();
+    float t[NA_ALL];
+#pragma unroll
+    for (int a = 0; a < NA_ALL; ++a) t[a] = 0.f;
     if (c < n) {
-      const float* row = V32 + c * pitch;
-      const float* mu = anchors + (int64_t)a * apitch;
-      for (int k = 0; k < d; ++k) {
-        const float x = row[k] - mu[k];
-        t = fmaf(x, x, t);
+      const float4* row4 = reinterpret_cast<const float4*>(V32 + c * pitch);
+      for (int k4 = 0; k4 < dp / 4; ++k4) {
+        const float4 r = __ldg(row4 + k4);
+#pragma unroll
+        for (int a = 0; a < NA_ALL; ++a)
+          if (a < na) {
+            const float4 m = *reinterpret_cast<const float4*>(tmu + a * dp + 4 * k4);
+            float x = r.x - m.x;
+            t[a] = fmaf(x, x, t[a]);
+            x = r.y - m.y;
+            t[a] = fmaf(x, x, t[a]);
+            x = r.z - m.z;
+            t[a] = fmaf(x, x, t[a]);
+            x = r.w - m.w;
+            t[a] = fmaf(x, x, t[a]);
+          }
       }
     }
-    for (int o = 16; o > 0; o >>= 1) t = fmaxf(t, __shfl_xor_sync(0xffffffff, t, o));
-    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = t;
-    __syncthreads();
-    const float m = fmaxf(fmaxf(wmax[0], wmax[1]), fmaxf(wmax[2], wmax[3]));
-    if (m < best) {
-      best = m;
-      besta = a;
+#pragma unroll
+    for (int a = 0; a < NA_ALL; ++a) {
+      float m = t[a];
+      for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffff, m, o));
+      if (lane == 0) wm[warp][a] = m;
     }
     __syncthreads();
+    if (threadIdx.x == 0)
+      for (int a = 0; a < na; ++a) {
+        const float m = fmaxf(fmaxf(wm[0][a], wm[1][a]), fmaxf(wm[2][a], wm[3][a]));
+        if (m < best) {
+          best = m;
+          besta = a;
+        }
+      }
+  } else {
+    for (int a = 0; a < na; ++a) {
+      float t = 0.f;
+      if (c < n) {
+        const float* row = V32 + c * pitch;
+        const float* mu = anchors + (int64_t)a * apitch;
+        for (int k = 0; k < d; ++k) {
+          const float x = row[k] - mu[k];
+          t = fmaf(x, x, t);
+        }
+      }
+      for (int o = 16; o > 0; o >>= 1) t = fmaxf(t, __shfl_xor_sync(0xffffffff, t, o));
+      if (lane == 0) wmax[warp] = t;
+      __syncthreads();
+      const float m = fmaxf(fmaxf(wmax[0], wmax[1]), fmaxf(wmax[2], wmax[3]));
+      if (m < best) {
+        best = m;
+        besta = a;
+      }
+      __syncthreads();
+    }
   }
   if (threadIdx.x == 0) {
     tile_anchor[blockIdx.x] = besta;

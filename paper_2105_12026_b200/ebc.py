@@ -9,6 +9,7 @@ goes through the C-ABI -- there is no host arithmetic on the hot path.
 from __future__ import annotations
 
 import ctypes
+import weakref
 import os
 from typing import Optional, Sequence
 
@@ -27,6 +28,29 @@ def default_device() -> int:
         if os.environ.get(var, "").strip():
             return int(os.environ[var])
     return 0
+
+
+_PIN_MIN_BYTES = 1 << 20
+
+
+def _unregister(lib, data):
+    lib.ebc_host_unregister(data.ctypes.data_as(ctypes.c_void_p))
+
+
+def _host_rows(lib, ground: GroundMatrix) -> np.ndarray:
+    """The ground's rows as the C-contiguous host buffer ebc_create uploads.
+    Grounds of >= 1 MiB are page-locked once (ebc_host_register) at their first
+    context and stay so for the GroundMatrix's lifetime, so every later context
+    uploads them by one direct DMA (the bench's e2e contract: host inputs in
+    pinned memory).  If the driver refuses, the buffer stays pageable and the
+    library's staged upload is used."""
+    data = np.ascontiguousarray(ground.data)
+    if data is ground.data and data.nbytes >= _PIN_MIN_BYTES and not getattr(ground, "_b200_pinned", False):
+        ok = lib.ebc_host_register(data.ctypes.data_as(ctypes.c_void_p), data.nbytes) == 0
+        ground._b200_pinned = True  # tried once either way
+        if ok:
+            weakref.finalize(ground, _unregister, lib, data)
+    return data
 
 
 class EbcFunction:
@@ -57,7 +81,7 @@ class EbcFunction:
         self.device = default_device() if device is None else int(device)
         self._lib = _native.load()
         self._ctx = ctypes.c_void_p()
-        data = np.ascontiguousarray(ground.data)
+        data = _host_rows(self._lib, ground)
         rc = self._lib.ebc_create(data.ctypes.data_as(ctypes.c_void_p), ground.n, ground.dims,
                                   _DTYPE[ground.precision],
                                   self.e0.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
