@@ -311,12 +311,18 @@ struct ebc_ctx {
   double* ub_next = nullptr;       // best stale bound outside the first batch
   int lazy_batch = 4;              // EBC200_LAZY_BATCH (1..RW): candidates refined first in a lazy step
   bool probe_on = true;            // EBC200_LAZY_PROBE=0: no ring-probe batch on undecided steps
+  bool fuse_batch = true;          // EBC200_FUSE_BATCH=0: the next step's first batch not folded into K4
+  int batch_ready_step = -1;       // enqueue-time: that step's first batch was launched with the last update
+  cudaGraphConditionalHandle batch_hrest = 0;
+  int ub_rows = 128;               // EBC200_UB_ROWS: rows per k_update_batch slice (64, 128, 256)
   ProbeBuf probe;                  // k_lazy_rings: ring winners, ticket, the probe list
   bool nb_on = false;              // EBC200_LAZY_NEARBOUND=0: no near-centre bound (k_lazy_nearbound)
   ChunkGeo geo;                    // per-chunk mean / radius / e0 sums for the near-centre bound
   unsigned int* counter3 = nullptr;  // k_refine's finalize ticket
   bool refine2 = true;             // EBC200_REFINE2=0: the lazy batch on the classic k_refine
   DevBuf rterms;                   // RW x nchunks chunk sums of the short refine
+  DevBuf sxt;                      // short refine: RW x n_pad point terms, then nchunks tickets
+  DevBuf ubpack;                   // k_batch_pack: the rows k_update_batch stages (BatchPackLayout)
   // CUDA-graph conditional nodes for the undecided part of a lazy step (captured
   // runs only: an eager run gates those kernels on level[0] instead)
   bool use_cond = true;            // EBC200_GRAPH_COND=0: plain gated kernels in graphs too
@@ -433,14 +439,19 @@ int ensure(ebc_ctx* ctx, DevBuf& b, size_t bytes) {
   return EBC_OK;
 }
 
-// Row pitch (elements) of the device copy: 16-byte rows; for fp32 the pitch in
-// float4 units is odd so that 4 or 8 consecutive rows read by one LDS.128 hit
-// disjoint bank groups (DESIGN.md §3).
 // Dynamic shared memory of k_tile_anchor's staged form (0: the looped form).
 size_t tile_anchor_smem(const ebc_ctx* ctx) {
   const size_t b = (size_t)ctx->tc_na * ((ctx->d + 3) / 4 * 4) * sizeof(float);
   return ctx->tc_na <= NA_ALL && b <= 160 * 1024 ? b : 0;
 }
+
+// Dynamic shared memory of k_refine_short (the window's rows in fp64); above
+// 180 KB the classic k_refine serves short windows.
+size_t short_refine_smem(const ebc_ctx* ctx) { return (size_t)RW * ctx->d * (sizeof(double) + sizeof(float)); }
+
+// Row pitch (elements) of the device copy: 16-byte rows; for fp32 the pitch in
+// float4 units is odd so that 4 or 8 consecutive rows read by one LDS.128 hit
+// disjoint bank groups (DESIGN.md §3).
 
 int pitch_for(int d, int dtype) {
   if (dtype == EBC_F64) return (d + 1) / 2 * 2;
@@ -1026,24 +1037,42 @@ int enqueue_refine_short(ebc_ctx* ctx, int ng, const RefineFinal& fin, const int
     pr.np = ctx->tc_np;
     pr.crad = ctx->crad;
   }
-  const size_t smem = (size_t)RW * (ctx->d + RCH) * sizeof(double);
+  const size_t smem = short_refine_smem(ctx);
   if (smem > 180 * 1024) {
-    if (wcount != ctx->wcount) return EBC_EINVAL;  // callers check short_refine_fits first
+    if (wcount != ctx->wcount) return EBC_EINVAL;  // callers check short_refine_smem first
     return enqueue_refine(ctx, ng, nullptr, fin);
   }
   int rc = ensure(ctx, ctx->rterms, (size_t)RW * ctx->nchunks * sizeof(double));
   if (rc) return rc;
-  if (ctx->dtype == EBC_F64) {
-    CU(cudaFuncSetAttribute(k_refine_short<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_refine_short<double><<<ctx->nchunks, SHORT_THREADS, smem, ctx->stream>>>(
-        ctx->V64, ctx->pitch, ctx->n, ctx->d, ctx->cm64, wcount, wlist, ctx->nchunks, ng,
-        (double*)ctx->rterms.p, (double*)ctx->part_r.p, pr, fin);
-  } else {
-    CU(cudaFuncSetAttribute(k_refine_short<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_refine_short<float><<<ctx->nchunks, SHORT_THREADS, smem, ctx->stream>>>(
-        ctx->V32, ctx->pitch, ctx->n, ctx->d, ctx->cm64, wcount, wlist, ctx->nchunks, ng,
-        (double*)ctx->rterms.p, (double*)ctx->part_r.p, pr, fin);
-  }
+  // per-point terms (RW x n_pad) and the per-chunk tickets (zeroed when allocated)
+  const size_t xbytes = (size_t)RW * ctx->n_pad * sizeof(double);
+  const size_t sbytes = xbytes + (size_t)ctx->nchunks * sizeof(unsigned int);
+  const bool fresh = ctx->sxt.bytes < sbytes;
+  if ((rc = ensure(ctx, ctx->sxt, sbytes))) return rc;
+  if (fresh) CU(cudaMemsetAsync((unsigned char*)ctx->sxt.p + xbytes, 0, sbytes - xbytes, ctx->stream));
+  ShortBufs sb;
+  sb.xt = (double*)ctx->sxt.p;
+  sb.xstride = ctx->n_pad;
+  sb.chunk_ticket = (unsigned int*)((unsigned char*)ctx->sxt.p + xbytes);
+  const unsigned grid = (unsigned)(ctx->nchunks * SHORT_SPLIT);
+  // staged rows (bulk copies) when a 256-row slice fits next to the window rows
+  const size_t esz = ctx->dtype == EBC_F64 ? sizeof(double) : sizeof(float);
+  const size_t stage = (size_t)RED_THREADS * ctx->pitch * esz + RED_THREADS * sizeof(double);
+  const char* se = getenv("EBC200_SHORT_STAGE");
+  const bool staged = stage + smem <= 110 * 1024 && se && se[0] == '1';  // measured slower: opt-in
+  const size_t dsm = smem + (staged ? stage : 0);
+  auto go = [&](auto kern, const auto* V) -> int {
+    CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+    kern<<<grid, SHORT_THREADS, dsm, ctx->stream>>>(V, ctx->pitch, ctx->n, ctx->d, ctx->cm64, wcount, wlist,
+                                                    ctx->nchunks, ng, (double*)ctx->rterms.p,
+                                                    (double*)ctx->part_r.p, pr, fin, sb);
+    return EBC_OK;
+  };
+  if (ctx->dtype == EBC_F64)
+    rc = staged ? go(k_refine_short<double, true>, ctx->V64) : go(k_refine_short<double, false>, ctx->V64);
+  else
+    rc = staged ? go(k_refine_short<float, true>, ctx->V32) : go(k_refine_short<float, false>, ctx->V32);
+  if (rc) return rc;
   KCHECK();
   return EBC_OK;
 }
@@ -1120,6 +1149,41 @@ RefineFinal step_final(ebc_ctx* ctx, int commit, int step, int64_t* sel_dev) {
   return f;
 }
 
+double lazy_margin(const ebc_ctx* ctx) {
+  return (double)ctx->n * 1e-12 * std::max(1.0, std::fabs(ctx->baseline)) * 1.01;
+}
+
+// Point-chunk groups per window candidate: as many as 256 MB of partials allow
+// (a short window is latency-bound: more groups = more blocks in flight).
+int refine_groups(const ebc_ctx* ctx) {
+  const int64_t ng_mem = (int64_t)(256ull << 20) / (8 * (ctx->n + RW));
+  return (int)std::max<int64_t>(1, std::min<int64_t>(ctx->nchunks, std::max<int64_t>(32, ng_mem)));
+}
+
+// The first batch of lazy step `step`: k_lazy_topk (its wlist / ub_next) and
+// the RefineFinal of its refine, which decides the step; the caller launches
+// that refine (k_refine_short / k_refine, or k_update_batch with the previous
+// step's update).  Device-sharded runs all-reduce the batch's bound before the
+// decision (batch 2), so every rank's stale set is its share of the
+// single-device one (a rank whose own candidates are all weak would otherwise
+// re-screen them against its own low bound).
+void lazy_batch_begin(ebc_ctx* ctx, int step, int commit, int64_t* sel_dev, RefineFinal& fb) {
+  const int64_t ncand = ctx->c1 - ctx->c0;
+  const int ag = (int)std::max<int64_t>(1, std::min<int64_t>(2 * ctx->num_sms, (ncand + 1023) / 1024));
+  k_lazy_topk<<<ag, 256, 0, ctx->stream>>>(ctx->c0, ctx->c1, ctx->ubp, ctx->selected, ctx->lazy_batch,
+                                          (unsigned long long*)ctx->lazy_part, ctx->counter2, ctx->wcount, ctx->wlist,
+                                          ctx->ub_next);
+  ++ctx->launches;
+  const bool global_lb = ctx->in_sharded_run && ctx->comm && (ctx->nranks > 1 || ctx->force_global_lb);
+  fb = step_final(ctx, commit, step, sel_dev);
+  fb.batch = global_lb ? 2 : 1;
+  fb.ub_next = ctx->ub_next;
+  fb.margin = lazy_margin(ctx);
+  fb.maxlb = ctx->maxlb;
+  fb.scount = ctx->scount;
+  fb.hrest = cond_handle(ctx);
+}
+
 // One step's selection: screen + certified window + exact refine + pick, or a
 // lazy step (DESIGN.md §4 "Lazy steps"): the lazy_batch best stale bounds are
 // refined first and decide the step when they hold the whole stale set;
@@ -1136,10 +1200,7 @@ int run_step_select(ebc_ctx* ctx, int step, int commit, int64_t* sel_dev) {
   const bool has_screen = ctx->dtype != EBC_F64 && plan_screen(ctx, sp) == EBC_OK;
   const bool lazy = ctx->lazy_on && ctx->ubp_seeded;
   if (!lazy) CU(cudaMemsetAsync(ctx->wcount, 0, sizeof(int), ctx->stream));  // a lazy step's k_lazy_topk writes it
-  // point-chunk groups per window candidate: as many as 256 MB of partials allow
-  // (a short window is latency-bound: more groups = more blocks in flight)
-  const int64_t ng_mem = (int64_t)(256ull << 20) / (8 * (ctx->n + RW));
-  const int ng = (int)std::max<int64_t>(1, std::min<int64_t>(ctx->nchunks, std::max<int64_t>(32, ng_mem)));
+  const int ng = refine_groups(ctx);
   int rc = ensure(ctx, ctx->part_r, (size_t)(ctx->n + RW) * ng * sizeof(double));
   if (rc) return rc;
   RefineFinal fin = step_final(ctx, commit, step, sel_dev);
@@ -1154,29 +1215,23 @@ int run_step_select(ebc_ctx* ctx, int step, int commit, int64_t* sel_dev) {
     return EBC_OK;
   }
   // lazy step: the first batch (k_lazy_topk) and its refine, which decides
-  // (it also sets maxlb = lb and zeroes scount; no memset nodes on this path)
+  // (it also sets maxlb = lb and zeroes scount; no memset nodes on this path).
+  // Fused runs launched both with the previous step's update (k_update_batch).
   const int ag = (int)std::max<int64_t>(1, std::min<int64_t>(2 * ctx->num_sms, (ncand + 1023) / 1024));
-  k_lazy_topk<<<ag, 256, 0, ctx->stream>>>(ctx->c0, ctx->c1, ctx->ubp, ctx->selected, ctx->lazy_batch,
-                                          (unsigned long long*)ctx->lazy_part, ctx->counter2, ctx->wcount, ctx->wlist,
-                                          ctx->ub_next);
-  KCHECK();
-  const cudaGraphConditionalHandle hrest = cond_handle(ctx);
-  const double margin = (double)ctx->n * 1e-12 * std::max(1.0, std::fabs(ctx->baseline)) * 1.01;
-  // device-sharded runs: the batch's bound is all-reduced (max) across the
-  // ranks before the decision, so every rank's stale set is its share of the
-  // single-device one (a rank whose own candidates are all weak would
-  // otherwise re-screen them against its own low bound)
+  const double margin = lazy_margin(ctx);
   const bool global_lb = ctx->in_sharded_run && ctx->comm && (ctx->nranks > 1 || ctx->force_global_lb);
-  RefineFinal fb = fin;
-  fb.batch = global_lb ? 2 : 1;
-  fb.ub_next = ctx->ub_next;
-  fb.margin = margin;
-  fb.maxlb = ctx->maxlb;
-  fb.scount = ctx->scount;
-  fb.hrest = hrest;
-  ctx->cmx_fresh = ctx->cmx_valid;  // an earlier step's tile maxima still bound cm (it only decreases)
-  rc = ctx->refine2 ? enqueue_refine_short(ctx, ng, fb) : enqueue_refine(ctx, ng, nullptr, fb);
-  if (rc) return rc;
+  cudaGraphConditionalHandle hrest = 0;
+  if (ctx->batch_ready_step == step) {
+    hrest = ctx->batch_hrest;
+    ctx->batch_ready_step = -1;
+  } else {
+    RefineFinal fb;
+    lazy_batch_begin(ctx, step, commit, sel_dev, fb);
+    hrest = fb.hrest;
+    ctx->cmx_fresh = ctx->cmx_valid;  // an earlier step's tile maxima still bound cm (it only decreases)
+    rc = ctx->refine2 ? enqueue_refine_short(ctx, ng, fb) : enqueue_refine(ctx, ng, nullptr, fb);
+    if (rc) return rc;
+  }
   if (global_lb) {
     const NcclApi& api = nccl_api();
     const ncclResult_t r = api.AllReduce(ctx->maxlb, ctx->maxlb, 1, ncclInt64, ncclMax, ctx->comm, ctx->stream);
@@ -1198,7 +1253,7 @@ int run_step_select(ebc_ctx* ctx, int step, int commit, int64_t* sel_dev) {
     // undecided step (level[0] == -3): stale set -> mode -> screen / refine
     CondScope ca;
     CU(ca.open(ctx, hrest, 0));
-    if (ctx->probe_on && has_screen && ctx->refine2 && (size_t)RW * (ctx->d + RCH) * sizeof(double) <= 180 * 1024) {
+    if (ctx->probe_on && has_screen && ctx->refine2 && short_refine_smem(ctx) <= 180 * 1024) {
       // probe batch: ring winners around the last selected centre raise lb
       // (k_lazy_rings) before the stale set is listed
       k_lazy_rings<<<ag, 256, (size_t)ctx->d * sizeof(float), ctx->stream>>>(
@@ -1323,7 +1378,7 @@ int run_update(ebc_ctx* ctx, int step, double* val_dev, double* gain_dev) {
     // rows, 256 by default; 64 and 128 measured the same on C2 and C4), f(S) by
     // the block that completes the last chunk
     // (DESIGN.md §4 K4)
-    const size_t head = ((size_t)ctx->d * 8 + 15) & ~(size_t)15;
+    const size_t head = (((size_t)ctx->d * 8 + 15) & ~(size_t)15) + (((size_t)((ctx->d + 3) & ~3) * 4 + 15) & ~(size_t)15);
     const int rows = ctx->uf_rows;
     const size_t dsm = head + (size_t)rows * (ctx->pitch * 4 + 16);
     UpdateCounters uc{ctx->uf_ctr + 1, ctx->uf_ctr};
@@ -1378,6 +1433,73 @@ int ensure_events(ebc_ctx* ctx, size_t count) {
 int do_reset(ebc_ctx* ctx);
 int run_step_select(ebc_ctx* ctx, int step, int commit, int64_t* sel_dev);
 int run_update(ebc_ctx* ctx, int step, double* val_dev, double* gain_dev);
+
+// Dynamic shared memory of k_update_batch<rows> (0: does not fit one block).
+size_t update_batch_smem(const ebc_ctx* ctx, int rows) {
+  const size_t stage = std::max<size_t>((size_t)rows * ctx->pitch * 4 + (size_t)rows * 16,
+                                        ((size_t)(RW + 1) * RED_THREADS + (size_t)RW * refine_groups(ctx)) *
+                                            sizeof(double));
+  const size_t b = BatchPackLayout(ctx->d).bytes() + stage;
+  return b <= 200 * 1024 ? b : 0;
+}
+
+// Single-device lazy runs fold the next step's first batch into this step's
+// K4 (k_update_batch): fp32 rows on the fused K4 path, the short refine.
+bool batch_fusable(const ebc_ctx* ctx) {
+  return ctx->fuse_batch && ctx->lazy_on && ctx->refine2 && ctx->uf_on && ctx->dtype != EBC_F64 &&
+         !ctx->in_sharded_run && short_refine_smem(ctx) <= 180 * 1024 && update_batch_smem(ctx, ctx->ub_rows) > 0;
+}
+
+// K4 of `step` together with the first batch of lazy step step + 1: k_lazy_topk,
+// then one pass over the rows (k_update_batch) -- the batch's refine and its
+// decision are those of k_refine_short after k_update_fused, bit for bit.
+int run_update_batch(ebc_ctx* ctx, int step, double* val_dev, double* gain_dev, int64_t* sel_dev) {
+  const int eb = 4 * step;
+  RefineFinal fb;
+  lazy_batch_begin(ctx, step + 1, 1, sel_dev, fb);
+  int rc = ensure(ctx, ctx->rterms, (size_t)RW * ctx->nchunks * sizeof(double));
+  if (rc) return rc;
+  const size_t xbytes = (size_t)RW * ctx->n_pad * sizeof(double);
+  const size_t sbytes = xbytes + (size_t)ctx->nchunks * sizeof(unsigned int);
+  const bool fresh = ctx->sxt.bytes < sbytes;
+  if ((rc = ensure(ctx, ctx->sxt, sbytes))) return rc;
+  if (fresh) CU(cudaMemsetAsync((unsigned char*)ctx->sxt.p + xbytes, 0, sbytes - xbytes, ctx->stream));
+  BatchArgs ba;
+  ba.wcount = ctx->wcount;
+  ba.wlist = ctx->wlist;
+  ba.xch = (double*)ctx->rterms.p;
+  ba.part_r = (double*)ctx->part_r.p;
+  ba.ng = refine_groups(ctx);
+  ba.sb.xt = (double*)ctx->sxt.p;
+  ba.sb.xstride = ctx->n_pad;
+  ba.fin = fb;
+  const int rows = ctx->ub_rows;
+  const size_t dsm = update_batch_smem(ctx, rows);
+  const size_t pbytes = BatchPackLayout(ctx->d).bytes();
+  const bool pfresh = ctx->ubpack.bytes < pbytes;
+  if ((rc = ensure(ctx, ctx->ubpack, pbytes))) return rc;
+  (void)pfresh;
+  k_batch_pack<<<RW + 1, 128, 0, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->d, ctx->nv32, ctx->best, ctx->wcount,
+                                               ctx->wlist, (unsigned char*)ctx->ubpack.p);
+  KCHECK();
+  UpdateCounters uc{ctx->uf_ctr + 1, ctx->uf_ctr};
+  const unsigned grid = (unsigned)((ctx->n + rows - 1) / rows);
+  auto go = [&](auto kern) -> int {
+    CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+    kern<<<grid, rows, dsm, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->n, ctx->d, ctx->best, ctx->pk, ctx->e0d,
+                                           ctx->nv32, ctx->cm64, ctx->pt, tc_seeds(ctx), ctx->terms,
+                                           ctx->chunkpart, uc, 1.0 / (double)ctx->n, ctx->cur, val_dev, gain_dev,
+                                           step, ba, (const unsigned char*)ctx->ubpack.p);
+    return EBC_OK;
+  };
+  rc = rows == 64 ? go(k_update_batch<64>) : (rows == 256 ? go(k_update_batch<256>) : go(k_update_batch<128>));
+  if (rc) return rc;
+  KCHECK();
+  ctx->batch_ready_step = step + 1;
+  ctx->batch_hrest = fb.hrest;
+  if (ctx->timing) CU(record_step_event(ctx, ctx->ev[eb + 3]));
+  return EBC_OK;
+}
 
 // Reset + the k steps of a Greedy run, all on ctx->stream (no host sync).
 // One sharded Greedy step entirely on the device: local screen + window +
@@ -1443,13 +1565,17 @@ int enqueue_greedy(ebc_ctx* ctx, int k) {
   for (int s = 0; s < k; ++s) {
     rc = run_step_select(ctx, s, 1, (int64_t*)ctx->sel_out.p);
     if (rc) return rc;
-    rc = run_update(ctx, s, (double*)ctx->val_out.p, (double*)ctx->gain_out.p);
+    if (s + 1 < k && ctx->ubp_seeded && batch_fusable(ctx))
+      rc = run_update_batch(ctx, s, (double*)ctx->val_out.p, (double*)ctx->gain_out.p, (int64_t*)ctx->sel_out.p);
+    else
+      rc = run_update(ctx, s, (double*)ctx->val_out.p, (double*)ctx->gain_out.p);
     if (rc) return rc;
   }
   return EBC_OK;
 }
 
 int do_reset(ebc_ctx* ctx) {
+  ctx->batch_ready_step = -1;
   const int blocks = (int)((ctx->n + 255) / 256);
   CU(cudaMemsetAsync(ctx->stats, 0, 8 * sizeof(long long), ctx->stream));
   k_reset<<<blocks, 256, 0, ctx->stream>>>(ctx->n, ctx->e0d, ctx->nv32, ctx->pk, ctx->cm64, ctx->pt, ctx->selected,
@@ -1483,7 +1609,7 @@ void free_ctx(ebc_ctx* c) {
                   c->geo.mu, c->geo.r, c->geo.mn, c->geo.e0s, c->geo.muf};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, c->stream);
-  DevBuf* bufs[] = {&c->tie_rec, &c->tie_all, &c->sel_hash, &c->ms_tanchor, &c->ms_trad, &c->part_g, &c->part_e, &c->part_a, &c->part_r, &c->rterms, &c->sv_cm, &c->sv_de, &c->sv_slots, &c->sv_part, &c->sv_out, &c->sel_out, &c->val_out, &c->gain_out, &c->ms_part,
+  DevBuf* bufs[] = {&c->tie_rec, &c->tie_all, &c->sel_hash, &c->ms_tanchor, &c->ms_trad, &c->part_g, &c->part_e, &c->part_a, &c->part_r, &c->rterms, &c->sxt, &c->ubpack, &c->sv_cm, &c->sv_de, &c->sv_slots, &c->sv_part, &c->sv_out, &c->sel_out, &c->val_out, &c->gain_out, &c->ms_part,
                     &c->ms_off, &c->ms_idx, &c->ms_out, &c->ms_mbuf, &c->ms_setof, &c->ms_pairs, &c->ms_keys,
                     &c->ms_vals, &c->ms_keys2, &c->ms_vals2, &c->ms_ukeys, &c->ms_uvals, &c->ms_cub};
   void* more[] = {c->pt0, c->ms_count, c->ms_nruns};
@@ -1765,6 +1891,37 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
     CUC(cudaGetLastError());
   }
   mark("pad");
+  {
+    // L2 residency of the rows: every lazy step streams V twice (the batch
+    // refine and the cached-min update); a persisting access-policy window on
+    // the context's streams (captured into the graphs' kernel nodes) keeps
+    // them in L2 when they fit the persisting carve-out.  EBC200_L2_PERSIST=0: off.
+    const char* lp = getenv("EBC200_L2_PERSIST");
+    int maxp = 0, maxw = 0;
+    const size_t vbytes = (size_t)ctx->n_pad * ctx->pitch * esz;
+    if (!(lp && lp[0] == '0') && cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, device) == cudaSuccess &&
+        cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, device) == cudaSuccess && maxp > 0 &&
+        maxw > 0) {
+      size_t cur = 0;
+      cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+      const size_t want = std::min<size_t>((size_t)maxp, vbytes);
+      if (cur < want) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+      cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+      cudaStreamAttrValue av{};
+      av.accessPolicyWindow.base_ptr = Vdev;
+      av.accessPolicyWindow.num_bytes = std::min<size_t>(vbytes, (size_t)maxw);
+      av.accessPolicyWindow.hitRatio =
+          (float)std::min(1.0, (double)cur / (double)av.accessPolicyWindow.num_bytes);
+      av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      for (cudaStream_t st : {ctx->stream, ctx->side[0], ctx->side[1]})
+        cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &av);
+      (void)cudaGetLastError();
+      if (prof)
+        fprintf(stderr, "[ebc_create] L2 persist: max %d B, window max %d B, carve-out %zu B, V %zu B, hit ratio %.3f\n",
+                maxp, maxw, cur, vbytes, av.accessPolicyWindow.hitRatio);
+    }
+  }
   if (dtype != EBC_F64) {
     // fp32 range guard: every screen (and the sparse work-matrix flag screen)
     // forms squared distances, norms and short sums in fp32.  Grounds whose
@@ -1953,6 +2110,13 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
     ctx->probe.plist = (int64_t*)(pbm + NRING * 8 + 16);
     const char* pe = getenv("EBC200_LAZY_PROBE");
     if (pe && pe[0] == '0') ctx->probe_on = false;
+    const char* fz = getenv("EBC200_FUSE_BATCH");
+    if (fz && fz[0] == '0') ctx->fuse_batch = false;
+    const char* ur = getenv("EBC200_UB_ROWS");
+    if (ur && ur[0]) {
+      const int r = atoi(ur);
+      ctx->ub_rows = r == 64 || r == 256 ? r : 128;
+    }
   }
   {
     const char* lb = getenv("EBC200_LAZY_BATCH");

@@ -89,6 +89,29 @@ __device__ __forceinline__ double dkey_inv(long long k) {
 
 // fp64 squared distance of stored row `row` (type T, `pitch` elements) to a
 // candidate held in shared memory as fp64 -- sequential over dims.
+// fp32 pre-test of an exact term max(0, cm - d64(v, c)): d32 = the fp32
+// distance (fl(x - c) squared and summed with FMAs, all terms >= 0) is within
+// (d + 3) 2^-24 of the exact one, so d32 (1 - (d + 4) 2^-23) > cm (1 + 2^-40)
+// certifies d_exact > cm and hence d64 >= cm: the fp64 term is exactly +0.0
+// (underflow and flushing only lower d32: never a false skip).  Kernels compute
+// the fp64 sum only where this fails -- the same values, far fewer DFMAs.
+__device__ __forceinline__ double far32_scale(int d) { return 1.0 - (double)(d + 4) * 0x1p-23; }
+__device__ __forceinline__ bool far32(float d32, double ks, double cm) {
+  // an overflowed fp32 sum proves nothing (cm may be beyond the fp32 range too)
+  return d32 <= 3.0e38f && (double)d32 * ks > cm * (1.0 + 0x1p-40);
+}
+
+// Gram form of the same pre-test, one FFMA per coordinate: g = fl32 v.c (one
+// sequential FFMA chain), nv / nc = fp32 |v|^2, |c|^2 (each within 2^-24
+// relative of the exact norm), so |(nv + nc - 2 g) - d_exact| <= (d + 1) 2^-24
+// (nv + nc) plus d 2^-149 per underflowed product; skip when the lower end still
+// exceeds cm.  Overflow gives inf / NaN and never skips.
+__device__ __forceinline__ bool far32_gram(float g, float nv, float nc, int d, double cm) {
+  const double s2 = (double)nv + (double)nc;
+  const double lo = s2 - 2.0 * (double)g - ((double)(d + 4) * 0x1p-24 * 1.01 * s2 + (double)(d + 4) * 0x1p-148);
+  return lo > cm * (1.0 + 0x1p-40);
+}
+
 template <typename T>
 __device__ __forceinline__ double dist64_row(const T* __restrict__ row, const double* cd, int d) {
   double s = 0.0;
@@ -1736,9 +1759,11 @@ struct RefineFinal {
 
 // nt: the participating threads (the first nt of the block; every thread of
 // the block must call it -- it synchronises the block)
+// pre: (optional) the wc x ng partials already in shared memory (the caller
+// computed them there); otherwise they are read from part_r.
 __device__ void refine_finalize_n(const RefineFinal& F, int wc, const int64_t* __restrict__ wlist,
                                   const double* __restrict__ part_r, int ng, double* sred, long long* sidx,
-                                  int nt) {
+                                  int nt, const double* pre = nullptr) {
   const int tid = threadIdx.x;
   const bool on = tid < nt;
   const double f = *F.cur;
@@ -1746,14 +1771,15 @@ __device__ void refine_finalize_n(const RefineFinal& F, int wc, const int64_t* _
   // short windows: every partial loaded by the whole block first (one memory
   // round trip), then each candidate's left-to-right sum from shared memory --
   // the same additions in the same order as chunk_total
-  const bool staged = wc <= nt && (int64_t)wc * ng <= 2 * (int64_t)nt;
-  if (staged) {
+  const bool staged = wc <= nt && (pre || (int64_t)wc * ng <= 2 * (int64_t)nt);
+  if (staged && !pre) {
     for (int i = tid; i < wc * ng && on; i += nt) sred[i] = __ldcg(part_r + i);
     __syncthreads();
   }
+  const double* sp = pre ? pre : sred;
   double gs = 0.0;
   if (staged && tid < wc)
-    for (int q = 0; q < ng; ++q) gs += sred[tid * ng + q];
+    for (int q = 0; q < ng; ++q) gs += sp[tid * ng + q];
   __syncthreads();
   for (int w = tid; w < wc && on; w += nt) {
     const double gsum = staged ? gs : chunk_total(part_r + (int64_t)w * ng, ng);
@@ -2042,43 +2068,71 @@ __global__ void __launch_bounds__(RED_THREADS) k_refine(const T* __restrict__ V,
 }
 static_assert(RW == RED_THREADS / 32, "one reducing warp per window candidate");
 
-// Refine of a short window (<= RW candidates: the lazy first batch), one block
-// of RCH threads per chunk.  The classic k_refine gives each (window group,
-// chunk group) unit to a 256-thread block (4 points per thread, the row loads
-// on its critical path), so a short window runs latency-bound on nchunks
-// blocks.  Here every point is one thread: term(v, j) = max(0, cm(v) -
-// d64(v, c_j)) with the same sequential fp64 operations per (point, candidate)
-// (certified-unreachable tiles give 0, exactly what the classic computes
-// there); then the classic chunk reduction replayed in shared memory -- thread
-// t < 256 adds the terms of points t, t+256, t+512, t+768 in order, the same
-// 8-sequential + butterfly warp sums -- and the chunk sums are combined by the
-// last block in the classic order (chunks of a group left to right, then the
-// groups): bit-identical partials, so both refines serve any candidate.
-constexpr int SHORT_THREADS = RCH;
-template <typename T>
-__global__ void __launch_bounds__(SHORT_THREADS, 1) k_refine_short(const T* __restrict__ V, int pitch, int64_t n,
-                                                                   int d, const double* __restrict__ cm64,
-                                                                   const int* __restrict__ wcount,
-                                                                   const int64_t* __restrict__ wlist, int nchunks,
-                                                                   int ng, double* __restrict__ xch,
-                                                                   double* __restrict__ part_r, RefinePrune pr,
-                                                                   RefineFinal fin) {
-  extern __shared__ double dsm[];  // cd: RW * d doubles, then terms [RW][RCH]
-  double* cd = dsm;
-  double* tr = dsm + RW * d;
+// Refine of a short window (<= RW candidates: the lazy first batch).  The
+// classic k_refine gives each (window group, chunk group) unit to a 256-thread
+// block (4 points per thread, the row loads on its critical path), so a short
+// window runs latency-bound on nchunks blocks.  Here every point is one thread
+// and every chunk is SHORT_SPLIT blocks of RED_THREADS (all SMs stream V):
+// term(v, j) = max(0, cm(v) - d64(v, c_j)) with the same sequential fp64
+// operations per (point, candidate) (certified-unreachable tiles give 0,
+// exactly what the classic computes there), written to xt; the block taking a
+// chunk's last ticket replays the classic chunk reduction -- thread t adds the
+// terms of points t, t+256, t+512, t+768 in order, the same 8-sequential +
+// butterfly warp sums -- and the chunk sums are combined by the last chunk in
+// the classic order (chunks of a group left to right, then the groups):
+// bit-identical partials, so both refines serve any candidate.
+constexpr int SHORT_THREADS = RED_THREADS;
+constexpr int SHORT_SPLIT = RCH / RED_THREADS;  // blocks per chunk
+struct ShortBufs {
+  double* xt = nullptr;              // RW x n_pad terms
+  int64_t xstride = 0;               // n_pad
+  unsigned int* chunk_ticket = nullptr;  // nchunks (zero between launches)
+};
+// STAGE: the block's 256 rows and cm values arrive by two bulk copies on one
+// mbarrier (one request in flight per block instead of a row walk per thread).
+template <typename T, bool STAGE>
+__global__ void __launch_bounds__(SHORT_THREADS) k_refine_short(const T* __restrict__ V, int pitch, int64_t n,
+                                                                int d, const double* __restrict__ cm64,
+                                                                const int* __restrict__ wcount,
+                                                                const int64_t* __restrict__ wlist, int nchunks,
+                                                                int ng, double* __restrict__ xch,
+                                                                double* __restrict__ part_r, RefinePrune pr,
+                                                                RefineFinal fin, ShortBufs sb) {
+  // dynamic smem: STAGE ? [rows 256 x pitch T][cm 256 doubles] : [], then cd: RW * d doubles,
+  // then (fp32 rows) cf: RW * d floats for the far32 pre-test
+  extern __shared__ __align__(128) unsigned char rs_smem[];
+  const size_t stage_bytes = STAGE ? (size_t)RED_THREADS * pitch * sizeof(T) + RED_THREADS * sizeof(double) : 0;
+  double* cd = reinterpret_cast<double*>(rs_smem + stage_bytes);
+  float* cf = reinterpret_cast<float*>(cd + RW * d);
+  __shared__ uint64_t sfull;
   __shared__ double red[RW][RED_THREADS];
-  __shared__ int lmask[RCH / 64];  // live candidates per point tile of the chunk
+  __shared__ int lmask[RED_THREADS / 64];  // live candidates per point tile of this block
+  __shared__ int flag;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int wc = min(RW, *wcount);
-  const int ch = blockIdx.x;
+  const int ch = blockIdx.x / SHORT_SPLIT, qb = blockIdx.x - ch * SHORT_SPLIT;
+  const int64_t bs = (int64_t)ch * RCH + (int64_t)qb * RED_THREADS;
+  if (STAGE && tid == 0) {
+    mbar_init(&sfull, 1);
+    fence_mbar_init();
+    if (bs < n && wc > 0) {  // rows < n_pad: always a whole slice
+      const uint32_t rb = (uint32_t)RED_THREADS * pitch * sizeof(T);
+      mbar_arrive_expect_tx(&sfull, rb + RED_THREADS * 8);
+      bulk_g2s(rs_smem, V + bs * pitch, rb, &sfull);
+      bulk_g2s(rs_smem + rb, cm64 + bs, RED_THREADS * 8, &sfull);
+    }
+  }
   for (int i = tid; i < RW * d; i += blockDim.x) {
     const int j = i / d, k = i - j * d;
-    cd[i] = j < wc ? (double)V[wlist[j] * pitch + k] : 0.0;
+    const T x = j < wc ? V[wlist[j] * pitch + k] : (T)0;
+    cd[i] = (double)x;
+    if constexpr (sizeof(T) == 4) cf[i] = (float)x;
   }
-  const int tpc = RCH / pr.np;
-  if (tid < tpc) {
+  const int64_t b0 = (int64_t)ch * RCH + (int64_t)qb * RED_THREADS;  // first point of this block
+  const int tpb = RED_THREADS / pr.np;                                // point tiles per block (np <= 256)
+  if (tid < max(tpb, 1)) {
     unsigned m = (1u << wc) - 1u;
-    const int64_t t = (int64_t)ch * tpc + tid;
+    const int64_t t = b0 / pr.np + tid;
     if (pr.rho && t * pr.np < n) {
       m = 0;
       for (int j = 0; j < wc; ++j) {
@@ -2090,13 +2144,59 @@ __global__ void __launch_bounds__(SHORT_THREADS, 1) k_refine_short(const T* __re
     lmask[tid] = (int)m;
   }
   __syncthreads();
-  const int64_t v = (int64_t)ch * RCH + tid;
-  const unsigned lm = (unsigned)lmask[tid / pr.np];
+  const int64_t v = b0 + tid;
+  unsigned lm = (unsigned)lmask[tpb > 0 ? tid / pr.np : 0];
+  if (STAGE && bs < n && wc > 0) mbar_wait(&sfull, 0);
+  const double c = v < n ? (STAGE ? reinterpret_cast<const double*>(rs_smem + (size_t)RED_THREADS * pitch *
+                                                                              sizeof(T))[tid]
+                                  : cm64[v])
+                         : 0.0;
   double s[RW];
 #pragma unroll
   for (int j = 0; j < RW; ++j) s[j] = 0.0;
+  if constexpr (sizeof(T) == 4) {
+    // far32 pre-test: only candidates that may be closer than cm get the fp64 sum
+    if (v < n && lm) {
+      const float4* r4 = STAGE ? reinterpret_cast<const float4*>(reinterpret_cast<const float*>(rs_smem) +
+                                                                 (size_t)tid * pitch)
+                               : reinterpret_cast<const float4*>(V + v * pitch);
+      float q32[RW];
+#pragma unroll
+      for (int j = 0; j < RW; ++j) q32[j] = 0.f;
+      int k = 0;
+      for (; k + 4 <= d; k += 4) {
+        const float4 q = STAGE ? r4[k >> 2] : __ldg(r4 + (k >> 2));
+#pragma unroll
+        for (int j = 0; j < RW; ++j)
+          if (lm >> j & 1u) {
+            const float* cj = cf + j * d + k;
+            float x = q.x - cj[0];
+            q32[j] = fmaf(x, x, q32[j]);
+            x = q.y - cj[1];
+            q32[j] = fmaf(x, x, q32[j]);
+            x = q.z - cj[2];
+            q32[j] = fmaf(x, x, q32[j]);
+            x = q.w - cj[3];
+            q32[j] = fmaf(x, x, q32[j]);
+          }
+      }
+      for (; k < d; ++k) {
+        const float xr = reinterpret_cast<const float*>(r4)[k];
+#pragma unroll
+        for (int j = 0; j < RW; ++j)
+          if (lm >> j & 1u) {
+            const float x = xr - cf[j * d + k];
+            q32[j] = fmaf(x, x, q32[j]);
+          }
+      }
+      const double ks = far32_scale(d);
+#pragma unroll
+      for (int j = 0; j < RW; ++j)
+        if ((lm >> j & 1u) && far32(q32[j], ks, c)) lm &= ~(1u << j);
+    }
+  }
   if (v < n && lm) {
-    const T* row = V + v * pitch;
+    const T* row = STAGE ? reinterpret_cast<const T*>(rs_smem) + (size_t)tid * pitch : V + v * pitch;
     auto step = [&](int k, double x) {
 #pragma unroll
       for (int j = 0; j < RW; ++j)
@@ -2110,7 +2210,9 @@ __global__ void __launch_bounds__(SHORT_THREADS, 1) k_refine_short(const T* __re
       for (; k + 16 <= d; k += 16) {  // 4 x LDG.128 in flight
         float4 q[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) q[i] = __ldg(reinterpret_cast<const float4*>(row) + (k >> 2) + i);
+        for (int i = 0; i < 4; ++i)
+          q[i] = STAGE ? reinterpret_cast<const float4*>(row)[(k >> 2) + i]
+                       : __ldg(reinterpret_cast<const float4*>(row) + (k >> 2) + i);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           step(k + 4 * i, (double)q[i].x);
@@ -2120,7 +2222,8 @@ __global__ void __launch_bounds__(SHORT_THREADS, 1) k_refine_short(const T* __re
         }
       }
       for (; k + 4 <= d; k += 4) {
-        const float4 q = __ldg(reinterpret_cast<const float4*>(row) + (k >> 2));
+        const float4 q = STAGE ? reinterpret_cast<const float4*>(row)[k >> 2]
+                               : __ldg(reinterpret_cast<const float4*>(row) + (k >> 2));
         step(k, (double)q.x);
         step(k + 1, (double)q.y);
         step(k + 2, (double)q.z);
@@ -2129,24 +2232,33 @@ __global__ void __launch_bounds__(SHORT_THREADS, 1) k_refine_short(const T* __re
     }
     for (; k < d; ++k) step(k, (double)row[k]);
   }
-  const double c = v < n ? cm64[v] : 0.0;
-#pragma unroll
-  for (int j = 0; j < RW; ++j) {
-    const double t = c - s[j];
-    tr[j * RCH + tid] = (lm >> j & 1u) && t > 0.0 ? t : 0.0;
-  }
-  __syncthreads();
-  // the classic reduction: thread t < 256 adds its 4 points in order
-  if (tid < RED_THREADS) {
+  if (v < n) {
 #pragma unroll
     for (int j = 0; j < RW; ++j) {
-      double acc = 0.0;
-      if (j < wc)
-#pragma unroll
-        for (int i = 0; i < RCH / RED_THREADS; ++i)
-          if ((int64_t)ch * RCH + tid + i * RED_THREADS < n) acc += tr[j * RCH + tid + i * RED_THREADS];
-      red[j][tid] = acc;
+      const double t = c - s[j];
+      if (j < wc) sb.xt[(int64_t)j * sb.xstride + v] = (lm >> j & 1u) && t > 0.0 ? t : 0.0;
     }
+  }
+  // the block taking the chunk's last ticket reduces it
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    flag = atomicAdd(sb.chunk_ticket + ch, 1u) == (unsigned)(SHORT_SPLIT - 1);
+  }
+  __syncthreads();
+  if (!flag) return;
+  __threadfence();
+  // the classic reduction: thread t adds the terms of points t, t+256, t+512, t+768 in order
+#pragma unroll
+  for (int j = 0; j < RW; ++j) {
+    double acc = 0.0;
+    if (j < wc)
+#pragma unroll
+      for (int i = 0; i < RCH / RED_THREADS; ++i) {
+        const int64_t w = (int64_t)ch * RCH + tid + i * RED_THREADS;
+        if (w < n) acc += __ldcg(sb.xt + (int64_t)j * sb.xstride + w);
+      }
+    red[j][tid] = acc;
   }
   __syncthreads();
   if (warp < RW) {
@@ -2160,8 +2272,9 @@ __global__ void __launch_bounds__(SHORT_THREADS, 1) k_refine_short(const T* __re
   __shared__ bool last;
   __syncthreads();
   if (tid == 0) {
+    sb.chunk_ticket[ch] = 0u;
     __threadfence();
-    last = atomicAdd(fin.counter, 1u) == gridDim.x - 1;
+    last = atomicAdd(fin.counter, 1u) == (unsigned)nchunks - 1;
   }
   __syncthreads();
   if (!last) return;
@@ -2561,7 +2674,8 @@ __global__ void __launch_bounds__(UFR) k_update_fused(
   // rows < n_pad: always a full slice; cm64 / e0d are allocated n_pad long
   const uint32_t row_bytes = (uint32_t)UFR * pitch * 4;
   double* cd = reinterpret_cast<double*>(uf_smem);
-  unsigned char* stage = uf_smem + (((size_t)d * 8 + 15) & ~(size_t)15);
+  float* cdf = reinterpret_cast<float*>(uf_smem + (((size_t)d * 8 + 15) & ~(size_t)15));  // fp32 copy
+  unsigned char* stage = uf_smem + (((size_t)d * 8 + 15) & ~(size_t)15) + (((size_t)((d + 3) & ~3) * 4 + 15) & ~(size_t)15);
   if (t == 0) {
     mbar_init(&full, 1);
     fence_mbar_init();
@@ -2570,18 +2684,48 @@ __global__ void __launch_bounds__(UFR) k_update_fused(
     bulk_g2s(stage + row_bytes, cm64 + (int64_t)id * UFR, UFR * 8, &full);
     bulk_g2s(stage + row_bytes + UFR * 8, e0d + (int64_t)id * UFR, UFR * 8, &full);
   }
-  for (int k = t; k < d; k += UFR) cd[k] = (double)V[s * pitch + k];
+  for (int k = t; k < d; k += UFR) {
+    const float x = V[s * pitch + k];
+    cd[k] = (double)x;
+    cdf[k] = x;
+  }
   __syncthreads();
   mbar_wait(&full, 0);
   const int64_t v = (int64_t)id * UFR + t;
   if (v < n) {
-    const double dist = dist64_smem_row(reinterpret_cast<const float*>(stage) + (size_t)t * pitch, cd, d);
+    const float* row = reinterpret_cast<const float*>(stage) + (size_t)t * pitch;
     double m = reinterpret_cast<const double*>(stage + row_bytes)[t];
-    if (dist < m) {
-      m = dist;
-      cm64[v] = m;
-      pt[v] = make_pt((float)m, nv32[v], pk);
-      if (seeds.ipa) write_seeds(seeds, v, (float)m);
+    // far32 pre-test: the fp64 distance only where the winner may be closer than cm
+    float q32 = 0.f;
+    {
+      const float4* r4 = reinterpret_cast<const float4*>(row);
+      int k = 0;
+      float qa = 0.f, qb = 0.f;
+      for (; k + 4 <= d; k += 4) {
+        const float4 q = r4[k >> 2];
+        float x = q.x - cdf[k];
+        qa = fmaf(x, x, qa);
+        x = q.y - cdf[k + 1];
+        qb = fmaf(x, x, qb);
+        x = q.z - cdf[k + 2];
+        qa = fmaf(x, x, qa);
+        x = q.w - cdf[k + 3];
+        qb = fmaf(x, x, qb);
+      }
+      for (; k < d; ++k) {
+        const float x = row[k] - cdf[k];
+        qa = fmaf(x, x, qa);
+      }
+      q32 = qa + qb;
+    }
+    if (!far32(q32, far32_scale(d), m)) {
+      const double dist = dist64_smem_row(row, cd, d);
+      if (dist < m) {
+        m = dist;
+        cm64[v] = m;
+        pt[v] = make_pt((float)m, nv32[v], pk);
+        if (seeds.ipa) write_seeds(seeds, v, (float)m);
+      }
     }
     terms[v] = reinterpret_cast<const double*>(stage + row_bytes + UFR * 8)[t] - m;
   }
@@ -2643,6 +2787,275 @@ __global__ void __launch_bounds__(UFR) k_update_fused(
     *cur = fnew;
     *ctr.chunks_done = 0u;
   }
+}
+
+// K4 fused with the NEXT lazy step's first batch (DESIGN.md §4 "update + batch"):
+// each 256-row slice is staged once (bulk copies, as k_update_fused) and serves
+// both the winner's distances -> cm (k_update_fused's operations) and, with the
+// NEW cm, the batch candidates' terms (k_refine_short's operations: the
+// sequential fp64 sum per (point, candidate), max(0, cm - d)).  A chunk's last
+// ticket taker sums its f(S) terms (k_update_reduce's order) and its batch terms
+// (the classic chunk reduction); the block completing the last chunk records
+// f(S), then the batch's group partials and finalize, which decides the next
+// step reading the f(S) it just wrote -- the same values as the two launches.
+struct BatchArgs {
+  const int* wcount = nullptr;
+  const int64_t* wlist = nullptr;
+  double* xch = nullptr;     // RW x nchunks chunk sums
+  double* part_r = nullptr;  // RW x ng group partials
+  int ng = 1;
+  ShortBufs sb;              // xt terms (the per-chunk tickets are the update's)
+  RefineFinal fin;
+};
+// The rows k_update_batch keeps in shared memory, packed once per step in its
+// smem layout (one bulk copy per block instead of every block walking the
+// winner's and the batch's rows): [cd: the winner's row, fp64][cb: RW batch
+// rows, fp64][cg: RW batch rows + the winner's, fp32, stride dp][cn: their
+// fp32 norms].  One block per row (RW + 1 blocks).
+struct BatchPackLayout {
+  size_t dbytes, cbytes, fbytes;
+  __host__ __device__ BatchPackLayout(int d) {
+    const size_t dp = (size_t)((d + 3) & ~3);
+    dbytes = ((size_t)d * 8 + 15) & ~(size_t)15;
+    cbytes = ((size_t)RW * d * 8 + 15) & ~(size_t)15;
+    fbytes = (((size_t)(RW + 1) * dp + RW + 1) * 4 + 15) & ~(size_t)15;
+  }
+  __host__ __device__ size_t bytes() const { return dbytes + cbytes + fbytes; }
+};
+__global__ void k_batch_pack(const float* __restrict__ V, int pitch, int d, const float* __restrict__ nv32,
+                             const int64_t* __restrict__ best, const int* __restrict__ wcount,
+                             const int64_t* __restrict__ wlist, unsigned char* __restrict__ pack) {
+  const BatchPackLayout L(d);
+  const int dp = (d + 3) & ~3;
+  double* cd = reinterpret_cast<double*>(pack);
+  double* cb = reinterpret_cast<double*>(pack + L.dbytes);
+  float* cg = reinterpret_cast<float*>(pack + L.dbytes + L.cbytes);
+  float* cn = cg + (size_t)(RW + 1) * dp;
+  const int j = blockIdx.x;  // 0..RW-1 batch rows, RW the winner
+  const int wc = min(RW, *wcount);
+  const bool on = j == RW ? *best >= 0 : j < wc;
+  const int64_t src = on ? (j == RW ? *best : wlist[j]) : 0;
+  for (int k = threadIdx.x; k < dp; k += blockDim.x) {
+    const float x = on && k < d ? V[src * pitch + k] : 0.f;
+    cg[j * dp + k] = x;
+    if (k < d) {
+      if (j == RW)
+        cd[k] = (double)x;
+      else
+        cb[j * d + k] = (double)x;
+    }
+  }
+  if (threadIdx.x == 0) cn[j] = on ? nv32[src] : 0.f;
+}
+
+// UFR rows per slice (64, 128 or 256; k_update_fused's virtual reduction
+// threads).  Dynamic smem: the winner's row and the batch rows (fp64), then the
+// slice stage, which the chunk reductions reuse once every row is consumed.
+template <int UFR>
+__host__ __device__ constexpr size_t update_batch_stage_min() {
+  return (size_t)(RW + 1) * RED_THREADS * sizeof(double);
+}
+template <int UFR>
+__global__ void __launch_bounds__(UFR) k_update_batch(
+    const float* __restrict__ V, int pitch, int64_t n, int d, const int64_t* __restrict__ best, PtCoef pk,
+    const double* __restrict__ e0d, const float* __restrict__ nv32, double* __restrict__ cm64,
+    float4* __restrict__ pt, TcSeeds seeds, double* __restrict__ terms, double* __restrict__ fpart,
+    UpdateCounters ctr, double inv_n, double* __restrict__ cur, double* __restrict__ val_out,
+    double* __restrict__ gain_out, int step, BatchArgs ba, const unsigned char* __restrict__ pack) {
+  static_assert(RED_THREADS % UFR == 0 && RCH % UFR == 0 && UFR >= 64, "slices tile the chunk reduction");
+  constexpr int VT = RED_THREADS / UFR;
+  extern __shared__ __align__(16) unsigned char uf_smem[];
+  __shared__ uint64_t full;
+  __shared__ int flag;
+  const int64_t s = *best;
+  if (s < 0) return;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int id = blockIdx.x;
+  const int nslices = gridDim.x;
+  const int nchunks = (int)((n + RCH - 1) / RCH);
+  const int wc = min(RW, *ba.wcount);
+  const uint32_t row_bytes = (uint32_t)UFR * pitch * 4;
+  const int dp = (d + 3) & ~3;
+  const BatchPackLayout L(d);
+  double* cd = reinterpret_cast<double*>(uf_smem);                     // the winner's row
+  double* cb = reinterpret_cast<double*>(uf_smem + L.dbytes);          // the batch rows (RW x d)
+  float* cg = reinterpret_cast<float*>(uf_smem + L.dbytes + L.cbytes);  // fp32 rows (RW batch + the winner), stride dp
+  float* cn = cg + (size_t)(RW + 1) * dp;                               // their fp32 norms
+  unsigned char* stage = uf_smem + L.bytes();
+  double (*red)[RED_THREADS] = reinterpret_cast<double (*)[RED_THREADS]>(stage);  // after the rows
+  double* sbuf = reinterpret_cast<double*>(stage) + RW * RED_THREADS;
+  if (t == 0) {
+    mbar_init(&full, 1);
+    fence_mbar_init();
+    mbar_arrive_expect_tx(&full, row_bytes + 2 * UFR * 8 + (uint32_t)L.bytes());
+    bulk_g2s(uf_smem, pack, (uint32_t)L.bytes(), &full);
+    bulk_g2s(stage, V + (int64_t)id * UFR * pitch, row_bytes, &full);
+    bulk_g2s(stage + row_bytes, cm64 + (int64_t)id * UFR, UFR * 8, &full);
+    bulk_g2s(stage + row_bytes + UFR * 8, e0d + (int64_t)id * UFR, UFR * 8, &full);
+  }
+  __syncthreads();
+  mbar_wait(&full, 0);
+  const int64_t v = (int64_t)id * UFR + t;
+  if (v < n) {
+    const float* row = reinterpret_cast<const float*>(stage) + (size_t)t * pitch;
+    const float4* r4 = reinterpret_cast<const float4*>(row);
+    // Gram-form fp32 pre-tests (far32_gram) for the winner and the batch, one pass
+    float g[RW + 1];
+#pragma unroll
+    for (int j = 0; j <= RW; ++j) g[j] = 0.f;
+    for (int k4 = 0; k4 < dp / 4; ++k4) {
+      const float4 q = r4[k4];
+#pragma unroll
+      for (int j = 0; j <= RW; ++j)
+        if (j == RW || j < wc) {
+          const float4 c4 = reinterpret_cast<const float4*>(cg + j * dp)[k4];
+          g[j] = fmaf(q.x, c4.x, g[j]);
+          g[j] = fmaf(q.y, c4.y, g[j]);
+          g[j] = fmaf(q.z, c4.z, g[j]);
+          g[j] = fmaf(q.w, c4.w, g[j]);
+        }
+    }
+    const float nv = nv32[v];
+    double m = reinterpret_cast<const double*>(stage + row_bytes)[t];
+    if (!far32_gram(g[RW], nv, cn[RW], d, m)) {
+      const double dist = dist64_smem_row(row, cd, d);
+      if (dist < m) {
+        m = dist;
+        cm64[v] = m;
+        pt[v] = make_pt((float)m, nv32[v], pk);
+        if (seeds.ipa) write_seeds(seeds, v, (float)m);
+      }
+    }
+    terms[v] = reinterpret_cast<const double*>(stage + row_bytes + UFR * 8)[t] - m;
+    // the batch's terms with the new minimum (k_refine_short's operation order),
+    // fp64 only where the pre-test cannot rule the term out
+    unsigned lm = 0;
+#pragma unroll
+    for (int j = 0; j < RW; ++j)
+      if (j < wc && !far32_gram(g[j], nv, cn[j], d, m)) lm |= 1u << j;
+    double sj[RW];
+#pragma unroll
+    for (int j = 0; j < RW; ++j) sj[j] = 0.0;
+    if (lm) {
+      auto step_k = [&](int k, double x) {
+#pragma unroll
+        for (int j = 0; j < RW; ++j)
+          if (lm >> j & 1u) {
+            const double tt = x - cb[j * d + k];
+            sj[j] = fma(tt, tt, sj[j]);
+          }
+      };
+      int k = 0;
+      for (; k + 4 <= d; k += 4) {
+        const float4 q = r4[k >> 2];
+        step_k(k, (double)q.x);
+        step_k(k + 1, (double)q.y);
+        step_k(k + 2, (double)q.z);
+        step_k(k + 3, (double)q.w);
+      }
+      for (; k < d; ++k) step_k(k, (double)row[k]);
+    }
+#pragma unroll
+    for (int j = 0; j < RW; ++j)
+      if (j < wc) {
+        const double tt = m - sj[j];
+        ba.sb.xt[(int64_t)j * ba.sb.xstride + v] = (lm >> j & 1u) && tt > 0.0 ? tt : 0.0;
+      }
+  }
+  __syncthreads();  // every row consumed: the stage is reused below
+  const int c = id / (RCH / UFR);
+  if (t == 0) {
+    __threadfence();  // the block's terms (ordered by the barrier) before the ticket
+    const int in_chunk = min(RCH / UFR, nslices - c * (RCH / UFR));
+    flag = atomicAdd(ctr.chunk_ticket + c, 1u) == (unsigned int)(in_chunk - 1);
+  }
+  __syncthreads();
+  if (!flag) return;
+  __threadfence();
+  // virtual thread u = t + q UFR: the f(S) terms of points u, u+256, u+512, u+768
+  // in order (k_update_reduce), and the batch terms likewise (k_refine_short)
+#pragma unroll
+  for (int q = 0; q < VT; ++q) {
+    const int u = t + q * UFR;
+    double acc = 0.0;
+#pragma unroll
+    for (int i = 0; i < RCH / RED_THREADS; ++i) {
+      const int64_t w = (int64_t)c * RCH + u + (int64_t)i * RED_THREADS;
+      if (w < n) acc += __ldcg(terms + w);
+    }
+    sbuf[u] = acc;
+#pragma unroll
+    for (int j = 0; j < RW; ++j) {
+      double bj = 0.0;
+      if (j < wc)
+#pragma unroll
+        for (int i = 0; i < RCH / RED_THREADS; ++i) {
+          const int64_t w = (int64_t)c * RCH + u + i * RED_THREADS;
+          if (w < n) bj += __ldcg(ba.sb.xt + (int64_t)j * ba.sb.xstride + w);
+        }
+      red[j][u] = bj;
+    }
+  }
+  __syncthreads();
+  // block_sum_256's tree over the virtual threads
+#pragma unroll
+  for (int st = RED_THREADS / 2; st > 0; st >>= 1) {
+    for (int u = t; u < st; u += UFR) sbuf[u] += sbuf[u + st];
+    __syncthreads();
+  }
+  for (int wj = warp; wj < RW; wj += UFR / 32) {
+    double x = 0.0;
+#pragma unroll
+    for (int q = 0; q < RED_THREADS / 32; ++q) x += red[wj][lane * (RED_THREADS / 32) + q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0 && wj < wc) ba.xch[(int64_t)wj * nchunks + c] = x;
+  }
+  const double bs = sbuf[0];
+  __syncthreads();
+  if (t == 0) {
+    ctr.chunk_ticket[c] = 0u;
+    fpart[c] = bs;
+    __threadfence();
+    flag = atomicAdd(ctr.chunks_done, 1u) == (unsigned int)(nchunks - 1);
+  }
+  __syncthreads();
+  if (!flag) return;
+  __threadfence();
+  // chunk partials left to right (chunk_total_block with this block's width)
+  double fsum = 0.0;
+  for (int c0 = 0; c0 < nchunks; c0 += UFR) {
+    const int m = min(UFR, nchunks - c0);
+    if (t < m) sbuf[t] = __ldcg(fpart + c0 + t);
+    __syncthreads();
+    if (t == 0)
+      for (int i = 0; i < m; ++i) fsum += sbuf[i];
+    __syncthreads();
+  }
+  const double fnew = fsum * inv_n;
+  if (t == 0) {
+    const double fold = *cur;
+    if (val_out) val_out[step] = fnew;
+    if (gain_out) gain_out[step] = fnew - fold;
+    *cur = fnew;
+    *ctr.chunks_done = 0u;
+  }
+  __syncthreads();
+  // the batch: group partials in the classic order, computed into shared memory
+  // (after red: the stage holds RW * RED_THREADS + (RW x ng) doubles, see the
+  // host's update_batch_smem), then its finalize (reads *cur)
+  double* grp_s = reinterpret_cast<double*>(stage) + (RW + 1) * RED_THREADS;
+  const int cpg = (nchunks + ba.ng - 1) / ba.ng;
+  for (int i = t; i < wc * ba.ng; i += UFR) {
+    const int w = i / ba.ng, grp = i - w * ba.ng;
+    double tot = 0.0;
+    const int c1 = min(nchunks, (grp + 1) * cpg);
+    for (int q = grp * cpg; q < c1; ++q) tot += __ldcg(ba.xch + (int64_t)w * nchunks + q);
+    grp_s[i] = tot;
+  }
+  __syncthreads();
+  refine_finalize_n(ba.fin, wc, ba.wlist, ba.part_r, ba.ng, &red[0][0], reinterpret_cast<long long*>(&red[2][0]),
+                    UFR, grp_s);
 }
 
 // ---------------------------------------------------------------- K2: multiset (work matrix)
