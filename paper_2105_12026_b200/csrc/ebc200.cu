@@ -1891,37 +1891,6 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
     CUC(cudaGetLastError());
   }
   mark("pad");
-  {
-    // L2 residency of the rows: every lazy step streams V twice (the batch
-    // refine and the cached-min update); a persisting access-policy window on
-    // the context's streams (captured into the graphs' kernel nodes) keeps
-    // them in L2 when they fit the persisting carve-out.  EBC200_L2_PERSIST=0: off.
-    const char* lp = getenv("EBC200_L2_PERSIST");
-    int maxp = 0, maxw = 0;
-    const size_t vbytes = (size_t)ctx->n_pad * ctx->pitch * esz;
-    if (!(lp && lp[0] == '0') && cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, device) == cudaSuccess &&
-        cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, device) == cudaSuccess && maxp > 0 &&
-        maxw > 0) {
-      size_t cur = 0;
-      cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
-      const size_t want = std::min<size_t>((size_t)maxp, vbytes);
-      if (cur < want) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
-      cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
-      cudaStreamAttrValue av{};
-      av.accessPolicyWindow.base_ptr = Vdev;
-      av.accessPolicyWindow.num_bytes = std::min<size_t>(vbytes, (size_t)maxw);
-      av.accessPolicyWindow.hitRatio =
-          (float)std::min(1.0, (double)cur / (double)av.accessPolicyWindow.num_bytes);
-      av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-      av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-      for (cudaStream_t st : {ctx->stream, ctx->side[0], ctx->side[1]})
-        cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &av);
-      (void)cudaGetLastError();
-      if (prof)
-        fprintf(stderr, "[ebc_create] L2 persist: max %d B, window max %d B, carve-out %zu B, V %zu B, hit ratio %.3f\n",
-                maxp, maxw, cur, vbytes, av.accessPolicyWindow.hitRatio);
-    }
-  }
   if (dtype != EBC_F64) {
     // fp32 range guard: every screen (and the sparse work-matrix flag screen)
     // forms squared distances, norms and short sums in fp32.  Grounds whose
