@@ -312,6 +312,7 @@ struct ebc_ctx {
   int lazy_batch = 4;              // EBC200_LAZY_BATCH (1..RW): candidates refined first in a lazy step
   bool probe_on = true;            // EBC200_LAZY_PROBE=0: no ring-probe batch on undecided steps
   bool fuse_batch = true;          // EBC200_FUSE_BATCH=0: the next step's first batch not folded into K4
+  int64_t probe_min_n = 32768;     // EBC200_PROBE_MIN_N: candidates below which undecided steps skip probe / near bound
   int batch_ready_step = -1;       // enqueue-time: that step's first batch was launched with the last update
   cudaGraphConditionalHandle batch_hrest = 0;
   int ub_rows = 128;               // EBC200_UB_ROWS: rows per k_update_batch slice (64, 128, 256)
@@ -1253,7 +1254,11 @@ int run_step_select(ebc_ctx* ctx, int step, int commit, int64_t* sel_dev) {
     // undecided step (level[0] == -3): stale set -> mode -> screen / refine
     CondScope ca;
     CU(ca.open(ctx, hrest, 0));
-    if (ctx->probe_on && has_screen && ctx->refine2 && short_refine_smem(ctx) <= 180 * 1024) {
+    // probe batch and near-centre bound: only where a stale set can be large
+    // enough to matter (small grounds' undecided steps go to the exact refine
+    // anyway; the extra launches would only add latency, C1 0.68 -> 0.90 ms)
+    const bool big = ncand >= ctx->probe_min_n;
+    if (big && ctx->probe_on && has_screen && ctx->refine2 && short_refine_smem(ctx) <= 180 * 1024) {
       // probe batch: ring winners around the last selected centre raise lb
       // (k_lazy_rings) before the stale set is listed
       k_lazy_rings<<<ag, 256, (size_t)ctx->d * sizeof(float), ctx->stream>>>(
@@ -1269,7 +1274,7 @@ int run_step_select(ebc_ctx* ctx, int step, int commit, int64_t* sel_dev) {
       ctx->cmx_fresh = false;
       if (rc) return rc;
     }
-    if (ctx->nb_on && has_screen) {
+    if (big && ctx->nb_on && has_screen) {
       // near-centre bound: the neighbours of the centre just selected leave the
       // stale set without a screen (k_lazy_nearbound)
       const bool regs = ctx->d <= 32;
@@ -2079,6 +2084,8 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
     ctx->probe.plist = (int64_t*)(pbm + NRING * 8 + 16);
     const char* pe = getenv("EBC200_LAZY_PROBE");
     if (pe && pe[0] == '0') ctx->probe_on = false;
+    const char* pm = getenv("EBC200_PROBE_MIN_N");
+    if (pm && pm[0]) ctx->probe_min_n = std::max(0, atoi(pm));
     const char* fz = getenv("EBC200_FUSE_BATCH");
     if (fz && fz[0] == '0') ctx->fuse_batch = false;
     const char* ur = getenv("EBC200_UB_ROWS");

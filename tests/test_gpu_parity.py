@@ -852,10 +852,14 @@ def test_lazy_steps_bit_identical_to_full_screens(monkeypatch, kind):
                       ("nocond", {"EBC200_GRAPH_COND": "0"}), ("nogather", {"EBC200_GATHER": "0"}),
                       ("noeagersync", {"EBC200_EAGER_SYNC": "0"}), ("noprobe", {"EBC200_LAZY_PROBE": "0"}),
                       ("nonear", {"EBC200_LAZY_NEARBOUND": "0"}), ("nofuse", {"EBC200_FUSE_BATCH": "0"}),
-                      ("fuse64", {"EBC200_UB_ROWS": "64"}), ("fuse256", {"EBC200_UB_ROWS": "256"})):
+                      ("fuse64", {"EBC200_UB_ROWS": "64"}), ("fuse256", {"EBC200_UB_ROWS": "256"}),
+                      ("probe_gated", {"EBC200_PROBE_MIN_N": "32768"})):
         for key in ("EBC200_LAZY", "EBC200_REFINE2", "EBC200_GRAPH_COND", "EBC200_GATHER", "EBC200_EAGER_SYNC",
                     "EBC200_LAZY_PROBE", "EBC200_LAZY_NEARBOUND", "EBC200_FUSE_BATCH", "EBC200_UB_ROWS"):
             monkeypatch.delenv(key, raising=False)
+        # the probe batch and the near-centre bound on every case size (the
+        # library skips them below 32k candidates; "probe_gated" keeps that)
+        monkeypatch.setenv("EBC200_PROBE_MIN_N", "0")
         for key, val in env.items():
             monkeypatch.setenv(key, val)
         f = fn(X, prec)
