@@ -315,7 +315,7 @@ struct ebc_ctx {
   int64_t probe_min_n = 32768;     // EBC200_PROBE_MIN_N: candidates below which undecided steps skip probe / near bound
   int batch_ready_step = -1;       // enqueue-time: that step's first batch was launched with the last update
   cudaGraphConditionalHandle batch_hrest = 0;
-  int ub_rows = 128;               // EBC200_UB_ROWS: rows per k_update_batch slice (64, 128, 256)
+  int ub_rows = 128;               // EBC200_UB_ROWS: rows per k_update_batch slice (64 or 128; two threads per row)
   ProbeBuf probe;                  // k_lazy_rings: ring winners, ticket, the probe list
   bool nb_on = false;              // EBC200_LAZY_NEARBOUND=0: no near-centre bound (k_lazy_nearbound)
   ChunkGeo geo;                    // per-chunk mean / radius / e0 sums for the near-centre bound
@@ -1442,8 +1442,7 @@ int run_update(ebc_ctx* ctx, int step, double* val_dev, double* gain_dev);
 // Dynamic shared memory of k_update_batch<rows> (0: does not fit one block).
 size_t update_batch_smem(const ebc_ctx* ctx, int rows) {
   const size_t stage = std::max<size_t>((size_t)rows * ctx->pitch * 4 + (size_t)rows * 16,
-                                        ((size_t)(RW + 1) * RED_THREADS + (size_t)RW * refine_groups(ctx)) *
-                                            sizeof(double));
+                                        ((size_t)(RW + 1) * RED_THREADS + RW + 1) * sizeof(double));
   const size_t b = BatchPackLayout(ctx->d).bytes() + stage;
   return b <= 200 * 1024 ? b : 0;
 }
@@ -1452,7 +1451,8 @@ size_t update_batch_smem(const ebc_ctx* ctx, int rows) {
 // K4 (k_update_batch): fp32 rows on the fused K4 path, the short refine.
 bool batch_fusable(const ebc_ctx* ctx) {
   return ctx->fuse_batch && ctx->lazy_on && ctx->refine2 && ctx->uf_on && ctx->dtype != EBC_F64 &&
-         !ctx->in_sharded_run && short_refine_smem(ctx) <= 180 * 1024 && update_batch_smem(ctx, ctx->ub_rows) > 0;
+         !ctx->in_sharded_run && short_refine_smem(ctx) <= 180 * 1024 && update_batch_smem(ctx, ctx->ub_rows) > 0 &&
+         refine_groups(ctx) <= 256;
 }
 
 // K4 of `step` together with the first batch of lazy step step + 1: k_lazy_topk,
@@ -1478,7 +1478,7 @@ int run_update_batch(ebc_ctx* ctx, int step, double* val_dev, double* gain_dev, 
   ba.sb.xt = (double*)ctx->sxt.p;
   ba.sb.xstride = ctx->n_pad;
   ba.fin = fb;
-  const int rows = ctx->ub_rows;
+  const int rows = ctx->ub_rows;  // two threads per row: 128 or 256 threads
   const size_t dsm = update_batch_smem(ctx, rows);
   const size_t pbytes = BatchPackLayout(ctx->d).bytes();
   const bool pfresh = ctx->ubpack.bytes < pbytes;
@@ -1491,13 +1491,13 @@ int run_update_batch(ebc_ctx* ctx, int step, double* val_dev, double* gain_dev, 
   const unsigned grid = (unsigned)((ctx->n + rows - 1) / rows);
   auto go = [&](auto kern) -> int {
     CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
-    kern<<<grid, rows, dsm, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->n, ctx->d, ctx->best, ctx->pk, ctx->e0d,
+    kern<<<grid, 2 * rows, dsm, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->n, ctx->d, ctx->best, ctx->pk, ctx->e0d,
                                            ctx->nv32, ctx->cm64, ctx->pt, tc_seeds(ctx), ctx->terms,
                                            ctx->chunkpart, uc, 1.0 / (double)ctx->n, ctx->cur, val_dev, gain_dev,
                                            step, ba, (const unsigned char*)ctx->ubpack.p);
     return EBC_OK;
   };
-  rc = rows == 64 ? go(k_update_batch<64>) : (rows == 256 ? go(k_update_batch<256>) : go(k_update_batch<128>));
+  rc = rows == 64 ? go(k_update_batch<64>) : go(k_update_batch<128>);
   if (rc) return rc;
   KCHECK();
   ctx->batch_ready_step = step + 1;
@@ -2091,7 +2091,7 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
     const char* ur = getenv("EBC200_UB_ROWS");
     if (ur && ur[0]) {
       const int r = atoi(ur);
-      ctx->ub_rows = r == 64 || r == 256 ? r : 128;
+      ctx->ub_rows = r == 64 ? 64 : 128;
     }
   }
   {
@@ -2377,6 +2377,25 @@ int ebc_last_timings(const ebc_ctx* ctx, double* out_ms4) {
 }
 
 int64_t ebc_last_launches(const ebc_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+#ifdef EBC200_TRACE
+// Development only (-DEBC200_TRACE): read (and with reset, re-arm) the fused
+// update's per-step phase stamps; out = 64 x 8 globaltimer values.
+int ebc_debug_ub_trace(unsigned long long* out, int reset) {
+  if (cudaDeviceSynchronize() != cudaSuccess) return EBC_ECUDA;
+  if (out && cudaMemcpyFromSymbol(out, g_ub_trace, sizeof(g_ub_trace)) != cudaSuccess) return EBC_ECUDA;
+  if (out && cudaMemcpyFromSymbol(out + 64 * 8, g_ub_blk, sizeof(g_ub_blk)) != cudaSuccess) return EBC_ECUDA;
+  if (reset) {
+    static unsigned long long init[64][8];
+    for (auto& r : init) {
+      for (auto& x : r) x = 0ull;
+      r[0] = ~0ull;
+    }
+    if (cudaMemcpyToSymbol(g_ub_trace, init, sizeof(init)) != cudaSuccess) return EBC_ECUDA;
+  }
+  return EBC_OK;
+}
+#endif
 
 int ebc_screen_info(const ebc_ctx* ctx, int64_t* out4) {
   if (!ctx || !out4) return fail(nullptr, EBC_EINVAL, "ebc_screen_info: NULL argument");

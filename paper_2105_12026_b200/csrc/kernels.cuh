@@ -1763,11 +1763,21 @@ struct RefineFinal {
 // computed them there); otherwise they are read from part_r.
 __device__ void refine_finalize_n(const RefineFinal& F, int wc, const int64_t* __restrict__ wlist,
                                   const double* __restrict__ part_r, int ng, double* sred, long long* sidx,
-                                  int nt, const double* pre = nullptr) {
+                                  int nt, const double* pre = nullptr, const double* fsm = nullptr) {
   const int tid = threadIdx.x;
   const bool on = tid < nt;
-  const double f = *F.cur;
-  double top = -INFINITY, gmax = 0.0;
+  // thread 0's reads of the step state go out first (no latency on the tail)
+  long long st[8] = {0, 0, 0, 0, 0, 0, 0, 0}, lvl1 = -1, mlb = 0;
+  double ubn = 0.0;
+  if (tid == 0) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) st[i] = F.stats[i];
+    if (F.level) lvl1 = F.level[1];
+    if (F.batch == 1) ubn = *F.ub_next;
+    if (F.batch == 3) mlb = *F.maxlb;
+  }
+  const double f = fsm ? *fsm : *F.cur;
+  double top = -INFINITY, gmax = 0.0, mine = 0.0;
   // short windows: every partial loaded by the whole block first (one memory
   // round trip), then each candidate's left-to-right sum from shared memory --
   // the same additions in the same order as chunk_total
@@ -1783,6 +1793,7 @@ __device__ void refine_finalize_n(const RefineFinal& F, int wc, const int64_t* _
   __syncthreads();
   for (int w = tid; w < wc && on; w += nt) {
     const double gsum = staged ? gs : chunk_total(part_r + (int64_t)w * ng, ng);
+    mine = gsum;  // staged: w == tid, read back below without a memory round trip
     F.wgain[w] = gsum;
     if (F.ubp) F.ubp[wlist[w] - F.c0] = gsum;  // the exact gain bounds every later one (submodularity)
     top = fmax(top, __dadd_rn(f, __dmul_rn(gsum, F.inv_n)));  // no FMA contraction: host pick() matches
@@ -1804,16 +1815,16 @@ __device__ void refine_finalize_n(const RefineFinal& F, int wc, const int64_t* _
   if (F.batch == 3) {  // probe batch (k_lazy_rings): raises lb, decides nothing
     if (tid == 0 && wc > 0) {
       const long long k = dkey(sred[nt]);
-      if (k > *F.maxlb) *F.maxlb = k;
-      F.stats[6] += wc;
+      if (k > mlb) *F.maxlb = k;
+      F.stats[6] = st[6] + wc;
     }
     return;
   }
   if (F.batch == 2) {  // sharded: the decision waits for the global bound (k_lazy_decide)
     if (tid == 0) {
       *F.maxlb = dkey(sred[nt]);
-      F.stats[7] += 1;
-      F.stats[6] += wc;
+      F.stats[7] = st[7] + 1;
+      F.stats[6] = st[6] + wc;
       F.level[0] = -3;
       *F.scount = 0;  // for the undecided path
     }
@@ -1823,11 +1834,11 @@ __device__ void refine_finalize_n(const RefineFinal& F, int wc, const int64_t* _
     __shared__ int sdone;
     if (tid == 0) {
       const double lb = sred[nt];
-      const int done = *F.ub_next < lb - F.margin - 1e-9 * fabs(lb);
+      const int done = ubn < lb - F.margin - 1e-9 * fabs(lb);
       *F.maxlb = dkey(lb);
-      F.stats[7] += 1;
-      F.stats[5] += done;
-      F.stats[6] += wc;
+      F.stats[7] = st[7] + 1;
+      F.stats[5] = st[5] + done;
+      F.stats[6] = st[6] + wc;
       F.level[0] = done ? -2 : -3;
       *F.scount = 0;
       if (F.hrest) cudaGraphSetConditional(F.hrest, done ? 0u : 1u);
@@ -1839,7 +1850,7 @@ __device__ void refine_finalize_n(const RefineFinal& F, int wc, const int64_t* _
   const double window = 1e-12 * fmax(1.0, fabs(top));
   long long bi = LLONG_MAX;
   for (int w = tid; w < wc && on; w += nt) {
-    const double val = __dadd_rn(f, __dmul_rn(F.wgain[w], F.inv_n));
+    const double val = __dadd_rn(f, __dmul_rn(staged ? mine : F.wgain[w], F.inv_n));
     if (val >= top - window) bi = min(bi, (long long)wlist[w]);
   }
   if (on) sidx[tid] = bi;
@@ -1851,10 +1862,10 @@ __device__ void refine_finalize_n(const RefineFinal& F, int wc, const int64_t* _
   if (tid == 0) {
     const long long b = sidx[0] == LLONG_MAX ? -1 : sidx[0];
     *F.best = b;
-    F.stats[0] += wc;
-    F.stats[1] = max(F.stats[1], (long long)wc);
-    F.stats[2] = F.level ? F.level[1] : -1;
-    F.stats[3] += 1;
+    F.stats[0] = st[0] + wc;
+    F.stats[1] = max(st[1], (long long)wc);
+    F.stats[2] = lvl1;
+    F.stats[3] = st[3] + 1;
     if (F.commit && b >= 0) {
       F.selected[b] = 1;
       F.sel_out[F.step] = b;
@@ -2732,13 +2743,11 @@ __global__ void __launch_bounds__(UFR) k_update_fused(
   __syncthreads();
   const int c = id / (RCH / UFR);
   if (t == 0) {
-    __threadfence();  // the block's terms (ordered by the barrier) before the ticket
     const int in_chunk = min(RCH / UFR, nslices - c * (RCH / UFR));
-    flag = atomicAdd(ctr.chunk_ticket + c, 1u) == (unsigned int)(in_chunk - 1);
+    flag = ticket_acq_rel(ctr.chunk_ticket + c) == (unsigned int)(in_chunk - 1);
   }
   __syncthreads();
   if (!flag) return;
-  __threadfence();
   // virtual thread u = t + q UFR: its 4 points u, u+256, u+512, u+768 in order
 #pragma unroll
   for (int q = 0; q < VT; ++q) {
@@ -2763,12 +2772,10 @@ __global__ void __launch_bounds__(UFR) k_update_fused(
   if (t == 0) {
     ctr.chunk_ticket[c] = 0u;
     fpart[c] = bs;
-    __threadfence();
-    flag = atomicAdd(ctr.chunks_done, 1u) == (unsigned int)(nchunks - 1);
+    flag = ticket_acq_rel(ctr.chunks_done) == (unsigned int)(nchunks - 1);
   }
   __syncthreads();
   if (!flag) return;
-  __threadfence();
   // chunk partials left to right (chunk_total_block with this block's width)
   double fsum = 0.0;
   for (int c0 = 0; c0 < nchunks; c0 += UFR) {
@@ -2810,8 +2817,9 @@ struct BatchArgs {
 // The rows k_update_batch keeps in shared memory, packed once per step in its
 // smem layout (one bulk copy per block instead of every block walking the
 // winner's and the batch's rows): [cd: the winner's row, fp64][cb: RW batch
-// rows, fp64][cg: RW batch rows + the winner's, fp32, stride dp][cn: their
-// fp32 norms].  One block per row (RW + 1 blocks).
+// rows, fp64][cg: RW batch rows + the winner's, fp32, interleaved by 4 dims:
+// float4 (k4, j) at k4 (RW + 1) + j][cn: their fp32 norms].  One block per
+// row (RW + 1 blocks).
 struct BatchPackLayout {
   size_t dbytes, cbytes, fbytes;
   __host__ __device__ BatchPackLayout(int d) {
@@ -2837,7 +2845,7 @@ __global__ void k_batch_pack(const float* __restrict__ V, int pitch, int d, cons
   const int64_t src = on ? (j == RW ? *best : wlist[j]) : 0;
   for (int k = threadIdx.x; k < dp; k += blockDim.x) {
     const float x = on && k < d ? V[src * pitch + k] : 0.f;
-    cg[j * dp + k] = x;
+    cg[((k >> 2) * (RW + 1) + j) * 4 + (k & 3)] = x;  // interleaved by 4 dims: [dp / 4][RW + 1] float4
     if (k < d) {
       if (j == RW)
         cd[k] = (double)x;
@@ -2848,28 +2856,83 @@ __global__ void k_batch_pack(const float* __restrict__ V, int pitch, int d, cons
   if (threadIdx.x == 0) cn[j] = on ? nv32[src] : 0.f;
 }
 
+#ifdef EBC200_TRACE
+// Development trace (tools/ub_trace.py, -DEBC200_TRACE builds only): per step,
+// globaltimer stamps of the fused update's phases, min/max over blocks.
+__device__ unsigned long long g_ub_trace[64][8];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ unsigned long long g_ub_blk[8192][4];  // one step's per-block stamps (step == 10)
+#define UB_TRACE_BLK(step, i) \
+  if (threadIdx.x == 0 && step == 10 && blockIdx.x < 8192) g_ub_blk[blockIdx.x][i] = gtimer()
+#define UB_TRACE_MIN(step, i) \
+  if (threadIdx.x == 0 && step < 64) atomicMin(&g_ub_trace[step][i], gtimer())
+#define UB_TRACE_MAX(step, i) \
+  if (threadIdx.x == 0 && step < 64) atomicMax(&g_ub_trace[step][i], gtimer())
+#else
+#define UB_TRACE_BLK(step, i)
+#define UB_TRACE_MIN(step, i)
+#define UB_TRACE_MAX(step, i)
+#endif
+
+// fp32 Gram dots of one row (this lane's float4 range [k4b, k4e)) with the
+// first NB batch rows and the winner (g[RW]) of the interleaved pack: packed
+// FFMA2 on (even, odd) dim pairs, no per-candidate predicates (NB is a
+// template argument).  far32_gram's bound holds for any summation order.
+template <int NB>
+__device__ __forceinline__ void gram_dots(const float4* __restrict__ r4, const float4* __restrict__ cgi, int k4b,
+                                          int k4e, float (&g)[RW + 1]) {
+  float2 a[NB + 1];
+#pragma unroll
+  for (int j = 0; j <= NB; ++j) a[j] = make_float2(0.f, 0.f);
+  for (int k4 = k4b; k4 < k4e; ++k4) {
+    const float4 q = r4[k4];
+    const float2 q0 = make_float2(q.x, q.y), q1 = make_float2(q.z, q.w);
+    const float4* c = cgi + k4 * (RW + 1);
+#pragma unroll
+    for (int j = 0; j <= NB; ++j) {
+      const float4 c4 = c[j == NB ? RW : j];
+      a[j] = __ffma2_rn(q0, make_float2(c4.x, c4.y), a[j]);
+      a[j] = __ffma2_rn(q1, make_float2(c4.z, c4.w), a[j]);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < NB; ++j) g[j] = a[j].x + a[j].y;
+  g[RW] = a[NB].x + a[NB].y;
+}
+
 // UFR rows per slice (64, 128 or 256; k_update_fused's virtual reduction
 // threads).  Dynamic smem: the winner's row and the batch rows (fp64), then the
 // slice stage, which the chunk reductions reuse once every row is consumed.
 template <int UFR>
-__host__ __device__ constexpr size_t update_batch_stage_min() {
-  return (size_t)(RW + 1) * RED_THREADS * sizeof(double);
-}
-template <int UFR>
-__global__ void __launch_bounds__(UFR) k_update_batch(
+__global__ void __launch_bounds__(2 * UFR, UFR == 64 ? 5 : 3) k_update_batch(
     const float* __restrict__ V, int pitch, int64_t n, int d, const int64_t* __restrict__ best, PtCoef pk,
     const double* __restrict__ e0d, const float* __restrict__ nv32, double* __restrict__ cm64,
     float4* __restrict__ pt, TcSeeds seeds, double* __restrict__ terms, double* __restrict__ fpart,
     UpdateCounters ctr, double inv_n, double* __restrict__ cur, double* __restrict__ val_out,
     double* __restrict__ gain_out, int step, BatchArgs ba, const unsigned char* __restrict__ pack) {
-  static_assert(RED_THREADS % UFR == 0 && RCH % UFR == 0 && UFR >= 64, "slices tile the chunk reduction");
-  constexpr int VT = RED_THREADS / UFR;
+  // two threads per row (a pair of adjacent lanes): each takes half of the fp32
+  // Gram dots (combined by a shuffle: the far32_gram bound holds for any
+  // summation order), the even lane the winner's exact distance, and the
+  // batch's exact terms are split between the pair (candidate j on lane j & 1)
+  constexpr int NT = 2 * UFR;
+  static_assert(RED_THREADS % NT == 0 && RCH % UFR == 0 && UFR >= 64, "slices tile the chunk reduction");
+  constexpr int VT = RED_THREADS / NT;
+  constexpr int HW = RW / 2;  // batch candidates per lane
   extern __shared__ __align__(16) unsigned char uf_smem[];
   __shared__ uint64_t full;
   __shared__ int flag;
   const int64_t s = *best;
   if (s < 0) return;
+  UB_TRACE_MIN(step, 0);
+  UB_TRACE_MAX(step, 1);
+  UB_TRACE_BLK(step, 0);
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int r = t >> 1, p = t & 1;
+  const unsigned pm = 3u << (lane & 30);  // the pair's lanes (the pair always branches together)
   const int id = blockIdx.x;
   const int nslices = gridDim.x;
   const int nchunks = (int)((n + RCH - 1) / RCH);
@@ -2893,56 +2956,70 @@ __global__ void __launch_bounds__(UFR) k_update_batch(
     bulk_g2s(stage + row_bytes, cm64 + (int64_t)id * UFR, UFR * 8, &full);
     bulk_g2s(stage + row_bytes + UFR * 8, e0d + (int64_t)id * UFR, UFR * 8, &full);
   }
+  const int64_t v = (int64_t)id * UFR + r;
+  const float nv = v < n ? nv32[v] : 0.f;  // in flight during the bulk copies
   __syncthreads();
   mbar_wait(&full, 0);
-  const int64_t v = (int64_t)id * UFR + t;
+  UB_TRACE_MAX(step, 2);
+  UB_TRACE_BLK(step, 1);
   if (v < n) {
-    const float* row = reinterpret_cast<const float*>(stage) + (size_t)t * pitch;
+    const float* row = reinterpret_cast<const float*>(stage) + (size_t)r * pitch;
     const float4* r4 = reinterpret_cast<const float4*>(row);
-    // Gram-form fp32 pre-tests (far32_gram) for the winner and the batch, one pass
+    // Gram-form fp32 pre-tests (far32_gram) for the winner and the batch: this
+    // lane's half of the dims, then the pair's sum
     float g[RW + 1];
 #pragma unroll
     for (int j = 0; j <= RW; ++j) g[j] = 0.f;
-    for (int k4 = 0; k4 < dp / 4; ++k4) {
-      const float4 q = r4[k4];
-#pragma unroll
-      for (int j = 0; j <= RW; ++j)
-        if (j == RW || j < wc) {
-          const float4 c4 = reinterpret_cast<const float4*>(cg + j * dp)[k4];
-          g[j] = fmaf(q.x, c4.x, g[j]);
-          g[j] = fmaf(q.y, c4.y, g[j]);
-          g[j] = fmaf(q.z, c4.z, g[j]);
-          g[j] = fmaf(q.w, c4.w, g[j]);
-        }
+    const int h4 = (dp / 4 + 1) >> 1;
+    const int k4b = p ? h4 : 0, k4e = p ? dp / 4 : h4;
+    const float4* cgi = reinterpret_cast<const float4*>(cg);
+    switch (wc) {
+      case 0: gram_dots<0>(r4, cgi, k4b, k4e, g); break;
+      case 1: gram_dots<1>(r4, cgi, k4b, k4e, g); break;
+      case 2: gram_dots<2>(r4, cgi, k4b, k4e, g); break;
+      case 3: gram_dots<3>(r4, cgi, k4b, k4e, g); break;
+      case 4: gram_dots<4>(r4, cgi, k4b, k4e, g); break;
+      case 5: gram_dots<5>(r4, cgi, k4b, k4e, g); break;
+      case 6: gram_dots<6>(r4, cgi, k4b, k4e, g); break;
+      case 7: gram_dots<7>(r4, cgi, k4b, k4e, g); break;
+      default: gram_dots<RW>(r4, cgi, k4b, k4e, g); break;
     }
-    const float nv = nv32[v];
-    double m = reinterpret_cast<const double*>(stage + row_bytes)[t];
+#pragma unroll
+    for (int j = 0; j <= RW; ++j) g[j] += __shfl_xor_sync(pm, g[j], 1);
+    double m = reinterpret_cast<const double*>(stage + row_bytes)[r];
     if (!far32_gram(g[RW], nv, cn[RW], d, m)) {
-      const double dist = dist64_smem_row(row, cd, d);
+      double dist = 0.0;
+      if (p == 0) dist = dist64_smem_row(row, cd, d);
+      dist = __shfl_sync(pm, dist, lane & 30);  // the even lane's value to both
       if (dist < m) {
         m = dist;
-        cm64[v] = m;
-        pt[v] = make_pt((float)m, nv32[v], pk);
-        if (seeds.ipa) write_seeds(seeds, v, (float)m);
+        if (p == 0) {
+          cm64[v] = m;
+          pt[v] = make_pt((float)m, nv, pk);
+          if (seeds.ipa) write_seeds(seeds, v, (float)m);
+        }
       }
     }
-    terms[v] = reinterpret_cast<const double*>(stage + row_bytes + UFR * 8)[t] - m;
+    if (p == 0) terms[v] = reinterpret_cast<const double*>(stage + row_bytes + UFR * 8)[r] - m;
     // the batch's terms with the new minimum (k_refine_short's operation order),
-    // fp64 only where the pre-test cannot rule the term out
+    // fp64 only where the pre-test cannot rule the term out; candidate
+    // j = 2 i + p on this lane
     unsigned lm = 0;
 #pragma unroll
-    for (int j = 0; j < RW; ++j)
-      if (j < wc && !far32_gram(g[j], nv, cn[j], d, m)) lm |= 1u << j;
-    double sj[RW];
+    for (int i = 0; i < HW; ++i) {
+      const int j = 2 * i + p;
+      if (j < wc && !far32_gram(g[j], nv, cn[j], d, m)) lm |= 1u << i;
+    }
+    double sj[HW];
 #pragma unroll
-    for (int j = 0; j < RW; ++j) sj[j] = 0.0;
+    for (int i = 0; i < HW; ++i) sj[i] = 0.0;
     if (lm) {
       auto step_k = [&](int k, double x) {
 #pragma unroll
-        for (int j = 0; j < RW; ++j)
-          if (lm >> j & 1u) {
-            const double tt = x - cb[j * d + k];
-            sj[j] = fma(tt, tt, sj[j]);
+        for (int i = 0; i < HW; ++i)
+          if (lm >> i & 1u) {
+            const double tt = x - cb[(2 * i + p) * d + k];
+            sj[i] = fma(tt, tt, sj[i]);
           }
       };
       int k = 0;
@@ -2956,43 +3033,57 @@ __global__ void __launch_bounds__(UFR) k_update_batch(
       for (; k < d; ++k) step_k(k, (double)row[k]);
     }
 #pragma unroll
-    for (int j = 0; j < RW; ++j)
+    for (int i = 0; i < HW; ++i) {
+      const int j = 2 * i + p;
       if (j < wc) {
-        const double tt = m - sj[j];
-        ba.sb.xt[(int64_t)j * ba.sb.xstride + v] = (lm >> j & 1u) && tt > 0.0 ? tt : 0.0;
+        const double tt = m - sj[i];
+        ba.sb.xt[(int64_t)j * ba.sb.xstride + v] = (lm >> i & 1u) && tt > 0.0 ? tt : 0.0;
       }
+    }
   }
   __syncthreads();  // every row consumed: the stage is reused below
+  UB_TRACE_MAX(step, 3);
+  UB_TRACE_BLK(step, 2);
+#ifdef EBC200_TRACE
+  if (threadIdx.x == 0 && step == 10 && blockIdx.x < 8192) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_ub_blk[blockIdx.x][3] = smid;
+  }
+#endif
   const int c = id / (RCH / UFR);
   if (t == 0) {
-    __threadfence();  // the block's terms (ordered by the barrier) before the ticket
     const int in_chunk = min(RCH / UFR, nslices - c * (RCH / UFR));
-    flag = atomicAdd(ctr.chunk_ticket + c, 1u) == (unsigned int)(in_chunk - 1);
+    flag = ticket_acq_rel(ctr.chunk_ticket + c) == (unsigned int)(in_chunk - 1);
   }
   __syncthreads();
   if (!flag) return;
-  __threadfence();
-  // virtual thread u = t + q UFR: the f(S) terms of points u, u+256, u+512, u+768
-  // in order (k_update_reduce), and the batch terms likewise (k_refine_short)
-#pragma unroll
+  // virtual thread u = t + q NT: the f(S) terms of points u, u+256, u+512, u+768
+  // in order (k_update_reduce), and the batch terms likewise (k_refine_short);
+  // every load of a virtual thread is issued before its adds
+  constexpr int PPT = RCH / RED_THREADS;
+#pragma unroll 1
   for (int q = 0; q < VT; ++q) {
-    const int u = t + q * UFR;
+    const int u = t + q * NT;
+    double x[RW + 1][PPT];
+#pragma unroll
+    for (int i = 0; i < PPT; ++i) {
+      const int64_t w = (int64_t)c * RCH + u + (int64_t)i * RED_THREADS;
+      x[0][i] = w < n ? __ldcg(terms + w) : 0.0;
+#pragma unroll
+      for (int j = 0; j < RW; ++j) x[j + 1][i] = w < n && j < wc ? __ldcg(ba.sb.xt + (int64_t)j * ba.sb.xstride + w) : 0.0;
+    }
     double acc = 0.0;
 #pragma unroll
-    for (int i = 0; i < RCH / RED_THREADS; ++i) {
-      const int64_t w = (int64_t)c * RCH + u + (int64_t)i * RED_THREADS;
-      if (w < n) acc += __ldcg(terms + w);
-    }
+    for (int i = 0; i < PPT; ++i)
+      if ((int64_t)c * RCH + u + (int64_t)i * RED_THREADS < n) acc += x[0][i];
     sbuf[u] = acc;
 #pragma unroll
     for (int j = 0; j < RW; ++j) {
       double bj = 0.0;
-      if (j < wc)
 #pragma unroll
-        for (int i = 0; i < RCH / RED_THREADS; ++i) {
-          const int64_t w = (int64_t)c * RCH + u + i * RED_THREADS;
-          if (w < n) bj += __ldcg(ba.sb.xt + (int64_t)j * ba.sb.xstride + w);
-        }
+      for (int i = 0; i < PPT; ++i)
+        if (j < wc && (int64_t)c * RCH + u + (int64_t)i * RED_THREADS < n) bj += x[j + 1][i];
       red[j][u] = bj;
     }
   }
@@ -3000,10 +3091,10 @@ __global__ void __launch_bounds__(UFR) k_update_batch(
   // block_sum_256's tree over the virtual threads
 #pragma unroll
   for (int st = RED_THREADS / 2; st > 0; st >>= 1) {
-    for (int u = t; u < st; u += UFR) sbuf[u] += sbuf[u + st];
+    for (int u = t; u < st; u += NT) sbuf[u] += sbuf[u + st];
     __syncthreads();
   }
-  for (int wj = warp; wj < RW; wj += UFR / 32) {
+  for (int wj = warp; wj < RW; wj += NT / 32) {
     double x = 0.0;
 #pragma unroll
     for (int q = 0; q < RED_THREADS / 32; ++q) x += red[wj][lane * (RED_THREADS / 32) + q];
@@ -3016,46 +3107,109 @@ __global__ void __launch_bounds__(UFR) k_update_batch(
   if (t == 0) {
     ctr.chunk_ticket[c] = 0u;
     fpart[c] = bs;
-    __threadfence();
-    flag = atomicAdd(ctr.chunks_done, 1u) == (unsigned int)(nchunks - 1);
+    flag = ticket_acq_rel(ctr.chunks_done) == (unsigned int)(nchunks - 1);
   }
   __syncthreads();
   if (!flag) return;
-  __threadfence();
-  // chunk partials left to right (chunk_total_block with this block's width)
-  double fsum = 0.0;
-  for (int c0 = 0; c0 < nchunks; c0 += UFR) {
-    const int m = min(UFR, nchunks - c0);
-    if (t < m) sbuf[t] = __ldcg(fpart + c0 + t);
+  UB_TRACE_MAX(step, 4);
+  // The last block: f(S) = the chunk partials left to right (chunk_total_block)
+  // and each batch candidate's exact gain = its group partials (chunks
+  // [g cpg, (g+1) cpg) left to right) summed left to right, in the same order
+  // as the separate passes (identical bits).  Group partials of several chunks
+  // are summed in parallel first; the chunk partials are streamed through
+  // shared memory in tiles of RED_THREADS, one memory round trip per tile:
+  // thread 32 sums f(S), thread j < wc candidate j (with one chunk per group,
+  // cpg == 1, 0.0 + x == x, so the group step is a plain add).
+  double fold = 0.0;
+  if (t == 0) fold = *cur;
+  double* tb = reinterpret_cast<double*>(stage);  // (RW + 1) x RED_THREADS tile
+  double* tot_s = tb + (RW + 1) * RED_THREADS;     // wc exact gains, then f(S)
+  const int ng = ba.ng;
+  const int cpg = (nchunks + ng - 1) / ng;
+  double* grp = tb + RED_THREADS;  // cpg > 1: wc x ng group partials (ng <= 256: batch_fusable)
+  if (cpg > 1)
+    for (int i = t; i < wc * ng; i += NT) {
+      const int w = i / ng, gi = i - w * ng;
+      const int q1 = min(nchunks, (gi + 1) * cpg);
+      const double* src = ba.xch + (int64_t)w * nchunks;
+      double tot = 0.0;
+      int q = gi * cpg;
+      for (; q + 8 <= q1; q += 8) {
+        double x8[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) x8[e] = __ldcg(src + q + e);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) tot += x8[e];
+      }
+      for (; q < q1; ++q) tot += __ldcg(src + q);
+      grp[i] = tot;
+    }
+  double fsum = 0.0, gtot = 0.0;
+  for (int c0 = 0; c0 < nchunks; c0 += RED_THREADS) {
+    const int m = min(RED_THREADS, nchunks - c0);
+    const int rows_in = cpg == 1 ? wc : 0;
+#pragma unroll
+    for (int rr = 0; rr <= RW; ++rr)
+#pragma unroll
+      for (int q = 0; q < RED_THREADS / NT; ++q) {
+        const int cc = t + q * NT;
+        if (cc < m && rr <= rows_in)
+          tb[rr * RED_THREADS + cc] =
+              rr == 0 ? __ldcg(fpart + c0 + cc) : __ldcg(ba.xch + (int64_t)(rr - 1) * nchunks + c0 + cc);
+      }
     __syncthreads();
-    if (t == 0)
-      for (int i = 0; i < m; ++i) fsum += sbuf[i];
+    if (t == 32) {
+      int i = 0;
+      for (; i + 8 <= m; i += 8) {
+        double x8[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) x8[e] = tb[i + e];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) fsum += x8[e];
+      }
+      for (; i < m; ++i) fsum += tb[i];
+    }
+    if (t < rows_in) {
+      const double* row = tb + (t + 1) * RED_THREADS;
+      int i = 0;
+      for (; i + 8 <= m; i += 8) {
+        double x8[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) x8[e] = row[i + e];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) gtot += x8[e];
+      }
+      for (; i < m; ++i) gtot += row[i];
+    }
     __syncthreads();
   }
-  const double fnew = fsum * inv_n;
+  if (cpg > 1 && t < wc) {
+    const double* gp = grp + t * ng;
+    int i = 0;
+    for (; i + 8 <= ng; i += 8) {
+      double x8[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) x8[e] = gp[i + e];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) gtot += x8[e];
+    }
+    for (; i < ng; ++i) gtot += gp[i];
+  }
+  if (t < wc) tot_s[t] = gtot;
+  if (t == 32) tot_s[RW] = fsum * inv_n;
+  __syncthreads();
+  const double fnew = tot_s[RW];
   if (t == 0) {
-    const double fold = *cur;
     if (val_out) val_out[step] = fnew;
     if (gain_out) gain_out[step] = fnew - fold;
     *cur = fnew;
     *ctr.chunks_done = 0u;
   }
-  __syncthreads();
-  // the batch: group partials in the classic order, computed into shared memory
-  // (after red: the stage holds RW * RED_THREADS + (RW x ng) doubles, see the
-  // host's update_batch_smem), then its finalize (reads *cur)
-  double* grp_s = reinterpret_cast<double*>(stage) + (RW + 1) * RED_THREADS;
-  const int cpg = (nchunks + ba.ng - 1) / ba.ng;
-  for (int i = t; i < wc * ba.ng; i += UFR) {
-    const int w = i / ba.ng, grp = i - w * ba.ng;
-    double tot = 0.0;
-    const int c1 = min(nchunks, (grp + 1) * cpg);
-    for (int q = grp * cpg; q < c1; ++q) tot += __ldcg(ba.xch + (int64_t)w * nchunks + q);
-    grp_s[i] = tot;
-  }
-  __syncthreads();
-  refine_finalize_n(ba.fin, wc, ba.wlist, ba.part_r, ba.ng, &red[0][0], reinterpret_cast<long long*>(&red[2][0]),
-                    UFR, grp_s);
+  UB_TRACE_MAX(step, 5);
+  // the batch's finalize on the exact gains (one group each), f(S) from shared memory
+  refine_finalize_n(ba.fin, wc, ba.wlist, ba.part_r, 1, &red[0][0], reinterpret_cast<long long*>(&red[2][0]), NT,
+                    tot_s, tot_s + RW);
+  UB_TRACE_MAX(step, 6);
 }
 
 // ---------------------------------------------------------------- K2: multiset (work matrix)

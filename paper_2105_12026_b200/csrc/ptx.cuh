@@ -96,6 +96,16 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src)
 __device__ __forceinline__ void cp_async4(void* smem_dst, const void* gmem_src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(smem_dst)), "l"(gmem_src) : "memory");
 }
+// Grid ticket with release/acquire semantics at gpu scope (no SC fence): called
+// by one thread after a __syncthreads that orders the block's writes before it;
+// the release publishes them, and a taker that sees the last ticket acquires
+// every earlier block's (its block reads them after a __syncthreads).
+__device__ __forceinline__ unsigned int ticket_acq_rel(unsigned int* p) {
+  unsigned int old;
+  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(p) : "memory");
+  return old;
+}
+
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
