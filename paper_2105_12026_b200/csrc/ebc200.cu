@@ -1168,12 +1168,13 @@ int refine_groups(const ebc_ctx* ctx) {
 // decision (batch 2), so every rank's stale set is its share of the
 // single-device one (a rank whose own candidates are all weak would otherwise
 // re-screen them against its own low bound).
-void lazy_batch_begin(ebc_ctx* ctx, int step, int commit, int64_t* sel_dev, RefineFinal& fb) {
+void lazy_batch_begin(ebc_ctx* ctx, int step, int commit, int64_t* sel_dev, RefineFinal& fb,
+                      const PackArgs& pa = PackArgs()) {
   const int64_t ncand = ctx->c1 - ctx->c0;
   const int ag = (int)std::max<int64_t>(1, std::min<int64_t>(2 * ctx->num_sms, (ncand + 1023) / 1024));
   k_lazy_topk<<<ag, 256, 0, ctx->stream>>>(ctx->c0, ctx->c1, ctx->ubp, ctx->selected, ctx->lazy_batch,
                                           (unsigned long long*)ctx->lazy_part, ctx->counter2, ctx->wcount, ctx->wlist,
-                                          ctx->ub_next);
+                                          ctx->ub_next, pa, ctx->best, step);
   ++ctx->launches;
   const bool global_lb = ctx->in_sharded_run && ctx->comm && (ctx->nranks > 1 || ctx->force_global_lb);
   fb = step_final(ctx, commit, step, sel_dev);
@@ -1460,10 +1461,19 @@ bool batch_fusable(const ebc_ctx* ctx) {
 // decision are those of k_refine_short after k_update_fused, bit for bit.
 int run_update_batch(ebc_ctx* ctx, int step, double* val_dev, double* gain_dev, int64_t* sel_dev) {
   const int eb = 4 * step;
-  RefineFinal fb;
-  lazy_batch_begin(ctx, step + 1, 1, sel_dev, fb);
-  int rc = ensure(ctx, ctx->rterms, (size_t)RW * ctx->nchunks * sizeof(double));
+  const size_t pbytes = BatchPackLayout(ctx->d).bytes();
+  int rc = ensure(ctx, ctx->ubpack, pbytes);
   if (rc) return rc;
+  // the batch's top-k also packs the rows k_update_batch stages (winner + batch)
+  PackArgs pa;
+  pa.V = ctx->V32;
+  pa.pitch = ctx->pitch;
+  pa.d = ctx->d;
+  pa.nv32 = ctx->nv32;
+  pa.pack = (unsigned char*)ctx->ubpack.p;
+  RefineFinal fb;
+  lazy_batch_begin(ctx, step + 1, 1, sel_dev, fb, pa);
+  if ((rc = ensure(ctx, ctx->rterms, (size_t)RW * ctx->nchunks * sizeof(double)))) return rc;
   const size_t xbytes = (size_t)RW * ctx->n_pad * sizeof(double);
   const size_t sbytes = xbytes + (size_t)ctx->nchunks * sizeof(unsigned int);
   const bool fresh = ctx->sxt.bytes < sbytes;
@@ -1480,13 +1490,6 @@ int run_update_batch(ebc_ctx* ctx, int step, double* val_dev, double* gain_dev, 
   ba.fin = fb;
   const int rows = ctx->ub_rows;  // two threads per row: 128 or 256 threads
   const size_t dsm = update_batch_smem(ctx, rows);
-  const size_t pbytes = BatchPackLayout(ctx->d).bytes();
-  const bool pfresh = ctx->ubpack.bytes < pbytes;
-  if ((rc = ensure(ctx, ctx->ubpack, pbytes))) return rc;
-  (void)pfresh;
-  k_batch_pack<<<RW + 1, 128, 0, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->d, ctx->nv32, ctx->best, ctx->wcount,
-                                               ctx->wlist, (unsigned char*)ctx->ubpack.p);
-  KCHECK();
   UpdateCounters uc{ctx->uf_ctr + 1, ctx->uf_ctr};
   const unsigned grid = (unsigned)((ctx->n + rows - 1) / rows);
   auto go = [&](auto kern) -> int {
@@ -2385,6 +2388,8 @@ int ebc_debug_ub_trace(unsigned long long* out, int reset) {
   if (cudaDeviceSynchronize() != cudaSuccess) return EBC_ECUDA;
   if (out && cudaMemcpyFromSymbol(out, g_ub_trace, sizeof(g_ub_trace)) != cudaSuccess) return EBC_ECUDA;
   if (out && cudaMemcpyFromSymbol(out + 64 * 8, g_ub_blk, sizeof(g_ub_blk)) != cudaSuccess) return EBC_ECUDA;
+  if (out && cudaMemcpyFromSymbol(out + 64 * 8 + 8192 * 4, g_tk_trace, sizeof(g_tk_trace)) != cudaSuccess)
+    return EBC_ECUDA;
   if (reset) {
     static unsigned long long init[64][8];
     for (auto& r : init) {
@@ -2392,6 +2397,12 @@ int ebc_debug_ub_trace(unsigned long long* out, int reset) {
       r[0] = ~0ull;
     }
     if (cudaMemcpyToSymbol(g_ub_trace, init, sizeof(init)) != cudaSuccess) return EBC_ECUDA;
+    static unsigned long long tinit[64][4];
+    for (auto& r : tinit) {
+      for (auto& x : r) x = 0ull;
+      r[0] = ~0ull;
+    }
+    if (cudaMemcpyToSymbol(g_tk_trace, tinit, sizeof(tinit)) != cudaSuccess) return EBC_ECUDA;
   }
   return EBC_OK;
 }

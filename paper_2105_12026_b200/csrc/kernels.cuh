@@ -1082,12 +1082,12 @@ __device__ __forceinline__ void warp_topk(unsigned long long (&l)[TK], unsigned 
   const int lane = threadIdx.x & 31;
 #pragma unroll 1
   for (int r = 0; r < TK; ++r) {
-    unsigned long long b = l[0];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const unsigned long long x = __shfl_xor_sync(0xffffffffu, b, o);
-      b = x > b ? x : b;
-    }
+    // the 64-bit max as two 32-bit warp reductions (high word, then the low
+    // word among the lanes holding it)
+    const unsigned hi = (unsigned)(l[0] >> 32), lo = (unsigned)l[0];
+    const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+    const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+    const unsigned long long b = ((unsigned long long)mh << 32) | ml;
     if (lane == 0) out[r] = b;
     if (b != 0ull && l[0] == b) {
 #pragma unroll
@@ -1097,37 +1097,140 @@ __device__ __forceinline__ void warp_topk(unsigned long long (&l)[TK], unsigned 
   }
 }
 
+#ifdef EBC200_TRACE
+// Development trace (tools/ub_trace.py, -DEBC200_TRACE builds only): per step,
+// globaltimer stamps of the fused update's phases, min/max over blocks.
+__device__ unsigned long long g_ub_trace[64][8];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ unsigned long long g_ub_blk[8192][4];
+__device__ unsigned long long g_tk_trace[64][4];  // k_lazy_topk: start (min), scan done (max), last block, end
+#define TK_TRACE_MIN(step, i) \
+  if (threadIdx.x == 0 && step >= 0 && step < 64) atomicMin(&g_tk_trace[step][i], gtimer())
+#define TK_TRACE_MAX(step, i) \
+  if (threadIdx.x == 0 && step >= 0 && step < 64) atomicMax(&g_tk_trace[step][i], gtimer())  // one step's per-block stamps (step == 10)
+#define UB_TRACE_BLK(step, i) \
+  if (threadIdx.x == 0 && step == 10 && blockIdx.x < 8192) g_ub_blk[blockIdx.x][i] = gtimer()
+#define UB_TRACE_MIN(step, i) \
+  if (threadIdx.x == 0 && step < 64) atomicMin(&g_ub_trace[step][i], gtimer())
+#define UB_TRACE_MAX(step, i) \
+  if (threadIdx.x == 0 && step < 64) atomicMax(&g_ub_trace[step][i], gtimer())
+#else
+#define TK_TRACE_MIN(step, i)
+#define TK_TRACE_MAX(step, i)
+#define UB_TRACE_BLK(step, i)
+#define UB_TRACE_MIN(step, i)
+#define UB_TRACE_MAX(step, i)
+#endif
+
+// The rows k_update_batch keeps in shared memory, packed once per step in its
+// smem layout (one bulk copy per block instead of every block walking the
+// winner's and the batch's rows): [cd: the winner's row, fp64][cb: RW batch
+// rows, fp64][cg: RW batch rows + the winner's, fp32, interleaved by 4 dims:
+// float4 (k4, j) at k4 (RW + 1) + j][cn: their fp32 norms].  One block per
+// row (RW + 1 blocks).
+struct BatchPackLayout {
+  size_t dbytes, cbytes, fbytes;
+  __host__ __device__ BatchPackLayout(int d) {
+    const size_t dp = (size_t)((d + 3) & ~3);
+    dbytes = ((size_t)d * 8 + 15) & ~(size_t)15;
+    cbytes = ((size_t)RW * d * 8 + 15) & ~(size_t)15;
+    fbytes = (((size_t)(RW + 1) * dp + RW + 1) * 4 + 15) & ~(size_t)15;
+  }
+  __host__ __device__ size_t bytes() const { return dbytes + cbytes + fbytes; }
+};
+// The pack's rows: j < RW the batch (src[j] < 0: empty), j == RW the winner.
+// Called by every thread of a block (strided over the (RW + 1) x dp floats).
+struct PackArgs {
+  const float* V = nullptr;
+  int pitch = 0, d = 0;
+  const float* nv32 = nullptr;
+  unsigned char* pack = nullptr;  // nullptr: no pack
+};
+__device__ void batch_pack_rows(const PackArgs& a, const int64_t* src) {
+  const BatchPackLayout L(a.d);
+  const int d = a.d, dp = (d + 3) & ~3;
+  double* cd = reinterpret_cast<double*>(a.pack);
+  double* cb = reinterpret_cast<double*>(a.pack + L.dbytes);
+  float* cg = reinterpret_cast<float*>(a.pack + L.dbytes + L.cbytes);
+  float* cn = cg + (size_t)(RW + 1) * dp;
+  const float nvj = (int)threadIdx.x <= RW && src[threadIdx.x] >= 0 ? a.nv32[src[threadIdx.x]] : 0.f;
+  for (int i0 = 0; i0 < (RW + 1) * dp; i0 += 4 * (int)blockDim.x) {
+    float x[4];  // four elements' loads in flight before their stores
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int i = i0 + e * blockDim.x + threadIdx.x;
+      const int j = i / dp, k = i - j * dp;
+      x[e] = i < (RW + 1) * dp && src[j] >= 0 && k < d ? a.V[src[j] * a.pitch + k] : 0.f;
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int i = i0 + e * blockDim.x + threadIdx.x;
+      if (i >= (RW + 1) * dp) break;
+      const int j = i / dp, k = i - j * dp;
+      cg[((k >> 2) * (RW + 1) + j) * 4 + (k & 3)] = x[e];  // interleaved by 4 dims: [dp / 4][RW + 1] float4
+      if (k < d) {
+        if (j == RW)
+          cd[k] = (double)x[e];
+        else
+          cb[j * d + k] = (double)x[e];
+      }
+    }
+  }
+  if ((int)threadIdx.x <= RW) cn[threadIdx.x] = nvj;
+}
+
 // Writes the batch to wlist[0..m) (m = min(lb, unselected candidates)),
 // *wcount = m and *ub_next = the (rounded-up) best bound outside it (-inf if none).
 __global__ void __launch_bounds__(256) k_lazy_topk(int64_t c0, int64_t c1, const double* __restrict__ ubp,
                                                    const unsigned char* __restrict__ selected, int lb,
                                                    unsigned long long* __restrict__ part,
                                                    unsigned int* __restrict__ counter, int* __restrict__ wcount,
-                                                   int64_t* __restrict__ wlist, double* __restrict__ ub_next) {
+                                                   int64_t* __restrict__ wlist, double* __restrict__ ub_next,
+                                                   PackArgs pa, const int64_t* __restrict__ best, int step) {
   __shared__ unsigned long long wt[9 * TK];  // 8 warp lists + the merged one
+  __shared__ int64_t ssrc[RW + 1];           // the pack's rows (pa.pack)
   __shared__ bool last;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  TK_TRACE_MIN(step, 0);
   unsigned long long l[TK];
 #pragma unroll
   for (int j = 0; j < TK; ++j) l[j] = 0ull;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < c1; c += stride)
+  // four candidates' loads in flight per thread before their inserts
+  int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; c + 3 * stride < c1; c += 4 * stride) {
+    double u[4];
+    unsigned char sl[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      u[e] = ubp[c + e * stride - c0];
+      sl[e] = selected[c + e * stride];
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (!sl[e]) top_insert(l, top_key(u[e], c + e * stride - c0));
+  }
+  for (; c < c1; c += stride)
     if (!selected[c]) top_insert(l, top_key(ubp[c - c0], c - c0));
   warp_topk(l, wt + warp * TK);
   __syncthreads();
+  TK_TRACE_MAX(step, 1);
   if (warp == 0) {
 #pragma unroll
     for (int j = 0; j < TK; ++j) l[j] = 0ull;
     for (int q = lane; q < 8 * TK; q += 32) top_insert(l, wt[q]);
     warp_topk(l, part + (int64_t)blockIdx.x * TK);
-    if (lane == 0) {
-      __threadfence();
-      last = atomicAdd(counter, 1u) == gridDim.x - 1;
-    }
+    __syncwarp();
+    if (lane == 0) last = ticket_acq_rel(counter) == gridDim.x - 1;
   }
   __syncthreads();
   if (!last) return;
-  __threadfence();
+  TK_TRACE_MAX(step, 2);
+  const int64_t wsrc = pa.pack && threadIdx.x == 0 ? *best : -1;  // in flight during the merges
 #pragma unroll
   for (int j = 0; j < TK; ++j) l[j] = 0ull;
   const int total = (int)gridDim.x * TK;
@@ -1143,21 +1246,34 @@ __global__ void __launch_bounds__(256) k_lazy_topk(int64_t c0, int64_t c1, const
   for (int q = threadIdx.x + PT * blockDim.x; q < total; q += blockDim.x) top_insert(l, __ldcg(part + q));
   warp_topk(l, wt + warp * TK);
   __syncthreads();
-  if (warp != 0) return;
+  if (warp == 0) {
 #pragma unroll
-  for (int j = 0; j < TK; ++j) l[j] = 0ull;
-  for (int q = lane; q < 8 * TK; q += 32) top_insert(l, wt[q]);
-  warp_topk(l, wt + 8 * TK);
-  __syncwarp();
-  if (lane == 0) {
-    const unsigned long long* fin = wt + 8 * TK;
-    int m = 0;
-    for (int j = 0; j < lb; ++j)
-      if (fin[j]) wlist[m++] = c0 + (int64_t)(0xFFFFFFFFu - (unsigned)(fin[j] & 0xFFFFFFFFull));
-    *wcount = m;
-    *ub_next = fin[lb] ? (double)__uint_as_float((unsigned)(fin[lb] >> 32)) : -INFINITY;
-    *counter = 0u;
+    for (int j = 0; j < TK; ++j) l[j] = 0ull;
+    for (int q = lane; q < 8 * TK; q += 32) top_insert(l, wt[q]);
+    warp_topk(l, wt + 8 * TK);
+    __syncwarp();
+    if (lane == 0) {
+      const unsigned long long* fin = wt + 8 * TK;
+      int m = 0;
+      for (int j = 0; j < lb; ++j)
+        if (fin[j]) {
+          const int64_t c = c0 + (int64_t)(0xFFFFFFFFu - (unsigned)(fin[j] & 0xFFFFFFFFull));
+          ssrc[m] = c;
+          wlist[m++] = c;
+        }
+      for (int j = m; j < RW; ++j) ssrc[j] = -1;
+      ssrc[RW] = wsrc;
+      *wcount = m;
+      *ub_next = fin[lb] ? (double)__uint_as_float((unsigned)(fin[lb] >> 32)) : -INFINITY;
+      *counter = 0u;
+    }
   }
+  if (!pa.pack) return;
+  // the next update's pack (k_update_batch): the winner's row and the batch's
+  __syncthreads();
+  batch_pack_rows(pa, ssrc);
+  __syncthreads();
+  TK_TRACE_MAX(step, 3);
 }
 
 // Device-sharded lazy step: the decision of the batch refine's finalize, made
@@ -2814,69 +2930,6 @@ struct BatchArgs {
   ShortBufs sb;              // xt terms (the per-chunk tickets are the update's)
   RefineFinal fin;
 };
-// The rows k_update_batch keeps in shared memory, packed once per step in its
-// smem layout (one bulk copy per block instead of every block walking the
-// winner's and the batch's rows): [cd: the winner's row, fp64][cb: RW batch
-// rows, fp64][cg: RW batch rows + the winner's, fp32, interleaved by 4 dims:
-// float4 (k4, j) at k4 (RW + 1) + j][cn: their fp32 norms].  One block per
-// row (RW + 1 blocks).
-struct BatchPackLayout {
-  size_t dbytes, cbytes, fbytes;
-  __host__ __device__ BatchPackLayout(int d) {
-    const size_t dp = (size_t)((d + 3) & ~3);
-    dbytes = ((size_t)d * 8 + 15) & ~(size_t)15;
-    cbytes = ((size_t)RW * d * 8 + 15) & ~(size_t)15;
-    fbytes = (((size_t)(RW + 1) * dp + RW + 1) * 4 + 15) & ~(size_t)15;
-  }
-  __host__ __device__ size_t bytes() const { return dbytes + cbytes + fbytes; }
-};
-__global__ void k_batch_pack(const float* __restrict__ V, int pitch, int d, const float* __restrict__ nv32,
-                             const int64_t* __restrict__ best, const int* __restrict__ wcount,
-                             const int64_t* __restrict__ wlist, unsigned char* __restrict__ pack) {
-  const BatchPackLayout L(d);
-  const int dp = (d + 3) & ~3;
-  double* cd = reinterpret_cast<double*>(pack);
-  double* cb = reinterpret_cast<double*>(pack + L.dbytes);
-  float* cg = reinterpret_cast<float*>(pack + L.dbytes + L.cbytes);
-  float* cn = cg + (size_t)(RW + 1) * dp;
-  const int j = blockIdx.x;  // 0..RW-1 batch rows, RW the winner
-  const int wc = min(RW, *wcount);
-  const bool on = j == RW ? *best >= 0 : j < wc;
-  const int64_t src = on ? (j == RW ? *best : wlist[j]) : 0;
-  for (int k = threadIdx.x; k < dp; k += blockDim.x) {
-    const float x = on && k < d ? V[src * pitch + k] : 0.f;
-    cg[((k >> 2) * (RW + 1) + j) * 4 + (k & 3)] = x;  // interleaved by 4 dims: [dp / 4][RW + 1] float4
-    if (k < d) {
-      if (j == RW)
-        cd[k] = (double)x;
-      else
-        cb[j * d + k] = (double)x;
-    }
-  }
-  if (threadIdx.x == 0) cn[j] = on ? nv32[src] : 0.f;
-}
-
-#ifdef EBC200_TRACE
-// Development trace (tools/ub_trace.py, -DEBC200_TRACE builds only): per step,
-// globaltimer stamps of the fused update's phases, min/max over blocks.
-__device__ unsigned long long g_ub_trace[64][8];
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-__device__ unsigned long long g_ub_blk[8192][4];  // one step's per-block stamps (step == 10)
-#define UB_TRACE_BLK(step, i) \
-  if (threadIdx.x == 0 && step == 10 && blockIdx.x < 8192) g_ub_blk[blockIdx.x][i] = gtimer()
-#define UB_TRACE_MIN(step, i) \
-  if (threadIdx.x == 0 && step < 64) atomicMin(&g_ub_trace[step][i], gtimer())
-#define UB_TRACE_MAX(step, i) \
-  if (threadIdx.x == 0 && step < 64) atomicMax(&g_ub_trace[step][i], gtimer())
-#else
-#define UB_TRACE_BLK(step, i)
-#define UB_TRACE_MIN(step, i)
-#define UB_TRACE_MAX(step, i)
-#endif
 
 // fp32 Gram dots of one row (this lane's float4 range [k4b, k4e)) with the
 // first NB batch rows and the winner (g[RW]) of the interleaved pack: packed

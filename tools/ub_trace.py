@@ -17,14 +17,15 @@ f = eb.EbcFunction(eb.GroundMatrix(X, eb.Precision.FP32))
 lib = _native.load()
 fn = lib.ebc_debug_ub_trace
 fn.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
-buf = (ctypes.c_ulonglong * (64 * 8 + 8192 * 4))()
+buf = (ctypes.c_ulonglong * (64 * 8 + 8192 * 4 + 64 * 4))()
 for rep in range(3):
     fn(None, 1)
     eb.greedy_maximize(f, eb.OptimizerBudget(k=k))
     fn(buf, 0)
 allb = np.frombuffer(buf, dtype=np.uint64).astype(np.int64)
 a = allb[:512].reshape(64, 8)
-blk = allb[512:].reshape(8192, 4)
+blk = allb[512:512 + 8192 * 4].reshape(8192, 4)
+tk = allb[512 + 8192 * 4:].reshape(64, 4)
 nb = int(np.count_nonzero(blk[:, 0]))
 if nb:
     b = blk[:nb].copy()
@@ -49,3 +50,19 @@ for st in range(64):
         print(st, " ".join(f"{x:7.2f}" for x in rel))
 r = np.median(np.array(rows), axis=0)
 print("median us from first block start:", dict(zip(names, np.round(r, 2))))
+
+tr = []
+for st in range(64):
+    if 0 < tk[st, 0] < 2**62 and tk[st, 3] > 0:
+        tr.append((tk[st, 1:4] - tk[st, 0]) / 1e3)
+        # gap from the topk end to the update's first block (step st is the update's step + 1)
+if tr:
+    print("k_lazy_topk median us from its first block:", dict(zip(["scan done", "last block", "end (pack done)"],
+                                                               np.round(np.median(np.array(tr), axis=0), 2))))
+    gaps = [(a[st - 1, 0] - tk[st, 3]) / 1e3 for st in range(1, 64)
+            if 0 < tk[st, 0] < 2**62 and tk[st, 3] > 0 and 0 < a[st - 1, 0] < 2**62]
+    gaps2 = [(tk[st + 1, 0] - a[st, 6]) / 1e3 for st in range(0, 63)
+             if 0 < tk[st + 1, 0] < 2**62 and a[st, 6] > 0]
+    if gaps:
+        print("median gap topk end -> update start (us):", round(float(np.median(gaps)), 2),
+              " update end -> next topk start (us):", round(float(np.median(gaps2)), 2) if gaps2 else None)
