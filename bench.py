@@ -356,8 +356,11 @@ def screen_roofline(info, rung, d, work_pairs, screen_ms, step_ms, E, config):
 def update_roofline(n_pts, d, k, update_ms):
     """Second ceiling named by the north star: the cached-min update (K4) is
     HBM-bound; algorithmic bytes per step = N (4 pitch + 8 cm + 8 e0d + 8 term)
-    (the seed refresh of changed points not counted), against the measured HBM
-    copy bandwidth; its time is the update family per step (CUDA events)."""
+    (the seed refresh of changed points and the fused batch's term traffic not
+    counted), against the measured HBM copy bandwidth; its time is the update
+    family per step (CUDA events): on lazy runs k_update_batch alone (the
+    cached-min update fused with the next step's first batch refine; the
+    batch's top-k is timed with the selection)."""
     peaks = load_measured_peaks()
     hbm = (peaks or {}).get("hbm_gbs")
     per_step_ms = update_ms / k
@@ -366,7 +369,8 @@ def update_roofline(n_pts, d, k, update_ms):
         pitch += 4
     ubytes = n_pts * (4.0 * pitch + 24.0)
     ach = ubytes / (per_step_ms * 1e-3) / 1e9
-    return {"bound": "hbm", "kernel": "k_update_fused (cached-min update + fixed-order f(S), one launch)",
+    return {"bound": "hbm", "kernel": "k_update_batch (cached-min update + fixed-order f(S) + the next step's first "
+                                      "batch refine, one launch; k_update_fused on non-lazy steps)",
             "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": (ach / hbm) if hbm else None,
             "bytes_per_step": ubytes, "us_per_step": per_step_ms * 1e3,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs" if hbm else None,

@@ -315,6 +315,8 @@ struct ebc_ctx {
   int64_t probe_min_n = 32768;     // EBC200_PROBE_MIN_N: candidates below which undecided steps skip probe / near bound
   int batch_ready_step = -1;       // enqueue-time: that step's first batch was launched with the last update
   cudaGraphConditionalHandle batch_hrest = 0;
+  std::vector<char> fused_step;    // timing: step s's update was k_update_batch (ev[4 s + 2] after its top-k)
+  bool pdl = true;                  // EBC200_PDL: k_update_batch as a programmatic dependent of k_lazy_topk
   int ub_rows = 128;               // EBC200_UB_ROWS: rows per k_update_batch slice (64 or 128; two threads per row)
   ProbeBuf probe;                  // k_lazy_rings: ring winners, ticket, the probe list
   bool nb_on = false;              // EBC200_LAZY_NEARBOUND=0: no near-centre bound (k_lazy_nearbound)
@@ -1473,6 +1475,9 @@ int run_update_batch(ebc_ctx* ctx, int step, double* val_dev, double* gain_dev, 
   pa.pack = (unsigned char*)ctx->ubpack.p;
   RefineFinal fb;
   lazy_batch_begin(ctx, step + 1, 1, sel_dev, fb, pa);
+  // the top-k picks the next step's batch: timed with the selection family,
+  // so the update family is k_update_batch alone (re-recorded event)
+  if (ctx->timing) CU(record_step_event(ctx, ctx->ev[eb + 2]));
   if ((rc = ensure(ctx, ctx->rterms, (size_t)RW * ctx->nchunks * sizeof(double)))) return rc;
   const size_t xbytes = (size_t)RW * ctx->n_pad * sizeof(double);
   const size_t sbytes = xbytes + (size_t)ctx->nchunks * sizeof(unsigned int);
@@ -1494,10 +1499,21 @@ int run_update_batch(ebc_ctx* ctx, int step, double* val_dev, double* gain_dev, 
   const unsigned grid = (unsigned)((ctx->n + rows - 1) / rows);
   auto go = [&](auto kern) -> int {
     CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
-    kern<<<grid, 2 * rows, dsm, ctx->stream>>>(ctx->V32, ctx->pitch, ctx->n, ctx->d, ctx->best, ctx->pk, ctx->e0d,
-                                           ctx->nv32, ctx->cm64, ctx->pt, tc_seeds(ctx), ctx->terms,
-                                           ctx->chunkpart, uc, 1.0 / (double)ctx->n, ctx->cur, val_dev, gain_dev,
-                                           step, ba, (const unsigned char*)ctx->ubpack.p);
+    // a programmatic dependent of the top-k just launched (EBC200_PDL=0: plain launch)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(2 * rows);
+    cfg.dynamicSmemBytes = dsm;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = ctx->pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CU(cudaLaunchKernelEx(&cfg, kern, (const float*)ctx->V32, ctx->pitch, (int64_t)ctx->n, ctx->d,
+                          (const int64_t*)ctx->best, ctx->pk, (const double*)ctx->e0d, (const float*)ctx->nv32,
+                          ctx->cm64, ctx->pt, tc_seeds(ctx), ctx->terms, ctx->chunkpart, uc, 1.0 / (double)ctx->n,
+                          ctx->cur, val_dev, gain_dev, step, ba, (const unsigned char*)ctx->ubpack.p));
     return EBC_OK;
   };
   rc = rows == 64 ? go(k_update_batch<64>) : go(k_update_batch<128>);
@@ -1570,12 +1586,14 @@ int enqueue_greedy_sharded(ebc_ctx* ctx, int k) {
 int enqueue_greedy(ebc_ctx* ctx, int k) {
   int rc = do_reset(ctx);
   if (rc) return rc;
+  ctx->fused_step.assign((size_t)k, 0);
   for (int s = 0; s < k; ++s) {
     rc = run_step_select(ctx, s, 1, (int64_t*)ctx->sel_out.p);
     if (rc) return rc;
-    if (s + 1 < k && ctx->ubp_seeded && batch_fusable(ctx))
+    if (s + 1 < k && ctx->ubp_seeded && batch_fusable(ctx)) {
+      ctx->fused_step[s] = 1;
       rc = run_update_batch(ctx, s, (double*)ctx->val_out.p, (double*)ctx->gain_out.p, (int64_t*)ctx->sel_out.p);
-    else
+    } else
       rc = run_update(ctx, s, (double*)ctx->val_out.p, (double*)ctx->gain_out.p);
     if (rc) return rc;
   }
@@ -2096,6 +2114,9 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
       const int r = atoi(ur);
       ctx->ub_rows = r == 64 ? 64 : 128;
     }
+    if (const char* pe = getenv("EBC200_PDL")) {
+      ctx->pdl = atoi(pe) != 0;
+    }
   }
   {
     const char* lb = getenv("EBC200_LAZY_BATCH");
@@ -2594,9 +2615,12 @@ int greedy_run(ebc_ctx* ctx, int32_t k, bool sharded, int64_t* out_sel, double* 
     for (int st = 0; st < k; ++st) {
       float a = 0, b = 0, c = 0;
       if (ctx->lazy_on && st > 0) {
-        // lazy step: selection (batch, and the screen when re-run) + update
-        CU(cudaEventElapsedTime(&a, ctx->ev[4 * (st - 1) + 3], ctx->ev[4 * st + 1]));
-        CU(cudaEventElapsedTime(&c, ctx->ev[4 * st + 1], ctx->ev[4 * st + 3]));
+        // lazy step: selection (batch, and the screen when re-run) + update;
+        // a fused update (k_update_batch) is timed from after the next
+        // batch's top-k (selection work)
+        const bool fz = (size_t)st < ctx->fused_step.size() && ctx->fused_step[st];
+        CU(cudaEventElapsedTime(&a, ctx->ev[4 * (st - 1) + 3], ctx->ev[4 * st + (fz ? 2 : 1)]));
+        CU(cudaEventElapsedTime(&c, ctx->ev[4 * st + (fz ? 2 : 1)], ctx->ev[4 * st + 3]));
         acc_ms[0] += a;
         acc_ms[2] += c;
         continue;

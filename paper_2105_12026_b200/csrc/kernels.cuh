@@ -1196,6 +1196,7 @@ __global__ void __launch_bounds__(256) k_lazy_topk(int64_t c0, int64_t c1, const
   __shared__ bool last;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   TK_TRACE_MIN(step, 0);
+  pdl_launch_dependents();  // k_update_batch stages its rows while the top-k runs
   unsigned long long l[TK];
 #pragma unroll
   for (int j = 0; j < TK; ++j) l[j] = 0ull;
@@ -2989,7 +2990,6 @@ __global__ void __launch_bounds__(2 * UFR, UFR == 64 ? 5 : 3) k_update_batch(
   const int id = blockIdx.x;
   const int nslices = gridDim.x;
   const int nchunks = (int)((n + RCH - 1) / RCH);
-  const int wc = min(RW, *ba.wcount);
   const uint32_t row_bytes = (uint32_t)UFR * pitch * 4;
   const int dp = (d + 3) & ~3;
   const BatchPackLayout L(d);
@@ -3000,17 +3000,22 @@ __global__ void __launch_bounds__(2 * UFR, UFR == 64 ? 5 : 3) k_update_batch(
   unsigned char* stage = uf_smem + L.bytes();
   double (*red)[RED_THREADS] = reinterpret_cast<double (*)[RED_THREADS]>(stage);  // after the rows
   double* sbuf = reinterpret_cast<double*>(stage) + RW * RED_THREADS;
+  // launched as a programmatic dependent of k_lazy_topk (PDL): the rows, cm
+  // and e0d do not depend on it and are staged while it runs; the pack and the
+  // batch count are its output (after pdl_wait)
   if (t == 0) {
     mbar_init(&full, 1);
     fence_mbar_init();
     mbar_arrive_expect_tx(&full, row_bytes + 2 * UFR * 8 + (uint32_t)L.bytes());
-    bulk_g2s(uf_smem, pack, (uint32_t)L.bytes(), &full);
     bulk_g2s(stage, V + (int64_t)id * UFR * pitch, row_bytes, &full);
     bulk_g2s(stage + row_bytes, cm64 + (int64_t)id * UFR, UFR * 8, &full);
     bulk_g2s(stage + row_bytes + UFR * 8, e0d + (int64_t)id * UFR, UFR * 8, &full);
   }
   const int64_t v = (int64_t)id * UFR + r;
   const float nv = v < n ? nv32[v] : 0.f;  // in flight during the bulk copies
+  pdl_wait();
+  if (t == 0) bulk_g2s(uf_smem, pack, (uint32_t)L.bytes(), &full);
+  const int wc = min(RW, *ba.wcount);
   __syncthreads();
   mbar_wait(&full, 0);
   UB_TRACE_MAX(step, 2);

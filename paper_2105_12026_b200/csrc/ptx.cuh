@@ -106,6 +106,12 @@ __device__ __forceinline__ unsigned int ticket_acq_rel(unsigned int* p) {
   return old;
 }
 
+// Programmatic dependent launch: the dependent grid may start early
+// (launch_dependents, called by the prerequisite grid), and waits for the
+// prerequisite grid's completion and memory (wait) before reading its results.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
