@@ -1990,6 +1990,88 @@ __device__ void refine_finalize_n(const RefineFinal& F, int wc, const int64_t* _
   }
 }
 
+// refine_finalize_n for a window of at most 32 candidates whose exact gains
+// are in shared memory (gs[w]) and f(S) at *fsm: the same decisions and
+// writes, on ONE warp (shuffle reductions, no block barriers).  Called by
+// every lane of one warp.
+__device__ void refine_finalize_warp(const RefineFinal& F, int wc, const int64_t* __restrict__ wlist,
+                                     const double* gs, const double* fsm) {
+  const int lane = threadIdx.x & 31;
+  long long st[8] = {0, 0, 0, 0, 0, 0, 0, 0}, lvl1 = -1, mlb = 0;
+  double ubn = 0.0;
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) st[i] = F.stats[i];
+    if (F.level) lvl1 = F.level[1];
+    if (F.batch == 1) ubn = *F.ub_next;
+    if (F.batch == 3) mlb = *F.maxlb;
+  }
+  const double f = *fsm;
+  const bool on = lane < wc;
+  const double g = on ? gs[lane] : 0.0;
+  const int64_t c = on ? wlist[lane] : 0;
+  if (on) {
+    F.wgain[lane] = g;
+    if (F.ubp) F.ubp[c - F.c0] = g;  // the exact gain bounds every later one (submodularity)
+  }
+  double top = on ? __dadd_rn(f, __dmul_rn(g, F.inv_n)) : -INFINITY;  // no FMA contraction: host pick() matches
+  double gmax = on ? fmax(0.0, g) : 0.0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    top = fmax(top, __shfl_xor_sync(0xffffffffu, top, o));
+    gmax = fmax(gmax, __shfl_xor_sync(0xffffffffu, gmax, o));
+  }
+  if (F.batch == 3) {  // probe batch (k_lazy_rings): raises lb, decides nothing
+    if (lane == 0 && wc > 0) {
+      const long long k = dkey(gmax);
+      if (k > mlb) *F.maxlb = k;
+      F.stats[6] = st[6] + wc;
+    }
+    return;
+  }
+  if (F.batch == 2) {  // sharded: the decision waits for the global bound (k_lazy_decide)
+    if (lane == 0) {
+      *F.maxlb = dkey(gmax);
+      F.stats[7] = st[7] + 1;
+      F.stats[6] = st[6] + wc;
+      F.level[0] = -3;
+      *F.scount = 0;
+    }
+    return;
+  }
+  if (F.batch) {
+    int done = 0;
+    if (lane == 0) {
+      const double lb = gmax;
+      done = ubn < lb - F.margin - 1e-9 * fabs(lb);
+      *F.maxlb = dkey(lb);
+      F.stats[7] = st[7] + 1;
+      F.stats[5] = st[5] + done;
+      F.stats[6] = st[6] + wc;
+      F.level[0] = done ? -2 : -3;
+      *F.scount = 0;
+      if (F.hrest) cudaGraphSetConditional(F.hrest, done ? 0u : 1u);
+    }
+    if (!__shfl_sync(0xffffffffu, done, 0)) return;
+  }
+  const double window = 1e-12 * fmax(1.0, fabs(top));
+  long long bi = on && __dadd_rn(f, __dmul_rn(g, F.inv_n)) >= top - window ? (long long)c : LLONG_MAX;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) bi = min(bi, (long long)__shfl_xor_sync(0xffffffffu, bi, o));
+  if (lane == 0) {
+    const long long b = bi == LLONG_MAX ? -1 : bi;
+    *F.best = b;
+    F.stats[0] = st[0] + wc;
+    F.stats[1] = max(st[1], (long long)wc);
+    F.stats[2] = lvl1;
+    F.stats[3] = st[3] + 1;
+    if (F.commit && b >= 0) {
+      F.selected[b] = 1;
+      F.sel_out[F.step] = b;
+    }
+  }
+}
+
 __device__ __forceinline__ void refine_finalize(const RefineFinal& F, int wc, const int64_t* __restrict__ wlist,
                                                 const double* __restrict__ part_r, int ng, double* sred,
                                                 long long* sidx) {
@@ -3264,9 +3346,8 @@ __global__ void __launch_bounds__(2 * UFR, UFR == 64 ? 5 : 3) k_update_batch(
     *ctr.chunks_done = 0u;
   }
   UB_TRACE_MAX(step, 5);
-  // the batch's finalize on the exact gains (one group each), f(S) from shared memory
-  refine_finalize_n(ba.fin, wc, ba.wlist, ba.part_r, 1, &red[0][0], reinterpret_cast<long long*>(&red[2][0]), NT,
-                    tot_s, tot_s + RW);
+  // the batch's finalize on the exact gains, f(S) from shared memory, on warp 0
+  if (warp == 0) refine_finalize_warp(ba.fin, wc, ba.wlist, tot_s, tot_s + RW);
   UB_TRACE_MAX(step, 6);
 }
 
