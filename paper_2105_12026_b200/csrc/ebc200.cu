@@ -366,6 +366,7 @@ struct ebc_ctx {
     int64_t epoch;
     int64_t launches;
     cudaGraphExec_t exec;
+    long long decided = -1;  // decided lazy steps the replay must reproduce (-1: not specialised)
   };
   std::vector<Graph> graphs;
   // device-side sharded exchange (NCCL over NVLink, ebc_comm_init)
@@ -381,7 +382,12 @@ struct ebc_ctx {
     int k;
     int64_t c0, c1;
     int lv;
+    std::vector<char> dec;  // lazy steps the eager run decided with the first batch (1)
+    long long decided = -1; // the eager run's stats[5] (every replay reproduces it)
   };
+  std::vector<char>* rec_dec = nullptr;        // eager run: record each lazy step's decision here
+  const std::vector<char>* cap_dec = nullptr;  // capture: steps decided in the eager run (no conditional node)
+  bool spec_dec = true;                        // EBC200_SPEC_DECIDED=0: keep the conditional node on every lazy step
   std::vector<Eager> eager;
   int ladder_max = 3;         // deepest rung enqueued (L_DIRECT except while capturing)
   int64_t alloc_epoch = 0;
@@ -1083,6 +1089,15 @@ int enqueue_refine_short(ebc_ctx* ctx, int ng, const RefineFinal& fin, const int
 // Conditional graph nodes (captured runs): a handle of the graph ctx->stream is
 // capturing into (0 outside capture), and a scope that inserts an IF node with
 // it and captures the body on a side stream until the scope closes.
+// A Greedy run is a deterministic function of (V, e0, k): a lazy step the
+// eager run decided with its first batch is decided in every replay, so the
+// captured graph holds no conditional node for it (the node costs ~8 us of
+// scheduling per step even when skipped); greedy_run checks the replay's count
+// of decided steps against the eager run's and fails loudly on a difference.
+bool captured_decided(const ebc_ctx* ctx, int step) {
+  return ctx->capturing && ctx->cap_dec && step >= 0 && (size_t)step < ctx->cap_dec->size() && (*ctx->cap_dec)[step];
+}
+
 cudaGraphConditionalHandle cond_handle(ebc_ctx* ctx) {
   if (!ctx->capturing || !ctx->use_cond) return 0;
   cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
@@ -1185,7 +1200,7 @@ void lazy_batch_begin(ebc_ctx* ctx, int step, int commit, int64_t* sel_dev, Refi
   fb.margin = lazy_margin(ctx);
   fb.maxlb = ctx->maxlb;
   fb.scount = ctx->scount;
-  fb.hrest = cond_handle(ctx);
+  fb.hrest = captured_decided(ctx, step) ? 0 : cond_handle(ctx);
 }
 
 // One step's selection: screen + certified window + exact refine + pick, or a
@@ -1253,6 +1268,8 @@ int run_step_select(ebc_ctx* ctx, int step, int commit, int64_t* sel_dev) {
   };
   int mode = sync ? read_mode() : -3;
   if (mode == -4) return fail(ctx, EBC_ECUDA, "lazy step: mode read-back failed");
+  if (sync && ctx->rec_dec && (size_t)step < ctx->rec_dec->size()) (*ctx->rec_dec)[step] = mode == -2;
+  if (captured_decided(ctx, step)) mode = -2;
   if (mode != -2) {
     // undecided step (level[0] == -3): stale set -> mode -> screen / refine
     CondScope ca;
@@ -2131,6 +2148,8 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
     if (!ctx->mode_host) CUC(cudaMallocHost((void**)&ctx->mode_host, sizeof(int)));
     const char* gc = getenv("EBC200_GRAPH_COND");
     if (gc && gc[0] == '0') ctx->use_cond = false;
+    const char* sd = getenv("EBC200_SPEC_DECIDED");
+    if (sd && sd[0] == '0') ctx->spec_dec = false;
   }
   {
     const char* lz = getenv("EBC200_LAZY");
@@ -2549,6 +2568,8 @@ int greedy_run(ebc_ctx* ctx, int32_t k, bool sharded, int64_t* out_sel, double* 
     if (e.k == key && e.c0 == ctx->c0 && e.c1 == ctx->c1) er = &e;
   const bool seen = er != nullptr;
   const int seen_lv = er ? std::max(0, std::min(3, er->lv)) : 3;
+  std::vector<char> dec_rec;
+  long long dec_expect = -1, dec_run = -1;
   if (graph_ok && !cached && seen) {
     const int64_t before = ctx->launches;
     cudaGraph_t graph = nullptr;
@@ -2560,7 +2581,9 @@ int greedy_run(ebc_ctx* ctx, int32_t k, bool sharded, int64_t* out_sel, double* 
       // eager run's path down the ladder, so the graph holds only those rungs
       ctx->ladder_max = seen_lv;
       ctx->capturing = true;
+      if (!sharded && ctx->spec_dec && !er->dec.empty()) ctx->cap_dec = &er->dec;
       const int crc = enqueue();
+      ctx->cap_dec = nullptr;
       ctx->capturing = false;
       ctx->ladder_max = 3;
       ok = cudaStreamEndCapture(ctx->stream, &graph) == cudaSuccess && crc == EBC_OK && epoch == ctx->alloc_epoch;
@@ -2576,7 +2599,8 @@ int greedy_run(ebc_ctx* ctx, int32_t k, bool sharded, int64_t* out_sel, double* 
         } else {
           ++it;
         }
-      ctx->graphs.push_back({key, ctx->c0, ctx->c1, epoch, ctx->launches - before, exec});
+      const long long nd = !sharded && ctx->spec_dec && !er->dec.empty() ? er->decided : -1;
+      ctx->graphs.push_back({key, ctx->c0, ctx->c1, epoch, ctx->launches - before, exec, nd});
       cached = &ctx->graphs.back();
     } else {
       ctx->use_graphs = false;
@@ -2586,17 +2610,27 @@ int greedy_run(ebc_ctx* ctx, int32_t k, bool sharded, int64_t* out_sel, double* 
   if (graph_ok && cached) {
     CU(cudaGraphLaunch(cached->exec, ctx->stream));
     ctx->launches = cached->launches;
+    dec_expect = cached->decided;
+    if (dec_expect >= 0)
+      CU(cudaMemcpyAsync(&dec_run, ctx->stats + 5, sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));
   } else {
     // a repeated eager run (timing mode: per-step events, no graph) takes the
     // first run's path down the ladder, like a replayed graph
     if (seen) ctx->ladder_max = seen_lv;
+    if (!seen) {
+      dec_rec.assign((size_t)k, 0);
+      ctx->rec_dec = &dec_rec;
+    }
     rc = enqueue();
+    ctx->rec_dec = nullptr;
     ctx->ladder_max = 3;
     if (rc) return rc;
   }
-  long long lv_end = 3;
-  if (!(graph_ok && cached) && !seen)
+  long long lv_end = 3, dec_eager = -1;
+  if (!(graph_ok && cached) && !seen) {
     CU(cudaMemcpyAsync(&lv_end, ctx->stats + 2, sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(&dec_eager, ctx->stats + 5, sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));
+  }
   CU(cudaEventRecord(tend, ctx->stream));
   CU(cudaMemcpyAsync(out_sel, ctx->sel_out.p, (size_t)k * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaMemcpyAsync(out_val, ctx->val_out.p, (size_t)k * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
@@ -2604,7 +2638,12 @@ int greedy_run(ebc_ctx* ctx, int32_t k, bool sharded, int64_t* out_sel, double* 
   int tie_err = 0;
   if (sharded) CU(cudaMemcpyAsync(&tie_err, ctx->tie_err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
-  if (!(graph_ok && cached) && !seen) ctx->eager.push_back({key, ctx->c0, ctx->c1, lv_end < 0 ? 3 : (int)lv_end});
+  if (!(graph_ok && cached) && !seen)
+    ctx->eager.push_back({key, ctx->c0, ctx->c1, lv_end < 0 ? 3 : (int)lv_end,
+                          ctx->eager_sync ? dec_rec : std::vector<char>(), dec_eager});
+  if (dec_expect >= 0 && dec_run != dec_expect)
+    return fail(ctx, EBC_ECUDA, "Greedy graph replay diverged from its eager run (" + std::to_string(dec_run) +
+                                    " decided lazy steps, " + std::to_string(dec_expect) + " in the eager run)");
   ctx->comm_status = tie_err;
   if (tie_err & 2)
     return fail(ctx, EBC_ECOMM, "sharded Greedy: ranks disagree on the selection (end-of-run hash mismatch)");

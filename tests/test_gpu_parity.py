@@ -853,9 +853,14 @@ def test_lazy_steps_bit_identical_to_full_screens(monkeypatch, kind):
                       ("noeagersync", {"EBC200_EAGER_SYNC": "0"}), ("noprobe", {"EBC200_LAZY_PROBE": "0"}),
                       ("nonear", {"EBC200_LAZY_NEARBOUND": "0"}), ("nofuse", {"EBC200_FUSE_BATCH": "0"}),
                       ("fuse64", {"EBC200_UB_ROWS": "64"}), ("fuse256", {"EBC200_UB_ROWS": "256"}),
-                      ("probe_gated", {"EBC200_PROBE_MIN_N": "32768"})):
+                      ("probe_gated", {"EBC200_PROBE_MIN_N": "32768"}),
+                      # replays keep the conditional node on steps the eager run decided
+                      ("nospec", {"EBC200_SPEC_DECIDED": "0"}),
+                      # k_update_batch launched plainly after the top-k
+                      ("nopdl", {"EBC200_PDL": "0"})):
         for key in ("EBC200_LAZY", "EBC200_REFINE2", "EBC200_GRAPH_COND", "EBC200_GATHER", "EBC200_EAGER_SYNC",
-                    "EBC200_LAZY_PROBE", "EBC200_LAZY_NEARBOUND", "EBC200_FUSE_BATCH", "EBC200_UB_ROWS"):
+                    "EBC200_LAZY_PROBE", "EBC200_LAZY_NEARBOUND", "EBC200_FUSE_BATCH", "EBC200_UB_ROWS",
+                    "EBC200_SPEC_DECIDED", "EBC200_PDL"):
             monkeypatch.delenv(key, raising=False)
         # the probe batch and the near-centre bound on every case size (the
         # library skips them below 32k candidates; "probe_gated" keeps that)
@@ -864,7 +869,7 @@ def test_lazy_steps_bit_identical_to_full_screens(monkeypatch, kind):
             monkeypatch.setenv(key, val)
         f = fn(X, prec)
         a = eb.greedy_maximize(f, eb.OptimizerBudget(k=k))   # eager
-        b = eb.greedy_maximize(f, eb.OptimizerBudget(k=k))   # captured (conditional nodes)
+        b = eb.greedy_maximize(f, eb.OptimizerBudget(k=k))   # captured (conditional nodes on undecided steps)
         c = eb.greedy_maximize(f, eb.OptimizerBudget(k=k))   # replayed
         assert a.selected == b.selected == c.selected and a.gains == b.gains == c.gains, name
         runs[name] = c
