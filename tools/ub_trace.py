@@ -61,8 +61,10 @@ if tr:
                                                                np.round(np.median(np.array(tr), axis=0), 2))))
     gaps = [(a[st - 1, 0] - tk[st, 3]) / 1e3 for st in range(1, 64)
             if 0 < tk[st, 0] < 2**62 and tk[st, 3] > 0 and 0 < a[st - 1, 0] < 2**62]
-    gaps2 = [(tk[st + 1, 0] - a[st, 6]) / 1e3 for st in range(0, 63)
-             if 0 < tk[st + 1, 0] < 2**62 and a[st, 6] > 0]
+    # update(s) is followed by step s+1's select (conditional node) and then
+    # run_update_batch(s+1), whose top-k is traced as step s+2
+    gaps2 = [(tk[st + 2, 0] - a[st, 6]) / 1e3 for st in range(0, 62)
+             if 0 < tk[st + 2, 0] < 2**62 and 0 < a[st, 6] < 2**62]
     if gaps:
         print("median gap topk end -> update start (us):", round(float(np.median(gaps)), 2),
               " update end -> next topk start (us):", round(float(np.median(gaps2)), 2) if gaps2 else None)
