@@ -316,6 +316,7 @@ struct ebc_ctx {
   int batch_ready_step = -1;       // enqueue-time: that step's first batch was launched with the last update
   cudaGraphConditionalHandle batch_hrest = 0;
   std::vector<char> fused_step;    // timing: step s's update was k_update_batch (ev[4 s + 2] after its top-k)
+  int topk_cpb = 1024;              // EBC200_TOPK_CPB: candidates per k_lazy_topk block (grid <= 2 per SM)
   bool pdl = true;                  // EBC200_PDL: k_update_batch as a programmatic dependent of k_lazy_topk
   int ub_rows = 128;               // EBC200_UB_ROWS: rows per k_update_batch slice (64 or 128; two threads per row)
   ProbeBuf probe;                  // k_lazy_rings: ring winners, ticket, the probe list
@@ -1188,7 +1189,8 @@ int refine_groups(const ebc_ctx* ctx) {
 void lazy_batch_begin(ebc_ctx* ctx, int step, int commit, int64_t* sel_dev, RefineFinal& fb,
                       const PackArgs& pa = PackArgs()) {
   const int64_t ncand = ctx->c1 - ctx->c0;
-  const int ag = (int)std::max<int64_t>(1, std::min<int64_t>(2 * ctx->num_sms, (ncand + 1023) / 1024));
+  const int64_t tpb = ctx->topk_cpb;  // candidates per top-k block (EBC200_TOPK_CPB)
+  const int ag = (int)std::max<int64_t>(1, std::min<int64_t>(2 * ctx->num_sms, (ncand + tpb - 1) / tpb));
   k_lazy_topk<<<ag, 256, 0, ctx->stream>>>(ctx->c0, ctx->c1, ctx->ubp, ctx->selected, ctx->lazy_batch,
                                           (unsigned long long*)ctx->lazy_part, ctx->counter2, ctx->wcount, ctx->wlist,
                                           ctx->ub_next, pa, ctx->best, step);
@@ -2148,6 +2150,8 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
     if (!ctx->mode_host) CUC(cudaMallocHost((void**)&ctx->mode_host, sizeof(int)));
     const char* gc = getenv("EBC200_GRAPH_COND");
     if (gc && gc[0] == '0') ctx->use_cond = false;
+    const char* tc = getenv("EBC200_TOPK_CPB");
+    if (tc && atoi(tc) >= 256) ctx->topk_cpb = atoi(tc);
     const char* sd = getenv("EBC200_SPEC_DECIDED");
     if (sd && sd[0] == '0') ctx->spec_dec = false;
   }
