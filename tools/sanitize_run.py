@@ -15,7 +15,8 @@ for name, X, prec in runs:
     f = eb.EbcFunction(eb.GroundMatrix(X, prec))
     s = eb.greedy_maximize(f, eb.OptimizerBudget(k=6))
     s2 = eb.greedy_maximize(f, eb.OptimizerBudget(k=6))  # captured graph
-    assert s.selected == s2.selected
+    s3 = eb.greedy_maximize(f, eb.OptimizerBudget(k=6))  # replay (decided lazy steps without conditional nodes)
+    assert s.selected == s2.selected == s3.selected
     sets = [rng.choice(X.shape[0], size=10, replace=False).tolist() for _ in range(64)]
     v = eb.evaluate_with_backend(f, eb.EvalMultiset(sets))
     print(name, s.selected, float(v[0]))
