@@ -857,10 +857,15 @@ def test_lazy_steps_bit_identical_to_full_screens(monkeypatch, kind):
                       # replays keep the conditional node on steps the eager run decided
                       ("nospec", {"EBC200_SPEC_DECIDED": "0"}),
                       # k_update_batch launched plainly after the top-k
-                      ("nopdl", {"EBC200_PDL": "0"})):
+                      ("nopdl", {"EBC200_PDL": "0"}),
+                      # batch sizes 1, 7 and 8: every candidate count of the fused
+                      # update's Gram pre-tests (templated) and odd splits of the
+                      # batch between a row's two lanes
+                      ("batch1", {"EBC200_LAZY_BATCH": "1"}), ("batch7", {"EBC200_LAZY_BATCH": "7"}),
+                      ("batch8", {"EBC200_LAZY_BATCH": "8"})):
         for key in ("EBC200_LAZY", "EBC200_REFINE2", "EBC200_GRAPH_COND", "EBC200_GATHER", "EBC200_EAGER_SYNC",
                     "EBC200_LAZY_PROBE", "EBC200_LAZY_NEARBOUND", "EBC200_FUSE_BATCH", "EBC200_UB_ROWS",
-                    "EBC200_SPEC_DECIDED", "EBC200_PDL"):
+                    "EBC200_SPEC_DECIDED", "EBC200_PDL", "EBC200_LAZY_BATCH"):
             monkeypatch.delenv(key, raising=False)
         # the probe batch and the near-centre bound on every case size (the
         # library skips them below 32k candidates; "probe_gated" keeps that)
