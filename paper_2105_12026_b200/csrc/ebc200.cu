@@ -309,7 +309,7 @@ struct ebc_ctx {
   int* scount = nullptr;
   void* lazy_part = nullptr;       // 2 num_sms x TK 64-bit keys: k_lazy_topk's block lists
   double* ub_next = nullptr;       // best stale bound outside the first batch
-  int lazy_batch = 4;              // EBC200_LAZY_BATCH (1..RW): candidates refined first in a lazy step
+  int lazy_batch = 4;              // EBC200_LAZY_BATCH (1..RW): candidates refined first in a lazy step (3 for N >= 2^18)
   bool probe_on = true;            // EBC200_LAZY_PROBE=0: no ring-probe batch on undecided steps
   bool fuse_batch = true;          // EBC200_FUSE_BATCH=0: the next step's first batch not folded into K4
   int64_t probe_min_n = 32768;     // EBC200_PROBE_MIN_N: candidates below which undecided steps skip probe / near bound
@@ -2138,6 +2138,10 @@ int ebc_create(const void* V, int64_t n, int32_t d, int32_t dtype, const double*
     }
   }
   {
+    // measured (bench.py, EBC200_LAZY_BATCH A/B): 4 on C2 (N = 100k: 3.17 ms
+    // vs 3.27 with 3), 3 on C4 (N = 500k: 48.3 ms vs 52.0 with 4; fewer
+    // candidates re-examined), C4S50 equal
+    ctx->lazy_batch = ctx->n >= (int64_t)1 << 18 ? 3 : 4;
     const char* lb = getenv("EBC200_LAZY_BATCH");
     if (lb && lb[0]) ctx->lazy_batch = std::max(1, std::min(RW, atoi(lb)));
     const char* r2 = getenv("EBC200_REFINE2");

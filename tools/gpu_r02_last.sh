@@ -1,8 +1,8 @@
 # Round-2 (session 3) final measurements on one B200: suite, smoke, bench lines
 # C2 (default) / C4 / C1 / C5 / C4S50, the reference arm, C2 launch list and a
 # --set full capture of k_update_batch.
-mkdir -p gpurun_out/final4
-O=gpurun_out/final4
+mkdir -p gpurun_out/final5
+O=gpurun_out/final5
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/smi.txt
 timeout 1200 python -m pytest tests -m gpu -q -x --durations=8 > $O/gpu_tests.txt 2>&1; tail -3 $O/gpu_tests.txt
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.txt 2>&1; tail -1 $O/smoke.txt
